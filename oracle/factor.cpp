@@ -1,0 +1,262 @@
+// ORACLE (test infrastructure only) — exact direct factors used on the solve path.
+//  * DenseFullPivLU restates Eigen::FullPivLU as used by the AMG coarse solve
+//    (/root/reference/proj/core/src/amg.cpp:144-149,284-289) and the fixed-stress
+//    local solves (precond.cpp:273-278).
+//  * BandFactor restates SparseFactor (sparse_factor.cpp:30-67): LDL^T for
+//    Kind::spd (T in t-p-u, precond.cpp:129), LU with partial pivoting for
+//    Kind::general (S~2 in t-u-p, precond.cpp:182).  Bitwise parity with Eigen is
+//    not pinned by any reference test; the reference only checks
+//    residual-level properties (test_gmres.cpp:25-42), re-expressed in tests.
+// Solve order (part of the oracle's definition, reproduced by the GPU):
+// column sweeps — forward: for j ascending, finalize y_j, then subtract
+// L(i,j)*y_j from each later row i; backward: for j descending, finalize x_j,
+// then subtract U(i,j)*x_j from each earlier row i.
+#include <algorithm>
+#include <cmath>
+#include <limits>
+
+#include "fpo.hpp"
+
+namespace fpo {
+
+void DenseFullPivLU::compute(const std::vector<double>& a, int nn) {
+  n = nn;
+  lu = a;
+  prow.resize(static_cast<size_t>(n));
+  pcol.resize(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) prow[i] = pcol[i] = i;
+  double maxpivot = 0.0;
+  int nonzero = n;
+  for (int k = 0; k < n; ++k) {
+    int pi = k, pj = k;
+    double best = -1.0;
+    for (int i = k; i < n; ++i)
+      for (int j = k; j < n; ++j) {
+        const double v = std::abs(lu[size_t(i) * n + j]);
+        if (v > best) best = v, pi = i, pj = j;
+      }
+    if (best == 0.0) {  // the remaining block is exactly zero
+      nonzero = k;
+      break;
+    }
+    if (k == 0) maxpivot = best;
+    if (pi != k) {
+      for (int j = 0; j < n; ++j) std::swap(lu[size_t(k) * n + j], lu[size_t(pi) * n + j]);
+      std::swap(prow[k], prow[pi]);
+    }
+    if (pj != k) {
+      for (int i = 0; i < n; ++i) std::swap(lu[size_t(i) * n + k], lu[size_t(i) * n + pj]);
+      std::swap(pcol[k], pcol[pj]);
+    }
+    const double piv = lu[size_t(k) * n + k];
+    for (int i = k + 1; i < n; ++i) {
+      const double f = lu[size_t(i) * n + k] / piv;
+      lu[size_t(i) * n + k] = f;
+      for (int j = k + 1; j < n; ++j) lu[size_t(i) * n + j] -= f * lu[size_t(k) * n + j];
+    }
+  }
+  // rank: pivots above n * eps * |largest pivot| (Eigen's default threshold rule)
+  const double thr = double(n) * std::numeric_limits<double>::epsilon() * maxpivot;
+  rank = 0;
+  for (int k = 0; k < nonzero; ++k)
+    if (std::abs(lu[size_t(k) * n + k]) > thr) ++rank;
+}
+
+std::vector<double> DenseFullPivLU::solve(std::span<const double> b) const {
+  if (int(b.size()) != n) throw std::invalid_argument("DenseFullPivLU::solve: dimension mismatch");
+  std::vector<double> c(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) c[i] = b[prow[i]];
+  for (int j = 0; j < n; ++j) {  // unit lower, column sweep
+    const double cj = c[j];
+    for (int i = j + 1; i < n; ++i) c[i] -= lu[size_t(i) * n + j] * cj;
+  }
+  for (int j = rank - 1; j >= 0; --j) {  // upper on the leading rank x rank block
+    const double xj = c[j] / lu[size_t(j) * n + j];
+    c[j] = xj;
+    for (int i = 0; i < j; ++i) c[i] -= lu[size_t(i) * n + j] * xj;
+  }
+  std::vector<double> x(static_cast<size_t>(n), 0.0);
+  for (int i = 0; i < rank; ++i) x[pcol[i]] = c[i];
+  return x;
+}
+
+// ---------------------------------------------------------------- BandFactor
+namespace {
+
+// Dense band working storage for one diagonal block [b0, b1): row-major with
+// columns j in [i - lo, i + hi] mapped to slot (j - i + lo).
+struct Band {
+  int n, lo, hi, w;
+  std::vector<double> a;
+  Band(int n_, int lo_, int hi_) : n(n_), lo(lo_), hi(hi_), w(lo_ + hi_ + 1), a(static_cast<size_t>(n_) * (lo_ + hi_ + 1), 0.0) {}
+  double& at(int i, int j) { return a[size_t(i) * w + (j - i + lo)]; }
+  bool in(int i, int j) const { return j - i >= -lo && j - i <= hi; }
+};
+
+}  // namespace
+
+void BandFactor::factor(const CsrMatrix& A, Kind k) {
+  if (A.n_rows != A.n_cols) throw std::invalid_argument("SparseFactor: matrix must be square");
+  kind = k;
+  n = A.n_rows;
+  // Independent diagonal blocks: a split at s is valid when no row < s has a
+  // column >= s and no row >= s has a column < s.
+  std::vector<int> maxcol(static_cast<size_t>(n), 0), mincol(static_cast<size_t>(n), 0);
+  int lo = 0, hi = 0;
+  for (int i = 0; i < n; ++i) {
+    int mn = i, mx = i;
+    for (int64_t q = A.row_offsets[i]; q < A.row_offsets[i + 1]; ++q) {
+      mn = std::min(mn, A.col_indices[q]);
+      mx = std::max(mx, A.col_indices[q]);
+    }
+    mincol[i] = mn;
+    maxcol[i] = mx;
+    lo = std::max(lo, i - mn);
+    hi = std::max(hi, mx - i);
+  }
+  std::vector<int> suffix_min(static_cast<size_t>(n) + 1, n);
+  for (int s = n - 1; s >= 0; --s) suffix_min[s] = std::min(suffix_min[size_t(s) + 1], mincol[s]);
+  block_start.assign(1, 0);
+  int prefix_max = -1;
+  for (int s = 1; s < n; ++s) {
+    prefix_max = std::max(prefix_max, maxcol[s - 1]);
+    if (prefix_max < s && suffix_min[s] >= s) block_start.push_back(s);
+  }
+  block_start.push_back(n);
+  if (n == 0) block_start.assign(1, 0);
+  if (kind == Kind::spd) {
+    kl = lo;
+    ku = 0;
+    Lc.assign(static_cast<size_t>(n) * std::max(kl, 1), 0.0);
+    Lr.assign(static_cast<size_t>(n) * std::max(kl, 1), 0.0);
+    diag.assign(static_cast<size_t>(n), 0.0);
+    piv.clear();
+    for (size_t blk = 0; blk + 1 < block_start.size(); ++blk) {
+      const int b0 = block_start[blk], b1 = block_start[blk + 1], nb = b1 - b0;
+      Band L(nb, kl, 0);  // lower triangle of A (symmetric input: use the lower part)
+      for (int i = b0; i < b1; ++i)
+        for (int64_t q = A.row_offsets[i]; q < A.row_offsets[i + 1]; ++q) {
+          const int j = A.col_indices[q];
+          if (j <= i && j >= b0) L.at(i - b0, j - b0) = A.values[q];
+        }
+      // right-looking LDL^T inside the band: for each column j, D_j = pivot,
+      // l_ij = a_ij / D_j, then a_ik -= l_ij * D_j * l_kj for j < k <= i.
+      std::vector<double> D(static_cast<size_t>(nb));
+      for (int j = 0; j < nb; ++j) {
+        const double dj = L.at(j, j);
+        if (!(std::abs(dj) > 0.0) || !std::isfinite(dj))
+          throw numerical_error("SparseFactor: LDLT factorization failed (matrix not SPD?)");
+        D[j] = dj;
+        const int iend = std::min(nb, j + kl + 1);
+        for (int i = j + 1; i < iend; ++i) L.at(i, j) = L.at(i, j) / dj;
+        for (int i = j + 1; i < iend; ++i) {
+          const double lij = L.at(i, j);
+          if (lij == 0.0) continue;
+          const double t = lij * dj;
+          for (int kk = j + 1; kk <= i; ++kk) L.at(i, kk) -= t * L.at(kk, j);
+        }
+      }
+      for (int j = 0; j < nb; ++j) {
+        diag[b0 + j] = D[j];
+        for (int r = 0; r < kl; ++r) {
+          const int i = j + 1 + r;
+          Lc[size_t(b0 + j) * kl + r] = i < nb ? L.at(i, j) : 0.0;
+          const int c = j - 1 - r;
+          Lr[size_t(b0 + j) * kl + r] = c >= 0 ? L.at(j, c) : 0.0;
+        }
+      }
+    }
+    return;
+  }
+  // general: banded LU with partial pivoting (row interchanges within the band)
+  kl = lo;
+  ku = lo + hi;
+  Lc.assign(static_cast<size_t>(n) * std::max(kl, 1), 0.0);
+  Uc.assign(static_cast<size_t>(n) * std::max(ku, 1), 0.0);
+  diag.assign(static_cast<size_t>(n), 0.0);
+  piv.assign(static_cast<size_t>(n), 0);
+  Lr.clear();
+  for (size_t blk = 0; blk + 1 < block_start.size(); ++blk) {
+    const int b0 = block_start[blk], b1 = block_start[blk + 1], nb = b1 - b0;
+    Band W(nb, kl, ku);
+    for (int i = b0; i < b1; ++i)
+      for (int64_t q = A.row_offsets[i]; q < A.row_offsets[i + 1]; ++q) {
+        const int j = A.col_indices[q];
+        if (j >= b0 && j < b1) W.at(i - b0, j - b0) = A.values[q];
+      }
+    for (int j = 0; j < nb; ++j) {
+      const int iend = std::min(nb, j + kl + 1);
+      int p = j;
+      double best = std::abs(W.at(j, j));
+      for (int i = j + 1; i < iend; ++i)
+        if (std::abs(W.at(i, j)) > best) best = std::abs(W.at(i, j)), p = i;
+      if (best == 0.0 || !std::isfinite(best))
+        throw numerical_error("SparseFactor: sparse LU factorization failed (singular matrix?)");
+      piv[b0 + j] = b0 + p;
+      const int jend = std::min(nb, j + ku + 1);  // columns touched by row j after swaps
+      if (p != j)
+        for (int c = j; c < jend; ++c) std::swap(W.at(j, c), W.at(p, c));
+      const double ujj = W.at(j, j);
+      for (int i = j + 1; i < iend; ++i) {
+        const double f = W.at(i, j) / ujj;
+        W.at(i, j) = f;
+        if (f == 0.0) continue;
+        for (int c = j + 1; c < jend; ++c) W.at(i, c) -= f * W.at(j, c);
+      }
+    }
+    for (int j = 0; j < nb; ++j) {
+      diag[b0 + j] = W.at(j, j);
+      for (int r = 0; r < kl; ++r) {
+        const int i = j + 1 + r;
+        Lc[size_t(b0 + j) * kl + r] = i < nb ? W.at(i, j) : 0.0;
+      }
+      for (int r = 0; r < ku; ++r) {
+        const int i = j - 1 - r;
+        Uc[size_t(b0 + j) * ku + r] = (i >= 0 && W.in(i, j)) ? W.at(i, j) : 0.0;
+      }
+    }
+  }
+}
+
+std::vector<double> BandFactor::solve(std::span<const double> b) const {
+  if (int(b.size()) != n) throw std::invalid_argument("SparseFactor::solve: dimension mismatch");
+  std::vector<double> x(b.begin(), b.end());
+  for (size_t blk = 0; blk + 1 < block_start.size(); ++blk) {
+    const int b0 = block_start[blk], b1 = block_start[blk + 1];
+    // forward sweep: (pivot) + unit-lower L
+    for (int j = b0; j < b1; ++j) {
+      if (kind == Kind::general && piv[j] != j) std::swap(x[j], x[piv[j]]);
+      const double yj = x[j];
+      for (int r = 0; r < kl; ++r) {
+        const int i = j + 1 + r;
+        if (i >= b1) break;
+        x[i] -= Lc[size_t(j) * kl + r] * yj;
+      }
+    }
+    if (kind == Kind::spd) {
+      for (int j = b0; j < b1; ++j) x[j] = x[j] / diag[j];
+      // backward sweep with L^T: x_j final, then x_i -= L(j,i) x_j for i < j
+      for (int j = b1 - 1; j >= b0; --j) {
+        const double xj = x[j];
+        for (int r = 0; r < kl; ++r) {
+          const int i = j - 1 - r;
+          if (i < b0) break;
+          x[i] -= Lr[size_t(j) * kl + r] * xj;
+        }
+      }
+    } else {
+      for (int j = b1 - 1; j >= b0; --j) {
+        const double xj = x[j] / diag[j];
+        x[j] = xj;
+        for (int r = 0; r < ku; ++r) {
+          const int i = j - 1 - r;
+          if (i < b0) break;
+          x[i] -= Uc[size_t(j) * ku + r] * xj;
+        }
+      }
+    }
+  }
+  return x;
+}
+
+}  // namespace fpo
