@@ -1,0 +1,167 @@
+/*
+ * fracprec_b200 — C ABI of the B200-native solve phase (GMRES + block-AMG
+ * preconditioners t-p-u / t-u-p / t-u-p* for the 3x3 contact/fracture-flow
+ * Jacobian of arXiv 2112.12397).
+ *
+ * Every entry point replaces one call of the reference's C++ API
+ * (/root/reference/proj/core/include/fracprec/*.hpp); the mapping is noted per
+ * function.  Conventions:
+ *   - return value: FP_OK (0) or an error code; fp_last_error() gives the
+ *     message (thread-local).  Codes mirror the reference's exception classes:
+ *     std::invalid_argument -> FP_INVALID_ARGUMENT, fracprec::numerical_error ->
+ *     FP_NUMERICAL_ERROR (errors.hpp:15-18); CUDA failures -> FP_CUDA_ERROR.
+ *   - matrices cross the boundary as CSR views in the reference's layout
+ *     (csr.hpp:16-22: 0-based, columns sorted and unique per row).  Row offsets
+ *     may be 32-bit (row_offsets32, the reference's std::vector<int>) or 64-bit
+ *     (row_offsets64); exactly one must be non-null.
+ *   - handles own all device memory; host arrays are borrowed for the call.
+ *   - `mem` selects where vector arguments live: FP_MEM_HOST or FP_MEM_DEVICE.
+ *   - one CUDA stream per system handle; calls on one handle are serialized.
+ */
+#ifndef FRACPREC_B200_H
+#define FRACPREC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FP_OK 0
+#define FP_INVALID_ARGUMENT 1
+#define FP_NUMERICAL_ERROR 2
+#define FP_CUDA_ERROR 3
+#define FP_INTERNAL_ERROR 4
+
+#define FP_MEM_HOST 0
+#define FP_MEM_DEVICE 1
+
+/* PrecondConfig::Variant (precond.hpp:20) */
+#define FP_TPU 0
+#define FP_TUP 1
+#define FP_TUP_STAR 2
+
+/* AmgConfig::Smoother (amg.hpp:24) */
+#define FP_SMOOTHER_JACOBI 0
+#define FP_SMOOTHER_SGS 1
+
+typedef struct fp_csr {
+  int32_t n_rows, n_cols;
+  const int32_t* row_offsets32; /* n_rows + 1, or NULL */
+  const int64_t* row_offsets64; /* n_rows + 1, or NULL */
+  const int32_t* col_indices;
+  const double* values;
+} fp_csr;
+
+/* BlockSystem (block.hpp:36-45): J = [A C1 Q1; C2 -H 0; Q2 0 T] */
+typedef struct fp_block_system {
+  int32_t n_u, n_t, n_p;
+  fp_csr A, C1, Q1, C2, H, Q2, T, F_u; /* F_u may be empty (n_rows = 0) */
+} fp_block_system;
+
+/* AmgConfig (amg.hpp:19-31) */
+typedef struct fp_amg_config {
+  double strength_threshold;
+  int32_t max_coarse, pre_sweeps, post_sweeps;
+  int32_t smoother; /* the GPU path requires FP_SMOOTHER_JACOBI */
+  int32_t prolongation_smoothing;
+  int32_t cycles_per_apply;
+  double jacobi_omega, stall_ratio;
+  int32_t max_levels;
+} fp_amg_config;
+
+/* PrecondConfig (precond.hpp:19-30); inner is always AMG on this path */
+typedef struct fp_precond_config {
+  int32_t variant;
+  fp_amg_config amg;
+} fp_precond_config;
+
+typedef struct fp_gmres_options {
+  double tol;       /* relative, on ||b - op x|| (gmres.hpp:29-33) */
+  int32_t restart;  /* GMRES(m) restart length; >= max_iter gives full GMRES */
+  int32_t max_iter;
+  int32_t scaled;   /* 1: solve the driver's D J D system (driver.cpp:229-255) */
+} fp_gmres_options;
+
+/* SolveStats (gmres.hpp:15-22) + bookkeeping */
+typedef struct fp_solve_stats {
+  int32_t iterations, converged, breakdown, restarts, precond_applies;
+  double final_rel_residual;
+  double device_seconds;       /* CUDA-event time of the solve on the handle's stream */
+  double* residual_history;    /* optional caller buffer */
+  int32_t history_capacity;
+  int32_t history_len;
+} fp_solve_stats;
+
+typedef struct fp_system fp_system;           /* device-resident J (BlockSystem) */
+typedef struct fp_precond fp_precond;         /* device-resident M^-1 */
+typedef struct fp_host_precond fp_host_precond; /* host-built preconditioner data */
+
+/* Reference-built hierarchy upload (TpuPreconditioner / TupPreconditioner,
+ * precond.hpp:53-74, AmgHierarchy amg.hpp:35-50).  levels[0].A is S~ (t-p-u)
+ * or S1 (t-u-p); levels[l>0].P maps level l to level l-1; diag = smoother_diag.
+ * factor_matrix is T (t-p-u, factored LDL^T) or S~2 (t-u-p, factored LU);
+ * h_blocks are the n_p regularized 3x3 blocks of H~ (BlockDiagonal3, row-major). */
+typedef struct fp_amg_level_desc {
+  fp_csr A;
+  fp_csr P;
+  const double* smoother_diag;
+} fp_amg_level_desc;
+
+typedef struct fp_precond_desc {
+  int32_t variant;
+  const double* h_blocks;
+  fp_csr factor_matrix;
+  int32_t n_levels;
+  const fp_amg_level_desc* levels;
+  fp_amg_config amg;
+} fp_precond_desc;
+
+const char* fp_last_error(void);
+const char* fp_version(void);
+void fp_amg_config_default(fp_amg_config* cfg); /* reference defaults, smoother = Jacobi */
+
+/* ---- system: BlockSystem upload and BlockSystemOperator::apply (block.cpp:55-74) */
+int fp_system_create(const fp_block_system* J, fp_system** out);
+void fp_system_destroy(fp_system* s);
+int fp_system_dims(const fp_system* s, int32_t* n_u, int32_t* n_t, int32_t* n_p);
+/* y = J x */
+int fp_system_apply(fp_system* s, const double* x, double* y, int32_t mem);
+/* BlockScaling::from (driver.cpp:114-125) */
+int fp_block_scaling(const fp_system* s, double* st, double* sp);
+
+/* ---- preconditioner build: build_tpu / build_tup (precond.cpp:119-202) on the host */
+int fp_host_precond_build(const fp_block_system* J, const fp_precond_config* cfg, const double* node_coords,
+                          int32_t n_nodes, fp_host_precond** out);
+void fp_host_precond_destroy(fp_host_precond* p);
+/* number of AMG levels and the row count of each (levels[] may be NULL) */
+int fp_host_precond_levels(const fp_host_precond* p, int32_t* n_levels, int32_t* level_rows);
+/* copy out a host-built matrix: what 0 = A_l (level), 1 = P_l (level >= 1), 2 = T or S~2.
+ * Call with row_offsets == NULL first to get dims / nnz. */
+int fp_host_precond_matrix(const fp_host_precond* p, int32_t what, int32_t level, int32_t* n_rows, int32_t* n_cols,
+                           int64_t* nnz, int64_t* row_offsets, int32_t* col_indices, double* values);
+/* what 0 = H~ blocks (9 n_p), 1 = T_diag (t-p-u) or S_K (t-u-p), 2 = smoother diag of level `level` */
+int fp_host_precond_vector(const fp_host_precond* p, int32_t what, int32_t level, double* out, int64_t* len);
+
+/* ---- upload to the device */
+int fp_precond_create(fp_system* s, const fp_host_precond* hp, fp_precond** out);
+int fp_precond_upload(fp_system* s, const fp_precond_desc* desc, fp_precond** out);
+void fp_precond_destroy(fp_precond* p);
+
+/* ---- applies: TpuOperator / TupOperator::apply (precond.cpp:285-296), amg_apply (amg.cpp:293-305) */
+int fp_precond_apply(fp_precond* p, const double* x, double* y, int32_t mem);
+int fp_amg_apply(fp_precond* p, const double* r, double* x, int32_t mem);
+/* InnerSolver::call_count / reset_count (precond.hpp:34-42) */
+int64_t fp_precond_inner_calls(fp_precond* p, int32_t reset);
+/* algorithmic HBM bytes and kernel launches of one fp_precond_apply / fp_system_apply */
+int fp_precond_traffic(fp_precond* p, double* apply_bytes, int32_t* apply_launches, double* japply_bytes);
+
+/* ---- solve: gmres(op, precond, b, tol, max_iter) (gmres.hpp:29-33) + GMRES(m) restart */
+int fp_gmres(fp_system* s, fp_precond* p, const double* b, double* x, int32_t mem, const fp_gmres_options* opt,
+             fp_solve_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FRACPREC_B200_H */

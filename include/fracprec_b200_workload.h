@@ -1,0 +1,54 @@
+/*
+ * fracprec_b200 workload generator — synthetic inputs for the BASELINE.json
+ * configs (structured hex mesh with duplicated fracture nodes, trilinear
+ * elasticity, TPFA fracture flow, seeded contact state).  Restates the
+ * reference's input side (/root/reference/proj/core/src/mesh.cpp,
+ * assembly.cpp), which is not on the solve path; it is exported so tests and
+ * bench.py can build the same systems the GPU solves.
+ */
+#ifndef FRACPREC_B200_WORKLOAD_H
+#define FRACPREC_B200_WORKLOAD_H
+
+#include <stdint.h>
+
+#include "fracprec_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fp_fracture_spec { /* FractureSpec (mesh.hpp:28-33) */
+  int32_t normal_axis;
+  double coord, lo1, hi1, lo2, hi2;
+} fp_fracture_spec;
+
+typedef struct fp_workload_spec {
+  int32_t cells[3];
+  double length[3];
+  int32_t n_fractures;
+  const fp_fracture_spec* fractures;
+  double E_median, E_sigma_ln;
+  int32_t E_layers;
+  double nu, nu_lo, nu_hi;
+  double frac_stick, frac_slip;
+  double aperture_median, aperture_sigma_ln;
+  uint64_t seed;
+} fp_workload_spec;
+
+typedef struct fp_workload fp_workload;
+
+/* config_id 1..5 = BASELINE.json configs[0..4] */
+int fp_workload_preset(int32_t config_id, uint64_t seed, fp_workload** out);
+int fp_workload_custom(const fp_workload_spec* spec, fp_workload** out);
+void fp_workload_destroy(fp_workload* w);
+/* views into the workload's arrays (64-bit row offsets), valid until destroy */
+int fp_workload_system(const fp_workload* w, fp_block_system* J);
+int fp_workload_coords(const fp_workload* w, const double** xyz, int32_t* n_nodes);
+/* counts[0..3] = stick, slip, open, fractures */
+int fp_workload_info(const fp_workload* w, int32_t* counts);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

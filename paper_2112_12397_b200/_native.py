@@ -1,0 +1,147 @@
+"""ctypes binding of the C ABI in include/fracprec_b200.h.
+
+The shared library is built in-tree (``python -m paper_2112_12397_b200.build`` or
+``__graft_entry__.build()``) into ``paper_2112_12397_b200/_lib/``.  There is no
+fallback: if the library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libfracprec_b200.so")
+
+FP_OK, FP_INVALID_ARGUMENT, FP_NUMERICAL_ERROR, FP_CUDA_ERROR, FP_INTERNAL_ERROR = 0, 1, 2, 3, 4
+FP_MEM_HOST, FP_MEM_DEVICE = 0, 1
+FP_TPU, FP_TUP, FP_TUP_STAR = 0, 1, 2
+FP_SMOOTHER_JACOBI, FP_SMOOTHER_SGS = 0, 1
+
+
+class NumericalError(RuntimeError):
+    """fracprec::numerical_error (errors.hpp:15-18)."""
+
+
+class CudaError(RuntimeError):
+    """A CUDA failure inside the native library."""
+
+
+class FpCsr(C.Structure):
+    _fields_ = [("n_rows", C.c_int32), ("n_cols", C.c_int32),
+                ("row_offsets32", C.POINTER(C.c_int32)), ("row_offsets64", C.POINTER(C.c_int64)),
+                ("col_indices", C.POINTER(C.c_int32)), ("values", C.POINTER(C.c_double))]
+
+
+class FpBlockSystem(C.Structure):
+    _fields_ = [("n_u", C.c_int32), ("n_t", C.c_int32), ("n_p", C.c_int32)] + \
+               [(nm, FpCsr) for nm in ("A", "C1", "Q1", "C2", "H", "Q2", "T", "F_u")]
+
+
+class FpAmgConfig(C.Structure):
+    _fields_ = [("strength_threshold", C.c_double), ("max_coarse", C.c_int32), ("pre_sweeps", C.c_int32),
+                ("post_sweeps", C.c_int32), ("smoother", C.c_int32), ("prolongation_smoothing", C.c_int32),
+                ("cycles_per_apply", C.c_int32), ("jacobi_omega", C.c_double), ("stall_ratio", C.c_double),
+                ("max_levels", C.c_int32)]
+
+
+class FpPrecondConfig(C.Structure):
+    _fields_ = [("variant", C.c_int32), ("amg", FpAmgConfig)]
+
+
+class FpGmresOptions(C.Structure):
+    _fields_ = [("tol", C.c_double), ("restart", C.c_int32), ("max_iter", C.c_int32), ("scaled", C.c_int32)]
+
+
+class FpSolveStats(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("breakdown", C.c_int32),
+                ("restarts", C.c_int32), ("precond_applies", C.c_int32), ("final_rel_residual", C.c_double),
+                ("device_seconds", C.c_double), ("residual_history", C.POINTER(C.c_double)),
+                ("history_capacity", C.c_int32), ("history_len", C.c_int32)]
+
+
+class FpAmgLevelDesc(C.Structure):
+    _fields_ = [("A", FpCsr), ("P", FpCsr), ("smoother_diag", C.POINTER(C.c_double))]
+
+
+class FpPrecondDesc(C.Structure):
+    _fields_ = [("variant", C.c_int32), ("h_blocks", C.POINTER(C.c_double)), ("factor_matrix", FpCsr),
+                ("n_levels", C.c_int32), ("levels", C.POINTER(FpAmgLevelDesc)), ("amg", FpAmgConfig)]
+
+
+class FpFractureSpec(C.Structure):
+    _fields_ = [("normal_axis", C.c_int32), ("coord", C.c_double), ("lo1", C.c_double), ("hi1", C.c_double),
+                ("lo2", C.c_double), ("hi2", C.c_double)]
+
+
+class FpWorkloadSpec(C.Structure):
+    _fields_ = [("cells", C.c_int32 * 3), ("length", C.c_double * 3), ("n_fractures", C.c_int32),
+                ("fractures", C.POINTER(FpFractureSpec)), ("E_median", C.c_double), ("E_sigma_ln", C.c_double),
+                ("E_layers", C.c_int32), ("nu", C.c_double), ("nu_lo", C.c_double), ("nu_hi", C.c_double),
+                ("frac_stick", C.c_double), ("frac_slip", C.c_double), ("aperture_median", C.c_double),
+                ("aperture_sigma_ln", C.c_double), ("seed", C.c_uint64)]
+
+
+# Every symbol include/*.h declares, with its ctypes signature (restype, argtypes).
+_P = C.c_void_p
+_PP = C.POINTER(C.c_void_p)
+_DP = C.POINTER(C.c_double)
+SIGNATURES = {
+    "fp_last_error": (C.c_char_p, []),
+    "fp_version": (C.c_char_p, []),
+    "fp_amg_config_default": (None, [C.POINTER(FpAmgConfig)]),
+    "fp_system_create": (C.c_int, [C.POINTER(FpBlockSystem), _PP]),
+    "fp_system_destroy": (None, [_P]),
+    "fp_system_dims": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "fp_system_apply": (C.c_int, [_P, _P, _P, C.c_int32]),
+    "fp_block_scaling": (C.c_int, [_P, _DP, _DP]),
+    "fp_host_precond_build": (C.c_int, [C.POINTER(FpBlockSystem), C.POINTER(FpPrecondConfig), _DP, C.c_int32, _PP]),
+    "fp_host_precond_destroy": (None, [_P]),
+    "fp_host_precond_levels": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "fp_host_precond_matrix": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32), _DP]),
+    "fp_host_precond_vector": (C.c_int, [_P, C.c_int32, C.c_int32, _DP, C.POINTER(C.c_int64)]),
+    "fp_precond_create": (C.c_int, [_P, _P, _PP]),
+    "fp_precond_upload": (C.c_int, [_P, C.POINTER(FpPrecondDesc), _PP]),
+    "fp_precond_destroy": (None, [_P]),
+    "fp_precond_apply": (C.c_int, [_P, _P, _P, C.c_int32]),
+    "fp_amg_apply": (C.c_int, [_P, _P, _P, C.c_int32]),
+    "fp_precond_inner_calls": (C.c_int64, [_P, C.c_int32]),
+    "fp_precond_traffic": (C.c_int, [_P, _DP, C.POINTER(C.c_int32), _DP]),
+    "fp_gmres": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(FpGmresOptions), C.POINTER(FpSolveStats)]),
+    "fp_workload_preset": (C.c_int, [C.c_int32, C.c_uint64, _PP]),
+    "fp_workload_custom": (C.c_int, [C.POINTER(FpWorkloadSpec), _PP]),
+    "fp_workload_destroy": (None, [_P]),
+    "fp_workload_system": (C.c_int, [_P, C.POINTER(FpBlockSystem)]),
+    "fp_workload_coords": (C.c_int, [_P, C.POINTER(_DP), C.POINTER(C.c_int32)]),
+    "fp_workload_info": (C.c_int, [_P, C.POINTER(C.c_int32)]),
+}
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"fracprec_b200 native library not found at {LIB_PATH}; build it with "
+            "`python -m paper_2112_12397_b200.build` (there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int) -> None:
+    """Raise the Python image of the reference's exception classes."""
+    if status == FP_OK:
+        return
+    msg = (lib.fp_last_error() or b"").decode()
+    if status == FP_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if status == FP_NUMERICAL_ERROR:
+        raise NumericalError(msg)
+    if status == FP_CUDA_ERROR:
+        raise CudaError(msg)
+    raise RuntimeError(msg)

@@ -1,0 +1,408 @@
+"""Python host mirror of the reference's solve-path API over the C ABI.
+
+Names and argument meaning follow /root/reference/proj/core/include/fracprec/:
+``CsrMatrix`` (csr.hpp:16-49), ``BlockSystem`` (block.hpp:36-45),
+``AmgConfig`` (amg.hpp:19-31), ``PrecondConfig`` (precond.hpp:19-30),
+``build_tpu`` / ``build_tup`` (precond.hpp:76-85), ``TpuOperator`` /
+``TupOperator`` (precond.hpp:94-116), ``BlockSystemOperator`` (block.hpp:48-57),
+``gmres`` (gmres.hpp:29-33) and ``SolveStats`` (gmres.hpp:15-22).  Errors raise
+``ValueError`` (std::invalid_argument) or ``NumericalError``.
+
+Vectors may be NumPy arrays (host memory, copied through the ABI) or CUDA
+torch tensors (device memory, used in place).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from ._native import NumericalError  # noqa: F401  (re-export)
+
+_VARIANTS = {"tpu": N.FP_TPU, "tup": N.FP_TUP, "tup_star": N.FP_TUP_STAR}
+
+
+@dataclass
+class CsrMatrix:
+    n_rows: int
+    n_cols: int
+    row_offsets: np.ndarray
+    col_indices: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self):
+        self.row_offsets = np.ascontiguousarray(self.row_offsets, dtype=np.int64)
+        self.col_indices = np.ascontiguousarray(self.col_indices, dtype=np.int32)
+        self.values = np.ascontiguousarray(self.values, dtype=np.float64)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_offsets[-1]) if self.n_rows > 0 else 0
+
+    @staticmethod
+    def empty(rows: int, cols: int) -> "CsrMatrix":
+        return CsrMatrix(rows, cols, np.zeros(rows + 1, np.int64), np.zeros(0, np.int32), np.zeros(0))
+
+    def view(self) -> N.FpCsr:
+        v = N.FpCsr()
+        v.n_rows, v.n_cols = self.n_rows, self.n_cols
+        v.row_offsets64 = self.row_offsets.ctypes.data_as(C.POINTER(C.c_int64))
+        v.col_indices = self.col_indices.ctypes.data_as(C.POINTER(C.c_int32))
+        v.values = self.values.ctypes.data_as(C.POINTER(C.c_double))
+        return v
+
+    def matvec(self, x: np.ndarray) -> np.ndarray:  # host helper for checks (not on the solve path)
+        rows = np.repeat(np.arange(self.n_rows), np.diff(self.row_offsets))
+        y = np.zeros(self.n_rows)
+        np.add.at(y, rows, self.values * x[self.col_indices])
+        return y
+
+
+@dataclass
+class BlockSystem:
+    n_u: int
+    n_t: int
+    n_p: int
+    A: CsrMatrix
+    C1: CsrMatrix
+    Q1: CsrMatrix
+    C2: CsrMatrix
+    H: CsrMatrix
+    Q2: CsrMatrix
+    T: CsrMatrix
+    F_u: Optional[CsrMatrix] = None
+    node_coords: Optional[np.ndarray] = None  # (n_nodes, 3) for the rigid-body near-null space
+
+    def total_dimension(self) -> int:
+        return self.n_u + self.n_t + self.n_p
+
+    def view(self) -> N.FpBlockSystem:
+        s = N.FpBlockSystem()
+        s.n_u, s.n_t, s.n_p = self.n_u, self.n_t, self.n_p
+        for nm in ("A", "C1", "Q1", "C2", "H", "Q2", "T"):
+            setattr(s, nm, getattr(self, nm).view())
+        s.F_u = (self.F_u or CsrMatrix.empty(0, self.n_u)).view()
+        return s
+
+
+@dataclass
+class AmgConfig:
+    strength_threshold: float = 0.08
+    max_coarse: int = 100
+    pre_sweeps: int = 1
+    post_sweeps: int = 1
+    smoother: str = "weighted_jacobi"  # the reference default "sgs" has no GPU path
+    prolongation_smoothing: bool = True
+    cycles_per_apply: int = 1
+    jacobi_omega: float = 2.0 / 3.0
+    stall_ratio: float = 0.9
+    max_levels: int = 25
+
+    def native(self) -> N.FpAmgConfig:
+        c = N.FpAmgConfig()
+        c.strength_threshold, c.max_coarse = self.strength_threshold, self.max_coarse
+        c.pre_sweeps, c.post_sweeps = self.pre_sweeps, self.post_sweeps
+        c.smoother = N.FP_SMOOTHER_JACOBI if self.smoother == "weighted_jacobi" else N.FP_SMOOTHER_SGS
+        c.prolongation_smoothing = int(self.prolongation_smoothing)
+        c.cycles_per_apply, c.jacobi_omega = self.cycles_per_apply, self.jacobi_omega
+        c.stall_ratio, c.max_levels = self.stall_ratio, self.max_levels
+        return c
+
+
+@dataclass
+class PrecondConfig:
+    variant: str = "tup"
+    inner: str = "amg"
+    amg: AmgConfig = field(default_factory=AmgConfig)
+
+    def native(self) -> N.FpPrecondConfig:
+        if self.inner != "amg":
+            raise ValueError("the GPU path implements inner = amg only")
+        if self.variant not in _VARIANTS:
+            raise ValueError(f"unknown variant {self.variant!r}")
+        c = N.FpPrecondConfig()
+        c.variant = _VARIANTS[self.variant]
+        c.amg = self.amg.native()
+        return c
+
+
+@dataclass
+class SolveStats:
+    iterations: int = 0
+    relative_residuals: list = field(default_factory=list)
+    converged: bool = False
+    breakdown: bool = False
+    restarts: int = 0
+    precond_applies: int = 0
+    device_seconds: float = 0.0
+
+
+def _vec(x, n: int):
+    """(pointer, mem kind, keepalive) for a NumPy array or a CUDA tensor of length n."""
+    if hasattr(x, "is_cuda") and x.is_cuda:
+        import torch
+
+        if x.dtype != torch.float64 or not x.is_contiguous() or x.numel() != n:
+            raise ValueError("device vectors must be contiguous float64 tensors of the operator dimension")
+        return C.c_void_p(x.data_ptr()), N.FP_MEM_DEVICE, x
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    if a.size != n:
+        raise ValueError(f"dimension mismatch: expected {n}, got {a.size}")
+    return C.c_void_p(a.ctypes.data), N.FP_MEM_HOST, a
+
+
+def _out_like(x, n: int):
+    if hasattr(x, "is_cuda") and x.is_cuda:
+        import torch
+
+        return torch.empty(n, dtype=torch.float64, device=x.device)
+    return np.empty(n)
+
+
+class BlockSystemOperator:
+    """Device-resident J; ``apply`` is BlockSystemOperator::apply (block.cpp:70-74)."""
+
+    def __init__(self, J: BlockSystem):
+        self.J = J
+        self._h = C.c_void_p()
+        N.check(N.lib.fp_system_create(C.byref(J.view()), C.byref(self._h)))
+        self._n = J.total_dimension()
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.lib.fp_system_destroy(self._h)
+            self._h = None
+
+    def dimension(self) -> int:
+        return self._n
+
+    def apply(self, x, y=None):
+        y = _out_like(x, self._n) if y is None else y
+        xp, mem, _ka = _vec(x, self._n)
+        yp, mem2, _kb = _vec(y, self._n)
+        if mem != mem2:
+            raise ValueError("x and y must live in the same memory space")
+        N.check(N.lib.fp_system_apply(self._h, xp, yp, mem))
+        return y
+
+    __call__ = apply
+
+    def block_scaling(self):
+        st, sp = C.c_double(), C.c_double()
+        N.check(N.lib.fp_block_scaling(self._h, C.byref(st), C.byref(sp)))
+        return st.value, sp.value
+
+
+class HostPreconditioner:
+    """Host-built preconditioner data (build_tpu / build_tup, precond.cpp:119-202)."""
+
+    def __init__(self, J: BlockSystem, cfg: PrecondConfig):
+        self._h = C.c_void_p()
+        coords = None if J.node_coords is None else np.ascontiguousarray(J.node_coords, dtype=np.float64)
+        cp = coords.ctypes.data_as(C.POINTER(C.c_double)) if coords is not None else None
+        nn = 0 if coords is None else coords.shape[0]
+        N.check(N.lib.fp_host_precond_build(C.byref(J.view()), C.byref(cfg.native()), cp, nn, C.byref(self._h)))
+        self.variant = cfg.variant
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.lib.fp_host_precond_destroy(self._h)
+            self._h = None
+
+    def level_sizes(self) -> list:
+        nl = C.c_int32()
+        N.check(N.lib.fp_host_precond_levels(self._h, C.byref(nl), None))
+        rows = (C.c_int32 * nl.value)()
+        N.check(N.lib.fp_host_precond_levels(self._h, None, rows))
+        return list(rows)
+
+    def matrix(self, what: int, level: int = 0) -> CsrMatrix:
+        r, c, nz = C.c_int32(), C.c_int32(), C.c_int64()
+        N.check(N.lib.fp_host_precond_matrix(self._h, what, level, C.byref(r), C.byref(c), C.byref(nz), None, None, None))
+        rp = np.zeros(r.value + 1, np.int64)
+        ci = np.zeros(nz.value, np.int32)
+        v = np.zeros(nz.value)
+        N.check(N.lib.fp_host_precond_matrix(
+            self._h, what, level, None, None, None, rp.ctypes.data_as(C.POINTER(C.c_int64)),
+            ci.ctypes.data_as(C.POINTER(C.c_int32)), v.ctypes.data_as(C.POINTER(C.c_double))))
+        return CsrMatrix(r.value, c.value, rp, ci, v)
+
+    def vector(self, what: int, level: int = 0) -> np.ndarray:
+        n = C.c_int64()
+        N.check(N.lib.fp_host_precond_vector(self._h, what, level, None, C.byref(n)))
+        out = np.zeros(n.value)
+        N.check(N.lib.fp_host_precond_vector(self._h, what, level, out.ctypes.data_as(C.POINTER(C.c_double)), None))
+        return out
+
+
+class GpuPreconditioner:
+    """Device-resident M^-1; ``apply`` is TpuOperator / TupOperator::apply (precond.cpp:285-296)."""
+
+    def __init__(self, op: BlockSystemOperator, handle: C.c_void_p, variant: str):
+        self.op, self._h, self.variant = op, handle, variant
+        self._n = op.dimension()
+
+    @classmethod
+    def from_host(cls, op: BlockSystemOperator, hp: HostPreconditioner) -> "GpuPreconditioner":
+        h = C.c_void_p()
+        N.check(N.lib.fp_precond_create(op._h, hp._h, C.byref(h)))
+        return cls(op, h, hp.variant)
+
+    @classmethod
+    def upload(cls, op: BlockSystemOperator, variant: str, h_blocks: np.ndarray, factor_matrix: CsrMatrix,
+               levels: Sequence[tuple], amg: AmgConfig) -> "GpuPreconditioner":
+        """Upload a reference-built hierarchy: levels = [(A_l, P_l or None, smoother_diag_l), ...]."""
+        keep = []
+        descs = (N.FpAmgLevelDesc * len(levels))()
+        for i, (A, P, d) in enumerate(levels):
+            d = np.ascontiguousarray(d, dtype=np.float64)
+            keep.append(d)
+            descs[i].A = A.view()
+            descs[i].P = (P if P is not None else CsrMatrix.empty(0, 0)).view()
+            descs[i].smoother_diag = d.ctypes.data_as(C.POINTER(C.c_double))
+        hb = np.ascontiguousarray(h_blocks, dtype=np.float64)
+        desc = N.FpPrecondDesc()
+        desc.variant = _VARIANTS[variant]
+        desc.h_blocks = hb.ctypes.data_as(C.POINTER(C.c_double))
+        desc.factor_matrix = factor_matrix.view()
+        desc.n_levels = len(levels)
+        desc.levels = descs
+        desc.amg = amg.native()
+        h = C.c_void_p()
+        N.check(N.lib.fp_precond_upload(op._h, C.byref(desc), C.byref(h)))
+        return cls(op, h, variant)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.lib.fp_precond_destroy(self._h)
+            self._h = None
+
+    def dimension(self) -> int:
+        return self._n
+
+    def apply(self, x, y=None):
+        y = _out_like(x, self._n) if y is None else y
+        xp, mem, _ka = _vec(x, self._n)
+        yp, _mem2, _kb = _vec(y, self._n)
+        N.check(N.lib.fp_precond_apply(self._h, xp, yp, mem))
+        return y
+
+    __call__ = apply
+
+    def amg_apply(self, r):
+        n_u = self.op.J.n_u
+        x = _out_like(r, n_u)
+        rp, mem, _ka = _vec(r, n_u)
+        xp, _m, _kb = _vec(x, n_u)
+        N.check(N.lib.fp_amg_apply(self._h, rp, xp, mem))
+        return x
+
+    def call_count(self) -> int:
+        return int(N.lib.fp_precond_inner_calls(self._h, 0))
+
+    def reset_count(self) -> None:
+        N.lib.fp_precond_inner_calls(self._h, 1)
+
+    def traffic(self):
+        ab, jb, la = C.c_double(), C.c_double(), C.c_int32()
+        N.check(N.lib.fp_precond_traffic(self._h, C.byref(ab), C.byref(la), C.byref(jb)))
+        return {"apply_bytes": ab.value, "apply_launches": la.value, "japply_bytes": jb.value}
+
+
+def _build(J: BlockSystem, cfg: PrecondConfig, op: Optional[BlockSystemOperator]):
+    op = op or BlockSystemOperator(J)
+    return GpuPreconditioner.from_host(op, HostPreconditioner(J, cfg))
+
+
+def build_tpu(J: BlockSystem, cfg: Optional[PrecondConfig] = None, op: Optional[BlockSystemOperator] = None):
+    cfg = cfg or PrecondConfig()
+    cfg.variant = "tpu"
+    return _build(J, cfg, op)
+
+
+def build_tup(J: BlockSystem, cfg: Optional[PrecondConfig] = None, op: Optional[BlockSystemOperator] = None,
+              star: bool = False):
+    cfg = cfg or PrecondConfig()
+    cfg.variant = "tup_star" if star else "tup"
+    return _build(J, cfg, op)
+
+
+def gmres(op: BlockSystemOperator, precond: GpuPreconditioner, b, tol: float, max_iter: int = 500,
+          restart: Optional[int] = None, scaled: bool = False, x=None):
+    """Right-preconditioned GMRES, x0 = 0 (gmres.hpp:29-33); ``restart`` gives GMRES(m);
+    ``scaled`` solves the driver's D J D system with D^-1 M D^-1 (driver.cpp:229-255)."""
+    n = op.dimension()
+    x = _out_like(b, n) if x is None else x
+    bp, mem, _ka = _vec(b, n)
+    xp, _m, _kb = _vec(x, n)
+    o = N.FpGmresOptions()
+    o.tol, o.restart, o.max_iter, o.scaled = tol, restart or max_iter, max_iter, int(scaled)
+    hist = np.zeros(max(1, max_iter))
+    st = N.FpSolveStats()
+    st.residual_history = hist.ctypes.data_as(C.POINTER(C.c_double))
+    st.history_capacity = hist.size
+    N.check(N.lib.fp_gmres(op._h, precond._h, bp, xp, mem, C.byref(o), C.byref(st)))
+    stats = SolveStats(st.iterations, list(hist[: st.history_len]), bool(st.converged), bool(st.breakdown),
+                       st.restarts, st.precond_applies, st.device_seconds)
+    return x, stats
+
+
+# ----------------------------------------------------------------- workloads
+class Workload:
+    """Synthetic BASELINE config (include/fracprec_b200_workload.h)."""
+
+    def __init__(self, config_id: Optional[int] = None, seed: int = 42, spec: Optional[dict] = None):
+        self._h = C.c_void_p()
+        if spec is None:
+            N.check(N.lib.fp_workload_preset(int(config_id), seed, C.byref(self._h)))
+        else:
+            s = N.FpWorkloadSpec()
+            s.cells[:] = spec["cells"]
+            s.length[:] = spec.get("length", (1.0, 1.0, 1.0))
+            fr = spec.get("fractures", [])
+            arr = (N.FpFractureSpec * max(1, len(fr)))()
+            for i, f in enumerate(fr):
+                arr[i] = N.FpFractureSpec(*f)
+            s.n_fractures, s.fractures = len(fr), arr
+            s.E_median, s.E_sigma_ln = spec.get("E_median", 10e9), spec.get("E_sigma_ln", 0.0)
+            s.E_layers, s.nu = spec.get("E_layers", 0), spec.get("nu", 0.25)
+            s.nu_lo, s.nu_hi = spec.get("nu_lo", 0.0), spec.get("nu_hi", 0.0)
+            s.frac_stick, s.frac_slip = spec.get("frac_stick", 0.7), spec.get("frac_slip", 0.2)
+            s.aperture_median = spec.get("aperture_median", 1e-4)
+            s.aperture_sigma_ln = spec.get("aperture_sigma_ln", 0.0)
+            s.seed = seed
+            N.check(N.lib.fp_workload_custom(C.byref(s), C.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            N.lib.fp_workload_destroy(self._h)
+            self._h = None
+
+    def info(self) -> dict:
+        c = (C.c_int32 * 4)()
+        N.check(N.lib.fp_workload_info(self._h, c))
+        return {"stick": c[0], "slip": c[1], "open": c[2], "fractures": c[3]}
+
+    def system(self) -> BlockSystem:
+        """Copies the generated blocks into an owned BlockSystem (NumPy)."""
+        v = N.FpBlockSystem()
+        N.check(N.lib.fp_workload_system(self._h, C.byref(v)))
+
+        def take(m: N.FpCsr) -> CsrMatrix:
+            if m.n_rows == 0:
+                return CsrMatrix.empty(0, m.n_cols)
+            rp = np.ctypeslib.as_array(m.row_offsets64, shape=(m.n_rows + 1,)).copy()
+            nz = int(rp[-1])
+            ci = np.ctypeslib.as_array(m.col_indices, shape=(nz,)).copy() if nz else np.zeros(0, np.int32)
+            vv = np.ctypeslib.as_array(m.values, shape=(nz,)).copy() if nz else np.zeros(0)
+            return CsrMatrix(m.n_rows, m.n_cols, rp, ci, vv)
+
+        xyz = C.POINTER(C.c_double)()
+        nn = C.c_int32()
+        N.check(N.lib.fp_workload_coords(self._h, C.byref(xyz), C.byref(nn)))
+        coords = np.ctypeslib.as_array(xyz, shape=(nn.value * 3,)).copy().reshape(-1, 3) if nn.value else None
+        blocks = {nm: take(getattr(v, nm)) for nm in ("A", "C1", "Q1", "C2", "H", "Q2", "T", "F_u")}
+        return BlockSystem(v.n_u, v.n_t, v.n_p, node_coords=coords, **blocks)

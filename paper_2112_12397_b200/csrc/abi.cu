@@ -1,0 +1,476 @@
+// C ABI of the B200 solve path (include/fracprec_b200.h).  No exception crosses
+// the boundary: every entry point maps std::invalid_argument /
+// numerical_error / CUDA failures to status codes (errors.hpp:15-24 of the
+// reference; fracprec.cpp:453-465 maps them to CLI exit codes the same way).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/fracprec_b200.h"
+#include "../../include/fracprec_b200_workload.h"
+#include "device/engine.cuh"
+#include "host/setup.hpp"
+#include "host/workload.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct cuda_failure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return FP_OK;
+  } catch (const fpb::numerical_error& e) {
+    g_err = e.what();
+    return FP_NUMERICAL_ERROR;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return FP_INVALID_ARGUMENT;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("allocation failure: ") + e.what();
+    return FP_INTERNAL_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return std::strstr(e.what(), "CUDA") ? FP_CUDA_ERROR : FP_INTERNAL_ERROR;
+  }
+}
+
+void need(bool ok, const char* what) {
+  if (!ok) throw std::invalid_argument(what);
+}
+
+fpb::Csr to_csr(const fp_csr& m, const char* name) {
+  const std::string nm(name);
+  need(m.n_rows >= 0 && m.n_cols >= 0, (nm + ": negative dimension").c_str());
+  fpb::Csr A(m.n_rows, m.n_cols);
+  if (m.n_rows == 0) return A;
+  need((m.row_offsets32 != nullptr) != (m.row_offsets64 != nullptr),
+       (nm + ": exactly one of row_offsets32 / row_offsets64 must be set").c_str());
+  for (int i = 0; i <= m.n_rows; ++i) A.rp[i] = m.row_offsets32 ? int64_t(m.row_offsets32[i]) : m.row_offsets64[i];
+  need(A.rp[0] == 0, (nm + ": row_offsets[0] != 0").c_str());
+  const int64_t nnz = A.rp[m.n_rows];
+  for (int i = 0; i < m.n_rows; ++i) need(A.rp[i] <= A.rp[i + 1], (nm + ": row_offsets not monotone").c_str());
+  need(nnz == 0 || (m.col_indices && m.values), (nm + ": null column/value array").c_str());
+  A.ci.assign(m.col_indices, m.col_indices + nnz);
+  A.v.assign(m.values, m.values + nnz);
+  for (int i = 0; i < m.n_rows; ++i)
+    for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+      need(A.ci[k] >= 0 && A.ci[k] < m.n_cols, (nm + ": column out of range").c_str());
+      if (k > A.rp[i]) need(A.ci[k - 1] < A.ci[k], (nm + ": columns not strictly increasing within a row").c_str());
+    }
+  return A;
+}
+
+fpb::HostSystem to_system(const fp_block_system& J) {
+  fpb::HostSystem H;
+  H.n_u = J.n_u, H.n_t = J.n_t, H.n_p = J.n_p;
+  H.A = to_csr(J.A, "A");
+  H.C1 = to_csr(J.C1, "C1");
+  H.Q1 = to_csr(J.Q1, "Q1");
+  H.C2 = to_csr(J.C2, "C2");
+  H.H = to_csr(J.H, "H");
+  H.Q2 = to_csr(J.Q2, "Q2");
+  H.T = to_csr(J.T, "T");
+  H.F_u = to_csr(J.F_u, "F_u");
+  H.check_shapes();
+  return H;
+}
+
+fpb::AmgOptions to_amg(const fp_amg_config& c) {
+  fpb::AmgOptions o;
+  o.strength_threshold = c.strength_threshold;
+  o.max_coarse = c.max_coarse;
+  o.pre_sweeps = c.pre_sweeps;
+  o.post_sweeps = c.post_sweeps;
+  o.smoother = c.smoother;
+  o.prolongation_smoothing = c.prolongation_smoothing != 0;
+  o.cycles_per_apply = c.cycles_per_apply;
+  o.jacobi_omega = c.jacobi_omega;
+  o.stall_ratio = c.stall_ratio;
+  o.max_levels = c.max_levels;
+  return o;
+}
+
+fp_csr view_of(const fpb::Csr& A) {
+  fp_csr v{};
+  v.n_rows = A.n_rows, v.n_cols = A.n_cols;
+  v.row_offsets64 = A.rp.data();
+  v.col_indices = A.ci.data();
+  v.values = A.v.data();
+  return v;
+}
+
+}  // namespace
+
+struct fp_system {
+  std::unique_ptr<fpd::DeviceSystem> dev;
+  cudaStream_t stream = nullptr;
+  fpd::DevBuf<double> xin, yout;
+  ~fp_system() {
+    dev.reset();
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+struct fp_precond {
+  fp_system* sys = nullptr;
+  std::unique_ptr<fpd::DevicePrecond> dev;
+  std::unique_ptr<fpd::GmresSolver> solver;
+  int solver_restart = 0;
+  fpd::DevBuf<double> xin, yout, bdev, xdev;
+};
+
+struct fp_host_precond {
+  fpb::HostPrecond hp;
+};
+
+struct fp_workload {
+  fpb::Workload w;
+};
+
+extern "C" {
+
+const char* fp_last_error(void) { return g_err.c_str(); }
+const char* fp_version(void) { return "fracprec_b200 0.1 (sm_100a)"; }
+
+void fp_amg_config_default(fp_amg_config* c) {
+  const fpb::AmgOptions o;
+  c->strength_threshold = o.strength_threshold;
+  c->max_coarse = o.max_coarse;
+  c->pre_sweeps = o.pre_sweeps;
+  c->post_sweeps = o.post_sweeps;
+  c->smoother = FP_SMOOTHER_JACOBI;
+  c->prolongation_smoothing = 1;
+  c->cycles_per_apply = o.cycles_per_apply;
+  c->jacobi_omega = o.jacobi_omega;
+  c->stall_ratio = o.stall_ratio;
+  c->max_levels = o.max_levels;
+}
+
+// ------------------------------------------------------------------ system
+int fp_system_create(const fp_block_system* J, fp_system** out) {
+  return guard([&] {
+    need(J && out, "fp_system_create: null argument");
+    const fpb::HostSystem H = to_system(*J);
+    auto s = std::make_unique<fp_system>();
+    fpd::cuda_check(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    s->dev = std::make_unique<fpd::DeviceSystem>(H);
+    const int n = s->dev->n();
+    s->xin.alloc(n), s->yout.alloc(n);
+    *out = s.release();
+  });
+}
+
+void fp_system_destroy(fp_system* s) { delete s; }
+
+int fp_system_dims(const fp_system* s, int32_t* n_u, int32_t* n_t, int32_t* n_p) {
+  return guard([&] {
+    need(s, "fp_system_dims: null handle");
+    if (n_u) *n_u = s->dev->n_u;
+    if (n_t) *n_t = s->dev->n_t;
+    if (n_p) *n_p = s->dev->n_p;
+  });
+}
+
+int fp_block_scaling(const fp_system* s, double* st, double* sp) {
+  return guard([&] {
+    need(s, "fp_block_scaling: null handle");
+    if (st) *st = s->dev->st;
+    if (sp) *sp = s->dev->sp;
+  });
+}
+
+int fp_system_apply(fp_system* s, const double* x, double* y, int32_t mem) {
+  return guard([&] {
+    need(s && x && y, "fp_system_apply: null argument");
+    const size_t bytes = sizeof(double) * size_t(s->dev->n());
+    const double* xd = x;
+    double* yd = y;
+    if (mem == FP_MEM_HOST) {
+      fpd::cuda_check(cudaMemcpyAsync(s->xin.get(), x, bytes, cudaMemcpyHostToDevice, s->stream), "H2D");
+      xd = s->xin.get(), yd = s->yout.get();
+    }
+    s->dev->enqueue_apply(xd, yd, 1.0, 1.0, s->stream);
+    if (mem == FP_MEM_HOST)
+      fpd::cuda_check(cudaMemcpyAsync(y, yd, bytes, cudaMemcpyDeviceToHost, s->stream), "D2H");
+    fpd::cuda_check(cudaStreamSynchronize(s->stream), "fp_system_apply");
+  });
+}
+
+// ------------------------------------------------------------- host build
+int fp_host_precond_build(const fp_block_system* J, const fp_precond_config* cfg, const double* coords,
+                          int32_t n_nodes, fp_host_precond** out) {
+  return guard([&] {
+    need(J && cfg && out, "fp_host_precond_build: null argument");
+    const fpb::HostSystem H = to_system(*J);
+    std::vector<std::array<double, 3>> xyz;
+    if (coords)
+      for (int v = 0; v < n_nodes; ++v) xyz.push_back({coords[3 * v], coords[3 * v + 1], coords[3 * v + 2]});
+    auto p = std::make_unique<fp_host_precond>();
+    p->hp = fpb::build_precond(H, cfg->variant, to_amg(cfg->amg), xyz);
+    *out = p.release();
+  });
+}
+
+void fp_host_precond_destroy(fp_host_precond* p) { delete p; }
+
+int fp_host_precond_levels(const fp_host_precond* p, int32_t* n_levels, int32_t* rows) {
+  return guard([&] {
+    need(p, "null handle");
+    const auto& L = p->hp.amg.levels;
+    if (n_levels) *n_levels = int32_t(L.size());
+    if (rows)
+      for (size_t l = 0; l < L.size(); ++l) rows[l] = L[l].A.n_rows;
+  });
+}
+
+int fp_host_precond_matrix(const fp_host_precond* p, int32_t what, int32_t level, int32_t* n_rows, int32_t* n_cols,
+                           int64_t* nnz, int64_t* rp, int32_t* ci, double* v) {
+  return guard([&] {
+    need(p, "null handle");
+    const auto& L = p->hp.amg.levels;
+    const fpb::Csr* M = nullptr;
+    if (what == 2)
+      M = p->hp.variant == fpb::kTpu ? nullptr : &p->hp.S2;
+    else {
+      need(level >= 0 && level < int(L.size()), "level out of range");
+      M = what == 0 ? &L[level].A : &L[level].P;
+    }
+    need(M != nullptr, "matrix not available for this variant (T is part of the system)");
+    if (n_rows) *n_rows = M->n_rows;
+    if (n_cols) *n_cols = M->n_cols;
+    if (nnz) *nnz = M->nnz();
+    if (rp) std::memcpy(rp, M->rp.data(), sizeof(int64_t) * M->rp.size());
+    if (ci) std::memcpy(ci, M->ci.data(), sizeof(int32_t) * M->ci.size());
+    if (v) std::memcpy(v, M->v.data(), sizeof(double) * M->v.size());
+  });
+}
+
+int fp_host_precond_vector(const fp_host_precond* p, int32_t what, int32_t level, double* out, int64_t* len) {
+  return guard([&] {
+    need(p, "null handle");
+    const std::vector<double>* v = nullptr;
+    if (what == 0) v = &p->hp.hblocks;
+    if (what == 1) v = p->hp.variant == fpb::kTpu ? &p->hp.T_diag : &p->hp.S_K;
+    if (what == 2) {
+      need(level >= 0 && level < int(p->hp.amg.levels.size()), "level out of range");
+      v = &p->hp.amg.levels[level].diag;
+    }
+    need(v != nullptr, "unknown vector");
+    if (len) *len = int64_t(v->size());
+    if (out) std::memcpy(out, v->data(), sizeof(double) * v->size());
+  });
+}
+
+// ----------------------------------------------------------------- upload
+int fp_precond_create(fp_system* s, const fp_host_precond* hp, fp_precond** out) {
+  return guard([&] {
+    need(s && hp && out, "fp_precond_create: null argument");
+    auto p = std::make_unique<fp_precond>();
+    p->sys = s;
+    p->dev = std::make_unique<fpd::DevicePrecond>(*s->dev, hp->hp);
+    const int n = s->dev->n();
+    p->xin.alloc(n), p->yout.alloc(n), p->bdev.alloc(n), p->xdev.alloc(n);
+    *out = p.release();
+  });
+}
+
+int fp_precond_upload(fp_system* s, const fp_precond_desc* d, fp_precond** out) {
+  return guard([&] {
+    need(s && d && out && d->levels && d->n_levels >= 1 && d->h_blocks, "fp_precond_upload: null argument");
+    need(d->variant >= FP_TPU && d->variant <= FP_TUP_STAR, "fp_precond_upload: unknown variant");
+    fpb::HostPrecond hp;
+    hp.variant = d->variant;
+    hp.hblocks.assign(d->h_blocks, d->h_blocks + 9 * size_t(s->dev->n_p));
+    const fpb::Csr F = to_csr(d->factor_matrix, "factor_matrix");
+    hp.factor.factor(F, d->variant == FP_TPU ? fpb::BandFactor::Kind::spd : fpb::BandFactor::Kind::general);
+    hp.amg.opt = to_amg(d->amg);
+    for (int l = 0; l < d->n_levels; ++l) {
+      fpb::HostLevel L;
+      L.A = to_csr(d->levels[l].A, "level A");
+      if (l > 0) L.P = to_csr(d->levels[l].P, "level P");
+      need(d->levels[l].smoother_diag != nullptr, "level smoother_diag is null");
+      L.diag.assign(d->levels[l].smoother_diag, d->levels[l].smoother_diag + L.A.n_rows);
+      hp.amg.levels.push_back(std::move(L));
+    }
+    const fpb::Csr& Ac = hp.amg.levels.back().A;
+    hp.amg.coarse.compute(Ac.to_dense(), Ac.n_rows);
+    hp.S = hp.amg.levels.front().A;
+    auto p = std::make_unique<fp_precond>();
+    p->sys = s;
+    p->dev = std::make_unique<fpd::DevicePrecond>(*s->dev, hp);
+    const int n = s->dev->n();
+    p->xin.alloc(n), p->yout.alloc(n), p->bdev.alloc(n), p->xdev.alloc(n);
+    *out = p.release();
+  });
+}
+
+void fp_precond_destroy(fp_precond* p) { delete p; }
+
+int fp_precond_apply(fp_precond* p, const double* x, double* y, int32_t mem) {
+  return guard([&] {
+    need(p && x && y, "fp_precond_apply: null argument");
+    cudaStream_t st = p->sys->stream;
+    const size_t bytes = sizeof(double) * size_t(p->sys->dev->n());
+    const double* xd = x;
+    double* yd = y;
+    if (mem == FP_MEM_HOST) {
+      fpd::cuda_check(cudaMemcpyAsync(p->xin.get(), x, bytes, cudaMemcpyHostToDevice, st), "H2D");
+      xd = p->xin.get(), yd = p->yout.get();
+    }
+    p->dev->enqueue_apply(xd, yd, 1.0, 1.0, st);
+    p->dev->inner_calls += p->dev->inner_per_apply();
+    if (mem == FP_MEM_HOST) fpd::cuda_check(cudaMemcpyAsync(y, yd, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    fpd::cuda_check(cudaStreamSynchronize(st), "fp_precond_apply");
+  });
+}
+
+int fp_amg_apply(fp_precond* p, const double* r, double* x, int32_t mem) {
+  return guard([&] {
+    need(p && r && x, "fp_amg_apply: null argument");
+    cudaStream_t st = p->sys->stream;
+    const size_t bytes = sizeof(double) * size_t(p->dev->amg->fine_n());
+    const double* rd = r;
+    double* xd = x;
+    if (mem == FP_MEM_HOST) {
+      fpd::cuda_check(cudaMemcpyAsync(p->xin.get(), r, bytes, cudaMemcpyHostToDevice, st), "H2D");
+      rd = p->xin.get(), xd = p->yout.get();
+    }
+    p->dev->amg->enqueue_apply(rd, xd, nullptr, st);
+    if (mem == FP_MEM_HOST) fpd::cuda_check(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    fpd::cuda_check(cudaStreamSynchronize(st), "fp_amg_apply");
+  });
+}
+
+int64_t fp_precond_inner_calls(fp_precond* p, int32_t reset) {
+  if (!p) return -1;
+  const int64_t c = p->dev->inner_calls;
+  if (reset) p->dev->inner_calls = 0;
+  return c;
+}
+
+int fp_precond_traffic(fp_precond* p, double* apply_bytes, int32_t* launches, double* japply_bytes) {
+  return guard([&] {
+    need(p, "null handle");
+    fpd::Ledger a, j;
+    cudaStream_t tmp;
+    fpd::cuda_check(cudaStreamCreateWithFlags(&tmp, cudaStreamNonBlocking), "stream");
+    cudaGraph_t g;
+    fpd::cuda_check(cudaStreamBeginCapture(tmp, cudaStreamCaptureModeThreadLocal), "capture");
+    p->dev->enqueue_apply(p->xin.get(), p->yout.get(), 1.0, 1.0, tmp, &a);
+    p->sys->dev->enqueue_apply(p->xin.get(), p->yout.get(), 1.0, 1.0, tmp, &j);
+    fpd::cuda_check(cudaStreamEndCapture(tmp, &g), "end capture");
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(tmp);
+    if (apply_bytes) *apply_bytes = a.bytes;
+    if (launches) *launches = a.launches;
+    if (japply_bytes) *japply_bytes = j.bytes;
+  });
+}
+
+int fp_gmres(fp_system* s, fp_precond* p, const double* b, double* x, int32_t mem, const fp_gmres_options* o,
+             fp_solve_stats* stats) {
+  return guard([&] {
+    need(s && p && b && x && o, "fp_gmres: null argument");
+    need(p->sys == s, "fp_gmres: preconditioner belongs to another system");
+    need(o->max_iter >= 0, "fp_gmres: max_iter must be >= 0");
+    const int restart = std::max(1, std::min(o->restart > 0 ? o->restart : o->max_iter, std::max(1, o->max_iter)));
+    if (!p->solver || p->solver_restart != restart) {
+      p->solver.reset();
+      p->solver = std::make_unique<fpd::GmresSolver>(*s->dev, *p->dev, restart);
+      p->solver_restart = restart;
+    }
+    cudaStream_t st = s->stream;
+    const size_t bytes = sizeof(double) * size_t(s->dev->n());
+    const double* bd = b;
+    double* xd = x;
+    if (mem == FP_MEM_HOST) {
+      fpd::cuda_check(cudaMemcpyAsync(p->bdev.get(), b, bytes, cudaMemcpyHostToDevice, st), "H2D");
+      bd = p->bdev.get(), xd = p->xdev.get();
+    }
+    fpd::SolveOptions so;
+    so.tol = o->tol, so.restart = restart, so.max_iter = o->max_iter, so.scaled = o->scaled != 0;
+    const fpd::SolveResult r = p->solver->solve(bd, xd, so, st);
+    if (mem == FP_MEM_HOST) fpd::cuda_check(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    fpd::cuda_check(cudaStreamSynchronize(st), "fp_gmres");
+    if (stats) {
+      stats->iterations = r.iterations;
+      stats->converged = r.converged;
+      stats->breakdown = r.breakdown;
+      stats->restarts = r.restarts;
+      stats->precond_applies = r.precond_applies;
+      stats->final_rel_residual = r.final_rel_residual;
+      stats->device_seconds = r.device_seconds;
+      stats->history_len = int32_t(r.history.size());
+      if (stats->residual_history)
+        for (int i = 0; i < stats->history_capacity && i < int(r.history.size()); ++i)
+          stats->residual_history[i] = r.history[i];
+    }
+  });
+}
+
+// -------------------------------------------------------------- workload
+int fp_workload_preset(int32_t id, uint64_t seed, fp_workload** out) {
+  return guard([&] {
+    need(out != nullptr, "fp_workload_preset: null out");
+    auto w = std::make_unique<fp_workload>();
+    w->w = fpb::generate_workload(fpb::preset_config(id, seed));
+    *out = w.release();
+  });
+}
+
+int fp_workload_custom(const fp_workload_spec* sp, fp_workload** out) {
+  return guard([&] {
+    need(sp && out, "fp_workload_custom: null argument");
+    fpb::WorkloadSpec s;
+    for (int d = 0; d < 3; ++d) s.cells[d] = sp->cells[d], s.length[d] = sp->length[d];
+    for (int f = 0; f < sp->n_fractures; ++f) {
+      const fp_fracture_spec& q = sp->fractures[f];
+      s.fractures.push_back({q.normal_axis, q.coord, q.lo1, q.hi1, q.lo2, q.hi2});
+    }
+    s.E_median = sp->E_median, s.E_sigma_ln = sp->E_sigma_ln, s.E_layers = sp->E_layers;
+    s.nu = sp->nu, s.nu_lo = sp->nu_lo, s.nu_hi = sp->nu_hi;
+    s.frac_stick = sp->frac_stick, s.frac_slip = sp->frac_slip;
+    s.aperture_median = sp->aperture_median, s.aperture_sigma_ln = sp->aperture_sigma_ln;
+    s.seed = sp->seed;
+    auto w = std::make_unique<fp_workload>();
+    w->w = fpb::generate_workload(s);
+    *out = w.release();
+  });
+}
+
+void fp_workload_destroy(fp_workload* w) { delete w; }
+
+int fp_workload_system(const fp_workload* w, fp_block_system* J) {
+  return guard([&] {
+    need(w && J, "null argument");
+    const fpb::HostSystem& H = w->w.J;
+    J->n_u = H.n_u, J->n_t = H.n_t, J->n_p = H.n_p;
+    J->A = view_of(H.A), J->C1 = view_of(H.C1), J->Q1 = view_of(H.Q1), J->C2 = view_of(H.C2);
+    J->H = view_of(H.H), J->Q2 = view_of(H.Q2), J->T = view_of(H.T), J->F_u = view_of(H.F_u);
+  });
+}
+
+int fp_workload_coords(const fp_workload* w, const double** xyz, int32_t* n_nodes) {
+  return guard([&] {
+    need(w && xyz && n_nodes, "null argument");
+    *xyz = w->w.coords.empty() ? nullptr : w->w.coords[0].data();
+    *n_nodes = int32_t(w->w.coords.size());
+  });
+}
+
+int fp_workload_info(const fp_workload* w, int32_t* c) {
+  return guard([&] {
+    need(w && c, "null argument");
+    c[0] = w->w.n_stick, c[1] = w->w.n_slip, c[2] = w->w.n_open, c[3] = w->w.n_fractures;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+// Device-side data layout of the B200 solve path.
+//
+// Every sparse operator is stored "sliced by 32 rows" (SELL-32): within a slice,
+// the k-th stored entry of each of the 32 rows is contiguous, so one warp step
+// is one fully coalesced 256-byte load per stream.  One thread owns one output
+// row and accumulates it left to right in the reference's CSR order
+// (csr.cpp:109-119), which makes every SpMV bitwise equal to the CPU oracle
+// while streaming HBM at full width.
+//
+//  * Sell  — scalar CSR rows (C1, Q1, C2, H, Q2, T, coarse A_l, P_l, R_l = P_l^T).
+//  * Bsr3  — 3x3-block rows (A and the inner-AMG fine operator S~ / S1): per
+//            slice and block slot k, 9 x 32 doubles laid out [li][j][lane], read
+//            by three warps (li = 0,1,2), plus one int block column per slot.
+//            8.44 B per scalar nonzero instead of CSR's 12 B.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace fpd {
+
+struct SellView {
+  int n_rows = 0;
+  const long long* slice_off = nullptr;  // slot index of (slice, k=0, lane=0)
+  const int* row_len = nullptr;
+  const int* cols = nullptr;
+  const double* vals = nullptr;
+};
+
+struct Bsr3View {
+  int n_brows = 0;
+  const long long* slice_off = nullptr;  // block-slot index of (slice, k=0, lane=0)
+  const int* brow_len = nullptr;
+  const int* bcols = nullptr;            // one per block slot
+  const double* vals = nullptr;          // 9 per block slot, [li][j][lane] inside each (slice,k) group
+};
+
+struct BandView {
+  int n = 0, kl = 0, ku = 0, n_blocks = 0;
+  const int* block_start = nullptr;
+  const double* Lc = nullptr;    // n * kl, column j multipliers L(j+1+r, j)
+  const double* diag = nullptr;  // D (spd) or U diagonal (general)
+  const double* Lr = nullptr;    // spd: n * kl, L(j, j-1-r)
+  const double* Uc = nullptr;    // general: n * ku, U(j-1-r, j)
+  const int* piv = nullptr;      // general: absolute row swapped with j at step j
+  int spd = 1;
+};
+
+struct DenseLUView {  // coarse-level full-pivot LU, column-major n x n
+  int n = 0, rank = 0;
+  const double* lu = nullptr;
+  const int* prow = nullptr;
+  const int* pcol = nullptr;
+};
+
+// Arnoldi step status, written by the device into mapped host memory
+struct GmresStatus {
+  double est, hnext, wnorm_pre;
+  int happy, nonfinite, reorth, m;
+};
+
+// ---------------------------------------------------------------- buffers
+void cuda_check(cudaError_t e, const char* what);
+
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { alloc(n); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = o.p_, n_ = o.n_;
+      o.p_ = nullptr, o.n_ = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t n) {
+    release();
+    n_ = n;
+    if (n) cuda_check(cudaMalloc(&p_, n * sizeof(T)), "cudaMalloc");
+  }
+  void upload(const T* h, size_t n) {
+    alloc(n);
+    if (n) cuda_check(cudaMemcpy(p_, h, n * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+  }
+  void upload(const std::vector<T>& h) { upload(h.data(), h.size()); }
+  void zero() {
+    if (n_) cuda_check(cudaMemset(p_, 0, n_ * sizeof(T)), "cudaMemset");
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  size_t bytes() const { return n_ * sizeof(T); }
+
+ private:
+  void release() {
+    if (p_) cudaFree(p_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+}  // namespace fpd

@@ -1,0 +1,597 @@
+// Device engine implementation (see engine.cuh).
+#include "engine.cuh"
+
+#include <omp.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "gmres_kernels.cuh"
+#include "kernels.cuh"
+
+namespace fpd {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+inline unsigned blocks_for(long long n, int t) { return unsigned((n + t - 1) / t); }
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, c = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    return c;
+  }();
+  return n;
+}
+
+template <class G, class E>
+void launch_sell(const DSell& A, const G& g, const E& e, cudaStream_t s) {
+  if (A.n_rows == 0) return;
+  sell_kernel<<<blocks_for(A.n_rows, 256), 256, 0, s>>>(A.view(), g, e);
+  cuda_check(cudaGetLastError(), "sell_kernel launch");
+}
+
+template <class G, class E>
+void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s) {
+  if (A.n_brows == 0) return;
+  bsr3_kernel<<<blocks_for((long long)A.n_slices * 96, kBsrThreads), kBsrThreads, 0, s>>>(A.view(), g, e);
+  cuda_check(cudaGetLastError(), "bsr3_kernel launch");
+}
+
+template <class G, class E>
+void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s) {
+  if (L.bsr3)
+    launch_bsr3(L.Ab, g, e, s);
+  else
+    launch_sell(L.As, g, e, s);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ format upload
+DSell make_sell(const fpb::Csr& A) {
+  DSell D;
+  D.n_rows = A.n_rows, D.n_cols = A.n_cols, D.nnz = A.nnz();
+  D.n_slices = (A.n_rows + kSlice - 1) / kSlice;
+  std::vector<long long> off(static_cast<size_t>(D.n_slices) + 1, 0);
+  std::vector<int> len(static_cast<size_t>(A.n_rows));
+  for (int i = 0; i < A.n_rows; ++i) len[i] = A.row_len(i);
+  for (int s = 0; s < D.n_slices; ++s) {
+    int mx = 0;
+    for (int i = s * kSlice; i < std::min(A.n_rows, (s + 1) * kSlice); ++i) mx = std::max(mx, len[i]);
+    off[s + 1] = off[s] + (long long)mx * kSlice;
+  }
+  D.slots = off[D.n_slices];
+  std::vector<int> cols(static_cast<size_t>(D.slots), 0);
+  std::vector<double> vals(static_cast<size_t>(D.slots), 0.0);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < A.n_rows; ++i) {
+    const long long base = off[i / kSlice] + (i % kSlice);
+    for (int k = 0; k < len[i]; ++k) {
+      cols[base + (long long)k * kSlice] = A.ci[A.rp[i] + k];
+      vals[base + (long long)k * kSlice] = A.v[A.rp[i] + k];
+    }
+  }
+  D.off.upload(off);
+  D.len.upload(len);
+  D.cols.upload(cols);
+  D.vals.upload(vals);
+  return D;
+}
+
+DBsr3 make_bsr3(const fpb::Csr& A) {
+  if (A.n_rows != A.n_cols || A.n_rows % 3 != 0) throw std::invalid_argument("make_bsr3: needs a square matrix with n % 3 == 0");
+  DBsr3 D;
+  const int nb = A.n_rows / 3;
+  D.n_brows = nb;
+  D.n_slices = (nb + kSlice - 1) / kSlice;
+  // block columns of each block row: union over its three scalar rows
+  std::vector<std::vector<int>> bc(static_cast<size_t>(nb));
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int b = 0; b < nb; ++b) {
+    auto& L = bc[b];
+    for (int li = 0; li < 3; ++li)
+      for (int64_t k = A.rp[3 * b + li]; k < A.rp[3 * b + li + 1]; ++k) L.push_back(A.ci[k] / 3);
+    std::sort(L.begin(), L.end());
+    L.erase(std::unique(L.begin(), L.end()), L.end());
+  }
+  std::vector<long long> off(static_cast<size_t>(D.n_slices) + 1, 0);
+  std::vector<int> len(static_cast<size_t>(nb));
+  for (int b = 0; b < nb; ++b) len[b] = int(bc[b].size()), D.nblocks += len[b];
+  for (int s = 0; s < D.n_slices; ++s) {
+    int mx = 0;
+    for (int b = s * kSlice; b < std::min(nb, (s + 1) * kSlice); ++b) mx = std::max(mx, len[b]);
+    off[s + 1] = off[s] + (long long)mx * kSlice;
+  }
+  D.slots = off[D.n_slices];
+  std::vector<int> bcols(static_cast<size_t>(D.slots), 0);
+  std::vector<double> vals(static_cast<size_t>(D.slots) * 9, 0.0);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int b = 0; b < nb; ++b) {
+    const int s = b / kSlice, lane = b % kSlice;
+    const auto& L = bc[b];
+    for (int k = 0; k < len[b]; ++k) bcols[off[s] + (long long)k * kSlice + lane] = L[k];
+    for (int li = 0; li < 3; ++li) {
+      size_t slot = 0;
+      for (int64_t q = A.rp[3 * b + li]; q < A.rp[3 * b + li + 1]; ++q) {
+        const int c = A.ci[q], cb = c / 3, j = c % 3;
+        while (L[slot] != cb) ++slot;
+        vals[(off[s] + (long long)slot * kSlice) * 9 + (li * 3 + j) * kSlice + lane] = A.v[q];
+      }
+    }
+  }
+  D.off.upload(off);
+  D.len.upload(len);
+  D.bcols.upload(bcols);
+  D.vals.upload(vals);
+  return D;
+}
+
+// ------------------------------------------------------------------ system
+DeviceSystem::DeviceSystem(const fpb::HostSystem& J) {
+  J.check_shapes();
+  n_u = J.n_u, n_t = J.n_t, n_p = J.n_p;
+  a_bsr3 = n_u % 3 == 0;
+  if (a_bsr3)
+    A = make_bsr3(J.A);
+  else
+    A_sell = make_sell(J.A);
+  C1 = make_sell(J.C1);
+  Q1 = make_sell(J.Q1);
+  C2 = make_sell(J.C2);
+  H = make_sell(J.H);
+  Q2 = make_sell(J.Q2);
+  T = make_sell(J.T);
+  auto max_abs_diag = [](const fpb::Csr& M) {
+    double m = 0.0;
+    for (double v : fpb::diag_extract(M)) m = std::max(m, std::abs(v));
+    return m;
+  };
+  const double da = max_abs_diag(J.A), dh = max_abs_diag(J.H), dt = max_abs_diag(J.T);
+  if (da > 0.0 && dh > 0.0) st = std::sqrt(da / dh);
+  if (da > 0.0 && dt > 0.0) sp = std::sqrt(da / dt);
+}
+
+double DeviceSystem::bytes_apply() const {
+  const double nu = n_u, nt = n_t, np = n_p;
+  return (a_bsr3 ? A.matrix_bytes() : A_sell.matrix_bytes()) + C1.matrix_bytes() + Q1.matrix_bytes() + C2.matrix_bytes() + H.matrix_bytes() +
+         Q2.matrix_bytes() + T.matrix_bytes() + 8.0 * (2 * (nu + nt + np));
+}
+
+void DeviceSystem::enqueue_apply(const double* x, double* y, double st_, double sp_, cudaStream_t s, Ledger* L) const {
+  const double* xu = x;
+  const double* xt = x + n_u;
+  const double* xp = x + n_u + n_t;
+  const EJu ju{C1.view(), Q1.view(), xt, xp, st_, sp_, y};
+  if (a_bsr3)
+    launch_bsr3(A, GPlain{xu}, ju, s);
+  else
+    launch_sell(A_sell, GPlain{xu}, ju, s);
+  if (L) L->add((a_bsr3 ? A.matrix_bytes() : A_sell.matrix_bytes()) + C1.matrix_bytes() + Q1.matrix_bytes() + 8.0 * (2.0 * n_u + n_t + n_p));
+  const int m = n_t + n_p;
+  if (m > 0) {
+    jtp_kernel<<<blocks_for(m, 256), 256, 0, s>>>(C2.view(), H.view(), Q2.view(), T.view(), xu, xt, xp, st_, sp_,
+                                                   y + n_u, y + n_u + n_t);
+    cuda_check(cudaGetLastError(), "jtp_kernel launch");
+    if (L) L->add(C2.matrix_bytes() + H.matrix_bytes() + Q2.matrix_bytes() + T.matrix_bytes() + 8.0 * (2.0 * m));
+  }
+}
+
+// -------------------------------------------------------------------- AMG
+DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
+  opt = h.opt;
+  if (opt.smoother != 0)
+    throw std::invalid_argument(
+        "GPU AMG requires smoother = weighted_jacobi (the reference's symmetric Gauss-Seidel is sequential; "
+        "see DESIGN.md)");
+  const int L = int(h.levels.size());
+  lv.resize(static_cast<size_t>(L));
+  for (int l = 0; l < L; ++l) {
+    const fpb::HostLevel& H = h.levels[l];
+    DeviceLevel& D = lv[l];
+    D.n = H.A.n_rows;
+    if (l + 1 < L || L == 1) {
+      // coarsest level is solved densely; its A is not needed on the device
+      if (l == 0 && fine_bsr3 && H.A.n_rows % 3 == 0) {
+        D.bsr3 = true;
+        D.Ab = make_bsr3(H.A);
+      } else {
+        D.As = make_sell(H.A);
+      }
+    }
+    if (l > 0) {
+      D.P = make_sell(H.P);
+      D.R = make_sell(fpb::transpose(H.P));
+    }
+    D.d.upload(H.diag);
+    D.b.alloc(D.n), D.x.alloc(D.n), D.xt.alloc(D.n), D.xt2.alloc(D.n), D.r.alloc(D.n);
+  }
+  // coarse LU, column-major for contiguous column sweeps
+  coarse_n = h.coarse.n;
+  coarse_rank = h.coarse.rank;
+  std::vector<double> cm(size_t(coarse_n) * coarse_n);
+  for (int i = 0; i < coarse_n; ++i)
+    for (int j = 0; j < coarse_n; ++j) cm[size_t(j) * coarse_n + i] = h.coarse.lu[size_t(i) * coarse_n + j];
+  lu.upload(cm);
+  prow.upload(h.coarse.prow);
+  pcol.upload(h.coarse.pcol);
+  const size_t smem = sizeof(double) * size_t(std::max(coarse_n, 1));
+  if (smem > 48 * 1024)
+    cuda_check(cudaFuncSetAttribute(coarse_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+               "coarse smem attribute");
+  if (opt.cycles_per_apply > 1) top_x.alloc(fine_n()), top_res.alloc(fine_n()), top_dx.alloc(fine_n());
+}
+
+std::vector<int> DeviceAmg::level_sizes() const {
+  std::vector<int> s;
+  for (const auto& l : lv) s.push_back(l.n);
+  return s;
+}
+
+void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from, cudaStream_t s, Ledger* Lg) {
+  DeviceLevel& L = lv[l];
+  const int last = n_levels() - 1;
+  const double nd = L.n;
+  if (l == last) {
+    double* out = sub_from ? L.xt.get() : x;
+    coarse_solve_kernel<<<1, kCoarseThreads, sizeof(double) * std::max(coarse_n, 1), s>>>(
+        DenseLUView{coarse_n, coarse_rank, lu.get(), prow.get(), pcol.get()}, b, out);
+    cuda_check(cudaGetLastError(), "coarse_solve_kernel launch");
+    if (Lg) Lg->add(8.0 * coarse_n * double(coarse_n) + 16.0 * coarse_n + 8.0 * coarse_n);
+    if (sub_from) {
+      axpy_kernel<<<blocks_for(L.n, 256), 256, 0, s>>>(L.n, sub_from, out, -1.0, x);
+      if (Lg) Lg->add(24.0 * nd);
+    }
+    return;
+  }
+  const double w = opt.jacobi_omega;
+  const double* d = L.d.get();
+  const double A_b = L.a_bytes();
+  double* cur = L.xt.get();
+  if (opt.pre_sweeps == 1) {
+    // fused: x = (w b)/d (first sweep from zero) and r = b - A x with x gathered on the fly
+    launch_level(L, GPresmooth{b, d, w}, EResidPre{b, d, w, cur, L.r.get()}, s);
+    if (Lg) Lg->add(A_b + 16.0 * nd + 8.0 * 4 * nd);
+  } else {
+    presmooth_kernel<<<blocks_for(L.n, 256), 256, 0, s>>>(L.n, b, d, w, cur);
+    if (Lg) Lg->add(24.0 * nd);
+    for (int it = 1; it < opt.pre_sweeps; ++it) {
+      double* nxt = cur == L.xt.get() ? L.xt2.get() : L.xt.get();
+      launch_level(L, GPlain{cur}, EJacobi{b, d, w, cur, nxt}, s);
+      if (Lg) Lg->add(A_b + 8.0 * nd + 8.0 * 4 * nd);
+      cur = nxt;
+    }
+    launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s);
+    if (Lg) Lg->add(A_b + 8.0 * nd + 16.0 * nd);
+  }
+  DeviceLevel& C = lv[l + 1];
+  launch_sell(C.R, GPlain{L.r.get()}, EStore{C.b.get()}, s);  // r_c = P^T r  (amg.cpp:166)
+  if (Lg) Lg->add(C.R.matrix_bytes() + 8.0 * nd + 8.0 * C.n);
+  vcycle(l + 1, C.b.get(), C.x.get(), nullptr, s, Lg);
+  launch_sell(C.P, GPlain{C.x.get()}, EAddTo{cur, cur}, s);  // x += P e_c  (amg.cpp:168-169)
+  if (Lg) Lg->add(C.P.matrix_bytes() + 8.0 * C.n + 16.0 * nd);
+  for (int it = 0; it < opt.post_sweeps; ++it) {
+    const bool final_sweep = it + 1 == opt.post_sweeps;
+    double* nxt = final_sweep ? x : (cur == L.xt.get() ? L.xt2.get() : L.xt.get());
+    if (final_sweep && sub_from)
+      launch_level(L, GPlain{cur}, EJacobiSubFrom{b, d, w, cur, sub_from, nxt}, s);
+    else
+      launch_level(L, GPlain{cur}, EJacobi{b, d, w, cur, nxt}, s);
+    if (Lg) Lg->add(A_b + 8.0 * nd + 8.0 * (4 + (final_sweep && sub_from)) * nd);
+    cur = nxt;
+  }
+}
+
+void DeviceAmg::enqueue_apply(const double* r, double* x, const double* sub_from, cudaStream_t s, Ledger* Lg) {
+  if (opt.cycles_per_apply <= 1) {
+    vcycle(0, r, x, sub_from, s, Lg);
+    return;
+  }
+  const int n = fine_n();
+  vcycle(0, r, top_x.get(), nullptr, s, Lg);
+  for (int c = 1; c < opt.cycles_per_apply; ++c) {  // residual-correction cycles (amg.cpp:297-303)
+    launch_level(lv[0], GPlain{top_x.get()}, EResid{r, top_res.get()}, s);
+    if (Lg) Lg->add(lv[0].a_bytes() + 24.0 * n);
+    vcycle(0, top_res.get(), top_dx.get(), nullptr, s, Lg);
+    add_inplace_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, top_x.get(), top_dx.get());
+    if (Lg) Lg->add(24.0 * n);
+  }
+  if (sub_from)
+    axpy_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, sub_from, top_x.get(), -1.0, x);
+  else
+    cuda_check(cudaMemcpyAsync(x, top_x.get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, s), "copy");
+  if (Lg) Lg->add(24.0 * n);
+}
+
+// --------------------------------------------------------------- precond
+DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) : variant(hp.variant), sys(&s) {
+  if (hp.S.n_rows != s.n_u) throw std::invalid_argument("precond upload: inner operator size != n_u");
+  if (int(hp.hblocks.size()) != 9 * s.n_p) throw std::invalid_argument("precond upload: H~ blocks size != 9 n_p");
+  amg = std::make_unique<DeviceAmg>(hp.amg, true);
+  // pre-factor the H~ blocks with the reference's lu3_factor (deterministic)
+  std::vector<double> lu(hp.hblocks);
+  std::vector<int> piv(static_cast<size_t>(s.n_p));
+  for (int f = 0; f < s.n_p; ++f) {
+    int p[3];
+    if (!fpb::lu3_factor(lu.data() + 9 * size_t(f), p))
+      throw fpb::numerical_error("bdiag3_solve: singular 3x3 block at index " + std::to_string(f));
+    piv[f] = p[0] | (p[1] << 2) | (p[2] << 4);
+  }
+  hlu.upload(lu);
+  hpiv.upload(piv);
+  const fpb::BandFactor& F = hp.factor;
+  if (F.n != s.n_p) throw std::invalid_argument("precond upload: factor size != n_p");
+  band_start.upload(F.block_start);
+  band_Lc.upload(F.Lc);
+  band_diag.upload(F.diag);
+  if (F.kind == fpb::BandFactor::Kind::spd)
+    band_Lr.upload(F.Lr);
+  else
+    band_Uc.upload(F.Uc), band_piv.upload(F.piv);
+  for (size_t b = 0; b + 1 < F.block_start.size(); ++b)
+    band_max_block = std::max(band_max_block, F.block_start[b + 1] - F.block_start[b]);
+  band = BandView{F.n, F.kl, F.ku, int(F.block_start.size()) - 1, band_start.get(), band_Lc.get(), band_diag.get(),
+                  band_Lr.get(), band_Uc.get(), band_piv.get(), F.kind == fpb::BandFactor::Kind::spd ? 1 : 0};
+  const size_t smem = sizeof(double) * size_t(std::max(band_max_block, 1));
+  if (smem > 227 * 1024) throw std::invalid_argument("precond upload: fracture block too large for the band solver");
+  if (smem > 48 * 1024)
+    cuda_check(cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+               "band smem attribute");
+  const int nu = s.n_u, nt = s.n_t, np = s.n_p;
+  tt.alloc(nt), tu.alloc(nu), tp.alloc(np), su.alloc(nu), sp_.alloc(np), vp.alloc(np), tu2.alloc(nu), vu2.alloc(nu);
+}
+
+void DevicePrecond::enqueue_band(const double* rhs, double rs, double* out, double* out2, const double* sub, double os,
+                                 int mode, cudaStream_t s, Ledger* L) {
+  if (band.n == 0) return;
+  band_solve_kernel<<<band.n_blocks, 32, sizeof(double) * std::max(band_max_block, 1), s>>>(band, rhs, rs, out, out2,
+                                                                                              sub, os, mode);
+  cuda_check(cudaGetLastError(), "band_solve_kernel launch");
+  if (L) {
+    const double n = band.n;
+    const double fb = 8.0 * n * (band.kl + (band.spd ? band.kl : band.ku)) + 8.0 * n + (band.spd ? 0.0 : 4.0 * n);
+    L->add(fb + 8.0 * n * (2 + (mode == 1) + (mode == 2)));
+  }
+}
+
+void DevicePrecond::enqueue_apply(const double* x, double* y, double at, double ap, cudaStream_t s, Ledger* L) {
+  const DeviceSystem& S = *sys;
+  const int nu = S.n_u, nt = S.n_t, np = S.n_p;
+  const double* xu = x;
+  const double* xt = x + nu;
+  const double* xp = x + nu + nt;
+  double* yu = y;
+  double* yt = y + nu;
+  double* yp = y + nu + nt;
+  const unsigned fb = blocks_for(np, 256);
+  auto hin = [&](double* neg_out) {
+    if (np == 0) return;
+    hsolve_in_kernel<<<fb, 256, 0, s>>>(np, hlu.get(), hpiv.get(), xt, at, tt.get(), neg_out);
+    cuda_check(cudaGetLastError(), "hsolve_in launch");
+    if (L) L->add(72.0 * np + 4.0 * np + 8.0 * nt * (2 + (neg_out != nullptr)));
+  };
+  auto hout = [&](const double* vu) {
+    if (np == 0) return;
+    hsolve_out_kernel<<<fb, 256, 0, s>>>(np, S.C2.view(), vu, hlu.get(), hpiv.get(), tt.get(), at, yt);
+    cuda_check(cudaGetLastError(), "hsolve_out launch");
+    if (L) L->add(S.C2.matrix_bytes() + 8.0 * nu + 72.0 * np + 4.0 * np + 16.0 * nt);
+  };
+  if (variant == fpb::kTpu) {
+    enqueue_band(xp, ap, tp.get(), nullptr, nullptr, 1.0, 0, s, L);  // t_p = T^-1 w_p
+    hin(nullptr);                                                    // t_t = H~^-1 w_t
+    tpu_tu_kernel<<<blocks_for(nu, 256), 256, 0, s>>>(S.C1.view(), S.Q1.view(), xu, tt.get(), tp.get(), tu.get());
+    cuda_check(cudaGetLastError(), "tpu_tu launch");
+    if (L) L->add(S.C1.matrix_bytes() + S.Q1.matrix_bytes() + 8.0 * (2.0 * nu + nt + np));
+    amg->enqueue_apply(tu.get(), yu, nullptr, s, L);  // v_u = AMG(S~) t_u
+    launch_sell(S.Q2, GPlain{yu}, EStore{sp_.get()}, s);  // s_p = Q2 v_u
+    if (L) L->add(S.Q2.matrix_bytes() + 8.0 * (nu + np));
+    enqueue_band(sp_.get(), 1.0, yp, nullptr, tp.get(), ap, 1, s, L);  // v_p = t_p - T^-1 s_p
+    hout(yu);                                                          // v_t = H~^-1 C2 v_u - t_t
+    return;
+  }
+  hin(variant == fpb::kTupStar ? yt : nullptr);  // t_t = H~^-1 w_t   (t-u-p*: v_t = -t_t)
+  launch_sell(S.C1, GPlain{tt.get()}, EAddTo{xu, tu.get()}, s);  // t_u = w_u + C1 t_t
+  if (L) L->add(S.C1.matrix_bytes() + 8.0 * (nt + 2.0 * nu));
+  double* s_u = variant == fpb::kTupStar ? yu : su.get();
+  amg->enqueue_apply(tu.get(), s_u, nullptr, s, L);  // s_u = AMG(S1) t_u
+  launch_sell(S.Q2, GPlain{s_u}, ESubFromScaled{xp, ap, tp.get()}, s);  // t_p = w_p - Q2 s_u
+  if (L) L->add(S.Q2.matrix_bytes() + 8.0 * (nu + 2.0 * np));
+  enqueue_band(tp.get(), 1.0, vp.get(), yp, nullptr, ap, 2, s, L);  // v_p = S~2^-1 t_p
+  if (variant == fpb::kTupStar) return;
+  launch_sell(S.Q1, GPlain{vp.get()}, EStore{tu2.get()}, s);  // t_u2 = Q1 v_p
+  if (L) L->add(S.Q1.matrix_bytes() + 8.0 * (np + nu));
+  amg->enqueue_apply(tu2.get(), yu, su.get(), s, L);  // v_u = s_u - AMG(S1) t_u2
+  hout(yu);                                           // v_t = H~^-1 C2 v_u - t_t
+}
+
+// ------------------------------------------------------------------ GMRES
+GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart)
+    : sys_(sys), pc_(pc), restart_(restart), ldr_(restart + 1) {
+  if (restart < 1) throw std::invalid_argument("gmres: restart must be >= 1");
+  n_ = sys.n();
+  ldv_ = (n_ + 31) / 32 * 32;
+  V_.alloc(size_t(ldr_ + 1) * ldv_);  // V_0 .. V_restart plus staging column
+  z_.alloc(n_), jout_.alloc(n_), xtot_.alloc(n_), r_.alloc(n_), dx_.alloc(n_);
+  h_.alloc(ldr_ + 1), cs_.alloc(ldr_), sn_.alloc(ldr_), g_.alloc(ldr_ + 1), R_.alloc(size_t(ldr_) * ldr_), y_.alloc(ldr_);
+  scal_.alloc(4);
+  flag_.alloc(1);
+  int per_sm = 0;
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_kernel, kMgsThreads, 0), "occupancy");
+  mgs_grid_ = sm_count() * std::max(1, std::min(per_sm, 2));
+  red_grid_ = sm_count() * 2;
+  partial_.alloc(size_t(std::max(4 * mgs_grid_, red_grid_)));
+  cuda_check(cudaHostAlloc(&status_h_, sizeof(GmresStatus), cudaHostAllocMapped), "cudaHostAlloc");
+  cuda_check(cudaHostGetDevicePointer(&status_d_, status_h_, 0), "cudaHostGetDevicePointer");
+  cuda_check(cudaHostAlloc(&host_scalar_, sizeof(double), cudaHostAllocMapped), "cudaHostAlloc");
+  cuda_check(cudaHostGetDevicePointer(&host_scalar_d_, host_scalar_, 0), "cudaHostGetDevicePointer");
+  Ledger a, j;
+  // byte ledger of one preconditioner / J apply (enqueue into a capture that is discarded)
+  cudaStream_t tmp;
+  cuda_check(cudaStreamCreateWithFlags(&tmp, cudaStreamNonBlocking), "stream");
+  cudaGraph_t g;
+  cuda_check(cudaStreamBeginCapture(tmp, cudaStreamCaptureModeThreadLocal), "capture");
+  pc_.enqueue_apply(V_.get(), z_.get(), 1.0, 1.0, tmp, &a);
+  sys_.enqueue_apply(z_.get(), jout_.get(), 1.0, 1.0, tmp, &j);
+  cuda_check(cudaStreamEndCapture(tmp, &g), "end capture");
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(tmp);
+  apply_bytes = a.bytes, japply_bytes = j.bytes, apply_launches = a.launches;
+}
+
+GmresSolver::~GmresSolver() {
+  if (pj_exec_) cudaGraphExecDestroy(pj_exec_);
+  if (j_exec_) cudaGraphExecDestroy(j_exec_);
+  if (status_h_) cudaFreeHost(status_h_);
+  if (host_scalar_) cudaFreeHost(host_scalar_);
+}
+
+void GmresSolver::build_graphs(double st, double sp, cudaStream_t s) {
+  if (pj_exec_ && st == graph_st_ && sp == graph_sp_) return;
+  if (pj_exec_) cudaGraphExecDestroy(pj_exec_), pj_exec_ = nullptr;
+  if (j_exec_) cudaGraphExecDestroy(j_exec_), j_exec_ = nullptr;
+  double* stage = V_.get() + size_t(ldr_) * ldv_;
+  cudaGraph_t g;
+  cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture pj");
+  pc_.enqueue_apply(stage, z_.get(), 1.0 / st, 1.0 / sp, s);
+  sys_.enqueue_apply(z_.get(), jout_.get(), st, sp, s);
+  cuda_check(cudaStreamEndCapture(s, &g), "end capture pj");
+  cuda_check(cudaGraphInstantiate(&pj_exec_, g, 0), "instantiate pj");
+  cudaGraphDestroy(g);
+  cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture j");
+  sys_.enqueue_apply(xtot_.get(), jout_.get(), st, sp, s);
+  cuda_check(cudaStreamEndCapture(s, &g), "end capture j");
+  cuda_check(cudaGraphInstantiate(&j_exec_, g, 0), "instantiate j");
+  cudaGraphDestroy(g);
+  graph_st_ = st, graph_sp_ = sp;
+}
+
+double GmresSolver::norm_into(const double* a, const double* b, double* diff_out, double* dev_out, cudaStream_t s) {
+  sumsq_partial_kernel<<<red_grid_, kRedThreads, 0, s>>>(n_, a, b, diff_out, partial_.get());
+  finish_sum_kernel<<<1, 32, 0, s>>>(red_grid_, partial_.get(), dev_out, host_scalar_d_, 1);
+  cuda_check(cudaStreamSynchronize(s), "norm sync");
+  return *host_scalar_;
+}
+
+SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOptions& o, cudaStream_t s) {
+  if (!(o.tol > 0.0)) throw std::invalid_argument("gmres: tol must be positive");
+  SolveResult res;
+  const double st = o.scaled ? sys_.st : 1.0, sp = o.scaled ? sys_.sp : 1.0;
+  build_graphs(st, sp, s);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0), cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  double* stage = V_.get() + size_t(ldr_) * ldv_;
+  const size_t vb = sizeof(double) * size_t(n_);
+  cuda_check(cudaMemsetAsync(xtot_.get(), 0, vb, s), "memset");
+  const double bnorm = norm_into(b, nullptr, nullptr, nullptr, s);
+  if (bnorm == 0.0) {
+    res.converged = true;
+    cuda_check(cudaMemcpyAsync(x_out, xtot_.get(), vb, cudaMemcpyDeviceToDevice, s), "copy x");
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    res.device_seconds = ms * 1e-3;
+    cudaEventDestroy(e0), cudaEventDestroy(e1);
+    return res;
+  }
+  cuda_check(cudaMemcpyAsync(r_.get(), b, vb, cudaMemcpyDeviceToDevice, s), "copy r");
+  double rnorm = bnorm;
+  cuda_check(cudaMemcpyAsync(scal_.get(), &rnorm, sizeof(double), cudaMemcpyHostToDevice, s), "beta");
+  const int per_apply = pc_.inner_per_apply();
+  auto launch_pj = [&] {
+    cuda_check(cudaGraphLaunch(pj_exec_, s), "graph launch pj");
+    pc_.inner_calls += per_apply;
+    ++res.precond_applies;
+  };
+  for (;;) {
+    const int budget = std::min(restart_, o.max_iter - res.iterations);
+    if (budget <= 0) break;
+    const double tol_c = o.tol * bnorm / rnorm;
+    start_cycle_kernel<<<blocks_for(n_, 256), 256, 0, s>>>(n_, r_.get(), scal_.get(), V_.get(), stage);
+    cuda_check(cudaMemcpyAsync(g_.get(), &rnorm, sizeof(double), cudaMemcpyHostToDevice, s), "g0");
+    int m = 0, assembled_at = -1;
+    bool hit = false, cyc_done = false, happy = false;
+    double tr = 1.0;
+    auto assemble = [&](int mm) {
+      backsub_kernel<<<1, 1, 0, s>>>(mm, ldr_, R_.get(), g_.get(), y_.get(), flag_.get());
+      basis_combine_kernel<<<blocks_for(n_, 256), 256, 0, s>>>(n_, ldv_, mm, V_.get(), y_.get(), stage);
+      launch_pj();  // z = M^-1 (V y) = dx_cycle, jout = J dx_cycle
+      const double rr = norm_into(r_.get(), jout_.get(), nullptr, nullptr, s);
+      int sing = 0;
+      cuda_check(cudaMemcpy(&sing, flag_.get(), sizeof(int), cudaMemcpyDeviceToHost), "flag");
+      if (sing) throw fpb::numerical_error("gmres: singular least-squares system");
+      cuda_check(cudaMemcpyAsync(dx_.get(), z_.get(), vb, cudaMemcpyDeviceToDevice, s), "dx");
+      assembled_at = mm;
+      tr = rr / rnorm;
+    };
+    while (m < budget) {
+      launch_pj();
+      MgsArgs a{n_, ldv_, m, ldr_, V_.get(), jout_.get(), stage, partial_.get(), h_.get(), cs_.get(), sn_.get(),
+                g_.get(), R_.get(), rnorm, status_d_};
+      void* args[] = {&a};
+      cuda_check(cudaLaunchCooperativeKernel((void*)mgs_kernel, dim3(mgs_grid_), dim3(kMgsThreads), args, 0, s),
+                 "mgs launch");
+      cuda_check(cudaStreamSynchronize(s), "mgs sync");
+      const GmresStatus st_h = *status_h_;
+      if (st_h.nonfinite) throw fpb::numerical_error("gmres: non-finite vector in Arnoldi process");
+      ++m;
+      ++res.iterations;
+      res.history.push_back(st_h.est * rnorm / bnorm);
+      if (st_h.happy) {  // gmres.cpp:175-183
+        happy = true;
+        res.breakdown = true;
+        assemble(m);
+        cyc_done = true;
+        break;
+      }
+      if (st_h.est <= tol_c) {  // gmres.cpp:184-193
+        assemble(m);
+        if (tr <= tol_c) {
+          cyc_done = true;
+          break;
+        }
+        hit = true;
+      } else if (m % 50 == 0 || hit) {  // gmres.cpp:194-203
+        assemble(m);
+        if (tr <= tol_c) {
+          cyc_done = true;
+          break;
+        }
+      }
+      if (assembled_at == m && m < budget)  // keep iterating: restore the staged V_m
+        cuda_check(cudaMemcpyAsync(stage, V_.get() + size_t(m) * ldv_, vb, cudaMemcpyDeviceToDevice, s), "restage");
+    }
+    if (!cyc_done && assembled_at != m) assemble(m);
+    (void)happy;
+    add_inplace_kernel<<<blocks_for(n_, 256), 256, 0, s>>>(n_, xtot_.get(), dx_.get());
+    cuda_check(cudaGraphLaunch(j_exec_, s), "graph launch j");
+    rnorm = norm_into(b, jout_.get(), r_.get(), scal_.get(), s);  // r = b - J x, beta on device
+    if (!res.history.empty()) res.history.back() = rnorm / bnorm;
+    if (rnorm <= o.tol * bnorm) {
+      res.converged = true;
+      break;
+    }
+    if (res.iterations >= o.max_iter || m == 0) break;
+    if (res.breakdown && m < budget) break;
+    ++res.restarts;
+  }
+  res.final_rel_residual = rnorm / bnorm;
+  cuda_check(cudaMemcpyAsync(x_out, xtot_.get(), vb, cudaMemcpyDeviceToDevice, s), "copy x");
+  cudaEventRecord(e1, s);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  res.device_seconds = ms * 1e-3;
+  cudaEventDestroy(e0), cudaEventDestroy(e1);
+  return res;
+}
+
+}  // namespace fpd

@@ -1,0 +1,159 @@
+// Device engine: uploaded operators, the inner AMG V-cycle, the t-p-u / t-u-p /
+// t-u-p* block-triangular applies and the restarted GMRES driver.  Host code in
+// this file only enqueues work; everything on the solve path runs on the GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <vector>
+
+#include "../host/setup.hpp"
+#include "device.cuh"
+
+namespace fpd {
+
+// Algorithmic HBM bytes of the kernels an operation enqueues:
+// each stored matrix once per use, each vector once per read or write.
+struct Ledger {
+  double bytes = 0.0;
+  int launches = 0;
+  void add(double b) { bytes += b, ++launches; }
+};
+
+struct DSell {
+  int n_rows = 0, n_cols = 0, n_slices = 0;
+  long long slots = 0;
+  int64_t nnz = 0;
+  DevBuf<long long> off;
+  DevBuf<int> len, cols;
+  DevBuf<double> vals;
+  SellView view() const { return {n_rows, off.get(), len.get(), cols.get(), vals.get()}; }
+  double matrix_bytes() const { return 12.0 * double(nnz) + 4.0 * (n_rows + 1); }  // CSR-equivalent
+};
+
+struct DBsr3 {
+  int n_brows = 0, n_slices = 0;
+  long long slots = 0;
+  int64_t nblocks = 0;
+  DevBuf<long long> off;
+  DevBuf<int> len, bcols;
+  DevBuf<double> vals;
+  Bsr3View view() const { return {n_brows, off.get(), len.get(), bcols.get(), vals.get()}; }
+  double matrix_bytes() const { return 76.0 * double(nblocks) + 4.0 * (n_brows + 1); }
+};
+
+DSell make_sell(const fpb::Csr& A);
+DBsr3 make_bsr3(const fpb::Csr& A);  // A square, n % 3 == 0
+
+class DeviceSystem {
+ public:
+  explicit DeviceSystem(const fpb::HostSystem& J);
+  int n_u = 0, n_t = 0, n_p = 0;
+  int n() const { return n_u + n_t + n_p; }
+  double st = 1.0, sp = 1.0;  // driver block scaling (driver.cpp:114-125)
+  bool a_bsr3 = true;         // A as 3x3 blocks (n_u = 3 * nodes); SELL otherwise
+  DBsr3 A;
+  DSell A_sell;
+  DSell C1, Q1, C2, H, Q2, T;
+  // y = D J D x (D = blkdiag(I, st I, sp I)); st = sp = 1 gives J itself
+  void enqueue_apply(const double* x, double* y, double st_, double sp_, cudaStream_t s, Ledger* L = nullptr) const;
+  double bytes_apply() const;
+};
+
+struct DeviceLevel {
+  bool bsr3 = false;
+  DBsr3 Ab;
+  DSell As;
+  DSell P, R;  // P: this level <- next coarser; R = P^T (levels 0..L-2 hold the next level's P/R)
+  DevBuf<double> d, b, x, xt, xt2, r;
+  int n = 0;
+  double a_bytes() const { return bsr3 ? Ab.matrix_bytes() : As.matrix_bytes(); }
+};
+
+class DeviceAmg {
+ public:
+  DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3);
+  int n_levels() const { return int(lv.size()); }
+  int fine_n() const { return lv.empty() ? 0 : lv[0].n; }
+  // x = amg_apply(r) (amg.cpp:293-305); if sub_from != null writes sub_from - x instead
+  void enqueue_apply(const double* r, double* x, const double* sub_from, cudaStream_t s, Ledger* L = nullptr);
+  std::vector<int> level_sizes() const;
+  std::vector<DeviceLevel> lv;
+  DevBuf<double> lu;
+  DevBuf<int> prow, pcol;
+  int coarse_n = 0, coarse_rank = 0;
+  DevBuf<double> top_x, top_res, top_dx;
+  fpb::AmgOptions opt;
+
+ private:
+  void vcycle(int l, const double* b, double* x, const double* sub_from, cudaStream_t s, Ledger* L);
+};
+
+class DevicePrecond {
+ public:
+  DevicePrecond(const DeviceSystem& sys, const fpb::HostPrecond& hp);
+  int variant = 1;
+  const DeviceSystem* sys;
+  std::unique_ptr<DeviceAmg> amg;
+  DevBuf<double> hlu;
+  DevBuf<int> hpiv;
+  BandView band{};
+  DevBuf<int> band_start, band_piv;
+  DevBuf<double> band_Lc, band_diag, band_Lr, band_Uc;
+  int band_max_block = 0;
+  DevBuf<double> tt, tu, tp, su, sp_, vp, tu2, vu2;
+  long inner_calls = 0;
+  int inner_per_apply() const { return variant == 1 ? 2 : 1; }
+  // y = D^-1 M D^-1 x with at = 1/st, ap = 1/sp (at = ap = 1: M itself)
+  void enqueue_apply(const double* x, double* y, double at, double ap, cudaStream_t s, Ledger* L = nullptr);
+  void enqueue_band(const double* rhs, double rs, double* out, double* out2, const double* sub, double os, int mode,
+                    cudaStream_t s, Ledger* L);
+};
+
+struct SolveOptions {
+  double tol = 1e-10;
+  int restart = 50;
+  int max_iter = 500;
+  bool scaled = true;
+};
+
+struct SolveResult {
+  int iterations = 0, restarts = 0, precond_applies = 0;
+  bool converged = false, breakdown = false;
+  double final_rel_residual = 0.0;
+  std::vector<double> history;
+  double device_seconds = 0.0;
+};
+
+// Restarted right-preconditioned GMRES on the device (gmres.cpp semantics per
+// cycle + the GMRES(m) wrapper of SURVEY §8(a) G1).
+class GmresSolver {
+ public:
+  GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart);
+  ~GmresSolver();
+  SolveResult solve(const double* b_dev, double* x_dev, const SolveOptions& o, cudaStream_t s);
+  double apply_bytes = 0.0, japply_bytes = 0.0;  // algorithmic bytes of one precond / J apply
+  int apply_launches = 0;
+
+ private:
+  void build_graphs(double st, double sp, cudaStream_t s);
+  double norm_into(const double* a, const double* b, double* diff_out, double* dev_out, cudaStream_t s);
+  const DeviceSystem& sys_;
+  DevicePrecond& pc_;
+  int restart_, ldr_;
+  long long n_, ldv_;
+  DevBuf<double> V_, z_, jout_, xtot_, r_, dx_, partial_, h_, cs_, sn_, g_, R_, y_, scal_;
+  DevBuf<int> flag_;
+  GmresStatus* status_h_ = nullptr;
+  GmresStatus* status_d_ = nullptr;
+  double* host_scalar_ = nullptr;
+  double* host_scalar_d_ = nullptr;
+  int mgs_grid_ = 0, red_grid_ = 0;
+  cudaGraphExec_t pj_exec_ = nullptr, j_exec_ = nullptr;
+  double graph_st_ = -1, graph_sp_ = -1;
+};
+
+}  // namespace fpd

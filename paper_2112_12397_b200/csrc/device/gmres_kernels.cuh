@@ -1,0 +1,257 @@
+// Device-resident Arnoldi for right-preconditioned GMRES
+// (/root/reference/proj/core/src/gmres.cpp:118-174).  One cooperative kernel
+// per iteration performs modified Gram-Schmidt with the reference's selective
+// reorthogonalization (gmres.cpp:126-139), the happy-breakdown test (:144),
+// normalization (:145-149) and the Givens update of the least-squares problem
+// (:151-171).  Each MGS step is one fused pass "w -= h_i V_i ; partial(V_{i+1}.w)"
+// followed by a grid barrier; reductions are fixed-order (per-block tree, then
+// every block sums the block partials in index order), so runs are bitwise
+// reproducible.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "device.cuh"
+
+namespace fpd {
+
+struct MgsArgs {
+  long long n, ldv;
+  int m;        // V_0..V_m exist; the new column index is m
+  int ldr;      // leading dimension of R (restart + 1)
+  double* V;    // basis, V_i = V + i*ldv; V_{m+1} receives the new vector
+  const double* w_in;  // J z
+  double* stage;       // preconditioner input staging (receives V_{m+1})
+  double* partial;     // 2 * 2 * gridDim doubles (double-buffered)
+  double* h;           // ldr + 1
+  double* cs;          // rotations
+  double* sn;
+  double* g;           // ldr + 1
+  double* R;           // ldr * ldr, column j at R + j*ldr
+  double beta;         // ||r|| of the cycle
+  GmresStatus* status;
+};
+
+constexpr int kMgsThreads = 512;
+
+__device__ __forceinline__ double block_sum(double v, double* sm) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sm[i];
+  return s;  // valid in thread 0
+}
+
+// all blocks read the same partials in the same order -> identical totals
+__device__ __forceinline__ double grid_total(const double* part, int nb, double* sm) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[b];
+    sm[32] = s;
+  }
+  __syncthreads();
+  return sm[32];
+}
+
+__global__ void __launch_bounds__(kMgsThreads) mgs_kernel(MgsArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sm[40];
+  const int nb = gridDim.x;
+  const long long chunk = ((a.n + nb - 1) / nb + 31) / 32 * 32;
+  const long long lo = blockIdx.x * chunk, hi = lo + chunk < a.n ? lo + chunk : a.n;
+  double* w = a.V + (long long)(a.m + 1) * a.ldv;
+  int buf = 0;
+  auto publish = [&](double v) {
+    const double s = block_sum(v, sm);
+    if (threadIdx.x == 0) a.partial[buf * nb + blockIdx.x] = s;
+    grid.sync();
+    const double t = grid_total(a.partial + buf * nb, nb, sm);
+    buf ^= 1;
+    return t;
+  };
+  // pass 0: copy J z into the new column, ||w||^2 and V_0 . w
+  double n2 = 0.0, d0 = 0.0;
+  const double* V0 = a.V;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const double v = a.w_in[i];
+    w[i] = v;
+    n2 += v * v;
+    d0 += V0[i] * v;
+  }
+  {
+    const double s = block_sum(n2, sm);
+    const double t = block_sum(d0, sm);
+    if (threadIdx.x == 0) {
+      a.partial[2 * nb + blockIdx.x] = s;  // second half of the buffer as a scratch pair
+      a.partial[3 * nb + blockIdx.x] = t;
+    }
+    grid.sync();
+  }
+  const double wnorm_pre = sqrt(grid_total(a.partial + 2 * nb, nb, sm));
+  __syncthreads();
+  double hcur = grid_total(a.partial + 3 * nb, nb, sm);
+  __syncthreads();
+  buf = 0;
+  if (!isfinite(wnorm_pre)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.status->nonfinite = 1;
+      a.status->wnorm_pre = wnorm_pre;
+    }
+    return;  // uniform across the grid
+  }
+  double hloc[2] = {0, 0};
+  (void)hloc;
+  double nrm2 = 0.0;
+  for (int i = 0; i <= a.m; ++i) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.h[i] = hcur;
+    const double* Vi = a.V + (long long)i * a.ldv;
+    const double* Vn = i < a.m ? a.V + (long long)(i + 1) * a.ldv : nullptr;
+    double acc = 0.0;
+    for (long long k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+      const double wv = w[k] - hcur * Vi[k];
+      w[k] = wv;
+      acc += Vn ? Vn[k] * wv : wv * wv;
+    }
+    const double t = publish(acc);
+    __syncthreads();
+    if (i < a.m)
+      hcur = t;
+    else
+      nrm2 = t;
+  }
+  double hnext = sqrt(nrm2);
+  int reorth = 0;
+  if (hnext < 0.70710678118654752 * wnorm_pre) {  // gmres.cpp:133
+    reorth = 1;
+    double acc = 0.0;
+    for (long long k = lo + threadIdx.x; k < hi; k += blockDim.x) acc += V0[k] * w[k];
+    double c = publish(acc);
+    __syncthreads();
+    for (int i = 0; i <= a.m; ++i) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.h[i] += c;
+      const double* Vi = a.V + (long long)i * a.ldv;
+      const double* Vn = i < a.m ? a.V + (long long)(i + 1) * a.ldv : nullptr;
+      double acc2 = 0.0;
+      for (long long k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+        const double wv = w[k] - c * Vi[k];
+        w[k] = wv;
+        acc2 += Vn ? Vn[k] * wv : wv * wv;
+      }
+      const double t = publish(acc2);
+      __syncthreads();
+      if (i < a.m)
+        c = t;
+      else
+        nrm2 = t;
+    }
+    hnext = sqrt(nrm2);
+  }
+  const bool finite = isfinite(hnext);
+  const bool happy = hnext <= 1e-14 * fmax(1.0, wnorm_pre);
+  if (finite && !happy)
+    for (long long k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+      const double v = w[k] / hnext;
+      w[k] = v;
+      a.stage[k] = v;
+    }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    GmresStatus st;
+    st.hnext = hnext;
+    st.wnorm_pre = wnorm_pre;
+    st.happy = happy;
+    st.nonfinite = !finite;
+    st.reorth = reorth;
+    st.m = a.m;
+    st.est = 0.0;
+    if (finite) {
+      double* h = a.h;
+      const int m = a.m;
+      h[m + 1] = hnext;
+      for (int i = 0; i < m; ++i) {  // accumulated Givens rotations
+        const double t0 = a.cs[i] * h[i] + a.sn[i] * h[i + 1];
+        const double t1 = -a.sn[i] * h[i] + a.cs[i] * h[i + 1];
+        h[i] = t0;
+        h[i + 1] = t1;
+      }
+      const double denom = hypot(h[m], h[m + 1]);
+      const double c = denom == 0.0 ? 1.0 : h[m] / denom;
+      const double s = denom == 0.0 ? 0.0 : h[m + 1] / denom;
+      a.cs[m] = c;
+      a.sn[m] = s;
+      h[m] = denom;
+      h[m + 1] = 0.0;
+      for (int i = 0; i <= m; ++i) a.R[(long long)m * a.ldr + i] = h[i];
+      const double gm = a.g[m];
+      a.g[m] = c * gm;
+      a.g[m + 1] = -s * gm;
+      st.est = fabs(a.g[m + 1]) / a.beta;
+    }
+    *a.status = st;
+  }
+}
+
+// y = R(0:m,0:m)^-1 g(0:m)  (gmres.cpp:92-98), one thread; flags a zero pivot
+__global__ void backsub_kernel(int m, int ldr, const double* R, const double* g, double* y, int* singular) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  *singular = 0;
+  for (int i = m - 1; i >= 0; --i) {
+    double s = g[i];
+    for (int j = i + 1; j < m; ++j) s -= R[(long long)j * ldr + i] * y[j];
+    const double rii = R[(long long)i * ldr + i];
+    if (rii == 0.0) {
+      *singular = 1;
+      return;
+    }
+    y[i] = s / rii;
+  }
+}
+
+// u_i = sum_{j<m} V_j[i] y_j, j ascending from 0 (gmres.cpp:99-101)
+__global__ void basis_combine_kernel(long long n, long long ldv, int m, const double* V, const double* y, double* u) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int j = 0; j < m; ++j) s += V[(long long)j * ldv + i] * __ldg(y + j);
+  u[i] = s;
+}
+
+// deterministic sum of squares: per-block partials, then one block sums them in order
+constexpr int kRedThreads = 512;
+__global__ void __launch_bounds__(kRedThreads) sumsq_partial_kernel(long long n, const double* a, const double* b,
+                                                                    double* diff_out, double* partial) {
+  // v = a - b (b may be null); optionally stores v; partial[block] = sum v^2
+  __shared__ double sm[40];
+  const long long chunk = ((n + gridDim.x - 1) / gridDim.x + 31) / 32 * 32;
+  const long long lo = blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
+  double acc = 0.0;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const double v = b ? a[i] - b[i] : a[i];
+    if (diff_out) diff_out[i] = v;
+    acc += v * v;
+  }
+  const double s = block_sum(acc, sm);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+__global__ void finish_sum_kernel(int nb, const double* partial, double* out_dev, double* out_host, int take_sqrt) {
+  if (threadIdx.x != 0) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += partial[b];
+  if (take_sqrt) s = sqrt(s);
+  if (out_dev) *out_dev = s;
+  if (out_host) *out_host = s;
+}
+// V_0 = r / beta, also into the preconditioner staging buffer; g = [beta, 0...]
+__global__ void start_cycle_kernel(long long n, const double* r, const double* beta_dev, double* v0, double* stage) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = r[i] / *beta_dev;
+  v0[i] = v;
+  stage[i] = v;
+}
+
+}  // namespace fpd

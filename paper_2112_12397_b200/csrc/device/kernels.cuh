@@ -1,0 +1,359 @@
+// sm_100a kernels of the solve path.  Compiled with -fmad=false: every
+// multiply-add is a separately rounded DMUL + DADD, matching the CPU oracle
+// (built with -ffp-contract=off) bit for bit.  All kernels are HBM-bound
+// (SpMV ~0.24 flop/B): the levers are coalesced 256-byte warp loads (SELL-32
+// layout), read-only cache for matrix streams, enough loads in flight per
+// thread (unrolled row loops) and fusing the elementwise work of the reference
+// (Jacobi updates, residuals, axpys, block scaling) into the SpMV that produces
+// its operand.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "device.cuh"
+
+namespace fpd {
+
+constexpr int kSlice = 32;
+
+// ------------------------------------------------------------------ gathers
+struct GPlain {  // x_j
+  const double* x;
+  __device__ __forceinline__ double operator()(int j) const { return __ldg(x + j); }
+};
+struct GScaled {  // x_j * s  (driver block scaling D, driver.cpp:127-132)
+  const double* x;
+  double s;
+  __device__ __forceinline__ double operator()(int j) const { return __ldg(x + j) * s; }
+};
+struct GPresmooth {  // first Jacobi sweep from x = 0: (omega * b_j) / d_j  (amg.cpp:136-140)
+  const double* b;
+  const double* d;
+  double w;
+  __device__ __forceinline__ double operator()(int j) const { return (w * __ldg(b + j)) / __ldg(d + j); }
+};
+
+// One SELL-32 row, left to right (csr.cpp:109-119).
+template <class G>
+__device__ __forceinline__ double sell_row(const SellView& A, int row, const G& g) {
+  const long long base = A.slice_off[row >> 5] + (row & 31);
+  const int len = A.row_len[row];
+  const int* __restrict__ C = A.cols + base;
+  const double* __restrict__ V = A.vals + base;
+  double s = 0.0;
+  int k = 0;
+  for (; k + 4 <= len; k += 4) {
+    const int c0 = __ldg(C + 32 * k), c1 = __ldg(C + 32 * (k + 1)), c2 = __ldg(C + 32 * (k + 2)), c3 = __ldg(C + 32 * (k + 3));
+    const double v0 = __ldg(V + 32 * k), v1 = __ldg(V + 32 * (k + 1)), v2 = __ldg(V + 32 * (k + 2)), v3 = __ldg(V + 32 * (k + 3));
+    const double x0 = g(c0), x1 = g(c1), x2 = g(c2), x3 = g(c3);
+    s = s + v0 * x0;
+    s = s + v1 * x1;
+    s = s + v2 * x2;
+    s = s + v3 * x3;
+  }
+  for (; k < len; ++k) s = s + __ldg(V + 32 * k) * g(__ldg(C + 32 * k));
+  return s;
+}
+
+// ---------------------------------------------------------------- epilogues
+struct EStore {
+  double* y;
+  __device__ __forceinline__ void operator()(int i, double s) const { y[i] = s; }
+};
+struct EAddTo {  // y_i = a_i + s   (x += P e_c, amg.cpp:168-169; t_u = w_u + C1 t_t, precond.cpp:217)
+  const double* a;
+  double* y;
+  __device__ __forceinline__ void operator()(int i, double s) const { y[i] = a[i] + s; }
+};
+struct ESubFromScaled {  // y_i = a_i * sa - s   (t_p = w_p - Q2 s_u with w_p = D^-1 v_p)
+  const double* a;
+  double sa;
+  double* y;
+  __device__ __forceinline__ void operator()(int i, double s) const { y[i] = a[i] * sa - s; }
+};
+struct EResid {  // r_i = b_i - s   (amg.cpp:162-164)
+  const double* b;
+  double* r;
+  __device__ __forceinline__ void operator()(int i, double s) const { r[i] = b[i] - s; }
+};
+struct EResidPre {  // fused first pre-smoothing sweep + residual
+  const double* b;
+  const double* d;
+  double w;
+  double* x;
+  double* r;
+  __device__ __forceinline__ void operator()(int i, double s) const {
+    const double bi = b[i];
+    x[i] = (w * bi) / d[i];
+    r[i] = bi - s;
+  }
+};
+struct EJacobi {  // x'_i = x_i + (omega (b_i - s)) / d_i   (amg.cpp:139)
+  const double* b;
+  const double* d;
+  double w;
+  const double* x;
+  double* xo;
+  __device__ __forceinline__ void operator()(int i, double s) const { xo[i] = x[i] + (w * (b[i] - s)) / d[i]; }
+};
+struct EJacobiSubFrom {  // out_i = c_i - (Jacobi update)   (v_u = s_u - v_u2, precond.cpp:224)
+  const double* b;
+  const double* d;
+  double w;
+  const double* x;
+  const double* c;
+  double* out;
+  __device__ __forceinline__ void operator()(int i, double s) const {
+    const double xn = x[i] + (w * (b[i] - s)) / d[i];
+    out[i] = c[i] - xn;
+  }
+};
+// J apply, displacement rows: y_u = (A u + C1 (st v_t)) + Q1 (sp v_p)   (block.cpp:55-60)
+struct EJu {
+  SellView C1, Q1;
+  const double* vt;
+  const double* vp;
+  double st, sp;
+  double* y;
+  __device__ __forceinline__ void operator()(int i, double s) const {
+    const double b = sell_row(C1, i, GScaled{vt, st});
+    const double c = sell_row(Q1, i, GScaled{vp, sp});
+    y[i] = s + b + c;
+  }
+};
+
+// ------------------------------------------------------------- SELL kernels
+template <class G, class E>
+__global__ void __launch_bounds__(256) sell_kernel(SellView A, G g, E epi) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= A.n_rows) return;
+  epi(row, sell_row(A, row, g));
+}
+
+// ------------------------------------------------------------- BSR3 kernel
+// 96 threads per slice: warp li (0..2) computes scalar row 3*brow+li of the 32
+// block rows of the slice.  Sum order = block columns ascending, then j = 0,1,2:
+// the CSR column order.
+constexpr int kBsrThreads = 384;  // 4 slices per CTA
+
+template <class G, class E>
+__global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E epi) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int slice = t / 96, r = t - slice * 96, li = r >> 5, lane = r & 31;
+  const int brow = slice * kSlice + lane;
+  if (brow >= A.n_brows) return;
+  const long long base = A.slice_off[slice];
+  const int len = A.brow_len[brow];
+  const int* __restrict__ C = A.bcols + base + lane;
+  const double* __restrict__ V = A.vals + base * 9 + li * 96 + lane;
+  double s = 0.0;
+  int k = 0;
+  for (; k + 2 <= len; k += 2) {
+    const int c0 = 3 * __ldg(C + 32 * k), c1 = 3 * __ldg(C + 32 * (k + 1));
+    const double* V0 = V + 288 * k;
+    const double a00 = __ldg(V0), a01 = __ldg(V0 + 32), a02 = __ldg(V0 + 64);
+    const double a10 = __ldg(V0 + 288), a11 = __ldg(V0 + 320), a12 = __ldg(V0 + 352);
+    const double x00 = g(c0), x01 = g(c0 + 1), x02 = g(c0 + 2);
+    const double x10 = g(c1), x11 = g(c1 + 1), x12 = g(c1 + 2);
+    s = s + a00 * x00;
+    s = s + a01 * x01;
+    s = s + a02 * x02;
+    s = s + a10 * x10;
+    s = s + a11 * x11;
+    s = s + a12 * x12;
+  }
+  if (k < len) {
+    const int c0 = 3 * __ldg(C + 32 * k);
+    const double* V0 = V + 288 * k;
+    s = s + __ldg(V0) * g(c0);
+    s = s + __ldg(V0 + 32) * g(c0 + 1);
+    s = s + __ldg(V0 + 64) * g(c0 + 2);
+  }
+  epi(3 * brow + li, s);
+}
+
+// ------------------------------------------------ t/p rows of the J apply
+// y_t = st (C2 u - H (st v_t)),  y_p = sp (Q2 u + T (sp v_p))   (block.cpp:61-67)
+__global__ void __launch_bounds__(256) jtp_kernel(SellView C2, SellView H, SellView Q2, SellView T, const double* u,
+                                                  const double* vt, const double* vp, double st, double sp, double* yt,
+                                                  double* yp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < C2.n_rows) {
+    const double d = sell_row(C2, i, GPlain{u});
+    const double e = sell_row(H, i, GScaled{vt, st});
+    yt[i] = (d - e) * st;
+  } else if (i < C2.n_rows + Q2.n_rows) {
+    const int k = i - C2.n_rows;
+    const double f = sell_row(Q2, k, GPlain{u});
+    const double g = sell_row(T, k, GScaled{vp, sp});
+    yp[k] = (f + g) * sp;
+  }
+}
+
+// t_u = (w_u + C1 t_t) - Q1 t_p   (precond.cpp:159, t-p-u)
+__global__ void __launch_bounds__(256) tpu_tu_kernel(SellView C1, SellView Q1, const double* wu, const double* tt,
+                                                     const double* tp, double* tu) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= C1.n_rows) return;
+  const double b = sell_row(C1, i, GPlain{tt});
+  const double c = sell_row(Q1, i, GPlain{tp});
+  tu[i] = (wu[i] + b) - c;
+}
+
+// --------------------------------------------------------- 3x3 block solves
+// lu3_solve of csr.cpp:267-278 on blocks pre-factored at upload with the same
+// lu3_factor (factoring is deterministic, so this equals refactoring per call).
+__device__ __forceinline__ void lu3_solve_dev(const double* m, int pv, const double b[3], double x[3]) {
+  const int p0 = pv & 3, p1 = (pv >> 2) & 3, p2 = (pv >> 4) & 3;
+  double y0 = b[p0];
+  double y1 = b[p1];
+  y1 -= m[3] * y0;
+  double y2 = b[p2];
+  y2 -= m[6] * y0;
+  y2 -= m[7] * y1;
+  double x2 = y2;
+  x2 /= m[8];
+  double x1 = y1;
+  x1 -= m[5] * x2;
+  x1 /= m[4];
+  double x0 = y0;
+  x0 -= m[1] * x1;
+  x0 -= m[2] * x2;
+  x0 /= m[0];
+  x[0] = x0, x[1] = x1, x[2] = x2;
+}
+
+// t_t = H~^-1 (at * v_t); optionally y_t = (-t_t) * at  (t-u-p*: v_t = -t_t, precond.cpp:239)
+__global__ void __launch_bounds__(256) hsolve_in_kernel(int n_faces, const double* hlu, const int* hpiv, const double* vt,
+                                                        double at, double* tt, double* yt_neg) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n_faces) return;
+  const double w[3] = {vt[3 * f] * at, vt[3 * f + 1] * at, vt[3 * f + 2] * at};
+  double x[3];
+  lu3_solve_dev(hlu + 9 * size_t(f), hpiv[f], w, x);
+  for (int c = 0; c < 3; ++c) {
+    tt[3 * f + c] = x[c];
+    if (yt_neg) yt_neg[3 * f + c] = (-x[c]) * at;
+  }
+}
+
+// y_t = at * (H~^-1 (C2 v_u) - t_t)   (precond.cpp:163-164 / 226-227)
+__global__ void __launch_bounds__(256) hsolve_out_kernel(int n_faces, SellView C2, const double* vu, const double* hlu,
+                                                         const int* hpiv, const double* tt, double at, double* yt) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n_faces) return;
+  const double s[3] = {sell_row(C2, 3 * f, GPlain{vu}), sell_row(C2, 3 * f + 1, GPlain{vu}),
+                       sell_row(C2, 3 * f + 2, GPlain{vu})};
+  double x[3];
+  lu3_solve_dev(hlu + 9 * size_t(f), hpiv[f], s, x);
+  for (int c = 0; c < 3; ++c) yt[3 * f + c] = (x[c] - tt[3 * f + c]) * at;
+}
+
+// ------------------------------------------------------- banded solves
+// One warp per independent diagonal block (one fracture).  The block's
+// right-hand side lives in shared memory; each step finalizes one unknown and
+// the warp applies its column of L (forward) or U / L^T (backward) to the
+// following rows in parallel — the column-sweep order of the oracle.
+// Modes: out_mode 0: out = x;  1: out = (sub - x) * os;  2: out = x, out2 = x * os.
+__global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double* rhs, double rs, double* out,
+                                                        double* out2, const double* sub, double os, int out_mode) {
+  extern __shared__ double xs[];
+  const int blk = blockIdx.x, lane = threadIdx.x;
+  const int b0 = F.block_start[blk], b1 = F.block_start[blk + 1], nb = b1 - b0;
+  for (int i = lane; i < nb; i += 32) xs[i] = rhs[b0 + i] * rs;
+  __syncwarp();
+  const int kl = F.kl;
+  for (int j = 0; j < nb; ++j) {
+    const int gj = b0 + j;
+    if (!F.spd) {
+      const int p = F.piv[gj] - b0;
+      if (p != j && lane == 0) {
+        const double t = xs[j];
+        xs[j] = xs[p];
+        xs[p] = t;
+      }
+      __syncwarp();
+    }
+    const double yj = xs[j];
+    const double* Lj = F.Lc + size_t(gj) * kl;
+    for (int r = lane; r < kl && j + 1 + r < nb; r += 32) xs[j + 1 + r] -= Lj[r] * yj;
+    __syncwarp();
+  }
+  if (F.spd) {
+    for (int i = lane; i < nb; i += 32) xs[i] = xs[i] / F.diag[b0 + i];
+    __syncwarp();
+    for (int j = nb - 1; j >= 0; --j) {
+      const double xj = xs[j];
+      const double* Lj = F.Lr + size_t(b0 + j) * kl;
+      for (int r = lane; r < kl && j - 1 - r >= 0; r += 32) xs[j - 1 - r] -= Lj[r] * xj;
+      __syncwarp();
+    }
+  } else {
+    const int ku = F.ku;
+    for (int j = nb - 1; j >= 0; --j) {
+      const double xj = xs[j] / F.diag[b0 + j];
+      __syncwarp();
+      if (lane == 0) xs[j] = xj;
+      const double* Uj = F.Uc + size_t(b0 + j) * ku;
+      for (int r = lane; r < ku && j - 1 - r >= 0; r += 32) xs[j - 1 - r] -= Uj[r] * xj;
+      __syncwarp();
+    }
+  }
+  for (int i = lane; i < nb; i += 32) {
+    const double x = xs[i];
+    if (out_mode == 1)
+      out[b0 + i] = (sub[b0 + i] - x) * os;
+    else
+      out[b0 + i] = x;
+    if (out_mode == 2) out2[b0 + i] = x * os;
+  }
+}
+
+// ---------------------------------------------------- coarse dense solve
+// x = Q U^-1 L^-1 P b on the full-pivot LU (restated FullPivLU::solve), one CTA,
+// column sweeps.  LU is column-major so each step reads one contiguous column.
+constexpr int kCoarseThreads = 256;
+__global__ void __launch_bounds__(kCoarseThreads) coarse_solve_kernel(DenseLUView F, const double* b, double* x) {
+  extern __shared__ double c[];
+  const int n = F.n, tid = threadIdx.x;
+  for (int i = tid; i < n; i += blockDim.x) c[i] = b[F.prow[i]];
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const double cj = c[j];
+    const double* col = F.lu + size_t(j) * n;
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) c[i] -= col[i] * cj;
+    __syncthreads();
+  }
+  for (int j = F.rank - 1; j >= 0; --j) {
+    const double xj = c[j] / F.lu[size_t(j) * n + j];
+    __syncthreads();
+    if (tid == 0) c[j] = xj;
+    const double* col = F.lu + size_t(j) * n;
+    for (int i = tid; i < j; i += blockDim.x) c[i] -= col[i] * xj;
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += blockDim.x) x[F.pcol[i]] = i < F.rank ? c[i] : 0.0;
+}
+
+// ---------------------------------------------------------- elementwise
+__global__ void presmooth_kernel(int n, const double* b, const double* d, double w, double* x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = (w * b[i]) / d[i];
+}
+__global__ void scale_copy_kernel(int n_u, int n_t, int n_p, const double* x, double st, double sp, double* y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = n_u + n_t + n_p;
+  if (i >= n) return;
+  const double v = x[i];
+  y[i] = i < n_u ? v : (i < n_u + n_t ? v * st : v * sp);
+}
+__global__ void axpy_kernel(long long n, const double* a, const double* b, double beta, double* y) {  // y = a + beta b
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) y[i] = a[i] + beta * b[i];
+}
+__global__ void add_inplace_kernel(long long n, double* x, const double* dx) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = x[i] + dx[i];
+}
+
+}  // namespace fpd

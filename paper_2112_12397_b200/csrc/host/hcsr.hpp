@@ -1,0 +1,79 @@
+// Host-side sparse containers and kernels of the B200 solve framework.
+//
+// These run on the host during preconditioner *setup* (not on the timed solve
+// path).  Every row-local operation is parallelized over rows with OpenMP while
+// keeping, inside each row, the exact accumulation order of the reference
+// (/root/reference/proj/core/src/csr.cpp), so a setup built here is bitwise the
+// one the reference algorithm produces.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace fpb {
+
+class numerical_error : public std::runtime_error {
+ public:
+  explicit numerical_error(const std::string& w) : std::runtime_error(w) {}
+};
+
+// csr.hpp:16-49 with 64-bit row offsets
+struct Csr {
+  int n_rows = 0, n_cols = 0;
+  std::vector<int64_t> rp{0};
+  std::vector<int> ci;
+  std::vector<double> v;
+
+  Csr() = default;
+  Csr(int r, int c) : n_rows(r), n_cols(c), rp(static_cast<size_t>(r) + 1, 0) {}
+  int64_t nnz() const { return int64_t(ci.size()); }
+  int row_len(int i) const { return int(rp[i + 1] - rp[i]); }
+
+  struct Triplet { int row, col; double value; };
+  static Csr identity(int n);
+  static Csr from_triplets(int rows, int cols, std::vector<Triplet> t);  // stable (row,col) order
+  std::vector<double> to_dense() const;  // row-major, small matrices only
+};
+
+std::vector<double> spmv(const Csr& A, std::span<const double> x);
+Csr transpose(const Csr& A);
+Csr spgemm(const Csr& A, const Csr& B);
+Csr add_scaled(const Csr& A, const Csr& B, double alpha, double beta);
+Csr scale_rows(const Csr& A, std::span<const double> s);
+std::vector<double> diag_extract(const Csr& A);
+std::vector<double> restrict_dense(const Csr& A, std::span<const int> idx);  // A(idx, idx), row-major
+
+// 3x3 partial-pivot LU (csr.cpp:242-278)
+bool lu3_factor(double m[9], int piv[3]);
+void lu3_solve(const double m[9], const int piv[3], const double b[3], double x[3]);
+// Block-diagonal surrogate H~ = Bdiag(H,3) with the 1e-10 shift (csr.cpp:216-237)
+std::vector<double> bdiag3_extract(const Csr& H, double delta = 1e-10);
+Csr bdiag3_inverse_csr(const std::vector<double>& blocks);
+
+// Dense full-pivot LU: coarse AMG level and fixed-stress local solves.
+struct FullPivLU {
+  int n = 0, rank = 0;
+  std::vector<double> lu;
+  std::vector<int> prow, pcol;
+  void compute(std::vector<double> a_rowmajor, int n);
+  bool invertible() const { return rank == n; }
+  std::vector<double> solve(std::span<const double> b) const;
+};
+
+// Banded exact factor (SparseFactor semantics), per independent diagonal block.
+struct BandFactor {
+  enum class Kind { spd, general };
+  Kind kind = Kind::spd;
+  int n = 0, kl = 0, ku = 0;
+  std::vector<int> block_start;
+  std::vector<double> Lc, diag, Lr, Uc;
+  std::vector<int> piv;
+  void factor(const Csr& A, Kind k);
+  std::vector<double> solve(std::span<const double> b) const;  // host check path
+};
+
+}  // namespace fpb

@@ -1,0 +1,69 @@
+// Host-side preconditioner setup of the B200 solve framework: the work the
+// reference does in build_tpu/build_tup/amg_setup
+// (/root/reference/proj/core/src/precond.cpp:119-202, amg.cpp:181-291) before the
+// solve.  It runs multi-threaded on the host and its output is uploaded to HBM
+// (device.cuh).  Per-row/per-aggregate arithmetic follows the reference order so
+// the hierarchy is the one the reference algorithm builds.
+#pragma once
+
+#include <array>
+#include <vector>
+
+#include "hcsr.hpp"
+
+namespace fpb {
+
+struct AmgOptions {
+  double strength_threshold = 0.08;  // amg.hpp:20
+  int max_coarse = 100;
+  int pre_sweeps = 1, post_sweeps = 1;
+  int smoother = 0;  // 0 weighted Jacobi (GPU path), 1 symmetric Gauss-Seidel (reference default)
+  bool prolongation_smoothing = true;
+  int cycles_per_apply = 1;
+  double jacobi_omega = 2.0 / 3.0;
+  double stall_ratio = 0.9;
+  int max_levels = 25;
+};
+
+struct HostLevel {
+  Csr A;
+  Csr P;  // prolongation from this level to the previous finer one (empty at level 0)
+  std::vector<double> diag;
+  std::vector<int> aggregate;  // fine row -> aggregate id (coarse levels only)
+  std::vector<int> aggregate_offsets;
+};
+
+struct HostAmg {
+  std::vector<HostLevel> levels;
+  FullPivLU coarse;
+  AmgOptions opt;
+};
+
+HostAmg amg_setup(const Csr& A, const std::vector<std::vector<double>>& near_null, const AmgOptions& opt);
+std::vector<std::vector<double>> rigid_body_modes(const std::vector<std::array<double, 3>>& coords);
+int qr_colpiv(int m, int k, const std::vector<double>& B_colmajor, std::vector<double>& Q, std::vector<double>& Rp);
+
+struct HostSystem {
+  int n_u = 0, n_t = 0, n_p = 0;
+  Csr A, C1, Q1, C2, H, Q2, T, F_u;
+  void check_shapes() const;
+};
+
+enum Variant { kTpu = 0, kTup = 1, kTupStar = 2 };
+
+struct HostPrecond {
+  int variant = kTup;
+  std::vector<double> hblocks;  // regularized H~ = Bdiag(H,3), 9 per face
+  std::vector<double> T_diag;   // t-p-u
+  Csr S;                        // S~ (t-p-u) or S1 (t-u-p): the inner AMG operator
+  HostAmg amg;
+  std::vector<double> S_K;      // t-u-p fixed-stress diagonal
+  Csr S2;                       // t-u-p S~2 = T - diag(S_K)
+  BandFactor factor;            // T (t-p-u, LDL^T) or S~2 (t-u-p, LU)
+};
+
+HostPrecond build_precond(const HostSystem& J, int variant, const AmgOptions& opt,
+                          const std::vector<std::array<double, 3>>& coords);
+std::vector<double> fixed_stress_diag(const Csr& Q2, const Csr& S1, const Csr& Q1);
+
+}  // namespace fpb

@@ -1,0 +1,49 @@
+// Synthetic workload generator for the BASELINE.json configs: a restatement of
+// the reference's structured-hex mesh with duplicated fracture nodes
+// (/root/reference/proj/core/src/mesh.cpp:51-224) and its Jacobian assembly
+// (assembly.cpp:39-97,132-406), extended with per-cell Young's modulus and
+// Poisson ratio (BASELINE configs 2-5) and a seeded FractureState.  This is input
+// generation for the solve path, not part of it.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <vector>
+
+#include "setup.hpp"
+
+namespace fpb {
+
+struct FractureSpec {  // mesh.hpp:28-33
+  int normal_axis = 0;
+  double coord = 0, lo1 = 0, hi1 = 0, lo2 = 0, hi2 = 0;
+};
+
+struct WorkloadSpec {
+  int cells[3] = {20, 20, 20};
+  double length[3] = {1.0, 1.0, 1.0};
+  std::vector<FractureSpec> fractures;
+  // elasticity (per cell): E lognormal(median, sigma_ln) per element or per z-layer
+  double E_median = 10e9, E_sigma_ln = 0.0;
+  int E_layers = 0;                 // 0: independent per element; >0: per z-layer
+  double nu = 0.25, nu_lo = 0.0, nu_hi = 0.0;  // nu_hi > nu_lo: per-layer U(nu_lo, nu_hi)
+  // contact / flow (assembly.hpp:18-39)
+  double friction = 0.6, cohesion = 0.0, C_f0 = 9.87e-15, mu_f = 1e-3, stab_beta = 0.02, dt = 0.5;
+  double frac_stick = 0.7, frac_slip = 0.2;  // open = rest
+  double aperture_median = 1e-4, aperture_sigma_ln = 0.0;
+  double sigma_load = 1e7;  // top-face compressive load, Pa
+  double p0 = 1e6;          // fracture pressure level, Pa
+  uint64_t seed = 42;
+};
+
+struct Workload {
+  HostSystem J;
+  std::vector<std::array<double, 3>> coords;
+  int n_stick = 0, n_slip = 0, n_open = 0, n_fractures = 0;
+  double k_scale = 0.0;
+};
+
+WorkloadSpec preset_config(int config_id, uint64_t seed);  // BASELINE.json configs[0..4] as 1..5
+Workload generate_workload(const WorkloadSpec& spec);
+
+}  // namespace fpb

@@ -1,0 +1,139 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol the
+headers declare, validates arguments like the reference (std::invalid_argument
+-> FP_INVALID_ARGUMENT), and its host-side setup (build_tpu / build_tup,
+amg_setup) reproduces the oracle's bit for bit."""
+import ctypes as C
+import glob
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_2112_12397_b200 import _native as N
+from paper_2112_12397_b200 import api
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        txt = open(h).read()
+        names |= set(re.findall(r"^[A-Za-z_][\w \*]*?\b(fp_\w+)\s*\(", txt, flags=re.M))
+    return names
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_symbols()
+    assert len(names) >= 25
+    lib = C.CDLL(N.LIB_PATH)
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(N.SIGNATURES) == names, set(N.SIGNATURES) ^ names
+    assert b"sm_100a" in N.lib.fp_version()
+
+
+def test_shared_library_is_sm100a_only():
+    import subprocess
+
+    r = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", N.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in r.stdout
+    assert "sm_90" not in r.stdout and "sm_80" not in r.stdout
+
+
+def csr(rows, cols, trips):
+    rp = np.zeros(rows + 1, np.int64)
+    trips = sorted(trips)
+    for r, _, _ in trips:
+        rp[r + 1] += 1
+    return api.CsrMatrix(rows, cols, np.cumsum(rp), np.array([c for _, c, _ in trips], np.int32),
+                         np.array([v for _, _, v in trips]))
+
+
+def test_invalid_arguments_are_reported_not_thrown():
+    A = csr(3, 3, [(0, 0, 1.0), (1, 1, 1.0), (2, 2, 1.0)])
+    Z = api.CsrMatrix.empty
+    # n_t != 3 n_p (block.cpp:49-52)
+    J = api.BlockSystem(3, 2, 1, A, Z(3, 2), Z(3, 1), Z(2, 3), Z(2, 2), Z(1, 3), csr(1, 1, [(0, 0, 1.0)]))
+    h = C.c_void_p()
+    st = N.lib.fp_system_create(C.byref(J.view()), C.byref(h))
+    assert st == N.FP_INVALID_ARGUMENT and b"n_t must equal 3*n_p" in N.lib.fp_last_error()
+    # unsorted columns (csr.cpp:31-47 invariants)
+    bad = api.CsrMatrix(2, 2, np.array([0, 2, 2]), np.array([1, 0], np.int32), np.array([1.0, 1.0]))
+    J2 = api.BlockSystem(2, 0, 0, bad, Z(2, 0), Z(2, 0), Z(0, 2), Z(0, 0), Z(0, 2), Z(0, 0))
+    assert N.lib.fp_system_create(C.byref(J2.view()), C.byref(h)) == N.FP_INVALID_ARGUMENT
+    assert b"strictly increasing" in N.lib.fp_last_error()
+    # wrong shapes in the host builder
+    with pytest.raises(ValueError):
+        api.HostPreconditioner(J, api.PrecondConfig("tup"))
+    with pytest.raises(ValueError):
+        api.PrecondConfig("tpu", inner="direct").native()
+
+
+def test_zero_diagonal_is_a_numerical_error():
+    # amg_setup rejects a zero diagonal with numerical_error (amg.cpp:205-207)
+    n_u, n_p = 6, 1
+    trips = [(i, i, 2.0) for i in range(n_u) if i != 4] + [(4, 3, 1.0), (3, 4, 1.0)]
+    A = csr(n_u, n_u, trips)
+    Z = api.CsrMatrix.empty
+    H = csr(3, 3, [(0, 0, 1.0), (1, 1, 1.0), (2, 2, 1.0)])
+    J = api.BlockSystem(n_u, 3, n_p, A, Z(n_u, 3), Z(n_u, 1), Z(3, n_u), H, Z(1, n_u), csr(1, 1, [(0, 0, 1.0)]))
+    with pytest.raises(N.NumericalError, match="zero diagonal"):
+        api.HostPreconditioner(J, api.PrecondConfig("tup", amg=api.AmgConfig(max_coarse=2)))
+
+
+def small_workload(seed=7, cells=(6, 6, 6), fracs=((0, 0.5, 0.0, 1.0, 0.0, 1.0),), **kw):
+    spec = dict(cells=cells, fractures=list(fracs), frac_stick=0.5, frac_slip=0.3, E_sigma_ln=0.5,
+                aperture_sigma_ln=0.3, **kw)
+    return api.Workload(spec=spec, seed=seed).system()
+
+
+def oracle_system(J):
+    blocks = [(m.n_rows, m.n_cols, m.row_offsets, m.col_indices, m.values)
+              for m in (J.A, J.C1, J.Q1, J.C2, J.H, J.Q2, J.T, J.F_u)]
+    return O.OracleSystem.from_blocks(J.n_u, J.n_t, J.n_p, blocks)
+
+
+def same_csr(a, m: api.CsrMatrix):
+    return (a[0] == m.n_rows and np.array_equal(a[2], m.row_offsets) and np.array_equal(a[3], m.col_indices)
+            and np.array_equal(a[4], m.values))
+
+
+@pytest.mark.parametrize("variant", ["tpu", "tup"])
+def test_host_setup_is_bitwise_the_oracle_setup(variant):
+    J = small_workload()
+    osys = oracle_system(J)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords)
+    hp = api.HostPreconditioner(J, api.PrecondConfig(variant))
+    assert hp.level_sizes() == [opc.level_matrix(l, 0)[0] for l in range(opc.n_levels())]
+    for l in range(opc.n_levels()):
+        assert same_csr(opc.level_matrix(l, 0), hp.matrix(0, l)), f"A_{l}"
+        assert np.array_equal(opc.level_diag(l), hp.vector(2, l))
+        if l > 0:
+            assert same_csr(opc.level_matrix(l, 1), hp.matrix(1, l)), f"P_{l}"
+    assert np.array_equal(opc.hblocks(), hp.vector(0))
+    assert np.array_equal(opc.vec(), hp.vector(1))  # T_diag (tpu) / S_K (tup)
+    if variant == "tup":
+        assert same_csr(opc.matrix(1), hp.matrix(2))  # S~2
+
+
+def test_workload_sizes_follow_the_reference_mesh_rules():
+    # config 1 has 9261 + 19*19 duplicated nodes -> n_u = 28,866; nnz(A) = 2,074,086
+    J = api.Workload(1, 42).system()
+    assert (J.n_u, J.n_t, J.n_p) == (28866, 1200, 400)
+    assert J.A.nnz == 2074086
+    assert J.node_coords.shape == (9622, 3)
+    # the duplicated fracture nodes sit on the fracture plane x = 0.5
+    assert np.all(J.node_coords[9261:, 0] == 0.5)
+
+
+def test_workload_custom_mesh_counts():
+    # 4x4x2 box with a 2x2-face fracture (the reference's small_spec, test_model.cpp:22-32 geometry)
+    spec = dict(cells=(4, 4, 2), length=(4.0, 4.0, 2.0), fractures=[(0, 2.0, 1.0, 3.0, 0.0, 2.0)])
+    J = api.Workload(spec=spec, seed=1).system()
+    # nodes 5*5*3 = 75, interior patch nodes (jb in (1,3), jc in (0,2)) = 1*1 -> 1 duplicate
+    assert J.n_u == 3 * 76 and J.n_p == 4 and J.n_t == 12
+    with pytest.raises(ValueError, match="not grid aligned"):
+        api.Workload(spec=dict(cells=(2, 2, 2), fractures=[(0, 0.3, 0.0, 1.0, 0.0, 1.0)]), seed=1)

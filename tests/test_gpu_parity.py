@@ -1,0 +1,197 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle on
+the same seeded inputs.
+
+Bars (BASELINE.json north_star): one preconditioner application within 1e-12
+relative (fp64) — the kernels keep the reference's per-row summation order and
+never contract multiply-adds, so the applies are asserted *bitwise* equal as
+well; GMRES iteration count within +-2 and the solution within 1e-8 relative
+2-norm at rtol 1e-10.
+"""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_2112_12397_b200 import _native as N
+from paper_2112_12397_b200 import api
+from test_abi_cpu import oracle_system, small_workload
+
+pytestmark = pytest.mark.gpu
+
+TOL_APPLY = 1e-12
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def csr_of(t):
+    r, c, rp, ci, v = t
+    return api.CsrMatrix(r, c, rp, ci, v)
+
+
+def system_from_oracle(osys):
+    b = [csr_of(t) for t in osys.blocks()]
+    return api.BlockSystem(osys.n_u, osys.n_t, osys.n_p, *b[:7], F_u=b[7])
+
+
+def upload_oracle_precond(op, osys, opc, variant, amg):
+    """The 'reference-built hierarchy' path: every piece comes from the oracle."""
+    levels = []
+    for l in range(opc.n_levels()):
+        A = csr_of(opc.level_matrix(l, 0))
+        P = csr_of(opc.level_matrix(l, 1)) if l > 0 else None
+        levels.append((A, P, opc.level_diag(l)))
+    factor = csr_of(osys.block(6)) if variant == "tpu" else csr_of(opc.matrix(1))
+    return api.GpuPreconditioner.upload(op, variant, opc.hblocks(), factor, levels, amg)
+
+
+def amg_kw(amg: api.AmgConfig):
+    return dict(strength_threshold=amg.strength_threshold, jacobi_omega=amg.jacobi_omega, stall_ratio=amg.stall_ratio,
+                max_coarse=amg.max_coarse, pre_sweeps=amg.pre_sweeps, post_sweeps=amg.post_sweeps, smoother=0,
+                prolongation_smoothing=int(amg.prolongation_smoothing), cycles_per_apply=amg.cycles_per_apply,
+                max_levels=amg.max_levels)
+
+
+CASES = {
+    "toy-mixed": lambda: O.OracleSystem.toy(24, 2, "mixed", 44),
+    "toy-open": lambda: O.OracleSystem.toy(24, 2, "open_all", 123),
+    "toy-stick": lambda: O.OracleSystem.toy(30, 4, "stick", 99),
+    "toy-decoupled": lambda: O.OracleSystem.toy(18, 2, "decoupled", 99),
+    "mesh-6x6x6": lambda: oracle_system(small_workload(seed=7)),
+    "mesh-2frac": lambda: oracle_system(small_workload(seed=3, cells=(8, 6, 6),
+                                                       fracs=((0, 0.25, 0.0, 1.0, 0.0, 1.0),
+                                                              (0, 0.75, 0.0, 1.0, 0.5, 1.0)))),
+}
+
+
+def coords_for(name):
+    if name == "mesh-6x6x6":
+        return small_workload(seed=7).node_coords
+    if name == "mesh-2frac":
+        return small_workload(seed=3, cells=(8, 6, 6), fracs=((0, 0.25, 0.0, 1.0, 0.0, 1.0),
+                                                              (0, 0.75, 0.0, 1.0, 0.5, 1.0))).node_coords
+    return None
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_system_apply_bitwise(case):
+    osys = CASES[case]()
+    J = system_from_oracle(osys)
+    op = api.BlockSystemOperator(J)
+    x = np.random.default_rng(1).uniform(-1, 1, J.total_dimension())
+    y = op.apply(x)
+    ref = osys.apply(x)
+    assert rel(y, ref) <= TOL_APPLY
+    assert np.array_equal(y, ref)
+
+
+@pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_precond_apply_matches_oracle(case, variant):
+    osys = CASES[case]()
+    J = system_from_oracle(osys)
+    J.node_coords = coords_for(case)
+    amg = api.AmgConfig(max_coarse=8 if case.startswith("toy") else 100)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, **amg_kw(amg))
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, variant, amg)
+    rng = np.random.default_rng(5)
+    for trial in range(3):
+        x = rng.uniform(-1, 1, J.total_dimension())
+        y, ref = pc.apply(x), opc.apply(x)
+        assert rel(y, ref) <= TOL_APPLY, (trial, rel(y, ref))
+        assert np.array_equal(y, ref), (trial, rel(y, ref))
+
+
+@pytest.mark.parametrize("variant", ["tpu", "tup"])
+def test_product_built_precond_matches_oracle(variant):
+    J = small_workload(seed=11, cells=(7, 6, 5))
+    osys = oracle_system(J)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords)
+    op = api.BlockSystemOperator(J)
+    pc = (api.build_tpu if variant == "tpu" else api.build_tup)(J, op=op)
+    x = np.random.default_rng(2).uniform(-1, 1, J.total_dimension())
+    assert np.array_equal(pc.apply(x), opc.apply(x))
+
+
+def test_amg_apply_and_multi_sweep_cycles_match_oracle():
+    J = small_workload(seed=5)
+    osys = oracle_system(J)
+    amg = api.AmgConfig(pre_sweeps=2, post_sweeps=3, cycles_per_apply=2)
+    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, **amg_kw(amg))
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, "tup", amg)
+    r = np.random.default_rng(9).uniform(-1, 1, J.n_u)
+    assert np.array_equal(pc.amg_apply(r), opc.amg_apply(r))
+    x = np.random.default_rng(10).uniform(-1, 1, J.total_dimension())
+    assert rel(pc.apply(x), opc.apply(x)) <= TOL_APPLY
+
+
+def test_inner_call_contract_linearity_and_zero():
+    J = small_workload(seed=13)
+    op = api.BlockSystemOperator(J)
+    rng = np.random.default_rng(3)
+    x1, x2 = rng.uniform(-1, 1, (2, J.total_dimension()))
+    for variant, calls in (("tpu", 1), ("tup", 2), ("tup_star", 1)):
+        pc = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, api.PrecondConfig(variant)))
+        pc.reset_count()
+        y = pc.apply(0.7 * x1 - 1.3 * x2)
+        assert pc.call_count() == calls  # test_precond.cpp:323-343
+        y1, y2 = pc.apply(x1), pc.apply(x2)
+        assert np.linalg.norm(y - (0.7 * y1 - 1.3 * y2)) <= 1e-12 * max(1.0, np.linalg.norm(y))
+        assert np.all(pc.apply(np.zeros(J.total_dimension())) == 0.0)
+
+
+def test_device_memory_path_equals_host_path():
+    import torch
+
+    J = small_workload(seed=17)
+    op = api.BlockSystemOperator(J)
+    pc = api.build_tup(J, op=op)
+    x = np.random.default_rng(4).uniform(-1, 1, J.total_dimension())
+    xd = torch.tensor(x, device="cuda", dtype=torch.float64)
+    assert np.array_equal(pc.apply(xd).cpu().numpy(), pc.apply(x))
+    assert np.array_equal(op.apply(xd).cpu().numpy(), op.apply(x))
+
+
+def test_sgs_smoother_is_rejected_on_the_gpu():
+    J = small_workload(seed=19)
+    op = api.BlockSystemOperator(J)
+    hp = api.HostPreconditioner(J, api.PrecondConfig("tup", amg=api.AmgConfig(smoother="sgs")))
+    with pytest.raises(ValueError, match="weighted_jacobi"):
+        api.GpuPreconditioner.from_host(op, hp)
+
+
+@pytest.mark.parametrize("variant", ["tpu", "tup"])
+@pytest.mark.parametrize("restart", [50, 8])
+def test_gmres_matches_oracle(variant, restart):
+    J = small_workload(seed=23, cells=(8, 8, 6))
+    osys = oracle_system(J)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords)
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, variant, api.AmgConfig())
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=restart, max_iter=500, scaled=True)
+    x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=500, restart=restart, scaled=True)
+    assert st.converged == st_ref["converged"]
+    assert abs(st.iterations - st_ref["iterations"]) <= 2, (st.iterations, st_ref["iterations"])
+    if st_ref["converged"]:
+        assert rel(x, x_ref) <= 1e-8, rel(x, x_ref)
+    # the reported true residual of the scaled system
+    assert st.relative_residuals[-1] <= 1e-10 * (1 + 1e-6) or not st.converged
+
+
+def test_gmres_unscaled_and_zero_rhs():
+    J = small_workload(seed=29)
+    osys = oracle_system(J)
+    op = api.BlockSystemOperator(J)
+    pc = api.build_tup(J, op=op)
+    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords)
+    b = np.random.default_rng(1).uniform(-1, 1, J.total_dimension())
+    x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=300, restart=50, scaled=False)
+    x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=50, max_iter=300, scaled=False)
+    assert abs(st.iterations - st_ref["iterations"]) <= 2
+    if st_ref["converged"]:
+        assert rel(x, x_ref) <= 1e-8
+    x0, st0 = api.gmres(op, pc, np.zeros(J.total_dimension()), tol=1e-10)
+    assert st0.converged and st0.iterations == 0 and np.all(x0 == 0)
