@@ -88,6 +88,7 @@ typedef struct fp_solve_stats {
   int32_t iterations, converged, breakdown, restarts, precond_applies;
   double final_rel_residual;
   double device_seconds;       /* CUDA-event time of the solve on the handle's stream */
+  int64_t kernel_launches;     /* kernels of this library launched by the solve (graph nodes included) */
   double* residual_history;    /* optional caller buffer */
   int32_t history_capacity;
   int32_t history_len;
@@ -155,6 +156,23 @@ int fp_amg_apply(fp_precond* p, const double* r, double* x, int32_t mem);
 int64_t fp_precond_inner_calls(fp_precond* p, int32_t reset);
 /* algorithmic HBM bytes and kernel launches of one fp_precond_apply / fp_system_apply */
 int fp_precond_traffic(fp_precond* p, double* apply_bytes, int32_t* apply_launches, double* japply_bytes);
+
+/* Kernel timing for the roofline: each phase is launched `reps` times back to
+ * back on the handle's stream between CUDA events (ms = average per launch);
+ * bytes are the algorithmic HBM bytes of one launch. */
+typedef struct fp_profile {
+  double apply_ms, apply_bytes;     /* one full preconditioner application (CUDA graph) */
+  int32_t apply_launches;
+  double japply_ms, japply_bytes;   /* one J application */
+  double fine_resid_ms, fine_resid_bytes; /* finest level: fused first Jacobi sweep + residual (BSR3) */
+  double fine_post_ms, fine_post_bytes;   /* finest level: Jacobi post-smoothing sweep (BSR3) */
+  double band_ms, band_bytes;       /* banded T / S~2 solve */
+  double coarse_ms;                 /* dense coarse-level solve */
+  int32_t n_levels;
+  int32_t level_rows[32];
+  int64_t level_nnz[32];
+} fp_profile;
+int fp_precond_profile(fp_precond* p, int32_t reps, fp_profile* out);
 
 /* ---- solve: gmres(op, precond, b, tol, max_iter) (gmres.hpp:29-33) + GMRES(m) restart */
 int fp_gmres(fp_system* s, fp_precond* p, const double* b, double* x, int32_t mem, const fp_gmres_options* opt,

@@ -33,6 +33,7 @@ typedef struct fp_workload_spec {
   double frac_stick, frac_slip;
   double aperture_median, aperture_sigma_ln;
   uint64_t seed;
+  double stab_beta;  /* jump-penalty constant (assembly.hpp:26 / presets.cpp:246); <= 0 selects the preset value */
 } fp_workload_spec;
 
 typedef struct fp_workload fp_workload;

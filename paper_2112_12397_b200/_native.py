@@ -55,8 +55,17 @@ class FpGmresOptions(C.Structure):
 class FpSolveStats(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("breakdown", C.c_int32),
                 ("restarts", C.c_int32), ("precond_applies", C.c_int32), ("final_rel_residual", C.c_double),
-                ("device_seconds", C.c_double), ("residual_history", C.POINTER(C.c_double)),
+                ("device_seconds", C.c_double), ("kernel_launches", C.c_int64),
+                ("residual_history", C.POINTER(C.c_double)),
                 ("history_capacity", C.c_int32), ("history_len", C.c_int32)]
+
+
+class FpProfile(C.Structure):
+    _fields_ = [("apply_ms", C.c_double), ("apply_bytes", C.c_double), ("apply_launches", C.c_int32),
+                ("japply_ms", C.c_double), ("japply_bytes", C.c_double), ("fine_resid_ms", C.c_double),
+                ("fine_resid_bytes", C.c_double), ("fine_post_ms", C.c_double), ("fine_post_bytes", C.c_double),
+                ("band_ms", C.c_double), ("band_bytes", C.c_double), ("coarse_ms", C.c_double),
+                ("n_levels", C.c_int32), ("level_rows", C.c_int32 * 32), ("level_nnz", C.c_int64 * 32)]
 
 
 class FpAmgLevelDesc(C.Structure):
@@ -78,7 +87,7 @@ class FpWorkloadSpec(C.Structure):
                 ("fractures", C.POINTER(FpFractureSpec)), ("E_median", C.c_double), ("E_sigma_ln", C.c_double),
                 ("E_layers", C.c_int32), ("nu", C.c_double), ("nu_lo", C.c_double), ("nu_hi", C.c_double),
                 ("frac_stick", C.c_double), ("frac_slip", C.c_double), ("aperture_median", C.c_double),
-                ("aperture_sigma_ln", C.c_double), ("seed", C.c_uint64)]
+                ("aperture_sigma_ln", C.c_double), ("seed", C.c_uint64), ("stab_beta", C.c_double)]
 
 
 # Every symbol include/*.h declares, with its ctypes signature (restype, argtypes).
@@ -107,6 +116,7 @@ SIGNATURES = {
     "fp_amg_apply": (C.c_int, [_P, _P, _P, C.c_int32]),
     "fp_precond_inner_calls": (C.c_int64, [_P, C.c_int32]),
     "fp_precond_traffic": (C.c_int, [_P, _DP, C.POINTER(C.c_int32), _DP]),
+    "fp_precond_profile": (C.c_int, [_P, C.c_int32, C.POINTER(FpProfile)]),
     "fp_gmres": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(FpGmresOptions), C.POINTER(FpSolveStats)]),
     "fp_workload_preset": (C.c_int, [C.c_int32, C.c_uint64, _PP]),
     "fp_workload_custom": (C.c_int, [C.POINTER(FpWorkloadSpec), _PP]),

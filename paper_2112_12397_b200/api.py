@@ -138,6 +138,7 @@ class SolveStats:
     restarts: int = 0
     precond_applies: int = 0
     device_seconds: float = 0.0
+    kernel_launches: int = 0
 
 
 def _vec(x, n: int):
@@ -306,6 +307,15 @@ class GpuPreconditioner:
     def reset_count(self) -> None:
         N.lib.fp_precond_inner_calls(self._h, 1)
 
+    def profile(self, reps: int = 20) -> dict:
+        """Per-phase CUDA-event timings (ms per launch) and algorithmic bytes (fp_precond_profile)."""
+        p = N.FpProfile()
+        N.check(N.lib.fp_precond_profile(self._h, reps, C.byref(p)))
+        out = {k: getattr(p, k) for k, _ in N.FpProfile._fields_ if k not in ("level_rows", "level_nnz")}
+        out["level_rows"] = list(p.level_rows[: p.n_levels])
+        out["level_nnz"] = list(p.level_nnz[: p.n_levels])
+        return out
+
     def traffic(self):
         ab, jb, la = C.c_double(), C.c_double(), C.c_int32()
         N.check(N.lib.fp_precond_traffic(self._h, C.byref(ab), C.byref(la), C.byref(jb)))
@@ -346,7 +356,7 @@ def gmres(op: BlockSystemOperator, precond: GpuPreconditioner, b, tol: float, ma
     st.history_capacity = hist.size
     N.check(N.lib.fp_gmres(op._h, precond._h, bp, xp, mem, C.byref(o), C.byref(st)))
     stats = SolveStats(st.iterations, list(hist[: st.history_len]), bool(st.converged), bool(st.breakdown),
-                       st.restarts, st.precond_applies, st.device_seconds)
+                       st.restarts, st.precond_applies, st.device_seconds, int(st.kernel_launches))
     return x, stats
 
 
@@ -374,6 +384,7 @@ class Workload:
             s.aperture_median = spec.get("aperture_median", 1e-4)
             s.aperture_sigma_ln = spec.get("aperture_sigma_ln", 0.0)
             s.seed = seed
+            s.stab_beta = spec.get("stab_beta", 0.0)
             N.check(N.lib.fp_workload_custom(C.byref(s), C.byref(self._h)))
 
     def __del__(self):

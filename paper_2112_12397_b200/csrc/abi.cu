@@ -375,6 +375,25 @@ int fp_precond_traffic(fp_precond* p, double* apply_bytes, int32_t* launches, do
   });
 }
 
+int fp_precond_profile(fp_precond* p, int32_t reps, fp_profile* out) {
+  return guard([&] {
+    need(p && out, "fp_precond_profile: null argument");
+    const fpd::ProfileResult r = fpd::profile_precond(*p->sys->dev, *p->dev, reps, p->sys->stream);
+    std::memset(out, 0, sizeof(*out));
+    out->apply_ms = r.apply_ms, out->apply_bytes = r.apply_bytes, out->apply_launches = r.apply_launches;
+    out->japply_ms = r.japply_ms, out->japply_bytes = r.japply_bytes;
+    out->fine_resid_ms = r.fine_resid_ms, out->fine_resid_bytes = r.fine_resid_bytes;
+    out->fine_post_ms = r.fine_post_ms, out->fine_post_bytes = r.fine_post_bytes;
+    out->band_ms = r.band_ms, out->band_bytes = r.band_bytes, out->coarse_ms = r.coarse_ms;
+    const auto& lv = p->dev->amg->lv;
+    out->n_levels = int32_t(lv.size());
+    for (size_t l = 0; l < lv.size() && l < 32; ++l) {
+      out->level_rows[l] = lv[l].n;
+      out->level_nnz[l] = lv[l].bsr3 ? 9 * lv[l].Ab.nblocks : lv[l].As.nnz;
+    }
+  });
+}
+
 int fp_gmres(fp_system* s, fp_precond* p, const double* b, double* x, int32_t mem, const fp_gmres_options* o,
              fp_solve_stats* stats) {
   return guard([&] {
@@ -408,6 +427,7 @@ int fp_gmres(fp_system* s, fp_precond* p, const double* b, double* x, int32_t me
       stats->precond_applies = r.precond_applies;
       stats->final_rel_residual = r.final_rel_residual;
       stats->device_seconds = r.device_seconds;
+      stats->kernel_launches = r.launches;
       stats->history_len = int32_t(r.history.size());
       if (stats->residual_history)
         for (int i = 0; i < stats->history_capacity && i < int(r.history.size()); ++i)
@@ -440,6 +460,7 @@ int fp_workload_custom(const fp_workload_spec* sp, fp_workload** out) {
     s.frac_stick = sp->frac_stick, s.frac_slip = sp->frac_slip;
     s.aperture_median = sp->aperture_median, s.aperture_sigma_ln = sp->aperture_sigma_ln;
     s.seed = sp->seed;
+    if (sp->stab_beta > 0.0) s.stab_beta = sp->stab_beta;
     auto w = std::make_unique<fp_workload>();
     w->w = fpb::generate_workload(s);
     *out = w.release();

@@ -258,20 +258,20 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   if (opt.pre_sweeps == 1) {
     // fused: x = (w b)/d (first sweep from zero) and r = b - A x with x gathered on the fly
     launch_level(L, GPresmooth{b, d, w}, EResidPre{b, d, w, cur, L.r.get()}, s);
-    if (Lg) Lg->add(A_b + 16.0 * nd + 8.0 * 4 * nd);
+    if (Lg) Lg->add(A_b + 32.0 * nd);  // b, d gathered once; x, r written
   } else {
     presmooth_kernel<<<blocks_for(L.n, 256), 256, 0, s>>>(L.n, b, d, w, cur);
     if (Lg) Lg->add(24.0 * nd);
     for (int it = 1; it < opt.pre_sweeps; ++it) {
       double* nxt = cur == L.xt.get() ? L.xt2.get() : L.xt.get();
       launch_level(L, GPlain{cur}, EJacobi{b, d, w, cur, nxt}, s);
-      if (Lg) Lg->add(A_b + 8.0 * nd + 8.0 * 4 * nd);
+      if (Lg) Lg->add(A_b + 32.0 * nd);  // x gathered; b, d read; x' written
       cur = nxt;
     }
     launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s);
     if (Lg) Lg->add(A_b + 8.0 * nd + 16.0 * nd);
   }
-  DeviceLevel& C = lv[l + 1];
+  DeviceLevel& C = lv[l + 1];  // holds P_{l+1} (n_l x n_{l+1}) and R_{l+1} = P^T
   launch_sell(C.R, GPlain{L.r.get()}, EStore{C.b.get()}, s);  // r_c = P^T r  (amg.cpp:166)
   if (Lg) Lg->add(C.R.matrix_bytes() + 8.0 * nd + 8.0 * C.n);
   vcycle(l + 1, C.b.get(), C.x.get(), nullptr, s, Lg);
@@ -284,7 +284,7 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
       launch_level(L, GPlain{cur}, EJacobiSubFrom{b, d, w, cur, sub_from, nxt}, s);
     else
       launch_level(L, GPlain{cur}, EJacobi{b, d, w, cur, nxt}, s);
-    if (Lg) Lg->add(A_b + 8.0 * nd + 8.0 * (4 + (final_sweep && sub_from)) * nd);
+    if (Lg) Lg->add(A_b + 8.0 * (4 + (final_sweep && sub_from)) * nd);
     cur = nxt;
   }
 }
@@ -442,7 +442,7 @@ GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart
   cuda_check(cudaStreamEndCapture(tmp, &g), "end capture");
   cudaGraphDestroy(g);
   cudaStreamDestroy(tmp);
-  apply_bytes = a.bytes, japply_bytes = j.bytes, apply_launches = a.launches;
+  apply_bytes = a.bytes, japply_bytes = j.bytes, apply_launches = a.launches, japply_launches = j.launches;
 }
 
 GmresSolver::~GmresSolver() {
@@ -506,10 +506,12 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
   double rnorm = bnorm;
   cuda_check(cudaMemcpyAsync(scal_.get(), &rnorm, sizeof(double), cudaMemcpyHostToDevice, s), "beta");
   const int per_apply = pc_.inner_per_apply();
+  res.launches += 2;  // ||b||
   auto launch_pj = [&] {
     cuda_check(cudaGraphLaunch(pj_exec_, s), "graph launch pj");
     pc_.inner_calls += per_apply;
     ++res.precond_applies;
+    res.launches += apply_launches + japply_launches;
   };
   for (;;) {
     const int budget = std::min(restart_, o.max_iter - res.iterations);
@@ -520,7 +522,9 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
     int m = 0, assembled_at = -1;
     bool hit = false, cyc_done = false, happy = false;
     double tr = 1.0;
+    res.launches += 1;  // start_cycle
     auto assemble = [&](int mm) {
+      res.launches += 4;  // backsub, combine, 2 reductions (+ the graph, counted in launch_pj)
       backsub_kernel<<<1, 1, 0, s>>>(mm, ldr_, R_.get(), g_.get(), y_.get(), flag_.get());
       basis_combine_kernel<<<blocks_for(n_, 256), 256, 0, s>>>(n_, ldv_, mm, V_.get(), y_.get(), stage);
       launch_pj();  // z = M^-1 (V y) = dx_cycle, jout = J dx_cycle
@@ -540,6 +544,7 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
       cuda_check(cudaLaunchCooperativeKernel((void*)mgs_kernel, dim3(mgs_grid_), dim3(kMgsThreads), args, 0, s),
                  "mgs launch");
       cuda_check(cudaStreamSynchronize(s), "mgs sync");
+      res.launches += 1;
       const GmresStatus st_h = *status_h_;
       if (st_h.nonfinite) throw fpb::numerical_error("gmres: non-finite vector in Arnoldi process");
       ++m;
@@ -574,6 +579,7 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
     add_inplace_kernel<<<blocks_for(n_, 256), 256, 0, s>>>(n_, xtot_.get(), dx_.get());
     cuda_check(cudaGraphLaunch(j_exec_, s), "graph launch j");
     rnorm = norm_into(b, jout_.get(), r_.get(), scal_.get(), s);  // r = b - J x, beta on device
+    res.launches += 1 + japply_launches + 2;
     if (!res.history.empty()) res.history.back() = rnorm / bnorm;
     if (rnorm <= o.tol * bnorm) {
       res.converged = true;
@@ -592,6 +598,79 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
   res.device_seconds = ms * 1e-3;
   cudaEventDestroy(e0), cudaEventDestroy(e1);
   return res;
+}
+
+// ------------------------------------------------------------ profiling
+ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int reps, cudaStream_t s) {
+  ProfileResult r;
+  reps = std::max(1, reps);
+  const int n = sys.n();
+  DevBuf<double> x(n), y(n);
+  cuda_check(cudaMemsetAsync(x.get(), 0, x.bytes(), s), "memset");
+  cudaEvent_t e0, e1;
+  cuda_check(cudaEventCreate(&e0), "event");
+  cuda_check(cudaEventCreate(&e1), "event");
+  auto timed = [&](auto&& fn) {
+    fn();
+    cuda_check(cudaStreamSynchronize(s), "profile warmup");
+    cudaEventRecord(e0, s);
+    for (int i = 0; i < reps; ++i) fn();
+    cudaEventRecord(e1, s);
+    cuda_check(cudaEventSynchronize(e1), "profile sync");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return double(ms) / reps;
+  };
+  auto graph_of = [&](auto&& fn) {
+    cudaGraph_t g;
+    cudaGraphExec_t ex;
+    cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+    fn();
+    cuda_check(cudaStreamEndCapture(s, &g), "end capture");
+    cuda_check(cudaGraphInstantiate(&ex, g, 0), "instantiate");
+    cudaGraphDestroy(g);
+    return ex;
+  };
+  Ledger la, lj;
+  cudaGraphExec_t ga = graph_of([&] { pc.enqueue_apply(x.get(), y.get(), 1.0, 1.0, s, &la); });
+  r.apply_ms = timed([&] { cudaGraphLaunch(ga, s); });
+  r.apply_bytes = la.bytes, r.apply_launches = la.launches;
+  cudaGraphExecDestroy(ga);
+  cudaGraphExec_t gj = graph_of([&] { sys.enqueue_apply(x.get(), y.get(), 1.0, 1.0, s, &lj); });
+  r.japply_ms = timed([&] { cudaGraphLaunch(gj, s); });
+  r.japply_bytes = lj.bytes;
+  cudaGraphExecDestroy(gj);
+  DeviceAmg& A = *pc.amg;
+  if (A.n_levels() > 1) {
+    DeviceLevel& L = A.lv[0];
+    const double w = A.opt.jacobi_omega, nd = L.n;
+    cuda_check(cudaMemsetAsync(L.b.get(), 0, L.b.bytes(), s), "memset");
+    cuda_check(cudaMemsetAsync(L.xt.get(), 0, L.xt.bytes(), s), "memset");
+    r.fine_resid_ms = timed([&] {
+      launch_level(L, GPresmooth{L.b.get(), L.d.get(), w}, EResidPre{L.b.get(), L.d.get(), w, L.xt.get(), L.r.get()}, s);
+    });
+    r.fine_resid_bytes = L.a_bytes() + 32.0 * nd;
+    r.fine_post_ms = timed([&] {
+      launch_level(L, GPlain{L.xt.get()}, EJacobi{L.b.get(), L.d.get(), w, L.xt.get(), L.xt2.get()}, s);
+    });
+    r.fine_post_bytes = L.a_bytes() + 32.0 * nd;
+  }
+  if (pc.band.n > 0) {
+    Ledger lb;
+    pc.enqueue_band(pc.tp.get(), 1.0, pc.vp.get(), nullptr, nullptr, 1.0, 0, s, &lb);
+    r.band_bytes = lb.bytes;
+    r.band_ms = timed([&] { pc.enqueue_band(pc.tp.get(), 1.0, pc.vp.get(), nullptr, nullptr, 1.0, 0, s, nullptr); });
+  }
+  {
+    DeviceLevel& C = A.lv.back();
+    r.coarse_ms = timed([&] {
+      coarse_solve_kernel<<<1, kCoarseThreads, sizeof(double) * std::max(A.coarse_n, 1), s>>>(
+          DenseLUView{A.coarse_n, A.coarse_rank, A.lu.get(), A.prow.get(), A.pcol.get()}, C.b.get(), C.xt.get());
+    });
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return r;
 }
 
 }  // namespace fpd

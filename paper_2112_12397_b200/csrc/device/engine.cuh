@@ -126,7 +126,16 @@ struct SolveResult {
   double final_rel_residual = 0.0;
   std::vector<double> history;
   double device_seconds = 0.0;
+  long long launches = 0;
 };
+
+struct ProfileResult {
+  double apply_ms = 0, apply_bytes = 0, japply_ms = 0, japply_bytes = 0;
+  double fine_resid_ms = 0, fine_resid_bytes = 0, fine_post_ms = 0, fine_post_bytes = 0;
+  double band_ms = 0, band_bytes = 0, coarse_ms = 0;
+  int apply_launches = 0;
+};
+ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int reps, cudaStream_t s);
 
 // Restarted right-preconditioned GMRES on the device (gmres.cpp semantics per
 // cycle + the GMRES(m) wrapper of SURVEY §8(a) G1).
@@ -136,7 +145,7 @@ class GmresSolver {
   ~GmresSolver();
   SolveResult solve(const double* b_dev, double* x_dev, const SolveOptions& o, cudaStream_t s);
   double apply_bytes = 0.0, japply_bytes = 0.0;  // algorithmic bytes of one precond / J apply
-  int apply_launches = 0;
+  int apply_launches = 0, japply_launches = 0;
 
  private:
   void build_graphs(double st, double sp, cudaStream_t s);

@@ -12,11 +12,25 @@
 #include <cmath>
 #include <cstdio>
 #include <deque>
+#include <chrono>
+#include <cstdlib>
 #include <limits>
 
 namespace fpb {
 
 namespace {
+
+// FRACPREC_B200_VERBOSE=1 prints per-phase setup times to stderr
+struct PhaseLog {
+  bool on = std::getenv("FRACPREC_B200_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what, long a = -1, long b = -1) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[setup] %-28s %8.3f s  %ld %ld\n", what, std::chrono::duration<double>(now - t).count(), a, b);
+    t = now;
+  }
+};
 
 struct Strength {
   std::vector<int64_t> off;
@@ -206,14 +220,18 @@ HostAmg amg_setup(const Csr& A, const std::vector<std::vector<double>>& near_nul
     f.diag = diag_extract(A);
     h.levels.push_back(std::move(f));
   }
+  PhaseLog plog;
   for (;;) {
     HostLevel& fine = h.levels.back();
     const int n = fine.A.n_rows;
     for (int i = 0; i < n; ++i)
       if (fine.diag[i] == 0.0) throw numerical_error("amg_setup: zero diagonal entry at row " + std::to_string(i));
     if (n <= opt.max_coarse || int(h.levels.size()) >= opt.max_levels) break;
+    plog.mark("level start", n, long(fine.A.nnz()));
     const Strength g = build_strength(fine.A, opt.strength_threshold);
+    plog.mark("strength", long(g.nbr.size()));
     auto [agg, n_agg] = aggregate(g, n);
+    plog.mark("aggregate", n_agg);
     if (n_agg == 0) break;
     const int k = int(nn.size());
     // rows of each aggregate in ascending order (counting sort)
@@ -269,14 +287,21 @@ HostAmg amg_setup(const Csr& A, const std::vector<std::vector<double>>& near_nul
         }
       }
     }
+    plog.mark("tentative P", nc, long(P.nnz()));
     if (opt.prolongation_smoothing) {
       std::vector<double> dinv(static_cast<size_t>(n));
       for (int i = 0; i < n; ++i) dinv[i] = 1.0 / fine.diag[i];
       const Csr DA = scale_rows(fine.A, dinv);
       P = add_scaled(P, spgemm(DA, P), 1.0, -opt.jacobi_omega);
     }
+    plog.mark("smoothed P", long(P.nnz()));
     if (nc > opt.stall_ratio * n) break;
-    Csr Ac = spgemm(transpose(P), spgemm(fine.A, P));
+    const Csr AP = spgemm(fine.A, P);
+    plog.mark("A P", long(AP.nnz()));
+    const Csr Pt = transpose(P);
+    plog.mark("P^T");
+    Csr Ac = spgemm(Pt, AP);
+    plog.mark("P^T (A P)", long(Ac.nnz()));
     std::vector<std::vector<double>> nnc(static_cast<size_t>(k), std::vector<double>(static_cast<size_t>(nc), 0.0));
     for (int a = 0; a < n_agg; ++a)
       for (int r = 0; r < rank[a]; ++r)
@@ -292,6 +317,7 @@ HostAmg amg_setup(const Csr& A, const std::vector<std::vector<double>>& near_nul
   }
   const Csr& Ac = h.levels.back().A;
   h.coarse.compute(Ac.to_dense(), Ac.n_rows);
+  plog.mark("coarse LU", Ac.n_rows);
   return h;
 }
 

@@ -28,7 +28,10 @@ struct WorkloadSpec {
   int E_layers = 0;                 // 0: independent per element; >0: per z-layer
   double nu = 0.25, nu_lo = 0.0, nu_hi = 0.0;  // nu_hi > nu_lo: per-layer U(nu_lo, nu_hi)
   // contact / flow (assembly.hpp:18-39)
-  double friction = 0.6, cohesion = 0.0, C_f0 = 9.87e-15, mu_f = 1e-3, stab_beta = 0.02, dt = 0.5;
+  // stab_beta = 1.0: the reference's value for problems read from JSON (presets.cpp:246).  Its struct
+  // default 0.02 (assembly.hpp:26) makes the stick penalty C1 H~^-1 C2 50x stiffer and the
+  // AMG-preconditioned solve stagnates ("Workload").
+  double friction = 0.6, cohesion = 0.0, C_f0 = 9.87e-15, mu_f = 1e-3, stab_beta = 1.0, dt = 0.5;
   double frac_stick = 0.7, frac_slip = 0.2;  // open = rest
   double aperture_median = 1e-4, aperture_sigma_ln = 0.0;
   double sigma_load = 1e7;  // top-face compressive load, Pa

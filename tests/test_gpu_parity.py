@@ -105,7 +105,7 @@ def test_precond_apply_matches_oracle(case, variant):
 
 @pytest.mark.parametrize("variant", ["tpu", "tup"])
 def test_product_built_precond_matches_oracle(variant):
-    J = small_workload(seed=11, cells=(7, 6, 5))
+    J = small_workload(seed=11, cells=(8, 6, 5))
     osys = oracle_system(J)
     opc = O.OraclePrecond(osys, variant, coords=J.node_coords)
     op = api.BlockSystemOperator(J)
