@@ -34,6 +34,7 @@ typedef struct fp_workload_spec {
   double aperture_median, aperture_sigma_ln;
   uint64_t seed;
   double stab_beta;  /* jump-penalty constant (assembly.hpp:26 / presets.cpp:246); <= 0 selects the preset value */
+  double slip_factor; /* slip increment in units of the 0.1 tau/k freeze threshold; <= 0 selects the preset value */
 } fp_workload_spec;
 
 typedef struct fp_workload fp_workload;

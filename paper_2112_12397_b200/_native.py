@@ -87,7 +87,8 @@ class FpWorkloadSpec(C.Structure):
                 ("fractures", C.POINTER(FpFractureSpec)), ("E_median", C.c_double), ("E_sigma_ln", C.c_double),
                 ("E_layers", C.c_int32), ("nu", C.c_double), ("nu_lo", C.c_double), ("nu_hi", C.c_double),
                 ("frac_stick", C.c_double), ("frac_slip", C.c_double), ("aperture_median", C.c_double),
-                ("aperture_sigma_ln", C.c_double), ("seed", C.c_uint64), ("stab_beta", C.c_double)]
+                ("aperture_sigma_ln", C.c_double), ("seed", C.c_uint64), ("stab_beta", C.c_double),
+                ("slip_factor", C.c_double)]
 
 
 # Every symbol include/*.h declares, with its ctypes signature (restype, argtypes).

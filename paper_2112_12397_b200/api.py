@@ -173,7 +173,7 @@ class BlockSystemOperator:
         self._n = J.total_dimension()
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and N is not None and getattr(N, "lib", None) is not None:
             N.lib.fp_system_destroy(self._h)
             self._h = None
 
@@ -209,7 +209,7 @@ class HostPreconditioner:
         self.variant = cfg.variant
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and N is not None and getattr(N, "lib", None) is not None:
             N.lib.fp_host_precond_destroy(self._h)
             self._h = None
 
@@ -277,7 +277,7 @@ class GpuPreconditioner:
         return cls(op, h, variant)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and N is not None and getattr(N, "lib", None) is not None:
             N.lib.fp_precond_destroy(self._h)
             self._h = None
 
@@ -385,10 +385,11 @@ class Workload:
             s.aperture_sigma_ln = spec.get("aperture_sigma_ln", 0.0)
             s.seed = seed
             s.stab_beta = spec.get("stab_beta", 0.0)
+            s.slip_factor = spec.get("slip_factor", 0.0)
             N.check(N.lib.fp_workload_custom(C.byref(s), C.byref(self._h)))
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and N is not None and getattr(N, "lib", None) is not None:
             N.lib.fp_workload_destroy(self._h)
             self._h = None
 

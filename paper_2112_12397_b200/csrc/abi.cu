@@ -461,6 +461,7 @@ int fp_workload_custom(const fp_workload_spec* sp, fp_workload** out) {
     s.aperture_median = sp->aperture_median, s.aperture_sigma_ln = sp->aperture_sigma_ln;
     s.seed = sp->seed;
     if (sp->stab_beta > 0.0) s.stab_beta = sp->stab_beta;
+    if (sp->slip_factor > 0.0) s.slip_factor = sp->slip_factor;
     auto w = std::make_unique<fp_workload>();
     w->w = fpb::generate_workload(s);
     *out = w.release();

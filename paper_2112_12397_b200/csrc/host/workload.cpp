@@ -416,8 +416,8 @@ Workload generate_workload(const WorkloadSpec& s) {
       if (region[f] == Region::slip) {
         const double tau = s.cohesion - trac[f][0] * tan_th;
         const double thr = std::max(1e-12, 0.1 * std::max(tau, 0.0) / k_scale);
-        gap[f][1] = 10.0 * thr * mag * std::cos(phi);
-        gap[f][2] = 10.0 * thr * mag * std::sin(phi);
+        gap[f][1] = s.slip_factor * thr * mag * std::cos(phi);
+        gap[f][2] = s.slip_factor * thr * mag * std::sin(phi);
         sdir[f] = {std::cos(phi), std::sin(phi)};
       }
     }

@@ -34,6 +34,9 @@ struct WorkloadSpec {
   double friction = 0.6, cohesion = 0.0, C_f0 = 9.87e-15, mu_f = 1e-3, stab_beta = 1.0, dt = 0.5;
   double frac_stick = 0.7, frac_slip = 0.2;  // open = rest
   double aperture_median = 1e-4, aperture_sigma_ln = 0.0;
+  // slip increment |dg_T| = slip_factor * (0.1 tau / k) * (1 + U[0,1)): SURVEY §8(d) asks for >= 10x the
+  // direction-freeze threshold of assembly.cpp:20-23 so that dt_T/dg_T = (tau/|dg_T|)(I - m m^T) != 0
+  double slip_factor = 10.0;
   double sigma_load = 1e7;  // top-face compressive load, Pa
   double p0 = 1e6;          // fracture pressure level, Pa
   uint64_t seed = 42;
