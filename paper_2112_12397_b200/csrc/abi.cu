@@ -389,7 +389,7 @@ int fp_precond_profile(fp_precond* p, int32_t reps, fp_profile* out) {
     out->n_levels = int32_t(lv.size());
     for (size_t l = 0; l < lv.size() && l < 32; ++l) {
       out->level_rows[l] = lv[l].n;
-      out->level_nnz[l] = lv[l].bsr3 ? 9 * lv[l].Ab.nblocks : lv[l].As.nnz;
+      out->level_nnz[l] = lv[l].bsr3 ? 9 * lv[l].Ab.nblocks : lv[l].Am.nnz();
     }
   });
 }

@@ -31,6 +31,13 @@ struct SellView {
   const double* vals = nullptr;
 };
 
+struct CsrView {  // plain CSR, 64-bit offsets (warp-per-row kernel)
+  int n_rows = 0;
+  const long long* rp = nullptr;
+  const int* ci = nullptr;
+  const double* v = nullptr;
+};
+
 struct Bsr3View {
   int n_brows = 0;
   const long long* slice_off = nullptr;  // block-slot index of (slice, k=0, lane=0)

@@ -46,14 +46,44 @@ void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s) {
 }
 
 template <class G, class E>
+void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s) {
+  if (!A.warp) {
+    launch_sell(A.sell, g, e, s);
+    return;
+  }
+  if (A.csr.n_rows == 0) return;
+  csr_warp_kernel<<<blocks_for((long long)A.csr.n_rows * 32, kWarpRowThreads), kWarpRowThreads, 0, s>>>(A.csr.view(),
+                                                                                                         g, e);
+  cuda_check(cudaGetLastError(), "csr_warp_kernel launch");
+}
+
+template <class G, class E>
 void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s) {
   if (L.bsr3)
     launch_bsr3(L.Ab, g, e, s);
   else
-    launch_sell(L.As, g, e, s);
+    launch_mat(L.Am, g, e, s);
 }
 
 }  // namespace
+
+// Few or long rows (coarse levels, R = P^T) stream best one warp per row;
+// many short rows one thread per row in SELL-32 slices.
+DMat make_mat(const fpb::Csr& A) {
+  DMat M;
+  const double avg = A.n_rows > 0 ? double(A.nnz()) / A.n_rows : 0.0;
+  M.warp = A.n_rows > 0 && (avg >= 48.0 || (A.n_rows < 8192 && avg >= 8.0));
+  if (!M.warp) {
+    M.sell = make_sell(A);
+    return M;
+  }
+  M.csr.n_rows = A.n_rows, M.csr.n_cols = A.n_cols, M.csr.nnz = A.nnz();
+  std::vector<long long> rp(A.rp.begin(), A.rp.end());
+  M.csr.rp.upload(rp);
+  M.csr.ci.upload(A.ci);
+  M.csr.v.upload(A.v);
+  return M;
+}
 
 // ------------------------------------------------------------ format upload
 DSell make_sell(const fpb::Csr& A) {
@@ -203,15 +233,15 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
         D.bsr3 = true;
         D.Ab = make_bsr3(H.A);
       } else {
-        D.As = make_sell(H.A);
+        D.Am = make_mat(H.A);
       }
     }
     if (l > 0) {
-      D.P = make_sell(H.P);
-      D.R = make_sell(fpb::transpose(H.P));
+      D.P = make_mat(H.P);
+      D.R = make_mat(fpb::transpose(H.P));
     }
     D.d.upload(H.diag);
-    D.b.alloc(D.n), D.x.alloc(D.n), D.xt.alloc(D.n), D.xt2.alloc(D.n), D.r.alloc(D.n);
+    D.b.alloc(D.n), D.x.alloc(D.n), D.xt.alloc(D.n), D.xt2.alloc(D.n), D.xt3.alloc(D.n), D.r.alloc(D.n);
   }
   // coarse LU, column-major for contiguous column sweeps
   coarse_n = h.coarse.n;
@@ -222,7 +252,7 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
   lu.upload(cm);
   prow.upload(h.coarse.prow);
   pcol.upload(h.coarse.pcol);
-  const size_t smem = sizeof(double) * size_t(std::max(coarse_n, 1));
+  const size_t smem = coarse_smem_bytes(coarse_n);
   if (smem > 48 * 1024)
     cuda_check(cudaFuncSetAttribute(coarse_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
                "coarse smem attribute");
@@ -235,13 +265,14 @@ std::vector<int> DeviceAmg::level_sizes() const {
   return s;
 }
 
-void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from, cudaStream_t s, Ledger* Lg) {
+void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from, double* xhat, cudaStream_t s,
+                       Ledger* Lg) {
   DeviceLevel& L = lv[l];
   const int last = n_levels() - 1;
   const double nd = L.n;
   if (l == last) {
     double* out = sub_from ? L.xt.get() : x;
-    coarse_solve_kernel<<<1, kCoarseThreads, sizeof(double) * std::max(coarse_n, 1), s>>>(
+    coarse_solve_kernel<<<1, kCoarseThreads, coarse_smem_bytes(coarse_n), s>>>(
         DenseLUView{coarse_n, coarse_rank, lu.get(), prow.get(), pcol.get()}, b, out);
     cuda_check(cudaGetLastError(), "coarse_solve_kernel launch");
     if (Lg) Lg->add(8.0 * coarse_n * double(coarse_n) + 16.0 * coarse_n + 8.0 * coarse_n);
@@ -254,32 +285,47 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   const double w = opt.jacobi_omega;
   const double* d = L.d.get();
   const double A_b = L.a_bytes();
-  double* cur = L.xt.get();
-  if (opt.pre_sweeps == 1) {
-    // fused: x = (w b)/d (first sweep from zero) and r = b - A x with x gathered on the fly
-    launch_level(L, GPresmooth{b, d, w}, EResidPre{b, d, w, cur, L.r.get()}, s);
-    if (Lg) Lg->add(A_b + 32.0 * nd);  // b, d gathered once; x, r written
-  } else {
-    presmooth_kernel<<<blocks_for(L.n, 256), 256, 0, s>>>(L.n, b, d, w, cur);
+  // First Jacobi sweep from x = 0 is x = (w b)/d exactly (A 0 = 0, amg.cpp:138-139); it was
+  // written by the kernel that produced b (or by presmooth_kernel for an external input).
+  if (!xhat) {
+    xhat = L.xt.get();
+    presmooth_kernel<<<blocks_for(L.n, 256), 256, 0, s>>>(L.n, b, d, w, xhat);
     if (Lg) Lg->add(24.0 * nd);
-    for (int it = 1; it < opt.pre_sweeps; ++it) {
-      double* nxt = cur == L.xt.get() ? L.xt2.get() : L.xt.get();
-      launch_level(L, GPlain{cur}, EJacobi{b, d, w, cur, nxt}, s);
-      if (Lg) Lg->add(A_b + 32.0 * nd);  // x gathered; b, d read; x' written
-      cur = nxt;
-    }
-    launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s);
-    if (Lg) Lg->add(A_b + 8.0 * nd + 16.0 * nd);
   }
+  double* cur = xhat;
+  // two ping-pong buffers distinct from xhat (and from the output x)
+  double* pool[3] = {L.xt.get(), L.xt2.get(), L.xt3.get()};
+  double* tA = nullptr;
+  double* tB = nullptr;
+  for (double* p : pool) {
+    if (p == xhat) continue;
+    if (!tA)
+      tA = p;
+    else if (!tB)
+      tB = p;
+  }
+  auto other = [&](const double* c) { return c == tA ? tB : tA; };
+  for (int it = 1; it < opt.pre_sweeps; ++it) {
+    double* nxt = other(cur);
+    launch_level(L, GPlain{cur}, EJacobi{b, d, w, cur, nxt}, s);
+    if (Lg) Lg->add(A_b + 32.0 * nd);  // x gathered; b, d read; x' written
+    cur = nxt;
+  }
+  launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s);  // r = b - A x
+  if (Lg) Lg->add(A_b + 24.0 * nd);
   DeviceLevel& C = lv[l + 1];  // holds P_{l+1} (n_l x n_{l+1}) and R_{l+1} = P^T
-  launch_sell(C.R, GPlain{L.r.get()}, EStore{C.b.get()}, s);  // r_c = P^T r  (amg.cpp:166)
-  if (Lg) Lg->add(C.R.matrix_bytes() + 8.0 * nd + 8.0 * C.n);
-  vcycle(l + 1, C.b.get(), C.x.get(), nullptr, s, Lg);
-  launch_sell(C.P, GPlain{C.x.get()}, EAddTo{cur, cur}, s);  // x += P e_c  (amg.cpp:168-169)
+  const bool coarse_next = l + 1 == last;
+  if (coarse_next)
+    launch_mat(C.R, GPlain{L.r.get()}, EStore{C.b.get()}, s);  // r_c = P^T r  (amg.cpp:166)
+  else
+    launch_mat(C.R, GPlain{L.r.get()}, EStorePre{C.b.get(), C.d.get(), w, C.xt.get()}, s);
+  if (Lg) Lg->add(C.R.matrix_bytes() + 8.0 * nd + 8.0 * C.n * (coarse_next ? 1 : 3));
+  vcycle(l + 1, C.b.get(), C.x.get(), nullptr, coarse_next ? nullptr : C.xt.get(), s, Lg);
+  launch_mat(C.P, GPlain{C.x.get()}, EAddTo{cur, cur}, s);  // x += P e_c  (amg.cpp:168-169)
   if (Lg) Lg->add(C.P.matrix_bytes() + 8.0 * C.n + 16.0 * nd);
   for (int it = 0; it < opt.post_sweeps; ++it) {
     const bool final_sweep = it + 1 == opt.post_sweeps;
-    double* nxt = final_sweep ? x : (cur == L.xt.get() ? L.xt2.get() : L.xt.get());
+    double* nxt = final_sweep ? x : other(cur);
     if (final_sweep && sub_from)
       launch_level(L, GPlain{cur}, EJacobiSubFrom{b, d, w, cur, sub_from, nxt}, s);
     else
@@ -289,17 +335,19 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   }
 }
 
-void DeviceAmg::enqueue_apply(const double* r, double* x, const double* sub_from, cudaStream_t s, Ledger* Lg) {
+void DeviceAmg::enqueue_apply(const double* r, double* x, const double* sub_from, cudaStream_t s, Ledger* Lg,
+                              double* xhat) {
+  if (n_levels() == 1) xhat = nullptr;  // single level: direct coarse solve, no smoothing
   if (opt.cycles_per_apply <= 1) {
-    vcycle(0, r, x, sub_from, s, Lg);
+    vcycle(0, r, x, sub_from, xhat, s, Lg);
     return;
   }
   const int n = fine_n();
-  vcycle(0, r, top_x.get(), nullptr, s, Lg);
+  vcycle(0, r, top_x.get(), nullptr, xhat, s, Lg);
   for (int c = 1; c < opt.cycles_per_apply; ++c) {  // residual-correction cycles (amg.cpp:297-303)
     launch_level(lv[0], GPlain{top_x.get()}, EResid{r, top_res.get()}, s);
     if (Lg) Lg->add(lv[0].a_bytes() + 24.0 * n);
-    vcycle(0, top_res.get(), top_dx.get(), nullptr, s, Lg);
+    vcycle(0, top_res.get(), top_dx.get(), nullptr, nullptr, s, Lg);
     add_inplace_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, top_x.get(), top_dx.get());
     if (Lg) Lg->add(24.0 * n);
   }
@@ -346,6 +394,7 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
                "band smem attribute");
   const int nu = s.n_u, nt = s.n_t, np = s.n_p;
   tt.alloc(nt), tu.alloc(nu), tp.alloc(np), su.alloc(nu), sp_.alloc(np), vp.alloc(np), tu2.alloc(nu), vu2.alloc(nu);
+  xh.alloc(nu);
 }
 
 void DevicePrecond::enqueue_band(const double* rhs, double rs, double* out, double* out2, const double* sub, double os,
@@ -371,6 +420,8 @@ void DevicePrecond::enqueue_apply(const double* x, double* y, double at, double 
   double* yt = y + nu;
   double* yp = y + nu + nt;
   const unsigned fb = blocks_for(np, 256);
+  const double* d0 = amg->lv[0].d.get();  // producers of the V-cycle input also emit (w r)/d
+  const double w0 = amg->opt.jacobi_omega;
   auto hin = [&](double* neg_out) {
     if (np == 0) return;
     hsolve_in_kernel<<<fb, 256, 0, s>>>(np, hlu.get(), hpiv.get(), xt, at, tt.get(), neg_out);
@@ -386,10 +437,11 @@ void DevicePrecond::enqueue_apply(const double* x, double* y, double at, double 
   if (variant == fpb::kTpu) {
     enqueue_band(xp, ap, tp.get(), nullptr, nullptr, 1.0, 0, s, L);  // t_p = T^-1 w_p
     hin(nullptr);                                                    // t_t = H~^-1 w_t
-    tpu_tu_kernel<<<blocks_for(nu, 256), 256, 0, s>>>(S.C1.view(), S.Q1.view(), xu, tt.get(), tp.get(), tu.get());
+    tpu_tu_kernel<<<blocks_for(nu, 256), 256, 0, s>>>(S.C1.view(), S.Q1.view(), xu, tt.get(), tp.get(), tu.get(), d0, w0,
+                                                      xh.get());
     cuda_check(cudaGetLastError(), "tpu_tu launch");
     if (L) L->add(S.C1.matrix_bytes() + S.Q1.matrix_bytes() + 8.0 * (2.0 * nu + nt + np));
-    amg->enqueue_apply(tu.get(), yu, nullptr, s, L);  // v_u = AMG(S~) t_u
+    amg->enqueue_apply(tu.get(), yu, nullptr, s, L, xh.get());  // v_u = AMG(S~) t_u
     launch_sell(S.Q2, GPlain{yu}, EStore{sp_.get()}, s);  // s_p = Q2 v_u
     if (L) L->add(S.Q2.matrix_bytes() + 8.0 * (nu + np));
     enqueue_band(sp_.get(), 1.0, yp, nullptr, tp.get(), ap, 1, s, L);  // v_p = t_p - T^-1 s_p
@@ -397,17 +449,17 @@ void DevicePrecond::enqueue_apply(const double* x, double* y, double at, double 
     return;
   }
   hin(variant == fpb::kTupStar ? yt : nullptr);  // t_t = H~^-1 w_t   (t-u-p*: v_t = -t_t)
-  launch_sell(S.C1, GPlain{tt.get()}, EAddTo{xu, tu.get()}, s);  // t_u = w_u + C1 t_t
+  launch_sell(S.C1, GPlain{tt.get()}, EAddToPre{xu, tu.get(), d0, w0, xh.get()}, s);  // t_u = w_u + C1 t_t
   if (L) L->add(S.C1.matrix_bytes() + 8.0 * (nt + 2.0 * nu));
   double* s_u = variant == fpb::kTupStar ? yu : su.get();
-  amg->enqueue_apply(tu.get(), s_u, nullptr, s, L);  // s_u = AMG(S1) t_u
+  amg->enqueue_apply(tu.get(), s_u, nullptr, s, L, xh.get());  // s_u = AMG(S1) t_u
   launch_sell(S.Q2, GPlain{s_u}, ESubFromScaled{xp, ap, tp.get()}, s);  // t_p = w_p - Q2 s_u
   if (L) L->add(S.Q2.matrix_bytes() + 8.0 * (nu + 2.0 * np));
   enqueue_band(tp.get(), 1.0, vp.get(), yp, nullptr, ap, 2, s, L);  // v_p = S~2^-1 t_p
   if (variant == fpb::kTupStar) return;
-  launch_sell(S.Q1, GPlain{vp.get()}, EStore{tu2.get()}, s);  // t_u2 = Q1 v_p
+  launch_sell(S.Q1, GPlain{vp.get()}, EStorePre{tu2.get(), d0, w0, xh.get()}, s);  // t_u2 = Q1 v_p
   if (L) L->add(S.Q1.matrix_bytes() + 8.0 * (np + nu));
-  amg->enqueue_apply(tu2.get(), yu, su.get(), s, L);  // v_u = s_u - AMG(S1) t_u2
+  amg->enqueue_apply(tu2.get(), yu, su.get(), s, L, xh.get());  // v_u = s_u - AMG(S1) t_u2
   hout(yu);                                           // v_t = H~^-1 C2 v_u - t_t
 }
 
@@ -664,7 +716,7 @@ ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int re
   {
     DeviceLevel& C = A.lv.back();
     r.coarse_ms = timed([&] {
-      coarse_solve_kernel<<<1, kCoarseThreads, sizeof(double) * std::max(A.coarse_n, 1), s>>>(
+      coarse_solve_kernel<<<1, kCoarseThreads, coarse_smem_bytes(A.coarse_n), s>>>(
           DenseLUView{A.coarse_n, A.coarse_rank, A.lu.get(), A.prow.get(), A.pcol.get()}, C.b.get(), C.xt.get());
     });
   }

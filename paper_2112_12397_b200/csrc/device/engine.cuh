@@ -63,14 +63,38 @@ class DeviceSystem {
   double bytes_apply() const;
 };
 
+// Plain CSR on the device, consumed one warp per row (csr_warp_kernel).
+struct DCsr {
+  int n_rows = 0, n_cols = 0;
+  int64_t nnz = 0;
+  DevBuf<long long> rp;
+  DevBuf<int> ci;
+  DevBuf<double> v;
+  CsrView view() const { return {n_rows, rp.get(), ci.get(), v.get()}; }
+  double matrix_bytes() const { return 12.0 * double(nnz) + 8.0 * (n_rows + 1); }
+};
+
+// A scalar sparse operator in the layout that streams best for its shape:
+// SELL-32 (thread per row) for many short rows, warp-row CSR for few / long
+// rows (coarse AMG levels, restrictions).  Both sum each row left to right.
+struct DMat {
+  bool warp = false;
+  DSell sell;
+  DCsr csr;
+  int n_rows() const { return warp ? csr.n_rows : sell.n_rows; }
+  int64_t nnz() const { return warp ? csr.nnz : sell.nnz; }
+  double matrix_bytes() const { return warp ? csr.matrix_bytes() : sell.matrix_bytes(); }
+};
+DMat make_mat(const fpb::Csr& A);
+
 struct DeviceLevel {
   bool bsr3 = false;
   DBsr3 Ab;
-  DSell As;
-  DSell P, R;  // P: this level <- next coarser; R = P^T (levels 0..L-2 hold the next level's P/R)
-  DevBuf<double> d, b, x, xt, xt2, r;
+  DMat Am;
+  DMat P, R;  // P: this level <- next coarser; R = P^T (level l+1 holds P_{l+1}, R_{l+1})
+  DevBuf<double> d, b, x, xt, xt2, xt3, r;
   int n = 0;
-  double a_bytes() const { return bsr3 ? Ab.matrix_bytes() : As.matrix_bytes(); }
+  double a_bytes() const { return bsr3 ? Ab.matrix_bytes() : Am.matrix_bytes(); }
 };
 
 class DeviceAmg {
@@ -78,8 +102,11 @@ class DeviceAmg {
   DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3);
   int n_levels() const { return int(lv.size()); }
   int fine_n() const { return lv.empty() ? 0 : lv[0].n; }
-  // x = amg_apply(r) (amg.cpp:293-305); if sub_from != null writes sub_from - x instead
-  void enqueue_apply(const double* r, double* x, const double* sub_from, cudaStream_t s, Ledger* L = nullptr);
+  // x = amg_apply(r) (amg.cpp:293-305); if sub_from != null writes sub_from - x instead.
+  // xhat, if given, already holds the first Jacobi sweep from zero, (omega r_i) / d_i, computed
+  // by the kernel that produced r (it is used as scratch and overwritten).
+  void enqueue_apply(const double* r, double* x, const double* sub_from, cudaStream_t s, Ledger* L = nullptr,
+                     double* xhat = nullptr);
   std::vector<int> level_sizes() const;
   std::vector<DeviceLevel> lv;
   DevBuf<double> lu;
@@ -89,7 +116,7 @@ class DeviceAmg {
   fpb::AmgOptions opt;
 
  private:
-  void vcycle(int l, const double* b, double* x, const double* sub_from, cudaStream_t s, Ledger* L);
+  void vcycle(int l, const double* b, double* x, const double* sub_from, double* xhat, cudaStream_t s, Ledger* L);
 };
 
 class DevicePrecond {
@@ -104,7 +131,7 @@ class DevicePrecond {
   DevBuf<int> band_start, band_piv;
   DevBuf<double> band_Lc, band_diag, band_Lr, band_Uc;
   int band_max_block = 0;
-  DevBuf<double> tt, tu, tp, su, sp_, vp, tu2, vu2;
+  DevBuf<double> tt, tu, tp, su, sp_, vp, tu2, vu2, xh;
   long inner_calls = 0;
   int inner_per_apply() const { return variant == 1 ? 2 : 1; }
   // y = D^-1 M D^-1 x with at = 1/st, ap = 1/sp (at = ap = 1: M itself)

@@ -65,6 +65,31 @@ struct EAddTo {  // y_i = a_i + s   (x += P e_c, amg.cpp:168-169; t_u = w_u + C1
   double* y;
   __device__ __forceinline__ void operator()(int i, double s) const { y[i] = a[i] + s; }
 };
+// Producers of an AMG right-hand side b also emit the first Jacobi sweep from
+// zero, xh = (omega b_i) / d_i (amg.cpp:136-140 with x = 0), so the V-cycle's
+// first residual is a plain SpMV instead of a divide per gathered entry.
+struct EStorePre {  // y_i = s ; xh_i = (w s) / d_i   (restriction r_c = P^T r)
+  double* y;
+  const double* d;
+  double w;
+  double* xh;
+  __device__ __forceinline__ void operator()(int i, double s) const {
+    y[i] = s;
+    xh[i] = (w * s) / d[i];
+  }
+};
+struct EAddToPre {  // y_i = a_i + s ; xh_i = (w y_i) / d_i   (t_u = w_u + C1 t_t)
+  const double* a;
+  double* y;
+  const double* d;
+  double w;
+  double* xh;
+  __device__ __forceinline__ void operator()(int i, double s) const {
+    const double v = a[i] + s;
+    y[i] = v;
+    xh[i] = (w * v) / d[i];
+  }
+};
 struct ESubFromScaled {  // y_i = a_i * sa - s   (t_p = w_p - Q2 s_u with w_p = D^-1 v_p)
   const double* a;
   double sa;
@@ -130,6 +155,42 @@ __global__ void __launch_bounds__(256) sell_kernel(SellView A, G g, E epi) {
   epi(row, sell_row(A, row, g));
 }
 
+// ------------------------------------------------------- warp-row CSR kernel
+// For operators with few, long rows (coarse AMG levels, restrictions R = P^T):
+// one warp per row.  The 32 lanes load 32 consecutive entries (coalesced) and
+// form their products in parallel; the row sum is then accumulated strictly
+// left to right by broadcasting the products lane by lane, so the result is
+// the reference's sequential CSR sum bit for bit (csr.cpp:112-117) while the
+// loads for the next chunk are already in flight.
+constexpr int kWarpRowThreads = 256;
+
+template <class G, class E>
+__global__ void __launch_bounds__(kWarpRowThreads) csr_warp_kernel(CsrView A, G g, E epi) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= A.n_rows) return;  // warp-uniform
+  const long long b = A.rp[row], e = A.rp[row + 1];
+  double s = 0.0;
+  long long k = b + lane;
+  double p = 0.0;
+  if (k < e) p = __ldg(A.v + k) * g(__ldg(A.ci + k));
+  for (long long base = b; base < e; base += 32) {
+    // prefetch the next chunk's product while this chunk is summed
+    const long long kn = k + 32;
+    double pn = 0.0;
+    if (kn < e) pn = __ldg(A.v + kn) * g(__ldg(A.ci + kn));
+    const int cnt = e - base < 32 ? int(e - base) : 32;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+      const double pj = __shfl_sync(0xffffffffu, p, j);
+      if (j < cnt) s = s + pj;
+    }
+    p = pn;
+    k = kn;
+  }
+  if (lane == 0) epi(row, s);
+}
+
 // ------------------------------------------------------------- BSR3 kernel
 // 96 threads per slice: warp li (0..2) computes scalar row 3*brow+li of the 32
 // block rows of the slice.  Sum order = block columns ascending, then j = 0,1,2:
@@ -192,12 +253,15 @@ __global__ void __launch_bounds__(256) jtp_kernel(SellView C2, SellView H, SellV
 
 // t_u = (w_u + C1 t_t) - Q1 t_p   (precond.cpp:159, t-p-u)
 __global__ void __launch_bounds__(256) tpu_tu_kernel(SellView C1, SellView Q1, const double* wu, const double* tt,
-                                                     const double* tp, double* tu) {
+                                                     const double* tp, double* tu, const double* d, double w,
+                                                     double* xh) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= C1.n_rows) return;
   const double b = sell_row(C1, i, GPlain{tt});
   const double c = sell_row(Q1, i, GPlain{tp});
-  tu[i] = (wu[i] + b) - c;
+  const double v = (wu[i] + b) - c;
+  tu[i] = v;
+  xh[i] = (w * v) / d[i];
 }
 
 // --------------------------------------------------------- 3x3 block solves
@@ -254,7 +318,120 @@ __global__ void __launch_bounds__(256) hsolve_out_kernel(int n_faces, SellView C
 // right-hand side lives in shared memory; each step finalizes one unknown and
 // the warp applies its column of L (forward) or U / L^T (backward) to the
 // following rows in parallel — the column-sweep order of the oracle.
+// The columns of L / U needed D steps ahead are prefetched into a register ring
+// (lane l holds entries l, l+32, ... of a column), so a step costs one shared-
+// memory round trip instead of a global-memory latency.
 // Modes: out_mode 0: out = x;  1: out = (sub - x) * os;  2: out = x, out2 = x * os.
+constexpr int kBandPrefetch = 32;  // prefetch distance x chunks-per-lane
+
+// Forward sweep with (optional) partial-pivot row swaps: for j ascending,
+// y_j = x[piv_j] (swapped with x_j), then x_i -= L(i,j) y_j for i in (j, j+kl].
+template <int Q, bool PIV>
+__device__ __forceinline__ void band_forward(double* xs, int nb, int b0, int kl, const double* __restrict__ Lc,
+                                             const int* __restrict__ piv, int lane) {
+  constexpr int D = kBandPrefetch / Q < 4 ? 4 : kBandPrefetch / Q;
+  double ring[D][Q];
+  int pring[D];
+#pragma unroll
+  for (int u = 0; u < D; ++u) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int r = lane + 32 * q;
+      ring[u][q] = (u < nb && r < kl) ? __ldg(Lc + size_t(b0 + u) * kl + r) : 0.0;
+    }
+    pring[u] = (PIV && u < nb) ? __ldg(piv + b0 + u) - b0 : u;
+  }
+  for (int j0 = 0; j0 < nb; j0 += D) {
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      const int j = j0 + u;
+      if (j < nb) {
+        const double a = xs[j];
+        const int p = pring[u];
+        const double yj = PIV ? xs[p] : a;
+        if (PIV) __syncwarp();  // every lane has read x_p before its owner overwrites it
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int r = lane + 32 * q, i = j + 1 + r;
+          if (r < kl && i < nb) {
+            const double cur = (PIV && i == p) ? a : xs[i];
+            xs[i] = cur - ring[u][q] * yj;
+          }
+        }
+        __syncwarp();
+        if (PIV && lane == 0) xs[j] = yj;  // row j is never read again in this sweep
+        const int jn = j + D;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int r = lane + 32 * q;
+          ring[u][q] = (jn < nb && r < kl) ? __ldg(Lc + size_t(b0 + jn) * kl + r) : 0.0;
+        }
+        pring[u] = (PIV && jn < nb) ? __ldg(piv + b0 + jn) - b0 : jn;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// Backward sweep: for j descending, x_j = x_j / diag_j (DIV) then
+// x_i -= C(j, r) x_j for i = j-1-r, r < kb (C = U columns, or rows of L for L^T).
+template <int Q, bool DIV>
+__device__ __forceinline__ void band_backward(double* xs, int nb, int b0, int kb, const double* __restrict__ C,
+                                              const double* __restrict__ diag, int lane) {
+  constexpr int D = kBandPrefetch / Q < 4 ? 4 : kBandPrefetch / Q;
+  double ring[D][Q];
+  double dring[D];
+#pragma unroll
+  for (int u = 0; u < D; ++u) {
+    const int j = nb - 1 - u;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int r = lane + 32 * q;
+      ring[u][q] = (j >= 0 && r < kb) ? __ldg(C + size_t(b0 + j) * kb + r) : 0.0;
+    }
+    dring[u] = (DIV && j >= 0) ? __ldg(diag + b0 + j) : 1.0;
+  }
+  for (int j0 = nb - 1; j0 >= 0; j0 -= D) {
+#pragma unroll
+    for (int u = 0; u < D; ++u) {
+      const int j = j0 - u;
+      if (j >= 0) {
+        const double xj = DIV ? xs[j] / dring[u] : xs[j];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int r = lane + 32 * q, i = j - 1 - r;
+          if (r < kb && i >= 0) xs[i] -= ring[u][q] * xj;
+        }
+        __syncwarp();
+        if (DIV && lane == 0) xs[j] = xj;  // row j is never read again in this sweep
+        const int jn = j - D;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int r = lane + 32 * q;
+          ring[u][q] = (jn >= 0 && r < kb) ? __ldg(C + size_t(b0 + jn) * kb + r) : 0.0;
+        }
+        dring[u] = (DIV && jn >= 0) ? __ldg(diag + b0 + jn) : 1.0;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+template <int Q>
+__device__ __forceinline__ void band_forward_any(double* xs, int nb, int b0, const BandView& F, int lane) {
+  if (F.spd)
+    band_forward<Q, false>(xs, nb, b0, F.kl, F.Lc, F.piv, lane);
+  else
+    band_forward<Q, true>(xs, nb, b0, F.kl, F.Lc, F.piv, lane);
+}
+template <int Q>
+__device__ __forceinline__ void band_backward_any(double* xs, int nb, int b0, const BandView& F, int lane) {
+  if (F.spd)
+    band_backward<Q, false>(xs, nb, b0, F.kl, F.Lr, F.diag, lane);
+  else
+    band_backward<Q, true>(xs, nb, b0, F.ku, F.Uc, F.diag, lane);
+}
+
 __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double* rhs, double rs, double* out,
                                                         double* out2, const double* sub, double os, int out_mode) {
   extern __shared__ double xs[];
@@ -262,43 +439,28 @@ __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double
   const int b0 = F.block_start[blk], b1 = F.block_start[blk + 1], nb = b1 - b0;
   for (int i = lane; i < nb; i += 32) xs[i] = rhs[b0 + i] * rs;
   __syncwarp();
-  const int kl = F.kl;
-  for (int j = 0; j < nb; ++j) {
-    const int gj = b0 + j;
-    if (!F.spd) {
-      const int p = F.piv[gj] - b0;
-      if (p != j && lane == 0) {
-        const double t = xs[j];
-        xs[j] = xs[p];
-        xs[p] = t;
-      }
-      __syncwarp();
-    }
-    const double yj = xs[j];
-    const double* Lj = F.Lc + size_t(gj) * kl;
-    for (int r = lane; r < kl && j + 1 + r < nb; r += 32) xs[j + 1 + r] -= Lj[r] * yj;
-    __syncwarp();
-  }
+  const int qf = (F.kl + 31) / 32;
+  if (qf <= 1)
+    band_forward_any<1>(xs, nb, b0, F, lane);
+  else if (qf <= 2)
+    band_forward_any<2>(xs, nb, b0, F, lane);
+  else if (qf <= 4)
+    band_forward_any<4>(xs, nb, b0, F, lane);
+  else
+    band_forward_any<8>(xs, nb, b0, F, lane);
   if (F.spd) {
     for (int i = lane; i < nb; i += 32) xs[i] = xs[i] / F.diag[b0 + i];
     __syncwarp();
-    for (int j = nb - 1; j >= 0; --j) {
-      const double xj = xs[j];
-      const double* Lj = F.Lr + size_t(b0 + j) * kl;
-      for (int r = lane; r < kl && j - 1 - r >= 0; r += 32) xs[j - 1 - r] -= Lj[r] * xj;
-      __syncwarp();
-    }
-  } else {
-    const int ku = F.ku;
-    for (int j = nb - 1; j >= 0; --j) {
-      const double xj = xs[j] / F.diag[b0 + j];
-      __syncwarp();
-      if (lane == 0) xs[j] = xj;
-      const double* Uj = F.Uc + size_t(b0 + j) * ku;
-      for (int r = lane; r < ku && j - 1 - r >= 0; r += 32) xs[j - 1 - r] -= Uj[r] * xj;
-      __syncwarp();
-    }
   }
+  const int qb = ((F.spd ? F.kl : F.ku) + 31) / 32;
+  if (qb <= 1)
+    band_backward_any<1>(xs, nb, b0, F, lane);
+  else if (qb <= 2)
+    band_backward_any<2>(xs, nb, b0, F, lane);
+  else if (qb <= 4)
+    band_backward_any<4>(xs, nb, b0, F, lane);
+  else
+    band_backward_any<8>(xs, nb, b0, F, lane);
   for (int i = lane; i < nb; i += 32) {
     const double x = xs[i];
     if (out_mode == 1)
@@ -313,26 +475,38 @@ __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double
 // x = Q U^-1 L^-1 P b on the full-pivot LU (restated FullPivLU::solve), one CTA,
 // column sweeps.  LU is column-major so each step reads one contiguous column.
 constexpr int kCoarseThreads = 256;
+// When the factor fits (n <= kCoarseSmemN) it is staged in shared memory first,
+// so the 2n dependent steps cost shared-memory latency, not L2/HBM latency.
+constexpr int kCoarseSmemN = 160;
 __global__ void __launch_bounds__(kCoarseThreads) coarse_solve_kernel(DenseLUView F, const double* b, double* x) {
   extern __shared__ double c[];
   const int n = F.n, tid = threadIdx.x;
+  const double* lu = F.lu;
+  if (n <= kCoarseSmemN) {
+    double* s_lu = c + n;
+    for (int i = tid; i < n * n; i += blockDim.x) s_lu[i] = F.lu[i];
+    lu = s_lu;
+  }
   for (int i = tid; i < n; i += blockDim.x) c[i] = b[F.prow[i]];
   __syncthreads();
   for (int j = 0; j < n; ++j) {
     const double cj = c[j];
-    const double* col = F.lu + size_t(j) * n;
+    const double* col = lu + size_t(j) * n;
     for (int i = j + 1 + tid; i < n; i += blockDim.x) c[i] -= col[i] * cj;
     __syncthreads();
   }
   for (int j = F.rank - 1; j >= 0; --j) {
-    const double xj = c[j] / F.lu[size_t(j) * n + j];
+    const double xj = c[j] / lu[size_t(j) * n + j];
     __syncthreads();
     if (tid == 0) c[j] = xj;
-    const double* col = F.lu + size_t(j) * n;
+    const double* col = lu + size_t(j) * n;
     for (int i = tid; i < j; i += blockDim.x) c[i] -= col[i] * xj;
     __syncthreads();
   }
   for (int i = tid; i < n; i += blockDim.x) x[F.pcol[i]] = i < F.rank ? c[i] : 0.0;
+}
+inline size_t coarse_smem_bytes(int n) {
+  return sizeof(double) * (size_t(n > 0 ? n : 1) + (n <= kCoarseSmemN ? size_t(n) * n : 0));
 }
 
 // ---------------------------------------------------------- elementwise
