@@ -195,3 +195,92 @@ def test_gmres_unscaled_and_zero_rhs():
         assert rel(x, x_ref) <= 1e-8
     x0, st0 = api.gmres(op, pc, np.zeros(J.total_dimension()), tol=1e-10)
     assert st0.converged and st0.iterations == 0 and np.all(x0 == 0)
+
+
+def _grid_laplacian_blocks(nbs, shift_every=0, shift=0.0):
+    """Block-diagonal 5-point operators, one nb x nb grid per 'fracture' (natural order)."""
+    trips, off = [], 0
+    for nb in nbs:
+        for j in range(nb):
+            for i in range(nb):
+                r = off + i + nb * j
+                d = 4.3 + (shift if shift_every and r % shift_every == 0 else 0.0)
+                trips.append((r, r, d))
+                if i + 1 < nb:
+                    trips += [(r, r + 1, -1.0), (r + 1, r, -1.0)]
+                if j + 1 < nb:
+                    trips += [(r, r + nb, -1.0), (r + nb, r, -1.0)]
+        off += nb * nb
+    trips.sort()
+    n = off
+    rp = np.zeros(n + 1, np.int64)
+    for r, _, _ in trips:
+        rp[r + 1] += 1
+    return api.CsrMatrix(n, n, np.cumsum(rp), np.array([c for _, c, _ in trips], np.int32),
+                         np.array([v for _, _, v in trips]))
+
+
+def _decoupled_with_T(T):
+    n_p = T.n_rows
+    n_u = 24
+    osys = O.OracleSystem.toy(n_u, 1, "decoupled", 1)
+    b = [csr_of(t) for t in osys.blocks()]
+    Z = api.CsrMatrix.empty
+    ht = [(3 * f + c, 3 * f + c, 1.0 + 0.2 * c) for f in range(n_p) for c in range(3)]
+    H = api.CsrMatrix(3 * n_p, 3 * n_p, np.arange(3 * n_p + 1), np.array([c for _, c, _ in ht], np.int32),
+                      np.array([v for _, _, v in ht]))
+    J = api.BlockSystem(n_u, 3 * n_p, n_p, b[0], Z(n_u, 3 * n_p), Z(n_u, n_p), Z(3 * n_p, n_u), H, Z(n_p, n_u), T,
+                        F_u=Z(n_p, n_u))
+    blocks = [(m.n_rows, m.n_cols, m.row_offsets, m.col_indices, m.values)
+              for m in (J.A, J.C1, J.Q1, J.C2, J.H, J.Q2, J.T, J.F_u)]
+    return J, O.OracleSystem.from_blocks(J.n_u, J.n_t, J.n_p, blocks)
+
+
+@pytest.mark.parametrize("variant,shift", [("tpu", 0.0), ("tup", 0.0), ("tup", -8.0)])
+def test_banded_factor_solves_match_oracle(variant, shift):
+    """T / S~2 solves over several independent fracture blocks with bandwidths 7..40;
+    shift -8 makes S~2 indefinite so the LU takes row pivots (banded solve with swaps)."""
+    T = _grid_laplacian_blocks([7, 12, 40, 3], shift_every=3 if shift else 0, shift=shift)
+    J, osys = _decoupled_with_T(T)
+    amg = api.AmgConfig(max_coarse=8)
+    opc = O.OraclePrecond(osys, variant, **amg_kw(amg))
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, variant, amg)
+    x = np.random.default_rng(8).uniform(-1, 1, J.total_dimension())
+    y, ref = pc.apply(x), opc.apply(x)
+    assert np.array_equal(y, ref), rel(y, ref)
+
+
+@pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
+def test_theta0_hierarchy_apply_bitwise(variant):
+    """The bench's AMG setting (strength_threshold 0): wide coarse rows take the warp-row kernel."""
+    J = small_workload(seed=31, cells=(12, 12, 10))
+    osys = oracle_system(J)
+    amg = api.AmgConfig(strength_threshold=0.0)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, **amg_kw(amg))
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, variant, amg)
+    x = np.random.default_rng(12).uniform(-1, 1, J.total_dimension())
+    assert np.array_equal(pc.apply(x), opc.apply(x))
+    pc2 = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, api.PrecondConfig(variant, amg=amg)))
+    assert np.array_equal(pc2.apply(x), opc.apply(x))
+
+
+def test_theta0_gmres_matches_oracle_and_history():
+    J = small_workload(seed=37, cells=(12, 12, 12))
+    osys = oracle_system(J)
+    amg = api.AmgConfig(strength_threshold=0.0)
+    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, **amg_kw(amg))
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, "tup", amg)
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=50, max_iter=500, scaled=True)
+    x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=500, restart=50, scaled=True)
+    assert st.converged == st_ref["converged"]
+    assert abs(st.iterations - st_ref["iterations"]) <= 2
+    if st_ref["converged"]:
+        assert rel(x, x_ref) <= 1e-8
+    # residual histories agree (the criterion when both stop at max_iter, SURVEY §8(d))
+    k = min(len(st.relative_residuals), len(st_ref["history"])) - 1
+    h, hr = np.array(st.relative_residuals[:k]), st_ref["history"][:k]
+    assert np.all(np.abs(np.log10(h) - np.log10(hr)) < 0.5)
