@@ -52,9 +52,8 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s) {
     return;
   }
   if (A.csr.n_rows == 0) return;
-  csr_warp_kernel<<<blocks_for((long long)A.csr.n_rows * 32, kWarpRowThreads), kWarpRowThreads, 0, s>>>(A.csr.view(),
-                                                                                                         g, e);
-  cuda_check(cudaGetLastError(), "csr_warp_kernel launch");
+  csr_slice_kernel<<<blocks_for(A.csr.n_rows, 32), 256, 0, s>>>(A.csr.view(), g, e);
+  cuda_check(cudaGetLastError(), "csr_slice_kernel launch");
 }
 
 template <class G, class E>
@@ -272,7 +271,7 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   const double nd = L.n;
   if (l == last) {
     double* out = sub_from ? L.xt.get() : x;
-    coarse_solve_kernel<<<1, kCoarseThreads, coarse_smem_bytes(coarse_n), s>>>(
+    coarse_solve_kernel<<<1, coarse_threads(coarse_n), coarse_smem_bytes(coarse_n), s>>>(
         DenseLUView{coarse_n, coarse_rank, lu.get(), prow.get(), pcol.get()}, b, out);
     cuda_check(cudaGetLastError(), "coarse_solve_kernel launch");
     if (Lg) Lg->add(8.0 * coarse_n * double(coarse_n) + 16.0 * coarse_n + 8.0 * coarse_n);
@@ -716,7 +715,7 @@ ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int re
   {
     DeviceLevel& C = A.lv.back();
     r.coarse_ms = timed([&] {
-      coarse_solve_kernel<<<1, kCoarseThreads, coarse_smem_bytes(A.coarse_n), s>>>(
+      coarse_solve_kernel<<<1, coarse_threads(A.coarse_n), coarse_smem_bytes(A.coarse_n), s>>>(
           DenseLUView{A.coarse_n, A.coarse_rank, A.lu.get(), A.prow.get(), A.pcol.get()}, C.b.get(), C.xt.get());
     });
   }

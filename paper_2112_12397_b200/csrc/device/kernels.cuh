@@ -164,6 +164,47 @@ __global__ void __launch_bounds__(256) sell_kernel(SellView A, G g, E epi) {
 // loads for the next chunk are already in flight.
 constexpr int kWarpRowThreads = 256;
 
+// Slice kernel for few / long rows: one CTA per 32 consecutive rows.  In each
+// window of kSliceWin entries per row, the 8 warps load their rows' entries
+// (contiguous in CSR, so coalesced) and store the products a_ik x_k to shared
+// memory; then lane r of warp 0 adds row r's window strictly left to right.
+// The ordered sum costs two instructions per 32 entries (one per lane) instead
+// of per entry, and the loads of a window are all in flight together.
+constexpr int kSliceWin = 64;
+template <class G, class E>
+__global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
+  __shared__ double prod[2][32][kSliceWin + 1];
+  __shared__ long long rb[33];
+  const int row0 = blockIdx.x * 32;
+  const int nrows = A.n_rows - row0 < 32 ? A.n_rows - row0 : 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x <= nrows) rb[threadIdx.x] = A.rp[row0 + threadIdx.x];
+  __syncthreads();
+  long long maxlen = 0;
+  for (int r = 0; r < nrows; ++r) maxlen = max(maxlen, rb[r + 1] - rb[r]);
+  double s = 0.0;
+  int buf = 0;
+  for (long long w0 = 0; w0 < maxlen; w0 += kSliceWin) {
+    // produce: warp w handles rows w, w+8, w+16, w+24
+    for (int r = warp; r < nrows; r += 8) {
+      const long long b = rb[r] + w0, e = rb[r + 1];
+#pragma unroll
+      for (int h = 0; h < kSliceWin / 32; ++h) {
+        const long long k = b + lane + 32 * h;
+        prod[buf][r][lane + 32 * h] = k < e ? __ldg(A.v + k) * g(__ldg(A.ci + k)) : 0.0;
+      }
+    }
+    __syncthreads();
+    if (warp == 0 && lane < nrows) {
+      const long long len = rb[lane + 1] - rb[lane] - w0;
+      const int cnt = len < kSliceWin ? int(len) : kSliceWin;
+      for (int k = 0; k < cnt; ++k) s = s + prod[buf][lane][k];
+    }
+    buf ^= 1;  // the next window fills the other buffer while warp 0 sums this one
+  }
+  if (warp == 0 && lane < nrows) epi(row0 + lane, s);
+}
+
 template <class G, class E>
 __global__ void __launch_bounds__(kWarpRowThreads) csr_warp_kernel(CsrView A, G g, E epi) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -504,6 +545,10 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_solve_kernel(DenseLUVie
     __syncthreads();
   }
   for (int i = tid; i < n; i += blockDim.x) x[F.pcol[i]] = i < F.rank ? c[i] : 0.0;
+}
+inline int coarse_threads(int n) {  // small coarse systems: fewer threads, cheaper barriers
+  const int t = (n + 31) / 32 * 32;
+  return t < 32 ? 32 : (t > kCoarseThreads ? kCoarseThreads : t);
 }
 inline size_t coarse_smem_bytes(int n) {
   return sizeof(double) * (size_t(n > 0 ? n : 1) + (n <= kCoarseSmemN ? size_t(n) * n : 0));
