@@ -52,7 +52,19 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s) {
     return;
   }
   if (A.csr.n_rows == 0) return;
-  csr_slice_kernel<<<blocks_for(A.csr.n_rows, 32), 256, 0, s>>>(A.csr.view(), g, e);
+  if (A.slice_rows == 32) {
+    constexpr size_t smem = slice_smem_bytes<32, 64>();
+    static const bool attr = (cudaFuncSetAttribute(csr_slice_kernel<32, 64, G, E>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), true);
+    (void)attr;
+    csr_slice_kernel<32, 64><<<blocks_for(A.csr.n_rows, 32), 256, smem, s>>>(A.csr.view(), g, e);
+  } else {
+    constexpr size_t smem = slice_smem_bytes<8, 512>();
+    static const bool attr = (cudaFuncSetAttribute(csr_slice_kernel<8, 512, G, E>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), true);
+    (void)attr;
+    csr_slice_kernel<8, 512><<<blocks_for(A.csr.n_rows, 8), 256, smem, s>>>(A.csr.view(), g, e);
+  }
   cuda_check(cudaGetLastError(), "csr_slice_kernel launch");
 }
 
@@ -76,6 +88,7 @@ DMat make_mat(const fpb::Csr& A) {
     M.sell = make_sell(A);
     return M;
   }
+  M.slice_rows = A.n_rows >= 2048 ? 32 : 8;
   M.csr.n_rows = A.n_rows, M.csr.n_cols = A.n_cols, M.csr.nnz = A.nnz();
   std::vector<long long> rp(A.rp.begin(), A.rp.end());
   M.csr.rp.upload(rp);

@@ -79,6 +79,7 @@ struct DCsr {
 // rows (coarse AMG levels, restrictions).  Both sum each row left to right.
 struct DMat {
   bool warp = false;
+  int slice_rows = 32;  // rows per CTA of the slice kernel (8 for few-row operators)
   DSell sell;
   DCsr csr;
   int n_rows() const { return warp ? csr.n_rows : sell.n_rows; }

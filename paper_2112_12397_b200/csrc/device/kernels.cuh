@@ -170,13 +170,19 @@ constexpr int kWarpRowThreads = 256;
 // memory; then lane r of warp 0 adds row r's window strictly left to right.
 // The ordered sum costs two instructions per 32 entries (one per lane) instead
 // of per entry, and the loads of a window are all in flight together.
-constexpr int kSliceWin = 64;
-template <class G, class E>
+// Geometry: R rows per CTA, windows of W entries per row (dynamic shared memory
+// 2 R (W+1) doubles).  Many rows: R = 32, W = 64; few long rows: R = 8, W = 512
+// so that each CTA keeps 16 loads per lane in flight.
+template <int R, int W>
+constexpr size_t slice_smem_bytes() {
+  return sizeof(double) * 2 * R * (W + 1);
+}
+template <int R, int W, class G, class E>
 __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
-  __shared__ double prod[2][32][kSliceWin + 1];
-  __shared__ long long rb[33];
-  const int row0 = blockIdx.x * 32;
-  const int nrows = A.n_rows - row0 < 32 ? A.n_rows - row0 : 32;
+  extern __shared__ double prod[];  // [2][R][W + 1]
+  __shared__ long long rb[R + 1];
+  const int row0 = blockIdx.x * R;
+  const int nrows = A.n_rows - row0 < R ? A.n_rows - row0 : R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x <= nrows) rb[threadIdx.x] = A.rp[row0 + threadIdx.x];
   __syncthreads();
@@ -184,21 +190,23 @@ __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
   for (int r = 0; r < nrows; ++r) maxlen = max(maxlen, rb[r + 1] - rb[r]);
   double s = 0.0;
   int buf = 0;
-  for (long long w0 = 0; w0 < maxlen; w0 += kSliceWin) {
-    // produce: warp w handles rows w, w+8, w+16, w+24
+  for (long long w0 = 0; w0 < maxlen; w0 += W) {
+    // produce: warp w handles rows w, w+8, ...
     for (int r = warp; r < nrows; r += 8) {
       const long long b = rb[r] + w0, e = rb[r + 1];
+      double* dst = prod + (size_t(buf) * R + r) * (W + 1);
 #pragma unroll
-      for (int h = 0; h < kSliceWin / 32; ++h) {
+      for (int h = 0; h < W / 32; ++h) {
         const long long k = b + lane + 32 * h;
-        prod[buf][r][lane + 32 * h] = k < e ? __ldg(A.v + k) * g(__ldg(A.ci + k)) : 0.0;
+        dst[lane + 32 * h] = k < e ? __ldg(A.v + k) * g(__ldg(A.ci + k)) : 0.0;
       }
     }
     __syncthreads();
     if (warp == 0 && lane < nrows) {
       const long long len = rb[lane + 1] - rb[lane] - w0;
-      const int cnt = len < kSliceWin ? int(len) : kSliceWin;
-      for (int k = 0; k < cnt; ++k) s = s + prod[buf][lane][k];
+      const int cnt = len < W ? int(len) : W;
+      const double* src = prod + (size_t(buf) * R + lane) * (W + 1);
+      for (int k = 0; k < cnt; ++k) s = s + src[k];
     }
     buf ^= 1;  // the next window fills the other buffer while warp 0 sums this one
   }
@@ -363,7 +371,19 @@ __global__ void __launch_bounds__(256) hsolve_out_kernel(int n_faces, SellView C
 // (lane l holds entries l, l+32, ... of a column), so a step costs one shared-
 // memory round trip instead of a global-memory latency.
 // Modes: out_mode 0: out = x;  1: out = (sub - x) * os;  2: out = x, out2 = x * os.
-constexpr int kBandPrefetch = 32;  // prefetch distance x chunks-per-lane
+constexpr int kBandPrefetch = 32;  // prefetch distance x chunks-per-lane (32 ring doubles per lane)
+
+// Bulk prefetch of [p, p + bytes) into L2 (sm_90+ TMA-engine prefetch), so the
+// register ring below streams the block's factor from L2, not HBM.
+__device__ __forceinline__ void l2_prefetch_range(const void* p, size_t bytes) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~uintptr_t(15);
+  while (a < e) {
+    const uint32_t chunk = uint32_t((e - a) > (1u << 20) ? (1u << 20) : (e - a));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(chunk) : "memory");
+    a += chunk;
+  }
+}
 
 // Forward sweep with (optional) partial-pivot row swaps: for j ascending,
 // y_j = x[piv_j] (swapped with x_j), then x_i -= L(i,j) y_j for i in (j, j+kl].
@@ -478,6 +498,16 @@ __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double
   extern __shared__ double xs[];
   const int blk = blockIdx.x, lane = threadIdx.x;
   const int b0 = F.block_start[blk], b1 = F.block_start[blk + 1], nb = b1 - b0;
+  if (lane == 0) {
+    l2_prefetch_range(F.Lc + size_t(b0) * F.kl, sizeof(double) * size_t(nb) * F.kl);
+    if (F.spd)
+      l2_prefetch_range(F.Lr + size_t(b0) * F.kl, sizeof(double) * size_t(nb) * F.kl);
+    else {
+      l2_prefetch_range(F.Uc + size_t(b0) * F.ku, sizeof(double) * size_t(nb) * F.ku);
+      l2_prefetch_range(F.piv + b0, sizeof(int) * size_t(nb));
+    }
+    l2_prefetch_range(F.diag + b0, sizeof(double) * size_t(nb));
+  }
   for (int i = lane; i < nb; i += 32) xs[i] = rhs[b0 + i] * rs;
   __syncwarp();
   const int qf = (F.kl + 31) / 32;
@@ -485,6 +515,8 @@ __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double
     band_forward_any<1>(xs, nb, b0, F, lane);
   else if (qf <= 2)
     band_forward_any<2>(xs, nb, b0, F, lane);
+  else if (qf <= 3)
+    band_forward_any<3>(xs, nb, b0, F, lane);
   else if (qf <= 4)
     band_forward_any<4>(xs, nb, b0, F, lane);
   else
@@ -498,6 +530,8 @@ __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double
     band_backward_any<1>(xs, nb, b0, F, lane);
   else if (qb <= 2)
     band_backward_any<2>(xs, nb, b0, F, lane);
+  else if (qb <= 3)
+    band_backward_any<3>(xs, nb, b0, F, lane);
   else if (qb <= 4)
     band_backward_any<4>(xs, nb, b0, F, lane);
   else
