@@ -179,7 +179,7 @@ constexpr size_t slice_smem_bytes() {
 }
 template <int R, int W, class G, class E>
 __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
-  extern __shared__ double prod[];  // [2][R][W + 1]
+  __shared__ double prod[2 * R * (W + 1)];  // [2][R][W + 1]
   __shared__ long long rb[R + 1];
   const int row0 = blockIdx.x * R;
   const int nrows = A.n_rows - row0 < R ? A.n_rows - row0 : R;
@@ -371,7 +371,6 @@ __global__ void __launch_bounds__(256) hsolve_out_kernel(int n_faces, SellView C
 // (lane l holds entries l, l+32, ... of a column), so a step costs one shared-
 // memory round trip instead of a global-memory latency.
 // Modes: out_mode 0: out = x;  1: out = (sub - x) * os;  2: out = x, out2 = x * os.
-constexpr int kBandPrefetch = 32;  // prefetch distance x chunks-per-lane (32 ring doubles per lane)
 
 // Bulk prefetch of [p, p + bytes) into L2 (sm_90+ TMA-engine prefetch), so the
 // register ring below streams the block's factor from L2, not HBM.
@@ -385,30 +384,55 @@ __device__ __forceinline__ void l2_prefetch_range(const void* p, size_t bytes) {
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Prefetch ring: cp.async copies the factor column for step j + D into a
+// per-lane shared-memory slot while step j computes (async groups, not register
+// scoreboards, track completion; each lane reads back only what it copied).
+constexpr int kBandDepth = 16;
+__host__ __device__ constexpr int band_ring_doubles(int q) { return kBandDepth * 32 * (q + 1); }
+
 // Forward sweep with (optional) partial-pivot row swaps: for j ascending,
 // y_j = x[piv_j] (swapped with x_j), then x_i -= L(i,j) y_j for i in (j, j+kl].
 template <int Q, bool PIV>
-__device__ __forceinline__ void band_forward(double* xs, int nb, int b0, int kl, const double* __restrict__ Lc,
-                                             const int* __restrict__ piv, int lane) {
-  constexpr int D = kBandPrefetch / Q < 4 ? 4 : kBandPrefetch / Q;
-  double ring[D][Q];
-  int pring[D];
+__device__ __forceinline__ void band_forward(double* xs, double* ring, int nb, int b0, int kl,
+                                             const double* __restrict__ Lc, const int* __restrict__ piv, int lane) {
+  constexpr int D = kBandDepth;
+  double* R = ring + lane;                                           // slot (u,q): R[(u*Q+q)*32]
+  int* PR = reinterpret_cast<int*>(ring + D * Q * 32) + lane;        // slot u: PR[u*32]
+  auto issue = [&](int u, int jj) {
+    if (jj < nb) {
 #pragma unroll
-  for (int u = 0; u < D; ++u) {
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int r = lane + 32 * q;
-      ring[u][q] = (u < nb && r < kl) ? __ldg(Lc + size_t(b0 + u) * kl + r) : 0.0;
+      for (int q = 0; q < Q; ++q) {
+        const int r = lane + 32 * q;
+        if (r < kl) cp_async8(R + (u * Q + q) * 32, Lc + size_t(b0 + jj) * kl + r);
+      }
+      if (PIV) cp_async4(PR + u * 32, piv + b0 + jj);
     }
-    pring[u] = (PIV && u < nb) ? __ldg(piv + b0 + u) - b0 : u;
-  }
+    cp_commit();
+  };
+#pragma unroll
+  for (int u = 0; u < D; ++u) issue(u, u);
   for (int j0 = 0; j0 < nb; j0 += D) {
 #pragma unroll
     for (int u = 0; u < D; ++u) {
       const int j = j0 + u;
       if (j < nb) {
+        cp_wait<D - 1>();
         const double a = xs[j];
-        const int p = pring[u];
+        const int p = PIV ? PR[u * 32] - b0 : j;
         const double yj = PIV ? xs[p] : a;
         if (PIV) __syncwarp();  // every lane has read x_p before its owner overwrites it
 #pragma unroll
@@ -416,86 +440,85 @@ __device__ __forceinline__ void band_forward(double* xs, int nb, int b0, int kl,
           const int r = lane + 32 * q, i = j + 1 + r;
           if (r < kl && i < nb) {
             const double cur = (PIV && i == p) ? a : xs[i];
-            xs[i] = cur - ring[u][q] * yj;
+            xs[i] = cur - R[(u * Q + q) * 32] * yj;
           }
         }
         __syncwarp();
         if (PIV && lane == 0) xs[j] = yj;  // row j is never read again in this sweep
-        const int jn = j + D;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const int r = lane + 32 * q;
-          ring[u][q] = (jn < nb && r < kl) ? __ldg(Lc + size_t(b0 + jn) * kl + r) : 0.0;
-        }
-        pring[u] = (PIV && jn < nb) ? __ldg(piv + b0 + jn) - b0 : jn;
+        issue(u, j + D);
       }
     }
   }
+  cp_wait<0>();
   __syncwarp();
 }
 
 // Backward sweep: for j descending, x_j = x_j / diag_j (DIV) then
 // x_i -= C(j, r) x_j for i = j-1-r, r < kb (C = U columns, or rows of L for L^T).
 template <int Q, bool DIV>
-__device__ __forceinline__ void band_backward(double* xs, int nb, int b0, int kb, const double* __restrict__ C,
-                                              const double* __restrict__ diag, int lane) {
-  constexpr int D = kBandPrefetch / Q < 4 ? 4 : kBandPrefetch / Q;
-  double ring[D][Q];
-  double dring[D];
+__device__ __forceinline__ void band_backward(double* xs, double* ring, int nb, int b0, int kb,
+                                              const double* __restrict__ C, const double* __restrict__ diag,
+                                              int lane) {
+  constexpr int D = kBandDepth;
+  double* R = ring + lane;
+  double* DR = ring + D * Q * 32 + lane;  // slot u: DR[u*32]
+  auto issue = [&](int u, int j) {
+    if (j >= 0) {
 #pragma unroll
-  for (int u = 0; u < D; ++u) {
-    const int j = nb - 1 - u;
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const int r = lane + 32 * q;
-      ring[u][q] = (j >= 0 && r < kb) ? __ldg(C + size_t(b0 + j) * kb + r) : 0.0;
+      for (int q = 0; q < Q; ++q) {
+        const int r = lane + 32 * q;
+        if (r < kb) cp_async8(R + (u * Q + q) * 32, C + size_t(b0 + j) * kb + r);
+      }
+      if (DIV) cp_async8(DR + u * 32, diag + b0 + j);
     }
-    dring[u] = (DIV && j >= 0) ? __ldg(diag + b0 + j) : 1.0;
-  }
+    cp_commit();
+  };
+#pragma unroll
+  for (int u = 0; u < D; ++u) issue(u, nb - 1 - u);
   for (int j0 = nb - 1; j0 >= 0; j0 -= D) {
 #pragma unroll
     for (int u = 0; u < D; ++u) {
       const int j = j0 - u;
       if (j >= 0) {
-        const double xj = DIV ? xs[j] / dring[u] : xs[j];
+        cp_wait<D - 1>();
+        const double xj = DIV ? xs[j] / DR[u * 32] : xs[j];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           const int r = lane + 32 * q, i = j - 1 - r;
-          if (r < kb && i >= 0) xs[i] -= ring[u][q] * xj;
+          if (r < kb && i >= 0) xs[i] -= R[(u * Q + q) * 32] * xj;
         }
         __syncwarp();
         if (DIV && lane == 0) xs[j] = xj;  // row j is never read again in this sweep
-        const int jn = j - D;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const int r = lane + 32 * q;
-          ring[u][q] = (jn >= 0 && r < kb) ? __ldg(C + size_t(b0 + jn) * kb + r) : 0.0;
-        }
-        dring[u] = (DIV && jn >= 0) ? __ldg(diag + b0 + jn) : 1.0;
+        issue(u, j - D);
       }
     }
   }
+  cp_wait<0>();
   __syncwarp();
 }
 
 template <int Q>
-__device__ __forceinline__ void band_forward_any(double* xs, int nb, int b0, const BandView& F, int lane) {
+__device__ __forceinline__ void band_forward_any(double* xs, double* ring, int nb, int b0, const BandView& F,
+                                                 int lane) {
   if (F.spd)
-    band_forward<Q, false>(xs, nb, b0, F.kl, F.Lc, F.piv, lane);
+    band_forward<Q, false>(xs, ring, nb, b0, F.kl, F.Lc, F.piv, lane);
   else
-    band_forward<Q, true>(xs, nb, b0, F.kl, F.Lc, F.piv, lane);
+    band_forward<Q, true>(xs, ring, nb, b0, F.kl, F.Lc, F.piv, lane);
 }
 template <int Q>
-__device__ __forceinline__ void band_backward_any(double* xs, int nb, int b0, const BandView& F, int lane) {
+__device__ __forceinline__ void band_backward_any(double* xs, double* ring, int nb, int b0, const BandView& F,
+                                                  int lane) {
   if (F.spd)
-    band_backward<Q, false>(xs, nb, b0, F.kl, F.Lr, F.diag, lane);
+    band_backward<Q, false>(xs, ring, nb, b0, F.kl, F.Lr, F.diag, lane);
   else
-    band_backward<Q, true>(xs, nb, b0, F.ku, F.Uc, F.diag, lane);
+    band_backward<Q, true>(xs, ring, nb, b0, F.ku, F.Uc, F.diag, lane);
 }
 
 __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double* rhs, double rs, double* out,
                                                         double* out2, const double* sub, double os, int out_mode) {
-  extern __shared__ double xs[];
+  extern __shared__ double band_smem[];
+  double* ring = band_smem;                         // band_ring_doubles(8) doubles
+  double* xs = band_smem + band_ring_doubles(8);    // the block's right-hand side / solution
   const int blk = blockIdx.x, lane = threadIdx.x;
   const int b0 = F.block_start[blk], b1 = F.block_start[blk + 1], nb = b1 - b0;
   if (lane == 0) {
@@ -512,30 +535,30 @@ __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double
   __syncwarp();
   const int qf = (F.kl + 31) / 32;
   if (qf <= 1)
-    band_forward_any<1>(xs, nb, b0, F, lane);
+    band_forward_any<1>(xs, ring, nb, b0, F, lane);
   else if (qf <= 2)
-    band_forward_any<2>(xs, nb, b0, F, lane);
+    band_forward_any<2>(xs, ring, nb, b0, F, lane);
   else if (qf <= 3)
-    band_forward_any<3>(xs, nb, b0, F, lane);
+    band_forward_any<3>(xs, ring, nb, b0, F, lane);
   else if (qf <= 4)
-    band_forward_any<4>(xs, nb, b0, F, lane);
+    band_forward_any<4>(xs, ring, nb, b0, F, lane);
   else
-    band_forward_any<8>(xs, nb, b0, F, lane);
+    band_forward_any<8>(xs, ring, nb, b0, F, lane);
   if (F.spd) {
     for (int i = lane; i < nb; i += 32) xs[i] = xs[i] / F.diag[b0 + i];
     __syncwarp();
   }
   const int qb = ((F.spd ? F.kl : F.ku) + 31) / 32;
   if (qb <= 1)
-    band_backward_any<1>(xs, nb, b0, F, lane);
+    band_backward_any<1>(xs, ring, nb, b0, F, lane);
   else if (qb <= 2)
-    band_backward_any<2>(xs, nb, b0, F, lane);
+    band_backward_any<2>(xs, ring, nb, b0, F, lane);
   else if (qb <= 3)
-    band_backward_any<3>(xs, nb, b0, F, lane);
+    band_backward_any<3>(xs, ring, nb, b0, F, lane);
   else if (qb <= 4)
-    band_backward_any<4>(xs, nb, b0, F, lane);
+    band_backward_any<4>(xs, ring, nb, b0, F, lane);
   else
-    band_backward_any<8>(xs, nb, b0, F, lane);
+    band_backward_any<8>(xs, ring, nb, b0, F, lane);
   for (int i = lane; i < nb; i += 32) {
     const double x = xs[i];
     if (out_mode == 1)
