@@ -390,7 +390,7 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
     band_max_block = std::max(band_max_block, F.block_start[b + 1] - F.block_start[b]);
   band = BandView{F.n, F.kl, F.ku, int(F.block_start.size()) - 1, band_start.get(), band_Lc.get(), band_diag.get(),
                   band_Lr.get(), band_Uc.get(), band_piv.get(), F.kind == fpb::BandFactor::Kind::spd ? 1 : 0};
-  const size_t smem = sizeof(double) * (size_t(band_ring_doubles(8)) + size_t(std::max(band_max_block, 1)));
+  const size_t smem = sizeof(double) * (size_t(band_ring_doubles(kBandMaxQ)) + size_t(std::max(band_max_block, 1)));
   if (smem > 227 * 1024) throw std::invalid_argument("precond upload: fracture block too large for the band solver");
   if (smem > 48 * 1024)
     cuda_check(cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
@@ -403,7 +403,7 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
 void DevicePrecond::enqueue_band(const double* rhs, double rs, double* out, double* out2, const double* sub, double os,
                                  int mode, cudaStream_t s, Ledger* L) {
   if (band.n == 0) return;
-  band_solve_kernel<<<band.n_blocks, 32, sizeof(double) * (band_ring_doubles(8) + std::max(band_max_block, 1)), s>>>(
+  band_solve_kernel<<<band.n_blocks, 32, sizeof(double) * (band_ring_doubles(kBandMaxQ) + std::max(band_max_block, 1)), s>>>(
       band, rhs, rs, out, out2,
                                                                                               sub, os, mode);
   cuda_check(cudaGetLastError(), "band_solve_kernel launch");

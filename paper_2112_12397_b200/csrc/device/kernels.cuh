@@ -402,7 +402,34 @@ __device__ __forceinline__ void cp_wait() {
 // per-lane shared-memory slot while step j computes (async groups, not register
 // scoreboards, track completion; each lane reads back only what it copied).
 constexpr int kBandDepth = 16;
+constexpr int kBandMaxQ = 12;  // band widths up to 32*12 - 1 = 383 (fracture patches up to 191 faces wide)
 __host__ __device__ constexpr int band_ring_doubles(int q) { return kBandDepth * 32 * (q + 1); }
+
+// Register window.  At step j, lane l / slot q holds the current value of row
+// j + l + 32q (forward) or j - l - 32q (backward); the window spans 32Q > band
+// rows, so every row a step updates is in registers.  After the step the window
+// shifts by one row (shuffle down), the next pivot comes from lane 0 by
+// shuffle, and the row entering at the far end is read from shared memory.  The
+// dependent chain per step is DMUL, DADD and two shuffles; shared memory and
+// barriers stay off it.  Factor columns arrive through the cp.async ring.
+template <int Q>
+__device__ __forceinline__ double window_select(const double (&v)[Q], int sq) {
+  double s = v[0];
+#pragma unroll
+  for (int q = 1; q < Q; ++q)
+    if (sq == q) s = v[q];
+  return s;
+}
+
+template <int Q>
+__device__ __forceinline__ void window_shift(double (&v)[Q], int lane, double entering) {
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const double down = __shfl_down_sync(0xffffffffu, v[q], 1);
+    const double wrap = q + 1 < Q ? __shfl_sync(0xffffffffu, v[q + 1 < Q ? q + 1 : q], 0) : entering;
+    v[q] = lane == 31 ? wrap : down;
+  }
+}
 
 // Forward sweep with (optional) partial-pivot row swaps: for j ascending,
 // y_j = x[piv_j] (swapped with x_j), then x_i -= L(i,j) y_j for i in (j, j+kl].
@@ -410,14 +437,14 @@ template <int Q, bool PIV>
 __device__ __forceinline__ void band_forward(double* xs, double* ring, int nb, int b0, int kl,
                                              const double* __restrict__ Lc, const int* __restrict__ piv, int lane) {
   constexpr int D = kBandDepth;
-  double* R = ring + lane;                                           // slot (u,q): R[(u*Q+q)*32]
-  int* PR = reinterpret_cast<int*>(ring + D * Q * 32) + lane;        // slot u: PR[u*32]
+  double* R = ring + lane;                                     // slot (u,q): R[(u*Q+q)*32] = L(., lane+32q-1)
+  int* PR = reinterpret_cast<int*>(ring + D * Q * 32) + lane;  // slot u: PR[u*32]
   auto issue = [&](int u, int jj) {
     if (jj < nb) {
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const int r = lane + 32 * q;
-        if (r < kl) cp_async8(R + (u * Q + q) * 32, Lc + size_t(b0 + jj) * kl + r);
+        const int r = lane + 32 * q - 1;
+        if (r >= 0 && r < kl) cp_async8(R + (u * Q + q) * 32, Lc + size_t(b0 + jj) * kl + r);
       }
       if (PIV) cp_async4(PR + u * 32, piv + b0 + jj);
     }
@@ -425,26 +452,35 @@ __device__ __forceinline__ void band_forward(double* xs, double* ring, int nb, i
   };
 #pragma unroll
   for (int u = 0; u < D; ++u) issue(u, u);
+  double v[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) v[q] = lane + 32 * q < nb ? xs[lane + 32 * q] : 0.0;
   for (int j0 = 0; j0 < nb; j0 += D) {
 #pragma unroll
     for (int u = 0; u < D; ++u) {
       const int j = j0 + u;
       if (j < nb) {
         cp_wait<D - 1>();
-        const double a = xs[j];
-        const int p = PIV ? PR[u * 32] - b0 : j;
-        const double yj = PIV ? xs[p] : a;
-        if (PIV) __syncwarp();  // every lane has read x_p before its owner overwrites it
+        const double a = __shfl_sync(0xffffffffu, v[0], 0);
+        double yj = a;
+        if (PIV) {
+          const int d = PR[u * 32] - b0 - j;  // pivot row offset in the window, 0..kl
+          const int sq = d >> 5, ls = d & 31;
+          yj = __shfl_sync(0xffffffffu, window_select<Q>(v, sq), ls);
+          if (d > 0 && lane == ls) {  // the pivot row now holds the old x_j
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const int r = lane + 32 * q, i = j + 1 + r;
-          if (r < kl && i < nb) {
-            const double cur = (PIV && i == p) ? a : xs[i];
-            xs[i] = cur - R[(u * Q + q) * 32] * yj;
+            for (int q = 0; q < Q; ++q)
+              if (q == sq) v[q] = a;
           }
         }
-        __syncwarp();
-        if (PIV && lane == 0) xs[j] = yj;  // row j is never read again in this sweep
+        if (lane == 0) xs[j] = yj;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int r = lane + 32 * q - 1;
+          if (r >= 0 && r < kl) v[q] = v[q] - R[(u * Q + q) * 32] * yj;
+        }
+        const int ent = j + 32 * Q;
+        window_shift<Q>(v, lane, ent < nb ? xs[ent] : 0.0);
         issue(u, j + D);
       }
     }
@@ -461,34 +497,42 @@ __device__ __forceinline__ void band_backward(double* xs, double* ring, int nb, 
                                               int lane) {
   constexpr int D = kBandDepth;
   double* R = ring + lane;
-  double* DR = ring + D * Q * 32 + lane;  // slot u: DR[u*32]
+  double* DR = ring + D * Q * 32 + lane;  // slot u: DR[u*32] (lane 0's copy is used)
   auto issue = [&](int u, int j) {
     if (j >= 0) {
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
-        const int r = lane + 32 * q;
-        if (r < kb) cp_async8(R + (u * Q + q) * 32, C + size_t(b0 + j) * kb + r);
+        const int r = lane + 32 * q - 1;
+        if (r >= 0 && r < kb) cp_async8(R + (u * Q + q) * 32, C + size_t(b0 + j) * kb + r);
       }
-      if (DIV) cp_async8(DR + u * 32, diag + b0 + j);
+      if (DIV && lane == 0) cp_async8(DR + u * 32, diag + b0 + j);
     }
     cp_commit();
   };
 #pragma unroll
   for (int u = 0; u < D; ++u) issue(u, nb - 1 - u);
+  double v[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int i = nb - 1 - lane - 32 * q;
+    v[q] = i >= 0 ? xs[i] : 0.0;
+  }
   for (int j0 = nb - 1; j0 >= 0; j0 -= D) {
 #pragma unroll
     for (int u = 0; u < D; ++u) {
       const int j = j0 - u;
       if (j >= 0) {
         cp_wait<D - 1>();
-        const double xj = DIV ? xs[j] / DR[u * 32] : xs[j];
+        const double c0 = DIV && lane == 0 ? v[0] / DR[u * 32] : v[0];
+        const double xj = __shfl_sync(0xffffffffu, c0, 0);
+        if (lane == 0) xs[j] = xj;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-          const int r = lane + 32 * q, i = j - 1 - r;
-          if (r < kb && i >= 0) xs[i] -= R[(u * Q + q) * 32] * xj;
+          const int r = lane + 32 * q - 1;
+          if (r >= 0 && r < kb) v[q] = v[q] - R[(u * Q + q) * 32] * xj;
         }
-        __syncwarp();
-        if (DIV && lane == 0) xs[j] = xj;  // row j is never read again in this sweep
+        const int ent = j - 32 * Q;
+        window_shift<Q>(v, lane, ent >= 0 ? xs[ent] : 0.0);
         issue(u, j - D);
       }
     }
@@ -517,8 +561,8 @@ __device__ __forceinline__ void band_backward_any(double* xs, double* ring, int 
 __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double* rhs, double rs, double* out,
                                                         double* out2, const double* sub, double os, int out_mode) {
   extern __shared__ double band_smem[];
-  double* ring = band_smem;                         // band_ring_doubles(8) doubles
-  double* xs = band_smem + band_ring_doubles(8);    // the block's right-hand side / solution
+  double* ring = band_smem;                                    // band_ring_doubles(kBandMaxQ) doubles
+  double* xs = band_smem + band_ring_doubles(kBandMaxQ);       // the block's right-hand side / solution
   const int blk = blockIdx.x, lane = threadIdx.x;
   const int b0 = F.block_start[blk], b1 = F.block_start[blk + 1], nb = b1 - b0;
   if (lane == 0) {
@@ -533,7 +577,7 @@ __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double
   }
   for (int i = lane; i < nb; i += 32) xs[i] = rhs[b0 + i] * rs;
   __syncwarp();
-  const int qf = (F.kl + 31) / 32;
+  const int qf = (F.kl + 32) / 32;  // window of 32 Q rows must exceed the band (rows j+1 .. j+kl)
   if (qf <= 1)
     band_forward_any<1>(xs, ring, nb, b0, F, lane);
   else if (qf <= 2)
@@ -542,13 +586,15 @@ __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double
     band_forward_any<3>(xs, ring, nb, b0, F, lane);
   else if (qf <= 4)
     band_forward_any<4>(xs, ring, nb, b0, F, lane);
-  else
+  else if (qf <= 8)
     band_forward_any<8>(xs, ring, nb, b0, F, lane);
+  else
+    band_forward_any<12>(xs, ring, nb, b0, F, lane);
   if (F.spd) {
     for (int i = lane; i < nb; i += 32) xs[i] = xs[i] / F.diag[b0 + i];
     __syncwarp();
   }
-  const int qb = ((F.spd ? F.kl : F.ku) + 31) / 32;
+  const int qb = ((F.spd ? F.kl : F.ku) + 32) / 32;
   if (qb <= 1)
     band_backward_any<1>(xs, ring, nb, b0, F, lane);
   else if (qb <= 2)
@@ -557,8 +603,10 @@ __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double
     band_backward_any<3>(xs, ring, nb, b0, F, lane);
   else if (qb <= 4)
     band_backward_any<4>(xs, ring, nb, b0, F, lane);
-  else
+  else if (qb <= 8)
     band_backward_any<8>(xs, ring, nb, b0, F, lane);
+  else
+    band_backward_any<12>(xs, ring, nb, b0, F, lane);
   for (int i = lane; i < nb; i += 32) {
     const double x = xs[i];
     if (out_mode == 1)
