@@ -55,7 +55,7 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s) {
   if (A.slice_rows == 32)
     csr_slice_kernel<32, 64><<<blocks_for(A.csr.n_rows, 32), 256, 0, s>>>(A.csr.view(), g, e);
   else
-    csr_slice_kernel<8, 256><<<blocks_for(A.csr.n_rows, 8), 256, 0, s>>>(A.csr.view(), g, e);
+    csr_slice_kernel<2, 1024><<<blocks_for(A.csr.n_rows, 2), 256, 0, s>>>(A.csr.view(), g, e);
   cuda_check(cudaGetLastError(), "csr_slice_kernel launch");
 }
 

@@ -191,14 +191,14 @@ __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
   double s = 0.0;
   int buf = 0;
   for (long long w0 = 0; w0 < maxlen; w0 += W) {
-    // produce: warp w handles rows w, w+8, ...
-    for (int r = warp; r < nrows; r += 8) {
-      const long long b = rb[r] + w0, e = rb[r + 1];
-      double* dst = prod + (size_t(buf) * R + r) * (W + 1);
+    // produce: element t of the R x W window goes to thread t % 256 (consecutive
+    // threads read consecutive entries of one row: coalesced)
 #pragma unroll
-      for (int h = 0; h < W / 32; ++h) {
-        const long long k = b + lane + 32 * h;
-        dst[lane + 32 * h] = k < e ? __ldg(A.v + k) * g(__ldg(A.ci + k)) : 0.0;
+    for (int h = 0; h < R * W / 256; ++h) {
+      const int t = threadIdx.x + 256 * h, r = t / W, c = t - r * W;
+      if (r < nrows) {
+        const long long k = rb[r] + w0 + c;
+        prod[(size_t(buf) * R + r) * (W + 1) + c] = k < rb[r + 1] ? __ldg(A.v + k) * g(__ldg(A.ci + k)) : 0.0;
       }
     }
     __syncthreads();
