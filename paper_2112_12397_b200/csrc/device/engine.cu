@@ -480,7 +480,7 @@ GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart
   flag_.alloc(1);
   int per_sm = 0;
   cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_kernel, kMgsThreads, 0), "occupancy");
-  mgs_grid_ = sm_count() * std::max(1, std::min(per_sm, 2));
+  mgs_grid_ = sm_count() * std::max(1, std::min(per_sm, 1));  // one CTA per SM: fewer partials per barrier
   red_grid_ = sm_count() * 2;
   partial_.alloc(size_t(std::max(4 * mgs_grid_, red_grid_)));
   cuda_check(cudaHostAlloc(&status_h_, sizeof(GmresStatus), cudaHostAllocMapped), "cudaHostAlloc");
@@ -530,7 +530,7 @@ void GmresSolver::build_graphs(double st, double sp, cudaStream_t s) {
 
 double GmresSolver::norm_into(const double* a, const double* b, double* diff_out, double* dev_out, cudaStream_t s) {
   sumsq_partial_kernel<<<red_grid_, kRedThreads, 0, s>>>(n_, a, b, diff_out, partial_.get());
-  finish_sum_kernel<<<1, 32, 0, s>>>(red_grid_, partial_.get(), dev_out, host_scalar_d_, 1);
+  finish_sum_kernel<<<1, kRedThreads, 0, s>>>(red_grid_, partial_.get(), dev_out, host_scalar_d_, 1);
   cuda_check(cudaStreamSynchronize(s), "norm sync");
   return *host_scalar_;
 }

@@ -46,11 +46,20 @@ __device__ __forceinline__ double block_sum(double v, double* sm) {
   return s;  // valid in thread 0
 }
 
-// all blocks read the same partials in the same order -> identical totals
+// All blocks reduce the same partials with the same fixed tree (coalesced
+// load, warp shuffles, then the warp sums in index order) -> identical totals
+// in every block, bitwise reproducible run to run.
 __device__ __forceinline__ double grid_total(const double* part, int nb, double* sm) {
+  double v = 0.0;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v += __ldcg(part + b);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm[w] = v;
+  __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int b = 0; b < nb; ++b) s += part[b];
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += sm[i];
     sm[32] = s;
   }
   __syncthreads();
@@ -237,10 +246,11 @@ __global__ void __launch_bounds__(kRedThreads) sumsq_partial_kernel(long long n,
   const double s = block_sum(acc, sm);
   if (threadIdx.x == 0) partial[blockIdx.x] = s;
 }
-__global__ void finish_sum_kernel(int nb, const double* partial, double* out_dev, double* out_host, int take_sqrt) {
+__global__ void __launch_bounds__(kRedThreads) finish_sum_kernel(int nb, const double* partial, double* out_dev,
+                                                                 double* out_host, int take_sqrt) {
+  __shared__ double sm[40];
+  double s = grid_total(partial, nb, sm);
   if (threadIdx.x != 0) return;
-  double s = 0.0;
-  for (int b = 0; b < nb; ++b) s += partial[b];
   if (take_sqrt) s = sqrt(s);
   if (out_dev) *out_dev = s;
   if (out_host) *out_host = s;
