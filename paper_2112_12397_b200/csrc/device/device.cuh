@@ -55,6 +55,7 @@ struct BandView {
   const double* Uc = nullptr;    // general: n * ku, U(j-1-r, j)
   const int* piv = nullptr;      // general: absolute row swapped with j at step j
   int spd = 1;
+  int pivoted = 1;               // general: 0 when the LU took no row swaps
 };
 
 struct DenseLUView {  // coarse-level full-pivot LU, column-major n x n

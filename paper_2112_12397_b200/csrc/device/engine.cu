@@ -74,7 +74,9 @@ void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s) 
 DMat make_mat(const fpb::Csr& A) {
   DMat M;
   const double avg = A.n_rows > 0 ? double(A.nnz()) / A.n_rows : 0.0;
-  M.warp = A.n_rows > 0 && (avg >= 48.0 || (A.n_rows < 8192 && avg >= 8.0));
+  // SELL's thread-per-row chains need enough rows to hide latency; below ~64k
+  // rows the slice kernel's parallel loads win even for short rows
+  M.warp = A.n_rows > 0 && (avg >= 48.0 || (A.n_rows < 65536 && avg >= 8.0));
   if (!M.warp) {
     M.sell = make_sell(A);
     return M;
@@ -389,7 +391,8 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
   for (size_t b = 0; b + 1 < F.block_start.size(); ++b)
     band_max_block = std::max(band_max_block, F.block_start[b + 1] - F.block_start[b]);
   band = BandView{F.n, F.kl, F.ku, int(F.block_start.size()) - 1, band_start.get(), band_Lc.get(), band_diag.get(),
-                  band_Lr.get(), band_Uc.get(), band_piv.get(), F.kind == fpb::BandFactor::Kind::spd ? 1 : 0};
+                  band_Lr.get(), band_Uc.get(), band_piv.get(), F.kind == fpb::BandFactor::Kind::spd ? 1 : 0,
+                  F.pivoted ? 1 : 0};
   const size_t smem = sizeof(double) * (size_t(band_ring_doubles(kBandMaxQ)) + size_t(std::max(band_max_block, 1)));
   if (smem > 227 * 1024) throw std::invalid_argument("precond upload: fracture block too large for the band solver");
   if (smem > 48 * 1024)

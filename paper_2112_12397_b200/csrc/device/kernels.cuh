@@ -547,7 +547,10 @@ __device__ __forceinline__ void band_forward_any(double* xs, double* ring, int n
   if (F.spd)
     band_forward<Q, false>(xs, ring, nb, b0, F.kl, F.Lc, F.piv, lane);
   else
-    band_forward<Q, true>(xs, ring, nb, b0, F.kl, F.Lc, F.piv, lane);
+    if (F.pivoted)
+      band_forward<Q, true>(xs, ring, nb, b0, F.kl, F.Lc, F.piv, lane);
+    else
+      band_forward<Q, false>(xs, ring, nb, b0, F.kl, F.Lc, F.piv, lane);
 }
 template <int Q>
 __device__ __forceinline__ void band_backward_any(double* xs, double* ring, int nb, int b0, const BandView& F,

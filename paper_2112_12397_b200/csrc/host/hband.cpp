@@ -156,6 +156,25 @@ void BandFactor::factor(const Csr& A, Kind k) {
     }
   }
   if (failed) throw numerical_error("SparseFactor: sparse LU factorization failed (singular matrix?)");
+  // Trim U to its effective bandwidth and record whether any row swap happened.
+  // Dropped entries are exact zeros (x_i - 0 * x_j == x_i), so the solve is
+  // unchanged bit for bit; without swaps the device skips the pivot path.
+  pivoted = false;
+  for (int j = 0; j < n; ++j) pivoted = pivoted || piv[j] != j;
+  int ku_eff = 0;
+  for (int j = 0; j < n; ++j)
+    for (int r = ku - 1; r >= ku_eff; --r)
+      if (Uc[size_t(j) * ku + r] != 0.0) {
+        ku_eff = r + 1;
+        break;
+      }
+  if (ku_eff < ku) {
+    std::vector<double> U2(size_t(n) * std::max(ku_eff, 1), 0.0);
+    for (int j = 0; j < n; ++j)
+      for (int r = 0; r < ku_eff; ++r) U2[size_t(j) * ku_eff + r] = Uc[size_t(j) * ku + r];
+    Uc.swap(U2);
+    ku = ku_eff;
+  }
 }
 
 std::vector<double> BandFactor::solve(std::span<const double> b) const {

@@ -72,6 +72,7 @@ struct BandFactor {
   std::vector<int> block_start;
   std::vector<double> Lc, diag, Lr, Uc;
   std::vector<int> piv;
+  bool pivoted = false;  // general: any row swap (else the pivot path is skipped on the device)
   void factor(const Csr& A, Kind k);
   std::vector<double> solve(std::span<const double> b) const;  // host check path
 };
