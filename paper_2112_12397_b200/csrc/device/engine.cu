@@ -705,10 +705,8 @@ ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int re
     const double w = A.opt.jacobi_omega, nd = L.n;
     cuda_check(cudaMemsetAsync(L.b.get(), 0, L.b.bytes(), s), "memset");
     cuda_check(cudaMemsetAsync(L.xt.get(), 0, L.xt.bytes(), s), "memset");
-    r.fine_resid_ms = timed([&] {
-      launch_level(L, GPresmooth{L.b.get(), L.d.get(), w}, EResidPre{L.b.get(), L.d.get(), w, L.xt.get(), L.r.get()}, s);
-    });
-    r.fine_resid_bytes = L.a_bytes() + 32.0 * nd;
+    r.fine_resid_ms = timed([&] { launch_level(L, GPlain{L.xt.get()}, EResid{L.b.get(), L.r.get()}, s); });
+    r.fine_resid_bytes = L.a_bytes() + 24.0 * nd;
     r.fine_post_ms = timed([&] {
       launch_level(L, GPlain{L.xt.get()}, EJacobi{L.b.get(), L.d.get(), w, L.xt.get(), L.xt2.get()}, s);
     });

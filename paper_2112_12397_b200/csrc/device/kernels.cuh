@@ -56,14 +56,23 @@ __device__ __forceinline__ double sell_row(const SellView& A, int row, const G& 
 }
 
 // ---------------------------------------------------------------- epilogues
+// Two-phase epilogues: load(i) fetches the row's operands (b_i, d_i, x_i, ...)
+// before the row loop so their latency overlaps the matrix stream; apply
+// (operator()) then combines them with the row sum s.  Each formula is the
+// reference's expression order.
+struct NoPre {};
 struct EStore {
   double* y;
-  __device__ __forceinline__ void operator()(int i, double s) const { y[i] = s; }
+  using P = NoPre;
+  __device__ __forceinline__ P load(int) const { return {}; }
+  __device__ __forceinline__ void operator()(int i, double s, const P&) const { y[i] = s; }
 };
 struct EAddTo {  // y_i = a_i + s   (x += P e_c, amg.cpp:168-169; t_u = w_u + C1 t_t, precond.cpp:217)
   const double* a;
   double* y;
-  __device__ __forceinline__ void operator()(int i, double s) const { y[i] = a[i] + s; }
+  struct P { double a; };
+  __device__ __forceinline__ P load(int i) const { return {a[i]}; }
+  __device__ __forceinline__ void operator()(int i, double s, const P& p) const { y[i] = p.a + s; }
 };
 // Producers of an AMG right-hand side b also emit the first Jacobi sweep from
 // zero, xh = (omega b_i) / d_i (amg.cpp:136-140 with x = 0), so the V-cycle's
@@ -73,9 +82,11 @@ struct EStorePre {  // y_i = s ; xh_i = (w s) / d_i   (restriction r_c = P^T r)
   const double* d;
   double w;
   double* xh;
-  __device__ __forceinline__ void operator()(int i, double s) const {
+  struct P { double d; };
+  __device__ __forceinline__ P load(int i) const { return {d[i]}; }
+  __device__ __forceinline__ void operator()(int i, double s, const P& p) const {
     y[i] = s;
-    xh[i] = (w * s) / d[i];
+    xh[i] = (w * s) / p.d;
   }
 };
 struct EAddToPre {  // y_i = a_i + s ; xh_i = (w y_i) / d_i   (t_u = w_u + C1 t_t)
@@ -84,34 +95,28 @@ struct EAddToPre {  // y_i = a_i + s ; xh_i = (w y_i) / d_i   (t_u = w_u + C1 t_
   const double* d;
   double w;
   double* xh;
-  __device__ __forceinline__ void operator()(int i, double s) const {
-    const double v = a[i] + s;
+  struct P { double a, d; };
+  __device__ __forceinline__ P load(int i) const { return {a[i], d[i]}; }
+  __device__ __forceinline__ void operator()(int i, double s, const P& p) const {
+    const double v = p.a + s;
     y[i] = v;
-    xh[i] = (w * v) / d[i];
+    xh[i] = (w * v) / p.d;
   }
 };
 struct ESubFromScaled {  // y_i = a_i * sa - s   (t_p = w_p - Q2 s_u with w_p = D^-1 v_p)
   const double* a;
   double sa;
   double* y;
-  __device__ __forceinline__ void operator()(int i, double s) const { y[i] = a[i] * sa - s; }
+  struct P { double a; };
+  __device__ __forceinline__ P load(int i) const { return {a[i]}; }
+  __device__ __forceinline__ void operator()(int i, double s, const P& p) const { y[i] = p.a * sa - s; }
 };
 struct EResid {  // r_i = b_i - s   (amg.cpp:162-164)
   const double* b;
   double* r;
-  __device__ __forceinline__ void operator()(int i, double s) const { r[i] = b[i] - s; }
-};
-struct EResidPre {  // fused first pre-smoothing sweep + residual
-  const double* b;
-  const double* d;
-  double w;
-  double* x;
-  double* r;
-  __device__ __forceinline__ void operator()(int i, double s) const {
-    const double bi = b[i];
-    x[i] = (w * bi) / d[i];
-    r[i] = bi - s;
-  }
+  struct P { double b; };
+  __device__ __forceinline__ P load(int i) const { return {b[i]}; }
+  __device__ __forceinline__ void operator()(int i, double s, const P& p) const { r[i] = p.b - s; }
 };
 struct EJacobi {  // x'_i = x_i + (omega (b_i - s)) / d_i   (amg.cpp:139)
   const double* b;
@@ -119,7 +124,11 @@ struct EJacobi {  // x'_i = x_i + (omega (b_i - s)) / d_i   (amg.cpp:139)
   double w;
   const double* x;
   double* xo;
-  __device__ __forceinline__ void operator()(int i, double s) const { xo[i] = x[i] + (w * (b[i] - s)) / d[i]; }
+  struct P { double b, d, x; };
+  __device__ __forceinline__ P load(int i) const { return {b[i], d[i], x[i]}; }
+  __device__ __forceinline__ void operator()(int i, double s, const P& p) const {
+    xo[i] = p.x + (w * (p.b - s)) / p.d;
+  }
 };
 struct EJacobiSubFrom {  // out_i = c_i - (Jacobi update)   (v_u = s_u - v_u2, precond.cpp:224)
   const double* b;
@@ -128,23 +137,26 @@ struct EJacobiSubFrom {  // out_i = c_i - (Jacobi update)   (v_u = s_u - v_u2, p
   const double* x;
   const double* c;
   double* out;
-  __device__ __forceinline__ void operator()(int i, double s) const {
-    const double xn = x[i] + (w * (b[i] - s)) / d[i];
-    out[i] = c[i] - xn;
+  struct P { double b, d, x, c; };
+  __device__ __forceinline__ P load(int i) const { return {b[i], d[i], x[i], c[i]}; }
+  __device__ __forceinline__ void operator()(int i, double s, const P& p) const {
+    const double xn = p.x + (w * (p.b - s)) / p.d;
+    out[i] = p.c - xn;
   }
 };
-// J apply, displacement rows: y_u = (A u + C1 (st v_t)) + Q1 (sp v_p)   (block.cpp:55-60)
+// J apply, displacement rows: y_u = (A u + C1 (st v_t)) + Q1 (sp v_p)   (block.cpp:55-60);
+// the short C1 / Q1 row sums are formed before the A row loop.
 struct EJu {
   SellView C1, Q1;
   const double* vt;
   const double* vp;
   double st, sp;
   double* y;
-  __device__ __forceinline__ void operator()(int i, double s) const {
-    const double b = sell_row(C1, i, GScaled{vt, st});
-    const double c = sell_row(Q1, i, GScaled{vp, sp});
-    y[i] = s + b + c;
+  struct P { double b, c; };
+  __device__ __forceinline__ P load(int i) const {
+    return {sell_row(C1, i, GScaled{vt, st}), sell_row(Q1, i, GScaled{vp, sp})};
   }
+  __device__ __forceinline__ void operator()(int i, double s, const P& p) const { y[i] = s + p.b + p.c; }
 };
 
 // ------------------------------------------------------------- SELL kernels
@@ -152,7 +164,8 @@ template <class G, class E>
 __global__ void __launch_bounds__(256) sell_kernel(SellView A, G g, E epi) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= A.n_rows) return;
-  epi(row, sell_row(A, row, g));
+  const auto pre = epi.load(row);
+  epi(row, sell_row(A, row, g), pre);
 }
 
 // ------------------------------------------------------- warp-row CSR kernel
@@ -188,6 +201,8 @@ __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
   __syncthreads();
   long long maxlen = 0;
   for (int r = 0; r < nrows; ++r) maxlen = max(maxlen, rb[r + 1] - rb[r]);
+  typename E::P pre{};
+  if (warp == 0 && lane < nrows) pre = epi.load(row0 + lane);
   double s = 0.0;
   int buf = 0;
   for (long long w0 = 0; w0 < maxlen; w0 += W) {
@@ -210,7 +225,7 @@ __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
     }
     buf ^= 1;  // the next window fills the other buffer while warp 0 sums this one
   }
-  if (warp == 0 && lane < nrows) epi(row0 + lane, s);
+  if (warp == 0 && lane < nrows) epi(row0 + lane, s, pre);
 }
 
 template <class G, class E>
@@ -237,7 +252,7 @@ __global__ void __launch_bounds__(kWarpRowThreads) csr_warp_kernel(CsrView A, G 
     p = pn;
     k = kn;
   }
-  if (lane == 0) epi(row, s);
+  if (lane == 0) epi(row, s, epi.load(row));
 }
 
 // ------------------------------------------------------------- BSR3 kernel
@@ -254,6 +269,7 @@ __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E ep
   if (brow >= A.n_brows) return;
   const long long base = A.slice_off[slice];
   const int len = A.brow_len[brow];
+  const auto pre = epi.load(3 * brow + li);
   const int* __restrict__ C = A.bcols + base + lane;
   const double* __restrict__ V = A.vals + base * 9 + li * 96 + lane;
   double s = 0.0;
@@ -279,7 +295,7 @@ __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E ep
     s = s + __ldg(V0 + 32) * g(c0 + 1);
     s = s + __ldg(V0 + 64) * g(c0 + 2);
   }
-  epi(3 * brow + li, s);
+  epi(3 * brow + li, s, pre);
 }
 
 // ------------------------------------------------ t/p rows of the J apply
