@@ -55,6 +55,29 @@ def parse():
     return ap.parse_args()
 
 
+# ---- replica bookkeeping (tests/test_replicas.py runs these over gloo, world_size 2)
+def replica_seed(base: int, rank: int) -> int:
+    """Every rank solves its own system: the workload and rhs seeds are offset by the rank."""
+    return base + rank
+
+
+def replica_max(v: float, ws: int, device: str) -> float:
+    """Max over ranks of a per-rank device time (the job is as slow as its slowest replica)."""
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_seconds_per_system(total_s: float, steps: int, ws: int) -> float:
+    """ws replicas each solve `steps` systems in total_s (max over ranks): job seconds per system."""
+    return total_s / (steps * ws)
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -199,7 +222,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     from paper_2112_12397_b200 import api
 
-    seed = args.seed + rank  # replicas: independent systems
+    seed = replica_seed(args.seed, rank)  # replicas: independent systems
     t0 = time.perf_counter()
     W = api.Workload(args.config, seed)
     J = W.system()
@@ -230,13 +253,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def max_over_ranks(v: float) -> float:
-        if ws == 1:
-            return v
-        import torch.distributed as dist
-
-        t = torch.tensor([v], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return replica_max(v, ws, "cuda")
 
     clocks = ClockSampler(local)
     barrier()
@@ -254,7 +271,7 @@ def run_ours(args):
     dev_ms = ev0.elapsed_time(ev1)
     total_s = max_over_ranks(dev_ms / 1e3)
     per_solve = total_s / args.steps
-    value = total_s / (args.steps * ws)  # whole-job seconds per system (replicas)
+    value = whole_job_seconds_per_system(total_s, args.steps, ws)
 
     # e2e: through the C ABI with pinned host buffers; H2D of b and D2H of x inside the timed region
     b_pin = torch.tensor(b_host, dtype=torch.float64).pin_memory()
