@@ -85,6 +85,16 @@ def dist_env():
     return ws, rank, local
 
 
+def ncu_traffic(key: str):
+    """dram read+write bytes per launch of `key` from the committed ncu --set full capture (or None)."""
+    p = os.path.join(ROOT, "profiles", "round1", "ncu_full_bsr3.json")
+    try:
+        k = json.load(open(p))["kernels"][key]
+        return k["dram_bytes_read"] + k["dram_bytes_write"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -313,7 +323,9 @@ def run_ours(args):
             "e2e": {"value": round(e2e_value, 6), "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
             "roofline": {"bound": "hbm", "kernel": "bsr3 Jacobi post-smoothing sweep, finest AMG level (S1)",
                          "achieved": round(fine_gbs, 1) if fine_gbs else None, "peak": hbm, "unit": "GB/s",
-                         "frac": round(fine_gbs / hbm, 3) if fine_gbs else None, "traffic": None,
+                         "frac": round(fine_gbs / hbm, 3) if fine_gbs else None,
+                         "traffic": ncu_traffic("bsr3_EJacobi"),
+                         "traffic_source": "profiles/round1/ncu_full_bsr3.json (dram__bytes_read+write per launch)",
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": prof["fine_post_bytes"],
                          "avg_launch_ms": round(prof["fine_post_ms"], 4)},
             "precond_apply": {"GBps": round(apply_gbs, 1), "frac": round(apply_gbs / hbm, 3),
