@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--variant", default="tup", choices=["tup", "tpu", "tup_star"])
     ap.add_argument("--theta", type=float, default=0.0, help="AMG strength_threshold (amg.hpp:20)")
+    ap.add_argument("--factor-solve", default="auto", choices=["auto", "sweep", "inverse"],
+                    help="T / S~2 application: sweeps or explicit block inverses (DESIGN.md §5b)")
     ap.add_argument("--restart", type=int, default=50)
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--max-iter", type=int, default=500)
@@ -239,7 +241,8 @@ def run_ours(args):
     gen_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     op = api.BlockSystemOperator(J)
-    cfg = api.PrecondConfig(args.variant, amg=api.AmgConfig(strength_threshold=args.theta))
+    cfg = api.PrecondConfig(args.variant, amg=api.AmgConfig(strength_threshold=args.theta),
+                            factor_solve=args.factor_solve)
     hp = api.HostPreconditioner(J, cfg)
     pc = api.GpuPreconditioner.from_host(op, hp)
     setup_s = time.perf_counter() - t0
@@ -316,6 +319,7 @@ def run_ours(args):
             "config": {"workload": CONFIG_NAMES[args.config], "n_u": J.n_u, "n_t": J.n_t, "n_p": J.n_p,
                        "unknowns": n, "variant": args.variant, "gmres": f"GMRES({args.restart})", "rtol": args.tol,
                        "amg_strength_threshold": args.theta, "smoother": "weighted_jacobi",
+                       "factor_solve": pc.factor_solve,
                        "l2": "256 MB buffer written between timed solves; working set > 126 MB L2",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
             "iterations": st.iterations, "converged": st.converged, "restarts": st.restarts,

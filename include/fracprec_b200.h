@@ -70,10 +70,18 @@ typedef struct fp_amg_config {
   int32_t max_levels;
 } fp_amg_config;
 
+/* How the fracture-block factor (T or S~2, SparseFactor) is applied:
+ * FP_FACTOR_SWEEP   - forward/backward column sweeps on the banded factor;
+ * FP_FACTOR_INVERSE - the explicit inverse of every fracture block (columns =
+ *                     sweep solves of unit vectors), streamed as a block GEMV;
+ * FP_FACTOR_AUTO    - the faster of the two that fits device memory. */
+enum { FP_FACTOR_AUTO = 0, FP_FACTOR_SWEEP = 1, FP_FACTOR_INVERSE = 2 };
+
 /* PrecondConfig (precond.hpp:19-30); inner is always AMG on this path */
 typedef struct fp_precond_config {
   int32_t variant;
   fp_amg_config amg;
+  int32_t factor_solve; /* FP_FACTOR_* (0 = auto) */
 } fp_precond_config;
 
 typedef struct fp_gmres_options {
@@ -116,6 +124,7 @@ typedef struct fp_precond_desc {
   int32_t n_levels;
   const fp_amg_level_desc* levels;
   fp_amg_config amg;
+  int32_t factor_solve; /* FP_FACTOR_* (0 = auto) */
 } fp_precond_desc;
 
 const char* fp_last_error(void);
@@ -154,6 +163,8 @@ int fp_precond_apply(fp_precond* p, const double* x, double* y, int32_t mem);
 int fp_amg_apply(fp_precond* p, const double* r, double* x, int32_t mem);
 /* InnerSolver::call_count / reset_count (precond.hpp:34-42) */
 int64_t fp_precond_inner_calls(fp_precond* p, int32_t reset);
+/* The factor application the preconditioner resolved to: FP_FACTOR_SWEEP or FP_FACTOR_INVERSE */
+int fp_precond_factor_solve(const fp_precond* p, int32_t* mode);
 /* algorithmic HBM bytes and kernel launches of one fp_precond_apply / fp_system_apply */
 int fp_precond_traffic(fp_precond* p, double* apply_bytes, int32_t* apply_launches, double* japply_bytes);
 

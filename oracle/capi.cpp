@@ -179,6 +179,19 @@ int or_precond_build(void* s, int variant, int inner, const double* amg_d, const
 
 void or_precond_destroy(void* p) { delete static_cast<Pc*>(p); }
 
+// factor_solve: 0 = sweeps (SparseFactor::solve), 1 = explicit block inverse
+int or_precond_set_factor_solve(void* p, int mode) {
+  return guard([&] {
+    Pc* pc = static_cast<Pc*>(p);
+    BandFactor& F = pc->tpu ? pc->tpu->T_factor : pc->tup->S2_factor;
+    if (mode == 1) {
+      if (F.inv.empty()) F.build_inverse();
+    } else {
+      F.inv.clear(), F.inv_off.clear();
+    }
+  });
+}
+
 int or_precond_apply(void* p, const double* x, double* y) {
   return guard([&] {
     const Pc* pc = static_cast<Pc*>(p);

@@ -11,6 +11,9 @@
 // column sweeps — forward: for j ascending, finalize y_j, then subtract
 // L(i,j)*y_j from each later row i; backward: for j descending, finalize x_j,
 // then subtract U(i,j)*x_j from each earlier row i.
+// factor_solve = inverse: the same operator as an explicit per-block inverse
+// (columns = sweep solves of unit vectors) applied as a block GEMV whose row
+// sums are 32 lane-strided partials combined by a fixed xor tree.
 #include <algorithm>
 #include <cmath>
 #include <limits>
@@ -218,42 +221,89 @@ void BandFactor::factor(const CsrMatrix& A, Kind k) {
   }
 }
 
+void BandFactor::solve_block(int blk, double* x) const {
+  const int b0 = block_start[blk], b1 = block_start[blk + 1];
+  // forward sweep: (pivot) + unit-lower L
+  for (int j = b0; j < b1; ++j) {
+    if (kind == Kind::general && piv[j] != j) std::swap(x[j], x[piv[j]]);
+    const double yj = x[j];
+    for (int r = 0; r < kl; ++r) {
+      const int i = j + 1 + r;
+      if (i >= b1) break;
+      x[i] -= Lc[size_t(j) * kl + r] * yj;
+    }
+  }
+  if (kind == Kind::spd) {
+    for (int j = b0; j < b1; ++j) x[j] = x[j] / diag[j];
+    // backward sweep with L^T: x_j final, then x_i -= L(j,i) x_j for i < j
+    for (int j = b1 - 1; j >= b0; --j) {
+      const double xj = x[j];
+      for (int r = 0; r < kl; ++r) {
+        const int i = j - 1 - r;
+        if (i < b0) break;
+        x[i] -= Lr[size_t(j) * kl + r] * xj;
+      }
+    }
+  } else {
+    for (int j = b1 - 1; j >= b0; --j) {
+      const double xj = x[j] / diag[j];
+      x[j] = xj;
+      for (int r = 0; r < ku; ++r) {
+        const int i = j - 1 - r;
+        if (i < b0) break;
+        x[i] -= Uc[size_t(j) * ku + r] * xj;
+      }
+    }
+  }
+}
+
+void BandFactor::build_inverse() {
+  const int nblk = int(block_start.size()) - 1;
+  inv_off.assign(size_t(nblk) + 1, 0);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const size_t nb = size_t(block_start[blk + 1] - block_start[blk]);
+    inv_off[blk + 1] = inv_off[blk] + nb * nb;
+  }
+  inv.assign(inv_off.back(), 0.0);
+  std::vector<double> e(static_cast<size_t>(n), 0.0);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int b0 = block_start[blk], nb = block_start[blk + 1] - b0;
+    for (int c = 0; c < nb; ++c) {
+      std::fill(e.begin() + b0, e.begin() + b0 + nb, 0.0);
+      e[b0 + c] = 1.0;
+      solve_block(blk, e.data());
+      for (int i = 0; i < nb; ++i) inv[inv_off[blk] + size_t(i) * nb + c] = e[b0 + i];
+    }
+  }
+}
+
 std::vector<double> BandFactor::solve(std::span<const double> b) const {
   if (int(b.size()) != n) throw std::invalid_argument("SparseFactor::solve: dimension mismatch");
   std::vector<double> x(b.begin(), b.end());
-  for (size_t blk = 0; blk + 1 < block_start.size(); ++blk) {
-    const int b0 = block_start[blk], b1 = block_start[blk + 1];
-    // forward sweep: (pivot) + unit-lower L
-    for (int j = b0; j < b1; ++j) {
-      if (kind == Kind::general && piv[j] != j) std::swap(x[j], x[piv[j]]);
-      const double yj = x[j];
-      for (int r = 0; r < kl; ++r) {
-        const int i = j + 1 + r;
-        if (i >= b1) break;
-        x[i] -= Lc[size_t(j) * kl + r] * yj;
-      }
+  const int nblk = int(block_start.size()) - 1;
+  for (int blk = 0; blk < nblk; ++blk) {
+    if (inv.empty()) {
+      solve_block(blk, x.data());
+      continue;
     }
-    if (kind == Kind::spd) {
-      for (int j = b0; j < b1; ++j) x[j] = x[j] / diag[j];
-      // backward sweep with L^T: x_j final, then x_i -= L(j,i) x_j for i < j
-      for (int j = b1 - 1; j >= b0; --j) {
-        const double xj = x[j];
-        for (int r = 0; r < kl; ++r) {
-          const int i = j - 1 - r;
-          if (i < b0) break;
-          x[i] -= Lr[size_t(j) * kl + r] * xj;
-        }
+    // row i: 32 strided partial sums v[j] = sum_{c = j mod 32} inv(i,c) b_c (c
+    // ascending, from 0.0), combined by the xor tree v[j] += v[j ^ h], h = 16..1;
+    // x_i = v[0]  (a warp per row, lane j owning columns j, j+32, ...)
+    const int b0 = block_start[blk], nb = block_start[blk + 1] - b0;
+    for (int i = 0; i < nb; ++i) {
+      const double* row = inv.data() + inv_off[blk] + size_t(i) * nb;
+      double v[32];
+      for (int j = 0; j < 32; ++j) {
+        double s = 0.0;
+        for (int c = j; c < nb; c += 32) s = s + row[c] * b[b0 + c];
+        v[j] = s;
       }
-    } else {
-      for (int j = b1 - 1; j >= b0; --j) {
-        const double xj = x[j] / diag[j];
-        x[j] = xj;
-        for (int r = 0; r < ku; ++r) {
-          const int i = j - 1 - r;
-          if (i < b0) break;
-          x[i] -= Uc[size_t(j) * ku + r] * xj;
-        }
+      for (int h = 16; h >= 1; h >>= 1) {
+        double w[32];
+        for (int j = 0; j < 32; ++j) w[j] = v[j] + v[j ^ h];
+        std::copy(w, w + 32, v);
       }
+      x[b0 + i] = v[0];
     }
   }
   return x;

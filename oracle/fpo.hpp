@@ -212,7 +212,16 @@ struct BandFactor {
   // general: Uc[j*ku + r] = U(j-1-r, j)  (columns of U, for the backward sweep)
   std::vector<double> Lr, Uc;
   std::vector<int> piv;  // general: row swapped with j at step j (absolute index)
+  // factor_solve = inverse: the explicit inverse of every
+  // diagonal block, row-major, block blk at inv_off[blk]; column c is the sweep
+  // solve of the unit vector e_c.  When present, solve() is the block GEMV
+  // x_i = sum_c inv(i,c) b_c instead of the sweeps, summed as 32 partials over
+  // c = j (mod 32) (c ascending, from 0.0) combined by an xor tree (factor.cpp).
+  std::vector<double> inv;
+  std::vector<size_t> inv_off;
   void factor(const CsrMatrix& A, Kind k);
+  void build_inverse();
+  void solve_block(int blk, double* x) const;  // sweeps on one block, in place
   std::vector<double> solve(std::span<const double> b) const;
 };
 

@@ -45,7 +45,7 @@ class FpAmgConfig(C.Structure):
 
 
 class FpPrecondConfig(C.Structure):
-    _fields_ = [("variant", C.c_int32), ("amg", FpAmgConfig)]
+    _fields_ = [("variant", C.c_int32), ("amg", FpAmgConfig), ("factor_solve", C.c_int32)]
 
 
 class FpGmresOptions(C.Structure):
@@ -74,7 +74,8 @@ class FpAmgLevelDesc(C.Structure):
 
 class FpPrecondDesc(C.Structure):
     _fields_ = [("variant", C.c_int32), ("h_blocks", C.POINTER(C.c_double)), ("factor_matrix", FpCsr),
-                ("n_levels", C.c_int32), ("levels", C.POINTER(FpAmgLevelDesc)), ("amg", FpAmgConfig)]
+                ("n_levels", C.c_int32), ("levels", C.POINTER(FpAmgLevelDesc)), ("amg", FpAmgConfig),
+                ("factor_solve", C.c_int32)]
 
 
 class FpFractureSpec(C.Structure):
@@ -116,6 +117,7 @@ SIGNATURES = {
     "fp_precond_apply": (C.c_int, [_P, _P, _P, C.c_int32]),
     "fp_amg_apply": (C.c_int, [_P, _P, _P, C.c_int32]),
     "fp_precond_inner_calls": (C.c_int64, [_P, C.c_int32]),
+    "fp_precond_factor_solve": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "fp_precond_traffic": (C.c_int, [_P, _DP, C.POINTER(C.c_int32), _DP]),
     "fp_precond_profile": (C.c_int, [_P, C.c_int32, C.POINTER(FpProfile)]),
     "fp_gmres": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(FpGmresOptions), C.POINTER(FpSolveStats)]),

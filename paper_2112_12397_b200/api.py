@@ -112,11 +112,23 @@ class AmgConfig:
         return c
 
 
+_FACTOR_SOLVE = {"auto": 0, "sweep": 1, "inverse": 2}
+
+
+def _factor_mode(name: str) -> int:
+    if name not in _FACTOR_SOLVE:
+        raise ValueError(f"unknown factor_solve {name!r} (auto | sweep | inverse)")
+    return _FACTOR_SOLVE[name]
+
+
 @dataclass
 class PrecondConfig:
     variant: str = "tup"
     inner: str = "amg"
     amg: AmgConfig = field(default_factory=AmgConfig)
+    # how T / S~2 (SparseFactor) is applied: "sweep", "inverse" (explicit block
+    # inverses streamed from HBM) or "auto" (the faster that fits)
+    factor_solve: str = "auto"
 
     def native(self) -> N.FpPrecondConfig:
         if self.inner != "amg":
@@ -126,6 +138,7 @@ class PrecondConfig:
         c = N.FpPrecondConfig()
         c.variant = _VARIANTS[self.variant]
         c.amg = self.amg.native()
+        c.factor_solve = _factor_mode(self.factor_solve)
         return c
 
 
@@ -254,7 +267,7 @@ class GpuPreconditioner:
 
     @classmethod
     def upload(cls, op: BlockSystemOperator, variant: str, h_blocks: np.ndarray, factor_matrix: CsrMatrix,
-               levels: Sequence[tuple], amg: AmgConfig) -> "GpuPreconditioner":
+               levels: Sequence[tuple], amg: AmgConfig, factor_solve: str = "auto") -> "GpuPreconditioner":
         """Upload a reference-built hierarchy: levels = [(A_l, P_l or None, smoother_diag_l), ...]."""
         keep = []
         descs = (N.FpAmgLevelDesc * len(levels))()
@@ -272,6 +285,7 @@ class GpuPreconditioner:
         desc.n_levels = len(levels)
         desc.levels = descs
         desc.amg = amg.native()
+        desc.factor_solve = _factor_mode(factor_solve)
         h = C.c_void_p()
         N.check(N.lib.fp_precond_upload(op._h, C.byref(desc), C.byref(h)))
         return cls(op, h, variant)
@@ -300,6 +314,13 @@ class GpuPreconditioner:
         xp, _m, _kb = _vec(x, n_u)
         N.check(N.lib.fp_amg_apply(self._h, rp, xp, mem))
         return x
+
+    @property
+    def factor_solve(self) -> str:
+        """The factor application this preconditioner resolved to: 'sweep' or 'inverse'."""
+        m = C.c_int32()
+        N.check(N.lib.fp_precond_factor_solve(self._h, C.byref(m)))
+        return "inverse" if m.value == 2 else "sweep"
 
     def call_count(self) -> int:
         return int(N.lib.fp_precond_inner_calls(self._h, 0))

@@ -209,12 +209,14 @@ int fp_host_precond_build(const fp_block_system* J, const fp_precond_config* cfg
                           int32_t n_nodes, fp_host_precond** out) {
   return guard([&] {
     need(J && cfg && out, "fp_host_precond_build: null argument");
+    need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
     const fpb::HostSystem H = to_system(*J);
     std::vector<std::array<double, 3>> xyz;
     if (coords)
       for (int v = 0; v < n_nodes; ++v) xyz.push_back({coords[3 * v], coords[3 * v + 1], coords[3 * v + 2]});
     auto p = std::make_unique<fp_host_precond>();
     p->hp = fpb::build_precond(H, cfg->variant, to_amg(cfg->amg), xyz);
+    p->hp.factor_solve = cfg->factor_solve;
     *out = p.release();
   });
 }
@@ -291,6 +293,8 @@ int fp_precond_upload(fp_system* s, const fp_precond_desc* d, fp_precond** out) 
     hp.hblocks.assign(d->h_blocks, d->h_blocks + 9 * size_t(s->dev->n_p));
     const fpb::Csr F = to_csr(d->factor_matrix, "factor_matrix");
     hp.factor.factor(F, d->variant == FP_TPU ? fpb::BandFactor::Kind::spd : fpb::BandFactor::Kind::general);
+    need(d->factor_solve >= FP_FACTOR_AUTO && d->factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
+    hp.factor_solve = d->factor_solve;
     hp.amg.opt = to_amg(d->amg);
     for (int l = 0; l < d->n_levels; ++l) {
       fpb::HostLevel L;
@@ -313,6 +317,13 @@ int fp_precond_upload(fp_system* s, const fp_precond_desc* d, fp_precond** out) 
 }
 
 void fp_precond_destroy(fp_precond* p) { delete p; }
+
+int fp_precond_factor_solve(const fp_precond* p, int32_t* mode) {
+  return guard([&] {
+    need(p && mode, "null argument");
+    *mode = p->dev->inverse ? FP_FACTOR_INVERSE : FP_FACTOR_SWEEP;
+  });
+}
 
 int fp_precond_apply(fp_precond* p, const double* x, double* y, int32_t mem) {
   return guard([&] {

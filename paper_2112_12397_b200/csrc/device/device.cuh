@@ -58,6 +58,14 @@ struct BandView {
   int pivoted = 1;               // general: 0 when the LU took no row swaps
 };
 
+// factor_solve = inverse: explicit inverse of every fracture block, row-major,
+// block b at off[b] (rows of all blocks stacked in factor order).
+struct DinvView {
+  const int* block_start = nullptr;
+  const long long* off = nullptr;
+  const double* v = nullptr;
+};
+
 struct DenseLUView {  // coarse-level full-pivot LU, column-major n x n
   int n = 0, rank = 0;
   const double* lu = nullptr;

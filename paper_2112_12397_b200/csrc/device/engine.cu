@@ -393,9 +393,40 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
   band = BandView{F.n, F.kl, F.ku, int(F.block_start.size()) - 1, band_start.get(), band_Lc.get(), band_diag.get(),
                   band_Lr.get(), band_Uc.get(), band_piv.get(), F.kind == fpb::BandFactor::Kind::spd ? 1 : 0,
                   F.pivoted ? 1 : 0};
+  // factor_solve: sweeps (latency bound: ~2 * nb sequential steps per block) or the
+  // explicit block inverses (HBM bound: 8 nb^2 bytes per block, all blocks in one
+  // grid).  Auto picks the inverse when its streaming time is the smaller one and
+  // it fits a quarter of the free device memory.
+  {
+    double inv_bytes = 0.0;
+    for (size_t b = 0; b + 1 < F.block_start.size(); ++b) {
+      const double nb = F.block_start[b + 1] - F.block_start[b];
+      inv_bytes += 8.0 * nb * nb;
+    }
+    size_t free_b = 0, total_b = 0;
+    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const bool fits = inv_bytes <= 0.25 * double(free_b);
+    if (hp.factor_solve == 2 && !fits)
+      throw std::invalid_argument("precond upload: explicit block inverses do not fit in device memory");
+    const double t_inv = inv_bytes / 5.0e12 + 5e-6, t_sweep = 2.0 * band_max_block * 2.5e-7;
+    inverse = hp.factor_solve == 2 || (hp.factor_solve == 0 && fits && F.n > 0 && t_inv < t_sweep);
+  }
+  if (inverse) {
+    std::vector<double> inv;
+    std::vector<int64_t> off;
+    F.inverse_blocks(inv, off);
+    dinv_v.upload(inv);
+    inv.clear();
+    inv.shrink_to_fit();
+    std::vector<long long> offl(off.begin(), off.end());
+    dinv_off.upload(offl);
+    dinv = DinvView{band_start.get(), dinv_off.get(), dinv_v.get()};
+    dinv_bytes = 8.0 * double(off.back());
+  }
   const size_t smem = sizeof(double) * (size_t(band_ring_doubles(kBandMaxQ)) + size_t(std::max(band_max_block, 1)));
-  if (smem > 227 * 1024) throw std::invalid_argument("precond upload: fracture block too large for the band solver");
-  if (smem > 48 * 1024)
+  if (!inverse && smem > 227 * 1024)
+    throw std::invalid_argument("precond upload: fracture block too large for the band solver");
+  if (!inverse && smem > 48 * 1024)
     cuda_check(cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
                "band smem attribute");
   const int nu = s.n_u, nt = s.n_t, np = s.n_p;
@@ -406,6 +437,13 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
 void DevicePrecond::enqueue_band(const double* rhs, double rs, double* out, double* out2, const double* sub, double os,
                                  int mode, cudaStream_t s, Ledger* L) {
   if (band.n == 0) return;
+  if (inverse) {
+    dinv_kernel<<<blocks_for(size_t(band.n) * 32, kDinvThreads), kDinvThreads, 0, s>>>(dinv, band.n, band.n_blocks,
+                                                                                       rhs, rs, out, out2, sub, os, mode);
+    cuda_check(cudaGetLastError(), "dinv_kernel launch");
+    if (L) L->add(dinv_bytes + 8.0 * band.n * (2 + (mode == 1) + (mode == 2)));
+    return;
+  }
   band_solve_kernel<<<band.n_blocks, 32, sizeof(double) * (band_ring_doubles(kBandMaxQ) + std::max(band_max_block, 1)), s>>>(
       band, rhs, rs, out, out2,
                                                                                               sub, os, mode);

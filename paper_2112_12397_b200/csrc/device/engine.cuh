@@ -132,6 +132,12 @@ class DevicePrecond {
   DevBuf<int> band_start, band_piv;
   DevBuf<double> band_Lc, band_diag, band_Lr, band_Uc;
   int band_max_block = 0;
+  // factor_solve = inverse: explicit block inverses streamed by dinv_kernel
+  bool inverse = false;
+  DinvView dinv{};
+  DevBuf<double> dinv_v;
+  DevBuf<long long> dinv_off;
+  double dinv_bytes = 0;
   DevBuf<double> tt, tu, tp, su, sp_, vp, tu2, vu2, xh;
   long inner_calls = 0;
   int inner_per_apply() const { return variant == 1 ? 2 : 1; }

@@ -636,6 +636,47 @@ __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double
   }
 }
 
+// ------------------------------------------- explicit block inverse apply
+// factor_solve = inverse: one warp per row of the stacked block
+// inverses, streaming the row once with coalesced 256-byte loads; lane j keeps
+// the partial sum over columns c = j (mod 32) in ascending c and the partials
+// meet in the xor tree h = 16..1 — the order the oracle's BandFactor::solve
+// (factor.cpp) defines for this mode.  8 loads per lane in flight per step.
+constexpr int kDinvThreads = 256;
+__global__ void __launch_bounds__(kDinvThreads) dinv_kernel(DinvView D, int n, int n_blocks, const double* rhs,
+                                                            double rs, double* out, double* out2, const double* sub,
+                                                            double os, int out_mode) {
+  const int row = (blockIdx.x * kDinvThreads + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= n) return;  // warp-uniform
+  int lo = 0, hi = n_blocks - 1;  // block of this row: block_start[blk] <= row < block_start[blk + 1]
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (D.block_start[mid] <= row) lo = mid; else hi = mid - 1;
+  }
+  const int b0 = D.block_start[lo], nb = D.block_start[lo + 1] - b0;
+  const double* M = D.v + D.off[lo] + (long long)(row - b0) * nb;
+  const double* g = rhs + b0;
+  double s = 0.0;
+  int c = lane;
+  for (; c + 7 * 32 < nb; c += 8 * 32) {
+    double m[8], x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) m[u] = __ldcs(M + c + 32 * u), x[u] = __ldg(g + c + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = s + m[u] * (x[u] * rs);
+  }
+  for (; c < nb; c += 32) s = s + __ldcs(M + c) * (__ldg(g + c) * rs);
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) s = s + __shfl_xor_sync(0xffffffffu, s, h);
+  if (lane == 0) {
+    if (out_mode == 1)
+      out[row] = (sub[row] - s) * os;
+    else
+      out[row] = s;
+    if (out_mode == 2) out2[row] = s * os;
+  }
+}
+
 // ---------------------------------------------------- coarse dense solve
 // x = Q U^-1 L^-1 P b on the full-pivot LU (restated FullPivLU::solve), one CTA,
 // column sweeps.  LU is column-major so each step reads one contiguous column.

@@ -204,4 +204,56 @@ std::vector<double> BandFactor::solve(std::span<const double> b) const {
   return x;
 }
 
+void BandFactor::inverse_blocks(std::vector<double>& inv, std::vector<int64_t>& off) const {
+  const int nblk = int(block_start.size()) - 1;
+  off.assign(size_t(nblk) + 1, 0);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int64_t nb = block_start[blk + 1] - block_start[blk];
+    off[blk + 1] = off[blk] + nb * nb;
+  }
+  inv.assign(size_t(off.back()), 0.0);
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int b0 = block_start[blk], nb = block_start[blk + 1] - b0;
+    double* out = inv.data() + off[blk];
+#pragma omp parallel
+    {
+      std::vector<double> xv(static_cast<size_t>(nb));
+      double* x = xv.data() - b0;  // absolute indexing inside the block
+#pragma omp for schedule(dynamic, 16)
+      for (int c = 0; c < nb; ++c) {
+        std::fill(xv.begin(), xv.end(), 0.0);
+        x[b0 + c] = 1.0;
+        for (int j = b0; j < b0 + nb; ++j) {
+          if (kind == Kind::general && piv[j] != j) std::swap(x[j], x[piv[j]]);
+          const double yj = x[j];
+          if (yj == 0.0) continue;
+          const int e = std::min(kl, b0 + nb - 1 - j);
+          const double* l = Lc.data() + size_t(j) * kl;
+          for (int r = 0; r < e; ++r) x[j + 1 + r] -= l[r] * yj;
+        }
+        if (kind == Kind::spd) {
+          for (int j = b0; j < b0 + nb; ++j) x[j] = x[j] / diag[j];
+          for (int j = b0 + nb - 1; j >= b0; --j) {
+            const double xj = x[j];
+            if (xj == 0.0) continue;
+            const int e = std::min(kl, j - b0);
+            const double* l = Lr.data() + size_t(j) * kl;
+            for (int r = 0; r < e; ++r) x[j - 1 - r] -= l[r] * xj;
+          }
+        } else {
+          for (int j = b0 + nb - 1; j >= b0; --j) {
+            const double xj = x[j] / diag[j];
+            x[j] = xj;
+            if (xj == 0.0) continue;
+            const int e = std::min(ku, j - b0);
+            const double* u = Uc.data() + size_t(j) * ku;
+            for (int r = 0; r < e; ++r) x[j - 1 - r] -= u[r] * xj;
+          }
+        }
+        for (int i = 0; i < nb; ++i) out[size_t(i) * nb + c] = xv[size_t(i)];
+      }
+    }
+  }
+}
+
 }  // namespace fpb

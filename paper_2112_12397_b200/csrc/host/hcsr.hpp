@@ -75,6 +75,10 @@ struct BandFactor {
   bool pivoted = false;  // general: any row swap (else the pivot path is skipped on the device)
   void factor(const Csr& A, Kind k);
   std::vector<double> solve(std::span<const double> b) const;  // host check path
+  // Explicit inverse of every diagonal block (factor_solve = inverse), row-major,
+  // block blk at off[blk]: column c = the sweep solve of e_c.  Zero pivots are
+  // skipped, which changes at most the sign of zero entries (never a GEMV sum).
+  void inverse_blocks(std::vector<double>& inv, std::vector<int64_t>& off) const;
 };
 
 }  // namespace fpb

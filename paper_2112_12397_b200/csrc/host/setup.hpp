@@ -60,6 +60,7 @@ struct HostPrecond {
   std::vector<double> S_K;      // t-u-p fixed-stress diagonal
   Csr S2;                       // t-u-p S~2 = T - diag(S_K)
   BandFactor factor;            // T (t-p-u, LDL^T) or S~2 (t-u-p, LU)
+  int factor_solve = 0;         // 0 auto, 1 sweeps, 2 explicit block inverse
 };
 
 HostPrecond build_precond(const HostSystem& J, int variant, const AmgOptions& opt,

@@ -40,6 +40,7 @@ def _load():
         "or_csr_info": (C.c_int, [P, IP, IP, C.POINTER(C.c_int64)]),
         "or_csr_copy": (C.c_int, [P, C.POINTER(C.c_int64), IP, DP]),
         "or_precond_build": (C.c_int, [P, C.c_int, C.c_int, DP, IP, DP, C.c_int, PP]),
+        "or_precond_set_factor_solve": (C.c_int, [P, C.c_int]),
         "or_precond_destroy": (None, [P]),
         "or_precond_apply": (C.c_int, [P, DP, DP]),
         "or_precond_inner_calls": (C.c_long, [P, C.c_int]),
@@ -147,7 +148,7 @@ class OracleSystem:
 
 
 class OraclePrecond:
-    def __init__(self, sys: OracleSystem, variant="tup", inner="amg", coords=None, **amg):
+    def __init__(self, sys: OracleSystem, variant="tup", inner="amg", coords=None, factor_solve="sweep", **amg):
         cfg = dict(AMG_DEFAULT, **amg)
         d = np.array([cfg["strength_threshold"], cfg["jacobi_omega"], cfg["stall_ratio"]])
         i = np.array([cfg["max_coarse"], cfg["pre_sweeps"], cfg["post_sweeps"], cfg["smoother"],
@@ -160,6 +161,13 @@ class OraclePrecond:
             cp, nn = _dp(self._coords), self._coords.shape[0]
         _check(lib.or_precond_build(sys.h, VARIANT[variant], 0 if inner == "amg" else 1, _dp(d),
                                     i.ctypes.data_as(C.POINTER(C.c_int)), cp, nn, C.byref(self.h)))
+        self.set_factor_solve(factor_solve)
+
+    def set_factor_solve(self, mode: str) -> None:
+        """'sweep' (SparseFactor::solve) or 'inverse' (explicit block inverse, DESIGN.md §5b)."""
+        assert mode in ("sweep", "inverse"), mode
+        _check(lib.or_precond_set_factor_solve(self.h, 1 if mode == "inverse" else 0))
+        self.factor_solve = mode
 
     def __del__(self):
         if getattr(self, "h", None):

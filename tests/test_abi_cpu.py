@@ -137,3 +137,32 @@ def test_workload_custom_mesh_counts():
     assert J.n_u == 3 * 76 and J.n_p == 4 and J.n_t == 12
     with pytest.raises(ValueError, match="not grid aligned"):
         api.Workload(spec=dict(cells=(2, 2, 2), fractures=[(0, 0.3, 0.0, 1.0, 0.0, 1.0)]), seed=1)
+
+
+@pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
+def test_oracle_block_inverse_is_the_sweep_operator(variant):
+    """factor_solve = inverse applies the same operator as the
+    reference's SparseFactor sweeps, up to rounding (1e-12 relative, the apply bar)."""
+    J = small_workload(seed=41, cells=(8, 6, 6), fracs=((0, 0.25, 0.0, 1.0, 0.0, 1.0), (0, 0.75, 0.0, 1.0, 0.5, 1.0)))
+    osys = oracle_system(J)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords)
+    rng = np.random.default_rng(6)
+    xs = rng.uniform(-1, 1, (3, J.total_dimension()))
+    ref = [opc.apply(x) for x in xs]
+    opc.set_factor_solve("inverse")
+    for x, r in zip(xs, ref):
+        y = opc.apply(x)
+        assert np.linalg.norm(y - r) <= 1e-12 * np.linalg.norm(r)
+    opc.set_factor_solve("sweep")
+    assert all(np.array_equal(opc.apply(x), r) for x, r in zip(xs, ref))
+
+
+def test_factor_solve_is_validated():
+    with pytest.raises(ValueError, match="factor_solve"):
+        api.PrecondConfig(factor_solve="cholesky").native()
+    J = small_workload()
+    cfg = api.PrecondConfig("tup").native()
+    cfg.factor_solve = 7
+    h = C.c_void_p()
+    st = N.lib.fp_host_precond_build(C.byref(J.view()), C.byref(cfg), None, 0, C.byref(h))
+    assert st == N.FP_INVALID_ARGUMENT and b"factor_solve" in N.lib.fp_last_error()

@@ -18,6 +18,8 @@ from test_abi_cpu import oracle_system, small_workload
 pytestmark = pytest.mark.gpu
 
 TOL_APPLY = 1e-12
+# T / S~2 application: the reference's sweeps, and the explicit block inverse
+FACTOR_SOLVES = ["sweep", "inverse"]
 
 
 def rel(a, b):
@@ -42,7 +44,8 @@ def upload_oracle_precond(op, osys, opc, variant, amg):
         P = csr_of(opc.level_matrix(l, 1)) if l > 0 else None
         levels.append((A, P, opc.level_diag(l)))
     factor = csr_of(osys.block(6)) if variant == "tpu" else csr_of(opc.matrix(1))
-    return api.GpuPreconditioner.upload(op, variant, opc.hblocks(), factor, levels, amg)
+    return api.GpuPreconditioner.upload(op, variant, opc.hblocks(), factor, levels, amg,
+                                        factor_solve=opc.factor_solve)
 
 
 def amg_kw(amg: api.AmgConfig):
@@ -85,16 +88,18 @@ def test_system_apply_bitwise(case):
     assert np.array_equal(y, ref)
 
 
+@pytest.mark.parametrize("factor_solve", FACTOR_SOLVES)
 @pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_precond_apply_matches_oracle(case, variant):
+def test_precond_apply_matches_oracle(case, variant, factor_solve):
     osys = CASES[case]()
     J = system_from_oracle(osys)
     J.node_coords = coords_for(case)
     amg = api.AmgConfig(max_coarse=8 if case.startswith("toy") else 100)
-    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, **amg_kw(amg))
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, factor_solve=factor_solve, **amg_kw(amg))
     op = api.BlockSystemOperator(J)
     pc = upload_oracle_precond(op, osys, opc, variant, amg)
+    assert pc.factor_solve == factor_solve
     rng = np.random.default_rng(5)
     for trial in range(3):
         x = rng.uniform(-1, 1, J.total_dimension())
@@ -103,13 +108,15 @@ def test_precond_apply_matches_oracle(case, variant):
         assert np.array_equal(y, ref), (trial, rel(y, ref))
 
 
+@pytest.mark.parametrize("factor_solve", ["auto"] + FACTOR_SOLVES)
 @pytest.mark.parametrize("variant", ["tpu", "tup"])
-def test_product_built_precond_matches_oracle(variant):
+def test_product_built_precond_matches_oracle(variant, factor_solve):
     J = small_workload(seed=11, cells=(8, 6, 5))
     osys = oracle_system(J)
-    opc = O.OraclePrecond(osys, variant, coords=J.node_coords)
     op = api.BlockSystemOperator(J)
-    pc = (api.build_tpu if variant == "tpu" else api.build_tup)(J, op=op)
+    pc = (api.build_tpu if variant == "tpu" else api.build_tup)(J, api.PrecondConfig(factor_solve=factor_solve), op=op)
+    assert pc.factor_solve == ("inverse" if factor_solve == "auto" else factor_solve)  # small blocks: inverse wins
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, factor_solve=pc.factor_solve)
     x = np.random.default_rng(2).uniform(-1, 1, J.total_dimension())
     assert np.array_equal(pc.apply(x), opc.apply(x))
 
@@ -162,12 +169,13 @@ def test_sgs_smoother_is_rejected_on_the_gpu():
         api.GpuPreconditioner.from_host(op, hp)
 
 
+@pytest.mark.parametrize("factor_solve", FACTOR_SOLVES)
 @pytest.mark.parametrize("variant", ["tpu", "tup"])
 @pytest.mark.parametrize("restart", [50, 8])
-def test_gmres_matches_oracle(variant, restart):
+def test_gmres_matches_oracle(variant, restart, factor_solve):
     J = small_workload(seed=23, cells=(8, 8, 6))
     osys = oracle_system(J)
-    opc = O.OraclePrecond(osys, variant, coords=J.node_coords)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, factor_solve=factor_solve)
     op = api.BlockSystemOperator(J)
     pc = upload_oracle_precond(op, osys, opc, variant, api.AmgConfig())
     b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
@@ -186,7 +194,7 @@ def test_gmres_unscaled_and_zero_rhs():
     osys = oracle_system(J)
     op = api.BlockSystemOperator(J)
     pc = api.build_tup(J, op=op)
-    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords)
+    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, factor_solve=pc.factor_solve)
     b = np.random.default_rng(1).uniform(-1, 1, J.total_dimension())
     x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=300, restart=50, scaled=False)
     x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=50, max_iter=300, scaled=False)
@@ -236,14 +244,15 @@ def _decoupled_with_T(T):
     return J, O.OracleSystem.from_blocks(J.n_u, J.n_t, J.n_p, blocks)
 
 
+@pytest.mark.parametrize("factor_solve", FACTOR_SOLVES)
 @pytest.mark.parametrize("variant,shift", [("tpu", 0.0), ("tup", 0.0), ("tup", -8.0)])
-def test_banded_factor_solves_match_oracle(variant, shift):
+def test_banded_factor_solves_match_oracle(variant, shift, factor_solve):
     """T / S~2 solves over several independent fracture blocks with bandwidths 7..40;
     shift -8 makes S~2 indefinite so the LU takes row pivots (banded solve with swaps)."""
     T = _grid_laplacian_blocks([7, 12, 40, 3], shift_every=3 if shift else 0, shift=shift)
     J, osys = _decoupled_with_T(T)
     amg = api.AmgConfig(max_coarse=8)
-    opc = O.OraclePrecond(osys, variant, **amg_kw(amg))
+    opc = O.OraclePrecond(osys, variant, factor_solve=factor_solve, **amg_kw(amg))
     op = api.BlockSystemOperator(J)
     pc = upload_oracle_precond(op, osys, opc, variant, amg)
     x = np.random.default_rng(8).uniform(-1, 1, J.total_dimension())
@@ -251,26 +260,29 @@ def test_banded_factor_solves_match_oracle(variant, shift):
     assert np.array_equal(y, ref), rel(y, ref)
 
 
+@pytest.mark.parametrize("factor_solve", FACTOR_SOLVES)
 @pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
-def test_theta0_hierarchy_apply_bitwise(variant):
+def test_theta0_hierarchy_apply_bitwise(variant, factor_solve):
     """The bench's AMG setting (strength_threshold 0): wide coarse rows take the warp-row kernel."""
     J = small_workload(seed=31, cells=(12, 12, 10))
     osys = oracle_system(J)
     amg = api.AmgConfig(strength_threshold=0.0)
-    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, **amg_kw(amg))
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, factor_solve=factor_solve, **amg_kw(amg))
     op = api.BlockSystemOperator(J)
     pc = upload_oracle_precond(op, osys, opc, variant, amg)
     x = np.random.default_rng(12).uniform(-1, 1, J.total_dimension())
     assert np.array_equal(pc.apply(x), opc.apply(x))
-    pc2 = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, api.PrecondConfig(variant, amg=amg)))
+    pc2 = api.GpuPreconditioner.from_host(
+        op, api.HostPreconditioner(J, api.PrecondConfig(variant, amg=amg, factor_solve=factor_solve)))
     assert np.array_equal(pc2.apply(x), opc.apply(x))
 
 
-def test_theta0_gmres_matches_oracle_and_history():
+@pytest.mark.parametrize("factor_solve", FACTOR_SOLVES)
+def test_theta0_gmres_matches_oracle_and_history(factor_solve):
     J = small_workload(seed=37, cells=(12, 12, 12))
     osys = oracle_system(J)
     amg = api.AmgConfig(strength_threshold=0.0)
-    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, **amg_kw(amg))
+    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, factor_solve=factor_solve, **amg_kw(amg))
     op = api.BlockSystemOperator(J)
     pc = upload_oracle_precond(op, osys, opc, "tup", amg)
     b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())

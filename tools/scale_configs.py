@@ -3,6 +3,7 @@
     python tools/scale_configs.py 3 [4 ...]
 """
 import json
+import os
 import sys
 import time
 
@@ -20,7 +21,8 @@ for cfg in [int(a) for a in sys.argv[1:]]:
     gen = time.perf_counter() - t0
     t0 = time.perf_counter()
     op = api.BlockSystemOperator(J)
-    hp = api.HostPreconditioner(J, api.PrecondConfig("tup", amg=api.AmgConfig(strength_threshold=0.0)))
+    hp = api.HostPreconditioner(J, api.PrecondConfig("tup", amg=api.AmgConfig(strength_threshold=0.0),
+                                                  factor_solve=os.environ.get("FS", "auto")))
     host_setup = time.perf_counter() - t0
     t0 = time.perf_counter()
     pc = api.GpuPreconditioner.from_host(op, hp)
@@ -30,7 +32,7 @@ for cfg in [int(a) for a in sys.argv[1:]]:
     b = torch.tensor(np.random.default_rng(42).uniform(-1, 1, J.total_dimension()), device="cuda", dtype=torch.float64)
     x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=100, restart=50, scaled=True)
     free, total = torch.cuda.mem_get_info()
-    print(json.dumps(dict(config=cfg, n_u=J.n_u, n_t=J.n_t, n_p=J.n_p, info=W.info(), generate_s=round(gen, 1),
+    print(json.dumps(dict(config=cfg, factor_solve=pc.factor_solve, n_u=J.n_u, n_t=J.n_t, n_p=J.n_p, info=W.info(), generate_s=round(gen, 1),
                           host_setup_s=round(host_setup, 1), upload_s=round(upload, 1), levels=pr["level_rows"],
                           level_nnz=pr["level_nnz"], apply_ms=round(pr["apply_ms"], 3),
                           apply_GBps=round(pr["apply_bytes"] / pr["apply_ms"] / 1e6, 1),
