@@ -38,6 +38,20 @@ struct CsrView {  // plain CSR, 64-bit offsets (warp-per-row kernel)
   const double* v = nullptr;
 };
 
+// Windowed slices for the ordered long-row pipeline (csr_pipe_kernel): rows
+// grouped 32 to a slice (sorted by length inside chunks of 4096 rows to cut
+// padding), each slice stored as windows of 32 x 32 slots [window][row][lane]
+// holding entries w*32 + lane of each row in CSR order (padding: 0.0, column 0).
+struct PipeView {
+  int n_slices = 0;
+  const long long* woff = nullptr;  // n_slices + 1: first window of each slice
+  const int* row = nullptr;         // 32 per slice: original row index (-1 = padding)
+  const int* len = nullptr;         // 32 per slice: row length
+  const double* v = nullptr;
+  const int* ci = nullptr;
+  const int* cta_slice = nullptr;   // persistent CTAs: CTA b owns slices [cta_slice[b], cta_slice[b+1])
+};
+
 struct Bsr3View {
   int n_brows = 0;
   const long long* slice_off = nullptr;  // block-slot index of (slice, k=0, lane=0)

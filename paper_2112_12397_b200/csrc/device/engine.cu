@@ -51,9 +51,19 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s) {
     launch_sell(A.sell, g, e, s);
     return;
   }
+  if (A.pipe) {
+    if (A.pm.n_slices == 0) return;
+    static const bool smem_set = [] {
+      cuda_check(cudaFuncSetAttribute(csr_pipe_kernel<G, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPipeSmem)),
+                 "csr_pipe smem attribute");
+      return true;
+    }();
+    (void)smem_set;
+    csr_pipe_kernel<<<unsigned(A.pm.n_ctas), kPipeThreads, kPipeSmem, s>>>(A.pm.view(), g, e);
+    cuda_check(cudaGetLastError(), "csr_pipe_kernel launch");
+    return;
+  }
   if (A.csr.n_rows == 0) return;
-  if (A.slice_rows == 32)
-    csr_slice_kernel<32, 64><<<blocks_for(A.csr.n_rows, 32), 256, 0, s>>>(A.csr.view(), g, e);
   else
     csr_slice_kernel<2, 1024><<<blocks_for(A.csr.n_rows, 2), 256, 0, s>>>(A.csr.view(), g, e);
   cuda_check(cudaGetLastError(), "csr_slice_kernel launch");
@@ -82,6 +92,11 @@ DMat make_mat(const fpb::Csr& A) {
     return M;
   }
   M.slice_rows = A.n_rows >= 2048 ? 32 : 8;
+  if (M.slice_rows == 32) {
+    M.pipe = true;
+    M.pm = make_pipe(A);
+    return M;
+  }
   M.csr.n_rows = A.n_rows, M.csr.n_cols = A.n_cols, M.csr.nnz = A.nnz();
   std::vector<long long> rp(A.rp.begin(), A.rp.end());
   M.csr.rp.upload(rp);
@@ -91,6 +106,67 @@ DMat make_mat(const fpb::Csr& A) {
 }
 
 // ------------------------------------------------------------ format upload
+DPipe make_pipe(const fpb::Csr& A) {
+  constexpr int kSigma = 4096;  // rows are sorted by length only inside chunks (locality of the gathers)
+  DPipe D;
+  D.n_rows = A.n_rows, D.nnz = A.nnz();
+  D.n_slices = (A.n_rows + kPipeRows - 1) / kPipeRows;
+  std::vector<int> perm(static_cast<size_t>(D.n_slices) * kPipeRows, -1);
+  for (int i = 0; i < A.n_rows; ++i) perm[i] = i;
+  for (int c0 = 0; c0 < A.n_rows; c0 += kSigma) {
+    const int c1 = std::min(A.n_rows, c0 + kSigma);
+    std::stable_sort(perm.begin() + c0, perm.begin() + c1,
+                     [&](int a, int b) { return A.row_len(a) > A.row_len(b); });
+  }
+  std::vector<int> len(perm.size(), 0);
+  std::vector<long long> woff(static_cast<size_t>(D.n_slices) + 1, 0);
+  for (int s = 0; s < D.n_slices; ++s) {
+    int mx = 0;
+    for (int r = 0; r < kPipeRows; ++r) {
+      const int i = perm[size_t(s) * kPipeRows + r];
+      len[size_t(s) * kPipeRows + r] = i >= 0 ? A.row_len(i) : 0;
+      mx = std::max(mx, len[size_t(s) * kPipeRows + r]);
+    }
+    woff[s + 1] = woff[s] + (mx + kPipeW - 1) / kPipeW;
+  }
+  constexpr int64_t kWin = int64_t(kPipeRows) * kPipeW;
+  D.slots = woff.back() * kWin;
+  std::vector<double> v(static_cast<size_t>(D.slots), 0.0);
+  std::vector<int> ci(static_cast<size_t>(D.slots), 0);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int s = 0; s < D.n_slices; ++s)
+    for (int r = 0; r < kPipeRows; ++r) {
+      const int i = perm[size_t(s) * kPipeRows + r];
+      if (i < 0) continue;
+      const int64_t b = A.rp[i];
+      for (int k = 0; k < A.row_len(i); ++k) {
+        const int64_t idx = (woff[s] + k / kPipeW) * kWin + int64_t(r) * kPipeW + k % kPipeW;
+        v[size_t(idx)] = A.v[size_t(b + k)];
+        ci[size_t(idx)] = A.ci[size_t(b + k)];
+      }
+    }
+  // persistent CTAs (one per SM) over contiguous slice ranges of equal window count
+  int dev = 0, sms = 148;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+  D.n_ctas = std::max(1, std::min(D.n_slices, sms));
+  std::vector<int> cs(static_cast<size_t>(D.n_ctas) + 1, D.n_slices);
+  cs[0] = 0;
+  const long long tot = woff.back();
+  for (int b = 1; b < D.n_ctas; ++b) {
+    const long long target = (tot * b + D.n_ctas - 1) / D.n_ctas;
+    cs[b] = int(std::lower_bound(woff.begin(), woff.end() - 1, target) - woff.begin());
+    cs[b] = std::max(cs[b], cs[b - 1]);
+  }
+  D.cta_slice.upload(cs);
+  D.woff.upload(woff);
+  D.row.upload(perm);
+  D.len.upload(len);
+  D.v.upload(v);
+  D.ci.upload(ci);
+  return D;
+}
+
 DSell make_sell(const fpb::Csr& A) {
   DSell D;
   D.n_rows = A.n_rows, D.n_cols = A.n_cols, D.nnz = A.nnz();

@@ -74,17 +74,32 @@ struct DCsr {
   double matrix_bytes() const { return 12.0 * double(nnz) + 8.0 * (n_rows + 1); }
 };
 
+struct DPipe {
+  int n_rows = 0, n_slices = 0, n_ctas = 0;
+  int64_t nnz = 0, slots = 0;
+  DevBuf<long long> woff;
+  DevBuf<int> row, len, ci, cta_slice;
+  DevBuf<double> v;
+  PipeView view() const {
+    return {n_slices, woff.get(), row.get(), len.get(), v.get(), ci.get(), cta_slice.get()};
+  }
+  double matrix_bytes() const { return 12.0 * double(nnz) + 8.0 * n_rows; }
+};
+DPipe make_pipe(const fpb::Csr& A);
+
 // A scalar sparse operator in the layout that streams best for its shape:
 // SELL-32 (thread per row) for many short rows, warp-row CSR for few / long
 // rows (coarse AMG levels, restrictions).  Both sum each row left to right.
 struct DMat {
   bool warp = false;
   int slice_rows = 32;  // rows per CTA of the slice kernel (8 for few-row operators)
+  bool pipe = false;     // warp && many rows: the windowed producer/consumer pipeline
   DSell sell;
   DCsr csr;
-  int n_rows() const { return warp ? csr.n_rows : sell.n_rows; }
-  int64_t nnz() const { return warp ? csr.nnz : sell.nnz; }
-  double matrix_bytes() const { return warp ? csr.matrix_bytes() : sell.matrix_bytes(); }
+  DPipe pm;
+  int n_rows() const { return pipe ? pm.n_rows : warp ? csr.n_rows : sell.n_rows; }
+  int64_t nnz() const { return pipe ? pm.nnz : warp ? csr.nnz : sell.nnz; }
+  double matrix_bytes() const { return pipe ? pm.matrix_bytes() : warp ? csr.matrix_bytes() : sell.matrix_bytes(); }
 };
 DMat make_mat(const fpb::Csr& A);
 

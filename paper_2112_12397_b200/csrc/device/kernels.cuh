@@ -228,6 +228,87 @@ __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
   if (warp == 0 && lane < nrows) epi(row0 + lane, s, pre);
 }
 
+// ------------------------------------------------ ordered long-row CSR pipeline
+// Rows of tens to thousands of entries (AMG levels >= 1, R = P^T) whose sums
+// must stay in column order.  One CTA owns kPipeRows rows: warp 0 is the
+// consumer (lane r sums row r, in order), warps 1..kPipeStages are producers,
+// producer q filling stage q of a shared ring with the windows w = q (mod
+// kPipeStages) — kPipeW columns of every row, lane = column (coalesced) —
+// so up to kPipeStages windows of loads and gathers are in flight while the
+// consumer sums.  Stage q is handed over with named barriers: FULL = 1 + q
+// (producer arrives, consumer waits), EMPTY = 1 + kPipeStages + q (reverse).
+constexpr int kPipeRows = 32, kPipeW = 32, kPipeStages = 7, kPipeThreads = 32 * (kPipeStages + 1);
+constexpr size_t kPipeSmem = sizeof(double) * kPipeStages * kPipeRows * (kPipeW + 1);  // dynamic (> 48 KB)
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <class G, class E>
+__global__ void __launch_bounds__(kPipeThreads, 1) csr_pipe_kernel(PipeView A, G g, E epi) {
+  extern __shared__ double pipe_smem[];
+  double(*ring)[kPipeRows][kPipeW + 1] = reinterpret_cast<double(*)[kPipeRows][kPipeW + 1]>(pipe_smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s0 = A.cta_slice[blockIdx.x], s1 = A.cta_slice[blockIdx.x + 1];
+  if (s0 >= s1) return;
+  // this CTA's windows are contiguous: [woff[s0], woff[s1])
+  const long long w_first = A.woff[s0];
+  const long long nwin = A.woff[s1] - w_first;
+  if (warp == 0) {  // consumer: lane r sums row r of the current slice in column order
+    int sl = s0;
+    long long s_begin = A.woff[sl], s_end = A.woff[sl + 1];
+    int row = A.row[sl * kPipeRows + lane], len = A.len[sl * kPipeRows + lane];
+    typename E::P pre{};
+    if (row >= 0) pre = epi.load(row);
+    double s = 0.0;
+    for (long long w = 0; w < nwin; ++w) {
+      const long long wg = w_first + w;
+      while (wg >= s_end) {  // slice done (also skips empty slices)
+        if (row >= 0) epi(row, s, pre);
+        ++sl;
+        s_begin = s_end, s_end = A.woff[sl + 1];
+        row = A.row[sl * kPipeRows + lane], len = A.len[sl * kPipeRows + lane];
+        if (row >= 0) pre = epi.load(row);
+        s = 0.0;
+      }
+      const int q = int(w % kPipeStages);
+      named_sync(1 + q, 64);
+      const int rem = len - int(wg - s_begin) * kPipeW;
+      const double* src = &ring[q][lane][0];
+      if (rem >= kPipeW) {
+#pragma unroll
+        for (int k = 0; k < kPipeW; ++k) s = s + src[k];
+      } else {
+        for (int k = 0; k < rem; ++k) s = s + src[k];
+      }
+      if (w + kPipeStages < nwin) named_arrive(1 + kPipeStages + q, 64);
+    }
+    for (;;) {  // the last slice and any empty slices after it
+      if (row >= 0) epi(row, s, pre);
+      if (++sl >= s1) break;
+      row = A.row[sl * kPipeRows + lane];
+      if (row >= 0) pre = epi.load(row);
+      s = 0.0;
+    }
+    return;
+  }
+  const int q = warp - 1;  // producer q: windows q, q + kPipeStages, ... into stage q
+  for (long long w = q; w < nwin; w += kPipeStages) {
+    if (w >= kPipeStages) named_sync(1 + kPipeStages + q, 64);
+    const long long base = (w_first + w) * (kPipeRows * kPipeW) + lane;
+    const double* __restrict__ vp = A.v + base;
+    const int* __restrict__ cp = A.ci + base;
+    double v[kPipeRows];
+    int c[kPipeRows];
+#pragma unroll
+    for (int r = 0; r < kPipeRows; ++r) v[r] = __ldcs(vp + r * kPipeW), c[r] = __ldcs(cp + r * kPipeW);
+#pragma unroll
+    for (int r = 0; r < kPipeRows; ++r) ring[q][r][lane] = v[r] * g(c[r]);
+    named_arrive(1 + q, 64);
+  }
+}
+
 template <class G, class E>
 __global__ void __launch_bounds__(kWarpRowThreads) csr_warp_kernel(CsrView A, G g, E epi) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
