@@ -4,6 +4,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -598,7 +599,25 @@ GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart
   int per_sm = 0;
   cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mgs_kernel, kMgsThreads, 0), "occupancy");
   mgs_grid_ = sm_count() * std::max(1, std::min(per_sm, 1));  // one CTA per SM: fewer partials per barrier
+  if (const char* e = std::getenv("FRACPREC_B200_MGS_GRID")) mgs_grid_ = std::max(1, std::min(mgs_grid_, std::atoi(e)));
   red_grid_ = sm_count() * 2;
+  {  // register/shared-memory MGS when a block's slice fits E <= 24 values per thread
+    const long long chunk = ((n_ + mgs_grid_ - 1) / mgs_grid_ + 31) / 32 * 32;
+    for (int e : {2, 4, 8, 16, 24})
+      if (chunk <= (long long)e * kMgsThreads) {
+        mgs_ept_ = e;
+        break;
+      }
+    mgs_smem_ = size_t(chunk) * sizeof(double);
+    if (mgs_ept_ > 0 && mgs_smem_ > 48 * 1024) {
+      auto set = [&](const void* f) {
+        cuda_check(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(mgs_smem_)),
+                   "mgs smem attribute");
+      };
+      set((const void*)mgs_fast_kernel<2>), set((const void*)mgs_fast_kernel<4>), set((const void*)mgs_fast_kernel<8>);
+      set((const void*)mgs_fast_kernel<16>), set((const void*)mgs_fast_kernel<24>);
+    }
+  }
   partial_.alloc(size_t(std::max(4 * mgs_grid_, red_grid_)));
   cuda_check(cudaHostAlloc(&status_h_, sizeof(GmresStatus), cudaHostAllocMapped), "cudaHostAlloc");
   cuda_check(cudaHostGetDevicePointer(&status_d_, status_h_, 0), "cudaHostGetDevicePointer");
@@ -650,6 +669,23 @@ double GmresSolver::norm_into(const double* a, const double* b, double* diff_out
   finish_sum_kernel<<<1, kRedThreads, 0, s>>>(red_grid_, partial_.get(), dev_out, host_scalar_d_, 1);
   cuda_check(cudaStreamSynchronize(s), "norm sync");
   return *host_scalar_;
+}
+
+void GmresSolver::launch_mgs(MgsArgs& a, cudaStream_t s) {
+  void* args[] = {&a};
+  const void* f = (const void*)mgs_kernel;
+  size_t smem = 0;
+  if (mgs_ept_ > 0) {
+    smem = mgs_smem_;
+    switch (mgs_ept_) {
+      case 2: f = (const void*)mgs_fast_kernel<2>; break;
+      case 4: f = (const void*)mgs_fast_kernel<4>; break;
+      case 8: f = (const void*)mgs_fast_kernel<8>; break;
+      case 16: f = (const void*)mgs_fast_kernel<16>; break;
+      default: f = (const void*)mgs_fast_kernel<24>; break;
+    }
+  }
+  cuda_check(cudaLaunchCooperativeKernel(f, dim3(mgs_grid_), dim3(kMgsThreads), args, smem, s), "mgs launch");
 }
 
 SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOptions& o, cudaStream_t s) {
@@ -713,9 +749,7 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
       launch_pj();
       MgsArgs a{n_, ldv_, m, ldr_, V_.get(), jout_.get(), stage, partial_.get(), h_.get(), cs_.get(), sn_.get(),
                 g_.get(), R_.get(), rnorm, status_d_};
-      void* args[] = {&a};
-      cuda_check(cudaLaunchCooperativeKernel((void*)mgs_kernel, dim3(mgs_grid_), dim3(kMgsThreads), args, 0, s),
-                 "mgs launch");
+      launch_mgs(a, s);
       cuda_check(cudaStreamSynchronize(s), "mgs sync");
       res.launches += 1;
       const GmresStatus st_h = *status_h_;

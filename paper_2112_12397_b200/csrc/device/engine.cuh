@@ -186,6 +186,8 @@ struct ProfileResult {
 };
 ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int reps, cudaStream_t s);
 
+struct MgsArgs;  // gmres_kernels.cuh
+
 // Restarted right-preconditioned GMRES on the device (gmres.cpp semantics per
 // cycle + the GMRES(m) wrapper of SURVEY §8(a) G1).
 class GmresSolver {
@@ -210,6 +212,9 @@ class GmresSolver {
   double* host_scalar_ = nullptr;
   double* host_scalar_d_ = nullptr;
   int mgs_grid_ = 0, red_grid_ = 0;
+  int mgs_ept_ = 0;       // > 0: mgs_fast_kernel<E> (slices in registers / shared memory)
+  size_t mgs_smem_ = 0;
+  void launch_mgs(MgsArgs& a, cudaStream_t s);
   cudaGraphExec_t pj_exec_ = nullptr, j_exec_ = nullptr;
   double graph_st_ = -1, graph_sp_ = -1;
 };

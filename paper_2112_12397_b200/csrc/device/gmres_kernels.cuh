@@ -66,6 +66,43 @@ __device__ __forceinline__ double grid_total(const double* part, int nb, double*
   return sm[32];
 }
 
+// status + Givens update of the least-squares problem (gmres.cpp:151-171), one thread
+__device__ __forceinline__ void mgs_finish(const MgsArgs& a, double hnext, double wnorm_pre, int reorth, bool finite,
+                                           bool happy) {
+  GmresStatus st;
+  st.hnext = hnext;
+  st.wnorm_pre = wnorm_pre;
+  st.happy = happy;
+  st.nonfinite = !finite;
+  st.reorth = reorth;
+  st.m = a.m;
+  st.est = 0.0;
+  if (finite) {
+    double* h = a.h;
+    const int m = a.m;
+    h[m + 1] = hnext;
+    for (int i = 0; i < m; ++i) {  // accumulated Givens rotations
+      const double t0 = a.cs[i] * h[i] + a.sn[i] * h[i + 1];
+      const double t1 = -a.sn[i] * h[i] + a.cs[i] * h[i + 1];
+      h[i] = t0;
+      h[i + 1] = t1;
+    }
+    const double denom = hypot(h[m], h[m + 1]);
+    const double c = denom == 0.0 ? 1.0 : h[m] / denom;
+    const double s = denom == 0.0 ? 0.0 : h[m + 1] / denom;
+    a.cs[m] = c;
+    a.sn[m] = s;
+    h[m] = denom;
+    h[m + 1] = 0.0;
+    for (int i = 0; i <= m; ++i) a.R[(long long)m * a.ldr + i] = h[i];
+    const double gm = a.g[m];
+    a.g[m] = c * gm;
+    a.g[m + 1] = -s * gm;
+    st.est = fabs(a.g[m + 1]) / a.beta;
+  }
+  *a.status = st;
+}
+
 __global__ void __launch_bounds__(kMgsThreads) mgs_kernel(MgsArgs a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -168,40 +205,128 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_kernel(MgsArgs a) {
       w[k] = v;
       a.stage[k] = v;
     }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    GmresStatus st;
-    st.hnext = hnext;
-    st.wnorm_pre = wnorm_pre;
-    st.happy = happy;
-    st.nonfinite = !finite;
-    st.reorth = reorth;
-    st.m = a.m;
-    st.est = 0.0;
-    if (finite) {
-      double* h = a.h;
-      const int m = a.m;
-      h[m + 1] = hnext;
-      for (int i = 0; i < m; ++i) {  // accumulated Givens rotations
-        const double t0 = a.cs[i] * h[i] + a.sn[i] * h[i + 1];
-        const double t1 = -a.sn[i] * h[i] + a.cs[i] * h[i + 1];
-        h[i] = t0;
-        h[i + 1] = t1;
-      }
-      const double denom = hypot(h[m], h[m + 1]);
-      const double c = denom == 0.0 ? 1.0 : h[m] / denom;
-      const double s = denom == 0.0 ? 0.0 : h[m + 1] / denom;
-      a.cs[m] = c;
-      a.sn[m] = s;
-      h[m] = denom;
-      h[m + 1] = 0.0;
-      for (int i = 0; i <= m; ++i) a.R[(long long)m * a.ldr + i] = h[i];
-      const double gm = a.g[m];
-      a.g[m] = c * gm;
-      a.g[m + 1] = -s * gm;
-      st.est = fabs(a.g[m + 1]) / a.beta;
+  if (blockIdx.x == 0 && threadIdx.x == 0) mgs_finish(a, hnext, wnorm_pre, reorth, finite, happy);
+}
+
+// The grid MGS with this block's slice of w in shared memory and its slices
+// of the basis columns in registers (E per thread): step i loads V_{i+1} (and,
+// for E <= 8, already V_{i+2} before the barrier, hiding the load behind it),
+// so the only exposed latency per projection is the barrier + fixed-order sum.
+template <int E>
+__global__ void __launch_bounds__(kMgsThreads) mgs_fast_kernel(MgsArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr bool kAhead = E <= 8;
+  extern __shared__ double mgs_ws[];
+  __shared__ double sm[40];
+  const int nb = gridDim.x;
+  const long long chunk = ((a.n + nb - 1) / nb + 31) / 32 * 32;
+  const long long lo = blockIdx.x * chunk;
+  const int len = lo < a.n ? int(min(chunk, a.n - lo)) : 0;
+  int buf = 0;
+  auto publish = [&](double v) {
+    const double s = block_sum(v, sm);
+    if (threadIdx.x == 0) a.partial[buf * nb + blockIdx.x] = s;
+    grid.sync();
+    const double t = grid_total(a.partial + buf * nb, nb, sm);
+    __syncthreads();
+    buf ^= 1;
+    return t;
+  };
+  auto load = [&](const double* V, double (&r)[E]) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int k = threadIdx.x + j * kMgsThreads;
+      r[j] = k < len ? __ldcg(V + lo + k) : 0.0;
     }
-    *a.status = st;
+  };
+  double vc[E], vn[E];
+  // pass 0: w = J z, ||w||^2 and V_0 . w (two partial sets, one barrier)
+  {
+    double n2 = 0.0, d0 = 0.0;
+    load(a.V, vc);
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int k = threadIdx.x + j * kMgsThreads;
+      const double v = k < len ? a.w_in[lo + k] : 0.0;
+      if (k < len) mgs_ws[k] = v;
+      n2 += v * v;
+      d0 += vc[j] * v;
+    }
+    const double s = block_sum(n2, sm);
+    const double t = block_sum(d0, sm);
+    if (threadIdx.x == 0) {
+      a.partial[2 * nb + blockIdx.x] = s;
+      a.partial[3 * nb + blockIdx.x] = t;
+    }
+    if (kAhead && a.m >= 1) load(a.V + a.ldv, vn);
+    grid.sync();
   }
+  const double wnorm_pre = sqrt(grid_total(a.partial + 2 * nb, nb, sm));
+  __syncthreads();
+  const double h0 = grid_total(a.partial + 3 * nb, nb, sm);
+  __syncthreads();
+  if (!isfinite(wnorm_pre)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.status->nonfinite = 1;
+      a.status->wnorm_pre = wnorm_pre;
+    }
+    return;  // uniform across the grid
+  }
+  // one MGS sweep; on entry vc = V_0 slice and (kAhead) vn = V_1 slice
+  auto sweep = [&](double c, bool accumulate) {
+    double nrm2 = 0.0;
+    for (int i = 0; i <= a.m; ++i) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.h[i] = accumulate ? a.h[i] + c : c;
+      const bool last = i == a.m;
+      if (!kAhead && !last) load(a.V + (long long)(i + 1) * a.ldv, vn);
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const int k = threadIdx.x + j * kMgsThreads;
+        if (k < len) {
+          const double wv = mgs_ws[k] - c * vc[j];
+          mgs_ws[k] = wv;
+          acc += last ? wv * wv : vn[j] * wv;
+        }
+      }
+      if (!last) {
+#pragma unroll
+        for (int j = 0; j < E; ++j) vc[j] = vn[j];
+        if (kAhead && i + 2 <= a.m) load(a.V + (long long)(i + 2) * a.ldv, vn);  // behind the barrier
+      }
+      const double t = publish(acc);
+      if (!last)
+        c = t;
+      else
+        nrm2 = t;
+    }
+    return nrm2;
+  };
+  double hnext = sqrt(sweep(h0, false));
+  int reorth = 0;
+  if (hnext < 0.70710678118654752 * wnorm_pre) {  // gmres.cpp:133
+    reorth = 1;
+    load(a.V, vc);
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int k = threadIdx.x + j * kMgsThreads;
+      if (k < len) acc += vc[j] * mgs_ws[k];
+    }
+    if (kAhead && a.m >= 1) load(a.V + a.ldv, vn);
+    const double c = publish(acc);
+    hnext = sqrt(sweep(c, true));
+  }
+  const bool finite = isfinite(hnext);
+  const bool happy = hnext <= 1e-14 * fmax(1.0, wnorm_pre);
+  double* wg = a.V + (long long)(a.m + 1) * a.ldv + lo;
+  for (int k = threadIdx.x; k < len; k += blockDim.x) {
+    const double v = (finite && !happy) ? mgs_ws[k] / hnext : mgs_ws[k];
+    wg[k] = v;
+    if (finite && !happy) a.stage[lo + k] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) mgs_finish(a, hnext, wnorm_pre, reorth, finite, happy);
 }
 
 // y = R(0:m,0:m)^-1 g(0:m)  (gmres.cpp:92-98), one thread; flags a zero pivot

@@ -1,5 +1,2 @@
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 300 python __graft_entry__.py smoke 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
-tail -c 3000 gpurun_out/bench.json
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k gmres 2>&1 | tail -1
+for g in 148 96 64 32; do echo "grid $g"; FRACPREC_B200_MGS_GRID=$g timeout 600 python tools/profile_solve.py 2 tup 200 2>&1 | tail -1; done
