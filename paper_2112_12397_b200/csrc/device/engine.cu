@@ -70,6 +70,14 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s) {
   cuda_check(cudaGetLastError(), "csr_slice_kernel launch");
 }
 
+void launch_coarse(const DenseLUView& F, const double* b, double* x, cudaStream_t s) {
+  if (F.n <= kCoarseWarpN)
+    coarse_warp_kernel<<<1, 32, 0, s>>>(F, b, x);
+  else
+    coarse_solve_kernel<<<1, coarse_threads(F.n), coarse_smem_bytes(F.n), s>>>(F, b, x);
+  cuda_check(cudaGetLastError(), "coarse solve launch");
+}
+
 template <class G, class E>
 void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s) {
   if (L.bsr3)
@@ -354,9 +362,7 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   const double nd = L.n;
   if (l == last) {
     double* out = sub_from ? L.xt.get() : x;
-    coarse_solve_kernel<<<1, coarse_threads(coarse_n), coarse_smem_bytes(coarse_n), s>>>(
-        DenseLUView{coarse_n, coarse_rank, lu.get(), prow.get(), pcol.get()}, b, out);
-    cuda_check(cudaGetLastError(), "coarse_solve_kernel launch");
+    launch_coarse(DenseLUView{coarse_n, coarse_rank, lu.get(), prow.get(), pcol.get()}, b, out, s);
     if (Lg) Lg->add(8.0 * coarse_n * double(coarse_n) + 16.0 * coarse_n + 8.0 * coarse_n);
     if (sub_from) {
       axpy_kernel<<<blocks_for(L.n, 256), 256, 0, s>>>(L.n, sub_from, out, -1.0, x);
@@ -869,8 +875,8 @@ ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int re
   {
     DeviceLevel& C = A.lv.back();
     r.coarse_ms = timed([&] {
-      coarse_solve_kernel<<<1, coarse_threads(A.coarse_n), coarse_smem_bytes(A.coarse_n), s>>>(
-          DenseLUView{A.coarse_n, A.coarse_rank, A.lu.get(), A.prow.get(), A.pcol.get()}, C.b.get(), C.xt.get());
+      launch_coarse(DenseLUView{A.coarse_n, A.coarse_rank, A.lu.get(), A.prow.get(), A.pcol.get()}, C.b.get(),
+                    C.xt.get(), s);
     });
   }
   cudaEventDestroy(e0);

@@ -221,7 +221,15 @@ __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
       const long long len = rb[lane + 1] - rb[lane] - w0;
       const int cnt = len < W ? int(len) : W;
       const double* src = prod + (size_t(buf) * R + lane) * (W + 1);
-      for (int k = 0; k < cnt; ++k) s = s + src[k];
+      int k = 0;
+      for (; k + 8 <= cnt; k += 8) {  // loads batched ahead of the (in-order) add chain
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = src[k + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = s + t[u];
+      }
+      for (; k < cnt; ++k) s = s + src[k];
     }
     buf ^= 1;  // the next window fills the other buffer while warp 0 sums this one
   }
@@ -792,6 +800,35 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_solve_kernel(DenseLUVie
   }
   for (int i = tid; i < n; i += blockDim.x) x[F.pcol[i]] = i < F.rank ? c[i] : 0.0;
 }
+// n <= 64: one warp, no block barriers — rows lane and lane + 32 live in
+// registers, the pivot value travels by shuffle; same operation order as above.
+constexpr int kCoarseWarpN = 64;
+__global__ void __launch_bounds__(32) coarse_warp_kernel(DenseLUView F, const double* b, double* x) {
+  __shared__ double s_lu[kCoarseWarpN * kCoarseWarpN];
+  const int n = F.n, lane = threadIdx.x;
+#pragma unroll 8
+  for (int i = lane; i < n * n; i += 32) s_lu[i] = F.lu[i];
+  double c0 = lane < n ? b[F.prow[lane]] : 0.0;
+  double c1 = lane + 32 < n ? b[F.prow[lane + 32]] : 0.0;
+  __syncwarp();
+  for (int j = 0; j < n; ++j) {
+    const double cj = __shfl_sync(0xffffffffu, j < 32 ? c0 : c1, j & 31);
+    const double* col = s_lu + j * n;
+    if (lane > j && lane < n) c0 -= col[lane] * cj;
+    if (lane + 32 > j && lane + 32 < n) c1 -= col[lane + 32] * cj;
+  }
+  for (int j = F.rank - 1; j >= 0; --j) {
+    const double xj = __shfl_sync(0xffffffffu, j < 32 ? c0 : c1, j & 31) / s_lu[j * n + j];
+    if (lane == j) c0 = xj;
+    if (lane + 32 == j) c1 = xj;
+    const double* col = s_lu + j * n;
+    if (lane < j) c0 -= col[lane] * xj;
+    if (lane + 32 < j) c1 -= col[lane + 32] * xj;
+  }
+  if (lane < n) x[F.pcol[lane]] = lane < F.rank ? c0 : 0.0;
+  if (lane + 32 < n) x[F.pcol[lane + 32]] = lane + 32 < F.rank ? c1 : 0.0;
+}
+
 inline int coarse_threads(int n) {  // small coarse systems: fewer threads, cheaper barriers
   const int t = (n + 31) / 32 * 32;
   return t < 32 ? 32 : (t > kCoarseThreads ? kCoarseThreads : t);

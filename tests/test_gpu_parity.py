@@ -296,3 +296,22 @@ def test_theta0_gmres_matches_oracle_and_history(factor_solve):
     k = min(len(st.relative_residuals), len(st_ref["history"])) - 1
     h, hr = np.array(st.relative_residuals[:k]), st_ref["history"][:k]
     assert np.all(np.abs(np.log10(h) - np.log10(hr)) < 0.5)
+
+
+@pytest.mark.parametrize("max_levels,coarse_n", [(2, 206), (3, 158), (10, None)])
+def test_coarse_solve_paths_bitwise(max_levels, coarse_n):
+    """Coarse LU solve: one warp (n <= 64), a CTA with the factor in shared memory
+    (n <= 160) and from global memory (n > 160) — all in the oracle's order."""
+    J = small_workload(seed=7)
+    osys = oracle_system(J)
+    amg = api.AmgConfig(max_levels=max_levels)
+    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, **amg_kw(amg))
+    n_c = opc.level_matrix(opc.n_levels() - 1, 0)[0]
+    if coarse_n is not None:
+        assert n_c == coarse_n
+    else:
+        assert n_c <= 64
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, "tup", amg)
+    r = np.random.default_rng(21).uniform(-1, 1, J.n_u)
+    assert np.array_equal(pc.amg_apply(r), opc.amg_apply(r))

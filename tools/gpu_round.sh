@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k gmres 2>&1 | tail -1
-for g in 148 96 64 32; do echo "grid $g"; FRACPREC_B200_MGS_GRID=$g timeout 600 python tools/profile_solve.py 2 tup 200 2>&1 | tail -1; done
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 600 python tools/profile_solve.py 2 tup 500 2>&1 | tail -1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_solve_cfg2.csv python tools/profile_solve.py 2 tup 50 > gpurun_out/ncus.log 2>&1
