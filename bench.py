@@ -89,7 +89,7 @@ def dist_env():
 
 def ncu_traffic(key: str):
     """dram read+write bytes per launch of `key` from the committed ncu --set full capture (or None)."""
-    p = os.path.join(ROOT, "profiles", "round1", "ncu_full_bsr3.json")
+    p = os.path.join(ROOT, "profiles", "round1", "ncu_full_cfg2.json")
     try:
         k = json.load(open(p))["kernels"][key]
         return k["dram_bytes_read"] + k["dram_bytes_write"]
@@ -329,7 +329,7 @@ def run_ours(args):
                          "achieved": round(fine_gbs, 1) if fine_gbs else None, "peak": hbm, "unit": "GB/s",
                          "frac": round(fine_gbs / hbm, 3) if fine_gbs else None,
                          "traffic": ncu_traffic("bsr3_EJacobi"),
-                         "traffic_source": "profiles/round1/ncu_full_bsr3.json (dram__bytes_read+write per launch)",
+                         "traffic_source": "profiles/round1/ncu_full_cfg2.json (dram__bytes_read+write per launch)",
                          "peak_source": peak_src, "algorithmic_bytes_per_launch": prof["fine_post_bytes"],
                          "avg_launch_ms": round(prof["fine_post_ms"], 4)},
             "precond_apply": {"GBps": round(apply_gbs, 1), "frac": round(apply_gbs / hbm, 3),

@@ -1,3 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 600 python tools/profile_solve.py 2 tup 500 2>&1 | tail -1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launch_solve_cfg2.csv python tools/profile_solve.py 2 tup 50 > gpurun_out/ncus.log 2>&1
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo "ncu list rc=$?"
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"bsr3|dinv|csr_pipe|mgs_fast" -s 40 -c 14 -o gpurun_out/full_cfg2 -f python tools/profile_solve.py 2 tup 30 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
