@@ -48,6 +48,10 @@ int fp_workload_system(const fp_workload* w, fp_block_system* J);
 int fp_workload_coords(const fp_workload* w, const double** xyz, int32_t* n_nodes);
 /* counts[0..3] = stick, slip, open, fractures */
 int fp_workload_info(const fp_workload* w, int32_t* counts);
+/* build_tpu / build_tup (precond.cpp:119-202) on the generated system and node
+ * coordinates in place — fp_host_precond_build without copying the blocks
+ * (the large configs' fine operator is tens of GB on the host) */
+int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config* cfg, fp_host_precond** out);
 
 #ifdef __cplusplus
 }

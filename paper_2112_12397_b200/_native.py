@@ -127,6 +127,7 @@ SIGNATURES = {
     "fp_workload_system": (C.c_int, [_P, C.POINTER(FpBlockSystem)]),
     "fp_workload_coords": (C.c_int, [_P, C.POINTER(_DP), C.POINTER(C.c_int32)]),
     "fp_workload_info": (C.c_int, [_P, C.POINTER(C.c_int32)]),
+    "fp_workload_host_precond_build": (C.c_int, [_P, C.POINTER(FpPrecondConfig), _PP]),
 }
 
 

@@ -213,13 +213,21 @@ class BlockSystemOperator:
 class HostPreconditioner:
     """Host-built preconditioner data (build_tpu / build_tup, precond.cpp:119-202)."""
 
-    def __init__(self, J: BlockSystem, cfg: PrecondConfig):
+    def __init__(self, J: Optional[BlockSystem], cfg: PrecondConfig, _workload: "Optional[Workload]" = None):
         self._h = C.c_void_p()
+        self.variant = cfg.variant
+        if _workload is not None:  # from_workload: no copy of the blocks
+            N.check(N.lib.fp_workload_host_precond_build(_workload._h, C.byref(cfg.native()), C.byref(self._h)))
+            return
         coords = None if J.node_coords is None else np.ascontiguousarray(J.node_coords, dtype=np.float64)
         cp = coords.ctypes.data_as(C.POINTER(C.c_double)) if coords is not None else None
         nn = 0 if coords is None else coords.shape[0]
         N.check(N.lib.fp_host_precond_build(C.byref(J.view()), C.byref(cfg.native()), cp, nn, C.byref(self._h)))
-        self.variant = cfg.variant
+
+    @classmethod
+    def from_workload(cls, W: "Workload", cfg: PrecondConfig) -> "HostPreconditioner":
+        """build_tpu / build_tup on a generated workload in place (fp_workload_host_precond_build)."""
+        return cls(None, cfg, _workload=W)
 
     def __del__(self):
         if getattr(self, "_h", None) and N is not None and getattr(N, "lib", None) is not None:
@@ -419,18 +427,26 @@ class Workload:
         N.check(N.lib.fp_workload_info(self._h, c))
         return {"stick": c[0], "slip": c[1], "open": c[2], "fractures": c[3]}
 
-    def system(self) -> BlockSystem:
-        """Copies the generated blocks into an owned BlockSystem (NumPy)."""
+    def system(self, copy: bool = True) -> BlockSystem:
+        """The generated blocks as a BlockSystem: owned NumPy copies, or (copy=False) read-only
+        views into the workload's arrays that keep the Workload alive."""
         v = N.FpBlockSystem()
         N.check(N.lib.fp_workload_system(self._h, C.byref(v)))
+
+        def arr(p, n, dtype):
+            a = np.ctypeslib.as_array(p, shape=(n,))
+            if copy:
+                return a.copy()
+            a.flags.writeable = False
+            return a
 
         def take(m: N.FpCsr) -> CsrMatrix:
             if m.n_rows == 0:
                 return CsrMatrix.empty(0, m.n_cols)
-            rp = np.ctypeslib.as_array(m.row_offsets64, shape=(m.n_rows + 1,)).copy()
+            rp = arr(m.row_offsets64, m.n_rows + 1, np.int64)
             nz = int(rp[-1])
-            ci = np.ctypeslib.as_array(m.col_indices, shape=(nz,)).copy() if nz else np.zeros(0, np.int32)
-            vv = np.ctypeslib.as_array(m.values, shape=(nz,)).copy() if nz else np.zeros(0)
+            ci = arr(m.col_indices, nz, np.int32) if nz else np.zeros(0, np.int32)
+            vv = arr(m.values, nz, np.float64) if nz else np.zeros(0)
             return CsrMatrix(m.n_rows, m.n_cols, rp, ci, vv)
 
         xyz = C.POINTER(C.c_double)()
@@ -438,4 +454,7 @@ class Workload:
         N.check(N.lib.fp_workload_coords(self._h, C.byref(xyz), C.byref(nn)))
         coords = np.ctypeslib.as_array(xyz, shape=(nn.value * 3,)).copy().reshape(-1, 3) if nn.value else None
         blocks = {nm: take(getattr(v, nm)) for nm in ("A", "C1", "Q1", "C2", "H", "Q2", "T", "F_u")}
-        return BlockSystem(v.n_u, v.n_t, v.n_p, node_coords=coords, **blocks)
+        J = BlockSystem(v.n_u, v.n_t, v.n_p, node_coords=coords, **blocks)
+        if not copy:
+            J._owner = self  # the views point into this workload
+        return J

@@ -306,7 +306,6 @@ int fp_precond_upload(fp_system* s, const fp_precond_desc* d, fp_precond** out) 
     }
     const fpb::Csr& Ac = hp.amg.levels.back().A;
     hp.amg.coarse.compute(Ac.to_dense(), Ac.n_rows);
-    hp.S = hp.amg.levels.front().A;
     auto p = std::make_unique<fp_precond>();
     p->sys = s;
     p->dev = std::make_unique<fpd::DevicePrecond>(*s->dev, hp);
@@ -496,6 +495,17 @@ int fp_workload_coords(const fp_workload* w, const double** xyz, int32_t* n_node
     need(w && xyz && n_nodes, "null argument");
     *xyz = w->w.coords.empty() ? nullptr : w->w.coords[0].data();
     *n_nodes = int32_t(w->w.coords.size());
+  });
+}
+
+int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config* cfg, fp_host_precond** out) {
+  return guard([&] {
+    need(w && cfg && out, "fp_workload_host_precond_build: null argument");
+    need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
+    auto p = std::make_unique<fp_host_precond>();
+    p->hp = fpb::build_precond(w->w.J, cfg->variant, to_amg(cfg->amg), w->w.coords);
+    p->hp.factor_solve = cfg->factor_solve;
+    *out = p.release();
   });
 }
 

@@ -448,7 +448,7 @@ void DeviceAmg::enqueue_apply(const double* r, double* x, const double* sub_from
 
 // --------------------------------------------------------------- precond
 DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) : variant(hp.variant), sys(&s) {
-  if (hp.S.n_rows != s.n_u) throw std::invalid_argument("precond upload: inner operator size != n_u");
+  if (hp.amg.levels.empty() || hp.S().n_rows != s.n_u) throw std::invalid_argument("precond upload: inner operator size != n_u");
   if (int(hp.hblocks.size()) != 9 * s.n_p) throw std::invalid_argument("precond upload: H~ blocks size != 9 n_p");
   amg = std::make_unique<DeviceAmg>(hp.amg, true);
   // pre-factor the H~ blocks with the reference's lu3_factor (deterministic)

@@ -58,12 +58,13 @@ Csr build_rows(int n_rows, int n_cols, MakeScratch make_scratch, RowFn fn) {
       C.rp[size_t(c) * kChunk + q + 1] = acc;
     }
   }
-  C.ci.resize(static_cast<size_t>(chunk_off[n_chunks]));
-  C.v.resize(static_cast<size_t>(chunk_off[n_chunks]));
-#pragma omp parallel for schedule(dynamic, 1)
+  // append chunk by chunk into reserved (untouched) storage, releasing each piece
+  // right after: the peak is one output plus one piece, not two outputs
+  C.ci.reserve(static_cast<size_t>(chunk_off[n_chunks]));
+  C.v.reserve(static_cast<size_t>(chunk_off[n_chunks]));
   for (int c = 0; c < n_chunks; ++c) {
-    std::copy(pieces[c].cols.begin(), pieces[c].cols.end(), C.ci.begin() + chunk_off[c]);
-    std::copy(pieces[c].vals.begin(), pieces[c].vals.end(), C.v.begin() + chunk_off[c]);
+    C.ci.insert(C.ci.end(), pieces[c].cols.begin(), pieces[c].cols.end());
+    C.v.insert(C.v.end(), pieces[c].vals.begin(), pieces[c].vals.end());
     std::vector<int>().swap(pieces[c].cols);
     std::vector<double>().swap(pieces[c].vals);
   }
@@ -170,8 +171,10 @@ Csr transpose(const Csr& A) {
 }
 
 // Row-by-row Gustavson product with a dense accumulator (csr.cpp:149-179).
-Csr spgemm(const Csr& A, const Csr& B) {
+Csr spgemm(const Csr& A, const Csr& B, std::span<const double> row_scale) {
   need(A.n_cols == B.n_rows, "spgemm: dimension mismatch");
+  need(row_scale.empty() || int64_t(row_scale.size()) == A.n_rows, "spgemm: row scale length mismatch");
+  const bool scaled = !row_scale.empty();
   struct Acc {
     std::vector<double> acc;
     std::vector<char> seen;
@@ -190,7 +193,8 @@ Csr spgemm(const Csr& A, const Csr& B) {
         s.touched.clear();
         for (int64_t ka = A.rp[i]; ka < A.rp[i + 1]; ++ka) {
           const int k = A.ci[ka];
-          const double av = A.v[ka];
+          // scaled: the entries of scale_rows(A, row_scale), rounded the same way, without the copy
+          const double av = scaled ? A.v[ka] * row_scale[i] : A.v[ka];
           for (int64_t kb = B.rp[k]; kb < B.rp[k + 1]; ++kb) {
             const int j = B.ci[kb];
             if (!s.seen[j]) {

@@ -41,7 +41,8 @@ struct Csr {
 
 std::vector<double> spmv(const Csr& A, std::span<const double> x);
 Csr transpose(const Csr& A);
-Csr spgemm(const Csr& A, const Csr& B);
+// C = diag(row_scale) A B when row_scale is given (== spgemm(scale_rows(A, s), B) bitwise)
+Csr spgemm(const Csr& A, const Csr& B, std::span<const double> row_scale = {});
 Csr add_scaled(const Csr& A, const Csr& B, double alpha, double beta);
 Csr scale_rows(const Csr& A, std::span<const double> s);
 std::vector<double> diag_extract(const Csr& A);

@@ -9,6 +9,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <tuple>
 #include <cmath>
 #include <cstdio>
 #include <deque>
@@ -27,7 +28,13 @@ struct PhaseLog {
   void mark(const char* what, long a = -1, long b = -1) {
     if (!on) return;
     const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[setup] %-28s %8.3f s  %ld %ld\n", what, std::chrono::duration<double>(now - t).count(), a, b);
+    long pages = 0, rss = 0;
+    if (FILE* f = std::fopen("/proc/self/statm", "r")) {
+      if (std::fscanf(f, "%ld %ld", &pages, &rss) != 2) rss = 0;
+      std::fclose(f);
+    }
+    std::fprintf(stderr, "[setup] %-28s %8.3f s  %ld %ld  rss %.1f GB\n", what,
+                 std::chrono::duration<double>(now - t).count(), a, b, double(rss) * 4096.0 / 1e9);
     t = now;
   }
 };
@@ -203,7 +210,7 @@ int qr_colpiv(int m, int k, const std::vector<double>& B, std::vector<double>& Q
   return rank;
 }
 
-HostAmg amg_setup(const Csr& A, const std::vector<std::vector<double>>& near_null, const AmgOptions& opt) {
+HostAmg amg_setup(Csr A, const std::vector<std::vector<double>>& near_null, const AmgOptions& opt) {
   if (A.n_rows != A.n_cols) throw std::invalid_argument("amg_setup: matrix must be square");
   if (!(opt.strength_threshold >= 0.0 && opt.strength_threshold < 1.0))
     throw std::invalid_argument("amg_setup: strength_threshold must be in [0,1)");
@@ -216,8 +223,8 @@ HostAmg amg_setup(const Csr& A, const std::vector<std::vector<double>>& near_nul
     if (int(v.size()) != A.n_rows) throw std::invalid_argument("amg_setup: near-null vector length mismatch");
   {
     HostLevel f;
-    f.A = A;
     f.diag = diag_extract(A);
+    f.A = std::move(A);
     h.levels.push_back(std::move(f));
   }
   PhaseLog plog;
@@ -228,9 +235,13 @@ HostAmg amg_setup(const Csr& A, const std::vector<std::vector<double>>& near_nul
       if (fine.diag[i] == 0.0) throw numerical_error("amg_setup: zero diagonal entry at row " + std::to_string(i));
     if (n <= opt.max_coarse || int(h.levels.size()) >= opt.max_levels) break;
     plog.mark("level start", n, long(fine.A.nnz()));
-    const Strength g = build_strength(fine.A, opt.strength_threshold);
-    plog.mark("strength", long(g.nbr.size()));
-    auto [agg, n_agg] = aggregate(g, n);
+    std::vector<int> agg;
+    int n_agg = 0;
+    {  // the strength graph lives only for the aggregation
+      const Strength g = build_strength(fine.A, opt.strength_threshold);
+      plog.mark("strength", long(g.nbr.size()));
+      std::tie(agg, n_agg) = aggregate(g, n);
+    }
     plog.mark("aggregate", n_agg);
     if (n_agg == 0) break;
     const int k = int(nn.size());
@@ -291,8 +302,7 @@ HostAmg amg_setup(const Csr& A, const std::vector<std::vector<double>>& near_nul
     if (opt.prolongation_smoothing) {
       std::vector<double> dinv(static_cast<size_t>(n));
       for (int i = 0; i < n; ++i) dinv[i] = 1.0 / fine.diag[i];
-      const Csr DA = scale_rows(fine.A, dinv);
-      P = add_scaled(P, spgemm(DA, P), 1.0, -opt.jacobi_omega);
+      P = add_scaled(P, spgemm(fine.A, P, dinv), 1.0, -opt.jacobi_omega);  // P - w D^-1 A P
     }
     plog.mark("smoothed P", long(P.nnz()));
     if (nc > opt.stall_ratio * n) break;
@@ -397,10 +407,12 @@ HostPrecond build_precond(const HostSystem& J, int variant, const AmgOptions& op
   J.check_shapes();
   if (variant < kTpu || variant > kTupStar) throw std::invalid_argument("build_precond: unknown variant");
   HostPrecond M;
+  PhaseLog plog;
   M.variant = variant;
   M.hblocks = bdiag3_extract(J.H);
   const Csr HinvC2 = spgemm(bdiag3_inverse_csr(M.hblocks), J.C2);
-  const Csr core = add_scaled(J.A, spgemm(J.C1, HinvC2), 1.0, 1.0);
+  Csr core = add_scaled(J.A, spgemm(J.C1, HinvC2), 1.0, 1.0);
+  plog.mark("schur core", long(core.nnz()));
   std::vector<std::vector<double>> nn;
   if (!coords.empty() && int(coords.size()) * 3 == J.n_u) nn = rigid_body_modes(coords);
   if (variant == kTpu) {
@@ -410,12 +422,13 @@ HostPrecond build_precond(const HostSystem& J, int variant, const AmgOptions& op
     M.factor.factor(J.T, BandFactor::Kind::spd);
     std::vector<double> tinv(M.T_diag.size());
     for (size_t i = 0; i < tinv.size(); ++i) tinv[i] = 1.0 / M.T_diag[i];
-    M.S = add_scaled(core, spgemm(J.Q1, scale_rows(J.Q2, tinv)), 1.0, -1.0);
-    M.amg = amg_setup(M.S, nn, opt);
+    Csr S = add_scaled(core, spgemm(J.Q1, scale_rows(J.Q2, tinv)), 1.0, -1.0);
+    core = Csr();  // free the fine-size temporary before the hierarchy is built
+    M.amg = amg_setup(std::move(S), nn, opt);
   } else {
-    M.S = core;
-    M.amg = amg_setup(M.S, nn, opt);
-    M.S_K = fixed_stress_diag(J.Q2, M.S, J.Q1);
+    M.amg = amg_setup(std::move(core), nn, opt);
+    M.S_K = fixed_stress_diag(J.Q2, M.S(), J.Q1);
+    plog.mark("fixed stress");
     std::vector<Csr::Triplet> sk;
     for (int k = 0; k < J.n_p; ++k)
       if (M.S_K[k] != 0.0) sk.push_back({k, k, M.S_K[k]});

@@ -39,7 +39,8 @@ struct HostAmg {
   AmgOptions opt;
 };
 
-HostAmg amg_setup(const Csr& A, const std::vector<std::vector<double>>& near_null, const AmgOptions& opt);
+// A is taken by value and moved into level 0 (callers std::move the inner operator in)
+HostAmg amg_setup(Csr A, const std::vector<std::vector<double>>& near_null, const AmgOptions& opt);
 std::vector<std::vector<double>> rigid_body_modes(const std::vector<std::array<double, 3>>& coords);
 int qr_colpiv(int m, int k, const std::vector<double>& B_colmajor, std::vector<double>& Q, std::vector<double>& Rp);
 
@@ -55,7 +56,8 @@ struct HostPrecond {
   int variant = kTup;
   std::vector<double> hblocks;  // regularized H~ = Bdiag(H,3), 9 per face
   std::vector<double> T_diag;   // t-p-u
-  Csr S;                        // S~ (t-p-u) or S1 (t-u-p): the inner AMG operator
+  // the inner AMG operator S~ (t-p-u) or S1 (t-u-p) is amg.levels[0].A
+  const Csr& S() const { return amg.levels.front().A; }
   HostAmg amg;
   std::vector<double> S_K;      // t-u-p fixed-stress diagonal
   Csr S2;                       // t-u-p S~2 = T - diag(S_K)

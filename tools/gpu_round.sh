@@ -1,4 +1,8 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
-timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo "ncu list rc=$?"
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"bsr3|dinv|csr_pipe|mgs_fast" -s 40 -c 14 -o gpurun_out/full_cfg2 -f python tools/profile_solve.py 2 tup 30 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+grep -E "MemTotal|MemAvailable" /proc/meminfo; nproc
+avail_gb=$(awk '/MemAvailable/ {print int($2/1000/1000)}' /proc/meminfo)
+limit=$(( avail_gb - 20 ))
+echo "limit ${limit} GB"
+FRACPREC_B200_VERBOSE=1 LIMIT_GB=$limit timeout 2700 tools/watchdog.sh python tools/big_config.py 5 30 > gpurun_out/big5.json 2> gpurun_out/big5.err
+echo "rc=$?"
+tail -1 gpurun_out/big5.json; grep -E "watchdog|rss" gpurun_out/big5.err | tail -12
