@@ -52,6 +52,16 @@ int fp_workload_info(const fp_workload* w, int32_t* counts);
  * coordinates in place — fp_host_precond_build without copying the blocks
  * (the large configs' fine operator is tens of GB on the host) */
 int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config* cfg, fp_host_precond** out);
+/* per-face contact state ('s' stick, 'l' slip, 'o' open; Snapshot::region_string, snapshot.cpp:20-25)
+ * and the time step; the string is valid until destroy */
+int fp_workload_region(const fp_workload* w, const char** region, double* dt);
+
+/* ---- snapshot bundle (snapshot.cpp:28-104, mmio.cpp:15-76): manifest.json + Matrix Market blocks */
+/* import_snapshot: the bundle in `dir` as a workload handle (system views, coords, region, dt) */
+int fp_snapshot_import(const char* dir, fp_workload** out);
+/* export_snapshot: region = n_p characters s/l/o; node_coords may be null (n_nodes = 0) */
+int fp_snapshot_export(const char* dir, const fp_block_system* J, const char* region, double dt,
+                       const double* node_coords, int32_t n_nodes);
 
 #ifdef __cplusplus
 }

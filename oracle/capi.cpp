@@ -136,6 +136,21 @@ int or_system_apply(void* s, const double* x, double* y) {
 }
 
 // -------------------------------------------------------------------- CSR
+// Matrix Market (mmio.cpp:15-59): the CSR handle is owned by the caller (or_csr_destroy)
+int or_mm_read(const char* path, void** out) {
+  return guard([&] { *out = new CsrMatrix(read_matrix_market(path)); });
+}
+void or_csr_destroy(void* m) { delete static_cast<CsrMatrix*>(m); }
+int or_mm_write(const char* path, int rows, int cols, const int64_t* rp, const int* ci, const double* v) {
+  return guard([&] {
+    CsrMatrix A(rows, cols);
+    A.row_offsets.assign(rp, rp + rows + 1);
+    A.col_indices.assign(ci, ci + rp[rows]);
+    A.values.assign(v, v + rp[rows]);
+    write_matrix_market(path, A);
+  });
+}
+
 int or_csr_info(const void* m, int* rows, int* cols, int64_t* nnz) {
   const auto* M = static_cast<const CsrMatrix*>(m);
   if (!M) return 1;

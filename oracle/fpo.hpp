@@ -75,6 +75,10 @@ struct CsrMatrix {
   std::vector<double> to_dense() const;  // row-major
 };
 
+// mmio.hpp (snapshot bundle blocks): oracle/mmio.cpp
+CsrMatrix read_matrix_market(const std::string& path);
+void write_matrix_market(const std::string& path, const CsrMatrix& A);
+
 // csr.hpp:52-58
 struct BlockDiagonal3 {
   int n_blocks = 0;

@@ -393,9 +393,12 @@ def gmres(op: BlockSystemOperator, precond: GpuPreconditioner, b, tol: float, ma
 class Workload:
     """Synthetic BASELINE config (include/fracprec_b200_workload.h)."""
 
-    def __init__(self, config_id: Optional[int] = None, seed: int = 42, spec: Optional[dict] = None):
+    def __init__(self, config_id: Optional[int] = None, seed: int = 42, spec: Optional[dict] = None,
+                 _handle: Optional[C.c_void_p] = None):
         self._h = C.c_void_p()
-        if spec is None:
+        if _handle is not None:
+            self._h = _handle
+        elif spec is None:
             N.check(N.lib.fp_workload_preset(int(config_id), seed, C.byref(self._h)))
         else:
             s = N.FpWorkloadSpec()
@@ -421,6 +424,24 @@ class Workload:
         if getattr(self, "_h", None) and N is not None and getattr(N, "lib", None) is not None:
             N.lib.fp_workload_destroy(self._h)
             self._h = None
+
+    @classmethod
+    def from_snapshot(cls, directory: str) -> "Workload":
+        """import_snapshot (snapshot.cpp:67-104): a reference snapshot bundle as a workload."""
+        h = C.c_void_p()
+        N.check(N.lib.fp_snapshot_import(str(directory).encode(), C.byref(h)))
+        return cls(_handle=h)
+
+    def region(self) -> tuple:
+        """(per-face labels 's'/'l'/'o', dt)"""
+        r, dt = C.c_char_p(), C.c_double()
+        N.check(N.lib.fp_workload_region(self._h, C.byref(r), C.byref(dt)))
+        return r.value.decode(), dt.value
+
+    def save_snapshot(self, directory: str) -> None:
+        """export_snapshot of this workload (blocks, region labels, dt, node coordinates)."""
+        region, dt = self.region()
+        export_snapshot(directory, self.system(copy=False), region, dt)
 
     def info(self) -> dict:
         c = (C.c_int32 * 4)()
@@ -458,3 +479,11 @@ class Workload:
         if not copy:
             J._owner = self  # the views point into this workload
         return J
+
+
+def export_snapshot(directory: str, J: BlockSystem, region: str, dt: float = 0.5) -> None:
+    """export_snapshot (snapshot.cpp:28-65): manifest.json + Matrix Market blocks (+ coords.txt)."""
+    coords = None if J.node_coords is None else np.ascontiguousarray(J.node_coords, dtype=np.float64)
+    cp = coords.ctypes.data_as(C.POINTER(C.c_double)) if coords is not None else None
+    nn = 0 if coords is None else coords.shape[0]
+    N.check(N.lib.fp_snapshot_export(str(directory).encode(), C.byref(J.view()), region.encode(), float(dt), cp, nn))

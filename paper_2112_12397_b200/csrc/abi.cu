@@ -12,6 +12,7 @@
 #include "../../include/fracprec_b200_workload.h"
 #include "device/engine.cuh"
 #include "host/setup.hpp"
+#include "host/snapshot.hpp"
 #include "host/workload.hpp"
 
 namespace {
@@ -506,6 +507,35 @@ int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config
     p->hp = fpb::build_precond(w->w.J, cfg->variant, to_amg(cfg->amg), w->w.coords);
     p->hp.factor_solve = cfg->factor_solve;
     *out = p.release();
+  });
+}
+
+int fp_workload_region(const fp_workload* w, const char** region, double* dt) {
+  return guard([&] {
+    need(w && region && dt, "null argument");
+    *region = w->w.region.c_str();
+    *dt = w->w.dt;
+  });
+}
+
+int fp_snapshot_import(const char* dir, fp_workload** out) {
+  return guard([&] {
+    need(dir && out, "fp_snapshot_import: null argument");
+    auto p = std::make_unique<fp_workload>();
+    p->w = fpb::import_snapshot(dir);
+    *out = p.release();
+  });
+}
+
+int fp_snapshot_export(const char* dir, const fp_block_system* J, const char* region, double dt,
+                       const double* node_coords, int32_t n_nodes) {
+  return guard([&] {
+    need(dir && J && region, "fp_snapshot_export: null argument");
+    const fpb::HostSystem H = to_system(*J);
+    std::vector<std::array<double, 3>> xyz;
+    for (int v = 0; node_coords && v < n_nodes; ++v)
+      xyz.push_back({node_coords[3 * v], node_coords[3 * v + 1], node_coords[3 * v + 2]});
+    fpb::export_snapshot(dir, H, std::string(region, strnlen(region, size_t(H.n_p) + 1)), dt, xyz);
   });
 }
 

@@ -422,6 +422,9 @@ Workload generate_workload(const WorkloadSpec& s) {
       }
     }
     for (Region q : region) (q == Region::stick ? W.n_stick : q == Region::slip ? W.n_slip : W.n_open)++;
+    W.region.reserve(region.size());
+    for (Region q : region) W.region.push_back(q == Region::stick ? 's' : q == Region::slip ? 'l' : 'o');
+    W.dt = s.dt;
   }
 
   // ---- coupling C1, Q1 (assembly.cpp:190-216)

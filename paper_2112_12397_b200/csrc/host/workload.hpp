@@ -8,6 +8,7 @@
 
 #include <array>
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "setup.hpp"
@@ -47,6 +48,8 @@ struct Workload {
   std::vector<std::array<double, 3>> coords;
   int n_stick = 0, n_slip = 0, n_open = 0, n_fractures = 0;
   double k_scale = 0.0;
+  std::string region;  // per face 's' stick, 'l' slip, 'o' open (Snapshot::region_string, snapshot.cpp:20-25)
+  double dt = 0.5;
 };
 
 WorkloadSpec preset_config(int config_id, uint64_t seed);  // BASELINE.json configs[0..4] as 1..5

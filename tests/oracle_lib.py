@@ -54,6 +54,9 @@ def _load():
         "or_amg_apply": (C.c_int, [P, DP, DP]),
         "or_gmres": (C.c_int, [P, P, DP, C.c_double, C.c_int, C.c_int, C.c_int, DP, IP, DP, C.c_int, DP]),
         "or_block_scaling": (C.c_int, [P, DP]),
+        "or_mm_read": (C.c_int, [C.c_char_p, PP]),
+        "or_csr_destroy": (None, [P]),
+        "or_mm_write": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_int64), IP, DP]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -231,3 +234,21 @@ def oracle_gmres(sys: OracleSystem, pc, b, tol=1e-10, restart=50, max_iter=500, 
                         st.ctypes.data_as(C.POINTER(C.c_int)), _dp(hist), hist.size, _dp(secs)))
     return x, dict(iterations=int(st[0]), converged=bool(st[1]), breakdown=bool(st[2]), restarts=int(st[3]),
                    precond_applies=int(st[4]), history=hist[: st[0]].copy(), seconds=float(secs[0]))
+
+
+def mm_read(path: str) -> tuple:
+    """read_matrix_market (mmio.cpp:15-48) restated: (rows, cols, rp, ci, v)."""
+    h = C.c_void_p()
+    _check(lib.or_mm_read(str(path).encode(), C.byref(h)))
+    try:
+        return csr_from(h)
+    finally:
+        lib.or_csr_destroy(h)
+
+
+def mm_write(path: str, rows: int, cols: int, rp, ci, v) -> None:
+    rp = np.ascontiguousarray(rp, np.int64)
+    ci = np.ascontiguousarray(ci, np.int32)
+    v = np.ascontiguousarray(v, np.float64)
+    _check(lib.or_mm_write(str(path).encode(), rows, cols, rp.ctypes.data_as(C.POINTER(C.c_int64)),
+                           ci.ctypes.data_as(C.POINTER(C.c_int)), _dp(v)))
