@@ -93,6 +93,16 @@ struct GmresStatus {
   int happy, nonfinite, reorth, m;
 };
 
+// Programmatic dependent launch: every kernel of the apply first waits for its
+// predecessor grid to complete (and its writes to be visible), then lets the
+// next grid in the stream launch.  The successor's CTAs are scheduled into this
+// grid's tail instead of after a full drain + launch gap.  Without a programmatic
+// dependency (ordinary launches) both instructions return immediately.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- buffers
 void cuda_check(cudaError_t e, const char* what);
 

@@ -14,6 +14,26 @@
 
 namespace fpd {
 
+// Kernels of the solve path can be launched with programmatic stream
+// serialization (see pdl_entry).  Measured on config 2 it is slower (0.80 vs
+// 0.66 ms per GMRES iteration: successor CTAs parked in griddepcontrol.wait hold
+// SM slots the running grid needs), so it is opt-in: FRACPREC_B200_PDL=1.
+bool pdl_enabled() {
+  static const bool on = std::getenv("FRACPREC_B200_PDL") != nullptr;
+  return on;
+}
+
+template <class... P, class... A>
+void launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, const char* what, A&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid, cfg.blockDim = block, cfg.dynamicSmemBytes = smem, cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at, cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cuda_check(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...), what);
+}
+
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
@@ -35,14 +55,14 @@ int sm_count() {
 template <class G, class E>
 void launch_sell(const DSell& A, const G& g, const E& e, cudaStream_t s) {
   if (A.n_rows == 0) return;
-  sell_kernel<<<blocks_for(A.n_rows, 256), 256, 0, s>>>(A.view(), g, e);
+  launch(sell_kernel<G, E>, dim3(blocks_for(A.n_rows, 256)), dim3(256), 0, s, "sell_kernel", A.view(), g, e);
   cuda_check(cudaGetLastError(), "sell_kernel launch");
 }
 
 template <class G, class E>
 void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s) {
   if (A.n_brows == 0) return;
-  bsr3_kernel<<<blocks_for((long long)A.n_slices * 96, kBsrThreads), kBsrThreads, 0, s>>>(A.view(), g, e);
+  launch(bsr3_kernel<G, E>, dim3(blocks_for((long long)A.n_slices * 96, kBsrThreads)), dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
   cuda_check(cudaGetLastError(), "bsr3_kernel launch");
 }
 
@@ -60,21 +80,21 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s) {
       return true;
     }();
     (void)smem_set;
-    csr_pipe_kernel<<<unsigned(A.pm.n_ctas), kPipeThreads, kPipeSmem, s>>>(A.pm.view(), g, e);
+    launch(csr_pipe_kernel<G, E>, dim3(unsigned(A.pm.n_ctas)), dim3(kPipeThreads), kPipeSmem, s, "csr_pipe_kernel", A.pm.view(), g, e);
     cuda_check(cudaGetLastError(), "csr_pipe_kernel launch");
     return;
   }
   if (A.csr.n_rows == 0) return;
   else
-    csr_slice_kernel<2, 1024><<<blocks_for(A.csr.n_rows, 2), 256, 0, s>>>(A.csr.view(), g, e);
+    launch(csr_slice_kernel<2, 1024, G, E>, dim3(blocks_for(A.csr.n_rows, 2)), dim3(256), 0, s, "csr_slice_kernel", A.csr.view(), g, e);
   cuda_check(cudaGetLastError(), "csr_slice_kernel launch");
 }
 
 void launch_coarse(const DenseLUView& F, const double* b, double* x, cudaStream_t s) {
   if (F.n <= kCoarseWarpN)
-    coarse_warp_kernel<<<1, 32, 0, s>>>(F, b, x);
+    launch(coarse_warp_kernel, dim3(1), dim3(32), 0, s, "coarse_warp_kernel", F, b, x);
   else
-    coarse_solve_kernel<<<1, coarse_threads(F.n), coarse_smem_bytes(F.n), s>>>(F, b, x);
+    launch(coarse_solve_kernel, dim3(1), dim3(coarse_threads(F.n)), coarse_smem_bytes(F.n), s, "coarse_solve_kernel", F, b, x);
   cuda_check(cudaGetLastError(), "coarse solve launch");
 }
 
@@ -158,7 +178,7 @@ DPipe make_pipe(const fpb::Csr& A) {
   int dev = 0, sms = 148;
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
-  D.n_ctas = std::max(1, std::min(D.n_slices, sms));
+  D.n_ctas = std::max(1, std::min(D.n_slices, sms * kPipeCtasPerSm));
   std::vector<int> cs(static_cast<size_t>(D.n_ctas) + 1, D.n_slices);
   cs[0] = 0;
   const long long tot = woff.back();
@@ -297,7 +317,7 @@ void DeviceSystem::enqueue_apply(const double* x, double* y, double st_, double 
   if (L) L->add((a_bsr3 ? A.matrix_bytes() : A_sell.matrix_bytes()) + C1.matrix_bytes() + Q1.matrix_bytes() + 8.0 * (2.0 * n_u + n_t + n_p));
   const int m = n_t + n_p;
   if (m > 0) {
-    jtp_kernel<<<blocks_for(m, 256), 256, 0, s>>>(C2.view(), H.view(), Q2.view(), T.view(), xu, xt, xp, st_, sp_,
+    launch(jtp_kernel, dim3(blocks_for(m, 256)), dim3(256), 0, s, "jtp_kernel", C2.view(), H.view(), Q2.view(), T.view(), xu, xt, xp, st_, sp_,
                                                    y + n_u, y + n_u + n_t);
     cuda_check(cudaGetLastError(), "jtp_kernel launch");
     if (L) L->add(C2.matrix_bytes() + H.matrix_bytes() + Q2.matrix_bytes() + T.matrix_bytes() + 8.0 * (2.0 * m));
@@ -365,7 +385,7 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
     launch_coarse(DenseLUView{coarse_n, coarse_rank, lu.get(), prow.get(), pcol.get()}, b, out, s);
     if (Lg) Lg->add(8.0 * coarse_n * double(coarse_n) + 16.0 * coarse_n + 8.0 * coarse_n);
     if (sub_from) {
-      axpy_kernel<<<blocks_for(L.n, 256), 256, 0, s>>>(L.n, sub_from, out, -1.0, x);
+      launch(axpy_kernel, dim3(blocks_for(L.n, 256)), dim3(256), 0, s, "axpy_kernel", L.n, sub_from, out, -1.0, x);
       if (Lg) Lg->add(24.0 * nd);
     }
     return;
@@ -377,7 +397,7 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   // written by the kernel that produced b (or by presmooth_kernel for an external input).
   if (!xhat) {
     xhat = L.xt.get();
-    presmooth_kernel<<<blocks_for(L.n, 256), 256, 0, s>>>(L.n, b, d, w, xhat);
+    launch(presmooth_kernel, dim3(blocks_for(L.n, 256)), dim3(256), 0, s, "presmooth_kernel", L.n, b, d, w, xhat);
     if (Lg) Lg->add(24.0 * nd);
   }
   double* cur = xhat;
@@ -436,11 +456,11 @@ void DeviceAmg::enqueue_apply(const double* r, double* x, const double* sub_from
     launch_level(lv[0], GPlain{top_x.get()}, EResid{r, top_res.get()}, s);
     if (Lg) Lg->add(lv[0].a_bytes() + 24.0 * n);
     vcycle(0, top_res.get(), top_dx.get(), nullptr, nullptr, s, Lg);
-    add_inplace_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, top_x.get(), top_dx.get());
+    launch(add_inplace_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, s, "add_inplace_kernel", n, top_x.get(), top_dx.get());
     if (Lg) Lg->add(24.0 * n);
   }
   if (sub_from)
-    axpy_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, sub_from, top_x.get(), -1.0, x);
+    launch(axpy_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, s, "axpy_kernel", n, sub_from, top_x.get(), -1.0, x);
   else
     cuda_check(cudaMemcpyAsync(x, top_x.get(), sizeof(double) * n, cudaMemcpyDeviceToDevice, s), "copy");
   if (Lg) Lg->add(24.0 * n);
@@ -521,13 +541,13 @@ void DevicePrecond::enqueue_band(const double* rhs, double rs, double* out, doub
                                  int mode, cudaStream_t s, Ledger* L) {
   if (band.n == 0) return;
   if (inverse) {
-    dinv_kernel<<<blocks_for(size_t(band.n) * 32, kDinvThreads), kDinvThreads, 0, s>>>(dinv, band.n, band.n_blocks,
+    launch(dinv_kernel, dim3(blocks_for(size_t(band.n) * 32, kDinvThreads)), dim3(kDinvThreads), 0, s, "dinv_kernel", dinv, band.n, band.n_blocks,
                                                                                        rhs, rs, out, out2, sub, os, mode);
     cuda_check(cudaGetLastError(), "dinv_kernel launch");
     if (L) L->add(dinv_bytes + 8.0 * band.n * (2 + (mode == 1) + (mode == 2)));
     return;
   }
-  band_solve_kernel<<<band.n_blocks, 32, sizeof(double) * (band_ring_doubles(kBandMaxQ) + std::max(band_max_block, 1)), s>>>(
+  launch(band_solve_kernel, dim3(band.n_blocks), dim3(32), sizeof(double) * (band_ring_doubles(kBandMaxQ) + std::max(band_max_block, 1)), s, "band_solve_kernel", 
       band, rhs, rs, out, out2,
                                                                                               sub, os, mode);
   cuda_check(cudaGetLastError(), "band_solve_kernel launch");
@@ -552,20 +572,20 @@ void DevicePrecond::enqueue_apply(const double* x, double* y, double at, double 
   const double w0 = amg->opt.jacobi_omega;
   auto hin = [&](double* neg_out) {
     if (np == 0) return;
-    hsolve_in_kernel<<<fb, 256, 0, s>>>(np, hlu.get(), hpiv.get(), xt, at, tt.get(), neg_out);
+    launch(hsolve_in_kernel, dim3(fb), dim3(256), 0, s, "hsolve_in_kernel", np, hlu.get(), hpiv.get(), xt, at, tt.get(), neg_out);
     cuda_check(cudaGetLastError(), "hsolve_in launch");
     if (L) L->add(72.0 * np + 4.0 * np + 8.0 * nt * (2 + (neg_out != nullptr)));
   };
   auto hout = [&](const double* vu) {
     if (np == 0) return;
-    hsolve_out_kernel<<<fb, 256, 0, s>>>(np, S.C2.view(), vu, hlu.get(), hpiv.get(), tt.get(), at, yt);
+    launch(hsolve_out_kernel, dim3(fb), dim3(256), 0, s, "hsolve_out_kernel", np, S.C2.view(), vu, hlu.get(), hpiv.get(), tt.get(), at, yt);
     cuda_check(cudaGetLastError(), "hsolve_out launch");
     if (L) L->add(S.C2.matrix_bytes() + 8.0 * nu + 72.0 * np + 4.0 * np + 16.0 * nt);
   };
   if (variant == fpb::kTpu) {
     enqueue_band(xp, ap, tp.get(), nullptr, nullptr, 1.0, 0, s, L);  // t_p = T^-1 w_p
     hin(nullptr);                                                    // t_t = H~^-1 w_t
-    tpu_tu_kernel<<<blocks_for(nu, 256), 256, 0, s>>>(S.C1.view(), S.Q1.view(), xu, tt.get(), tp.get(), tu.get(), d0, w0,
+    launch(tpu_tu_kernel, dim3(blocks_for(nu, 256)), dim3(256), 0, s, "tpu_tu_kernel", S.C1.view(), S.Q1.view(), xu, tt.get(), tp.get(), tu.get(), d0, w0,
                                                       xh.get());
     cuda_check(cudaGetLastError(), "tpu_tu launch");
     if (L) L->add(S.C1.matrix_bytes() + S.Q1.matrix_bytes() + 8.0 * (2.0 * nu + nt + np));
@@ -671,8 +691,8 @@ void GmresSolver::build_graphs(double st, double sp, cudaStream_t s) {
 }
 
 double GmresSolver::norm_into(const double* a, const double* b, double* diff_out, double* dev_out, cudaStream_t s) {
-  sumsq_partial_kernel<<<red_grid_, kRedThreads, 0, s>>>(n_, a, b, diff_out, partial_.get());
-  finish_sum_kernel<<<1, kRedThreads, 0, s>>>(red_grid_, partial_.get(), dev_out, host_scalar_d_, 1);
+  launch(sumsq_partial_kernel, dim3(red_grid_), dim3(kRedThreads), 0, s, "sumsq_partial_kernel", n_, a, b, diff_out, partial_.get());
+  launch(finish_sum_kernel, dim3(1), dim3(kRedThreads), 0, s, "finish_sum_kernel", red_grid_, partial_.get(), dev_out, host_scalar_d_, 1);
   cuda_check(cudaStreamSynchronize(s), "norm sync");
   return *host_scalar_;
 }
@@ -732,7 +752,7 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
     const int budget = std::min(restart_, o.max_iter - res.iterations);
     if (budget <= 0) break;
     const double tol_c = o.tol * bnorm / rnorm;
-    start_cycle_kernel<<<blocks_for(n_, 256), 256, 0, s>>>(n_, r_.get(), scal_.get(), V_.get(), stage);
+    launch(start_cycle_kernel, dim3(blocks_for(n_, 256)), dim3(256), 0, s, "start_cycle_kernel", n_, r_.get(), scal_.get(), V_.get(), stage);
     cuda_check(cudaMemcpyAsync(g_.get(), &rnorm, sizeof(double), cudaMemcpyHostToDevice, s), "g0");
     int m = 0, assembled_at = -1;
     bool hit = false, cyc_done = false, happy = false;
@@ -740,8 +760,8 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
     res.launches += 1;  // start_cycle
     auto assemble = [&](int mm) {
       res.launches += 4;  // backsub, combine, 2 reductions (+ the graph, counted in launch_pj)
-      backsub_kernel<<<1, 1, 0, s>>>(mm, ldr_, R_.get(), g_.get(), y_.get(), flag_.get());
-      basis_combine_kernel<<<blocks_for(n_, 256), 256, 0, s>>>(n_, ldv_, mm, V_.get(), y_.get(), stage);
+      launch(backsub_kernel, dim3(1), dim3(1), 0, s, "backsub_kernel", mm, ldr_, R_.get(), g_.get(), y_.get(), flag_.get());
+      launch(basis_combine_kernel, dim3(blocks_for(n_, 256)), dim3(256), 0, s, "basis_combine_kernel", n_, ldv_, mm, V_.get(), y_.get(), stage);
       launch_pj();  // z = M^-1 (V y) = dx_cycle, jout = J dx_cycle
       const double rr = norm_into(r_.get(), jout_.get(), nullptr, nullptr, s);
       int sing = 0;
@@ -789,7 +809,7 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
     }
     if (!cyc_done && assembled_at != m) assemble(m);
     (void)happy;
-    add_inplace_kernel<<<blocks_for(n_, 256), 256, 0, s>>>(n_, xtot_.get(), dx_.get());
+    launch(add_inplace_kernel, dim3(blocks_for(n_, 256)), dim3(256), 0, s, "add_inplace_kernel", n_, xtot_.get(), dx_.get());
     cuda_check(cudaGraphLaunch(j_exec_, s), "graph launch j");
     rnorm = norm_into(b, jout_.get(), r_.get(), scal_.get(), s);  // r = b - J x, beta on device
     res.launches += 1 + japply_launches + 2;

@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_fast_kernel(MgsArgs a) {
 
 // y = R(0:m,0:m)^-1 g(0:m)  (gmres.cpp:92-98), one thread; flags a zero pivot
 __global__ void backsub_kernel(int m, int ldr, const double* R, const double* g, double* y, int* singular) {
+  pdl_entry();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   *singular = 0;
   for (int i = m - 1; i >= 0; --i) {
@@ -347,6 +348,7 @@ __global__ void backsub_kernel(int m, int ldr, const double* R, const double* g,
 
 // u_i = sum_{j<m} V_j[i] y_j, j ascending from 0 (gmres.cpp:99-101)
 __global__ void basis_combine_kernel(long long n, long long ldv, int m, const double* V, const double* y, double* u) {
+  pdl_entry();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
@@ -358,6 +360,7 @@ __global__ void basis_combine_kernel(long long n, long long ldv, int m, const do
 constexpr int kRedThreads = 512;
 __global__ void __launch_bounds__(kRedThreads) sumsq_partial_kernel(long long n, const double* a, const double* b,
                                                                     double* diff_out, double* partial) {
+  pdl_entry();
   // v = a - b (b may be null); optionally stores v; partial[block] = sum v^2
   __shared__ double sm[40];
   const long long chunk = ((n + gridDim.x - 1) / gridDim.x + 31) / 32 * 32;
@@ -373,6 +376,7 @@ __global__ void __launch_bounds__(kRedThreads) sumsq_partial_kernel(long long n,
 }
 __global__ void __launch_bounds__(kRedThreads) finish_sum_kernel(int nb, const double* partial, double* out_dev,
                                                                  double* out_host, int take_sqrt) {
+  pdl_entry();
   __shared__ double sm[40];
   double s = grid_total(partial, nb, sm);
   if (threadIdx.x != 0) return;
@@ -382,6 +386,7 @@ __global__ void __launch_bounds__(kRedThreads) finish_sum_kernel(int nb, const d
 }
 // V_0 = r / beta, also into the preconditioner staging buffer; g = [beta, 0...]
 __global__ void start_cycle_kernel(long long n, const double* r, const double* beta_dev, double* v0, double* stage) {
+  pdl_entry();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double v = r[i] / *beta_dev;

@@ -162,6 +162,7 @@ struct EJu {
 // ------------------------------------------------------------- SELL kernels
 template <class G, class E>
 __global__ void __launch_bounds__(256) sell_kernel(SellView A, G g, E epi) {
+  pdl_entry();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= A.n_rows) return;
   const auto pre = epi.load(row);
@@ -192,6 +193,7 @@ constexpr size_t slice_smem_bytes() {
 }
 template <int R, int W, class G, class E>
 __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
+  pdl_entry();
   __shared__ double prod[2 * R * (W + 1)];  // [2][R][W + 1]
   __shared__ long long rb[R + 1];
   const int row0 = blockIdx.x * R;
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
 // consumer sums.  Stage q is handed over with named barriers: FULL = 1 + q
 // (producer arrives, consumer waits), EMPTY = 1 + kPipeStages + q (reverse).
 constexpr int kPipeRows = 32, kPipeW = 32, kPipeStages = 7, kPipeThreads = 32 * (kPipeStages + 1);
+constexpr int kPipeCtasPerSm = 2;  // two resident pipelines per SM (registers capped at 128)
 constexpr size_t kPipeSmem = sizeof(double) * kPipeStages * kPipeRows * (kPipeW + 1);  // dynamic (> 48 KB)
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -254,7 +257,8 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
 }
 
 template <class G, class E>
-__global__ void __launch_bounds__(kPipeThreads, 1) csr_pipe_kernel(PipeView A, G g, E epi) {
+__global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) csr_pipe_kernel(PipeView A, G g, E epi) {
+  pdl_entry();
   extern __shared__ double pipe_smem[];
   double(*ring)[kPipeRows][kPipeW + 1] = reinterpret_cast<double(*)[kPipeRows][kPipeW + 1]>(pipe_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -319,6 +323,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) csr_pipe_kernel(PipeView A, G
 
 template <class G, class E>
 __global__ void __launch_bounds__(kWarpRowThreads) csr_warp_kernel(CsrView A, G g, E epi) {
+  pdl_entry();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= A.n_rows) return;  // warp-uniform
@@ -352,6 +357,7 @@ constexpr int kBsrThreads = 384;  // 4 slices per CTA
 
 template <class G, class E>
 __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E epi) {
+  pdl_entry();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int slice = t / 96, r = t - slice * 96, li = r >> 5, lane = r & 31;
   const int brow = slice * kSlice + lane;
@@ -392,6 +398,7 @@ __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E ep
 __global__ void __launch_bounds__(256) jtp_kernel(SellView C2, SellView H, SellView Q2, SellView T, const double* u,
                                                   const double* vt, const double* vp, double st, double sp, double* yt,
                                                   double* yp) {
+  pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < C2.n_rows) {
     const double d = sell_row(C2, i, GPlain{u});
@@ -409,6 +416,7 @@ __global__ void __launch_bounds__(256) jtp_kernel(SellView C2, SellView H, SellV
 __global__ void __launch_bounds__(256) tpu_tu_kernel(SellView C1, SellView Q1, const double* wu, const double* tt,
                                                      const double* tp, double* tu, const double* d, double w,
                                                      double* xh) {
+  pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= C1.n_rows) return;
   const double b = sell_row(C1, i, GPlain{tt});
@@ -444,6 +452,7 @@ __device__ __forceinline__ void lu3_solve_dev(const double* m, int pv, const dou
 // t_t = H~^-1 (at * v_t); optionally y_t = (-t_t) * at  (t-u-p*: v_t = -t_t, precond.cpp:239)
 __global__ void __launch_bounds__(256) hsolve_in_kernel(int n_faces, const double* hlu, const int* hpiv, const double* vt,
                                                         double at, double* tt, double* yt_neg) {
+  pdl_entry();
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= n_faces) return;
   const double w[3] = {vt[3 * f] * at, vt[3 * f + 1] * at, vt[3 * f + 2] * at};
@@ -458,6 +467,7 @@ __global__ void __launch_bounds__(256) hsolve_in_kernel(int n_faces, const doubl
 // y_t = at * (H~^-1 (C2 v_u) - t_t)   (precond.cpp:163-164 / 226-227)
 __global__ void __launch_bounds__(256) hsolve_out_kernel(int n_faces, SellView C2, const double* vu, const double* hlu,
                                                          const int* hpiv, const double* tt, double at, double* yt) {
+  pdl_entry();
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= n_faces) return;
   const double s[3] = {sell_row(C2, 3 * f, GPlain{vu}), sell_row(C2, 3 * f + 1, GPlain{vu}),
@@ -668,6 +678,7 @@ __device__ __forceinline__ void band_backward_any(double* xs, double* ring, int 
 
 __global__ void __launch_bounds__(32) band_solve_kernel(BandView F, const double* rhs, double rs, double* out,
                                                         double* out2, const double* sub, double os, int out_mode) {
+  pdl_entry();
   extern __shared__ double band_smem[];
   double* ring = band_smem;                                    // band_ring_doubles(kBandMaxQ) doubles
   double* xs = band_smem + band_ring_doubles(kBandMaxQ);       // the block's right-hand side / solution
@@ -735,6 +746,7 @@ constexpr int kDinvThreads = 256;
 __global__ void __launch_bounds__(kDinvThreads) dinv_kernel(DinvView D, int n, int n_blocks, const double* rhs,
                                                             double rs, double* out, double* out2, const double* sub,
                                                             double os, int out_mode) {
+  pdl_entry();
   const int row = (blockIdx.x * kDinvThreads + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= n) return;  // warp-uniform
   int lo = 0, hi = n_blocks - 1;  // block of this row: block_start[blk] <= row < block_start[blk + 1]
@@ -774,6 +786,7 @@ constexpr int kCoarseThreads = 256;
 // so the 2n dependent steps cost shared-memory latency, not L2/HBM latency.
 constexpr int kCoarseSmemN = 160;
 __global__ void __launch_bounds__(kCoarseThreads) coarse_solve_kernel(DenseLUView F, const double* b, double* x) {
+  pdl_entry();
   extern __shared__ double c[];
   const int n = F.n, tid = threadIdx.x;
   const double* lu = F.lu;
@@ -804,6 +817,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_solve_kernel(DenseLUVie
 // registers, the pivot value travels by shuffle; same operation order as above.
 constexpr int kCoarseWarpN = 64;
 __global__ void __launch_bounds__(32) coarse_warp_kernel(DenseLUView F, const double* b, double* x) {
+  pdl_entry();
   __shared__ double s_lu[kCoarseWarpN * kCoarseWarpN];
   const int n = F.n, lane = threadIdx.x;
 #pragma unroll 8
@@ -839,10 +853,12 @@ inline size_t coarse_smem_bytes(int n) {
 
 // ---------------------------------------------------------- elementwise
 __global__ void presmooth_kernel(int n, const double* b, const double* d, double w, double* x) {
+  pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) x[i] = (w * b[i]) / d[i];
 }
 __global__ void scale_copy_kernel(int n_u, int n_t, int n_p, const double* x, double st, double sp, double* y) {
+  pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int n = n_u + n_t + n_p;
   if (i >= n) return;
@@ -854,6 +870,7 @@ __global__ void axpy_kernel(long long n, const double* a, const double* b, doubl
   if (i < n) y[i] = a[i] + beta * b[i];
 }
 __global__ void add_inplace_kernel(long long n, double* x, const double* dx) {
+  pdl_entry();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < n) x[i] = x[i] + dx[i];
 }
