@@ -44,6 +44,7 @@ extern "C" {
 /* AmgConfig::Smoother (amg.hpp:24) */
 #define FP_SMOOTHER_JACOBI 0
 #define FP_SMOOTHER_SGS 1
+#define FP_SMOOTHER_CHEBYSHEV 2 /* extension: degree-k Chebyshev in D^-1 A (not in the reference) */
 
 typedef struct fp_csr {
   int32_t n_rows, n_cols;
@@ -63,11 +64,15 @@ typedef struct fp_block_system {
 typedef struct fp_amg_config {
   double strength_threshold;
   int32_t max_coarse, pre_sweeps, post_sweeps;
-  int32_t smoother; /* the GPU path requires FP_SMOOTHER_JACOBI */
+  int32_t smoother; /* the GPU path runs FP_SMOOTHER_JACOBI or FP_SMOOTHER_CHEBYSHEV */
   int32_t prolongation_smoothing;
   int32_t cycles_per_apply;
   double jacobi_omega, stall_ratio;
   int32_t max_levels;
+  /* FP_SMOOTHER_CHEBYSHEV: polynomial degree per sweep, lambda_max / lambda_min, power iterations */
+  int32_t chebyshev_degree;
+  double chebyshev_ratio;
+  int32_t power_iterations;
 } fp_amg_config;
 
 /* How the fracture-block factor (T or S~2, SparseFactor) is applied:
@@ -150,7 +155,8 @@ int fp_host_precond_levels(const fp_host_precond* p, int32_t* n_levels, int32_t*
  * Call with row_offsets == NULL first to get dims / nnz. */
 int fp_host_precond_matrix(const fp_host_precond* p, int32_t what, int32_t level, int32_t* n_rows, int32_t* n_cols,
                            int64_t* nnz, int64_t* row_offsets, int32_t* col_indices, double* values);
-/* what 0 = H~ blocks (9 n_p), 1 = T_diag (t-p-u) or S_K (t-u-p), 2 = smoother diag of level `level` */
+/* what 0 = H~ blocks (9 n_p), 1 = T_diag (t-p-u) or S_K (t-u-p), 2 = smoother diag of level `level`,
+ * 3 = {lambda_max} of level `level` (Chebyshev smoother, extension) */
 int fp_host_precond_vector(const fp_host_precond* p, int32_t what, int32_t level, double* out, int64_t* len);
 
 /* ---- upload to the device */

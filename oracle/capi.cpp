@@ -76,11 +76,16 @@ AmgConfig amg_cfg(const double* d, const int* i) {
     c.max_coarse = i[0];
     c.pre_sweeps = i[1];
     c.post_sweeps = i[2];
-    c.smoother = i[3] == 0 ? AmgConfig::Smoother::weighted_jacobi : AmgConfig::Smoother::sgs;
+    c.smoother = i[3] == 0   ? AmgConfig::Smoother::weighted_jacobi
+                 : i[3] == 2 ? AmgConfig::Smoother::chebyshev
+                             : AmgConfig::Smoother::sgs;
     c.prolongation_smoothing = i[4] != 0;
     c.cycles_per_apply = i[5];
     c.max_levels = i[6];
+    c.chebyshev_degree = i[7];
+    c.power_iterations = i[8];
   }
+  if (d) c.chebyshev_ratio = d[3];
   return c;
 }
 }  // namespace
@@ -167,8 +172,9 @@ int or_csr_copy(const void* m, int64_t* rp, int* ci, double* v) {
 
 // --------------------------------------------------------------- precond
 // variant 0 tpu, 1 tup, 2 tup_star; inner 0 amg, 1 direct.
-// amg_d = {strength_threshold, jacobi_omega, stall_ratio}
-// amg_i = {max_coarse, pre, post, smoother(0 jacobi,1 sgs), prolongation_smoothing, cycles, max_levels}
+// amg_d = {strength_threshold, jacobi_omega, stall_ratio, chebyshev_ratio}
+// amg_i = {max_coarse, pre, post, smoother(0 jacobi,1 sgs,2 chebyshev), prolongation_smoothing, cycles, max_levels,
+//          chebyshev_degree, power_iterations}
 int or_precond_build(void* s, int variant, int inner, const double* amg_d, const int* amg_i,
                      const double* coords, int n_nodes, void** out) {
   return guard([&] {
@@ -252,6 +258,12 @@ const void* or_amg_level_matrix(void* p, int l, int which) {
   const AmgLevel& L = static_cast<Pc*>(p)->amg().levels[size_t(l)];
   return which == 0 ? &L.A : &L.P;
 }
+double or_amg_level_lambda(void* p, int level) {
+  const Pc* pc = static_cast<Pc*>(p);
+  const auto& h = *pc->inner().amg;
+  return level >= 0 && level < int(h.levels.size()) ? h.levels[level].lambda_max : -1.0;
+}
+
 int or_amg_level_diag(void* p, int l, double* out) {
   const AmgLevel& L = static_cast<Pc*>(p)->amg().levels[size_t(l)];
   std::memcpy(out, L.smoother_diag.data(), sizeof(double) * L.smoother_diag.size());

@@ -234,8 +234,12 @@ struct AmgConfig {
   double strength_threshold = 0.08;
   int max_coarse = 100;
   int pre_sweeps = 1, post_sweeps = 1;
-  enum class Smoother { weighted_jacobi, sgs };
+  // chebyshev: EXTENSION (a non-goal of the reference), see amg.cpp
+  enum class Smoother { weighted_jacobi, sgs, chebyshev };
   Smoother smoother = Smoother::sgs;
+  int chebyshev_degree = 2;        // polynomial degree per sweep
+  double chebyshev_ratio = 10.0;   // lambda_min = lambda_max / ratio
+  int power_iterations = 10;       // lambda_max estimate of D^-1 A at setup
   bool prolongation_smoothing = true;
   int cycles_per_apply = 1;
   double jacobi_omega = 2.0 / 3.0;
@@ -247,6 +251,7 @@ struct AmgLevel {
   CsrMatrix A;
   CsrMatrix P;  // from this level to the previous finer one
   std::vector<double> smoother_diag;
+  double lambda_max = 0.0;  // chebyshev: 1.1 x power-iteration estimate of rho(D^-1 A)
   std::vector<int> fine_aggregate;
   std::vector<int> aggregate_offsets;
 };
@@ -264,6 +269,13 @@ AmgHierarchy amg_setup(const CsrMatrix& A, const std::vector<std::vector<double>
                        const AmgConfig& cfg);
 std::vector<double> amg_apply(const AmgHierarchy& h, std::span<const double> r);
 std::vector<std::vector<double>> constant_near_null(int n);
+// Chebyshev smoother support (extension): estimate and coefficients shared with the GPU path
+double chebyshev_lambda_max(const CsrMatrix& A, std::span<const double> diag, int iterations);
+struct ChebyshevCoefficients {
+  double theta = 0.0;           // (lambda_max + lambda_min) / 2 ; step 0: d = (r / D) / theta
+  std::vector<double> c1, c2;   // step k >= 1: d = c1[k] d + c2[k] (r / D)
+};
+ChebyshevCoefficients chebyshev_coefficients(double lambda_max, double ratio, int degree);
 std::vector<std::vector<double>> rigid_body_modes(std::span<const std::array<double, 3>> coords);
 
 // Column-pivoted Householder QR of a column-major m x k block (restates the

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libfracprec_b200.so")
 FP_OK, FP_INVALID_ARGUMENT, FP_NUMERICAL_ERROR, FP_CUDA_ERROR, FP_INTERNAL_ERROR = 0, 1, 2, 3, 4
 FP_MEM_HOST, FP_MEM_DEVICE = 0, 1
 FP_TPU, FP_TUP, FP_TUP_STAR = 0, 1, 2
-FP_SMOOTHER_JACOBI, FP_SMOOTHER_SGS = 0, 1
+FP_SMOOTHER_JACOBI, FP_SMOOTHER_SGS, FP_SMOOTHER_CHEBYSHEV = 0, 1, 2
 
 
 class NumericalError(RuntimeError):
@@ -41,7 +41,8 @@ class FpAmgConfig(C.Structure):
     _fields_ = [("strength_threshold", C.c_double), ("max_coarse", C.c_int32), ("pre_sweeps", C.c_int32),
                 ("post_sweeps", C.c_int32), ("smoother", C.c_int32), ("prolongation_smoothing", C.c_int32),
                 ("cycles_per_apply", C.c_int32), ("jacobi_omega", C.c_double), ("stall_ratio", C.c_double),
-                ("max_levels", C.c_int32)]
+                ("max_levels", C.c_int32), ("chebyshev_degree", C.c_int32), ("chebyshev_ratio", C.c_double),
+                ("power_iterations", C.c_int32)]
 
 
 class FpPrecondConfig(C.Structure):

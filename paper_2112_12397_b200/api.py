@@ -94,21 +94,32 @@ class AmgConfig:
     max_coarse: int = 100
     pre_sweeps: int = 1
     post_sweeps: int = 1
-    smoother: str = "weighted_jacobi"  # the reference default "sgs" has no GPU path
+    # "weighted_jacobi" (reference option), "sgs" (reference default; no GPU path) or
+    # "chebyshev" (extension: degree-k Chebyshev in D^-1 A, restated in the oracle)
+    smoother: str = "weighted_jacobi"
     prolongation_smoothing: bool = True
     cycles_per_apply: int = 1
     jacobi_omega: float = 2.0 / 3.0
     stall_ratio: float = 0.9
     max_levels: int = 25
+    chebyshev_degree: int = 2
+    chebyshev_ratio: float = 10.0
+    power_iterations: int = 10
+
+    _SMOOTHERS = {"weighted_jacobi": 0, "sgs": 1, "chebyshev": 2}
 
     def native(self) -> N.FpAmgConfig:
+        if self.smoother not in self._SMOOTHERS:
+            raise ValueError(f"unknown smoother {self.smoother!r}")
         c = N.FpAmgConfig()
         c.strength_threshold, c.max_coarse = self.strength_threshold, self.max_coarse
         c.pre_sweeps, c.post_sweeps = self.pre_sweeps, self.post_sweeps
-        c.smoother = N.FP_SMOOTHER_JACOBI if self.smoother == "weighted_jacobi" else N.FP_SMOOTHER_SGS
+        c.smoother = self._SMOOTHERS[self.smoother]
         c.prolongation_smoothing = int(self.prolongation_smoothing)
         c.cycles_per_apply, c.jacobi_omega = self.cycles_per_apply, self.jacobi_omega
         c.stall_ratio, c.max_levels = self.stall_ratio, self.max_levels
+        c.chebyshev_degree, c.chebyshev_ratio = self.chebyshev_degree, self.chebyshev_ratio
+        c.power_iterations = self.power_iterations
         return c
 
 

@@ -96,6 +96,12 @@ fpb::AmgOptions to_amg(const fp_amg_config& c) {
   o.jacobi_omega = c.jacobi_omega;
   o.stall_ratio = c.stall_ratio;
   o.max_levels = c.max_levels;
+  o.chebyshev_degree = c.chebyshev_degree;
+  o.chebyshev_ratio = c.chebyshev_ratio;
+  o.power_iterations = c.power_iterations;
+  need(o.smoother >= 0 && o.smoother <= 2, "AmgConfig: unknown smoother");
+  need(o.smoother != 2 || (o.chebyshev_degree >= 1 && o.chebyshev_ratio > 1.0 && o.power_iterations >= 1),
+       "AmgConfig: chebyshev needs degree >= 1, ratio > 1, power_iterations >= 1");
   return o;
 }
 
@@ -153,6 +159,9 @@ void fp_amg_config_default(fp_amg_config* c) {
   c->jacobi_omega = o.jacobi_omega;
   c->stall_ratio = o.stall_ratio;
   c->max_levels = o.max_levels;
+  c->chebyshev_degree = o.chebyshev_degree;
+  c->chebyshev_ratio = o.chebyshev_ratio;
+  c->power_iterations = o.power_iterations;
 }
 
 // ------------------------------------------------------------------ system
@@ -266,6 +275,12 @@ int fp_host_precond_vector(const fp_host_precond* p, int32_t what, int32_t level
       need(level >= 0 && level < int(p->hp.amg.levels.size()), "level out of range");
       v = &p->hp.amg.levels[level].diag;
     }
+    std::vector<double> lam;
+    if (what == 3) {  // Chebyshev lambda_max of the level (extension), a 1-vector
+      need(level >= 0 && level < int(p->hp.amg.levels.size()), "level out of range");
+      lam.assign(1, p->hp.amg.levels[level].lambda_max);
+      v = &lam;
+    }
     need(v != nullptr, "unknown vector");
     if (len) *len = int64_t(v->size());
     if (out) std::memcpy(out, v->data(), sizeof(double) * v->size());
@@ -307,6 +322,10 @@ int fp_precond_upload(fp_system* s, const fp_precond_desc* d, fp_precond** out) 
     }
     const fpb::Csr& Ac = hp.amg.levels.back().A;
     hp.amg.coarse.compute(Ac.to_dense(), Ac.n_rows);
+    if (hp.amg.opt.smoother == 2)  // Chebyshev (extension): the oracle's lambda estimate on the uploaded levels
+      for (size_t l = 0; l + 1 < hp.amg.levels.size(); ++l)
+        hp.amg.levels[l].lambda_max =
+            fpb::chebyshev_lambda_max(hp.amg.levels[l].A, hp.amg.levels[l].diag, hp.amg.opt.power_iterations);
     auto p = std::make_unique<fp_precond>();
     p->sys = s;
     p->dev = std::make_unique<fpd::DevicePrecond>(*s->dev, hp);

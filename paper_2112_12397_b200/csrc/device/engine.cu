@@ -327,10 +327,10 @@ void DeviceSystem::enqueue_apply(const double* x, double* y, double st_, double 
 // -------------------------------------------------------------------- AMG
 DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
   opt = h.opt;
-  if (opt.smoother != 0)
+  if (opt.smoother != 0 && opt.smoother != 2)
     throw std::invalid_argument(
-        "GPU AMG requires smoother = weighted_jacobi (the reference's symmetric Gauss-Seidel is sequential; "
-        "see DESIGN.md)");
+        "GPU AMG requires smoother = weighted_jacobi or chebyshev (the reference's symmetric Gauss-Seidel is "
+        "sequential; see DESIGN.md)");
   const int L = int(h.levels.size());
   lv.resize(static_cast<size_t>(L));
   for (int l = 0; l < L; ++l) {
@@ -352,6 +352,12 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
     }
     D.d.upload(H.diag);
     D.b.alloc(D.n), D.x.alloc(D.n), D.xt.alloc(D.n), D.xt2.alloc(D.n), D.xt3.alloc(D.n), D.r.alloc(D.n);
+    if (opt.smoother == 2 && l + 1 < L) {
+      const fpb::ChebyshevCoefficients c =
+          fpb::chebyshev_coefficients(H.lambda_max, opt.chebyshev_ratio, opt.chebyshev_degree);
+      D.cheb_theta = c.theta, D.cheb_c1 = c.c1, D.cheb_c2 = c.c2;
+      D.cd.alloc(D.n);
+    }
   }
   // coarse LU, column-major for contiguous column sweeps
   coarse_n = h.coarse.n;
@@ -393,6 +399,10 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   const double w = opt.jacobi_omega;
   const double* d = L.d.get();
   const double A_b = L.a_bytes();
+  if (opt.smoother == 2) {
+    vcycle_chebyshev(l, b, x, sub_from, s, Lg);
+    return;
+  }
   // First Jacobi sweep from x = 0 is x = (w b)/d exactly (A 0 = 0, amg.cpp:138-139); it was
   // written by the kernel that produced b (or by presmooth_kernel for an external input).
   if (!xhat) {
@@ -441,6 +451,51 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
     if (Lg) Lg->add(A_b + 8.0 * (4 + (final_sweep && sub_from)) * nd);
     cur = nxt;
   }
+}
+
+// EXTENSION — the same V-cycle with Chebyshev sweeps (oracle/amg.cpp chebyshev_sweep): each sweep
+// is `degree` steps; the first pre-smoothing step starts from x = 0 (elementwise), every other
+// step is one SpMV with the ECheb epilogue (x ping-pongs between two buffers, d updated in place).
+void DeviceAmg::vcycle_chebyshev(int l, const double* b, double* x, const double* sub_from, cudaStream_t s,
+                                 Ledger* Lg) {
+  DeviceLevel& L = lv[l];
+  const int last = n_levels() - 1;
+  const double nd = L.n, A_b = L.a_bytes();
+  const double* d = L.d.get();
+  double* dv = L.cd.get();
+  double* tA = L.xt2.get();
+  double* tB = L.xt3.get();
+  auto other = [&](const double* c) { return c == tA ? tB : tA; };
+  const int m = opt.chebyshev_degree;
+  double* cur = tA;
+  auto step = [&](int k, double* nxt, const double* sub) {
+    ECheb e{b, d, dv, cur, nxt, sub, L.cheb_theta, k > 0 ? L.cheb_c1[k - 1] : 0.0, k > 0 ? L.cheb_c2[k - 1] : 0.0,
+            k == 0 ? 1 : 0};
+    launch_level(L, GPlain{cur}, e, s);
+    if (Lg) Lg->add(A_b + 8.0 * (6 + (sub != nullptr) - (k == 0)) * nd);
+    cur = nxt;
+  };
+  launch(cheb_first_kernel, dim3(blocks_for(L.n, 256)), dim3(256), 0, s, "cheb_first_kernel", L.n, b, d,
+         L.cheb_theta, dv, cur);
+  if (Lg) Lg->add(32.0 * nd);
+  for (int k = 1; k < m; ++k) step(k, other(cur), nullptr);
+  for (int it = 1; it < opt.pre_sweeps; ++it)
+    for (int k = 0; k < m; ++k) step(k, other(cur), nullptr);
+  launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s);  // r = b - A x
+  if (Lg) Lg->add(A_b + 24.0 * nd);
+  DeviceLevel& C = lv[l + 1];
+  const bool coarse_next = l + 1 == last;
+  if (coarse_next || opt.smoother == 2)
+    launch_mat(C.R, GPlain{L.r.get()}, EStore{C.b.get()}, s);  // r_c = P^T r  (amg.cpp:166)
+  if (Lg) Lg->add(C.R.matrix_bytes() + 8.0 * nd + 8.0 * C.n);
+  vcycle(l + 1, C.b.get(), C.x.get(), nullptr, nullptr, s, Lg);
+  launch_mat(C.P, GPlain{C.x.get()}, EAddTo{cur, cur}, s);  // x += P e_c  (amg.cpp:168-169)
+  if (Lg) Lg->add(C.P.matrix_bytes() + 8.0 * C.n + 16.0 * nd);
+  for (int it = 0; it < opt.post_sweeps; ++it)
+    for (int k = 0; k < m; ++k) {
+      const bool final_step = it + 1 == opt.post_sweeps && k + 1 == m;
+      step(k, final_step ? x : other(cur), final_step ? sub_from : nullptr);
+    }
 }
 
 void DeviceAmg::enqueue_apply(const double* r, double* x, const double* sub_from, cudaStream_t s, Ledger* Lg,

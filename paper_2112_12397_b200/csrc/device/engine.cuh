@@ -109,6 +109,10 @@ struct DeviceLevel {
   DMat Am;
   DMat P, R;  // P: this level <- next coarser; R = P^T (level l+1 holds P_{l+1}, R_{l+1})
   DevBuf<double> d, b, x, xt, xt2, xt3, r;
+  // Chebyshev smoother (extension): coefficients of this level and its direction vector
+  double cheb_theta = 0.0;
+  std::vector<double> cheb_c1, cheb_c2;
+  DevBuf<double> cd;
   int n = 0;
   double a_bytes() const { return bsr3 ? Ab.matrix_bytes() : Am.matrix_bytes(); }
 };
@@ -133,6 +137,7 @@ class DeviceAmg {
 
  private:
   void vcycle(int l, const double* b, double* x, const double* sub_from, double* xhat, cudaStream_t s, Ledger* L);
+  void vcycle_chebyshev(int l, const double* b, double* x, const double* sub_from, cudaStream_t s, Ledger* L);
 };
 
 class DevicePrecond {

@@ -144,6 +144,31 @@ struct EJacobiSubFrom {  // out_i = c_i - (Jacobi update)   (v_u = s_u - v_u2, p
     out[i] = p.c - xn;
   }
 };
+// EXTENSION — Chebyshev smoother step (oracle/amg.cpp chebyshev_sweep), s = (A x)_i:
+//   first (step 0, x != 0): d_i = ((b_i - s) / D_i) / theta
+//   else  (step k >= 1):    d_i = c1 d_i + c2 ((b_i - s) / D_i)
+//   x'_i = x_i + d_i, or out_i = c_i - x'_i on the last post-smoothing step of v_u = s_u - AMG(t_u2)
+struct ECheb {
+  const double* b;
+  const double* D;
+  double* dv;
+  const double* x;
+  double* xo;
+  const double* c;
+  double theta, c1, c2;
+  int first;
+  struct P { double b, D, d, x, c; };
+  __device__ __forceinline__ P load(int i) const {
+    return {b[i], D[i], first ? 0.0 : dv[i], x[i], c ? c[i] : 0.0};
+  }
+  __device__ __forceinline__ void operator()(int i, double s, const P& p) const {
+    const double r = p.b - s;
+    const double dn = first ? (r / p.D) / theta : c1 * p.d + c2 * (r / p.D);
+    dv[i] = dn;
+    const double xn = p.x + dn;
+    xo[i] = c ? p.c - xn : xn;
+  }
+};
 // J apply, displacement rows: y_u = (A u + C1 (st v_t)) + Q1 (sp v_p)   (block.cpp:55-60);
 // the short C1 / Q1 row sums are formed before the A row loop.
 struct EJu {
@@ -852,6 +877,15 @@ inline size_t coarse_smem_bytes(int n) {
 }
 
 // ---------------------------------------------------------- elementwise
+// EXTENSION — Chebyshev step 0 from x = 0: r = b exactly (A 0 = +0), d = (b / D) / theta, x = 0 + d
+__global__ void cheb_first_kernel(int n, const double* b, const double* D, double theta, double* dv, double* x) {
+  pdl_entry();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double dn = (b[i] / D[i]) / theta;
+  dv[i] = dn;
+  x[i] = 0.0 + dn;
+}
 __global__ void presmooth_kernel(int n, const double* b, const double* d, double w, double* x) {
   pdl_entry();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

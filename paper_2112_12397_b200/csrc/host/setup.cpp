@@ -328,7 +328,53 @@ HostAmg amg_setup(Csr A, const std::vector<std::vector<double>>& near_null, cons
   const Csr& Ac = h.levels.back().A;
   h.coarse.compute(Ac.to_dense(), Ac.n_rows);
   plog.mark("coarse LU", Ac.n_rows);
+  if (opt.smoother == 2) {
+    for (size_t l = 0; l + 1 < h.levels.size(); ++l)
+      h.levels[l].lambda_max = chebyshev_lambda_max(h.levels[l].A, h.levels[l].diag, opt.power_iterations);
+    plog.mark("chebyshev lambda_max");
+  }
   return h;
+}
+
+double chebyshev_lambda_max(const Csr& A, const std::vector<double>& diag, int iterations) {
+  const int n = A.n_rows;
+  if (n == 0) return 1.0;
+  std::vector<double> v(static_cast<size_t>(n), 1.0 / std::sqrt(double(n))), w(static_cast<size_t>(n));
+  double lam = 0.0;
+  for (int it = 0; it < std::max(1, iterations); ++it) {
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i) {  // each row summed left to right from 0.0 (csr.cpp:112-117)
+      double s = 0.0;
+      for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) s += A.v[k] * v[A.ci[k]];
+      w[i] = s / diag[i];
+    }
+    double s = 0.0;  // index order, one thread: the oracle's sum
+    for (int i = 0; i < n; ++i) s += w[i] * w[i];
+    const double nrm = std::sqrt(s);
+    if (!(nrm > 0.0) || !std::isfinite(nrm)) throw numerical_error("chebyshev: power iteration broke down");
+    lam = nrm;
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i) v[i] = w[i] / nrm;
+  }
+  return 1.1 * lam;
+}
+
+ChebyshevCoefficients chebyshev_coefficients(double lambda_max, double ratio, int degree) {
+  if (!(lambda_max > 0.0) || !(ratio > 1.0) || degree < 1)
+    throw std::invalid_argument("chebyshev: need lambda_max > 0, ratio > 1, degree >= 1");
+  ChebyshevCoefficients c;
+  const double lmin = lambda_max / ratio;
+  c.theta = (lambda_max + lmin) / 2.0;
+  const double delta = (lambda_max - lmin) / 2.0;
+  const double sigma = c.theta / delta;
+  double rho = 1.0 / sigma;
+  for (int k = 1; k < degree; ++k) {
+    const double rho_new = 1.0 / (2.0 * sigma - rho);
+    c.c1.push_back(rho_new * rho);
+    c.c2.push_back(2.0 * rho_new / delta);
+    rho = rho_new;
+  }
+  return c;
 }
 
 std::vector<std::vector<double>> rigid_body_modes(const std::vector<std::array<double, 3>>& c) {

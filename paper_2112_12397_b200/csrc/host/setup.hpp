@@ -17,7 +17,11 @@ struct AmgOptions {
   double strength_threshold = 0.08;  // amg.hpp:20
   int max_coarse = 100;
   int pre_sweeps = 1, post_sweeps = 1;
-  int smoother = 0;  // 0 weighted Jacobi (GPU path), 1 symmetric Gauss-Seidel (reference default)
+  int smoother = 0;  // 0 weighted Jacobi (GPU path), 1 symmetric Gauss-Seidel (reference default),
+                     // 2 Chebyshev (extension; restated in oracle/amg.cpp)
+  int chebyshev_degree = 2;
+  double chebyshev_ratio = 10.0;
+  int power_iterations = 10;
   bool prolongation_smoothing = true;
   int cycles_per_apply = 1;
   double jacobi_omega = 2.0 / 3.0;
@@ -29,6 +33,7 @@ struct HostLevel {
   Csr A;
   Csr P;  // prolongation from this level to the previous finer one (empty at level 0)
   std::vector<double> diag;
+  double lambda_max = 0.0;     // chebyshev: 1.1 x power-iteration estimate of rho(D^-1 A)
   std::vector<int> aggregate;  // fine row -> aggregate id (coarse levels only)
   std::vector<int> aggregate_offsets;
 };
@@ -38,6 +43,15 @@ struct HostAmg {
   FullPivLU coarse;
   AmgOptions opt;
 };
+
+// Chebyshev smoother (extension): the oracle's chebyshev_lambda_max / chebyshev_coefficients
+// (oracle/amg.cpp), computed with the same operation order so the GPU matches it bit for bit.
+double chebyshev_lambda_max(const Csr& A, const std::vector<double>& diag, int iterations);
+struct ChebyshevCoefficients {
+  double theta = 0.0;
+  std::vector<double> c1, c2;
+};
+ChebyshevCoefficients chebyshev_coefficients(double lambda_max, double ratio, int degree);
 
 // A is taken by value and moved into level 0 (callers std::move the inner operator in)
 HostAmg amg_setup(Csr A, const std::vector<std::vector<double>>& near_null, const AmgOptions& opt);

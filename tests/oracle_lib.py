@@ -50,6 +50,7 @@ def _load():
         "or_amg_levels": (C.c_int, [P]),
         "or_amg_level_matrix": (P, [P, C.c_int, C.c_int]),
         "or_amg_level_diag": (C.c_int, [P, C.c_int, DP]),
+        "or_amg_level_lambda": (C.c_double, [P, C.c_int]),
         "or_amg_level_aggregates": (C.c_int, [P, C.c_int, IP]),
         "or_amg_apply": (C.c_int, [P, DP, DP]),
         "or_gmres": (C.c_int, [P, P, DP, C.c_double, C.c_int, C.c_int, C.c_int, DP, IP, DP, C.c_int, DP]),
@@ -91,7 +92,8 @@ def csr_from(handle) -> tuple:
 
 
 AMG_DEFAULT = dict(strength_threshold=0.08, jacobi_omega=2.0 / 3.0, stall_ratio=0.9, max_coarse=100, pre_sweeps=1,
-                   post_sweeps=1, smoother=0, prolongation_smoothing=1, cycles_per_apply=1, max_levels=25)
+                   post_sweeps=1, smoother=0, prolongation_smoothing=1, cycles_per_apply=1, max_levels=25,
+                   chebyshev_degree=2, chebyshev_ratio=10.0, power_iterations=10)
 VARIANT = {"tpu": 0, "tup": 1, "tup_star": 2}
 
 
@@ -153,9 +155,10 @@ class OracleSystem:
 class OraclePrecond:
     def __init__(self, sys: OracleSystem, variant="tup", inner="amg", coords=None, factor_solve="sweep", **amg):
         cfg = dict(AMG_DEFAULT, **amg)
-        d = np.array([cfg["strength_threshold"], cfg["jacobi_omega"], cfg["stall_ratio"]])
+        d = np.array([cfg["strength_threshold"], cfg["jacobi_omega"], cfg["stall_ratio"], cfg["chebyshev_ratio"]])
         i = np.array([cfg["max_coarse"], cfg["pre_sweeps"], cfg["post_sweeps"], cfg["smoother"],
-                      cfg["prolongation_smoothing"], cfg["cycles_per_apply"], cfg["max_levels"]], np.int32)
+                      cfg["prolongation_smoothing"], cfg["cycles_per_apply"], cfg["max_levels"],
+                      cfg["chebyshev_degree"], cfg["power_iterations"]], np.int32)
         self.sys, self.variant = sys, variant
         self.h = C.c_void_p()
         cp, nn = None, 0
@@ -191,6 +194,10 @@ class OraclePrecond:
 
     def level_matrix(self, level: int, which: int) -> tuple:
         return csr_from(lib.or_amg_level_matrix(self.h, level, which))
+
+    def level_lambda(self, level: int) -> float:
+        """Chebyshev lambda_max estimate of the level (0.0 for other smoothers)."""
+        return float(lib.or_amg_level_lambda(self.h, level))
 
     def level_diag(self, level: int) -> np.ndarray:
         n = self.level_matrix(level, 0)[0]

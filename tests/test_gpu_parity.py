@@ -50,9 +50,11 @@ def upload_oracle_precond(op, osys, opc, variant, amg):
 
 def amg_kw(amg: api.AmgConfig):
     return dict(strength_threshold=amg.strength_threshold, jacobi_omega=amg.jacobi_omega, stall_ratio=amg.stall_ratio,
-                max_coarse=amg.max_coarse, pre_sweeps=amg.pre_sweeps, post_sweeps=amg.post_sweeps, smoother=0,
+                max_coarse=amg.max_coarse, pre_sweeps=amg.pre_sweeps, post_sweeps=amg.post_sweeps,
+                smoother=api.AmgConfig._SMOOTHERS[amg.smoother],
                 prolongation_smoothing=int(amg.prolongation_smoothing), cycles_per_apply=amg.cycles_per_apply,
-                max_levels=amg.max_levels)
+                max_levels=amg.max_levels, chebyshev_degree=amg.chebyshev_degree,
+                chebyshev_ratio=amg.chebyshev_ratio, power_iterations=amg.power_iterations)
 
 
 CASES = {
@@ -315,3 +317,40 @@ def test_coarse_solve_paths_bitwise(max_levels, coarse_n):
     pc = upload_oracle_precond(op, osys, opc, "tup", amg)
     r = np.random.default_rng(21).uniform(-1, 1, J.n_u)
     assert np.array_equal(pc.amg_apply(r), opc.amg_apply(r))
+
+
+@pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
+@pytest.mark.parametrize("degree,pre,post", [(1, 1, 1), (2, 1, 1), (3, 2, 1), (2, 1, 3)])
+def test_chebyshev_smoother_apply_bitwise(variant, degree, pre, post):
+    """Chebyshev smoother (extension): GPU apply == oracle apply bit for bit,
+    for the oracle-built hierarchy uploaded and for the product-built one."""
+    J = small_workload(seed=47, cells=(8, 6, 6))
+    osys = oracle_system(J)
+    amg = api.AmgConfig(smoother="chebyshev", chebyshev_degree=degree, pre_sweeps=pre, post_sweeps=post)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, **amg_kw(amg))
+    op = api.BlockSystemOperator(J)
+    x = np.random.default_rng(31).uniform(-1, 1, J.total_dimension())
+    ref = opc.apply(x)
+    pc = upload_oracle_precond(op, osys, opc, variant, amg)
+    assert np.array_equal(pc.apply(x), ref)
+    pc2 = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, api.PrecondConfig(variant, amg=amg)))
+    opc.set_factor_solve(pc2.factor_solve)
+    assert np.array_equal(pc2.apply(x), opc.apply(x))
+
+
+def test_chebyshev_theta0_and_gmres_match_oracle():
+    J = small_workload(seed=53, cells=(12, 12, 10))
+    osys = oracle_system(J)
+    amg = api.AmgConfig(strength_threshold=0.0, smoother="chebyshev")
+    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, **amg_kw(amg))
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, "tup", amg)
+    r = np.random.default_rng(2).uniform(-1, 1, J.n_u)
+    assert np.array_equal(pc.amg_apply(r), opc.amg_apply(r))
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=50, max_iter=300, scaled=True)
+    x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=300, restart=50, scaled=True)
+    assert st.converged == st_ref["converged"]
+    assert abs(st.iterations - st_ref["iterations"]) <= 2
+    if st_ref["converged"]:
+        assert rel(x, x_ref) <= 1e-8
