@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 1500 python tools/smoother_compare.py 2 2>&1 | tail -8
