@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libfracprec_b200.so")
+# FRACPREC_B200_LIB overrides the in-tree library (A/B builds of kernel variants)
+LIB_PATH = os.environ.get("FRACPREC_B200_LIB") or os.path.join(_HERE, "_lib", "libfracprec_b200.so")
 
 FP_OK, FP_INVALID_ARGUMENT, FP_NUMERICAL_ERROR, FP_CUDA_ERROR, FP_INTERNAL_ERROR = 0, 1, 2, 3, 4
 FP_MEM_HOST, FP_MEM_DEVICE = 0, 1

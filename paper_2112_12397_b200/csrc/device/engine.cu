@@ -277,6 +277,9 @@ DBsr3 make_bsr3(const fpb::Csr& A) {
 // ------------------------------------------------------------------ system
 DeviceSystem::DeviceSystem(const fpb::HostSystem& J) {
   J.check_shapes();
+  cuda_check(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "side stream");
+  cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "fork event");
+  cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "join event");
   n_u = J.n_u, n_t = J.n_t, n_p = J.n_p;
   a_bsr3 = n_u % 3 == 0;
   if (a_bsr3)
@@ -310,18 +313,27 @@ void DeviceSystem::enqueue_apply(const double* x, double* y, double st_, double 
   const double* xt = x + n_u;
   const double* xp = x + n_u + n_t;
   const EJu ju{C1.view(), Q1.view(), xt, xp, st_, sp_, y};
+  const int m = n_t + n_p;
+  if (m > 0) {  // y_t, y_p = t/p rows on the side stream, concurrent with the A rows below
+    cuda_check(cudaEventRecord(ev_fork, s), "fork record");
+    cuda_check(cudaStreamWaitEvent(side, ev_fork, 0), "fork wait");
+    launch(jtp_kernel, dim3(blocks_for(m, 256)), dim3(256), 0, side, "jtp_kernel", C2.view(), H.view(), Q2.view(),
+           T.view(), xu, xt, xp, st_, sp_, y + n_u, y + n_u + n_t);
+    cuda_check(cudaEventRecord(ev_join, side), "join record");
+    if (L) L->add(C2.matrix_bytes() + H.matrix_bytes() + Q2.matrix_bytes() + T.matrix_bytes() + 8.0 * (2.0 * m));
+  }
   if (a_bsr3)
     launch_bsr3(A, GPlain{xu}, ju, s);
   else
     launch_sell(A_sell, GPlain{xu}, ju, s);
   if (L) L->add((a_bsr3 ? A.matrix_bytes() : A_sell.matrix_bytes()) + C1.matrix_bytes() + Q1.matrix_bytes() + 8.0 * (2.0 * n_u + n_t + n_p));
-  const int m = n_t + n_p;
-  if (m > 0) {
-    launch(jtp_kernel, dim3(blocks_for(m, 256)), dim3(256), 0, s, "jtp_kernel", C2.view(), H.view(), Q2.view(), T.view(), xu, xt, xp, st_, sp_,
-                                                   y + n_u, y + n_u + n_t);
-    cuda_check(cudaGetLastError(), "jtp_kernel launch");
-    if (L) L->add(C2.matrix_bytes() + H.matrix_bytes() + Q2.matrix_bytes() + T.matrix_bytes() + 8.0 * (2.0 * m));
-  }
+  if (m > 0) cuda_check(cudaStreamWaitEvent(s, ev_join, 0), "join wait");
+}
+
+DeviceSystem::~DeviceSystem() {
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (side) cudaStreamDestroy(side);
 }
 
 // -------------------------------------------------------------------- AMG

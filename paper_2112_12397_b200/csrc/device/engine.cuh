@@ -51,7 +51,14 @@ DBsr3 make_bsr3(const fpb::Csr& A);  // A square, n % 3 == 0
 class DeviceSystem {
  public:
   explicit DeviceSystem(const fpb::HostSystem& J);
+  ~DeviceSystem();
+  DeviceSystem(const DeviceSystem&) = delete;
+  DeviceSystem& operator=(const DeviceSystem&) = delete;
   int n_u = 0, n_t = 0, n_p = 0;
+  // the t/p rows (jtp_kernel) run on a side stream, concurrently with the A rows (fork/join
+  // through events; captured into the graphs as parallel branches)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int n() const { return n_u + n_t + n_p; }
   double st = 1.0, sp = 1.0;  // driver block scaling (driver.cpp:114-125)
   bool a_bsr3 = true;         // A as 3x3 blocks (n_u = 3 * nodes); SELL otherwise

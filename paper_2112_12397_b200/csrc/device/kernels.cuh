@@ -378,7 +378,10 @@ __global__ void __launch_bounds__(kWarpRowThreads) csr_warp_kernel(CsrView A, G 
 // 96 threads per slice: warp li (0..2) computes scalar row 3*brow+li of the 32
 // block rows of the slice.  Sum order = block columns ascending, then j = 0,1,2:
 // the CSR column order.
-constexpr int kBsrThreads = 384;  // 4 slices per CTA
+#ifndef FP_BSR_THREADS
+#define FP_BSR_THREADS 384
+#endif
+constexpr int kBsrThreads = FP_BSR_THREADS;  // slices of 96 threads per CTA
 
 template <class G, class E>
 __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E epi) {
