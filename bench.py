@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--max-iter", type=int, default=500)
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the extra t-p-u / t-u-p* measurements")
     ap.add_argument("--cpu-budget", type=float, default=30.0, help="seconds of oracle work for cpu_baseline")
     return ap.parse_args()
 
@@ -95,6 +96,34 @@ def ncu_traffic(key: str):
         return k["dram_bytes_read"] + k["dram_bytes_write"]
     except (OSError, KeyError, ValueError):
         return None
+
+
+def other_variants(op, J, b, flush, args) -> dict:
+    """The other block preconditioners on the same system and protocol (BASELINE: both variants, t-p-u and
+    t-u-p, optionally t-u-p*): the solver's CUDA-event time of 2 solves after one warm-up, L2 flushed between."""
+    import torch
+
+    from paper_2112_12397_b200 import api
+
+    out = {}
+    for v in ("tpu", "tup", "tup_star"):
+        if v == args.variant:
+            continue
+        cfg = api.PrecondConfig(v, amg=api.AmgConfig(strength_threshold=args.theta), factor_solve=args.factor_solve)
+        pc = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, cfg))
+        x = torch.empty_like(b)
+        api.gmres(op, pc, b, tol=args.tol, max_iter=args.max_iter, restart=args.restart, scaled=True, x=x)
+        torch.cuda.synchronize()
+        t = 0.0
+        for _ in range(2):
+            flush.zero_()
+            _, st = api.gmres(op, pc, b, tol=args.tol, max_iter=args.max_iter, restart=args.restart, scaled=True, x=x)
+            t += st.device_seconds
+        out[v] = {"s_per_system": round(t / 2, 6), "iterations": st.iterations,
+                  "converged": st.converged, "final_rel_residual": st.relative_residuals[-1],
+                  "precond_apply_ms": round(pc.profile(reps=10)["apply_ms"], 4)}
+        del pc
+    return out
 
 
 def peaks():
@@ -281,8 +310,11 @@ def run_ours(args):
     ev1.record()
     barrier()
     clk = clocks.stop()
-    dev_ms = ev0.elapsed_time(ev1)
-    total_s = max_over_ranks(dev_ms / 1e3)
+    # device time of the solves, from CUDA events the solver records on its own (launching) stream
+    # around each solve (fp_solve_stats.device_seconds); the torch-stream bracket is a cross-check
+    dev_s = sum(st_.device_seconds for st_ in stats)
+    bracket_ms = ev0.elapsed_time(ev1)
+    total_s = max_over_ranks(dev_s)
     per_solve = total_s / args.steps
     value = whole_job_seconds_per_system(total_s, args.steps, ws)
 
@@ -339,8 +371,12 @@ def run_ours(args):
                                                           "band_ms", "coarse_ms")},
             "amg_levels": prof["level_rows"], "amg_level_nnz": prof["level_nnz"],
             "gpu_launches": int(launches),
+            "timing": "value = CUDA events on the solver's stream around each solve (max over ranks); "
+                      f"torch-stream bracket incl. L2 flush: {bracket_ms / args.steps:.3f} ms per step",
             "clocks": clk, "setup_s": round(setup_s, 2), "generate_s": round(gen_s, 2),
         }
+        if not args.no_variants:
+            line["variants"] = other_variants(op, J, b, flush, args)
         if not args.no_cpu_baseline and ws == 1:
             line["cpu_baseline"] = cpu_baseline(J, b_host, args, st.iterations)
         print(json.dumps(line), flush=True)
