@@ -110,12 +110,13 @@ void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s) 
 
 // Few or long rows (coarse levels, R = P^T) stream best one warp per row;
 // many short rows one thread per row in SELL-32 slices.
-DMat make_mat(const fpb::Csr& A) {
+DMat make_mat(const fpb::Csr& A, bool few_rows_parallel) {
   DMat M;
   const double avg = A.n_rows > 0 ? double(A.nnz()) / A.n_rows : 0.0;
   // SELL's thread-per-row chains need enough rows to hide latency; below ~64k
   // rows the slice kernel's parallel loads win even for short rows
-  M.warp = A.n_rows > 0 && (avg >= 48.0 || (A.n_rows < 65536 && avg >= 8.0));
+  M.warp = A.n_rows > 0 && (avg >= 48.0 || (A.n_rows < 65536 && avg >= 8.0) ||
+                            (few_rows_parallel && A.n_rows < 2048 && avg >= 2.0));
   if (!M.warp) {
     M.sell = make_sell(A);
     return M;
@@ -291,6 +292,7 @@ DeviceSystem::DeviceSystem(const fpb::HostSystem& J) {
   C2 = make_sell(J.C2);
   H = make_sell(J.H);
   Q2 = make_sell(J.Q2);
+  Q2m = make_mat(J.Q2, true);
   T = make_sell(J.T);
   auto max_abs_diag = [](const fpb::Csr& M) {
     double m = 0.0;
@@ -645,7 +647,7 @@ void DevicePrecond::enqueue_apply(const double* x, double* y, double at, double 
   };
   auto hout = [&](const double* vu) {
     if (np == 0) return;
-    launch(hsolve_out_kernel, dim3(fb), dim3(256), 0, s, "hsolve_out_kernel", np, S.C2.view(), vu, hlu.get(), hpiv.get(), tt.get(), at, yt);
+    launch(hsolve_out_kernel, dim3(blocks_for(np, kHoutFaces)), dim3(3 * kHoutFaces), 0, s, "hsolve_out_kernel", np, S.C2.view(), vu, hlu.get(), hpiv.get(), tt.get(), at, yt);
     cuda_check(cudaGetLastError(), "hsolve_out launch");
     if (L) L->add(S.C2.matrix_bytes() + 8.0 * nu + 72.0 * np + 4.0 * np + 16.0 * nt);
   };
@@ -657,7 +659,7 @@ void DevicePrecond::enqueue_apply(const double* x, double* y, double at, double 
     cuda_check(cudaGetLastError(), "tpu_tu launch");
     if (L) L->add(S.C1.matrix_bytes() + S.Q1.matrix_bytes() + 8.0 * (2.0 * nu + nt + np));
     amg->enqueue_apply(tu.get(), yu, nullptr, s, L, xh.get());  // v_u = AMG(S~) t_u
-    launch_sell(S.Q2, GPlain{yu}, EStore{sp_.get()}, s);  // s_p = Q2 v_u
+    launch_mat(S.Q2m, GPlain{yu}, EStore{sp_.get()}, s);  // s_p = Q2 v_u
     if (L) L->add(S.Q2.matrix_bytes() + 8.0 * (nu + np));
     enqueue_band(sp_.get(), 1.0, yp, nullptr, tp.get(), ap, 1, s, L);  // v_p = t_p - T^-1 s_p
     hout(yu);                                                          // v_t = H~^-1 C2 v_u - t_t
@@ -668,7 +670,7 @@ void DevicePrecond::enqueue_apply(const double* x, double* y, double at, double 
   if (L) L->add(S.C1.matrix_bytes() + 8.0 * (nt + 2.0 * nu));
   double* s_u = variant == fpb::kTupStar ? yu : su.get();
   amg->enqueue_apply(tu.get(), s_u, nullptr, s, L, xh.get());  // s_u = AMG(S1) t_u
-  launch_sell(S.Q2, GPlain{s_u}, ESubFromScaled{xp, ap, tp.get()}, s);  // t_p = w_p - Q2 s_u
+  launch_mat(S.Q2m, GPlain{s_u}, ESubFromScaled{xp, ap, tp.get()}, s);  // t_p = w_p - Q2 s_u
   if (L) L->add(S.Q2.matrix_bytes() + 8.0 * (nu + 2.0 * np));
   enqueue_band(tp.get(), 1.0, vp.get(), yp, nullptr, ap, 2, s, L);  // v_p = S~2^-1 t_p
   if (variant == fpb::kTupStar) return;

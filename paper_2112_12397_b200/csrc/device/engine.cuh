@@ -48,27 +48,6 @@ struct DBsr3 {
 DSell make_sell(const fpb::Csr& A);
 DBsr3 make_bsr3(const fpb::Csr& A);  // A square, n % 3 == 0
 
-class DeviceSystem {
- public:
-  explicit DeviceSystem(const fpb::HostSystem& J);
-  ~DeviceSystem();
-  DeviceSystem(const DeviceSystem&) = delete;
-  DeviceSystem& operator=(const DeviceSystem&) = delete;
-  int n_u = 0, n_t = 0, n_p = 0;
-  // the t/p rows (jtp_kernel) run on a side stream, concurrently with the A rows (fork/join
-  // through events; captured into the graphs as parallel branches)
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  int n() const { return n_u + n_t + n_p; }
-  double st = 1.0, sp = 1.0;  // driver block scaling (driver.cpp:114-125)
-  bool a_bsr3 = true;         // A as 3x3 blocks (n_u = 3 * nodes); SELL otherwise
-  DBsr3 A;
-  DSell A_sell;
-  DSell C1, Q1, C2, H, Q2, T;
-  // y = D J D x (D = blkdiag(I, st I, sp I)); st = sp = 1 gives J itself
-  void enqueue_apply(const double* x, double* y, double st_, double sp_, cudaStream_t s, Ledger* L = nullptr) const;
-  double bytes_apply() const;
-};
 
 // Plain CSR on the device, consumed one warp per row (csr_warp_kernel).
 struct DCsr {
@@ -108,7 +87,32 @@ struct DMat {
   int64_t nnz() const { return pipe ? pm.nnz : warp ? csr.nnz : sell.nnz; }
   double matrix_bytes() const { return pipe ? pm.matrix_bytes() : warp ? csr.matrix_bytes() : sell.matrix_bytes(); }
 };
-DMat make_mat(const fpb::Csr& A);
+// few_rows_parallel: operators with under 2048 rows take the row-parallel slice kernel even
+// for short rows (a thread-per-row chain would be the whole kernel's latency)
+DMat make_mat(const fpb::Csr& A, bool few_rows_parallel = false);
+
+class DeviceSystem {
+ public:
+  explicit DeviceSystem(const fpb::HostSystem& J);
+  ~DeviceSystem();
+  DeviceSystem(const DeviceSystem&) = delete;
+  DeviceSystem& operator=(const DeviceSystem&) = delete;
+  int n_u = 0, n_t = 0, n_p = 0;
+  // the t/p rows (jtp_kernel) run on a side stream, concurrently with the A rows (fork/join
+  // through events; captured into the graphs as parallel branches)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int n() const { return n_u + n_t + n_p; }
+  double st = 1.0, sp = 1.0;  // driver block scaling (driver.cpp:114-125)
+  bool a_bsr3 = true;         // A as 3x3 blocks (n_u = 3 * nodes); SELL otherwise
+  DBsr3 A;
+  DSell A_sell;
+  DSell C1, Q1, C2, H, Q2, T;
+  DMat Q2m;  // Q2 for the preconditioner's s_p / t_p products (layout chosen by make_mat)
+  // y = D J D x (D = blkdiag(I, st I, sp I)); st = sp = 1 gives J itself
+  void enqueue_apply(const double* x, double* y, double st_, double sp_, cudaStream_t s, Ledger* L = nullptr) const;
+  double bytes_apply() const;
+};
 
 struct DeviceLevel {
   bool bsr3 = false;

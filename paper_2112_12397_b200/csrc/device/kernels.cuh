@@ -33,8 +33,9 @@ struct GPresmooth {  // first Jacobi sweep from x = 0: (omega * b_j) / d_j  (amg
   __device__ __forceinline__ double operator()(int j) const { return (w * __ldg(b + j)) / __ldg(d + j); }
 };
 
-// One SELL-32 row, left to right (csr.cpp:109-119).
-template <class G>
+// One SELL-32 row, left to right (csr.cpp:109-119).  U entries per batch: all U column and
+// value loads (then all U gathers) are issued before the U ordered adds.
+template <class G, int U = 4>
 __device__ __forceinline__ double sell_row(const SellView& A, int row, const G& g) {
   const long long base = A.slice_off[row >> 5] + (row & 31);
   const int len = A.row_len[row];
@@ -42,14 +43,15 @@ __device__ __forceinline__ double sell_row(const SellView& A, int row, const G& 
   const double* __restrict__ V = A.vals + base;
   double s = 0.0;
   int k = 0;
-  for (; k + 4 <= len; k += 4) {
-    const int c0 = __ldg(C + 32 * k), c1 = __ldg(C + 32 * (k + 1)), c2 = __ldg(C + 32 * (k + 2)), c3 = __ldg(C + 32 * (k + 3));
-    const double v0 = __ldg(V + 32 * k), v1 = __ldg(V + 32 * (k + 1)), v2 = __ldg(V + 32 * (k + 2)), v3 = __ldg(V + 32 * (k + 3));
-    const double x0 = g(c0), x1 = g(c1), x2 = g(c2), x3 = g(c3);
-    s = s + v0 * x0;
-    s = s + v1 * x1;
-    s = s + v2 * x2;
-    s = s + v3 * x3;
+  for (; k + U <= len; k += U) {
+    int c[U];
+    double v[U], x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = __ldg(C + 32 * (k + u)), v[u] = __ldg(V + 32 * (k + u));
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = g(c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) s = s + v[u] * x[u];
   }
   for (; k < len; ++k) s = s + __ldg(V + 32 * k) * g(__ldg(C + 32 * k));
   return s;
@@ -493,13 +495,21 @@ __global__ void __launch_bounds__(256) hsolve_in_kernel(int n_faces, const doubl
 }
 
 // y_t = at * (H~^-1 (C2 v_u) - t_t)   (precond.cpp:163-164 / 226-227)
-__global__ void __launch_bounds__(256) hsolve_out_kernel(int n_faces, SellView C2, const double* vu, const double* hlu,
-                                                         const int* hpiv, const double* tt, double at, double* yt) {
+// 32 faces per 96-thread CTA: thread r sums C2 row r (16-wide load batches, in order), then
+// thread f of the first warp solves face f's 3x3 system from the three row sums.
+constexpr int kHoutFaces = 32;
+__global__ void __launch_bounds__(3 * kHoutFaces) hsolve_out_kernel(int n_faces, SellView C2, const double* vu,
+                                                                   const double* hlu, const int* hpiv,
+                                                                   const double* tt, double at, double* yt) {
   pdl_entry();
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= n_faces) return;
-  const double s[3] = {sell_row(C2, 3 * f, GPlain{vu}), sell_row(C2, 3 * f + 1, GPlain{vu}),
-                       sell_row(C2, 3 * f + 2, GPlain{vu})};
+  __shared__ double srow[3 * kHoutFaces];
+  const int f0 = blockIdx.x * kHoutFaces;
+  const int row = 3 * f0 + threadIdx.x;
+  if (row < 3 * n_faces) srow[threadIdx.x] = sell_row<GPlain, 16>(C2, row, GPlain{vu});
+  __syncthreads();
+  const int f = f0 + threadIdx.x;
+  if (threadIdx.x >= kHoutFaces || f >= n_faces) return;
+  const double s[3] = {srow[3 * threadIdx.x], srow[3 * threadIdx.x + 1], srow[3 * threadIdx.x + 2]};
   double x[3];
   lu3_solve_dev(hlu + 9 * size_t(f), hpiv[f], s, x);
   for (int c = 0; c < 3; ++c) yt[3 * f + c] = (x[c] - tt[3 * f + c]) * at;

@@ -1,5 +1,4 @@
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
-python -c "
-import json; d=json.loads(open('gpurun_out/bench.json').read().strip().splitlines()[-1])
-print({k: d[k] for k in ('value','ms_per_step','e2e','gpu_launches','timing','variants')})
-print(d['roofline']['achieved'], d['roofline']['frac'], d['precond_apply'], d['cpu_baseline']['value'], d['clocks'])"
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 600 python tools/scale_configs.py 2 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print({k:d[k] for k in ('apply_ms','fine_post_GBps','japply_GBps','per_iter_ms')})"
+timeout 600 python tools/profile_solve.py 2 tup 500 2>&1 | tail -1
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launch_apply_cfg2.csv python tools/profile_apply.py 2 tup 1 > gpurun_out/ncu2.log 2>&1
