@@ -169,6 +169,11 @@ int fp_precond_apply(fp_precond* p, const double* x, double* y, int32_t mem);
 int fp_amg_apply(fp_precond* p, const double* r, double* x, int32_t mem);
 /* InnerSolver::call_count / reset_count (precond.hpp:34-42) */
 int64_t fp_precond_inner_calls(fp_precond* p, int32_t reset);
+/* Where the preconditioner setup's sparse products (amg_setup's Galerkin products, the Schur
+ * cores) run: 1 = device SpGEMM (bitwise the host routine), 0 = host (default; or set
+ * FRACPREC_B200_DEVICE_SETUP=1).  Applies to builds started afterwards. */
+int fp_set_setup_backend(int32_t device);
+int fp_setup_backend(int32_t* device);
 /* The factor application the preconditioner resolved to: FP_FACTOR_SWEEP or FP_FACTOR_INVERSE */
 int fp_precond_factor_solve(const fp_precond* p, int32_t* mode);
 /* algorithmic HBM bytes and kernel launches of one fp_precond_apply / fp_system_apply */

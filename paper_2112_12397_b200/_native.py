@@ -131,6 +131,8 @@ SIGNATURES = {
     "fp_workload_info": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "fp_workload_host_precond_build": (C.c_int, [_P, C.POINTER(FpPrecondConfig), _PP]),
     "fp_workload_region": (C.c_int, [_P, C.POINTER(C.c_char_p), C.POINTER(C.c_double)]),
+    "fp_setup_backend": (C.c_int, [C.POINTER(C.c_int32)]),
+    "fp_set_setup_backend": (C.c_int, [C.c_int32]),
     "fp_snapshot_import": (C.c_int, [C.c_char_p, _PP]),
     "fp_snapshot_export": (C.c_int, [C.c_char_p, C.POINTER(FpBlockSystem), C.c_char_p, C.c_double, _DP, C.c_int32]),
 }

@@ -498,3 +498,15 @@ def export_snapshot(directory: str, J: BlockSystem, region: str, dt: float = 0.5
     cp = coords.ctypes.data_as(C.POINTER(C.c_double)) if coords is not None else None
     nn = 0 if coords is None else coords.shape[0]
     N.check(N.lib.fp_snapshot_export(str(directory).encode(), C.byref(J.view()), region.encode(), float(dt), cp, nn))
+
+
+def set_setup_backend(where: str) -> None:
+    """Run the setup's sparse products on the "device" (bitwise the host routine) or the "host"."""
+    N.check(N.lib.fp_set_setup_backend(1 if where == "device" else 0))
+
+
+def setup_backend() -> str:
+    """Where the preconditioner setup's sparse products run: "device" or "host" (the default)."""
+    d = C.c_int32()
+    N.check(N.lib.fp_setup_backend(C.byref(d)))
+    return "device" if d.value else "host"

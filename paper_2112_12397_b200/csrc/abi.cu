@@ -4,8 +4,10 @@
 // reference; fracprec.cpp:453-465 maps them to CLI exit codes the same way).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <span>
 #include <string>
 
 #include "../../include/fracprec_b200.h"
@@ -134,6 +136,27 @@ struct fp_precond {
   fpd::DevBuf<double> xin, yout, bdev, xdev;
 };
 
+namespace fpd {
+bool spgemm_device(const fpb::Csr& A, const fpb::Csr& B, std::span<const double> row_scale, fpb::Csr& C);
+}
+
+namespace {
+// The setup's SpGEMMs can run on the device (bitwise the host routine).  With the
+// hierarchy still built on the host that is transfer-bound, so the
+// default is the host; FRACPREC_B200_DEVICE_SETUP=1 or fp_set_setup_backend(1) selects
+// the device.  The environment is read on first use, not at load.
+void ensure_setup_backend() {
+  static const bool once = [] {
+    int n = 0;
+    if (std::getenv("FRACPREC_B200_DEVICE_SETUP") != nullptr && cudaGetDeviceCount(&n) == cudaSuccess && n > 0)
+      fpb::set_spgemm_backend(&fpd::spgemm_device);
+    cudaGetLastError();
+    return true;
+  }();
+  (void)once;
+}
+}  // namespace
+
 struct fp_host_precond {
   fpb::HostPrecond hp;
 };
@@ -218,6 +241,7 @@ int fp_system_apply(fp_system* s, const double* x, double* y, int32_t mem) {
 int fp_host_precond_build(const fp_block_system* J, const fp_precond_config* cfg, const double* coords,
                           int32_t n_nodes, fp_host_precond** out) {
   return guard([&] {
+    ensure_setup_backend();
     need(J && cfg && out, "fp_host_precond_build: null argument");
     need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
     const fpb::HostSystem H = to_system(*J);
@@ -302,6 +326,7 @@ int fp_precond_create(fp_system* s, const fp_host_precond* hp, fp_precond** out)
 
 int fp_precond_upload(fp_system* s, const fp_precond_desc* d, fp_precond** out) {
   return guard([&] {
+    ensure_setup_backend();
     need(s && d && out && d->levels && d->n_levels >= 1 && d->h_blocks, "fp_precond_upload: null argument");
     need(d->variant >= FP_TPU && d->variant <= FP_TUP_STAR, "fp_precond_upload: unknown variant");
     fpb::HostPrecond hp;
@@ -520,12 +545,36 @@ int fp_workload_coords(const fp_workload* w, const double** xyz, int32_t* n_node
 
 int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config* cfg, fp_host_precond** out) {
   return guard([&] {
+    ensure_setup_backend();
     need(w && cfg && out, "fp_workload_host_precond_build: null argument");
     need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
     auto p = std::make_unique<fp_host_precond>();
     p->hp = fpb::build_precond(w->w.J, cfg->variant, to_amg(cfg->amg), w->w.coords);
     p->hp.factor_solve = cfg->factor_solve;
     *out = p.release();
+  });
+}
+
+int fp_set_setup_backend(int32_t device) {
+  return guard([&] {
+    ensure_setup_backend();
+    if (!device) {
+      fpb::set_spgemm_backend(nullptr);
+      return;
+    }
+    int n = 0;
+    const bool has = cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+    cudaGetLastError();
+    need(has, "fp_set_setup_backend: no CUDA device");
+    fpb::set_spgemm_backend(&fpd::spgemm_device);
+  });
+}
+
+int fp_setup_backend(int32_t* device) {
+  return guard([&] {
+    need(device, "null argument");
+    ensure_setup_backend();
+    *device = fpb::spgemm_backend_active() ? 1 : 0;
   });
 }
 

@@ -302,15 +302,15 @@ HostAmg amg_setup(Csr A, const std::vector<std::vector<double>>& near_null, cons
     if (opt.prolongation_smoothing) {
       std::vector<double> dinv(static_cast<size_t>(n));
       for (int i = 0; i < n; ++i) dinv[i] = 1.0 / fine.diag[i];
-      P = add_scaled(P, spgemm(fine.A, P, dinv), 1.0, -opt.jacobi_omega);  // P - w D^-1 A P
+      P = add_scaled(P, spgemm_setup(fine.A, P, dinv), 1.0, -opt.jacobi_omega);  // P - w D^-1 A P
     }
     plog.mark("smoothed P", long(P.nnz()));
     if (nc > opt.stall_ratio * n) break;
-    const Csr AP = spgemm(fine.A, P);
+    const Csr AP = spgemm_setup(fine.A, P);
     plog.mark("A P", long(AP.nnz()));
     const Csr Pt = transpose(P);
     plog.mark("P^T");
-    Csr Ac = spgemm(Pt, AP);
+    Csr Ac = spgemm_setup(Pt, AP);
     plog.mark("P^T (A P)", long(Ac.nnz()));
     std::vector<std::vector<double>> nnc(static_cast<size_t>(k), std::vector<double>(static_cast<size_t>(nc), 0.0));
     for (int a = 0; a < n_agg; ++a)
@@ -448,6 +448,17 @@ std::vector<double> fixed_stress_diag(const Csr& Q2, const Csr& S1, const Csr& Q
   return sk;
 }
 
+namespace {
+SpgemmBackend g_spgemm_backend = nullptr;
+}
+void set_spgemm_backend(SpgemmBackend fn) { g_spgemm_backend = fn; }
+bool spgemm_backend_active() { return g_spgemm_backend != nullptr; }
+Csr spgemm_setup(const Csr& A, const Csr& B, std::span<const double> row_scale) {
+  Csr C;
+  if (g_spgemm_backend && g_spgemm_backend(A, B, row_scale, C)) return C;
+  return spgemm(A, B, row_scale);
+}
+
 HostPrecond build_precond(const HostSystem& J, int variant, const AmgOptions& opt,
                           const std::vector<std::array<double, 3>>& coords) {
   J.check_shapes();
@@ -456,8 +467,8 @@ HostPrecond build_precond(const HostSystem& J, int variant, const AmgOptions& op
   PhaseLog plog;
   M.variant = variant;
   M.hblocks = bdiag3_extract(J.H);
-  const Csr HinvC2 = spgemm(bdiag3_inverse_csr(M.hblocks), J.C2);
-  Csr core = add_scaled(J.A, spgemm(J.C1, HinvC2), 1.0, 1.0);
+  const Csr HinvC2 = spgemm_setup(bdiag3_inverse_csr(M.hblocks), J.C2);
+  Csr core = add_scaled(J.A, spgemm_setup(J.C1, HinvC2), 1.0, 1.0);
   plog.mark("schur core", long(core.nnz()));
   std::vector<std::vector<double>> nn;
   if (!coords.empty() && int(coords.size()) * 3 == J.n_u) nn = rigid_body_modes(coords);
@@ -468,7 +479,7 @@ HostPrecond build_precond(const HostSystem& J, int variant, const AmgOptions& op
     M.factor.factor(J.T, BandFactor::Kind::spd);
     std::vector<double> tinv(M.T_diag.size());
     for (size_t i = 0; i < tinv.size(); ++i) tinv[i] = 1.0 / M.T_diag[i];
-    Csr S = add_scaled(core, spgemm(J.Q1, scale_rows(J.Q2, tinv)), 1.0, -1.0);
+    Csr S = add_scaled(core, spgemm_setup(J.Q1, scale_rows(J.Q2, tinv)), 1.0, -1.0);
     core = Csr();  // free the fine-size temporary before the hierarchy is built
     M.amg = amg_setup(std::move(S), nn, opt);
   } else {

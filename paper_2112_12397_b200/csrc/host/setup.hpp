@@ -44,6 +44,14 @@ struct HostAmg {
   AmgOptions opt;
 };
 
+// SpGEMM of the setup (Galerkin products, Schur cores): a registered backend (the device
+// SpGEMM, csrc/device/spgemm.cu, bitwise this routine) or the host spgemm.  The backend may
+// decline a product (returns false) and the host routine runs instead.
+using SpgemmBackend = bool (*)(const Csr&, const Csr&, std::span<const double>, Csr&);
+void set_spgemm_backend(SpgemmBackend fn);
+bool spgemm_backend_active();
+Csr spgemm_setup(const Csr& A, const Csr& B, std::span<const double> row_scale = {});
+
 // Chebyshev smoother (extension): the oracle's chebyshev_lambda_max / chebyshev_coefficients
 // (oracle/amg.cpp), computed with the same operation order so the GPU matches it bit for bit.
 double chebyshev_lambda_max(const Csr& A, const std::vector<double>& diag, int iterations);

@@ -354,3 +354,29 @@ def test_chebyshev_theta0_and_gmres_match_oracle():
     assert abs(st.iterations - st_ref["iterations"]) <= 2
     if st_ref["converged"]:
         assert rel(x, x_ref) <= 1e-8
+
+
+@pytest.mark.parametrize("variant,theta", [("tpu", 0.08), ("tup", 0.08), ("tup", 0.0)])
+def test_device_setup_is_bitwise_the_oracle_setup(variant, theta):
+    """Setup on the device: the Galerkin products and Schur cores run
+    through the device SpGEMM; the hierarchy must equal the oracle's bit for bit."""
+    J = small_workload(seed=59, cells=(10, 8, 8))
+    osys = oracle_system(J)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, strength_threshold=theta)
+    api.set_setup_backend("device")
+    try:
+        assert api.setup_backend() == "device"
+        hp = api.HostPreconditioner(J, api.PrecondConfig(variant, amg=api.AmgConfig(strength_threshold=theta)))
+    finally:
+        api.set_setup_backend("host")
+    assert hp.level_sizes() == [opc.level_matrix(l, 0)[0] for l in range(opc.n_levels())]
+    for l in range(opc.n_levels()):
+        r, c, rp, ci, v = opc.level_matrix(l, 0)
+        m = hp.matrix(0, l)
+        assert np.array_equal(m.row_offsets, rp) and np.array_equal(m.col_indices, ci)
+        assert np.array_equal(m.values.view(np.uint64), v.view(np.uint64)), f"A_{l}"
+        if l > 0:
+            r, c, rp, ci, v = opc.level_matrix(l, 1)
+            m = hp.matrix(1, l)
+            assert np.array_equal(m.row_offsets, rp) and np.array_equal(m.values.view(np.uint64), v.view(np.uint64))
+    assert np.array_equal(opc.vec(), hp.vector(1))
