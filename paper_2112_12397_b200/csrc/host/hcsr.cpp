@@ -58,10 +58,24 @@ Csr build_rows(int n_rows, int n_cols, MakeScratch make_scratch, RowFn fn) {
       C.rp[size_t(c) * kChunk + q + 1] = acc;
     }
   }
-  // append chunk by chunk into reserved (untouched) storage, releasing each piece
-  // right after: the peak is one output plus one piece, not two outputs
-  C.ci.reserve(static_cast<size_t>(chunk_off[n_chunks]));
-  C.v.reserve(static_cast<size_t>(chunk_off[n_chunks]));
+  const size_t nnz = static_cast<size_t>(chunk_off[n_chunks]);
+  if (nnz * (sizeof(int) + sizeof(double)) <= (size_t(8) << 30)) {
+    // up to 8 GB of output: copy the pieces in parallel (transiently pieces + output)
+    C.ci.resize(nnz);
+    C.v.resize(nnz);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int c = 0; c < n_chunks; ++c) {
+      std::copy(pieces[c].cols.begin(), pieces[c].cols.end(), C.ci.begin() + chunk_off[c]);
+      std::copy(pieces[c].vals.begin(), pieces[c].vals.end(), C.v.begin() + chunk_off[c]);
+      std::vector<int>().swap(pieces[c].cols);
+      std::vector<double>().swap(pieces[c].vals);
+    }
+    return C;
+  }
+  // larger (config 5): append chunk by chunk into reserved (untouched) storage, releasing
+  // each piece right after, so the peak is one output plus one piece instead of two outputs
+  C.ci.reserve(nnz);
+  C.v.reserve(nnz);
   for (int c = 0; c < n_chunks; ++c) {
     C.ci.insert(C.ci.end(), pieces[c].cols.begin(), pieces[c].cols.end());
     C.v.insert(C.v.end(), pieces[c].vals.begin(), pieces[c].vals.end());
