@@ -212,6 +212,33 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_kernel(MgsArgs a) {
 // of the basis columns in registers (E per thread): step i loads V_{i+1} (and,
 // for E <= 8, already V_{i+2} before the barrier, hiding the load behind it),
 // so the only exposed latency per projection is the barrier + fixed-order sum.
+// Leaner fixed-order reductions for mgs_fast_kernel: warp shuffles, then warp 0
+// combines the warp sums (one block barrier); after the grid barrier warp 0 alone
+// reads the nb partials and broadcasts through shared memory (one more barrier).
+// Same order in every block and every run: deterministic.
+__device__ __forceinline__ double block_sum_w0(double v, double* sm) {  // valid in warp 0
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (w == 0) {
+    s = l < int(blockDim.x >> 5) ? sm[l] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  return s;
+}
+__device__ __forceinline__ double grid_total_w0(const double* part, int nb, double* sm) {
+  if (threadIdx.x < 32) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < nb; b += 32) v += __ldcg(part + b);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) sm[36] = v;
+  }
+  __syncthreads();
+  return sm[36];
+}
+
 template <int E>
 __global__ void __launch_bounds__(kMgsThreads) mgs_fast_kernel(MgsArgs a) {
   namespace cg = cooperative_groups;
@@ -225,11 +252,10 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_fast_kernel(MgsArgs a) {
   const int len = lo < a.n ? int(min(chunk, a.n - lo)) : 0;
   int buf = 0;
   auto publish = [&](double v) {
-    const double s = block_sum(v, sm);
+    const double s = block_sum_w0(v, sm);
     if (threadIdx.x == 0) a.partial[buf * nb + blockIdx.x] = s;
     grid.sync();
-    const double t = grid_total(a.partial + buf * nb, nb, sm);
-    __syncthreads();
+    const double t = grid_total_w0(a.partial + buf * nb, nb, sm);
     buf ^= 1;
     return t;
   };
@@ -253,8 +279,8 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_fast_kernel(MgsArgs a) {
       n2 += v * v;
       d0 += vc[j] * v;
     }
-    const double s = block_sum(n2, sm);
-    const double t = block_sum(d0, sm);
+    const double s = block_sum_w0(n2, sm);
+    const double t = block_sum_w0(d0, sm + 16);
     if (threadIdx.x == 0) {
       a.partial[2 * nb + blockIdx.x] = s;
       a.partial[3 * nb + blockIdx.x] = t;
@@ -262,10 +288,9 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_fast_kernel(MgsArgs a) {
     if (kAhead && a.m >= 1) load(a.V + a.ldv, vn);
     grid.sync();
   }
-  const double wnorm_pre = sqrt(grid_total(a.partial + 2 * nb, nb, sm));
+  const double wnorm_pre = sqrt(grid_total_w0(a.partial + 2 * nb, nb, sm));
   __syncthreads();
-  const double h0 = grid_total(a.partial + 3 * nb, nb, sm);
-  __syncthreads();
+  const double h0 = grid_total_w0(a.partial + 3 * nb, nb, sm);
   if (!isfinite(wnorm_pre)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       a.status->nonfinite = 1;

@@ -1,2 +1,3 @@
-for c in 2 3 4; do timeout 900 python tools/setup_time.py $c 2>&1 | tail -1; done
-FRACPREC_B200_VERBOSE=1 timeout 900 python tools/setup_time.py 3 2>&1 | grep -v "level start" | head -9
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+timeout 600 python tools/profile_solve.py 2 tup 500 2>&1 | tail -1
+timeout 600 python tools/profile_solve.py 3 tup 100 2>&1 | tail -1
