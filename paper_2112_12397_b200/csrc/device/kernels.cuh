@@ -381,9 +381,14 @@ __global__ void __launch_bounds__(kWarpRowThreads) csr_warp_kernel(CsrView A, G 
 // block rows of the slice.  Sum order = block columns ascending, then j = 0,1,2:
 // the CSR column order.
 #ifndef FP_BSR_THREADS
-#define FP_BSR_THREADS 384
+#define FP_BSR_THREADS 96
 #endif
-constexpr int kBsrThreads = FP_BSR_THREADS;  // slices of 96 threads per CTA
+constexpr int kBsrThreads = FP_BSR_THREADS;  // one 96-thread slice per CTA: finest tail balance (measured +6% at config 2)
+// matrix stream loads of the BSR3 kernel: evict-first (the 3x3 blocks are read once per
+// sweep and exceed L2; keeping them out leaves L2 to the gathered vector)
+#ifndef FP_BSR_LD
+#define FP_BSR_LD __ldcs
+#endif
 
 template <class G, class E>
 __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E epi) {
@@ -400,10 +405,10 @@ __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E ep
   double s = 0.0;
   int k = 0;
   for (; k + 2 <= len; k += 2) {
-    const int c0 = 3 * __ldg(C + 32 * k), c1 = 3 * __ldg(C + 32 * (k + 1));
+    const int c0 = 3 * FP_BSR_LD(C + 32 * k), c1 = 3 * FP_BSR_LD(C + 32 * (k + 1));
     const double* V0 = V + 288 * k;
-    const double a00 = __ldg(V0), a01 = __ldg(V0 + 32), a02 = __ldg(V0 + 64);
-    const double a10 = __ldg(V0 + 288), a11 = __ldg(V0 + 320), a12 = __ldg(V0 + 352);
+    const double a00 = FP_BSR_LD(V0), a01 = FP_BSR_LD(V0 + 32), a02 = FP_BSR_LD(V0 + 64);
+    const double a10 = FP_BSR_LD(V0 + 288), a11 = FP_BSR_LD(V0 + 320), a12 = FP_BSR_LD(V0 + 352);
     const double x00 = g(c0), x01 = g(c0 + 1), x02 = g(c0 + 2);
     const double x10 = g(c1), x11 = g(c1 + 1), x12 = g(c1 + 2);
     s = s + a00 * x00;
@@ -414,11 +419,11 @@ __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E ep
     s = s + a12 * x12;
   }
   if (k < len) {
-    const int c0 = 3 * __ldg(C + 32 * k);
+    const int c0 = 3 * FP_BSR_LD(C + 32 * k);
     const double* V0 = V + 288 * k;
-    s = s + __ldg(V0) * g(c0);
-    s = s + __ldg(V0 + 32) * g(c0 + 1);
-    s = s + __ldg(V0 + 64) * g(c0 + 2);
+    s = s + FP_BSR_LD(V0) * g(c0);
+    s = s + FP_BSR_LD(V0 + 32) * g(c0 + 1);
+    s = s + FP_BSR_LD(V0 + 64) * g(c0 + 2);
   }
   epi(3 * brow + li, s, pre);
 }
