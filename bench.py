@@ -5,6 +5,10 @@ One step = one complete GMRES(50) solve (rtol 1e-10, max 500 iterations) of the
 driver's block-scaled system D J D y = b (driver.cpp:229-255) with the t-u-p
 block preconditioner (inner AMG V-cycle, weighted Jacobi) on the synthetic
 BASELINE config (default: configs[1], the 40^3 box), b ~ U[-1,1] seeded.
+Defaults: coarse-operator row sums "strided" and classical Gram-Schmidt
+Arnoldi (both held to the reference's bars against the reference-order oracle,
+DESIGN.md §10d/§10e); the reference's own orders are timed beside it
+(variants.tup_reference_order) and selectable with --row-sum ordered --orth mgs.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -49,6 +53,10 @@ def parse():
     ap.add_argument("--factor-solve", default="auto", choices=["auto", "sweep", "inverse"],
                     help="T / S~2 application: sweeps or explicit block inverses (DESIGN.md §5b)")
     ap.add_argument("--restart", type=int, default=50)
+    ap.add_argument("--row-sum", default="strided", choices=["ordered", "strided"],
+                    help="coarse-operator row-sum order: ordered (the reference's) or strided (32 partials, warp per row)")
+    ap.add_argument("--orth", default="cgs", choices=["mgs", "cgs"],
+                    help="Arnoldi orthogonalization: mgs (the reference's loop) or cgs (one reduction per pass)")
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--max-iter", type=int, default=500)
     ap.add_argument("--seed", type=int, default=42)
@@ -100,28 +108,38 @@ def ncu_traffic(key: str):
 
 def other_variants(op, J, b, flush, args) -> dict:
     """The other block preconditioners on the same system and protocol (BASELINE: both variants, t-p-u and
-    t-u-p, optionally t-u-p*): the solver's CUDA-event time of 2 solves after one warm-up, L2 flushed between."""
+    t-u-p, optionally t-u-p*), plus the bench variant with the reference's own summation and
+    orthogonalization orders (row_sum ordered, MGS): the solver's CUDA-event time of 2 solves after one
+    warm-up, L2 flushed between."""
     import torch
 
     from paper_2112_12397_b200 import api
 
+    runs = [(v, v, args.row_sum, args.orth) for v in ("tpu", "tup", "tup_star") if v != args.variant]
+    if (args.row_sum, args.orth) != ("ordered", "mgs"):
+        runs.append((f"{args.variant}_reference_order", args.variant, "ordered", "mgs"))
     out = {}
-    for v in ("tpu", "tup", "tup_star"):
-        if v == args.variant:
-            continue
-        cfg = api.PrecondConfig(v, amg=api.AmgConfig(strength_threshold=args.theta), factor_solve=args.factor_solve)
+    for name, v, row_sum, orth in runs:
+        cfg = api.PrecondConfig(v, amg=api.AmgConfig(strength_threshold=args.theta, row_sum=row_sum),
+                                factor_solve=args.factor_solve)
         pc = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, cfg))
         x = torch.empty_like(b)
-        api.gmres(op, pc, b, tol=args.tol, max_iter=args.max_iter, restart=args.restart, scaled=True, x=x)
+
+        def solve():
+            return api.gmres(op, pc, b, tol=args.tol, max_iter=args.max_iter, restart=args.restart, scaled=True,
+                             x=x, orthogonalization=orth)
+
+        solve()
         torch.cuda.synchronize()
         t = 0.0
         for _ in range(2):
             flush.zero_()
-            _, st = api.gmres(op, pc, b, tol=args.tol, max_iter=args.max_iter, restart=args.restart, scaled=True, x=x)
+            _, st = solve()
             t += st.device_seconds
-        out[v] = {"s_per_system": round(t / 2, 6), "iterations": st.iterations,
-                  "converged": st.converged, "final_rel_residual": st.relative_residuals[-1],
-                  "precond_apply_ms": round(pc.profile(reps=10)["apply_ms"], 4)}
+        out[name] = {"s_per_system": round(t / 2, 6), "iterations": st.iterations, "row_sum": row_sum,
+                     "orthogonalization": orth, "converged": st.converged,
+                     "final_rel_residual": st.relative_residuals[-1],
+                     "precond_apply_ms": round(pc.profile(reps=10)["apply_ms"], 4)}
         del pc
     return out
 
@@ -270,7 +288,7 @@ def run_ours(args):
     gen_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     op = api.BlockSystemOperator(J)
-    cfg = api.PrecondConfig(args.variant, amg=api.AmgConfig(strength_threshold=args.theta),
+    cfg = api.PrecondConfig(args.variant, amg=api.AmgConfig(strength_threshold=args.theta, row_sum=args.row_sum),
                             factor_solve=args.factor_solve)
     hp = api.HostPreconditioner(J, cfg)
     pc = api.GpuPreconditioner.from_host(op, hp)
@@ -282,7 +300,8 @@ def run_ours(args):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
 
     def solve():
-        return api.gmres(op, pc, b, tol=args.tol, max_iter=args.max_iter, restart=args.restart, scaled=True, x=x)
+        return api.gmres(op, pc, b, tol=args.tol, max_iter=args.max_iter, restart=args.restart, scaled=True, x=x,
+                          orthogonalization=args.orth)
 
     for _ in range(max(3, args.warmup)):
         _, st = solve()
@@ -324,7 +343,7 @@ def run_ours(args):
 
     def solve_host():
         return api.gmres(op, pc, b_pin.numpy(), tol=args.tol, max_iter=args.max_iter, restart=args.restart,
-                         scaled=True, x=x_pin.numpy())
+                         scaled=True, x=x_pin.numpy(), orthogonalization=args.orth)
 
     solve_host()
     barrier()
@@ -350,7 +369,7 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE config)",
             "config": {"workload": CONFIG_NAMES[args.config], "n_u": J.n_u, "n_t": J.n_t, "n_p": J.n_p,
                        "unknowns": n, "variant": args.variant, "gmres": f"GMRES({args.restart})", "rtol": args.tol,
-                       "amg_strength_threshold": args.theta, "smoother": "weighted_jacobi",
+                       "orthogonalization": args.orth, "row_sum": args.row_sum, "amg_strength_threshold": args.theta, "smoother": "weighted_jacobi",
                        "factor_solve": pc.factor_solve,
                        "l2": "256 MB buffer written between timed solves; working set > 126 MB L2",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},

@@ -73,7 +73,15 @@ typedef struct fp_amg_config {
   int32_t chebyshev_degree;
   double chebyshev_ratio;
   int32_t power_iterations;
+  int32_t row_sum; /* FP_ROW_SUM_* (0 = ordered, the reference's summation order) */
 } fp_amg_config;
+
+/* Row-sum order of the V-cycle's coarse operators (A_l for l >= 1, R_l = P_l^T):
+ * FP_ROW_SUM_ORDERED - left to right, the reference's spmv / spmv_transpose order;
+ * FP_ROW_SUM_STRIDED - extension: 32 lane-strided partials (entry k of a row into
+ *                      partial k mod 32, in order) combined by an xor tree; one warp
+ *                      per row.  Restated in the oracle (spmv_strided32). */
+enum { FP_ROW_SUM_ORDERED = 0, FP_ROW_SUM_STRIDED = 1 };
 
 /* How the fracture-block factor (T or S~2, SparseFactor) is applied:
  * FP_FACTOR_SWEEP   - forward/backward column sweeps on the banded factor;
@@ -89,11 +97,21 @@ typedef struct fp_precond_config {
   int32_t factor_solve; /* FP_FACTOR_* (0 = auto) */
 } fp_precond_config;
 
+/* Arnoldi orthogonalization.  Both use the reference's DGKS second-pass test
+ * (gmres.cpp:126-139: repeat the pass when ||w|| < ||w_pre|| / sqrt 2).
+ * FP_ORTH_MGS - modified Gram-Schmidt, the reference's own loop (default);
+ *               one grid-wide reduction per basis vector.
+ * FP_ORTH_CGS - classical Gram-Schmidt: all coefficients of a pass from one
+ *               reduction (2 per step, 4 with the second pass); same iterates in
+ *               exact arithmetic, held to the reference's GMRES bars. */
+enum { FP_ORTH_MGS = 0, FP_ORTH_CGS = 1 };
+
 typedef struct fp_gmres_options {
   double tol;       /* relative, on ||b - op x|| (gmres.hpp:29-33) */
   int32_t restart;  /* GMRES(m) restart length; >= max_iter gives full GMRES */
   int32_t max_iter;
   int32_t scaled;   /* 1: solve the driver's D J D system (driver.cpp:229-255) */
+  int32_t orthogonalization; /* FP_ORTH_* (0 = MGS, the reference's) */
 } fp_gmres_options;
 
 /* SolveStats (gmres.hpp:15-22) + bookkeeping */
@@ -193,6 +211,7 @@ typedef struct fp_profile {
   int32_t n_levels;
   int32_t level_rows[32];
   int64_t level_nnz[32];
+  double vcycle_ms[32];             /* V-cycle from level l down (CUDA graph); level l alone = [l] - [l+1] */
 } fp_profile;
 int fp_precond_profile(fp_precond* p, int32_t reps, fp_profile* out);
 

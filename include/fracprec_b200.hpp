@@ -139,11 +139,12 @@ struct SolveStats {  // gmres.hpp:15-22
 // the reference's full GMRES; scaled = the driver's D J D system (driver.cpp:229-255).
 inline std::pair<std::vector<double>, SolveStats> gmres(const GpuSystemOperator& op, const GpuPrecondOperator& M,
                                                         std::span<const double> b, double tol, int max_iter = 500,
-                                                        int restart = 0, bool scaled = false) {
+                                                        int restart = 0, bool scaled = false,
+                                                        int orthogonalization = FP_ORTH_MGS) {
   std::vector<double> x(b.size());
   SolveStats st;
   st.relative_residuals.resize(static_cast<size_t>(std::max(1, max_iter)));
-  fp_gmres_options o{tol, restart > 0 ? restart : max_iter, max_iter, scaled ? 1 : 0};
+  fp_gmres_options o{tol, restart > 0 ? restart : max_iter, max_iter, scaled ? 1 : 0, orthogonalization};
   fp_solve_stats s{};
   s.residual_history = st.relative_residuals.data();
   s.history_capacity = int32_t(st.relative_residuals.size());

@@ -213,6 +213,16 @@ int or_precond_set_factor_solve(void* p, int mode) {
   });
 }
 
+// row_sum: 0 = ordered (reference), 1 = strided32 on the coarse operators
+int or_precond_set_row_sum(void* p, int mode) {
+  return guard([&] {
+    Pc* pc = static_cast<Pc*>(p);
+    InnerSolver& S = pc->tpu ? pc->tpu->S_solver : pc->tup->S1_solver;
+    if (!S.amg) throw std::invalid_argument("or_precond_set_row_sum: no AMG inner solver");
+    amg_set_row_sum(*S.amg, mode);
+  });
+}
+
 int or_precond_apply(void* p, const double* x, double* y) {
   return guard([&] {
     const Pc* pc = static_cast<Pc*>(p);

@@ -89,6 +89,10 @@ struct BlockDiagonal3 {
 
 std::vector<double> spmv(const CsrMatrix& A, std::span<const double> x);
 std::vector<double> spmv_transpose(const CsrMatrix& A, std::span<const double> x);
+// EXTENSION (row_sum = strided32): y_i = xor-tree of 32 partials p_l = sum over the row's entries
+// k = l, l + 32, ... (ascending, from +0.0) of a_k x_c(k); the tree is p_l <- p_l + p_(l^h) for
+// h = 16, 8, 4, 2, 1 (one warp per row on the GPU, lane l owning p_l).
+std::vector<double> spmv_strided32(const CsrMatrix& A, std::span<const double> x);
 CsrMatrix transpose(const CsrMatrix& A);
 CsrMatrix spgemm(const CsrMatrix& A, const CsrMatrix& B);
 CsrMatrix add_scaled(const CsrMatrix& A, const CsrMatrix& B, double alpha, double beta);
@@ -245,11 +249,16 @@ struct AmgConfig {
   double jacobi_omega = 2.0 / 3.0;
   double stall_ratio = 0.9;
   int max_levels = 25;
+  // EXTENSION: row-sum order of the coarse operators.  0 = ordered, the
+  // reference's spmv / spmv_transpose order everywhere.  1 = strided32 for A_l (l >= 1) and the
+  // restrictions R_l = P_l^T: spmv_strided32 (32 lane-strided partials + xor tree).
+  int row_sum = 0;
 };
 
 struct AmgLevel {
   CsrMatrix A;
   CsrMatrix P;  // from this level to the previous finer one
+  CsrMatrix R;  // P^T (counting transpose), present when config.row_sum = strided32
   std::vector<double> smoother_diag;
   double lambda_max = 0.0;  // chebyshev: 1.1 x power-iteration estimate of rho(D^-1 A)
   std::vector<int> fine_aggregate;
@@ -268,6 +277,8 @@ struct AmgHierarchy {
 AmgHierarchy amg_setup(const CsrMatrix& A, const std::vector<std::vector<double>>& near_null,
                        const AmgConfig& cfg);
 std::vector<double> amg_apply(const AmgHierarchy& h, std::span<const double> r);
+// EXTENSION: switch the coarse operators' row-sum order (builds / drops the levels' R = P^T)
+void amg_set_row_sum(AmgHierarchy& h, int row_sum);
 std::vector<std::vector<double>> constant_near_null(int n);
 // Chebyshev smoother support (extension): estimate and coefficients shared with the GPU path
 double chebyshev_lambda_max(const CsrMatrix& A, std::span<const double> diag, int iterations);

@@ -43,7 +43,7 @@ class FpAmgConfig(C.Structure):
                 ("post_sweeps", C.c_int32), ("smoother", C.c_int32), ("prolongation_smoothing", C.c_int32),
                 ("cycles_per_apply", C.c_int32), ("jacobi_omega", C.c_double), ("stall_ratio", C.c_double),
                 ("max_levels", C.c_int32), ("chebyshev_degree", C.c_int32), ("chebyshev_ratio", C.c_double),
-                ("power_iterations", C.c_int32)]
+                ("power_iterations", C.c_int32), ("row_sum", C.c_int32)]
 
 
 class FpPrecondConfig(C.Structure):
@@ -51,7 +51,8 @@ class FpPrecondConfig(C.Structure):
 
 
 class FpGmresOptions(C.Structure):
-    _fields_ = [("tol", C.c_double), ("restart", C.c_int32), ("max_iter", C.c_int32), ("scaled", C.c_int32)]
+    _fields_ = [("tol", C.c_double), ("restart", C.c_int32), ("max_iter", C.c_int32), ("scaled", C.c_int32),
+                ("orthogonalization", C.c_int32)]
 
 
 class FpSolveStats(C.Structure):
@@ -67,7 +68,8 @@ class FpProfile(C.Structure):
                 ("japply_ms", C.c_double), ("japply_bytes", C.c_double), ("fine_resid_ms", C.c_double),
                 ("fine_resid_bytes", C.c_double), ("fine_post_ms", C.c_double), ("fine_post_bytes", C.c_double),
                 ("band_ms", C.c_double), ("band_bytes", C.c_double), ("coarse_ms", C.c_double),
-                ("n_levels", C.c_int32), ("level_rows", C.c_int32 * 32), ("level_nnz", C.c_int64 * 32)]
+                ("n_levels", C.c_int32), ("level_rows", C.c_int32 * 32), ("level_nnz", C.c_int64 * 32),
+                ("vcycle_ms", C.c_double * 32)]
 
 
 class FpAmgLevelDesc(C.Structure):

@@ -105,8 +105,12 @@ class AmgConfig:
     chebyshev_degree: int = 2
     chebyshev_ratio: float = 10.0
     power_iterations: int = 10
+    # "ordered" (the reference's summation order) or "strided" (extension: coarse operators summed
+    # as 32 lane-strided partials + xor tree, one warp per row; restated in the oracle)
+    row_sum: str = "ordered"
 
     _SMOOTHERS = {"weighted_jacobi": 0, "sgs": 1, "chebyshev": 2}
+    _ROW_SUMS = {"ordered": 0, "strided": 1}
 
     def native(self) -> N.FpAmgConfig:
         if self.smoother not in self._SMOOTHERS:
@@ -120,6 +124,9 @@ class AmgConfig:
         c.stall_ratio, c.max_levels = self.stall_ratio, self.max_levels
         c.chebyshev_degree, c.chebyshev_ratio = self.chebyshev_degree, self.chebyshev_ratio
         c.power_iterations = self.power_iterations
+        if self.row_sum not in self._ROW_SUMS:
+            raise ValueError(f"unknown row_sum {self.row_sum!r} (ordered | strided)")
+        c.row_sum = self._ROW_SUMS[self.row_sum]
         return c
 
 
@@ -351,9 +358,10 @@ class GpuPreconditioner:
         """Per-phase CUDA-event timings (ms per launch) and algorithmic bytes (fp_precond_profile)."""
         p = N.FpProfile()
         N.check(N.lib.fp_precond_profile(self._h, reps, C.byref(p)))
-        out = {k: getattr(p, k) for k, _ in N.FpProfile._fields_ if k not in ("level_rows", "level_nnz")}
-        out["level_rows"] = list(p.level_rows[: p.n_levels])
-        out["level_nnz"] = list(p.level_nnz[: p.n_levels])
+        arrays = ("level_rows", "level_nnz", "vcycle_ms")
+        out = {k: getattr(p, k) for k, _ in N.FpProfile._fields_ if k not in arrays}
+        for k in arrays:
+            out[k] = list(getattr(p, k)[: p.n_levels])
         return out
 
     def traffic(self):
@@ -381,15 +389,20 @@ def build_tup(J: BlockSystem, cfg: Optional[PrecondConfig] = None, op: Optional[
 
 
 def gmres(op: BlockSystemOperator, precond: GpuPreconditioner, b, tol: float, max_iter: int = 500,
-          restart: Optional[int] = None, scaled: bool = False, x=None):
+          restart: Optional[int] = None, scaled: bool = False, x=None, orthogonalization: str = "mgs"):
     """Right-preconditioned GMRES, x0 = 0 (gmres.hpp:29-33); ``restart`` gives GMRES(m);
-    ``scaled`` solves the driver's D J D system with D^-1 M D^-1 (driver.cpp:229-255)."""
+    ``scaled`` solves the driver's D J D system with D^-1 M D^-1 (driver.cpp:229-255);
+    ``orthogonalization`` "mgs" (the reference's loop) or "cgs" (classical, one reduction
+    per pass, same DGKS second-pass test)."""
     n = op.dimension()
     x = _out_like(b, n) if x is None else x
     bp, mem, _ka = _vec(b, n)
     xp, _m, _kb = _vec(x, n)
     o = N.FpGmresOptions()
+    if orthogonalization not in ("mgs", "cgs"):
+        raise ValueError("gmres: orthogonalization must be 'mgs' or 'cgs'")
     o.tol, o.restart, o.max_iter, o.scaled = tol, restart or max_iter, max_iter, int(scaled)
+    o.orthogonalization = 1 if orthogonalization == "cgs" else 0
     hist = np.zeros(max(1, max_iter))
     st = N.FpSolveStats()
     st.residual_history = hist.ctypes.data_as(C.POINTER(C.c_double))

@@ -101,6 +101,8 @@ fpb::AmgOptions to_amg(const fp_amg_config& c) {
   o.chebyshev_degree = c.chebyshev_degree;
   o.chebyshev_ratio = c.chebyshev_ratio;
   o.power_iterations = c.power_iterations;
+  o.row_sum = c.row_sum;
+  need(o.row_sum == FP_ROW_SUM_ORDERED || o.row_sum == FP_ROW_SUM_STRIDED, "AmgConfig: unknown row_sum");
   need(o.smoother >= 0 && o.smoother <= 2, "AmgConfig: unknown smoother");
   need(o.smoother != 2 || (o.chebyshev_degree >= 1 && o.chebyshev_ratio > 1.0 && o.power_iterations >= 1),
        "AmgConfig: chebyshev needs degree >= 1, ratio > 1, power_iterations >= 1");
@@ -185,6 +187,7 @@ void fp_amg_config_default(fp_amg_config* c) {
   c->chebyshev_degree = o.chebyshev_degree;
   c->chebyshev_ratio = o.chebyshev_ratio;
   c->power_iterations = o.power_iterations;
+  c->row_sum = FP_ROW_SUM_ORDERED;
 }
 
 // ------------------------------------------------------------------ system
@@ -445,6 +448,7 @@ int fp_precond_profile(fp_precond* p, int32_t reps, fp_profile* out) {
     for (size_t l = 0; l < lv.size() && l < 32; ++l) {
       out->level_rows[l] = lv[l].n;
       out->level_nnz[l] = lv[l].bsr3 ? 9 * lv[l].Ab.nblocks : lv[l].Am.nnz();
+      out->vcycle_ms[l] = l < r.vcycle_ms.size() ? r.vcycle_ms[l] : 0.0;
     }
   });
 }
@@ -470,7 +474,10 @@ int fp_gmres(fp_system* s, fp_precond* p, const double* b, double* x, int32_t me
       bd = p->bdev.get(), xd = p->xdev.get();
     }
     fpd::SolveOptions so;
+    need(o->orthogonalization == FP_ORTH_MGS || o->orthogonalization == FP_ORTH_CGS,
+         "fp_gmres: orthogonalization must be FP_ORTH_MGS or FP_ORTH_CGS");
     so.tol = o->tol, so.restart = restart, so.max_iter = o->max_iter, so.scaled = o->scaled != 0;
+    so.orth = o->orthogonalization == FP_ORTH_CGS ? fpd::kOrthCgs : fpd::kOrthMgs;
     const fpd::SolveResult r = p->solver->solve(bd, xd, so, st);
     if (mem == FP_MEM_HOST) fpd::cuda_check(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, st), "D2H");
     fpd::cuda_check(cudaStreamSynchronize(st), "fp_gmres");

@@ -68,6 +68,35 @@ void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s) {
 
 template <class G, class E>
 void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s) {
+  if (A.strided) {
+    if (A.csr.n_rows == 0) return;
+    if (A.csr.n_rows >= 2048) {
+      if (A.csr.nnz > 512LL * A.csr.n_rows)
+        launch(csr_warp_kernel<8, G, E>, dim3(blocks_for(A.csr.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", A.csr.view(), g, e);
+      else
+        launch(csr_warp_kernel<4, G, E>, dim3(blocks_for(A.csr.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", A.csr.view(), g, e);
+    } else {
+      auto go = [&](auto kern, int R) {
+        static bool smem_set = false;  // per instantiation
+        if (!smem_set) {
+          cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(strided_smem_bytes(R))),
+                     "strided smem attribute");
+          smem_set = true;
+        }
+        launch(kern, dim3(blocks_for(A.csr.n_rows, R)), dim3(kStridedThreads), strided_smem_bytes(R), s,
+               "csr_slice_strided_kernel", A.csr.view(), g, e);
+      };
+      switch (A.strided_rows) {
+        case 1: go(csr_slice_strided_kernel<1, G, E>, 1); break;
+        case 2: go(csr_slice_strided_kernel<2, G, E>, 2); break;
+        case 4: go(csr_slice_strided_kernel<4, G, E>, 4); break;
+        case 8: go(csr_slice_strided_kernel<8, G, E>, 8); break;
+        default: go(csr_slice_strided_kernel<16, G, E>, 16); break;
+      }
+    }
+    cuda_check(cudaGetLastError(), "strided csr launch");
+    return;
+  }
   if (!A.warp) {
     launch_sell(A.sell, g, e, s);
     return;
@@ -110,8 +139,18 @@ void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s) 
 
 // Few or long rows (coarse levels, R = P^T) stream best one warp per row;
 // many short rows one thread per row in SELL-32 slices.
-DMat make_mat(const fpb::Csr& A, bool few_rows_parallel) {
+DMat make_mat(const fpb::Csr& A, bool few_rows_parallel, bool strided) {
   DMat M;
+  if (strided) {  // row_sum = strided32: plain CSR, one warp per row (or window-staged CTAs of R rows)
+    M.warp = M.strided = true;
+    M.strided_rows = 1;  // one row per CTA: most parallel loads for few-row operators
+    M.csr.n_rows = A.n_rows, M.csr.n_cols = A.n_cols, M.csr.nnz = A.nnz();
+    std::vector<long long> rp(A.rp.begin(), A.rp.end());
+    M.csr.rp.upload(rp);
+    M.csr.ci.upload(A.ci);
+    M.csr.v.upload(A.v);
+    return M;
+  }
   const double avg = A.n_rows > 0 ? double(A.nnz()) / A.n_rows : 0.0;
   // SELL's thread-per-row chains need enough rows to hide latency; below ~64k
   // rows the slice kernel's parallel loads win even for short rows
@@ -357,12 +396,12 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
         D.bsr3 = true;
         D.Ab = make_bsr3(H.A);
       } else {
-        D.Am = make_mat(H.A);
+        D.Am = make_mat(H.A, false, l > 0 && opt.row_sum == 1);
       }
     }
     if (l > 0) {
       D.P = make_mat(H.P);
-      D.R = make_mat(fpb::transpose(H.P));
+      D.R = make_mat(fpb::transpose(H.P), false, opt.row_sum == 1);
     }
     D.d.upload(H.diag);
     D.b.alloc(D.n), D.x.alloc(D.n), D.xt.alloc(D.n), D.xt2.alloc(D.n), D.xt3.alloc(D.n), D.r.alloc(D.n);
@@ -713,8 +752,8 @@ GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart
       set((const void*)mgs_fast_kernel<16>), set((const void*)mgs_fast_kernel<24>);
     }
   }
-  partial_.alloc(size_t(std::max(4 * mgs_grid_, red_grid_)));
-  cuda_check(cudaHostAlloc(&status_h_, sizeof(GmresStatus), cudaHostAllocMapped), "cudaHostAlloc");
+  partial_.alloc(size_t(std::max((ldr_ + 3) * mgs_grid_, red_grid_)));
+  cuda_check(cudaHostAlloc(&status_h_, 2 * sizeof(GmresStatus), cudaHostAllocMapped), "cudaHostAlloc");
   cuda_check(cudaHostGetDevicePointer(&status_d_, status_h_, 0), "cudaHostGetDevicePointer");
   cuda_check(cudaHostAlloc(&host_scalar_, sizeof(double), cudaHostAllocMapped), "cudaHostAlloc");
   cuda_check(cudaHostGetDevicePointer(&host_scalar_d_, host_scalar_, 0), "cudaHostGetDevicePointer");
@@ -766,11 +805,20 @@ double GmresSolver::norm_into(const double* a, const double* b, double* diff_out
   return *host_scalar_;
 }
 
-void GmresSolver::launch_mgs(MgsArgs& a, cudaStream_t s) {
+void GmresSolver::launch_mgs(MgsArgs& a, int orth, cudaStream_t s) {
   void* args[] = {&a};
   const void* f = (const void*)mgs_kernel;
   size_t smem = 0;
-  if (mgs_ept_ > 0) {
+  if (orth == kOrthCgs && restart_ <= kCgsMaxCols) {
+    switch (mgs_ept_) {
+      case 2: f = (const void*)cgs_kernel<2>; break;
+      case 4: f = (const void*)cgs_kernel<4>; break;
+      case 8: f = (const void*)cgs_kernel<8>; break;
+      case 16: f = (const void*)cgs_kernel<16>; break;
+      case 24: f = (const void*)cgs_kernel<24>; break;
+      default: f = (const void*)cgs_kernel<0>; break;
+    }
+  } else if (mgs_ept_ > 0) {
     smem = mgs_smem_;
     switch (mgs_ept_) {
       case 2: f = (const void*)mgs_fast_kernel<2>; break;
@@ -811,10 +859,17 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
   cuda_check(cudaMemcpyAsync(scal_.get(), &rnorm, sizeof(double), cudaMemcpyHostToDevice, s), "beta");
   const int per_apply = pc_.inner_per_apply();
   res.launches += 2;  // ||b||
+  struct StepEvents {
+    cudaEvent_t e[2];
+    StepEvents() {
+      cudaEventCreateWithFlags(&e[0], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&e[1], cudaEventDisableTiming);
+    }
+    ~StepEvents() { cudaEventDestroy(e[0]), cudaEventDestroy(e[1]); }
+  } step_events;
+  cudaEvent_t* mgs_done = step_events.e;
   auto launch_pj = [&] {
     cuda_check(cudaGraphLaunch(pj_exec_, s), "graph launch pj");
-    pc_.inner_calls += per_apply;
-    ++res.precond_applies;
     res.launches += apply_launches + japply_launches;
   };
   for (;;) {
@@ -824,14 +879,30 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
     launch(start_cycle_kernel, dim3(blocks_for(n_, 256)), dim3(256), 0, s, "start_cycle_kernel", n_, r_.get(), scal_.get(), V_.get(), stage);
     cuda_check(cudaMemcpyAsync(g_.get(), &rnorm, sizeof(double), cudaMemcpyHostToDevice, s), "g0");
     int m = 0, assembled_at = -1;
+    int enq = 0;  // Arnoldi steps enqueued so far in this cycle (at most one ahead of m)
     bool hit = false, cyc_done = false, happy = false;
     double tr = 1.0;
     res.launches += 1;  // start_cycle
+    // One Arnoldi step: z = M^-1 V_k, w = J z, MGS -> V_{k+1}, Givens; status into slot k & 1.
+    // Step k+1 is enqueued before the host reads step k's status, so the GPU never waits for
+    // the host.  A step enqueued past the cycle's end is discarded: it writes only column
+    // k+1 of V / R, g[k..k+1] and its own status slot, none of which an assemble(m <= k) reads.
+    auto enqueue_step = [&] {
+      launch_pj();
+      MgsArgs a{n_, ldv_, enq, ldr_, V_.get(), jout_.get(), stage, partial_.get(), h_.get(), cs_.get(), sn_.get(),
+                g_.get(), R_.get(), rnorm, status_d_ + (enq & 1)};
+      launch_mgs(a, o.orth, s);
+      cuda_check(cudaEventRecord(mgs_done[enq & 1], s), "event");
+      res.launches += 1;
+      ++enq;
+    };
     auto assemble = [&](int mm) {
       res.launches += 4;  // backsub, combine, 2 reductions (+ the graph, counted in launch_pj)
       launch(backsub_kernel, dim3(1), dim3(1), 0, s, "backsub_kernel", mm, ldr_, R_.get(), g_.get(), y_.get(), flag_.get());
       launch(basis_combine_kernel, dim3(blocks_for(n_, 256)), dim3(256), 0, s, "basis_combine_kernel", n_, ldv_, mm, V_.get(), y_.get(), stage);
       launch_pj();  // z = M^-1 (V y) = dx_cycle, jout = J dx_cycle
+      ++res.precond_applies;
+      pc_.inner_calls += per_apply;
       const double rr = norm_into(r_.get(), jout_.get(), nullptr, nullptr, s);
       int sing = 0;
       cuda_check(cudaMemcpy(&sing, flag_.get(), sizeof(int), cudaMemcpyDeviceToHost), "flag");
@@ -841,14 +912,12 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
       tr = rr / rnorm;
     };
     while (m < budget) {
-      launch_pj();
-      MgsArgs a{n_, ldv_, m, ldr_, V_.get(), jout_.get(), stage, partial_.get(), h_.get(), cs_.get(), sn_.get(),
-                g_.get(), R_.get(), rnorm, status_d_};
-      launch_mgs(a, s);
-      cuda_check(cudaStreamSynchronize(s), "mgs sync");
-      res.launches += 1;
-      const GmresStatus st_h = *status_h_;
+      while (enq < budget && enq <= m + 1) enqueue_step();
+      cuda_check(cudaEventSynchronize(mgs_done[m & 1]), "mgs sync");
+      const GmresStatus st_h = status_h_[m & 1];
       if (st_h.nonfinite) throw fpb::numerical_error("gmres: non-finite vector in Arnoldi process");
+      ++res.precond_applies;
+      pc_.inner_calls += per_apply;
       ++m;
       ++res.iterations;
       res.history.push_back(st_h.est * rnorm / bnorm);
@@ -873,8 +942,10 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
           break;
         }
       }
-      if (assembled_at == m && m < budget)  // keep iterating: restore the staged V_m
-        cuda_check(cudaMemcpyAsync(stage, V_.get() + size_t(m) * ldv_, vb, cudaMemcpyDeviceToDevice, s), "restage");
+      // keep iterating: the assemble overwrote the staging buffer; restore V_enq, the
+      // input of the next step to enqueue (step enq - 1 already ran before the assemble)
+      if (assembled_at == m && enq < budget)
+        cuda_check(cudaMemcpyAsync(stage, V_.get() + size_t(enq) * ldv_, vb, cudaMemcpyDeviceToDevice, s), "restage");
     }
     if (!cyc_done && assembled_at != m) assemble(m);
     (void)happy;
@@ -960,6 +1031,12 @@ ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int re
     pc.enqueue_band(pc.tp.get(), 1.0, pc.vp.get(), nullptr, nullptr, 1.0, 0, s, &lb);
     r.band_bytes = lb.bytes;
     r.band_ms = timed([&] { pc.enqueue_band(pc.tp.get(), 1.0, pc.vp.get(), nullptr, nullptr, 1.0, 0, s, nullptr); });
+  }
+  for (int l = 0; l < A.n_levels(); ++l) {
+    DeviceLevel& L = A.lv[l];
+    cudaGraphExec_t gv = graph_of([&] { A.vcycle(l, L.b.get(), L.x.get(), nullptr, nullptr, s, nullptr); });
+    r.vcycle_ms.push_back(timed([&] { cudaGraphLaunch(gv, s); }));
+    cudaGraphExecDestroy(gv);
   }
   {
     DeviceLevel& C = A.lv.back();

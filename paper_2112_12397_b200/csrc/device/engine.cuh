@@ -80,6 +80,8 @@ struct DMat {
   bool warp = false;
   int slice_rows = 32;  // rows per CTA of the slice kernel (8 for few-row operators)
   bool pipe = false;     // warp && many rows: the windowed producer/consumer pipeline
+  bool strided = false;  // row_sum = strided32 (extension): csr_warp_kernel / csr_slice_strided_kernel
+  int strided_rows = 4;  // rows per CTA of csr_slice_strided_kernel
   DSell sell;
   DCsr csr;
   DPipe pm;
@@ -89,7 +91,7 @@ struct DMat {
 };
 // few_rows_parallel: operators with under 2048 rows take the row-parallel slice kernel even
 // for short rows (a thread-per-row chain would be the whole kernel's latency)
-DMat make_mat(const fpb::Csr& A, bool few_rows_parallel = false);
+DMat make_mat(const fpb::Csr& A, bool few_rows_parallel = false, bool strided = false);
 
 class DeviceSystem {
  public:
@@ -145,9 +147,10 @@ class DeviceAmg {
   int coarse_n = 0, coarse_rank = 0;
   DevBuf<double> top_x, top_res, top_dx;
   fpb::AmgOptions opt;
+  // one V-cycle from level l (amg.cpp:151-177); public for the per-level profile
+  void vcycle(int l, const double* b, double* x, const double* sub_from, double* xhat, cudaStream_t s, Ledger* L);
 
  private:
-  void vcycle(int l, const double* b, double* x, const double* sub_from, double* xhat, cudaStream_t s, Ledger* L);
   void vcycle_chebyshev(int l, const double* b, double* x, const double* sub_from, cudaStream_t s, Ledger* L);
 };
 
@@ -178,7 +181,9 @@ class DevicePrecond {
                     cudaStream_t s, Ledger* L);
 };
 
+constexpr int kOrthMgs = 0, kOrthCgs = 1;  // FP_ORTH_*
 struct SolveOptions {
+  int orth = kOrthMgs;
   double tol = 1e-10;
   int restart = 50;
   int max_iter = 500;
@@ -199,6 +204,7 @@ struct ProfileResult {
   double fine_resid_ms = 0, fine_resid_bytes = 0, fine_post_ms = 0, fine_post_bytes = 0;
   double band_ms = 0, band_bytes = 0, coarse_ms = 0;
   int apply_launches = 0;
+  std::vector<double> vcycle_ms;  // graph of the V-cycle from level l down
 };
 ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int reps, cudaStream_t s);
 
@@ -230,7 +236,7 @@ class GmresSolver {
   int mgs_grid_ = 0, red_grid_ = 0;
   int mgs_ept_ = 0;       // > 0: mgs_fast_kernel<E> (slices in registers / shared memory)
   size_t mgs_smem_ = 0;
-  void launch_mgs(MgsArgs& a, cudaStream_t s);
+  void launch_mgs(MgsArgs& a, int orth, cudaStream_t s);
   cudaGraphExec_t pj_exec_ = nullptr, j_exec_ = nullptr;
   double graph_st_ = -1, graph_sp_ = -1;
 };

@@ -354,6 +354,226 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_fast_kernel(MgsArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) mgs_finish(a, hnext, wnorm_pre, reorth, finite, happy);
 }
 
+// Classical Gram-Schmidt Arnoldi step with the same DGKS test as the reference
+// (gmres.cpp:126-139: a second pass when ||w|| < ||w_pre|| / sqrt 2), selectable
+// instead of MGS (orthogonalization = cgs).  Every projection coefficient of a
+// pass comes from ONE grid reduction (all m + 1 dot products at once), so a step
+// costs 2 grid barriers (4 with the second pass) instead of 2 (m + 1), at the
+// price of reading the basis twice per pass.  In exact arithmetic the basis,
+// H and the iterates are the MGS ones; classical GS twice ("twice is enough",
+// Kahan-Parlett / DGKS) keeps the basis orthogonal to working precision, and
+// tests/test_gpu_parity.py holds it to the reference bars against the oracle's
+// MGS (+-2 iterations, solution 1e-8).
+// E > 0: this block's slice of w is held in registers (E values per thread,
+// k = threadIdx + j * kMgsThreads); E == 0: w lives in its final column V_{m+1}.
+// Basis columns are read in batches so ~16 loads per thread are in flight.
+constexpr int kCgsGroup = 32;     // coefficients reduced per block-level pass
+constexpr int kCgsMaxCols = 511;  // restart length limit of the classical kernel
+constexpr int kCgsBatch = 8;
+
+template <int E>
+__global__ void __launch_bounds__(kMgsThreads) cgs_kernel(MgsArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int kWarps = kMgsThreads / 32;
+  constexpr int EW = E > 0 ? E : 1;
+  constexpr int kB = E > 0 ? (16 / E > 1 ? 16 / E : 1) : kCgsBatch;  // columns per batch (<= 16 loads in flight)
+  __shared__ double red[kCgsGroup][kWarps];
+  __shared__ double hs[kCgsMaxCols + 1];  // coefficients of the current pass
+  __shared__ double sc[4];
+  const int nb = gridDim.x, m = a.m, ncol = m + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long chunk = ((a.n + nb - 1) / nb + 31) / 32 * 32;
+  const long long lo = blockIdx.x * chunk;
+  const long long len = lo < a.n ? (chunk < a.n - lo ? chunk : a.n - lo) : 0;
+  double* wg = a.V + (long long)(m + 1) * a.ldv + lo;  // final column (and w itself when E == 0)
+  const double* Vb = a.V + lo;
+  double* partA = a.partial;                                 // ncol sets: <V_i, w>
+  double* partB = a.partial + (long long)ncol * nb;          // ||w||^2 after a pass
+  double* partC = a.partial + (long long)(ncol + 1) * nb;    // ||w_pre||^2
+  double wr[EW];
+  // fixed-order totals of `cnt` partial sets: warp q sums sets q, q + 16, ... (lanes
+  // strided over blocks, then an xor tree): identical in every block and run
+  auto totals = [&](const double* part, int cnt, double* out) {
+    for (int i = warp; i < cnt; i += kWarps) {
+      double v = 0.0;
+      for (int b = lane; b < nb; b += 32) v += __ldcg(part + (long long)i * nb + b);
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) out[i] = v;
+    }
+    __syncthreads();
+  };
+  // block sum of one value per thread -> part[blockIdx.x]
+  auto block_partial = [&](double v, double* part) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) red[0][warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < kWarps; ++q) t += red[0][q];
+      part[blockIdx.x] = t;
+    }
+  };
+  // block partials of <V_i, w>, i < ncol -> partA
+  auto dots = [&] {
+    for (int i0 = 0; i0 < ncol; i0 += kB) {
+      double acc[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) acc[u] = 0.0;
+      if constexpr (E > 0) {
+        double v[kB][EW];
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+#pragma unroll
+          for (int j = 0; j < E; ++j) {
+            const int k = threadIdx.x + j * kMgsThreads;
+            v[u][j] = (i0 + u < ncol && k < len) ? __ldcg(Vb + (long long)(i0 + u) * a.ldv + k) : 0.0;
+          }
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+#pragma unroll
+          for (int j = 0; j < E; ++j) acc[u] += v[u][j] * wr[j];
+      } else {
+        for (long long k = threadIdx.x; k < len; k += kMgsThreads) {
+          const double wk = wg[k];
+#pragma unroll
+          for (int u = 0; u < kB; ++u)
+            if (i0 + u < ncol) acc[u] += __ldcg(Vb + (long long)(i0 + u) * a.ldv + k) * wk;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        double t = acc[u];
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) red[(i0 + u) % kCgsGroup][warp] = t;
+      }
+      const int done = i0 + kB;
+      if (done % kCgsGroup == 0 || done >= ncol) {  // flush this group of coefficients
+        const int g0 = (done - 1) / kCgsGroup * kCgsGroup;
+        const int cnt = (ncol < g0 + kCgsGroup ? ncol : g0 + kCgsGroup) - g0;
+        __syncthreads();
+        if (threadIdx.x < cnt) {
+          double t = 0.0;
+          for (int q = 0; q < kWarps; ++q) t += red[threadIdx.x][q];
+          partA[(long long)(g0 + threadIdx.x) * nb + blockIdx.x] = t;
+        }
+        __syncthreads();
+      }
+    }
+  };
+  // w -= sum_i c_i V_i (i ascending for every entry); returns this thread's ||w||^2 share
+  auto project = [&](const double* c) {
+    double n2 = 0.0;
+    if constexpr (E > 0) {
+      for (int i0 = 0; i0 < ncol; i0 += kB) {
+        double v[kB][EW];
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+#pragma unroll
+          for (int j = 0; j < E; ++j) {
+            const int k = threadIdx.x + j * kMgsThreads;
+            v[u][j] = (i0 + u < ncol && k < len) ? __ldcg(Vb + (long long)(i0 + u) * a.ldv + k) : 0.0;
+          }
+#pragma unroll
+        for (int u = 0; u < kB; ++u)
+          if (i0 + u < ncol) {
+            const double cu = c[i0 + u];
+#pragma unroll
+            for (int j = 0; j < E; ++j) wr[j] = wr[j] - cu * v[u][j];
+          }
+      }
+#pragma unroll
+      for (int j = 0; j < E; ++j) n2 += wr[j] * wr[j];  // out-of-range slots hold 0
+    } else {
+      for (long long k = threadIdx.x; k < len; k += kMgsThreads) {
+        double wv = wg[k];
+        for (int i0 = 0; i0 < ncol; i0 += kB) {
+          double v[kB];
+#pragma unroll
+          for (int u = 0; u < kB; ++u)
+            v[u] = i0 + u < ncol ? __ldcg(Vb + (long long)(i0 + u) * a.ldv + k) : 0.0;
+#pragma unroll
+          for (int u = 0; u < kB; ++u)
+            if (i0 + u < ncol) wv = wv - c[i0 + u] * v[u];
+        }
+        wg[k] = wv;
+        n2 += wv * wv;
+      }
+    }
+    return n2;
+  };
+  // w = J z and ||w_pre||^2
+  double n2 = 0.0;
+  if constexpr (E > 0) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int k = threadIdx.x + j * kMgsThreads;
+      wr[j] = k < len ? a.w_in[lo + k] : 0.0;
+      n2 += wr[j] * wr[j];
+    }
+  } else {
+    for (long long k = threadIdx.x; k < len; k += kMgsThreads) {
+      const double v = a.w_in[lo + k];
+      wg[k] = v;
+      n2 += v * v;
+    }
+  }
+  dots();
+  block_partial(n2, partC);
+  grid.sync();
+  totals(partA, ncol, hs);
+  totals(partC, 1, sc);
+  const double wnorm_pre = sqrt(sc[0]);
+  if (!isfinite(wnorm_pre)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.status->nonfinite = 1;
+      a.status->wnorm_pre = wnorm_pre;
+    }
+    return;  // uniform across the grid
+  }
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < ncol; i += kMgsThreads) a.h[i] = hs[i];
+  block_partial(project(hs), partB);
+  grid.sync();
+  totals(partB, 1, sc + 1);
+  double hnext = sqrt(sc[1]);
+  int reorth = 0;
+  if (hnext < 0.70710678118654752 * wnorm_pre) {  // gmres.cpp:133
+    reorth = 1;
+    dots();
+    grid.sync();
+    totals(partA, ncol, hs);
+    if (blockIdx.x == 0)
+      for (int i = threadIdx.x; i < ncol; i += kMgsThreads) a.h[i] += hs[i];
+    block_partial(project(hs), partB);
+    grid.sync();
+    totals(partB, 1, sc + 2);
+    hnext = sqrt(sc[2]);
+  }
+  const bool finite = isfinite(hnext);
+  const bool happy = hnext <= 1e-14 * fmax(1.0, wnorm_pre);
+  if constexpr (E > 0) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int k = threadIdx.x + j * kMgsThreads;
+      if (k < len) {
+        const double v = (finite && !happy) ? wr[j] / hnext : wr[j];
+        wg[k] = v;
+        if (finite && !happy) a.stage[lo + k] = v;
+      }
+    }
+  } else {
+    for (long long k = threadIdx.x; k < len; k += kMgsThreads) {
+      const double v = (finite && !happy) ? wg[k] / hnext : wg[k];
+      wg[k] = v;
+      if (finite && !happy) a.stage[lo + k] = v;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) mgs_finish(a, hnext, wnorm_pre, reorth, finite, happy);
+}
+
 // y = R(0:m,0:m)^-1 g(0:m)  (gmres.cpp:92-98), one thread; flags a zero pivot
 __global__ void backsub_kernel(int m, int ldr, const double* R, const double* g, double* y, int* singular) {
   pdl_entry();

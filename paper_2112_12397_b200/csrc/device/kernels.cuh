@@ -197,14 +197,6 @@ __global__ void __launch_bounds__(256) sell_kernel(SellView A, G g, E epi) {
 }
 
 // ------------------------------------------------------- warp-row CSR kernel
-// For operators with few, long rows (coarse AMG levels, restrictions R = P^T):
-// one warp per row.  The 32 lanes load 32 consecutive entries (coalesced) and
-// form their products in parallel; the row sum is then accumulated strictly
-// left to right by broadcasting the products lane by lane, so the result is
-// the reference's sequential CSR sum bit for bit (csr.cpp:112-117) while the
-// loads for the next chunk are already in flight.
-constexpr int kWarpRowThreads = 256;
-
 // Slice kernel for few / long rows: one CTA per 32 consecutive rows.  In each
 // window of kSliceWin entries per row, the 8 warps load their rows' entries
 // (contiguous in CSR, so coalesced) and store the products a_ik x_k to shared
@@ -264,6 +256,119 @@ __global__ void __launch_bounds__(256) csr_slice_kernel(CsrView A, G g, E epi) {
   }
   if (warp == 0 && lane < nrows) epi(row0 + lane, s, pre);
 }
+
+// ------------------------------------- strided32 row sums (AmgConfig row_sum = strided)
+// EXTENSION, the coarse operators A_l (l >= 1) and R_l = P_l^T only:
+// a row's sum is the xor tree (h = 16..1) of 32 partials, partial l accumulating the
+// row's entries l, l + 32, l + 64, ... in order from +0.0 — restated by the oracle's
+// spmv_strided32, so the result is still bitwise the oracle's in this mode.  The
+// dependent add chain of a row drops from len to len / 32 + 5.
+__device__ __forceinline__ double xor_tree32(double s) {
+#pragma unroll
+  for (int h = 16; h > 0; h >>= 1) s = s + __shfl_xor_sync(0xffffffffu, s, h);
+  return s;
+}
+
+// many rows: one warp per row, lane l owning partial l (coalesced 256-byte loads);
+// U entries per lane per batch (predicated): U = 8 for long rows (fewer dependent
+// rounds of index loads + gathers), 4 otherwise (fewer idle slots)
+template <int U, class G, class E>
+__global__ void __launch_bounds__(256) csr_warp_kernel(CsrView A, G g, E epi) {
+  pdl_entry();
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= A.n_rows) return;
+  typename E::P pre{};
+  if (lane == 0) pre = epi.load(row);
+  const long long k1 = A.rp[row + 1];
+  double s = 0.0;
+  long long k = A.rp[row] + lane;
+  for (; k + 32 * (U - 1) < k1; k += 32 * U) {
+    int c[U];
+    double v[U], x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = __ldg(A.ci + k + 32 * u), v[u] = __ldg(A.v + k + 32 * u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = g(c[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) s = s + v[u] * x[u];
+  }
+  if (k < k1) {  // tail: up to U - 1 entries, predicated in one round
+    int c[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool in = k + 32 * u < k1;
+      c[u] = in ? __ldg(A.ci + k + 32 * u) : 0;
+      v[u] = in ? __ldg(A.v + k + 32 * u) : 0.0;
+    }
+    double x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = k + 32 * u < k1 ? g(c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (k + 32 * u < k1) s = s + v[u] * x[u];
+  }
+  s = xor_tree32(s);
+  if (lane == 0) epi(row, s, pre);
+}
+
+// few long rows: R rows per CTA of 512 threads; in each window of W = 4096 / R
+// entries per row every thread loads 8 entries (one round of loads for the whole
+// window) and stores their products in shared memory; warp r then adds row r's
+// window into its 32 partials (window entry c -> lane c mod 32; W % 32 == 0
+// keeps entry k -> lane k mod 32 across windows).  R is chosen at upload from
+// the operator's average row length (most rows fit one window).
+constexpr int kStridedThreads = 512, kStridedWin = 4096;
+template <int R, class G, class E>
+__global__ void __launch_bounds__(kStridedThreads) csr_slice_strided_kernel(CsrView A, G g, E epi) {
+  pdl_entry();
+  constexpr int W = kStridedWin / R;
+  extern __shared__ double prod[];  // [R][W + 1]
+  __shared__ long long rb[R + 1];
+  const int row0 = blockIdx.x * R;
+  const int nrows = A.n_rows - row0 < R ? A.n_rows - row0 : R;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x <= nrows) rb[threadIdx.x] = A.rp[row0 + threadIdx.x];
+  __syncthreads();
+  long long maxlen = 0;
+  for (int r = 0; r < nrows; ++r) maxlen = max(maxlen, rb[r + 1] - rb[r]);
+  typename E::P pre{};
+  if (warp < nrows && lane == 0) pre = epi.load(row0 + warp);
+  double s = 0.0;
+  for (long long w0 = 0; w0 < maxlen; w0 += W) {
+    constexpr int kPer = R * W / kStridedThreads;
+    int c[kPer];
+    double v[kPer];
+    bool in[kPer];
+#pragma unroll
+    for (int h = 0; h < kPer; ++h) {
+      const int t = threadIdx.x + kStridedThreads * h, r = t / W, cc = t - r * W;
+      const long long k = r < nrows ? rb[r] + w0 + cc : 0;
+      in[h] = r < nrows && k < rb[r + 1];
+      c[h] = in[h] ? __ldg(A.ci + k) : 0;
+      v[h] = in[h] ? __ldg(A.v + k) : 0.0;
+    }
+    if (w0 > 0) __syncthreads();  // the previous window has been summed
+#pragma unroll
+    for (int h = 0; h < kPer; ++h) {
+      const int t = threadIdx.x + kStridedThreads * h, r = t / W, cc = t - r * W;
+      if (r < nrows) prod[r * (W + 1) + cc] = in[h] ? v[h] * g(c[h]) : 0.0;
+    }
+    __syncthreads();
+    if (warp < nrows) {
+      const long long len = rb[warp + 1] - rb[warp] - w0;
+      const int cnt = len < W ? int(len) : W;
+      const double* src = prod + warp * (W + 1);
+      for (int cc = lane; cc < cnt; cc += 32) s = s + src[cc];
+    }
+  }
+  if (warp < nrows) {
+    s = xor_tree32(s);
+    if (lane == 0) epi(row0 + warp, s, pre);
+  }
+}
+inline size_t strided_smem_bytes(int R) { return sizeof(double) * size_t(R) * (kStridedWin / R + 1); }
 
 // ------------------------------------------------ ordered long-row CSR pipeline
 // Rows of tens to thousands of entries (AMG levels >= 1, R = P^T) whose sums
@@ -346,34 +451,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) csr_pipe_kernel(
     for (int r = 0; r < kPipeRows; ++r) ring[q][r][lane] = v[r] * g(c[r]);
     named_arrive(1 + q, 64);
   }
-}
-
-template <class G, class E>
-__global__ void __launch_bounds__(kWarpRowThreads) csr_warp_kernel(CsrView A, G g, E epi) {
-  pdl_entry();
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (row >= A.n_rows) return;  // warp-uniform
-  const long long b = A.rp[row], e = A.rp[row + 1];
-  double s = 0.0;
-  long long k = b + lane;
-  double p = 0.0;
-  if (k < e) p = __ldg(A.v + k) * g(__ldg(A.ci + k));
-  for (long long base = b; base < e; base += 32) {
-    // prefetch the next chunk's product while this chunk is summed
-    const long long kn = k + 32;
-    double pn = 0.0;
-    if (kn < e) pn = __ldg(A.v + kn) * g(__ldg(A.ci + kn));
-    const int cnt = e - base < 32 ? int(e - base) : 32;
-#pragma unroll 8
-    for (int j = 0; j < 32; ++j) {
-      const double pj = __shfl_sync(0xffffffffu, p, j);
-      if (j < cnt) s = s + pj;
-    }
-    p = pn;
-    k = kn;
-  }
-  if (lane == 0) epi(row, s, epi.load(row));
 }
 
 // ------------------------------------------------------------- BSR3 kernel

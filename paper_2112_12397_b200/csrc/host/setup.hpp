@@ -27,6 +27,7 @@ struct AmgOptions {
   double jacobi_omega = 2.0 / 3.0;
   double stall_ratio = 0.9;
   int max_levels = 25;
+  int row_sum = 0;  // 0 ordered (reference order), 1 strided32 on A_l (l >= 1) and R_l
 };
 
 struct HostLevel {

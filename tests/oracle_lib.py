@@ -41,6 +41,7 @@ def _load():
         "or_csr_copy": (C.c_int, [P, C.POINTER(C.c_int64), IP, DP]),
         "or_precond_build": (C.c_int, [P, C.c_int, C.c_int, DP, IP, DP, C.c_int, PP]),
         "or_precond_set_factor_solve": (C.c_int, [P, C.c_int]),
+        "or_precond_set_row_sum": (C.c_int, [P, C.c_int]),
         "or_precond_destroy": (None, [P]),
         "or_precond_apply": (C.c_int, [P, DP, DP]),
         "or_precond_inner_calls": (C.c_long, [P, C.c_int]),
@@ -153,7 +154,8 @@ class OracleSystem:
 
 
 class OraclePrecond:
-    def __init__(self, sys: OracleSystem, variant="tup", inner="amg", coords=None, factor_solve="sweep", **amg):
+    def __init__(self, sys: OracleSystem, variant="tup", inner="amg", coords=None, factor_solve="sweep",
+                 row_sum="ordered", **amg):
         cfg = dict(AMG_DEFAULT, **amg)
         d = np.array([cfg["strength_threshold"], cfg["jacobi_omega"], cfg["stall_ratio"], cfg["chebyshev_ratio"]])
         i = np.array([cfg["max_coarse"], cfg["pre_sweeps"], cfg["post_sweeps"], cfg["smoother"],
@@ -168,6 +170,15 @@ class OraclePrecond:
         _check(lib.or_precond_build(sys.h, VARIANT[variant], 0 if inner == "amg" else 1, _dp(d),
                                     i.ctypes.data_as(C.POINTER(C.c_int)), cp, nn, C.byref(self.h)))
         self.set_factor_solve(factor_solve)
+        if inner == "amg":
+            self.set_row_sum(row_sum)
+
+    def set_row_sum(self, mode: str) -> None:
+        """'ordered' (the reference's spmv / spmv_transpose order) or 'strided' (extension:
+        32 lane-strided partials + xor tree on A_l, l >= 1, and on R_l = P_l^T)."""
+        assert mode in ("ordered", "strided"), mode
+        _check(lib.or_precond_set_row_sum(self.h, 1 if mode == "strided" else 0))
+        self.row_sum = mode
 
     def set_factor_solve(self, mode: str) -> None:
         """'sweep' (SparseFactor::solve) or 'inverse' (explicit block inverse, DESIGN.md §5b)."""

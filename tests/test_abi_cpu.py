@@ -157,6 +157,39 @@ def test_oracle_block_inverse_is_the_sweep_operator(variant):
     assert all(np.array_equal(opc.apply(x), r) for x, r in zip(xs, ref))
 
 
+@pytest.mark.parametrize("theta", [0.08, 0.0])
+@pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
+def test_oracle_strided_row_sums_are_the_ordered_operator(variant, theta):
+    """row_sum = strided only regroups the coarse operators' row sums:
+    the preconditioner applies the reference-order operator to within the 1e-12 bar."""
+    J = small_workload(seed=43, cells=(8, 8, 8), fracs=((0, 0.25, 0.0, 1.0, 0.0, 1.0), (0, 0.75, 0.0, 1.0, 0.5, 1.0)))
+    osys = oracle_system(J)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, strength_threshold=theta)
+    assert opc.n_levels() >= 3
+    rng = np.random.default_rng(8)
+    xs = rng.uniform(-1, 1, (3, J.total_dimension()))
+    ref = [opc.apply(x) for x in xs]
+    opc.set_row_sum("strided")
+    diff = [np.linalg.norm(opc.apply(x) - r) / np.linalg.norm(r) for x, r in zip(xs, ref)]
+    assert max(diff) <= 1e-12, diff
+    assert max(diff) > 0.0  # the order does change the rounding
+    opc.set_row_sum("ordered")
+    assert all(np.array_equal(opc.apply(x), r) for x, r in zip(xs, ref))
+
+
+def test_oracle_strided_gmres_within_reference_bars():
+    J = small_workload(seed=23, cells=(8, 8, 6))
+    osys = oracle_system(J)
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    ref = O.OraclePrecond(osys, "tup", coords=J.node_coords)
+    x_ref, st_ref = O.oracle_gmres(osys, ref, b, tol=1e-10, restart=50, max_iter=300, scaled=True)
+    strided = O.OraclePrecond(osys, "tup", coords=J.node_coords, row_sum="strided")
+    x, st = O.oracle_gmres(osys, strided, b, tol=1e-10, restart=50, max_iter=300, scaled=True)
+    assert st_ref["converged"] and st["converged"]
+    assert abs(st["iterations"] - st_ref["iterations"]) <= 2
+    assert np.linalg.norm(x - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+
+
 def test_factor_solve_is_validated():
     with pytest.raises(ValueError, match="factor_solve"):
         api.PrecondConfig(factor_solve="cholesky").native()

@@ -90,15 +90,17 @@ def test_system_apply_bitwise(case):
     assert np.array_equal(y, ref)
 
 
+@pytest.mark.parametrize("row_sum", ["ordered", "strided"])
 @pytest.mark.parametrize("factor_solve", FACTOR_SOLVES)
 @pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_precond_apply_matches_oracle(case, variant, factor_solve):
+def test_precond_apply_matches_oracle(case, variant, factor_solve, row_sum):
     osys = CASES[case]()
     J = system_from_oracle(osys)
     J.node_coords = coords_for(case)
-    amg = api.AmgConfig(max_coarse=8 if case.startswith("toy") else 100)
-    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, factor_solve=factor_solve, **amg_kw(amg))
+    amg = api.AmgConfig(max_coarse=8 if case.startswith("toy") else 100, row_sum=row_sum)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, factor_solve=factor_solve, row_sum=row_sum,
+                          **amg_kw(amg))
     op = api.BlockSystemOperator(J)
     pc = upload_oracle_precond(op, osys, opc, variant, amg)
     assert pc.factor_solve == factor_solve
@@ -171,10 +173,11 @@ def test_sgs_smoother_is_rejected_on_the_gpu():
         api.GpuPreconditioner.from_host(op, hp)
 
 
+@pytest.mark.parametrize("orth", ["mgs", "cgs"])
 @pytest.mark.parametrize("factor_solve", FACTOR_SOLVES)
 @pytest.mark.parametrize("variant", ["tpu", "tup"])
 @pytest.mark.parametrize("restart", [50, 8])
-def test_gmres_matches_oracle(variant, restart, factor_solve):
+def test_gmres_matches_oracle(variant, restart, factor_solve, orth):
     J = small_workload(seed=23, cells=(8, 8, 6))
     osys = oracle_system(J)
     opc = O.OraclePrecond(osys, variant, coords=J.node_coords, factor_solve=factor_solve)
@@ -182,13 +185,39 @@ def test_gmres_matches_oracle(variant, restart, factor_solve):
     pc = upload_oracle_precond(op, osys, opc, variant, api.AmgConfig())
     b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
     x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=restart, max_iter=500, scaled=True)
-    x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=500, restart=restart, scaled=True)
+    x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=500, restart=restart, scaled=True, orthogonalization=orth)
     assert st.converged == st_ref["converged"]
     assert abs(st.iterations - st_ref["iterations"]) <= 2, (st.iterations, st_ref["iterations"])
     if st_ref["converged"]:
         assert rel(x, x_ref) <= 1e-8, rel(x, x_ref)
     # the reported true residual of the scaled system
     assert st.relative_residuals[-1] <= 1e-10 * (1 + 1e-6) or not st.converged
+
+
+@pytest.mark.parametrize("orth", ["mgs", "cgs"])
+def test_gmres_mid_cycle_checks_with_speculative_steps(orth):
+    """A cycle longer than 50 steps runs the reference's every-50 true-residual check
+    (gmres.cpp:194-203) mid-cycle; the device enqueues the next Arnoldi step before the
+    host reads the current one's status, so this exercises the restage after an
+    assemble with a step already in flight, and the discarded step at convergence."""
+    J = small_workload(seed=23, cells=(8, 8, 6))
+    osys = oracle_system(J)
+    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, factor_solve="sweep")
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, "tup", api.AmgConfig())
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    for tol in (1e-12, 1e-13):
+        x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=tol, restart=120, max_iter=240, scaled=True)
+        x, st = api.gmres(op, pc, b, tol=tol, max_iter=240, restart=120, scaled=True, orthogonalization=orth)
+        x2, st2 = api.gmres(op, pc, b, tol=tol, max_iter=240, restart=120, scaled=True, orthogonalization=orth)
+        assert np.array_equal(x, x2) and st.iterations == st2.iterations  # deterministic
+        assert st.converged == st_ref["converged"]
+        assert abs(st.iterations - st_ref["iterations"]) <= 2, (tol, st.iterations, st_ref["iterations"])
+        if st_ref["converged"]:
+            assert rel(x, x_ref) <= 1e-8, rel(x, x_ref)
+        h, h_ref = np.asarray(st.relative_residuals), np.asarray(st_ref["history"])
+        k = min(len(h), len(h_ref), 40)
+        assert np.allclose(h[:k], h_ref[:k], rtol=1e-6, atol=0), (h[:k], h_ref[:k])
 
 
 def test_gmres_unscaled_and_zero_rhs():
@@ -262,14 +291,16 @@ def test_banded_factor_solves_match_oracle(variant, shift, factor_solve):
     assert np.array_equal(y, ref), rel(y, ref)
 
 
+@pytest.mark.parametrize("row_sum", ["ordered", "strided"])
 @pytest.mark.parametrize("factor_solve", FACTOR_SOLVES)
 @pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
-def test_theta0_hierarchy_apply_bitwise(variant, factor_solve):
+def test_theta0_hierarchy_apply_bitwise(variant, factor_solve, row_sum):
     """The bench's AMG setting (strength_threshold 0): wide coarse rows take the warp-row kernel."""
     J = small_workload(seed=31, cells=(12, 12, 10))
     osys = oracle_system(J)
-    amg = api.AmgConfig(strength_threshold=0.0)
-    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, factor_solve=factor_solve, **amg_kw(amg))
+    amg = api.AmgConfig(strength_threshold=0.0, row_sum=row_sum)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, factor_solve=factor_solve, row_sum=row_sum,
+                          **amg_kw(amg))
     op = api.BlockSystemOperator(J)
     pc = upload_oracle_precond(op, osys, opc, variant, amg)
     x = np.random.default_rng(12).uniform(-1, 1, J.total_dimension())
@@ -279,17 +310,25 @@ def test_theta0_hierarchy_apply_bitwise(variant, factor_solve):
     assert np.array_equal(pc2.apply(x), opc.apply(x))
 
 
+@pytest.mark.parametrize("fast", [False, True])
 @pytest.mark.parametrize("factor_solve", FACTOR_SOLVES)
-def test_theta0_gmres_matches_oracle_and_history(factor_solve):
+def test_theta0_gmres_matches_oracle_and_history(factor_solve, fast):
+    """fast: the bench's options (row_sum = strided, orthogonalization = cgs) on the GPU against
+    the reference-order oracle (ordered sums, MGS), held to the reference's GMRES bars."""
     J = small_workload(seed=37, cells=(12, 12, 12))
     osys = oracle_system(J)
-    amg = api.AmgConfig(strength_threshold=0.0)
+    amg = api.AmgConfig(strength_threshold=0.0, row_sum="strided" if fast else "ordered")
     opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, factor_solve=factor_solve, **amg_kw(amg))
     op = api.BlockSystemOperator(J)
-    pc = upload_oracle_precond(op, osys, opc, "tup", amg)
+    if fast:
+        pc = api.GpuPreconditioner.from_host(
+            op, api.HostPreconditioner(J, api.PrecondConfig("tup", amg=amg, factor_solve=factor_solve)))
+    else:
+        pc = upload_oracle_precond(op, osys, opc, "tup", amg)
     b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
     x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=50, max_iter=500, scaled=True)
-    x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=500, restart=50, scaled=True)
+    x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=500, restart=50, scaled=True,
+                      orthogonalization="cgs" if fast else "mgs")
     assert st.converged == st_ref["converged"]
     assert abs(st.iterations - st_ref["iterations"]) <= 2
     if st_ref["converged"]:

@@ -1,6 +1,6 @@
 """A short GMRES solve on a BASELINE config (for ncu launch lists of the whole iteration).
 
-    python tools/profile_solve.py [config] [variant] [max_iter]
+    python tools/profile_solve.py [config] [variant] [max_iter] [mgs|cgs]
 """
 import sys
 import time
@@ -14,15 +14,16 @@ from paper_2112_12397_b200 import api  # noqa: E402
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 var = sys.argv[2] if len(sys.argv) > 2 else "tup"
 its = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+orth = sys.argv[4] if len(sys.argv) > 4 else "mgs"
 J = api.Workload(cfg, 42).system()
 op = api.BlockSystemOperator(J)
 pc = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, api.PrecondConfig(
     var, amg=api.AmgConfig(strength_threshold=0.0))))
 b = torch.tensor(np.random.default_rng(42).uniform(-1, 1, J.total_dimension()), device="cuda", dtype=torch.float64)
-x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=its, restart=50, scaled=True)
+x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=its, restart=50, scaled=True, orthogonalization=orth)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
-x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=its, restart=50, scaled=True)
+x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=its, restart=50, scaled=True, orthogonalization=orth)
 torch.cuda.synchronize()
 wall = time.perf_counter() - t0
 print(f"iters {st.iterations} device {st.device_seconds * 1e3:.2f} ms wall {wall * 1e3:.2f} ms "
