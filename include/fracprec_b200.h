@@ -112,6 +112,8 @@ typedef struct fp_gmres_options {
   int32_t max_iter;
   int32_t scaled;   /* 1: solve the driver's D J D system (driver.cpp:229-255) */
   int32_t orthogonalization; /* FP_ORTH_* (0 = MGS, the reference's) */
+  int32_t probe;             /* 1: time the finest-level Jacobi sweep of every 8th Arnoldi step
+                                (CUDA events inside the graph) into fp_solve_stats.probe_* */
 } fp_gmres_options;
 
 /* SolveStats (gmres.hpp:15-22) + bookkeeping */
@@ -123,6 +125,8 @@ typedef struct fp_solve_stats {
   double* residual_history;    /* optional caller buffer */
   int32_t history_capacity;
   int32_t history_len;
+  double probe_ms;             /* with fp_gmres_options.probe: summed time of the probed launches */
+  int32_t probe_launches;
 } fp_solve_stats;
 
 typedef struct fp_system fp_system;           /* device-resident J (BlockSystem) */

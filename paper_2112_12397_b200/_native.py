@@ -52,7 +52,7 @@ class FpPrecondConfig(C.Structure):
 
 class FpGmresOptions(C.Structure):
     _fields_ = [("tol", C.c_double), ("restart", C.c_int32), ("max_iter", C.c_int32), ("scaled", C.c_int32),
-                ("orthogonalization", C.c_int32)]
+                ("orthogonalization", C.c_int32), ("probe", C.c_int32)]
 
 
 class FpSolveStats(C.Structure):
@@ -60,7 +60,8 @@ class FpSolveStats(C.Structure):
                 ("restarts", C.c_int32), ("precond_applies", C.c_int32), ("final_rel_residual", C.c_double),
                 ("device_seconds", C.c_double), ("kernel_launches", C.c_int64),
                 ("residual_history", C.POINTER(C.c_double)),
-                ("history_capacity", C.c_int32), ("history_len", C.c_int32)]
+                ("history_capacity", C.c_int32), ("history_len", C.c_int32), ("probe_ms", C.c_double),
+                ("probe_launches", C.c_int32)]
 
 
 class FpProfile(C.Structure):

@@ -170,6 +170,8 @@ class SolveStats:
     precond_applies: int = 0
     device_seconds: float = 0.0
     kernel_launches: int = 0
+    probe_ms: float = 0.0      # probe=True: summed CUDA-event time of the finest-level Jacobi sweeps
+    probe_launches: int = 0
 
 
 def _vec(x, n: int):
@@ -389,11 +391,13 @@ def build_tup(J: BlockSystem, cfg: Optional[PrecondConfig] = None, op: Optional[
 
 
 def gmres(op: BlockSystemOperator, precond: GpuPreconditioner, b, tol: float, max_iter: int = 500,
-          restart: Optional[int] = None, scaled: bool = False, x=None, orthogonalization: str = "mgs"):
+          restart: Optional[int] = None, scaled: bool = False, x=None, orthogonalization: str = "mgs",
+          probe: bool = False):
     """Right-preconditioned GMRES, x0 = 0 (gmres.hpp:29-33); ``restart`` gives GMRES(m);
     ``scaled`` solves the driver's D J D system with D^-1 M D^-1 (driver.cpp:229-255);
     ``orthogonalization`` "mgs" (the reference's loop) or "cgs" (classical, one reduction
-    per pass, same DGKS second-pass test)."""
+    per pass, same DGKS second-pass test); ``probe`` times the finest-level Jacobi sweep of
+    every Arnoldi step with CUDA events inside the graph (stats.probe_ms / probe_launches)."""
     n = op.dimension()
     x = _out_like(b, n) if x is None else x
     bp, mem, _ka = _vec(b, n)
@@ -403,13 +407,15 @@ def gmres(op: BlockSystemOperator, precond: GpuPreconditioner, b, tol: float, ma
         raise ValueError("gmres: orthogonalization must be 'mgs' or 'cgs'")
     o.tol, o.restart, o.max_iter, o.scaled = tol, restart or max_iter, max_iter, int(scaled)
     o.orthogonalization = 1 if orthogonalization == "cgs" else 0
+    o.probe = int(probe)
     hist = np.zeros(max(1, max_iter))
     st = N.FpSolveStats()
     st.residual_history = hist.ctypes.data_as(C.POINTER(C.c_double))
     st.history_capacity = hist.size
     N.check(N.lib.fp_gmres(op._h, precond._h, bp, xp, mem, C.byref(o), C.byref(st)))
     stats = SolveStats(st.iterations, list(hist[: st.history_len]), bool(st.converged), bool(st.breakdown),
-                       st.restarts, st.precond_applies, st.device_seconds, int(st.kernel_launches))
+                       st.restarts, st.precond_applies, st.device_seconds, int(st.kernel_launches), st.probe_ms,
+                       st.probe_launches)
     return x, stats
 
 

@@ -478,6 +478,7 @@ int fp_gmres(fp_system* s, fp_precond* p, const double* b, double* x, int32_t me
          "fp_gmres: orthogonalization must be FP_ORTH_MGS or FP_ORTH_CGS");
     so.tol = o->tol, so.restart = restart, so.max_iter = o->max_iter, so.scaled = o->scaled != 0;
     so.orth = o->orthogonalization == FP_ORTH_CGS ? fpd::kOrthCgs : fpd::kOrthMgs;
+    so.probe = o->probe != 0;
     const fpd::SolveResult r = p->solver->solve(bd, xd, so, st);
     if (mem == FP_MEM_HOST) fpd::cuda_check(cudaMemcpyAsync(x, xd, bytes, cudaMemcpyDeviceToHost, st), "D2H");
     fpd::cuda_check(cudaStreamSynchronize(st), "fp_gmres");
@@ -491,6 +492,8 @@ int fp_gmres(fp_system* s, fp_precond* p, const double* b, double* x, int32_t me
       stats->device_seconds = r.device_seconds;
       stats->kernel_launches = r.launches;
       stats->history_len = int32_t(r.history.size());
+      stats->probe_ms = r.probe_ms;
+      stats->probe_launches = r.probe_count;
       if (stats->residual_history)
         for (int i = 0; i < stats->history_capacity && i < int(r.history.size()); ++i)
           stats->residual_history[i] = r.history[i];

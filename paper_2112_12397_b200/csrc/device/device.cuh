@@ -58,6 +58,7 @@ struct Bsr3View {
   const int* brow_len = nullptr;
   const int* bcols = nullptr;            // one per block slot
   const double* vals = nullptr;          // 9 per block slot, [li][j][lane] inside each (slice,k) group
+  float l2_keep = 0.f;                   // > 0: fraction of lines loaded evict-last (bsr3_kernel<.., true>)
 };
 
 struct BandView {

@@ -62,7 +62,10 @@ void launch_sell(const DSell& A, const G& g, const E& e, cudaStream_t s) {
 template <class G, class E>
 void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s) {
   if (A.n_brows == 0) return;
-  launch(bsr3_kernel<G, E>, dim3(blocks_for((long long)A.n_slices * 96, kBsrThreads)), dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+  if (A.l2_keep > 0.f)
+    launch(bsr3_kernel<G, E, true>, dim3(blocks_for((long long)A.n_slices * 96, kBsrThreads)), dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+  else
+    launch(bsr3_kernel<G, E>, dim3(blocks_for((long long)A.n_slices * 96, kBsrThreads)), dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
   cuda_check(cudaGetLastError(), "bsr3_kernel launch");
 }
 
@@ -378,6 +381,17 @@ DeviceSystem::~DeviceSystem() {
 }
 
 // -------------------------------------------------------------------- AMG
+// Fraction of the finest operator's lines loaded evict-last: the part of it that fits a
+// budget of L2 (FRACPREC_B200_L2_KEEP_MB, default 48 MB; 0 disables) stays resident
+// between the four sweeps of a t-u-p apply instead of being re-streamed from HBM.
+float fine_l2_keep(const DBsr3& A) {
+  double mb = 48.0;  // measured at config 2: 0 / 32 / 48 / 64 / 96 MB -> 0.250 / 0.242 / 0.239 / 0.241 / 0.252 s
+  if (const char* e = std::getenv("FRACPREC_B200_L2_KEEP_MB")) mb = std::atof(e);
+  const double bytes = A.matrix_bytes();
+  if (mb <= 0.0 || bytes <= 0.0) return 0.f;
+  return float(std::min(1.0, mb * 1048576.0 / bytes));
+}
+
 DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
   opt = h.opt;
   if (opt.smoother != 0 && opt.smoother != 2)
@@ -395,6 +409,7 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
       if (l == 0 && fine_bsr3 && H.A.n_rows % 3 == 0) {
         D.bsr3 = true;
         D.Ab = make_bsr3(H.A);
+        D.Ab.l2_keep = fine_l2_keep(D.Ab);
       } else {
         D.Am = make_mat(H.A, false, l > 0 && opt.row_sum == 1);
       }
@@ -482,10 +497,10 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
     if (Lg) Lg->add(A_b + 32.0 * nd);  // x gathered; b, d read; x' written
     cur = nxt;
   }
-  launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s);  // r = b - A x
-  if (Lg) Lg->add(A_b + 24.0 * nd);
   DeviceLevel& C = lv[l + 1];  // holds P_{l+1} (n_l x n_{l+1}) and R_{l+1} = P^T
   const bool coarse_next = l + 1 == last;
+  launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s);  // r = b - A x
+  if (Lg) Lg->add(A_b + 24.0 * nd);
   if (coarse_next)
     launch_mat(C.R, GPlain{L.r.get()}, EStore{C.b.get()}, s);  // r_c = P^T r  (amg.cpp:166)
   else
@@ -497,10 +512,15 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   for (int it = 0; it < opt.post_sweeps; ++it) {
     const bool final_sweep = it + 1 == opt.post_sweeps;
     double* nxt = final_sweep ? x : other(cur);
-    if (final_sweep && sub_from)
+    if (final_sweep && sub_from) {
       launch_level(L, GPlain{cur}, EJacobiSubFrom{b, d, w, cur, sub_from, nxt}, s);
-    else
+    } else {
+      const bool probe = l == 0 && final_sweep && probe_ev[0];
+      // External: inside stream capture this becomes an event-record node of the graph
+      if (probe) cuda_check(cudaEventRecordWithFlags(probe_ev[0], s, cudaEventRecordExternal), "probe event");
       launch_level(L, GPlain{cur}, EJacobi{b, d, w, cur, nxt}, s);
+      if (probe) cuda_check(cudaEventRecordWithFlags(probe_ev[1], s, cudaEventRecordExternal), "probe event");
+    }
     if (Lg) Lg->add(A_b + 8.0 * (4 + (final_sweep && sub_from)) * nd);
     cur = nxt;
   }
@@ -772,30 +792,45 @@ GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart
 }
 
 GmresSolver::~GmresSolver() {
-  if (pj_exec_) cudaGraphExecDestroy(pj_exec_);
+  for (auto e : pj_exec_)
+    if (e) cudaGraphExecDestroy(e);
   if (j_exec_) cudaGraphExecDestroy(j_exec_);
+  for (auto& pr : probe_ev_)
+    for (auto e : pr)
+      if (e) cudaEventDestroy(e);
   if (status_h_) cudaFreeHost(status_h_);
   if (host_scalar_) cudaFreeHost(host_scalar_);
 }
 
-void GmresSolver::build_graphs(double st, double sp, cudaStream_t s) {
-  if (pj_exec_ && st == graph_st_ && sp == graph_sp_) return;
-  if (pj_exec_) cudaGraphExecDestroy(pj_exec_), pj_exec_ = nullptr;
+void GmresSolver::build_graphs(double st, double sp, bool probe, cudaStream_t s) {
+  if (pj_exec_[0] && st == graph_st_ && sp == graph_sp_ && probe == graph_probe_) return;
+  for (auto& e : pj_exec_)
+    if (e) cudaGraphExecDestroy(e), e = nullptr;
   if (j_exec_) cudaGraphExecDestroy(j_exec_), j_exec_ = nullptr;
   double* stage = V_.get() + size_t(ldr_) * ldv_;
   cudaGraph_t g;
-  cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture pj");
-  pc_.enqueue_apply(stage, z_.get(), 1.0 / st, 1.0 / sp, s);
-  sys_.enqueue_apply(z_.get(), jout_.get(), st, sp, s);
-  cuda_check(cudaStreamEndCapture(s, &g), "end capture pj");
-  cuda_check(cudaGraphInstantiate(&pj_exec_, g, 0), "instantiate pj");
-  cudaGraphDestroy(g);
+  // with probe, two more copies of the graph, each recording its own event pair around the
+  // roofline kernel; a probed step's pair is read once its MGS has completed
+  for (int slot = 0; slot < (probe ? 3 : 1); ++slot) {
+    if (slot > 0) {
+      for (auto& e : probe_ev_[slot - 1])
+        if (!e) cuda_check(cudaEventCreate(&e), "probe event");
+      pc_.amg->probe_ev[0] = probe_ev_[slot - 1][0], pc_.amg->probe_ev[1] = probe_ev_[slot - 1][1];
+    }
+    cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture pj");
+    pc_.enqueue_apply(stage, z_.get(), 1.0 / st, 1.0 / sp, s);
+    sys_.enqueue_apply(z_.get(), jout_.get(), st, sp, s);
+    cuda_check(cudaStreamEndCapture(s, &g), "end capture pj");
+    pc_.amg->probe_ev[0] = pc_.amg->probe_ev[1] = nullptr;
+    cuda_check(cudaGraphInstantiate(&pj_exec_[slot], g, 0), "instantiate pj");
+    cudaGraphDestroy(g);
+  }
   cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture j");
   sys_.enqueue_apply(xtot_.get(), jout_.get(), st, sp, s);
   cuda_check(cudaStreamEndCapture(s, &g), "end capture j");
   cuda_check(cudaGraphInstantiate(&j_exec_, g, 0), "instantiate j");
   cudaGraphDestroy(g);
-  graph_st_ = st, graph_sp_ = sp;
+  graph_st_ = st, graph_sp_ = sp, graph_probe_ = probe;
 }
 
 double GmresSolver::norm_into(const double* a, const double* b, double* diff_out, double* dev_out, cudaStream_t s) {
@@ -835,7 +870,7 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
   if (!(o.tol > 0.0)) throw std::invalid_argument("gmres: tol must be positive");
   SolveResult res;
   const double st = o.scaled ? sys_.st : 1.0, sp = o.scaled ? sys_.sp : 1.0;
-  build_graphs(st, sp, s);
+  build_graphs(st, sp, o.probe, s);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0), cudaEventCreate(&e1);
   cudaEventRecord(e0, s);
@@ -868,8 +903,10 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
     ~StepEvents() { cudaEventDestroy(e[0]), cudaEventDestroy(e[1]); }
   } step_events;
   cudaEvent_t* mgs_done = step_events.e;
-  auto launch_pj = [&] {
-    cuda_check(cudaGraphLaunch(pj_exec_, s), "graph launch pj");
+  auto probed = [&](int step) { return o.probe && step % kProbeEvery == 0; };
+  auto launch_pj = [&](int step) {  // step < 0: the assemble's apply
+    const int g = step >= 0 && probed(step) ? 1 + (step / kProbeEvery) % 2 : 0;
+    cuda_check(cudaGraphLaunch(pj_exec_[g], s), "graph launch pj");
     res.launches += apply_launches + japply_launches;
   };
   for (;;) {
@@ -888,7 +925,7 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
     // the host.  A step enqueued past the cycle's end is discarded: it writes only column
     // k+1 of V / R, g[k..k+1] and its own status slot, none of which an assemble(m <= k) reads.
     auto enqueue_step = [&] {
-      launch_pj();
+      launch_pj(enq);
       MgsArgs a{n_, ldv_, enq, ldr_, V_.get(), jout_.get(), stage, partial_.get(), h_.get(), cs_.get(), sn_.get(),
                 g_.get(), R_.get(), rnorm, status_d_ + (enq & 1)};
       launch_mgs(a, o.orth, s);
@@ -900,7 +937,7 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
       res.launches += 4;  // backsub, combine, 2 reductions (+ the graph, counted in launch_pj)
       launch(backsub_kernel, dim3(1), dim3(1), 0, s, "backsub_kernel", mm, ldr_, R_.get(), g_.get(), y_.get(), flag_.get());
       launch(basis_combine_kernel, dim3(blocks_for(n_, 256)), dim3(256), 0, s, "basis_combine_kernel", n_, ldv_, mm, V_.get(), y_.get(), stage);
-      launch_pj();  // z = M^-1 (V y) = dx_cycle, jout = J dx_cycle
+      launch_pj(-1);  // z = M^-1 (V y) = dx_cycle, jout = J dx_cycle
       ++res.precond_applies;
       pc_.inner_calls += per_apply;
       const double rr = norm_into(r_.get(), jout_.get(), nullptr, nullptr, s);
@@ -914,6 +951,12 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
     while (m < budget) {
       while (enq < budget && enq <= m + 1) enqueue_step();
       cuda_check(cudaEventSynchronize(mgs_done[m & 1]), "mgs sync");
+      if (probed(m)) {  // this step's roofline-kernel launch (its graph ran before its MGS)
+        float pms = 0.f;
+        const auto& pe = probe_ev_[(m / kProbeEvery) % 2];
+        cuda_check(cudaEventElapsedTime(&pms, pe[0], pe[1]), "probe time");
+        res.probe_ms += pms, ++res.probe_count;
+      }
       const GmresStatus st_h = status_h_[m & 1];
       if (st_h.nonfinite) throw fpb::numerical_error("gmres: non-finite vector in Arnoldi process");
       ++res.precond_applies;

@@ -41,7 +41,8 @@ struct DBsr3 {
   DevBuf<long long> off;
   DevBuf<int> len, bcols;
   DevBuf<double> vals;
-  Bsr3View view() const { return {n_brows, off.get(), len.get(), bcols.get(), vals.get()}; }
+  float l2_keep = 0.f;  // finest AMG operator: fraction kept L2-resident across sweeps
+  Bsr3View view() const { return {n_brows, off.get(), len.get(), bcols.get(), vals.get(), l2_keep}; }
   double matrix_bytes() const { return 76.0 * double(nblocks) + 4.0 * (n_brows + 1); }
 };
 
@@ -147,6 +148,9 @@ class DeviceAmg {
   int coarse_n = 0, coarse_rank = 0;
   DevBuf<double> top_x, top_res, top_dx;
   fpb::AmgOptions opt;
+  // when set, the finest level's Jacobi post-sweep of a V-cycle without sub_from (the bench's
+  // roofline kernel) is bracketed by these two events, recorded into the captured graph
+  cudaEvent_t probe_ev[2] = {nullptr, nullptr};
   // one V-cycle from level l (amg.cpp:151-177); public for the per-level profile
   void vcycle(int l, const double* b, double* x, const double* sub_from, double* xhat, cudaStream_t s, Ledger* L);
 
@@ -184,6 +188,7 @@ class DevicePrecond {
 constexpr int kOrthMgs = 0, kOrthCgs = 1;  // FP_ORTH_*
 struct SolveOptions {
   int orth = kOrthMgs;
+  bool probe = false;  // time the roofline kernel in every Arnoldi step (CUDA events in the graph)
   double tol = 1e-10;
   int restart = 50;
   int max_iter = 500;
@@ -197,6 +202,8 @@ struct SolveResult {
   std::vector<double> history;
   double device_seconds = 0.0;
   long long launches = 0;
+  double probe_ms = 0.0;  // summed CUDA-event time of the probed kernel
+  int probe_count = 0;
 };
 
 struct ProfileResult {
@@ -221,7 +228,7 @@ class GmresSolver {
   int apply_launches = 0, japply_launches = 0;
 
  private:
-  void build_graphs(double st, double sp, cudaStream_t s);
+  void build_graphs(double st, double sp, bool probe, cudaStream_t s);
   double norm_into(const double* a, const double* b, double* diff_out, double* dev_out, cudaStream_t s);
   const DeviceSystem& sys_;
   DevicePrecond& pc_;
@@ -237,8 +244,13 @@ class GmresSolver {
   int mgs_ept_ = 0;       // > 0: mgs_fast_kernel<E> (slices in registers / shared memory)
   size_t mgs_smem_ = 0;
   void launch_mgs(MgsArgs& a, int orth, cudaStream_t s);
-  cudaGraphExec_t pj_exec_ = nullptr, j_exec_ = nullptr;
+  // [0] the apply + J graph; with probe, [1] / [2] the same graph with a probe event pair
+  // each, used by every kProbeEvery-th Arnoldi step (alternating)
+  cudaGraphExec_t pj_exec_[3] = {nullptr, nullptr, nullptr}, j_exec_ = nullptr;
+  static constexpr int kProbeEvery = 8;
   double graph_st_ = -1, graph_sp_ = -1;
+  bool graph_probe_ = false;
+  cudaEvent_t probe_ev_[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
 };
 
 }  // namespace fpd

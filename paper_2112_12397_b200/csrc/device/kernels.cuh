@@ -467,13 +467,40 @@ constexpr int kBsrThreads = FP_BSR_THREADS;  // one 96-thread slice per CTA: fin
 #define FP_BSR_LD __ldcs
 #endif
 
-template <class G, class E>
+// kKeep: the finest AMG operator, streamed four times per t-u-p apply — a fraction
+// A.l2_keep of its lines is loaded evict-last (createpolicy.fractional), the rest
+// evict-first, so that fraction stays L2-resident from one sweep to the next.
+__device__ __forceinline__ unsigned long long l2_keep_policy(float fraction) {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(p) : "f"(fraction));
+  return p;
+}
+__device__ __forceinline__ double ld_hint(const double* a, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_hint(const int* a, unsigned long long pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
+template <class G, class E, bool kKeep = false>
 __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E epi) {
   pdl_entry();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int slice = t / 96, r = t - slice * 96, li = r >> 5, lane = r & 31;
   const int brow = slice * kSlice + lane;
   if (brow >= A.n_brows) return;
+  unsigned long long pol = 0;
+  if constexpr (kKeep) pol = l2_keep_policy(A.l2_keep);
+  auto LD = [&](auto* p) {
+    if constexpr (kKeep)
+      return ld_hint(p, pol);
+    else
+      return FP_BSR_LD(p);
+  };
   const long long base = A.slice_off[slice];
   const int len = A.brow_len[brow];
   const auto pre = epi.load(3 * brow + li);
@@ -482,10 +509,10 @@ __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E ep
   double s = 0.0;
   int k = 0;
   for (; k + 2 <= len; k += 2) {
-    const int c0 = 3 * FP_BSR_LD(C + 32 * k), c1 = 3 * FP_BSR_LD(C + 32 * (k + 1));
+    const int c0 = 3 * LD(C + 32 * k), c1 = 3 * LD(C + 32 * (k + 1));
     const double* V0 = V + 288 * k;
-    const double a00 = FP_BSR_LD(V0), a01 = FP_BSR_LD(V0 + 32), a02 = FP_BSR_LD(V0 + 64);
-    const double a10 = FP_BSR_LD(V0 + 288), a11 = FP_BSR_LD(V0 + 320), a12 = FP_BSR_LD(V0 + 352);
+    const double a00 = LD(V0), a01 = LD(V0 + 32), a02 = LD(V0 + 64);
+    const double a10 = LD(V0 + 288), a11 = LD(V0 + 320), a12 = LD(V0 + 352);
     const double x00 = g(c0), x01 = g(c0 + 1), x02 = g(c0 + 2);
     const double x10 = g(c1), x11 = g(c1 + 1), x12 = g(c1 + 2);
     s = s + a00 * x00;
@@ -496,11 +523,11 @@ __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E ep
     s = s + a12 * x12;
   }
   if (k < len) {
-    const int c0 = 3 * FP_BSR_LD(C + 32 * k);
+    const int c0 = 3 * LD(C + 32 * k);
     const double* V0 = V + 288 * k;
-    s = s + FP_BSR_LD(V0) * g(c0);
-    s = s + FP_BSR_LD(V0 + 32) * g(c0 + 1);
-    s = s + FP_BSR_LD(V0 + 64) * g(c0 + 2);
+    s = s + LD(V0) * g(c0);
+    s = s + LD(V0 + 32) * g(c0 + 1);
+    s = s + LD(V0 + 64) * g(c0 + 2);
   }
   epi(3 * brow + li, s, pre);
 }

@@ -220,6 +220,19 @@ def test_gmres_mid_cycle_checks_with_speculative_steps(orth):
         assert np.allclose(h[:k], h_ref[:k], rtol=1e-6, atol=0), (h[:k], h_ref[:k])
 
 
+def test_gmres_probe_times_every_step_without_changing_the_solve():
+    J = small_workload(seed=23, cells=(8, 8, 6))
+    op = api.BlockSystemOperator(J)
+    pc = api.build_tup(J, api.PrecondConfig(amg=api.AmgConfig(row_sum="strided")), op=op)
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    x0, st0 = api.gmres(op, pc, b, tol=1e-10, max_iter=120, restart=30, scaled=True, orthogonalization="cgs")
+    x1, st1 = api.gmres(op, pc, b, tol=1e-10, max_iter=120, restart=30, scaled=True, orthogonalization="cgs",
+                        probe=True)
+    assert np.array_equal(x0, x1) and st0.iterations == st1.iterations
+    assert st1.probe_launches >= st1.iterations // 8 and st1.probe_ms > 0.0
+    assert st0.probe_launches == 0
+
+
 def test_gmres_unscaled_and_zero_rhs():
     J = small_workload(seed=29)
     osys = oracle_system(J)

@@ -1,6 +1,6 @@
 """A short GMRES solve on a BASELINE config (for ncu launch lists of the whole iteration).
 
-    python tools/profile_solve.py [config] [variant] [max_iter] [mgs|cgs]
+    python tools/profile_solve.py [config] [variant] [max_iter] [mgs|cgs] [ordered|strided]
 """
 import sys
 import time
@@ -14,11 +14,12 @@ from paper_2112_12397_b200 import api  # noqa: E402
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 var = sys.argv[2] if len(sys.argv) > 2 else "tup"
 its = int(sys.argv[3]) if len(sys.argv) > 3 else 10
-orth = sys.argv[4] if len(sys.argv) > 4 else "mgs"
+orth = sys.argv[4] if len(sys.argv) > 4 else "cgs"
+row_sum = sys.argv[5] if len(sys.argv) > 5 else "strided"
 J = api.Workload(cfg, 42).system()
 op = api.BlockSystemOperator(J)
 pc = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, api.PrecondConfig(
-    var, amg=api.AmgConfig(strength_threshold=0.0))))
+    var, amg=api.AmgConfig(strength_threshold=0.0, row_sum=row_sum))))
 b = torch.tensor(np.random.default_rng(42).uniform(-1, 1, J.total_dimension()), device="cuda", dtype=torch.float64)
 x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=its, restart=50, scaled=True, orthogonalization=orth)
 torch.cuda.synchronize()
