@@ -31,6 +31,18 @@ struct SellView {
   const double* vals = nullptr;
 };
 
+// Node-blocked rows (the finest prolongation P_1 with a 3x3-block fine level): the three
+// scalar rows of a node share one column pattern, so a slot holds one column index and
+// three values.  SELL-32 over nodes: slot (slice s, k, lane) at q = slice_off[s] + 32 k + lane;
+// its column at cols[q], its values at vals[3 (slice_off[s] + 32 k) + 32 d + lane], d = 0..2.
+struct Bp3View {
+  int n_nodes = 0;
+  const long long* slice_off = nullptr;
+  const int* node_len = nullptr;
+  const int* cols = nullptr;
+  const double* vals = nullptr;
+};
+
 struct CsrView {  // plain CSR, 64-bit offsets (warp-per-row kernel)
   int n_rows = 0;
   const long long* rp = nullptr;

@@ -47,6 +47,19 @@ struct DBsr3 {
 };
 
 DSell make_sell(const fpb::Csr& A);
+
+struct DBp3 {  // node-blocked rows (Bp3View)
+  int n_nodes = 0;
+  int64_t nnz = 0, slots = 0;
+  DevBuf<long long> off;
+  DevBuf<int> len, cols;
+  DevBuf<double> vals;
+  Bp3View view() const { return {n_nodes, off.get(), len.get(), cols.get(), vals.get()}; }
+  // format bytes: one column index per node entry + three values
+  double matrix_bytes() const { return 28.0 * double(nnz) / 3.0 + 4.0 * (n_nodes + 1); }
+};
+// empty (n_nodes = 0) unless the three rows of every node share one column pattern
+DBp3 make_bp3(const fpb::Csr& A);
 DBsr3 make_bsr3(const fpb::Csr& A);  // A square, n % 3 == 0
 
 
@@ -82,13 +95,17 @@ struct DMat {
   int slice_rows = 32;  // rows per CTA of the slice kernel (8 for few-row operators)
   bool pipe = false;     // warp && many rows: the windowed producer/consumer pipeline
   bool strided = false;  // row_sum = strided32 (extension): csr_warp_kernel / csr_slice_strided_kernel
+  bool bp3 = false;      // node-blocked rows (finest prolongation): bp3_kernel
+  DBp3 bp;
   int strided_rows = 4;  // rows per CTA of csr_slice_strided_kernel
   DSell sell;
   DCsr csr;
   DPipe pm;
-  int n_rows() const { return pipe ? pm.n_rows : warp ? csr.n_rows : sell.n_rows; }
-  int64_t nnz() const { return pipe ? pm.nnz : warp ? csr.nnz : sell.nnz; }
-  double matrix_bytes() const { return pipe ? pm.matrix_bytes() : warp ? csr.matrix_bytes() : sell.matrix_bytes(); }
+  int n_rows() const { return bp3 ? 3 * bp.n_nodes : pipe ? pm.n_rows : warp ? csr.n_rows : sell.n_rows; }
+  int64_t nnz() const { return bp3 ? bp.nnz : pipe ? pm.nnz : warp ? csr.nnz : sell.nnz; }
+  double matrix_bytes() const {
+    return bp3 ? bp.matrix_bytes() : pipe ? pm.matrix_bytes() : warp ? csr.matrix_bytes() : sell.matrix_bytes();
+  }
 };
 // few_rows_parallel: operators with under 2048 rows take the row-parallel slice kernel even
 // for short rows (a thread-per-row chain would be the whole kernel's latency)

@@ -196,6 +196,50 @@ __global__ void __launch_bounds__(256) sell_kernel(SellView A, G g, E epi) {
   epi(row, sell_row(A, row, g), pre);
 }
 
+// Node-blocked rows (Bp3View): one thread per node, its three scalar rows summed left to
+// right in three independent chains (each exactly the CSR row sum of csr.cpp:112-117);
+// one column load and one gather serve all three rows.
+template <class G, class E, int U = 4>
+__global__ void __launch_bounds__(256) bp3_kernel(Bp3View A, G g, E epi) {
+  pdl_entry();
+  const int node = blockIdx.x * blockDim.x + threadIdx.x;
+  if (node >= A.n_nodes) return;
+  const auto p0 = epi.load(3 * node), p1 = epi.load(3 * node + 1), p2 = epi.load(3 * node + 2);
+  const long long s0 = A.slice_off[node >> 5];
+  const int lane = node & 31, len = A.node_len[node];
+  const int* __restrict__ C = A.cols + s0 + lane;
+  const double* __restrict__ V = A.vals + 3 * s0 + lane;
+  double a = 0.0, b = 0.0, c = 0.0;
+  int k = 0;
+  for (; k + U <= len; k += U) {
+    int col[U];
+    double x[U], v[U][3];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      col[u] = __ldg(C + 32 * (k + u));
+#pragma unroll
+      for (int d = 0; d < 3; ++d) v[u][d] = __ldg(V + 96 * (k + u) + 32 * d);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = g(col[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a = a + v[u][0] * x[u];
+      b = b + v[u][1] * x[u];
+      c = c + v[u][2] * x[u];
+    }
+  }
+  for (; k < len; ++k) {
+    const double x = g(__ldg(C + 32 * k));
+    a = a + __ldg(V + 96 * k) * x;
+    b = b + __ldg(V + 96 * k + 32) * x;
+    c = c + __ldg(V + 96 * k + 64) * x;
+  }
+  epi(3 * node, a, p0);
+  epi(3 * node + 1, b, p1);
+  epi(3 * node + 2, c, p2);
+}
+
 // ------------------------------------------------------- warp-row CSR kernel
 // Slice kernel for few / long rows: one CTA per 32 consecutive rows.  In each
 // window of kSliceWin entries per row, the 8 warps load their rows' entries

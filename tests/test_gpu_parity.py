@@ -323,6 +323,26 @@ def test_theta0_hierarchy_apply_bitwise(variant, factor_solve, row_sum):
     assert np.array_equal(pc2.apply(x), opc.apply(x))
 
 
+@pytest.mark.parametrize("variant", ["tup", "tup_star"])
+def test_node_blocked_prolongation_bitwise(variant, monkeypatch):
+    """The finest prolongation in node-blocked rows (bp3_kernel, one column index per node
+    entry; used above 200k nodes when the three rows of every node share a pattern, as they
+    do for S1) keeps every row's ordered sum: bitwise the oracle."""
+    monkeypatch.setenv("FRACPREC_B200_BP3_MIN_NODES", "1")
+    J = small_workload(seed=31, cells=(12, 12, 10))
+    osys = oracle_system(J)
+    amg = api.AmgConfig(strength_threshold=0.0)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, **amg_kw(amg))
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, variant, amg)
+    x = np.random.default_rng(13).uniform(-1, 1, J.total_dimension())
+    assert np.array_equal(pc.apply(x), opc.apply(x))
+    monkeypatch.delenv("FRACPREC_B200_BP3_MIN_NODES")
+    pc_sell = upload_oracle_precond(op, osys, opc, variant, amg)  # below the threshold: SELL rows
+    assert pc.traffic()["apply_bytes"] < pc_sell.traffic()["apply_bytes"]  # the node-blocked format did run
+    assert np.array_equal(pc_sell.apply(x), opc.apply(x))
+
+
 @pytest.mark.parametrize("fast", [False, True])
 @pytest.mark.parametrize("factor_solve", FACTOR_SOLVES)
 def test_theta0_gmres_matches_oracle_and_history(factor_solve, fast):
