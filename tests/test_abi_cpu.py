@@ -72,6 +72,25 @@ def test_invalid_arguments_are_reported_not_thrown():
         api.PrecondConfig("tpu", inner="direct").native()
 
 
+def test_new_options_are_validated():
+    """row_sum / orthogonalization: unknown values are rejected at the API and at the ABI."""
+    J = small_workload(seed=7)
+    with pytest.raises(ValueError, match="row_sum"):
+        api.AmgConfig(row_sum="pairwise").native()
+    c = api.AmgConfig().native()
+    c.row_sum = 7
+    cfg = N.FpPrecondConfig()
+    cfg.variant, cfg.amg, cfg.factor_solve = 1, c, 0
+    h = C.c_void_p()
+    st = N.lib.fp_host_precond_build(C.byref(J.view()), C.byref(cfg), None, 0, C.byref(h))
+    assert st == N.FP_INVALID_ARGUMENT and b"row_sum" in N.lib.fp_last_error()
+    # defaults are the reference's orders
+    d = N.FpAmgConfig()
+    N.lib.fp_amg_config_default(C.byref(d))
+    assert d.row_sum == 0 and api.AmgConfig().row_sum == "ordered"
+    assert N.FpGmresOptions().orthogonalization == 0
+
+
 def test_zero_diagonal_is_a_numerical_error():
     # amg_setup rejects a zero diagonal with numerical_error (amg.cpp:205-207)
     n_u, n_p = 6, 1
