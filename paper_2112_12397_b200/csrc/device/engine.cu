@@ -63,10 +63,20 @@ void launch_sell(const DSell& A, const G& g, const E& e, cudaStream_t s) {
 template <class G, class E>
 void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s) {
   if (A.n_brows == 0) return;
-  if (A.l2_keep > 0.f)
-    launch(bsr3_kernel<G, E, true>, dim3(blocks_for((long long)A.n_slices * 96, kBsrThreads)), dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
-  else
-    launch(bsr3_kernel<G, E>, dim3(blocks_for((long long)A.n_slices * 96, kBsrThreads)), dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+  const dim3 grid(blocks_for((long long)A.n_slices * 96, kBsrThreads));
+  // values prefetched one pair ahead when the grid spans several waves
+  const bool pv = A.n_slices >= 24 * sm_count();
+  if (A.l2_keep > 0.f) {
+    if (pv)
+      launch(bsr3_kernel<G, E, true, true>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+    else
+      launch(bsr3_kernel<G, E, true>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+  } else {
+    if (pv)
+      launch(bsr3_kernel<G, E, false, true>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+    else
+      launch(bsr3_kernel<G, E>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+  }
   cuda_check(cudaGetLastError(), "bsr3_kernel launch");
 }
 
