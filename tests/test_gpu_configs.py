@@ -1,0 +1,75 @@
+"""Parity at BASELINE.json's own sizes: configs[0] (the "PR1 oracle" case, 30,466 unknowns) and
+configs[1] (the bench's 40^3 box, 217,726 unknowns), both preconditioner variants, against the
+CPU oracle on the same seeded inputs (SURVEY §8(d) generator, b ~ U[-1, 1]).
+
+Bars (BASELINE north_star): one preconditioner application within 1e-12 (asserted bitwise), GMRES
+iteration count within +-2 and the solution within 1e-8 at rtol 1e-10; when both sides stop at
+max_iter (non-convergence), the residual histories are compared instead.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle_lib as O
+from paper_2112_12397_b200 import api
+from test_abi_cpu import oracle_system
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def setup(config, variant, row_sum):
+    J = api.Workload(config, 42).system()
+    osys = oracle_system(J)
+    amg = api.AmgConfig(strength_threshold=0.0, row_sum=row_sum)
+    op = api.BlockSystemOperator(J)
+    pc = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, api.PrecondConfig(variant, amg=amg)))
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, factor_solve=pc.factor_solve, row_sum=row_sum,
+                          strength_threshold=0.0)
+    return J, osys, op, pc, opc
+
+
+@pytest.mark.parametrize("row_sum", ["ordered", "strided"])
+@pytest.mark.parametrize("variant", ["tpu", "tup"])
+def test_config1_apply_and_gmres(variant, row_sum):
+    J, osys, op, pc, opc = setup(1, variant, row_sum)
+    x = np.random.default_rng(3).uniform(-1, 1, J.total_dimension())
+    xd = torch.tensor(x, device="cuda", dtype=torch.float64)
+    assert np.array_equal(pc.apply(xd).cpu().numpy(), opc.apply(x))
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=50, max_iter=500, scaled=True)
+    orth = "cgs" if row_sum == "strided" else "mgs"  # the bench's pairing, and the reference's
+    xs, st = api.gmres(op, pc, torch.tensor(b, device="cuda", dtype=torch.float64), tol=1e-10, max_iter=500,
+                       restart=50, scaled=True, orthogonalization=orth)
+    assert st.converged == st_ref["converged"]
+    assert abs(st.iterations - st_ref["iterations"]) <= 2, (st.iterations, st_ref["iterations"])
+    if st_ref["converged"]:
+        assert rel(xs.cpu().numpy(), x_ref) <= 1e-8
+    else:
+        k = min(len(st.relative_residuals), len(st_ref["history"])) - 1
+        h, hr = np.array(st.relative_residuals[:k]), st_ref["history"][:k]
+        assert np.all(np.abs(np.log10(h) - np.log10(hr)) < 0.5)
+
+
+@pytest.mark.parametrize("variant", ["tpu", "tup"])
+def test_config2_apply_bitwise_and_gmres_history(variant):
+    """The bench's workload at full size: applies bitwise in both row-sum orders, and 60 GMRES(50)
+    iterations of the bench's solver (strided rows, CGS) track the reference-order oracle (ordered
+    rows, MGS) step by step."""
+    J, osys, op, pc, opc = setup(2, variant, "strided")
+    x = np.random.default_rng(4).uniform(-1, 1, J.total_dimension())
+    xd = torch.tensor(x, device="cuda", dtype=torch.float64)
+    assert np.array_equal(pc.apply(xd).cpu().numpy(), opc.apply(x))
+    opc.set_row_sum("ordered")
+    ref = opc.apply(x)
+    assert rel(pc.apply(xd).cpu().numpy(), ref) <= 1e-12  # strided vs the reference order: the apply bar
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    _, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=50, max_iter=60, scaled=True)
+    _, st = api.gmres(op, pc, torch.tensor(b, device="cuda", dtype=torch.float64), tol=1e-10, max_iter=60,
+                      restart=50, scaled=True, orthogonalization="cgs")
+    assert st.iterations == st_ref["iterations"] == 60
+    h, hr = np.array(st.relative_residuals), st_ref["history"]
+    assert np.allclose(h, hr, rtol=1e-6, atol=0), np.max(np.abs(h / hr - 1))
