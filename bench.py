@@ -134,6 +134,7 @@ def other_variants(op, J, b, flush, args) -> dict:
         t = 0.0
         for _ in range(2):
             flush.zero_()
+            torch.cuda.synchronize()  # the solver's stream does not order after torch's
             _, st = solve()
             t += st.device_seconds
         out[name] = {"s_per_system": round(t / 2, 6), "iterations": st.iterations, "row_sum": row_sum,
@@ -324,6 +325,7 @@ def run_ours(args):
     ev0.record()
     for _ in range(args.steps):
         flush.zero_()
+        torch.cuda.synchronize()  # flush complete before the solve (the solver's stream is non-blocking)
         _, st = solve()
         stats.append(st)
         launches += st.kernel_launches
@@ -351,6 +353,7 @@ def run_ours(args):
     t0 = time.perf_counter()
     for _ in range(args.steps):
         flush.zero_()
+        torch.cuda.synchronize()  # flush complete before the solve (the solver's stream is non-blocking)
         solve_host()
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
