@@ -484,6 +484,7 @@ HostPrecond build_precond(const HostSystem& J, int variant, const AmgOptions& op
     M.amg = amg_setup(std::move(S), nn, opt);
   } else {
     M.amg = amg_setup(std::move(core), nn, opt);
+    plog.mark("amg setup (all levels)");
     M.S_K = fixed_stress_diag(J.Q2, M.S(), J.Q1);
     plog.mark("fixed stress");
     std::vector<Csr::Triplet> sk;
