@@ -61,27 +61,29 @@ void launch_sell(const DSell& A, const G& g, const E& e, cudaStream_t s) {
 }
 
 template <class G, class E>
-void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s) {
+void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s, const unsigned char* mask = nullptr) {
   if (A.n_brows == 0) return;
+  Bsr3View V = A.view();
+  V.mask = mask;
   const dim3 grid(blocks_for((long long)A.n_slices * 96, kBsrThreads));
   // values prefetched one pair ahead when the grid spans several waves
   const bool pv = A.n_slices >= 24 * sm_count();
   if (A.l2_keep > 0.f) {
     if (pv)
-      launch(bsr3_kernel<G, E, true, true>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+      launch(bsr3_kernel<G, E, true, true>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", V, g, e);
     else
-      launch(bsr3_kernel<G, E, true>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+      launch(bsr3_kernel<G, E, true>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", V, g, e);
   } else {
     if (pv)
-      launch(bsr3_kernel<G, E, false, true>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+      launch(bsr3_kernel<G, E, false, true>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", V, g, e);
     else
-      launch(bsr3_kernel<G, E>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", A.view(), g, e);
+      launch(bsr3_kernel<G, E>, grid, dim3(kBsrThreads), 0, s, "bsr3_kernel", V, g, e);
   }
   cuda_check(cudaGetLastError(), "bsr3_kernel launch");
 }
 
 template <class G, class E>
-void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s) {
+void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s, const unsigned char* mask = nullptr) {
   if (A.bp3) {
     launch(bp3_kernel<G, E>, dim3(blocks_for(A.bp.n_nodes, 256)), dim3(256), 0, s, "bp3_kernel", A.bp.view(), g, e);
     cuda_check(cudaGetLastError(), "bp3_kernel launch");
@@ -90,11 +92,13 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s) {
   if (A.strided) {
     if (A.csr.n_rows == 0) return;
     if (A.csr.n_rows >= 2048) {
+      CsrView V = A.csr.view();
+      V.mask = mask;  // only the warp-row kernel honours a row mask (the other kernels compute every row)
       // 8 entries per lane per round above 256 entries per row (A/B: config 3 apply 1.874 -> 1.860 ms)
       if (A.csr.nnz > 256LL * A.csr.n_rows)
-        launch(csr_warp_kernel<8, G, E>, dim3(blocks_for(A.csr.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", A.csr.view(), g, e);
+        launch(csr_warp_kernel<8, G, E>, dim3(blocks_for(A.csr.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", V, g, e);
       else
-        launch(csr_warp_kernel<4, G, E>, dim3(blocks_for(A.csr.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", A.csr.view(), g, e);
+        launch(csr_warp_kernel<4, G, E>, dim3(blocks_for(A.csr.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", V, g, e);
     } else {
       auto go = [&](auto kern, int R) {
         static bool smem_set = false;  // per instantiation
@@ -148,9 +152,9 @@ void launch_coarse(const DenseLUView& F, const double* b, double* x, cudaStream_
 }
 
 template <class G, class E>
-void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s) {
+void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s, const unsigned char* mask = nullptr) {
   if (L.bsr3)
-    launch_bsr3(L.Ab, g, e, s);
+    launch_bsr3(L.Ab, g, e, s, mask);
   else
     launch_mat(L.Am, g, e, s);
 }
@@ -516,6 +520,44 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
   if (opt.cycles_per_apply > 1) top_x.alloc(fine_n()), top_res.alloc(fine_n()), top_dx.alloc(fine_n());
 }
 
+void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows, const fpb::HostAmg& h) {
+  sp_ready = false;
+  if (lv.size() < 2 || !lv[0].bsr3 || h.levels.size() < 2) return;
+  const fpb::Csr& A = h.levels[0].A;
+  const fpb::Csr& P = h.levels[1].P;
+  const int n = A.n_rows;
+  if (int(rhs_rows.size()) != n || n % 3 != 0) return;
+  // rows whose residual b - A x^ can be nonzero: the rhs support F0 and its structural neighbours
+  std::vector<unsigned char> act(static_cast<size_t>(n), 0);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < n; ++i) {
+    bool a = rhs_rows[i] != 0;
+    for (int64_t k = A.rp[i]; k < A.rp[i + 1] && !a; ++k) a = rhs_rows[A.ci[k]] != 0;
+    act[i] = a;
+  }
+  std::vector<unsigned char> fine(static_cast<size_t>(n / 3), 0);
+  double on = 0.0;
+  for (int b = 0; b < n / 3; ++b) {
+    fine[b] = act[3 * b] | act[3 * b + 1] | act[3 * b + 2];
+    if (fine[b]) on += double(A.rp[3 * b + 3] - A.rp[3 * b]);
+  }
+  // rows of R_1 = P_1^T that gather an active fine row
+  std::vector<unsigned char> coarse(static_cast<size_t>(P.n_cols), 0);
+  for (int i = 0; i < n; ++i)
+    if (fine[i / 3])
+      for (int64_t k = P.rp[i]; k < P.rp[i + 1]; ++k) coarse[P.ci[k]] = 1;
+  double ron = 0.0;
+  std::vector<int64_t> cnt(static_cast<size_t>(P.n_cols), 0);
+  for (int64_t k = 0; k < P.nnz(); ++k) ++cnt[P.ci[k]];
+  for (int c = 0; c < P.n_cols; ++c)
+    if (coarse[c]) ron += double(cnt[c]);
+  sp_fine_mask.upload(fine);
+  sp_r1_mask.upload(coarse);
+  sp_fine_frac = A.nnz() > 0 ? on / double(A.nnz()) : 1.0;
+  sp_r1_frac = P.nnz() > 0 ? ron / double(P.nnz()) : 1.0;
+  sp_ready = true;
+}
+
 std::vector<int> DeviceAmg::level_sizes() const {
   std::vector<int> s;
   for (const auto& l : lv) s.push_back(l.n);
@@ -523,7 +565,7 @@ std::vector<int> DeviceAmg::level_sizes() const {
 }
 
 void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from, double* xhat, cudaStream_t s,
-                       Ledger* Lg) {
+                       Ledger* Lg, bool sparse_rhs) {
   DeviceLevel& L = lv[l];
   const int last = n_levels() - 1;
   const double nd = L.n;
@@ -572,13 +614,16 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   }
   DeviceLevel& C = lv[l + 1];  // holds P_{l+1} (n_l x n_{l+1}) and R_{l+1} = P^T
   const bool coarse_next = l + 1 == last;
-  launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s);  // r = b - A x
-  if (Lg) Lg->add(A_b + 24.0 * nd);
+  // sparse right-hand side (level 0, one pre-sweep from x = 0): rows off the masks are exact +0 sums
+  const bool sp = sparse_rhs && l == 0 && sp_ready && opt.pre_sweeps == 1;
+  launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s, sp ? sp_fine_mask.get() : nullptr);  // r = b - A x
+  if (Lg) Lg->add((sp ? sp_fine_frac : 1.0) * A_b + 24.0 * nd);
+  const unsigned char* rmask = sp && C.R.strided ? sp_r1_mask.get() : nullptr;
   if (coarse_next)
-    launch_mat(C.R, GPlain{L.r.get()}, EStore{C.b.get()}, s);  // r_c = P^T r  (amg.cpp:166)
+    launch_mat(C.R, GPlain{L.r.get()}, EStore{C.b.get()}, s, rmask);  // r_c = P^T r  (amg.cpp:166)
   else
-    launch_mat(C.R, GPlain{L.r.get()}, EStorePre{C.b.get(), C.d.get(), w, C.xt.get()}, s);
-  if (Lg) Lg->add(C.R.matrix_bytes() + 8.0 * nd + 8.0 * C.n * (coarse_next ? 1 : 3));
+    launch_mat(C.R, GPlain{L.r.get()}, EStorePre{C.b.get(), C.d.get(), w, C.xt.get()}, s, rmask);
+  if (Lg) Lg->add((rmask ? sp_r1_frac : 1.0) * C.R.matrix_bytes() + 8.0 * nd + 8.0 * C.n * (coarse_next ? 1 : 3));
   vcycle(l + 1, C.b.get(), C.x.get(), nullptr, coarse_next ? nullptr : C.xt.get(), s, Lg);
   launch_mat(C.P, GPlain{C.x.get()}, EAddTo{cur, cur}, s);  // x += P e_c  (amg.cpp:168-169)
   if (Lg) Lg->add(C.P.matrix_bytes() + 8.0 * C.n + 16.0 * nd);
@@ -645,10 +690,10 @@ void DeviceAmg::vcycle_chebyshev(int l, const double* b, double* x, const double
 }
 
 void DeviceAmg::enqueue_apply(const double* r, double* x, const double* sub_from, cudaStream_t s, Ledger* Lg,
-                              double* xhat) {
+                              double* xhat, bool sparse_rhs) {
   if (n_levels() == 1) xhat = nullptr;  // single level: direct coarse solve, no smoothing
   if (opt.cycles_per_apply <= 1) {
-    vcycle(0, r, x, sub_from, xhat, s, Lg);
+    vcycle(0, r, x, sub_from, xhat, s, Lg, sparse_rhs && opt.smoother == 0 && xhat != nullptr);
     return;
   }
   const int n = fine_n();
@@ -672,6 +717,15 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
   if (hp.amg.levels.empty() || hp.S().n_rows != s.n_u) throw std::invalid_argument("precond upload: inner operator size != n_u");
   if (int(hp.hblocks.size()) != 9 * s.n_p) throw std::invalid_argument("precond upload: H~ blocks size != 9 n_p");
   amg = std::make_unique<DeviceAmg>(hp.amg, true);
+  const char* sp_env = std::getenv("FRACPREC_B200_SPARSE_RHS");
+  if (hp.variant == fpb::kTup && s.Q1.n_rows == s.n_u && !(sp_env && std::atoi(sp_env) == 0)) {
+    // t_u2 = Q1 v_p is nonzero only on the rows Q1 touches (fracture-adjacent displacements)
+    std::vector<int> len(static_cast<size_t>(s.n_u));
+    cuda_check(cudaMemcpy(len.data(), s.Q1.len.get(), sizeof(int) * len.size(), cudaMemcpyDeviceToHost), "Q1 rows");
+    std::vector<unsigned char> rows(len.size());
+    for (size_t i = 0; i < len.size(); ++i) rows[i] = len[i] > 0;
+    amg->set_sparse_rhs(rows, hp.amg);
+  }
   // pre-factor the H~ blocks with the reference's lu3_factor (deterministic)
   std::vector<double> lu(hp.hblocks);
   std::vector<int> piv(static_cast<size_t>(s.n_p));
@@ -808,7 +862,7 @@ void DevicePrecond::enqueue_apply(const double* x, double* y, double at, double 
   if (variant == fpb::kTupStar) return;
   launch_sell(S.Q1, GPlain{vp.get()}, EStorePre{tu2.get(), d0, w0, xh.get()}, s);  // t_u2 = Q1 v_p
   if (L) L->add(S.Q1.matrix_bytes() + 8.0 * (np + nu));
-  amg->enqueue_apply(tu2.get(), yu, su.get(), s, L, xh.get());  // v_u = s_u - AMG(S1) t_u2
+  amg->enqueue_apply(tu2.get(), yu, su.get(), s, L, xh.get(), true);  // v_u = s_u - AMG(S1) t_u2 (t_u2 sparse)
   hout(yu);                                           // v_t = H~^-1 C2 v_u - t_t
 }
 

@@ -157,7 +157,14 @@ class DeviceAmg {
   // xhat, if given, already holds the first Jacobi sweep from zero, (omega r_i) / d_i, computed
   // by the kernel that produced r (it is used as scratch and overwritten).
   void enqueue_apply(const double* r, double* x, const double* sub_from, cudaStream_t s, Ledger* L = nullptr,
-                     double* xhat = nullptr);
+                     double* xhat = nullptr, bool sparse_rhs = false);
+  // Sparse right-hand sides (t-u-p's second V-cycle: t_u2 = Q1 v_p is +0 off the rows Q1 touches):
+  // block rows of level 0 whose residual can be nonzero, and rows of R_1 that can gather a nonzero;
+  // every other row's sum is an exact +0, so those rows skip their loads (bitwise the full sweep).
+  void set_sparse_rhs(const std::vector<unsigned char>& rhs_rows, const fpb::HostAmg& h);
+  DevBuf<unsigned char> sp_fine_mask, sp_r1_mask;
+  double sp_fine_frac = 1.0, sp_r1_frac = 1.0;  // active share of the masked operators' entries
+  bool sp_ready = false;
   std::vector<int> level_sizes() const;
   std::vector<DeviceLevel> lv;
   DevBuf<double> lu;
@@ -169,7 +176,8 @@ class DeviceAmg {
   // roofline kernel) is bracketed by these two events, recorded into the captured graph
   cudaEvent_t probe_ev[2] = {nullptr, nullptr};
   // one V-cycle from level l (amg.cpp:151-177); public for the per-level profile
-  void vcycle(int l, const double* b, double* x, const double* sub_from, double* xhat, cudaStream_t s, Ledger* L);
+  void vcycle(int l, const double* b, double* x, const double* sub_from, double* xhat, cudaStream_t s, Ledger* L,
+              bool sparse_rhs = false);
 
  private:
   void vcycle_chebyshev(int l, const double* b, double* x, const double* sub_from, cudaStream_t s, Ledger* L);

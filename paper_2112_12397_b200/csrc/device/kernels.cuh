@@ -324,6 +324,10 @@ __global__ void __launch_bounds__(256) csr_warp_kernel(CsrView A, G g, E epi) {
   if (row >= A.n_rows) return;
   typename E::P pre{};
   if (lane == 0) pre = epi.load(row);
+  if (A.mask && !A.mask[row]) {  // every gathered entry is +0: the sum is +0 (sparse right-hand side)
+    if (lane == 0) epi(row, 0.0, pre);
+    return;
+  }
   const long long k1 = A.rp[row + 1];
   double s = 0.0;
   long long k = A.rp[row] + lane;
@@ -548,6 +552,10 @@ __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E ep
   const long long base = A.slice_off[slice];
   const int len = A.brow_len[brow];
   const auto pre = epi.load(3 * brow + li);
+  if (A.mask && !A.mask[brow]) {  // every gathered entry is +0: the row sum is +0 (sparse right-hand side)
+    epi(3 * brow + li, 0.0, pre);
+    return;
+  }
   const int* __restrict__ C = A.bcols + base + lane;
   const double* __restrict__ V = A.vals + base * 9 + li * 96 + lane;
   double s = 0.0;
