@@ -48,7 +48,7 @@ struct CsrView {  // plain CSR, 64-bit offsets (warp-per-row kernel)
   const long long* rp = nullptr;
   const int* ci = nullptr;
   const double* v = nullptr;
-  const unsigned char* mask = nullptr;  // optional (csr_warp_kernel): inactive rows have an exact +0 sum
+  const int* row_map = nullptr;  // optional (csr_warp_kernel): compute only rows row_map[0 .. n_rows)
 };
 
 // Windowed slices for the ordered long-row pipeline (csr_pipe_kernel): rows
@@ -72,7 +72,7 @@ struct Bsr3View {
   const int* bcols = nullptr;            // one per block slot
   const double* vals = nullptr;          // 9 per block slot, [li][j][lane] inside each (slice,k) group
   float l2_keep = 0.f;                   // > 0: fraction of lines loaded evict-last (bsr3_kernel<.., true>)
-  const unsigned char* mask = nullptr;   // optional: rows of inactive block rows are exactly +0 sums
+  const int* brow_map = nullptr;         // optional: block row b of this (row-subset) matrix is global row brow_map[b]
 };
 
 struct BandView {

@@ -61,10 +61,9 @@ void launch_sell(const DSell& A, const G& g, const E& e, cudaStream_t s) {
 }
 
 template <class G, class E>
-void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s, const unsigned char* mask = nullptr) {
+void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s) {
   if (A.n_brows == 0) return;
-  Bsr3View V = A.view();
-  V.mask = mask;
+  const Bsr3View V = A.view();
   const dim3 grid(blocks_for((long long)A.n_slices * 96, kBsrThreads));
   // values prefetched one pair ahead when the grid spans several waves
   const bool pv = A.n_slices >= 24 * sm_count();
@@ -82,8 +81,9 @@ void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s, const u
   cuda_check(cudaGetLastError(), "bsr3_kernel launch");
 }
 
+// rows / n_sub: compute only rows rows[0 .. n_sub) (honoured by the strided warp-row kernel)
 template <class G, class E>
-void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s, const unsigned char* mask = nullptr) {
+void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s, const int* rows = nullptr, int n_sub = 0) {
   if (A.bp3) {
     launch(bp3_kernel<G, E>, dim3(blocks_for(A.bp.n_nodes, 256)), dim3(256), 0, s, "bp3_kernel", A.bp.view(), g, e);
     cuda_check(cudaGetLastError(), "bp3_kernel launch");
@@ -93,12 +93,13 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s, const uns
     if (A.csr.n_rows == 0) return;
     if (A.csr.n_rows >= 2048) {
       CsrView V = A.csr.view();
-      V.mask = mask;  // only the warp-row kernel honours a row mask (the other kernels compute every row)
+      if (rows) V.row_map = rows, V.n_rows = n_sub;  // row subset (sparse right-hand side)
+      if (V.n_rows == 0) return;
       // 8 entries per lane per round above 256 entries per row (A/B: config 3 apply 1.874 -> 1.860 ms)
       if (A.csr.nnz > 256LL * A.csr.n_rows)
-        launch(csr_warp_kernel<8, G, E>, dim3(blocks_for(A.csr.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", V, g, e);
+        launch(csr_warp_kernel<8, G, E>, dim3(blocks_for(V.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", V, g, e);
       else
-        launch(csr_warp_kernel<4, G, E>, dim3(blocks_for(A.csr.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", V, g, e);
+        launch(csr_warp_kernel<4, G, E>, dim3(blocks_for(V.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", V, g, e);
     } else {
       auto go = [&](auto kern, int R) {
         static bool smem_set = false;  // per instantiation
@@ -152,9 +153,9 @@ void launch_coarse(const DenseLUView& F, const double* b, double* x, cudaStream_
 }
 
 template <class G, class E>
-void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s, const unsigned char* mask = nullptr) {
+void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s) {
   if (L.bsr3)
-    launch_bsr3(L.Ab, g, e, s, mask);
+    launch_bsr3(L.Ab, g, e, s);
   else
     launch_mat(L.Am, g, e, s);
 }
@@ -335,10 +336,11 @@ DBp3 make_bp3(const fpb::Csr& A) {
   return D;
 }
 
-DBsr3 make_bsr3(const fpb::Csr& A) {
+DBsr3 make_bsr3(const fpb::Csr& A, const std::vector<int>* brows) {
   if (A.n_rows != A.n_cols || A.n_rows % 3 != 0) throw std::invalid_argument("make_bsr3: needs a square matrix with n % 3 == 0");
   DBsr3 D;
-  const int nb = A.n_rows / 3;
+  const int nb = brows ? int(brows->size()) : A.n_rows / 3;
+  auto src = [&](int b) { return brows ? (*brows)[b] : b; };  // global block row of block row b
   D.n_brows = nb;
   D.n_slices = (nb + kSlice - 1) / kSlice;
   // block columns of each block row: union over its three scalar rows
@@ -346,8 +348,9 @@ DBsr3 make_bsr3(const fpb::Csr& A) {
 #pragma omp parallel for schedule(dynamic, 256)
   for (int b = 0; b < nb; ++b) {
     auto& L = bc[b];
+    const int g = src(b);
     for (int li = 0; li < 3; ++li)
-      for (int64_t k = A.rp[3 * b + li]; k < A.rp[3 * b + li + 1]; ++k) L.push_back(A.ci[k] / 3);
+      for (int64_t k = A.rp[3 * g + li]; k < A.rp[3 * g + li + 1]; ++k) L.push_back(A.ci[k] / 3);
     std::sort(L.begin(), L.end());
     L.erase(std::unique(L.begin(), L.end()), L.end());
   }
@@ -367,9 +370,10 @@ DBsr3 make_bsr3(const fpb::Csr& A) {
     const int s = b / kSlice, lane = b % kSlice;
     const auto& L = bc[b];
     for (int k = 0; k < len[b]; ++k) bcols[off[s] + (long long)k * kSlice + lane] = L[k];
+    const int g = src(b);
     for (int li = 0; li < 3; ++li) {
       size_t slot = 0;
-      for (int64_t q = A.rp[3 * b + li]; q < A.rp[3 * b + li + 1]; ++q) {
+      for (int64_t q = A.rp[3 * g + li]; q < A.rp[3 * g + li + 1]; ++q) {
         const int c = A.ci[q], cb = c / 3, j = c % 3;
         while (L[slot] != cb) ++slot;
         vals[(off[s] + (long long)slot * kSlice) * 9 + (li * 3 + j) * kSlice + lane] = A.v[q];
@@ -380,6 +384,7 @@ DBsr3 make_bsr3(const fpb::Csr& A) {
   D.len.upload(len);
   D.bcols.upload(bcols);
   D.vals.upload(vals);
+  if (brows) D.brow_map.upload(*brows);
   return D;
 }
 
@@ -535,26 +540,26 @@ void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows, const
     for (int64_t k = A.rp[i]; k < A.rp[i + 1] && !a; ++k) a = rhs_rows[A.ci[k]] != 0;
     act[i] = a;
   }
+  std::vector<int> brows;
   std::vector<unsigned char> fine(static_cast<size_t>(n / 3), 0);
-  double on = 0.0;
-  for (int b = 0; b < n / 3; ++b) {
-    fine[b] = act[3 * b] | act[3 * b + 1] | act[3 * b + 2];
-    if (fine[b]) on += double(A.rp[3 * b + 3] - A.rp[3 * b]);
-  }
+  for (int b = 0; b < n / 3; ++b)
+    if ((fine[b] = act[3 * b] | act[3 * b + 1] | act[3 * b + 2])) brows.push_back(b);
   // rows of R_1 = P_1^T that gather an active fine row
   std::vector<unsigned char> coarse(static_cast<size_t>(P.n_cols), 0);
   for (int i = 0; i < n; ++i)
     if (fine[i / 3])
       for (int64_t k = P.rp[i]; k < P.rp[i + 1]; ++k) coarse[P.ci[k]] = 1;
-  double ron = 0.0;
   std::vector<int64_t> cnt(static_cast<size_t>(P.n_cols), 0);
   for (int64_t k = 0; k < P.nnz(); ++k) ++cnt[P.ci[k]];
+  std::vector<int> rrows;
+  sp_r1_bytes = 0.0;
   for (int c = 0; c < P.n_cols; ++c)
-    if (coarse[c]) ron += double(cnt[c]);
-  sp_fine_mask.upload(fine);
-  sp_r1_mask.upload(coarse);
-  sp_fine_frac = A.nnz() > 0 ? on / double(A.nnz()) : 1.0;
-  sp_r1_frac = P.nnz() > 0 ? ron / double(P.nnz()) : 1.0;
+    if (coarse[c]) rrows.push_back(c), sp_r1_bytes += 12.0 * double(cnt[c]) + 8.0;
+  sp_fine = make_bsr3(A, &brows);
+  sp_r1_rows.upload(rrows);
+  sp_r1_n = int(rrows.size());
+  sp_r.alloc(size_t(n)), sp_r.zero();
+  sp_b1.alloc(size_t(P.n_cols)), sp_b1.zero();
   sp_ready = true;
 }
 
@@ -614,17 +619,30 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   }
   DeviceLevel& C = lv[l + 1];  // holds P_{l+1} (n_l x n_{l+1}) and R_{l+1} = P^T
   const bool coarse_next = l + 1 == last;
-  // sparse right-hand side (level 0, one pre-sweep from x = 0): rows off the masks are exact +0 sums
+  // sparse right-hand side (level 0, one pre-sweep from x = 0, §10f): the residual and R_1 rows that can
+  // only sum +0 products are set to +0 and the rest computed from row-subset copies of the operators
   const bool sp = sparse_rhs && l == 0 && sp_ready && opt.pre_sweeps == 1;
-  launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s, sp ? sp_fine_mask.get() : nullptr);  // r = b - A x
-  if (Lg) Lg->add((sp ? sp_fine_frac : 1.0) * A_b + 24.0 * nd);
-  const unsigned char* rmask = sp && C.R.strided ? sp_r1_mask.get() : nullptr;
+  // the sparse pass keeps its own residual / coarse right-hand side, +0 off the active rows since setup
+  double* rr = sp ? sp_r.get() : L.r.get();
+  if (sp) {
+    launch_bsr3(sp_fine, GPlain{cur}, EResid{b, rr}, s);  // r = b - A x on the active rows
+    if (Lg) Lg->add(sp_fine.matrix_bytes() + 8.0 * nd + 24.0 * 3.0 * sp_fine.n_brows);
+  } else {
+    launch_level(L, GPlain{cur}, EResid{b, rr}, s);  // r = b - A x
+    if (Lg) Lg->add(A_b + 24.0 * nd);
+  }
+  const bool rsub = sp && C.R.strided;
+  double* bc = rsub ? sp_b1.get() : C.b.get();
+  if (rsub && !coarse_next)  // the level's scratch x^ is overwritten by the coarse correction: re-zero it
+    cuda_check(cudaMemsetAsync(C.xt.get(), 0, sizeof(double) * C.n, s), "memset xh_c");
+  const int* rrows = rsub ? sp_r1_rows.get() : nullptr;
+  const int rn = rsub ? sp_r1_n : 0;
   if (coarse_next)
-    launch_mat(C.R, GPlain{L.r.get()}, EStore{C.b.get()}, s, rmask);  // r_c = P^T r  (amg.cpp:166)
+    launch_mat(C.R, GPlain{rr}, EStore{bc}, s, rrows, rn);  // r_c = P^T r  (amg.cpp:166)
   else
-    launch_mat(C.R, GPlain{L.r.get()}, EStorePre{C.b.get(), C.d.get(), w, C.xt.get()}, s, rmask);
-  if (Lg) Lg->add((rmask ? sp_r1_frac : 1.0) * C.R.matrix_bytes() + 8.0 * nd + 8.0 * C.n * (coarse_next ? 1 : 3));
-  vcycle(l + 1, C.b.get(), C.x.get(), nullptr, coarse_next ? nullptr : C.xt.get(), s, Lg);
+    launch_mat(C.R, GPlain{rr}, EStorePre{bc, C.d.get(), w, C.xt.get()}, s, rrows, rn);
+  if (Lg) Lg->add((rsub ? sp_r1_bytes : C.R.matrix_bytes()) + 8.0 * nd + 8.0 * C.n * (coarse_next ? 1 : 3));
+  vcycle(l + 1, bc, C.x.get(), nullptr, coarse_next ? nullptr : C.xt.get(), s, Lg);
   launch_mat(C.P, GPlain{C.x.get()}, EAddTo{cur, cur}, s);  // x += P e_c  (amg.cpp:168-169)
   if (Lg) Lg->add(C.P.matrix_bytes() + 8.0 * C.n + 16.0 * nd);
   for (int it = 0; it < opt.post_sweeps; ++it) {

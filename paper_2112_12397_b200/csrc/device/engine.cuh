@@ -42,7 +42,8 @@ struct DBsr3 {
   DevBuf<int> len, bcols;
   DevBuf<double> vals;
   float l2_keep = 0.f;  // finest AMG operator: fraction kept L2-resident across sweeps
-  Bsr3View view() const { return {n_brows, off.get(), len.get(), bcols.get(), vals.get(), l2_keep}; }
+  DevBuf<int> brow_map;  // row-subset matrices: global block row of each block row
+  Bsr3View view() const { return {n_brows, off.get(), len.get(), bcols.get(), vals.get(), l2_keep, brow_map.get()}; }
   double matrix_bytes() const { return 76.0 * double(nblocks) + 4.0 * (n_brows + 1); }
 };
 
@@ -60,7 +61,8 @@ struct DBp3 {  // node-blocked rows (Bp3View)
 };
 // empty (n_nodes = 0) unless the three rows of every node share one column pattern
 DBp3 make_bp3(const fpb::Csr& A);
-DBsr3 make_bsr3(const fpb::Csr& A);  // A square, n % 3 == 0
+// A square, n % 3 == 0; brows: only these block rows (in order; their global indices go to brow_map)
+DBsr3 make_bsr3(const fpb::Csr& A, const std::vector<int>* brows = nullptr);
 
 
 // Plain CSR on the device, consumed one warp per row (csr_warp_kernel).
@@ -162,8 +164,11 @@ class DeviceAmg {
   // block rows of level 0 whose residual can be nonzero, and rows of R_1 that can gather a nonzero;
   // every other row's sum is an exact +0, so those rows skip their loads (bitwise the full sweep).
   void set_sparse_rhs(const std::vector<unsigned char>& rhs_rows, const fpb::HostAmg& h);
-  DevBuf<unsigned char> sp_fine_mask, sp_r1_mask;
-  double sp_fine_frac = 1.0, sp_r1_frac = 1.0;  // active share of the masked operators' entries
+  DBsr3 sp_fine;              // the level-0 operator restricted to the block rows whose residual can be nonzero
+  DevBuf<int> sp_r1_rows;     // rows of R_1 that can gather a nonzero
+  int sp_r1_n = 0;
+  double sp_r1_bytes = 0.0;   // their CSR bytes
+  DevBuf<double> sp_r, sp_b1; // the sparse pass's level-0 residual and level-1 rhs (+0 off the active rows)
   bool sp_ready = false;
   std::vector<int> level_sizes() const;
   std::vector<DeviceLevel> lv;

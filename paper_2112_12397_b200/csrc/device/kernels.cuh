@@ -322,15 +322,12 @@ __global__ void __launch_bounds__(256) csr_warp_kernel(CsrView A, G g, E epi) {
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= A.n_rows) return;
+  const int grow = A.row_map ? A.row_map[row] : row;  // row subset: sum global row grow
   typename E::P pre{};
-  if (lane == 0) pre = epi.load(row);
-  if (A.mask && !A.mask[row]) {  // every gathered entry is +0: the sum is +0 (sparse right-hand side)
-    if (lane == 0) epi(row, 0.0, pre);
-    return;
-  }
-  const long long k1 = A.rp[row + 1];
+  if (lane == 0) pre = epi.load(grow);
+  const long long k1 = A.rp[grow + 1];
   double s = 0.0;
-  long long k = A.rp[row] + lane;
+  long long k = A.rp[grow] + lane;
   for (; k + 32 * (U - 1) < k1; k += 32 * U) {
     int c[U];
     double v[U], x[U];
@@ -358,7 +355,7 @@ __global__ void __launch_bounds__(256) csr_warp_kernel(CsrView A, G g, E epi) {
       if (k + 32 * u < k1) s = s + v[u] * x[u];
   }
   s = xor_tree32(s);
-  if (lane == 0) epi(row, s, pre);
+  if (lane == 0) epi(grow, s, pre);
 }
 
 // few long rows: R rows per CTA of 512 threads; in each window of W = 4096 / R
@@ -551,11 +548,8 @@ __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E ep
   };
   const long long base = A.slice_off[slice];
   const int len = A.brow_len[brow];
-  const auto pre = epi.load(3 * brow + li);
-  if (A.mask && !A.mask[brow]) {  // every gathered entry is +0: the row sum is +0 (sparse right-hand side)
-    epi(3 * brow + li, 0.0, pre);
-    return;
-  }
+  const int grow = A.brow_map ? A.brow_map[brow] : brow;  // row-subset matrix: global block row
+  const auto pre = epi.load(3 * grow + li);
   const int* __restrict__ C = A.bcols + base + lane;
   const double* __restrict__ V = A.vals + base * 9 + li * 96 + lane;
   double s = 0.0;
@@ -599,7 +593,7 @@ __global__ void __launch_bounds__(kBsrThreads) bsr3_kernel(Bsr3View A, G g, E ep
     s = s + LD(V0 + 32) * g(c0 + 1);
     s = s + LD(V0 + 64) * g(c0 + 2);
   }
-  epi(3 * brow + li, s, pre);
+  epi(3 * grow + li, s, pre);
 }
 
 // ------------------------------------------------ t/p rows of the J apply
