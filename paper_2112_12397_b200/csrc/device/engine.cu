@@ -453,10 +453,12 @@ DeviceSystem::~DeviceSystem() {
 
 // -------------------------------------------------------------------- AMG
 // Fraction of the finest operator's lines loaded evict-last: the part of it that fits a
-// budget of L2 (FRACPREC_B200_L2_KEEP_MB, default 48 MB; 0 disables) stays resident
+// budget of L2 (FRACPREC_B200_L2_KEEP_MB, default 32 MB; 0 disables) stays resident
 // between the four sweeps of a t-u-p apply instead of being re-streamed from HBM.
 float fine_l2_keep(const DBsr3& A) {
-  double mb = 48.0;  // measured at config 2: 0 / 32 / 48 / 64 / 96 MB -> 0.250 / 0.242 / 0.239 / 0.241 / 0.252 s
+  // bench A/B at config 2, same session (s / system): 0 / 32 / 48 / 64 MB -> 0.2268 / 0.2264 / 0.2275 / 0.2281;
+  // the sweep itself 36.5 -> 32.8 us with 32 MB
+  double mb = 32.0;
   if (const char* e = std::getenv("FRACPREC_B200_L2_KEEP_MB")) mb = std::atof(e);
   const double bytes = A.matrix_bytes();
   if (mb <= 0.0 || bytes <= 0.0) return 0.f;
