@@ -904,11 +904,14 @@ GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart
   red_grid_ = sm_count() * 2;
   {  // register/shared-memory MGS when a block's slice fits E <= 24 values per thread
     const long long chunk = ((n_ + mgs_grid_ - 1) / mgs_grid_ + 31) / 32 * 32;
-    for (int e : {2, 4, 8, 16, 24})
-      if (chunk <= (long long)e * kMgsThreads) {
-        mgs_ept_ = e;
-        break;
-      }
+    // FRACPREC_B200_WIDE_ORTH=1 forces the large-n paths (tests exercise them on small systems)
+    const char* wide = std::getenv("FRACPREC_B200_WIDE_ORTH");
+    if (!(wide && std::atoi(wide) != 0))
+      for (int e : {2, 4, 8, 16, 24})
+        if (chunk <= (long long)e * kMgsThreads) {
+          mgs_ept_ = e;
+          break;
+        }
     mgs_smem_ = size_t(chunk) * sizeof(double);
     if (mgs_ept_ > 0 && mgs_smem_ > 48 * 1024) {
       auto set = [&](const void* f) {
@@ -919,7 +922,11 @@ GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart
       set((const void*)mgs_fast_kernel<16>), set((const void*)mgs_fast_kernel<24>);
     }
   }
-  partial_.alloc(size_t(std::max((ldr_ + 3) * mgs_grid_, red_grid_)));
+  big_nblk_ = int((n_ + kBigTile - 1) / kBigTile);
+  partial_.alloc(size_t(std::max({(ldr_ + 3) * (long long)mgs_grid_, (long long)red_grid_,
+                                  (ldr_ + 2) * (long long)big_nblk_})));
+  big_coef_.alloc(size_t(ldr_ + 2));
+  big_state_.alloc(1);
   cuda_check(cudaHostAlloc(&status_h_, 2 * sizeof(GmresStatus), cudaHostAllocMapped), "cudaHostAlloc");
   cuda_check(cudaHostGetDevicePointer(&status_d_, status_h_, 0), "cudaHostGetDevicePointer");
   cuda_check(cudaHostAlloc(&host_scalar_, sizeof(double), cudaHostAllocMapped), "cudaHostAlloc");
@@ -991,14 +998,28 @@ void GmresSolver::launch_mgs(MgsArgs& a, int orth, cudaStream_t s) {
   void* args[] = {&a};
   const void* f = (const void*)mgs_kernel;
   size_t smem = 0;
+  if (orth == kOrthCgs && restart_ <= kCgsMaxCols && mgs_ept_ == 0) {
+    // large n: the classical passes as a chain of wide kernels (no basis slice fits a block's registers)
+    CgsBigArgs b{a, big_nblk_, partial_.get(), big_coef_.get(), big_state_.get(), 0};
+    cuda_check(cudaMemsetAsync(big_state_.get(), 0, sizeof(CgsState), s), "cgs state");
+    const dim3 tiles(big_nblk_), one(1), T(kBigT);
+    for (int pass = 0; pass < 2; ++pass) {
+      b.pass = pass;
+      launch(cgs_big_dots, tiles, T, 0, s, "cgs_big_dots", b);
+      launch(cgs_big_reduce, one, T, 0, s, "cgs_big_reduce", b);
+      launch(cgs_big_project, tiles, T, 0, s, "cgs_big_project", b);
+      launch(cgs_big_norm, one, T, 0, s, "cgs_big_norm", b, pass);
+    }
+    launch(cgs_big_normalize, tiles, T, 0, s, "cgs_big_normalize", b);
+    return;
+  }
   if (orth == kOrthCgs && restart_ <= kCgsMaxCols) {
     switch (mgs_ept_) {
       case 2: f = (const void*)cgs_kernel<2>; break;
       case 4: f = (const void*)cgs_kernel<4>; break;
       case 8: f = (const void*)cgs_kernel<8>; break;
       case 16: f = (const void*)cgs_kernel<16>; break;
-      case 24: f = (const void*)cgs_kernel<24>; break;
-      default: f = (const void*)cgs_kernel<0>; break;
+      default: f = (const void*)cgs_kernel<24>; break;
     }
   } else if (mgs_ept_ > 0) {
     smem = mgs_smem_;

@@ -245,7 +245,8 @@ struct ProfileResult {
 };
 ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int reps, cudaStream_t s);
 
-struct MgsArgs;  // gmres_kernels.cuh
+struct MgsArgs;   // gmres_kernels.cuh
+struct CgsState;
 
 // Restarted right-preconditioned GMRES on the device (gmres.cpp semantics per
 // cycle + the GMRES(m) wrapper of SURVEY §8(a) G1).
@@ -272,6 +273,9 @@ class GmresSolver {
   double* host_scalar_d_ = nullptr;
   int mgs_grid_ = 0, red_grid_ = 0;
   int mgs_ept_ = 0;       // > 0: mgs_fast_kernel<E> (slices in registers / shared memory)
+  int big_nblk_ = 0;      // classical GS for large n: tiles of the wide-kernel chain
+  DevBuf<double> big_coef_;
+  DevBuf<CgsState> big_state_;
   size_t mgs_smem_ = 0;
   void launch_mgs(MgsArgs& a, int orth, cudaStream_t s);
   // [0] the apply + J graph; with probe, [1] / [2] the same graph with a probe event pair

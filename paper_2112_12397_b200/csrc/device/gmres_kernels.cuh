@@ -574,6 +574,193 @@ __global__ void __launch_bounds__(kMgsThreads) cgs_kernel(MgsArgs a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) mgs_finish(a, hnext, wnorm_pre, reorth, finite, happy);
 }
 
+// ---- classical Gram-Schmidt for large n (the basis slice of a block no longer fits
+// registers): the same pass structure as cgs_kernel as a chain of ordinary kernels over
+// a wide grid (tiles of kBigTile entries, 8 per thread in registers), partial sums per
+// tile reduced in a fixed order by one warp per coefficient.  The DGKS decision and the
+// non-finite checks live in a device-side state, so the chain runs without the host.
+constexpr int kBigT = 512, kBigE = 8, kBigTile = kBigT * kBigE, kBigB = 2;  // kBigB columns per load round
+struct CgsState {
+  double wnorm_pre, hnext;
+  int reorth, abort;
+};
+struct CgsBigArgs {
+  MgsArgs a;
+  int nblk;            // tiles
+  double* part;        // (ncol + 1) * nblk tile partials
+  double* coef;        // ncol + 1: this pass's coefficients (+ ||w||^2)
+  CgsState* st;
+  int pass;            // 0: first pass, 1: the DGKS second pass
+};
+
+__device__ __forceinline__ double big_block_sum(double v, double* red) {  // valid in thread 0
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kBigT / 32; ++q) t += red[q];
+  __syncthreads();
+  return t;
+}
+
+// tile partials of <V_i, w> (i <= m) and, in the first pass, ||w||^2 (w = J z is copied to V_{m+1})
+__global__ void __launch_bounds__(kBigT) cgs_big_dots(CgsBigArgs b) {
+  if (b.st->abort || (b.pass == 1 && !b.st->reorth)) return;
+  __shared__ double red[kBigT / 32];
+  const MgsArgs& a = b.a;
+  const int ncol = a.m + 1;
+  const long long lo = (long long)blockIdx.x * kBigTile;
+  double* wg = a.V + (long long)(a.m + 1) * a.ldv;
+  double wr[kBigE];
+  double n2 = 0.0;
+#pragma unroll
+  for (int j = 0; j < kBigE; ++j) {
+    const long long k = lo + threadIdx.x + (long long)j * kBigT;
+    wr[j] = k < a.n ? (b.pass == 0 ? a.w_in[k] : wg[k]) : 0.0;
+    if (b.pass == 0 && k < a.n) wg[k] = wr[j];
+    n2 += wr[j] * wr[j];
+  }
+  for (int i0 = 0; i0 < ncol; i0 += kBigB) {
+    double acc[kBigB] = {};
+    double v[kBigB][kBigE];
+#pragma unroll
+    for (int u = 0; u < kBigB; ++u)
+#pragma unroll
+      for (int j = 0; j < kBigE; ++j) {
+        const long long k = lo + threadIdx.x + (long long)j * kBigT;
+        v[u][j] = (i0 + u < ncol && k < a.n) ? __ldcs(a.V + (long long)(i0 + u) * a.ldv + k) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < kBigB; ++u)
+#pragma unroll
+      for (int j = 0; j < kBigE; ++j) acc[u] += v[u][j] * wr[j];
+#pragma unroll
+    for (int u = 0; u < kBigB; ++u) {
+      const double t = big_block_sum(acc[u], red);
+      if (threadIdx.x == 0 && i0 + u < ncol) b.part[(long long)(i0 + u) * b.nblk + blockIdx.x] = t;
+    }
+  }
+  if (b.pass == 0) {
+    const double t = big_block_sum(n2, red);
+    if (threadIdx.x == 0) b.part[(long long)ncol * b.nblk + blockIdx.x] = t;
+  }
+}
+
+// coefficients: warp q sums the tile partials of sets q, q + 16, ... (lane-strided, then an
+// xor tree); the first pass also sets h and ||w_pre||, the second adds to h (gmres.cpp:126-139)
+__global__ void __launch_bounds__(kBigT) cgs_big_reduce(CgsBigArgs b) {
+  if (b.st->abort || (b.pass == 1 && !b.st->reorth)) return;
+  const MgsArgs& a = b.a;
+  const int ncol = a.m + 1, nsets = ncol + (b.pass == 0 ? 1 : 0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = warp; i < nsets; i += kBigT / 32) {
+    double v = 0.0;
+    for (int t = lane; t < b.nblk; t += 32) v += b.part[(long long)i * b.nblk + t];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+      if (i < ncol) {
+        b.coef[i] = v;
+        a.h[i] = b.pass == 0 ? v : a.h[i] + v;
+      } else {
+        b.st->wnorm_pre = sqrt(v);
+      }
+    }
+  }
+  __syncthreads();
+  if (b.pass == 0 && threadIdx.x == 0 && !isfinite(b.st->wnorm_pre)) {
+    b.st->abort = 1;
+    a.status->nonfinite = 1;
+    a.status->wnorm_pre = b.st->wnorm_pre;
+  }
+}
+
+// w -= sum_i coef_i V_i (i ascending per entry); tile partials of ||w||^2 into set 0
+__global__ void __launch_bounds__(kBigT) cgs_big_project(CgsBigArgs b) {
+  if (b.st->abort || (b.pass == 1 && !b.st->reorth)) return;
+  __shared__ double red[kBigT / 32];
+  __shared__ double c[kCgsMaxCols + 1];
+  const MgsArgs& a = b.a;
+  const int ncol = a.m + 1;
+  for (int i = threadIdx.x; i < ncol; i += kBigT) c[i] = b.coef[i];
+  __syncthreads();
+  const long long lo = (long long)blockIdx.x * kBigTile;
+  double* wg = a.V + (long long)(a.m + 1) * a.ldv;
+  double wr[kBigE];
+#pragma unroll
+  for (int j = 0; j < kBigE; ++j) {
+    const long long k = lo + threadIdx.x + (long long)j * kBigT;
+    wr[j] = k < a.n ? wg[k] : 0.0;
+  }
+  for (int i0 = 0; i0 < ncol; i0 += kBigB) {
+    double v[kBigB][kBigE];
+#pragma unroll
+    for (int u = 0; u < kBigB; ++u)
+#pragma unroll
+      for (int j = 0; j < kBigE; ++j) {
+        const long long k = lo + threadIdx.x + (long long)j * kBigT;
+        v[u][j] = (i0 + u < ncol && k < a.n) ? __ldcs(a.V + (long long)(i0 + u) * a.ldv + k) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < kBigB; ++u)
+      if (i0 + u < ncol)
+#pragma unroll
+        for (int j = 0; j < kBigE; ++j) wr[j] = wr[j] - c[i0 + u] * v[u][j];
+  }
+  double n2 = 0.0;
+#pragma unroll
+  for (int j = 0; j < kBigE; ++j) {
+    const long long k = lo + threadIdx.x + (long long)j * kBigT;
+    if (k < a.n) wg[k] = wr[j];
+    n2 += wr[j] * wr[j];
+  }
+  const double t = big_block_sum(n2, red);
+  if (threadIdx.x == 0) b.part[blockIdx.x] = t;
+}
+
+// ||w|| after a pass (fixed order), the DGKS test after the first, and after the last
+// pass the status, h[m+1] and the Givens update (mgs_finish); one block
+__global__ void __launch_bounds__(kBigT) cgs_big_norm(CgsBigArgs b, int last) {
+  if (b.st->abort || (b.pass == 1 && !b.st->reorth && !last)) return;
+  const MgsArgs& a = b.a;
+  __shared__ double sm[40];
+  if (!(b.pass == 1 && !b.st->reorth)) {  // the pass ran: its norm
+    double v = 0.0;
+    for (int t = threadIdx.x; t < b.nblk; t += kBigT) v += b.part[t];
+    const double tot = big_block_sum(v, sm);
+    if (threadIdx.x == 0) b.st->hnext = sqrt(tot);
+  }
+  if (threadIdx.x != 0) return;
+  if (b.pass == 0 && !last) {
+    b.st->reorth = b.st->hnext < 0.70710678118654752 * b.st->wnorm_pre;  // gmres.cpp:133
+    return;
+  }
+  const double hnext = b.st->hnext, wnorm_pre = b.st->wnorm_pre;
+  const bool finite = isfinite(hnext);
+  const bool happy = hnext <= 1e-14 * fmax(1.0, wnorm_pre);
+  mgs_finish(a, hnext, wnorm_pre, b.st->reorth, finite, happy);
+}
+
+// V_{m+1} = w / ||w|| (and the preconditioner's staging copy) unless happy / non-finite
+__global__ void __launch_bounds__(kBigT) cgs_big_normalize(CgsBigArgs b) {
+  if (b.st->abort) return;
+  const MgsArgs& a = b.a;
+  const double hnext = b.st->hnext;
+  if (!isfinite(hnext) || hnext <= 1e-14 * fmax(1.0, b.st->wnorm_pre)) return;
+  double* wg = a.V + (long long)(a.m + 1) * a.ldv;
+  const long long lo = (long long)blockIdx.x * kBigTile;
+#pragma unroll
+  for (int j = 0; j < kBigE; ++j) {
+    const long long k = lo + threadIdx.x + (long long)j * kBigT;
+    if (k < a.n) {
+      const double v = wg[k] / hnext;
+      wg[k] = v;
+      a.stage[k] = v;
+    }
+  }
+}
+
 // y = R(0:m,0:m)^-1 g(0:m)  (gmres.cpp:92-98), one thread; flags a zero pivot
 __global__ void backsub_kernel(int m, int ldr, const double* R, const double* g, double* y, int* singular) {
   pdl_entry();

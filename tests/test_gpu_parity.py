@@ -220,6 +220,29 @@ def test_gmres_mid_cycle_checks_with_speculative_steps(orth):
         assert np.allclose(h[:k], h_ref[:k], rtol=1e-6, atol=0), (h[:k], h_ref[:k])
 
 
+@pytest.mark.parametrize("orth", ["mgs", "cgs"])
+def test_gmres_large_n_orthogonalization_paths(orth, monkeypatch):
+    """The Arnoldi paths for systems whose per-block basis slice no longer fits registers
+    (configs 4-5: mgs_kernel, and the classical passes as a chain of wide kernels), forced on a
+    small system: held to the reference's GMRES bars against the oracle's MGS, and deterministic."""
+    monkeypatch.setenv("FRACPREC_B200_WIDE_ORTH", "1")
+    J = small_workload(seed=23, cells=(8, 8, 6))
+    osys = oracle_system(J)
+    opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, factor_solve="sweep")
+    op = api.BlockSystemOperator(J)
+    pc = upload_oracle_precond(op, osys, opc, "tup", api.AmgConfig())
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    for restart in (50, 8):
+        x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=restart, max_iter=500, scaled=True)
+        x, st = api.gmres(op, pc, b, tol=1e-10, max_iter=500, restart=restart, scaled=True, orthogonalization=orth)
+        x2, st2 = api.gmres(op, pc, b, tol=1e-10, max_iter=500, restart=restart, scaled=True, orthogonalization=orth)
+        assert np.array_equal(x, x2)
+        assert st.converged == st_ref["converged"]
+        assert abs(st.iterations - st_ref["iterations"]) <= 2, (restart, st.iterations, st_ref["iterations"])
+        if st_ref["converged"]:
+            assert rel(x, x_ref) <= 1e-8
+
+
 def test_gmres_probe_times_every_step_without_changing_the_solve():
     J = small_workload(seed=23, cells=(8, 8, 6))
     op = api.BlockSystemOperator(J)
