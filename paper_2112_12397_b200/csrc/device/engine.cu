@@ -529,40 +529,69 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
 
 void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows, const fpb::HostAmg& h) {
   sp_ready = false;
-  if (lv.size() < 2 || !lv[0].bsr3 || h.levels.size() < 2) return;
-  const fpb::Csr& A = h.levels[0].A;
-  const fpb::Csr& P = h.levels[1].P;
-  const int n = A.n_rows;
-  if (int(rhs_rows.size()) != n || n % 3 != 0) return;
-  // rows whose residual b - A x^ can be nonzero: the rhs support F0 and its structural neighbours
-  std::vector<unsigned char> act(static_cast<size_t>(n), 0);
+  sp_lv.clear();
+  const int L = int(h.levels.size());
+  if (L < 2 || lv.size() != size_t(L) || !lv[0].bsr3) return;
+  std::vector<unsigned char> f0 = rhs_rows;  // rows where this level's rhs can be nonzero
+  for (int l = 0; l + 1 < L; ++l) {
+    const fpb::Csr& A = h.levels[l].A;
+    const fpb::Csr& P = h.levels[l + 1].P;
+    const int n = A.n_rows;
+    if (int(f0.size()) != n) break;
+    // rows whose residual b - A x^ can be nonzero: the rhs support and its structural neighbours
+    std::vector<unsigned char> act(static_cast<size_t>(n), 0);
 #pragma omp parallel for schedule(static)
-  for (int i = 0; i < n; ++i) {
-    bool a = rhs_rows[i] != 0;
-    for (int64_t k = A.rp[i]; k < A.rp[i + 1] && !a; ++k) a = rhs_rows[A.ci[k]] != 0;
-    act[i] = a;
+    for (int i = 0; i < n; ++i) {
+      bool a = f0[i] != 0;
+      for (int64_t k = A.rp[i]; k < A.rp[i + 1] && !a; ++k) a = f0[A.ci[k]] != 0;
+      act[i] = a;
+    }
+    SpLevel S;
+    double res_nnz = 0.0;
+    if (l == 0) {  // whole 3x3 block rows (a superset)
+      if (n % 3 != 0) break;
+      std::vector<int> brows;
+      for (int bq = 0; bq < n / 3; ++bq) {
+        const unsigned char on = act[3 * bq] | act[3 * bq + 1] | act[3 * bq + 2];
+        act[3 * bq] = act[3 * bq + 1] = act[3 * bq + 2] = on;
+        if (on) brows.push_back(bq);
+      }
+      S.fine = make_bsr3(A, &brows);
+    } else if (lv[l].Am.strided && lv[l].Am.csr.n_rows >= 2048) {  // the warp-row kernel takes a row list
+      std::vector<int> rows;
+      for (int i = 0; i < n; ++i)
+        if (act[i]) rows.push_back(i), res_nnz += double(A.rp[i + 1] - A.rp[i]);
+      if (rows.size() < size_t(n)) {
+        S.res_rows.upload(rows);
+        S.res_n = int(rows.size());
+        S.res_bytes = 12.0 * res_nnz + 8.0 * S.res_n;
+      }
+    }
+    // rows of R_{l+1} = P_{l+1}^T that gather an active row
+    std::vector<unsigned char> coarse(static_cast<size_t>(P.n_cols), 0);
+    for (int i = 0; i < n; ++i)
+      if (act[i])
+        for (int64_t k = P.rp[i]; k < P.rp[i + 1]; ++k) coarse[P.ci[k]] = 1;
+    const DMat& R = lv[l + 1].R;
+    if (R.strided && R.csr.n_rows >= 2048) {
+      std::vector<int64_t> cnt(static_cast<size_t>(P.n_cols), 0);
+      for (int64_t k = 0; k < P.nnz(); ++k) ++cnt[P.ci[k]];
+      std::vector<int> rrows;
+      for (int c = 0; c < P.n_cols; ++c)
+        if (coarse[c]) rrows.push_back(c), S.r_bytes += 12.0 * double(cnt[c]) + 8.0;
+      S.r_rows.upload(rrows);
+      S.r_n = int(rrows.size());
+    }
+    S.r.alloc(size_t(n)), S.r.zero();
+    S.bnext.alloc(size_t(P.n_cols)), S.bnext.zero();
+    sp_lv.push_back(std::move(S));
+    // the next level runs the sparse pass while its rhs stays mostly zero
+    long long on = 0;
+    for (unsigned char c : coarse) on += c;
+    if (l + 2 >= L || 2 * on > P.n_cols) break;
+    f0 = std::move(coarse);
   }
-  std::vector<int> brows;
-  std::vector<unsigned char> fine(static_cast<size_t>(n / 3), 0);
-  for (int b = 0; b < n / 3; ++b)
-    if ((fine[b] = act[3 * b] | act[3 * b + 1] | act[3 * b + 2])) brows.push_back(b);
-  // rows of R_1 = P_1^T that gather an active fine row
-  std::vector<unsigned char> coarse(static_cast<size_t>(P.n_cols), 0);
-  for (int i = 0; i < n; ++i)
-    if (fine[i / 3])
-      for (int64_t k = P.rp[i]; k < P.rp[i + 1]; ++k) coarse[P.ci[k]] = 1;
-  std::vector<int64_t> cnt(static_cast<size_t>(P.n_cols), 0);
-  for (int64_t k = 0; k < P.nnz(); ++k) ++cnt[P.ci[k]];
-  std::vector<int> rrows;
-  sp_r1_bytes = 0.0;
-  for (int c = 0; c < P.n_cols; ++c)
-    if (coarse[c]) rrows.push_back(c), sp_r1_bytes += 12.0 * double(cnt[c]) + 8.0;
-  sp_fine = make_bsr3(A, &brows);
-  sp_r1_rows.upload(rrows);
-  sp_r1_n = int(rrows.size());
-  sp_r.alloc(size_t(n)), sp_r.zero();
-  sp_b1.alloc(size_t(P.n_cols)), sp_b1.zero();
-  sp_ready = true;
+  sp_ready = !sp_lv.empty();
 }
 
 std::vector<int> DeviceAmg::level_sizes() const {
@@ -621,30 +650,37 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
   }
   DeviceLevel& C = lv[l + 1];  // holds P_{l+1} (n_l x n_{l+1}) and R_{l+1} = P^T
   const bool coarse_next = l + 1 == last;
-  // sparse right-hand side (level 0, one pre-sweep from x = 0, §10f): the residual and R_1 rows that can
-  // only sum +0 products are set to +0 and the rest computed from row-subset copies of the operators
-  const bool sp = sparse_rhs && l == 0 && sp_ready && opt.pre_sweeps == 1;
-  // the sparse pass keeps its own residual / coarse right-hand side, +0 off the active rows since setup
-  double* rr = sp ? sp_r.get() : L.r.get();
-  if (sp) {
-    launch_bsr3(sp_fine, GPlain{cur}, EResid{b, rr}, s);  // r = b - A x on the active rows
-    if (Lg) Lg->add(sp_fine.matrix_bytes() + 8.0 * nd + 24.0 * 3.0 * sp_fine.n_brows);
+  // sparse right-hand side (one pre-sweep from x = 0, §10f): the residual and R_{l+1} rows that can
+  // only sum +0 products stay +0 in the pass's own buffers; the rest come from row-subset operators
+  const bool sp = sparse_rhs && sp_ready && l < int(sp_lv.size()) && opt.pre_sweeps == 1;
+  SpLevel* S = sp ? &sp_lv[l] : nullptr;
+  double* rr = sp ? S->r.get() : L.r.get();
+  if (sp && l == 0) {
+    launch_bsr3(S->fine, GPlain{cur}, EResid{b, rr}, s);  // r = b - A x on the active rows
+    if (Lg) Lg->add(S->fine.matrix_bytes() + 8.0 * nd + 24.0 * 3.0 * S->fine.n_brows);
+  } else if (sp && S->res_n > 0) {
+    launch_mat(L.Am, GPlain{cur}, EResid{b, rr}, s, S->res_rows.get(), S->res_n);
+    if (Lg) Lg->add(S->res_bytes + 8.0 * nd + 24.0 * S->res_n);
   } else {
     launch_level(L, GPlain{cur}, EResid{b, rr}, s);  // r = b - A x
     if (Lg) Lg->add(A_b + 24.0 * nd);
   }
-  const bool rsub = sp && C.R.strided;
-  double* bc = rsub ? sp_b1.get() : C.b.get();
-  if (rsub && !coarse_next)  // the level's scratch x^ is overwritten by the coarse correction: re-zero it
+  const bool rsub = sp && S->r_n > 0;
+  double* bc = sp ? S->bnext.get() : C.b.get();
+  if (sp && !coarse_next)  // the level's scratch x^ is overwritten by the coarse correction: re-zero it
     cuda_check(cudaMemsetAsync(C.xt.get(), 0, sizeof(double) * C.n, s), "memset xh_c");
-  const int* rrows = rsub ? sp_r1_rows.get() : nullptr;
-  const int rn = rsub ? sp_r1_n : 0;
+  const int* rrows = rsub ? S->r_rows.get() : nullptr;
+  const int rn = rsub ? S->r_n : 0;
   if (coarse_next)
     launch_mat(C.R, GPlain{rr}, EStore{bc}, s, rrows, rn);  // r_c = P^T r  (amg.cpp:166)
   else
     launch_mat(C.R, GPlain{rr}, EStorePre{bc, C.d.get(), w, C.xt.get()}, s, rrows, rn);
-  if (Lg) Lg->add((rsub ? sp_r1_bytes : C.R.matrix_bytes()) + 8.0 * nd + 8.0 * C.n * (coarse_next ? 1 : 3));
-  vcycle(l + 1, bc, C.x.get(), nullptr, coarse_next ? nullptr : C.xt.get(), s, Lg);
+  if (Lg) Lg->add((rsub ? S->r_bytes : C.R.matrix_bytes()) + 8.0 * nd + 8.0 * C.n * (coarse_next ? 1 : 3));
+  if (sp && l + 1 < int(sp_lv.size()) && !coarse_next) {
+    vcycle(l + 1, bc, C.x.get(), nullptr, C.xt.get(), s, Lg, true);
+  } else {
+    vcycle(l + 1, bc, C.x.get(), nullptr, coarse_next ? nullptr : C.xt.get(), s, Lg);
+  }
   launch_mat(C.P, GPlain{C.x.get()}, EAddTo{cur, cur}, s);  // x += P e_c  (amg.cpp:168-169)
   if (Lg) Lg->add(C.P.matrix_bytes() + 8.0 * C.n + 16.0 * nd);
   for (int it = 0; it < opt.post_sweeps; ++it) {

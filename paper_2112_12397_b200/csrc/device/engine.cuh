@@ -164,11 +164,17 @@ class DeviceAmg {
   // block rows of level 0 whose residual can be nonzero, and rows of R_1 that can gather a nonzero;
   // every other row's sum is an exact +0, so those rows skip their loads (bitwise the full sweep).
   void set_sparse_rhs(const std::vector<unsigned char>& rhs_rows, const fpb::HostAmg& h);
-  DBsr3 sp_fine;              // the level-0 operator restricted to the block rows whose residual can be nonzero
-  DevBuf<int> sp_r1_rows;     // rows of R_1 that can gather a nonzero
-  int sp_r1_n = 0;
-  double sp_r1_bytes = 0.0;   // their CSR bytes
-  DevBuf<double> sp_r, sp_b1; // the sparse pass's level-0 residual and level-1 rhs (+0 off the active rows)
+  struct SpLevel {             // the sparse pass at one level (§10f)
+    DBsr3 fine;                // level 0: the operator restricted to the block rows whose residual can be nonzero
+    DevBuf<int> res_rows;      // level >= 1: those rows (warp-row kernel row list)
+    int res_n = 0;
+    double res_bytes = 0.0;
+    DevBuf<int> r_rows;        // rows of R_{l+1} that can gather a nonzero
+    int r_n = 0;
+    double r_bytes = 0.0;
+    DevBuf<double> r, bnext;   // this level's residual and the next level's rhs: +0 off the active rows
+  };
+  std::vector<SpLevel> sp_lv;  // levels 0 .. sp_lv.size()-1 run the sparse pass
   bool sp_ready = false;
   std::vector<int> level_sizes() const;
   std::vector<DeviceLevel> lv;
