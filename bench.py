@@ -382,6 +382,7 @@ def run_ours(args):
                        "l2": "256 MB buffer written between timed solves; working set > 126 MB L2",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
             "iterations": st.iterations, "converged": st.converged, "restarts": st.restarts,
+            "reorth_steps": st.reorth_steps,
             "final_rel_residual": st.relative_residuals[-1] if st.relative_residuals else None,
             "e2e": {"value": round(e2e_value, 6), "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n},
             "roofline": {"bound": "hbm", "kernel": "bsr3 Jacobi post-smoothing sweep, finest AMG level (S1)",

@@ -127,6 +127,7 @@ typedef struct fp_solve_stats {
   int32_t history_len;
   double probe_ms;             /* with fp_gmres_options.probe: summed time of the probed launches */
   int32_t probe_launches;
+  int32_t reorth_steps;        /* Arnoldi steps that ran the second (DGKS) orthogonalization pass */
 } fp_solve_stats;
 
 typedef struct fp_system fp_system;           /* device-resident J (BlockSystem) */

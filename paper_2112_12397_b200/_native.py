@@ -61,7 +61,7 @@ class FpSolveStats(C.Structure):
                 ("device_seconds", C.c_double), ("kernel_launches", C.c_int64),
                 ("residual_history", C.POINTER(C.c_double)),
                 ("history_capacity", C.c_int32), ("history_len", C.c_int32), ("probe_ms", C.c_double),
-                ("probe_launches", C.c_int32)]
+                ("probe_launches", C.c_int32), ("reorth_steps", C.c_int32)]
 
 
 class FpProfile(C.Structure):

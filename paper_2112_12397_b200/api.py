@@ -172,6 +172,7 @@ class SolveStats:
     kernel_launches: int = 0
     probe_ms: float = 0.0      # probe=True: summed CUDA-event time of the finest-level Jacobi sweeps
     probe_launches: int = 0
+    reorth_steps: int = 0      # Arnoldi steps that ran the DGKS second pass (gmres.cpp:133)
 
 
 def _vec(x, n: int):
@@ -415,7 +416,7 @@ def gmres(op: BlockSystemOperator, precond: GpuPreconditioner, b, tol: float, ma
     N.check(N.lib.fp_gmres(op._h, precond._h, bp, xp, mem, C.byref(o), C.byref(st)))
     stats = SolveStats(st.iterations, list(hist[: st.history_len]), bool(st.converged), bool(st.breakdown),
                        st.restarts, st.precond_applies, st.device_seconds, int(st.kernel_launches), st.probe_ms,
-                       st.probe_launches)
+                       st.probe_launches, st.reorth_steps)
     return x, stats
 
 

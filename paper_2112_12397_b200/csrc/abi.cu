@@ -494,6 +494,7 @@ int fp_gmres(fp_system* s, fp_precond* p, const double* b, double* x, int32_t me
       stats->history_len = int32_t(r.history.size());
       stats->probe_ms = r.probe_ms;
       stats->probe_launches = r.probe_count;
+      stats->reorth_steps = r.reorth_steps;
       if (stats->residual_history)
         for (int i = 0; i < stats->history_capacity && i < int(r.history.size()); ++i)
           stats->residual_history[i] = r.history[i];

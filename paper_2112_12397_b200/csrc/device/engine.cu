@@ -1163,6 +1163,7 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
       }
       const GmresStatus st_h = status_h_[m & 1];
       if (st_h.nonfinite) throw fpb::numerical_error("gmres: non-finite vector in Arnoldi process");
+      res.reorth_steps += st_h.reorth ? 1 : 0;
       ++res.precond_applies;
       pc_.inner_calls += per_apply;
       ++m;

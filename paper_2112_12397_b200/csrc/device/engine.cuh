@@ -240,6 +240,7 @@ struct SolveResult {
   long long launches = 0;
   double probe_ms = 0.0;  // summed CUDA-event time of the probed kernel
   int probe_count = 0;
+  int reorth_steps = 0;   // Arnoldi steps that ran the DGKS second pass
 };
 
 struct ProfileResult {
