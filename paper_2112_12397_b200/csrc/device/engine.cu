@@ -56,7 +56,11 @@ int sm_count() {
 template <class G, class E>
 void launch_sell(const DSell& A, const G& g, const E& e, cudaStream_t s) {
   if (A.n_rows == 0) return;
-  launch(sell_kernel<G, E>, dim3(blocks_for(A.n_rows, 256)), dim3(256), 0, s, "sell_kernel", A.view(), g, e);
+  // 8 entries per round from 16 entries per row on (P_1: A/B config 2 apply 0.3521 -> 0.3510 ms)
+  if (A.nnz >= 16LL * A.n_rows)
+    launch(sell_kernel<G, E, 8>, dim3(blocks_for(A.n_rows, 256)), dim3(256), 0, s, "sell_kernel", A.view(), g, e);
+  else
+    launch(sell_kernel<G, E>, dim3(blocks_for(A.n_rows, 256)), dim3(256), 0, s, "sell_kernel", A.view(), g, e);
   cuda_check(cudaGetLastError(), "sell_kernel launch");
 }
 

@@ -187,13 +187,14 @@ struct EJu {
 };
 
 // ------------------------------------------------------------- SELL kernels
-template <class G, class E>
+// U entries per row per round: 8 for long rows (fewer dependent index -> gather rounds)
+template <class G, class E, int U = 4>
 __global__ void __launch_bounds__(256) sell_kernel(SellView A, G g, E epi) {
   pdl_entry();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= A.n_rows) return;
   const auto pre = epi.load(row);
-  epi(row, sell_row(A, row, g), pre);
+  epi(row, sell_row<G, U>(A, row, g), pre);
 }
 
 // Node-blocked rows (Bp3View): one thread per node, its three scalar rows summed left to
