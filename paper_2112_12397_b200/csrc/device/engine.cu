@@ -963,7 +963,7 @@ GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart
     }
   }
   big_nblk_ = int((n_ + kBigTile - 1) / kBigTile);
-  partial_.alloc(size_t(std::max({(ldr_ + 3) * (long long)mgs_grid_, (long long)red_grid_,
+  partial_.alloc(size_t(std::max({(2 * ldr_ + 4) * (long long)mgs_grid_, (long long)red_grid_,
                                   (ldr_ + 2) * (long long)big_nblk_})));
   big_coef_.alloc(size_t(ldr_ + 2));
   big_state_.alloc(1);

@@ -391,6 +391,8 @@ __global__ void __launch_bounds__(kMgsThreads) cgs_kernel(MgsArgs a) {
   double* partA = a.partial;                                 // ncol sets: <V_i, w>
   double* partB = a.partial + (long long)ncol * nb;          // ||w||^2 after a pass
   double* partC = a.partial + (long long)(ncol + 1) * nb;    // ||w_pre||^2
+  double* partD = a.partial + (long long)(ncol + 2) * nb;    // ncol sets: second-pass <V_i, w'>
+  double* partE = a.partial + (long long)(2 * ncol + 2) * nb;  // ||w''||^2
   double wr[EW];
   // fixed-order totals of `cnt` partial sets: warp q sums sets q, q + 16, ... (lanes
   // strided over blocks, then an xor tree): identical in every block and run
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(kMgsThreads) cgs_kernel(MgsArgs a) {
     }
   };
   // block partials of <V_i, w>, i < ncol -> partA
-  auto dots = [&] {
+  auto dots = [&](double* dst) {
     for (int i0 = 0; i0 < ncol; i0 += kB) {
       double acc[kB];
 #pragma unroll
@@ -456,7 +458,7 @@ __global__ void __launch_bounds__(kMgsThreads) cgs_kernel(MgsArgs a) {
         if (threadIdx.x < cnt) {
           double t = 0.0;
           for (int q = 0; q < kWarps; ++q) t += red[threadIdx.x][q];
-          partA[(long long)(g0 + threadIdx.x) * nb + blockIdx.x] = t;
+          dst[(long long)(g0 + threadIdx.x) * nb + blockIdx.x] = t;
         }
         __syncthreads();
       }
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(kMgsThreads) cgs_kernel(MgsArgs a) {
       n2 += v * v;
     }
   }
-  dots();
+  dots(partA);
   block_partial(n2, partC);
   grid.sync();
   totals(partA, ncol, hs);
@@ -534,21 +536,28 @@ __global__ void __launch_bounds__(kMgsThreads) cgs_kernel(MgsArgs a) {
   }
   if (blockIdx.x == 0)
     for (int i = threadIdx.x; i < ncol; i += kMgsThreads) a.h[i] = hs[i];
-  block_partial(project(hs), partB);
+  // E > 0: the second pass's dot products are formed right after the first projection from the
+  // same registers (speculatively: the DGKS test, true in ~97% of the bench's steps, decides after
+  // the barrier whether they are used), saving one grid barrier; same sums, same order
+  const double n2p = project(hs);
+  if constexpr (E > 0) dots(partD);
+  block_partial(n2p, partB);
   grid.sync();
   totals(partB, 1, sc + 1);
   double hnext = sqrt(sc[1]);
   int reorth = 0;
   if (hnext < 0.70710678118654752 * wnorm_pre) {  // gmres.cpp:133
     reorth = 1;
-    dots();
-    grid.sync();
-    totals(partA, ncol, hs);
+    if constexpr (E == 0) {
+      dots(partD);
+      grid.sync();
+    }
+    totals(partD, ncol, hs);
     if (blockIdx.x == 0)
       for (int i = threadIdx.x; i < ncol; i += kMgsThreads) a.h[i] += hs[i];
-    block_partial(project(hs), partB);
+    block_partial(project(hs), partE);
     grid.sync();
-    totals(partB, 1, sc + 2);
+    totals(partE, 1, sc + 2);
     hnext = sqrt(sc[2]);
   }
   const bool finite = isfinite(hnext);
