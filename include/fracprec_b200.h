@@ -16,7 +16,12 @@
  *     (row_offsets64); exactly one must be non-null.
  *   - handles own all device memory; host arrays are borrowed for the call.
  *   - `mem` selects where vector arguments live: FP_MEM_HOST or FP_MEM_DEVICE.
- *   - one CUDA stream per system handle; calls on one handle are serialized.
+ *   - one CUDA stream per system handle (non-blocking); calls on one handle are
+ *     serialized.  Ordering contract for FP_MEM_DEVICE vectors: the call does
+ *     not wait on any other stream, so the caller must complete the producers
+ *     of its inputs first (the Python mirror synchronizes torch's current
+ *     stream); every call returns only after its outputs are written, so they
+ *     may be consumed on any stream afterwards.
  */
 #ifndef FRACPREC_B200_H
 #define FRACPREC_B200_H
@@ -98,7 +103,7 @@ typedef struct fp_precond_config {
 } fp_precond_config;
 
 /* Arnoldi orthogonalization.  Both use the reference's DGKS second-pass test
- * (gmres.cpp:126-139: repeat the pass when ||w|| < ||w_pre|| / sqrt 2).
+ * (gmres.cpp:96-102: repeat the pass when ||w|| < ||w_pre|| / sqrt 2).
  * FP_ORTH_MGS - modified Gram-Schmidt, the reference's own loop (default);
  *               one grid-wide reduction per basis vector.
  * FP_ORTH_CGS - classical Gram-Schmidt: all coefficients of a pass from one
@@ -181,6 +186,12 @@ int fp_host_precond_matrix(const fp_host_precond* p, int32_t what, int32_t level
 /* what 0 = H~ blocks (9 n_p), 1 = T_diag (t-p-u) or S_K (t-u-p), 2 = smoother diag of level `level`,
  * 3 = {lambda_max} of level `level` (Chebyshev smoother, extension) */
 int fp_host_precond_vector(const fp_host_precond* p, int32_t what, int32_t level, double* out, int64_t* len);
+
+/* build_tpu / build_tup (precond.cpp:119-202) on a generated workload (libfp_workload.so,
+ * include/fracprec_workload.h) and its node coordinates in place — fp_host_precond_build
+ * without copying the blocks (the large configs' fine operator is tens of GB on the host) */
+typedef struct fp_workload fp_workload;
+int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config* cfg, fp_host_precond** out);
 
 /* ---- upload to the device */
 int fp_precond_create(fp_system* s, const fp_host_precond* hp, fp_precond** out);

@@ -49,7 +49,12 @@ inline fp_csr csr_view(int rows, int cols, const int* row_offsets, const int* co
   return v;
 }
 
-// Mirror of fracprec::LinearOperator (operator.hpp:17-28).
+// Mirror of fracprec::LinearOperator (operator.hpp:17-28).  The GPU operators below are
+// templates over their base class, so a reference build derives them from the reference's own
+// interface instead: after #include "fracprec/operator.hpp",
+//   using GpuSystemOperator = fracprec_b200::GpuSystemOperatorT<fracprec::LinearOperator>;
+// and fracprec::gmres(op, &M, b, tol) drives the B200 applies unchanged (
+// tests/cpp/oracle_gmres_dropin.cpp does exactly this with the oracle's restated gmres()).
 class LinearOperator {
  public:
   virtual ~LinearOperator() = default;
@@ -62,38 +67,52 @@ class LinearOperator {
   }
 };
 
+// The reference's "spmv: dimension mismatch" / "gmres: rhs dimension mismatch" checks: the C ABI
+// reads and writes n doubles through raw pointers, so a short span is rejected before the call.
+inline void check_dims(const char* what, size_t n, std::span<const double> x, std::span<double> y) {
+  if (x.size() != n || y.size() != n) throw std::invalid_argument(std::string(what) + ": dimension mismatch");
+}
+
 // Device-resident J (BlockSystemOperator, block.hpp:48-57).
-class GpuSystemOperator : public LinearOperator {
+template <class Base = LinearOperator>
+class GpuSystemOperatorT : public Base {
  public:
-  explicit GpuSystemOperator(const fp_block_system& J) { check(fp_system_create(&J, &h_)); }
-  ~GpuSystemOperator() override { fp_system_destroy(h_); }
-  GpuSystemOperator(const GpuSystemOperator&) = delete;
-  GpuSystemOperator& operator=(const GpuSystemOperator&) = delete;
-  int dimension() const override {
+  explicit GpuSystemOperatorT(const fp_block_system& J) {
+    check(fp_system_create(&J, &h_));
     int32_t nu = 0, nt = 0, np = 0;
     check(fp_system_dims(h_, &nu, &nt, &np));
-    return nu + nt + np;
+    n_ = nu + nt + np;
   }
+  ~GpuSystemOperatorT() override { fp_system_destroy(h_); }
+  GpuSystemOperatorT(const GpuSystemOperatorT&) = delete;
+  GpuSystemOperatorT& operator=(const GpuSystemOperatorT&) = delete;
+  int dimension() const override { return n_; }
   void apply(std::span<const double> x, std::span<double> y) const override {
+    check_dims("BlockSystemOperator::apply", size_t(n_), x, y);
     check(fp_system_apply(h_, x.data(), y.data(), FP_MEM_HOST));
   }
+  // x, y: device pointers to n = dimension() doubles whose producers have completed
   void apply_device(const double* x, double* y) const { check(fp_system_apply(h_, x, y, FP_MEM_DEVICE)); }
   fp_system* handle() const { return h_; }
 
  private:
   fp_system* h_ = nullptr;
+  int n_ = 0;
 };
 
 // Device-resident M^-1 (TpuOperator / TupOperator, precond.hpp:94-116) with the
 // inner-solver call counter of InnerSolver (precond.hpp:34-42).
-class GpuPrecondOperator : public LinearOperator {
+template <class Base = LinearOperator>
+class GpuPrecondOperatorT : public Base {
  public:
-  GpuPrecondOperator(const GpuSystemOperator& sys, fp_precond* h) : sys_(&sys), h_(h) {}
-  ~GpuPrecondOperator() override { fp_precond_destroy(h_); }
-  GpuPrecondOperator(const GpuPrecondOperator&) = delete;
-  GpuPrecondOperator& operator=(const GpuPrecondOperator&) = delete;
-  int dimension() const override { return sys_->dimension(); }
+  template <class SysBase>
+  GpuPrecondOperatorT(const GpuSystemOperatorT<SysBase>& sys, fp_precond* h) : h_(h), n_(sys.dimension()) {}
+  ~GpuPrecondOperatorT() override { fp_precond_destroy(h_); }
+  GpuPrecondOperatorT(const GpuPrecondOperatorT&) = delete;
+  GpuPrecondOperatorT& operator=(const GpuPrecondOperatorT&) = delete;
+  int dimension() const override { return n_; }
   void apply(std::span<const double> x, std::span<double> y) const override {
+    check_dims("TupOperator::apply", size_t(n_), x, y);
     check(fp_precond_apply(h_, x.data(), y.data(), FP_MEM_HOST));
   }
   void apply_device(const double* x, double* y) const { check(fp_precond_apply(h_, x, y, FP_MEM_DEVICE)); }
@@ -102,9 +121,12 @@ class GpuPrecondOperator : public LinearOperator {
   fp_precond* handle() const { return h_; }
 
  private:
-  const GpuSystemOperator* sys_;
   fp_precond* h_;
+  int n_;
 };
+
+using GpuSystemOperator = GpuSystemOperatorT<>;
+using GpuPrecondOperator = GpuPrecondOperatorT<>;
 
 inline fp_amg_config default_amg() {
   fp_amg_config c;
@@ -113,8 +135,10 @@ inline fp_amg_config default_amg() {
 }
 
 // build_tpu / build_tup / t-u-p* (precond.cpp:119-202): host setup, then upload.
-inline GpuPrecondOperator* build(const GpuSystemOperator& sys, const fp_block_system& J, int variant,
-                                 const fp_amg_config& amg, std::span<const std::array<double, 3>> coords = {}) {
+template <class Base = LinearOperator, class SysBase>
+inline GpuPrecondOperatorT<Base>* build(const GpuSystemOperatorT<SysBase>& sys, const fp_block_system& J,
+                                        int variant, const fp_amg_config& amg,
+                                        std::span<const std::array<double, 3>> coords = {}) {
   fp_precond_config cfg{variant, amg};
   fp_host_precond* hp = nullptr;
   check(fp_host_precond_build(&J, &cfg, coords.empty() ? nullptr : coords.data()->data(),
@@ -123,7 +147,7 @@ inline GpuPrecondOperator* build(const GpuSystemOperator& sys, const fp_block_sy
   const int st = fp_precond_create(sys.handle(), hp, &p);
   fp_host_precond_destroy(hp);
   check(st);
-  return new GpuPrecondOperator(sys, p);
+  return new GpuPrecondOperatorT<Base>(sys, p);
 }
 
 struct SolveStats {  // gmres.hpp:15-22
@@ -137,10 +161,15 @@ struct SolveStats {  // gmres.hpp:15-22
 
 // gmres(op, precond, b, tol, max_iter) (gmres.hpp:29-33); restart >= max_iter is
 // the reference's full GMRES; scaled = the driver's D J D system (driver.cpp:229-255).
-inline std::pair<std::vector<double>, SolveStats> gmres(const GpuSystemOperator& op, const GpuPrecondOperator& M,
+template <class SysBase, class PcBase>
+inline std::pair<std::vector<double>, SolveStats> gmres(const GpuSystemOperatorT<SysBase>& op,
+                                                        const GpuPrecondOperatorT<PcBase>& M,
                                                         std::span<const double> b, double tol, int max_iter = 500,
                                                         int restart = 0, bool scaled = false,
                                                         int orthogonalization = FP_ORTH_MGS) {
+  if (int(b.size()) != op.dimension()) throw std::invalid_argument("gmres: rhs dimension mismatch");
+  if (M.dimension() != op.dimension()) throw std::invalid_argument("gmres: preconditioner dimension mismatch");
+  if (!(tol > 0.0)) throw std::invalid_argument("gmres: tol must be positive");
   std::vector<double> x(b.size());
   SolveStats st;
   st.relative_residuals.resize(static_cast<size_t>(std::max(1, max_iter)));

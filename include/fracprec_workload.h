@@ -1,13 +1,18 @@
 /*
- * fracprec_b200 workload generator — synthetic inputs for the BASELINE.json
- * configs (structured hex mesh with duplicated fracture nodes, trilinear
- * elasticity, TPFA fracture flow, seeded contact state).  Restates the
- * reference's input side (/root/reference/proj/core/src/mesh.cpp,
- * assembly.cpp), which is not on the solve path; it is exported so tests and
- * bench.py can build the same systems the GPU solves.
+ * fracprec workload generator (libfp_workload.so, workload/) — synthetic inputs
+ * for the BASELINE.json configs (structured hex mesh with duplicated fracture
+ * nodes, trilinear elasticity, TPFA fracture flow, seeded contact state) and
+ * the snapshot bundle reader/writer.  Restates the reference's input side
+ * (/root/reference/proj/core/src/mesh.cpp, assembly.cpp, snapshot.cpp, mmio.cpp),
+ * which is not on the solve path.  A host-only library of its own: the B200
+ * solve library and the CPU oracle's callers both build the same systems from
+ * it, and the oracle-side callers never load the solve library.
+ *
+ * Only the data types of fracprec_b200.h are used (no link dependency).  Status
+ * codes are FP_*; fp_workload_last_error() gives this library's message.
  */
-#ifndef FRACPREC_B200_WORKLOAD_H
-#define FRACPREC_B200_WORKLOAD_H
+#ifndef FRACPREC_WORKLOAD_H
+#define FRACPREC_WORKLOAD_H
 
 #include <stdint.h>
 
@@ -39,6 +44,8 @@ typedef struct fp_workload_spec {
 
 typedef struct fp_workload fp_workload;
 
+const char* fp_workload_last_error(void);
+
 /* config_id 1..5 = BASELINE.json configs[0..4] */
 int fp_workload_preset(int32_t config_id, uint64_t seed, fp_workload** out);
 int fp_workload_custom(const fp_workload_spec* spec, fp_workload** out);
@@ -48,10 +55,6 @@ int fp_workload_system(const fp_workload* w, fp_block_system* J);
 int fp_workload_coords(const fp_workload* w, const double** xyz, int32_t* n_nodes);
 /* counts[0..3] = stick, slip, open, fractures */
 int fp_workload_info(const fp_workload* w, int32_t* counts);
-/* build_tpu / build_tup (precond.cpp:119-202) on the generated system and node
- * coordinates in place — fp_host_precond_build without copying the blocks
- * (the large configs' fine operator is tens of GB on the host) */
-int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config* cfg, fp_host_precond** out);
 /* per-face contact state ('s' stick, 'l' slip, 'o' open; Snapshot::region_string, snapshot.cpp:20-25)
  * and the time step; the string is valid until destroy */
 int fp_workload_region(const fp_workload* w, const char** region, double* dt);

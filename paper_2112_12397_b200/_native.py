@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # FRACPREC_B200_LIB overrides the in-tree library (A/B builds of kernel variants)
@@ -27,15 +28,11 @@ class CudaError(RuntimeError):
     """A CUDA failure inside the native library."""
 
 
-class FpCsr(C.Structure):
-    _fields_ = [("n_rows", C.c_int32), ("n_cols", C.c_int32),
-                ("row_offsets32", C.POINTER(C.c_int32)), ("row_offsets64", C.POINTER(C.c_int64)),
-                ("col_indices", C.POINTER(C.c_int32)), ("values", C.POINTER(C.c_double))]
-
-
-class FpBlockSystem(C.Structure):
-    _fields_ = [("n_u", C.c_int32), ("n_t", C.c_int32), ("n_p", C.c_int32)] + \
-               [(nm, FpCsr) for nm in ("A", "C1", "Q1", "C2", "H", "Q2", "T", "F_u")]
+# fp_csr / fp_block_system / the generator's spec structs: shared with the workload binding
+# (workload/, a sibling of this package; its library is a dependency of this one)
+if os.path.dirname(_HERE) not in sys.path:
+    sys.path.insert(0, os.path.dirname(_HERE))
+from workload.gen import FpBlockSystem, FpCsr, FpFractureSpec, FpWorkloadSpec  # noqa: E402,F401
 
 
 class FpAmgConfig(C.Structure):
@@ -83,21 +80,8 @@ class FpPrecondDesc(C.Structure):
                 ("factor_solve", C.c_int32)]
 
 
-class FpFractureSpec(C.Structure):
-    _fields_ = [("normal_axis", C.c_int32), ("coord", C.c_double), ("lo1", C.c_double), ("hi1", C.c_double),
-                ("lo2", C.c_double), ("hi2", C.c_double)]
-
-
-class FpWorkloadSpec(C.Structure):
-    _fields_ = [("cells", C.c_int32 * 3), ("length", C.c_double * 3), ("n_fractures", C.c_int32),
-                ("fractures", C.POINTER(FpFractureSpec)), ("E_median", C.c_double), ("E_sigma_ln", C.c_double),
-                ("E_layers", C.c_int32), ("nu", C.c_double), ("nu_lo", C.c_double), ("nu_hi", C.c_double),
-                ("frac_stick", C.c_double), ("frac_slip", C.c_double), ("aperture_median", C.c_double),
-                ("aperture_sigma_ln", C.c_double), ("seed", C.c_uint64), ("stab_beta", C.c_double),
-                ("slip_factor", C.c_double)]
-
-
-# Every symbol include/*.h declares, with its ctypes signature (restype, argtypes).
+# Every symbol include/fracprec_b200.h declares, with its ctypes signature (restype, argtypes).
+# (include/fracprec_workload.h: libfp_workload.so, workload/gen.py SIGNATURES)
 _P = C.c_void_p
 _PP = C.POINTER(C.c_void_p)
 _DP = C.POINTER(C.c_double)
@@ -126,18 +110,9 @@ SIGNATURES = {
     "fp_precond_traffic": (C.c_int, [_P, _DP, C.POINTER(C.c_int32), _DP]),
     "fp_precond_profile": (C.c_int, [_P, C.c_int32, C.POINTER(FpProfile)]),
     "fp_gmres": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(FpGmresOptions), C.POINTER(FpSolveStats)]),
-    "fp_workload_preset": (C.c_int, [C.c_int32, C.c_uint64, _PP]),
-    "fp_workload_custom": (C.c_int, [C.POINTER(FpWorkloadSpec), _PP]),
-    "fp_workload_destroy": (None, [_P]),
-    "fp_workload_system": (C.c_int, [_P, C.POINTER(FpBlockSystem)]),
-    "fp_workload_coords": (C.c_int, [_P, C.POINTER(_DP), C.POINTER(C.c_int32)]),
-    "fp_workload_info": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "fp_workload_host_precond_build": (C.c_int, [_P, C.POINTER(FpPrecondConfig), _PP]),
-    "fp_workload_region": (C.c_int, [_P, C.POINTER(C.c_char_p), C.POINTER(C.c_double)]),
     "fp_setup_backend": (C.c_int, [C.POINTER(C.c_int32)]),
     "fp_set_setup_backend": (C.c_int, [C.c_int32]),
-    "fp_snapshot_import": (C.c_int, [C.c_char_p, _PP]),
-    "fp_snapshot_export": (C.c_int, [C.c_char_p, C.POINTER(FpBlockSystem), C.c_char_p, C.c_double, _DP, C.c_int32]),
 }
 
 

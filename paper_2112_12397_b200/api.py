@@ -20,6 +20,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _native as N
+from workload import gen as _wl  # the input-side generator library (loaded with the solve library)
 from ._native import NumericalError  # noqa: F401  (re-export)
 
 _VARIANTS = {"tpu": N.FP_TPU, "tup": N.FP_TUP, "tup_star": N.FP_TUP_STAR}
@@ -172,21 +173,38 @@ class SolveStats:
     kernel_launches: int = 0
     probe_ms: float = 0.0      # probe=True: summed CUDA-event time of the finest-level Jacobi sweeps
     probe_launches: int = 0
-    reorth_steps: int = 0      # Arnoldi steps that ran the DGKS second pass (gmres.cpp:133)
+    reorth_steps: int = 0      # Arnoldi steps that ran the DGKS second pass (gmres.cpp:96-102)
 
 
 def _vec(x, n: int):
-    """(pointer, mem kind, keepalive) for a NumPy array or a CUDA tensor of length n."""
+    """(pointer, mem kind, keepalive) for an input vector: a NumPy array or a CUDA tensor of length n.
+
+    The library runs on its own non-blocking stream, so before a device pointer is handed over the
+    producing torch stream is synchronized (the ABI call returns only after its results are written;
+    include/fracprec_b200.h states the ordering contract)."""
     if hasattr(x, "is_cuda") and x.is_cuda:
         import torch
 
         if x.dtype != torch.float64 or not x.is_contiguous() or x.numel() != n:
             raise ValueError("device vectors must be contiguous float64 tensors of the operator dimension")
+        torch.cuda.current_stream(x.device).synchronize()
         return C.c_void_p(x.data_ptr()), N.FP_MEM_DEVICE, x
     a = np.ascontiguousarray(x, dtype=np.float64)
     if a.size != n:
         raise ValueError(f"dimension mismatch: expected {n}, got {a.size}")
     return C.c_void_p(a.ctypes.data), N.FP_MEM_HOST, a
+
+
+def _out(y, n: int):
+    """(pointer, mem kind, keepalive) for an output vector, written in place: a writeable C-contiguous
+    float64 NumPy array or a contiguous float64 CUDA tensor of length n (no silent temporary copy)."""
+    if hasattr(y, "is_cuda") and y.is_cuda:
+        return _vec(y, n)
+    if not (isinstance(y, np.ndarray) and y.dtype == np.float64 and y.flags.c_contiguous and y.flags.writeable):
+        raise ValueError("output vectors must be writeable C-contiguous float64 arrays (or CUDA float64 tensors)")
+    if y.size != n:
+        raise ValueError(f"dimension mismatch: expected {n}, got {y.size}")
+    return C.c_void_p(y.ctypes.data), N.FP_MEM_HOST, y
 
 
 def _out_like(x, n: int):
@@ -217,7 +235,7 @@ class BlockSystemOperator:
     def apply(self, x, y=None):
         y = _out_like(x, self._n) if y is None else y
         xp, mem, _ka = _vec(x, self._n)
-        yp, mem2, _kb = _vec(y, self._n)
+        yp, mem2, _kb = _out(y, self._n)
         if mem != mem2:
             raise ValueError("x and y must live in the same memory space")
         N.check(N.lib.fp_system_apply(self._h, xp, yp, mem))
@@ -330,7 +348,9 @@ class GpuPreconditioner:
     def apply(self, x, y=None):
         y = _out_like(x, self._n) if y is None else y
         xp, mem, _ka = _vec(x, self._n)
-        yp, _mem2, _kb = _vec(y, self._n)
+        yp, mem2, _kb = _out(y, self._n)
+        if mem != mem2:
+            raise ValueError("x and y must live in the same memory space")
         N.check(N.lib.fp_precond_apply(self._h, xp, yp, mem))
         return y
 
@@ -340,7 +360,7 @@ class GpuPreconditioner:
         n_u = self.op.J.n_u
         x = _out_like(r, n_u)
         rp, mem, _ka = _vec(r, n_u)
-        xp, _m, _kb = _vec(x, n_u)
+        xp, _m, _kb = _out(x, n_u)
         N.check(N.lib.fp_amg_apply(self._h, rp, xp, mem))
         return x
 
@@ -402,7 +422,9 @@ def gmres(op: BlockSystemOperator, precond: GpuPreconditioner, b, tol: float, ma
     n = op.dimension()
     x = _out_like(b, n) if x is None else x
     bp, mem, _ka = _vec(b, n)
-    xp, _m, _kb = _vec(x, n)
+    xp, mem_x, _kb = _out(x, n)
+    if mem != mem_x:
+        raise ValueError("gmres: b and x must live in the same memory space")
     o = N.FpGmresOptions()
     if orthogonalization not in ("mgs", "cgs"):
         raise ValueError("gmres: orthogonalization must be 'mgs' or 'cgs'")
@@ -421,92 +443,45 @@ def gmres(op: BlockSystemOperator, precond: GpuPreconditioner, b, tol: float, ma
 
 
 # ----------------------------------------------------------------- workloads
+def _csr(t) -> CsrMatrix:
+    r, c, rp, ci, v = t
+    return CsrMatrix(r, c, rp, ci, v)
+
+
 class Workload:
-    """Synthetic BASELINE config (include/fracprec_b200_workload.h)."""
+    """Synthetic BASELINE config (include/fracprec_workload.h): the generator library's workload
+    (workload/gen.py) with its blocks as this API's BlockSystem."""
 
     def __init__(self, config_id: Optional[int] = None, seed: int = 42, spec: Optional[dict] = None,
-                 _handle: Optional[C.c_void_p] = None):
-        self._h = C.c_void_p()
-        if _handle is not None:
-            self._h = _handle
-        elif spec is None:
-            N.check(N.lib.fp_workload_preset(int(config_id), seed, C.byref(self._h)))
-        else:
-            s = N.FpWorkloadSpec()
-            s.cells[:] = spec["cells"]
-            s.length[:] = spec.get("length", (1.0, 1.0, 1.0))
-            fr = spec.get("fractures", [])
-            arr = (N.FpFractureSpec * max(1, len(fr)))()
-            for i, f in enumerate(fr):
-                arr[i] = N.FpFractureSpec(*f)
-            s.n_fractures, s.fractures = len(fr), arr
-            s.E_median, s.E_sigma_ln = spec.get("E_median", 10e9), spec.get("E_sigma_ln", 0.0)
-            s.E_layers, s.nu = spec.get("E_layers", 0), spec.get("nu", 0.25)
-            s.nu_lo, s.nu_hi = spec.get("nu_lo", 0.0), spec.get("nu_hi", 0.0)
-            s.frac_stick, s.frac_slip = spec.get("frac_stick", 0.7), spec.get("frac_slip", 0.2)
-            s.aperture_median = spec.get("aperture_median", 1e-4)
-            s.aperture_sigma_ln = spec.get("aperture_sigma_ln", 0.0)
-            s.seed = seed
-            s.stab_beta = spec.get("stab_beta", 0.0)
-            s.slip_factor = spec.get("slip_factor", 0.0)
-            N.check(N.lib.fp_workload_custom(C.byref(s), C.byref(self._h)))
+                 _gen: "Optional[_wl.Workload]" = None):
+        self._w = _gen if _gen is not None else _wl.Workload(config_id, seed, spec)
 
-    def __del__(self):
-        if getattr(self, "_h", None) and N is not None and getattr(N, "lib", None) is not None:
-            N.lib.fp_workload_destroy(self._h)
-            self._h = None
+    @property
+    def _h(self):
+        return self._w.handle
 
     @classmethod
     def from_snapshot(cls, directory: str) -> "Workload":
         """import_snapshot (snapshot.cpp:67-104): a reference snapshot bundle as a workload."""
-        h = C.c_void_p()
-        N.check(N.lib.fp_snapshot_import(str(directory).encode(), C.byref(h)))
-        return cls(_handle=h)
+        return cls(_gen=_wl.Workload.from_snapshot(directory))
 
     def region(self) -> tuple:
         """(per-face labels 's'/'l'/'o', dt)"""
-        r, dt = C.c_char_p(), C.c_double()
-        N.check(N.lib.fp_workload_region(self._h, C.byref(r), C.byref(dt)))
-        return r.value.decode(), dt.value
+        return self._w.region()
 
     def save_snapshot(self, directory: str) -> None:
         """export_snapshot of this workload (blocks, region labels, dt, node coordinates)."""
-        region, dt = self.region()
-        export_snapshot(directory, self.system(copy=False), region, dt)
+        self._w.save_snapshot(directory)
 
     def info(self) -> dict:
-        c = (C.c_int32 * 4)()
-        N.check(N.lib.fp_workload_info(self._h, c))
-        return {"stick": c[0], "slip": c[1], "open": c[2], "fractures": c[3]}
+        return self._w.info()
 
     def system(self, copy: bool = True) -> BlockSystem:
         """The generated blocks as a BlockSystem: owned NumPy copies, or (copy=False) read-only
         views into the workload's arrays that keep the Workload alive."""
-        v = N.FpBlockSystem()
-        N.check(N.lib.fp_workload_system(self._h, C.byref(v)))
-
-        def arr(p, n, dtype):
-            a = np.ctypeslib.as_array(p, shape=(n,))
-            if copy:
-                return a.copy()
-            a.flags.writeable = False
-            return a
-
-        def take(m: N.FpCsr) -> CsrMatrix:
-            if m.n_rows == 0:
-                return CsrMatrix.empty(0, m.n_cols)
-            rp = arr(m.row_offsets64, m.n_rows + 1, np.int64)
-            nz = int(rp[-1])
-            ci = arr(m.col_indices, nz, np.int32) if nz else np.zeros(0, np.int32)
-            vv = arr(m.values, nz, np.float64) if nz else np.zeros(0)
-            return CsrMatrix(m.n_rows, m.n_cols, rp, ci, vv)
-
-        xyz = C.POINTER(C.c_double)()
-        nn = C.c_int32()
-        N.check(N.lib.fp_workload_coords(self._h, C.byref(xyz), C.byref(nn)))
-        coords = np.ctypeslib.as_array(xyz, shape=(nn.value * 3,)).copy().reshape(-1, 3) if nn.value else None
-        blocks = {nm: take(getattr(v, nm)) for nm in ("A", "C1", "Q1", "C2", "H", "Q2", "T", "F_u")}
-        J = BlockSystem(v.n_u, v.n_t, v.n_p, node_coords=coords, **blocks)
+        S = self._w.system(copy=copy)
+        blocks = {nm: _csr(t) for nm, t in S.blocks.items()}
+        J = BlockSystem(S.n_u, S.n_t, S.n_p, node_coords=S.node_coords, **blocks)
         if not copy:
             J._owner = self  # the views point into this workload
         return J
@@ -514,10 +489,10 @@ class Workload:
 
 def export_snapshot(directory: str, J: BlockSystem, region: str, dt: float = 0.5) -> None:
     """export_snapshot (snapshot.cpp:28-65): manifest.json + Matrix Market blocks (+ coords.txt)."""
-    coords = None if J.node_coords is None else np.ascontiguousarray(J.node_coords, dtype=np.float64)
-    cp = coords.ctypes.data_as(C.POINTER(C.c_double)) if coords is not None else None
-    nn = 0 if coords is None else coords.shape[0]
-    N.check(N.lib.fp_snapshot_export(str(directory).encode(), C.byref(J.view()), region.encode(), float(dt), cp, nn))
+    blocks = {nm: (m.n_rows, m.n_cols, m.row_offsets, m.col_indices, m.values)
+              for nm, m in zip(_wl.BLOCK_NAMES, (J.A, J.C1, J.Q1, J.C2, J.H, J.Q2, J.T,
+                                                 J.F_u or CsrMatrix.empty(0, J.n_u)))}
+    _wl.export_snapshot(directory, blocks, J.n_u, J.n_t, J.n_p, region, dt, J.node_coords)
 
 
 def set_setup_backend(where: str) -> None:

@@ -11,11 +11,9 @@
 #include <string>
 
 #include "../../include/fracprec_b200.h"
-#include "../../include/fracprec_b200_workload.h"
 #include "device/engine.cuh"
 #include "host/setup.hpp"
-#include "host/snapshot.hpp"
-#include "host/workload.hpp"
+#include "workload.hpp"  // workload/ (libfp_workload.so): the fp_workload handle
 
 namespace {
 
@@ -161,10 +159,6 @@ void ensure_setup_backend() {
 
 struct fp_host_precond {
   fpb::HostPrecond hp;
-};
-
-struct fp_workload {
-  fpb::Workload w;
 };
 
 extern "C" {
@@ -503,56 +497,6 @@ int fp_gmres(fp_system* s, fp_precond* p, const double* b, double* x, int32_t me
 }
 
 // -------------------------------------------------------------- workload
-int fp_workload_preset(int32_t id, uint64_t seed, fp_workload** out) {
-  return guard([&] {
-    need(out != nullptr, "fp_workload_preset: null out");
-    auto w = std::make_unique<fp_workload>();
-    w->w = fpb::generate_workload(fpb::preset_config(id, seed));
-    *out = w.release();
-  });
-}
-
-int fp_workload_custom(const fp_workload_spec* sp, fp_workload** out) {
-  return guard([&] {
-    need(sp && out, "fp_workload_custom: null argument");
-    fpb::WorkloadSpec s;
-    for (int d = 0; d < 3; ++d) s.cells[d] = sp->cells[d], s.length[d] = sp->length[d];
-    for (int f = 0; f < sp->n_fractures; ++f) {
-      const fp_fracture_spec& q = sp->fractures[f];
-      s.fractures.push_back({q.normal_axis, q.coord, q.lo1, q.hi1, q.lo2, q.hi2});
-    }
-    s.E_median = sp->E_median, s.E_sigma_ln = sp->E_sigma_ln, s.E_layers = sp->E_layers;
-    s.nu = sp->nu, s.nu_lo = sp->nu_lo, s.nu_hi = sp->nu_hi;
-    s.frac_stick = sp->frac_stick, s.frac_slip = sp->frac_slip;
-    s.aperture_median = sp->aperture_median, s.aperture_sigma_ln = sp->aperture_sigma_ln;
-    s.seed = sp->seed;
-    if (sp->stab_beta > 0.0) s.stab_beta = sp->stab_beta;
-    if (sp->slip_factor > 0.0) s.slip_factor = sp->slip_factor;
-    auto w = std::make_unique<fp_workload>();
-    w->w = fpb::generate_workload(s);
-    *out = w.release();
-  });
-}
-
-void fp_workload_destroy(fp_workload* w) { delete w; }
-
-int fp_workload_system(const fp_workload* w, fp_block_system* J) {
-  return guard([&] {
-    need(w && J, "null argument");
-    const fpb::HostSystem& H = w->w.J;
-    J->n_u = H.n_u, J->n_t = H.n_t, J->n_p = H.n_p;
-    J->A = view_of(H.A), J->C1 = view_of(H.C1), J->Q1 = view_of(H.Q1), J->C2 = view_of(H.C2);
-    J->H = view_of(H.H), J->Q2 = view_of(H.Q2), J->T = view_of(H.T), J->F_u = view_of(H.F_u);
-  });
-}
-
-int fp_workload_coords(const fp_workload* w, const double** xyz, int32_t* n_nodes) {
-  return guard([&] {
-    need(w && xyz && n_nodes, "null argument");
-    *xyz = w->w.coords.empty() ? nullptr : w->w.coords[0].data();
-    *n_nodes = int32_t(w->w.coords.size());
-  });
-}
 
 int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config* cfg, fp_host_precond** out) {
   return guard([&] {
@@ -586,42 +530,6 @@ int fp_setup_backend(int32_t* device) {
     need(device, "null argument");
     ensure_setup_backend();
     *device = fpb::spgemm_backend_active() ? 1 : 0;
-  });
-}
-
-int fp_workload_region(const fp_workload* w, const char** region, double* dt) {
-  return guard([&] {
-    need(w && region && dt, "null argument");
-    *region = w->w.region.c_str();
-    *dt = w->w.dt;
-  });
-}
-
-int fp_snapshot_import(const char* dir, fp_workload** out) {
-  return guard([&] {
-    need(dir && out, "fp_snapshot_import: null argument");
-    auto p = std::make_unique<fp_workload>();
-    p->w = fpb::import_snapshot(dir);
-    *out = p.release();
-  });
-}
-
-int fp_snapshot_export(const char* dir, const fp_block_system* J, const char* region, double dt,
-                       const double* node_coords, int32_t n_nodes) {
-  return guard([&] {
-    need(dir && J && region, "fp_snapshot_export: null argument");
-    const fpb::HostSystem H = to_system(*J);
-    std::vector<std::array<double, 3>> xyz;
-    for (int v = 0; node_coords && v < n_nodes; ++v)
-      xyz.push_back({node_coords[3 * v], node_coords[3 * v + 1], node_coords[3 * v + 2]});
-    fpb::export_snapshot(dir, H, std::string(region, strnlen(region, size_t(H.n_p) + 1)), dt, xyz);
-  });
-}
-
-int fp_workload_info(const fp_workload* w, int32_t* c) {
-  return guard([&] {
-    need(w && c, "null argument");
-    c[0] = w->w.n_stick, c[1] = w->w.n_slip, c[2] = w->w.n_open, c[3] = w->w.n_fractures;
   });
 }
 

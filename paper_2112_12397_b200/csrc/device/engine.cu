@@ -1121,6 +1121,7 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
     const int budget = std::min(restart_, o.max_iter - res.iterations);
     if (budget <= 0) break;
     const double tol_c = o.tol * bnorm / rnorm;
+    const double rnorm_start = rnorm;
     launch(start_cycle_kernel, dim3(blocks_for(n_, 256)), dim3(256), 0, s, "start_cycle_kernel", n_, r_.get(), scal_.get(), V_.get(), stage);
     cuda_check(cudaMemcpyAsync(g_.get(), &rnorm, sizeof(double), cudaMemcpyHostToDevice, s), "g0");
     int m = 0, assembled_at = -1;
@@ -1173,21 +1174,21 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
       ++m;
       ++res.iterations;
       res.history.push_back(st_h.est * rnorm / bnorm);
-      if (st_h.happy) {  // gmres.cpp:175-183
+      if (st_h.happy) {  // gmres.cpp:138-146
         happy = true;
         res.breakdown = true;
         assemble(m);
         cyc_done = true;
         break;
       }
-      if (st_h.est <= tol_c) {  // gmres.cpp:184-193
+      if (st_h.est <= tol_c) {  // gmres.cpp:147-156
         assemble(m);
         if (tr <= tol_c) {
           cyc_done = true;
           break;
         }
         hit = true;
-      } else if (m % 50 == 0 || hit) {  // gmres.cpp:194-203
+      } else if (m % 50 == 0 || hit) {  // gmres.cpp:157-166
         assemble(m);
         if (tr <= tol_c) {
           cyc_done = true;
@@ -1200,13 +1201,14 @@ SolveResult GmresSolver::solve(const double* b, double* x_out, const SolveOption
         cuda_check(cudaMemcpyAsync(stage, V_.get() + size_t(enq) * ldv_, vb, cudaMemcpyDeviceToDevice, s), "restage");
     }
     if (!cyc_done && assembled_at != m) assemble(m);
-    (void)happy;
     launch(add_inplace_kernel, dim3(blocks_for(n_, 256)), dim3(256), 0, s, "add_inplace_kernel", n_, xtot_.get(), dx_.get());
     cuda_check(cudaGraphLaunch(j_exec_, s), "graph launch j");
     rnorm = norm_into(b, jout_.get(), r_.get(), scal_.get(), s);  // r = b - J x, beta on device
     res.launches += 1 + japply_launches + 2;
     if (!res.history.empty()) res.history.back() = rnorm / bnorm;
-    if (rnorm <= o.tol * bnorm) {
+    // gmres.cpp:142: a happy breakdown also converges at a true relative residual <= 1e-12
+    // (relative to the cycle's right-hand side; for full GMRES that is ||b||)
+    if (rnorm <= o.tol * bnorm || (happy && rnorm <= 1e-12 * rnorm_start)) {
       res.converged = true;
       break;
     }

@@ -1,7 +1,7 @@
 // Device-resident Arnoldi for right-preconditioned GMRES
-// (/root/reference/proj/core/src/gmres.cpp:118-174).  One cooperative kernel
+// (/root/reference/proj/core/src/gmres.cpp:81-167).  One cooperative kernel
 // per iteration performs modified Gram-Schmidt with the reference's selective
-// reorthogonalization (gmres.cpp:126-139), the happy-breakdown test (:144),
+// reorthogonalization (gmres.cpp:96-102), the happy-breakdown test (:107),
 // normalization (:145-149) and the Givens update of the least-squares problem
 // (:151-171).  Each MGS step is one fused pass "w -= h_i V_i ; partial(V_{i+1}.w)"
 // followed by a grid barrier; reductions are fixed-order (per-block tree, then
@@ -66,7 +66,7 @@ __device__ __forceinline__ double grid_total(const double* part, int nb, double*
   return sm[32];
 }
 
-// status + Givens update of the least-squares problem (gmres.cpp:151-171), one thread
+// status + Givens update of the least-squares problem (gmres.cpp:114-131), one thread
 __device__ __forceinline__ void mgs_finish(const MgsArgs& a, double hnext, double wnorm_pre, int reorth, bool finite,
                                            bool happy) {
   GmresStatus st;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_kernel(MgsArgs a) {
   }
   double hnext = sqrt(nrm2);
   int reorth = 0;
-  if (hnext < 0.70710678118654752 * wnorm_pre) {  // gmres.cpp:133
+  if (hnext < 0.70710678118654752 * wnorm_pre) {  // gmres.cpp:96
     reorth = 1;
     double acc = 0.0;
     for (long long k = lo + threadIdx.x; k < hi; k += blockDim.x) acc += V0[k] * w[k];
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_fast_kernel(MgsArgs a) {
   };
   double hnext = sqrt(sweep(h0, false));
   int reorth = 0;
-  if (hnext < 0.70710678118654752 * wnorm_pre) {  // gmres.cpp:133
+  if (hnext < 0.70710678118654752 * wnorm_pre) {  // gmres.cpp:96
     reorth = 1;
     load(a.V, vc);
     double acc = 0.0;
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kMgsThreads) mgs_fast_kernel(MgsArgs a) {
 }
 
 // Classical Gram-Schmidt Arnoldi step with the same DGKS test as the reference
-// (gmres.cpp:126-139: a second pass when ||w|| < ||w_pre|| / sqrt 2), selectable
+// (gmres.cpp:96-102: a second pass when ||w|| < ||w_pre|| / sqrt 2), selectable
 // instead of MGS (orthogonalization = cgs).  Every projection coefficient of a
 // pass comes from ONE grid reduction (all m + 1 dot products at once), so a step
 // costs 2 grid barriers (4 with the second pass) instead of 2 (m + 1), at the
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(kMgsThreads) cgs_kernel(MgsArgs a) {
   totals(partB, 1, sc + 1);
   double hnext = sqrt(sc[1]);
   int reorth = 0;
-  if (hnext < 0.70710678118654752 * wnorm_pre) {  // gmres.cpp:133
+  if (hnext < 0.70710678118654752 * wnorm_pre) {  // gmres.cpp:96
     reorth = 1;
     if constexpr (E == 0) {
       dots(partD);
@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(kBigT) cgs_big_dots(CgsBigArgs b) {
 }
 
 // coefficients: warp q sums the tile partials of sets q, q + 16, ... (lane-strided, then an
-// xor tree); the first pass also sets h and ||w_pre||, the second adds to h (gmres.cpp:126-139)
+// xor tree); the first pass also sets h and ||w_pre||, the second adds to h (gmres.cpp:96-102)
 __global__ void __launch_bounds__(kBigT) cgs_big_reduce(CgsBigArgs b) {
   if (b.st->abort || (b.pass == 1 && !b.st->reorth)) return;
   const MgsArgs& a = b.a;
@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(kBigT) cgs_big_norm(CgsBigArgs b, int last) {
   }
   if (threadIdx.x != 0) return;
   if (b.pass == 0 && !last) {
-    b.st->reorth = b.st->hnext < 0.70710678118654752 * b.st->wnorm_pre;  // gmres.cpp:133
+    b.st->reorth = b.st->hnext < 0.70710678118654752 * b.st->wnorm_pre;  // gmres.cpp:96
     return;
   }
   const double hnext = b.st->hnext, wnorm_pre = b.st->wnorm_pre;
@@ -770,7 +770,7 @@ __global__ void __launch_bounds__(kBigT) cgs_big_normalize(CgsBigArgs b) {
   }
 }
 
-// y = R(0:m,0:m)^-1 g(0:m)  (gmres.cpp:92-98), one thread; flags a zero pivot
+// y = R(0:m,0:m)^-1 g(0:m)  (gmres.cpp:55-61), one thread; flags a zero pivot
 __global__ void backsub_kernel(int m, int ldr, const double* R, const double* g, double* y, int* singular) {
   pdl_entry();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -787,7 +787,7 @@ __global__ void backsub_kernel(int m, int ldr, const double* R, const double* g,
   }
 }
 
-// u_i = sum_{j<m} V_j[i] y_j, j ascending from 0 (gmres.cpp:99-101)
+// u_i = sum_{j<m} V_j[i] y_j, j ascending from 0 (gmres.cpp:62-64)
 __global__ void basis_combine_kernel(long long n, long long ldv, int m, const double* V, const double* y, double* u) {
   pdl_entry();
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;

@@ -89,44 +89,6 @@ struct NoScratch {};
 
 }  // namespace
 
-Csr Csr::identity(int n) {
-  Csr I(n, n);
-  I.ci.resize(static_cast<size_t>(n));
-  I.v.assign(static_cast<size_t>(n), 1.0);
-  for (int i = 0; i < n; ++i) I.ci[i] = i, I.rp[i + 1] = i + 1;
-  return I;
-}
-
-Csr Csr::from_triplets(int rows, int cols, std::vector<Triplet> t) {
-  for (const Triplet& e : t)
-    need(e.row >= 0 && e.row < rows && e.col >= 0 && e.col < cols, "from_triplets: entry out of range");
-  std::stable_sort(t.begin(), t.end(), [](const Triplet& a, const Triplet& b) {
-    return a.row != b.row ? a.row < b.row : a.col < b.col;
-  });
-  Csr A(rows, cols);
-  A.ci.reserve(t.size());
-  A.v.reserve(t.size());
-  size_t i = 0;
-  for (int r = 0; r < rows; ++r) {
-    while (i < t.size() && t[i].row == r) {
-      const int c = t[i].col;
-      double s = 0.0;
-      for (; i < t.size() && t[i].row == r && t[i].col == c; ++i) s += t[i].value;
-      A.ci.push_back(c);
-      A.v.push_back(s);
-    }
-    A.rp[r + 1] = int64_t(A.ci.size());
-  }
-  return A;
-}
-
-std::vector<double> Csr::to_dense() const {
-  std::vector<double> D(static_cast<size_t>(n_rows) * n_cols, 0.0);
-  for (int i = 0; i < n_rows; ++i)
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) D[size_t(i) * n_cols + ci[k]] = v[k];
-  return D;
-}
-
 std::vector<double> spmv(const Csr& A, std::span<const double> x) {
   need(int64_t(x.size()) == A.n_cols, "spmv: dimension mismatch");
   std::vector<double> y(static_cast<size_t>(A.n_rows));

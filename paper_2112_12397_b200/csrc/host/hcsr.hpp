@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include "wcsr.hpp"
+
 namespace fpb {
 
 class numerical_error : public std::runtime_error {
@@ -21,23 +23,7 @@ class numerical_error : public std::runtime_error {
   explicit numerical_error(const std::string& w) : std::runtime_error(w) {}
 };
 
-// csr.hpp:16-49 with 64-bit row offsets
-struct Csr {
-  int n_rows = 0, n_cols = 0;
-  std::vector<int64_t> rp{0};
-  std::vector<int> ci;
-  std::vector<double> v;
-
-  Csr() = default;
-  Csr(int r, int c) : n_rows(r), n_cols(c), rp(static_cast<size_t>(r) + 1, 0) {}
-  int64_t nnz() const { return int64_t(ci.size()); }
-  int row_len(int i) const { return int(rp[i + 1] - rp[i]); }
-
-  struct Triplet { int row, col; double value; };
-  static Csr identity(int n);
-  static Csr from_triplets(int rows, int cols, std::vector<Triplet> t);  // stable (row,col) order
-  std::vector<double> to_dense() const;  // row-major, small matrices only
-};
+// Csr (csr.hpp:16-49 with 64-bit row offsets) is shared with the workload generator: wcsr.hpp
 
 std::vector<double> spmv(const Csr& A, std::span<const double> x);
 Csr transpose(const Csr& A);

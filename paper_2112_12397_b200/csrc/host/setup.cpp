@@ -395,22 +395,6 @@ std::vector<std::vector<double>> rigid_body_modes(const std::vector<std::array<d
   return m;
 }
 
-void HostSystem::check_shapes() const {
-  auto expect = [](const Csr& M, int r, int c, const char* name) {
-    if (M.n_rows != r || M.n_cols != c)
-      throw std::invalid_argument(std::string("BlockSystem: bad shape for block ") + name);
-  };
-  expect(A, n_u, n_u, "A");
-  expect(C1, n_u, n_t, "C1");
-  expect(Q1, n_u, n_p, "Q1");
-  expect(C2, n_t, n_u, "C2");
-  expect(H, n_t, n_t, "H");
-  expect(Q2, n_p, n_u, "Q2");
-  expect(T, n_p, n_p, "T");
-  if (F_u.n_rows > 0) expect(F_u, n_p, n_u, "F_u");
-  if (n_t != 3 * n_p) throw std::invalid_argument("BlockSystem: n_t must equal 3*n_p");
-}
-
 std::vector<double> fixed_stress_diag(const Csr& Q2, const Csr& S1, const Csr& Q1) {
   if (Q1.n_cols != Q2.n_rows || Q1.n_rows != Q2.n_cols || S1.n_rows != Q1.n_rows || S1.n_rows != S1.n_cols)
     throw std::invalid_argument("fixed_stress_diag: inconsistent shapes");

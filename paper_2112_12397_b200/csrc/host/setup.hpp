@@ -67,11 +67,7 @@ HostAmg amg_setup(Csr A, const std::vector<std::vector<double>>& near_null, cons
 std::vector<std::vector<double>> rigid_body_modes(const std::vector<std::array<double, 3>>& coords);
 int qr_colpiv(int m, int k, const std::vector<double>& B_colmajor, std::vector<double>& Q, std::vector<double>& Rp);
 
-struct HostSystem {
-  int n_u = 0, n_t = 0, n_p = 0;
-  Csr A, C1, Q1, C2, H, Q2, T, F_u;
-  void check_shapes() const;
-};
+// HostSystem (block.hpp:36-45) is shared with the workload generator: wcsr.hpp
 
 enum Variant { kTpu = 0, kTup = 1, kTupStar = 2 };
 

@@ -8,7 +8,7 @@
 #include <vector>
 
 #include "fracprec_b200.hpp"
-#include "fracprec_b200_workload.h"
+#include "fracprec_workload.h"
 
 int main() {
   using namespace fracprec_b200;

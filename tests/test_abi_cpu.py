@@ -17,22 +17,31 @@ from paper_2112_12397_b200 import api
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    names = set()
-    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
-        txt = open(h).read()
-        names |= set(re.findall(r"^[A-Za-z_][\w \*]*?\b(fp_\w+)\s*\(", txt, flags=re.M))
-    return names
+def declared_symbols(header: str):
+    txt = open(os.path.join(ROOT, "include", header)).read()
+    return set(re.findall(r"^[A-Za-z_][\w \*]*?\b(fp_\w+)\s*\(", txt, flags=re.M))
 
 
 def test_library_exports_every_declared_symbol():
-    names = declared_symbols()
+    """include/fracprec_b200.h -> libfracprec_b200.so; include/fracprec_workload.h -> the generator's
+    libfp_workload.so, which does not pull in the solve library."""
+    from workload import gen
+
+    names = declared_symbols("fracprec_b200.h")
     assert len(names) >= 25
     lib = C.CDLL(N.LIB_PATH)
     missing = [n for n in sorted(names) if not hasattr(lib, n)]
     assert not missing, missing
     assert set(N.SIGNATURES) == names, set(N.SIGNATURES) ^ names
     assert b"sm_100a" in N.lib.fp_version()
+    wnames = declared_symbols("fracprec_workload.h")
+    assert set(gen.SIGNATURES) == wnames, set(gen.SIGNATURES) ^ wnames
+    wl = C.CDLL(gen.LIB_PATH)
+    assert not [n for n in sorted(wnames) if not hasattr(wl, n)]
+    import subprocess
+
+    r = subprocess.run(["ldd", gen.LIB_PATH], capture_output=True, text=True)
+    assert "fracprec_b200" not in r.stdout and "libcuda" not in r.stdout, r.stdout
 
 
 def test_shared_library_is_sm100a_only():

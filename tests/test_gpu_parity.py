@@ -197,7 +197,7 @@ def test_gmres_matches_oracle(variant, restart, factor_solve, orth):
 @pytest.mark.parametrize("orth", ["mgs", "cgs"])
 def test_gmres_mid_cycle_checks_with_speculative_steps(orth):
     """A cycle longer than 50 steps runs the reference's every-50 true-residual check
-    (gmres.cpp:194-203) mid-cycle; the device enqueues the next Arnoldi step before the
+    (gmres.cpp:157-166) mid-cycle; the device enqueues the next Arnoldi step before the
     host reads the current one's status, so this exercises the restage after an
     assemble with a step already in flight, and the discarded step at convergence."""
     J = small_workload(seed=23, cells=(8, 8, 6))

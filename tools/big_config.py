@@ -6,6 +6,7 @@ setup phases, host peak RSS, the apply profile and a short GMRES(50) run.
 The GMRES run is timed with classical (cgs) and modified (mgs) Gram-Schmidt.
 """
 import json
+import os
 import resource
 import sys
 import time
@@ -19,7 +20,8 @@ from paper_2112_12397_b200 import api  # noqa: E402
 cfg = int(sys.argv[1])
 its = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 row_sum = sys.argv[3] if len(sys.argv) > 3 else "strided"
-hbm = 6548.8
+_peaks = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+hbm = json.load(open(_peaks))["hbm_gbs"] if os.path.exists(_peaks) else 6650.0  # else B200_PROFILING.md fallback
 
 
 def rss_gb():

@@ -16,7 +16,6 @@
 #include <string>
 #include <vector>
 
-#include "hcsr.hpp"
 #include "workload.hpp"
 
 namespace fpb {

@@ -87,7 +87,7 @@ Mesh build_mesh(const WorkloadSpec& s) {
                                      node_id(i, j + 1, k),     node_id(i, j, k + 1),     node_id(i + 1, j, k + 1),
                                      node_id(i + 1, j + 1, k + 1), node_id(i, j + 1, k + 1)};
 
-  for (const FractureSpec& f : s.fractures) {  // mesh.cpp:175-277
+  for (const FractureSpec& f : s.fractures) {  // mesh.cpp:77-179
     const int a = f.normal_axis, b = (a + 1) % 3, c = (a + 2) % 3;
     const int ia = tick_of(f.coord, s.length[a], m.nc[a], "fracture plane");
     if (ia == 0 || ia == m.nc[a]) throw std::invalid_argument("build_mesh: fracture plane on the boundary");
@@ -588,7 +588,7 @@ Workload generate_workload(const WorkloadSpec& s) {
   J.H = Csr::from_triplets(n_t, n_t, std::move(h));
   J.T = Csr::from_triplets(n_p, n_p, std::move(t));
   J.F_u = Csr::from_triplets(n_p, n_u, std::move(fu));
-  J.Q2 = add_scaled(Csr::from_triplets(n_p, n_u, std::move(q2gap)), J.F_u, 1.0, 1.0);
+  J.Q2 = csr_add(Csr::from_triplets(n_p, n_u, std::move(q2gap)), J.F_u, 1.0, 1.0);
   J.check_shapes();
   return W;
 }

@@ -11,7 +11,7 @@
 #include <string>
 #include <vector>
 
-#include "setup.hpp"
+#include "wcsr.hpp"
 
 namespace fpb {
 
@@ -56,3 +56,8 @@ WorkloadSpec preset_config(int config_id, uint64_t seed);  // BASELINE.json conf
 Workload generate_workload(const WorkloadSpec& spec);
 
 }  // namespace fpb
+
+// the C ABI's opaque workload handle (include/fracprec_workload.h), shared with the solve library
+struct fp_workload {
+  fpb::Workload w;
+};
