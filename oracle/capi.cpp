@@ -7,6 +7,7 @@
 #include <string>
 
 #include "fpo.hpp"
+#include "par.hpp"
 
 using namespace fpo;
 
@@ -93,6 +94,10 @@ AmgConfig amg_cfg(const double* d, const int* i) {
 extern "C" {
 
 const char* or_last_error() { return g_err.c_str(); }
+
+// threads of the oracle's row / block / aggregate loops (par.hpp: results do not depend on it)
+void or_set_threads(int n) { fpo::set_threads(n); }
+int or_threads() { return fpo::threads(); }
 
 // ------------------------------------------------------------------ systems
 // blocks: 8 CSR views in the order A, C1, Q1, C2, H, Q2, T, F_u (F_u may be empty)

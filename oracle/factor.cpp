@@ -19,6 +19,7 @@
 #include <limits>
 
 #include "fpo.hpp"
+#include "par.hpp"
 
 namespace fpo {
 
@@ -134,7 +135,11 @@ void BandFactor::factor(const CsrMatrix& A, Kind k) {
     Lr.assign(static_cast<size_t>(n) * std::max(kl, 1), 0.0);
     diag.assign(static_cast<size_t>(n), 0.0);
     piv.clear();
-    for (size_t blk = 0; blk + 1 < block_start.size(); ++blk) {
+    LoopError err;
+    const long nblk = long(block_start.size()) - 1;
+#pragma omp parallel for num_threads(threads()) schedule(dynamic)
+    for (long blk = 0; blk < nblk; ++blk) {
+     try {
       const int b0 = block_start[blk], b1 = block_start[blk + 1], nb = b1 - b0;
       Band L(nb, kl, 0);  // lower triangle of A (symmetric input: use the lower part)
       for (int i = b0; i < b1; ++i)
@@ -168,7 +173,11 @@ void BandFactor::factor(const CsrMatrix& A, Kind k) {
           Lr[size_t(b0 + j) * kl + r] = c >= 0 ? L.at(j, c) : 0.0;
         }
       }
+     } catch (...) {
+      err.capture(blk);
+     }
     }
+    err.rethrow();
     return;
   }
   // general: banded LU with partial pivoting (row interchanges within the band)
@@ -179,7 +188,11 @@ void BandFactor::factor(const CsrMatrix& A, Kind k) {
   diag.assign(static_cast<size_t>(n), 0.0);
   piv.assign(static_cast<size_t>(n), 0);
   Lr.clear();
-  for (size_t blk = 0; blk + 1 < block_start.size(); ++blk) {
+  LoopError err;
+  const long nblk = long(block_start.size()) - 1;
+#pragma omp parallel for num_threads(threads()) schedule(dynamic)
+  for (long blk = 0; blk < nblk; ++blk) {
+   try {
     const int b0 = block_start[blk], b1 = block_start[blk + 1], nb = b1 - b0;
     Band W(nb, kl, ku);
     for (int i = b0; i < b1; ++i)
@@ -218,7 +231,11 @@ void BandFactor::factor(const CsrMatrix& A, Kind k) {
         Uc[size_t(b0 + j) * ku + r] = (i >= 0 && W.in(i, j)) ? W.at(i, j) : 0.0;
       }
     }
+   } catch (...) {
+    err.capture(blk);
+   }
   }
+  err.rethrow();
 }
 
 void BandFactor::solve_block(int blk, double* x) const {
@@ -265,14 +282,18 @@ void BandFactor::build_inverse() {
     inv_off[blk + 1] = inv_off[blk] + nb * nb;
   }
   inv.assign(inv_off.back(), 0.0);
-  std::vector<double> e(static_cast<size_t>(n), 0.0);
   for (int blk = 0; blk < nblk; ++blk) {
     const int b0 = block_start[blk], nb = block_start[blk + 1] - b0;
-    for (int c = 0; c < nb; ++c) {
-      std::fill(e.begin() + b0, e.begin() + b0 + nb, 0.0);
-      e[b0 + c] = 1.0;
-      solve_block(blk, e.data());
-      for (int i = 0; i < nb; ++i) inv[inv_off[blk] + size_t(i) * nb + c] = e[b0 + i];
+#pragma omp parallel num_threads(threads())
+    {
+      std::vector<double> e(static_cast<size_t>(n), 0.0);  // solve_block indexes absolute rows
+#pragma omp for schedule(dynamic, 16)
+      for (int c = 0; c < nb; ++c) {
+        std::fill(e.begin() + b0, e.begin() + b0 + nb, 0.0);
+        e[b0 + c] = 1.0;
+        solve_block(blk, e.data());
+        for (int i = 0; i < nb; ++i) inv[inv_off[blk] + size_t(i) * nb + c] = e[b0 + i];
+      }
     }
   }
 }
@@ -281,6 +302,7 @@ std::vector<double> BandFactor::solve(std::span<const double> b) const {
   if (int(b.size()) != n) throw std::invalid_argument("SparseFactor::solve: dimension mismatch");
   std::vector<double> x(b.begin(), b.end());
   const int nblk = int(block_start.size()) - 1;
+#pragma omp parallel for num_threads(threads()) schedule(dynamic)
   for (int blk = 0; blk < nblk; ++blk) {
     if (inv.empty()) {
       solve_block(blk, x.data());

@@ -30,6 +30,8 @@ def _load():
     P, PP, DP, IP = C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_double), C.POINTER(C.c_int)
     sig = {
         "or_last_error": (C.c_char_p, []),
+        "or_set_threads": (None, [C.c_int]),
+        "or_threads": (C.c_int, []),
         "or_system_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                        C.POINTER(C.c_void_p), IP, IP, PP]),
         "or_system_toy": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint, PP]),
@@ -67,6 +69,20 @@ def _load():
 
 
 lib = _load()
+
+
+def set_threads(n: int) -> None:
+    """Threads of the oracle's independent row / block / aggregate loops (oracle/par.hpp); every
+    result is bitwise independent of it.  Reductions stay sequential."""
+    lib.or_set_threads(int(n))
+
+
+def threads() -> int:
+    return int(lib.or_threads())
+
+
+# the checker runs on every host core; the timed CPU legs of bench.py choose their own count
+set_threads(int(os.environ.get("FRACPREC_ORACLE_THREADS", os.cpu_count() or 1)))
 
 
 def _check(st: int) -> None:
