@@ -193,6 +193,11 @@ int fp_host_precond_vector(const fp_host_precond* p, int32_t what, int32_t level
 typedef struct fp_workload fp_workload;
 int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config* cfg, fp_host_precond** out);
 
+/* Upload-time choices of a host-built preconditioner (they change no host data): the coarse
+ * row-sum order (FP_ROW_SUM_*) and the factor application (FP_FACTOR_*) the next
+ * fp_precond_create uses.  One host setup can so be uploaded in every mode. */
+int fp_host_precond_set_upload(fp_host_precond* p, int32_t row_sum, int32_t factor_solve);
+
 /* ---- upload to the device */
 int fp_precond_create(fp_system* s, const fp_host_precond* hp, fp_precond** out);
 int fp_precond_upload(fp_system* s, const fp_precond_desc* desc, fp_precond** out);

@@ -98,6 +98,8 @@ const char* or_last_error() { return g_err.c_str(); }
 // threads of the oracle's row / block / aggregate loops (par.hpp: results do not depend on it)
 void or_set_threads(int n) { fpo::set_threads(n); }
 int or_threads() { return fpo::threads(); }
+// GMRES dots as fixed-chunk sums (fpo::set_chunked_reductions; off = the reference's single sum)
+void or_set_chunked_reductions(int on) { fpo::set_chunked_reductions(on != 0); }
 
 // ------------------------------------------------------------------ systems
 // blocks: 8 CSR views in the order A, C1, Q1, C2, H, Q2, T, F_u (F_u may be empty)

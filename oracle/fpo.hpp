@@ -181,6 +181,12 @@ std::pair<std::vector<double>, SolveStats> gmres(
     const LinearOperator& op, const LinearOperator* precond, std::span<const double> b,
     double tol, int max_iter = 500, std::vector<std::vector<double>>* basis_out = nullptr);
 
+// OPTION (off by default): GMRES dot products and norms as fixed 32768-entry chunk sums added in
+// chunk order (deterministic, thread-count independent; not the reference's single left-to-right
+// sum).  For the large-config tests and the timed CPU legs of bench.py (gmres.cpp).
+void set_chunked_reductions(bool on);
+bool chunked_reductions();
+
 // GMRES(m): restart wrapper around the reference algorithm.
 //   r = b - op(x); if ||r|| <= tol ||b|| stop; else run gmres() on r with
 //   max_iter = min(m, remaining) and tol' = tol ||b|| / ||r||; x += dx.

@@ -100,6 +100,7 @@ SIGNATURES = {
     "fp_host_precond_matrix": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32), _DP]),
     "fp_host_precond_vector": (C.c_int, [_P, C.c_int32, C.c_int32, _DP, C.POINTER(C.c_int64)]),
+    "fp_host_precond_set_upload": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "fp_precond_create": (C.c_int, [_P, _P, _PP]),
     "fp_precond_upload": (C.c_int, [_P, C.POINTER(FpPrecondDesc), _PP]),
     "fp_precond_destroy": (None, [_P]),

@@ -273,6 +273,13 @@ class HostPreconditioner:
             N.lib.fp_host_precond_destroy(self._h)
             self._h = None
 
+    def set_upload(self, row_sum: str, factor_solve: str = "auto") -> None:
+        """Upload-time choices for the next GpuPreconditioner.from_host: coarse row-sum order
+        ("ordered" | "strided") and factor application ("auto" | "sweep" | "inverse")."""
+        if row_sum not in AmgConfig._ROW_SUMS:
+            raise ValueError(f"unknown row_sum {row_sum!r} (ordered | strided)")
+        N.check(N.lib.fp_host_precond_set_upload(self._h, AmgConfig._ROW_SUMS[row_sum], _factor_mode(factor_solve)))
+
     def level_sizes(self) -> list:
         nl = C.c_int32()
         N.check(N.lib.fp_host_precond_levels(self._h, C.byref(nl), None))

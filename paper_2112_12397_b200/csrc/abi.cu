@@ -309,6 +309,16 @@ int fp_host_precond_vector(const fp_host_precond* p, int32_t what, int32_t level
 }
 
 // ----------------------------------------------------------------- upload
+int fp_host_precond_set_upload(fp_host_precond* p, int32_t row_sum, int32_t factor_solve) {
+  return guard([&] {
+    need(p != nullptr, "fp_host_precond_set_upload: null handle");
+    need(row_sum == FP_ROW_SUM_ORDERED || row_sum == FP_ROW_SUM_STRIDED, "AmgConfig: unknown row_sum");
+    need(factor_solve >= FP_FACTOR_AUTO && factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
+    p->hp.amg.opt.row_sum = row_sum;
+    p->hp.factor_solve = factor_solve;
+  });
+}
+
 int fp_precond_create(fp_system* s, const fp_host_precond* hp, fp_precond** out) {
   return guard([&] {
     need(s && hp && out, "fp_precond_create: null argument");

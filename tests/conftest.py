@@ -13,9 +13,12 @@ for p in (ROOT, HERE):
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); runs the sm_100a path")
     config.addinivalue_line("markers", "slow: long-running (large workloads)")
+    config.addinivalue_line("markers", "large: BASELINE configs 3-5 at full size (run first)")
 
 
 def pytest_collection_modifyitems(config, items):
+    # the large-config parity tests run first, so that -x cannot hide them behind another failure
+    items.sort(key=lambda it: 0 if "large" in it.keywords else 1)
     try:
         import torch
 

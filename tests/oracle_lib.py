@@ -32,6 +32,7 @@ def _load():
         "or_last_error": (C.c_char_p, []),
         "or_set_threads": (None, [C.c_int]),
         "or_threads": (C.c_int, []),
+        "or_set_chunked_reductions": (None, [C.c_int]),
         "or_system_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
                                        C.POINTER(C.c_void_p), IP, IP, PP]),
         "or_system_toy": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint, PP]),
@@ -79,6 +80,12 @@ def set_threads(n: int) -> None:
 
 def threads() -> int:
     return int(lib.or_threads())
+
+
+def set_chunked_reductions(on: bool) -> None:
+    """GMRES dots / norms as fixed 32768-entry chunk sums (threaded, deterministic) instead of the
+    reference's single left-to-right sum: a different rounding of the same algorithm."""
+    lib.or_set_chunked_reductions(int(bool(on)))
 
 
 # the checker runs on every host core; the timed CPU legs of bench.py choose their own count

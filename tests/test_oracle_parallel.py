@@ -84,3 +84,20 @@ def test_threaded_transpose_and_factor_inverse(config1):
         z8 = pc8.apply(x)
     assert np.array_equal(y1, y8)
     assert np.array_equal(z1, z8)
+
+
+def test_chunked_reductions_stay_within_the_reference_bars(config1):
+    """The chunk-sum dot option (large-config tests, bench CPU legs) is a rounding change only."""
+    S, osys = config1
+    pc = build(osys, S, "tup", 8)
+    b = np.random.default_rng(42).uniform(-1, 1, osys.n)
+    with threads(8):
+        x1, st1 = O.oracle_gmres(osys, pc, b, tol=1e-10, restart=50, max_iter=500, scaled=True)
+        O.set_chunked_reductions(True)
+        try:
+            x2, st2 = O.oracle_gmres(osys, pc, b, tol=1e-10, restart=50, max_iter=500, scaled=True)
+        finally:
+            O.set_chunked_reductions(False)
+    assert st1["converged"] and st2["converged"]
+    assert abs(st1["iterations"] - st2["iterations"]) <= 2
+    assert np.linalg.norm(x1 - x2) <= 1e-8 * np.linalg.norm(x1)
