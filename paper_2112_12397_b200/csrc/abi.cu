@@ -4,6 +4,7 @@
 // reference; fracprec.cpp:453-465 maps them to CLI exit codes the same way).
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -84,6 +85,85 @@ fpb::HostSystem to_system(const fp_block_system& J) {
   return H;
 }
 
+// The C ABI's CSR views validated in place (row-parallel) and borrowed for an upload: no copy of
+// the entries (config 5's A alone is 25 GB).  32-bit row offsets are widened into `hold`.
+struct ViewHold {
+  std::vector<std::vector<int64_t>> widened;
+};
+
+fpd::HostCsrView checked_view(const fp_csr& m, const char* name, ViewHold& hold) {
+  const std::string nm(name);
+  need(m.n_rows >= 0 && m.n_cols >= 0, (nm + ": negative dimension").c_str());
+  fpd::HostCsrView v;
+  v.n_rows = m.n_rows, v.n_cols = m.n_cols;
+  if (m.n_rows == 0) {
+    hold.widened.emplace_back(1, 0);
+    v.rp = hold.widened.back().data();
+    return v;
+  }
+  need((m.row_offsets32 != nullptr) != (m.row_offsets64 != nullptr),
+       (nm + ": exactly one of row_offsets32 / row_offsets64 must be set").c_str());
+  if (m.row_offsets32) {
+    hold.widened.emplace_back(m.row_offsets32, m.row_offsets32 + m.n_rows + 1);
+    v.rp = hold.widened.back().data();
+  } else {
+    v.rp = m.row_offsets64;
+  }
+  need(v.rp[0] == 0, (nm + ": row_offsets[0] != 0").c_str());
+  need(v.rp[m.n_rows] == 0 || (m.col_indices && m.values), (nm + ": null column/value array").c_str());
+  v.ci = m.col_indices, v.v = m.values;
+  int bad = 0;  // 1 monotone, 2 range, 3 order: the first failing row reports, like the sequential check
+  long first = LONG_MAX;
+#pragma omp parallel for schedule(static) reduction(min : first)
+  for (long i = 0; i < m.n_rows; ++i) {
+    int why = 0;
+    if (v.rp[i] > v.rp[i + 1]) why = 1;
+    for (int64_t k = v.rp[i]; k < v.rp[i + 1] && !why; ++k) {
+      if (v.ci[k] < 0 || v.ci[k] >= m.n_cols) why = 2;
+      else if (k > v.rp[i] && v.ci[k - 1] >= v.ci[k]) why = 3;
+    }
+    if (why && i < first) first = i;
+  }
+  if (first != LONG_MAX) {
+    const long i = first;
+    bad = v.rp[i] > v.rp[i + 1] ? 1 : 0;
+    for (int64_t k = v.rp[i]; k < v.rp[i + 1] && !bad; ++k)
+      bad = (v.ci[k] < 0 || v.ci[k] >= m.n_cols) ? 2 : (k > v.rp[i] && v.ci[k - 1] >= v.ci[k]) ? 3 : 0;
+  }
+  need(bad != 1, (nm + ": row_offsets not monotone").c_str());
+  need(bad != 2, (nm + ": column out of range").c_str());
+  need(bad != 3, (nm + ": columns not strictly increasing within a row").c_str());
+  return v;
+}
+
+fpd::SystemView checked_system(const fp_block_system& J, ViewHold& hold) {
+  hold.widened.reserve(8);
+  fpd::SystemView S;
+  S.n_u = J.n_u, S.n_t = J.n_t, S.n_p = J.n_p;
+  S.A = checked_view(J.A, "A", hold);
+  S.C1 = checked_view(J.C1, "C1", hold);
+  S.Q1 = checked_view(J.Q1, "Q1", hold);
+  S.C2 = checked_view(J.C2, "C2", hold);
+  S.H = checked_view(J.H, "H", hold);
+  S.Q2 = checked_view(J.Q2, "Q2", hold);
+  S.T = checked_view(J.T, "T", hold);
+  S.F_u = checked_view(J.F_u, "F_u", hold);
+  auto expect = [](const fpd::HostCsrView& M, int r, int c, const char* name) {
+    if (M.n_rows != r || M.n_cols != c)
+      throw std::invalid_argument(std::string("BlockSystem: bad shape for block ") + name);
+  };
+  expect(S.A, S.n_u, S.n_u, "A");
+  expect(S.C1, S.n_u, S.n_t, "C1");
+  expect(S.Q1, S.n_u, S.n_p, "Q1");
+  expect(S.C2, S.n_t, S.n_u, "C2");
+  expect(S.H, S.n_t, S.n_t, "H");
+  expect(S.Q2, S.n_p, S.n_u, "Q2");
+  expect(S.T, S.n_p, S.n_p, "T");
+  if (S.F_u.n_rows > 0) expect(S.F_u, S.n_p, S.n_u, "F_u");
+  if (S.n_t != 3 * S.n_p) throw std::invalid_argument("BlockSystem: n_t must equal 3*n_p");
+  return S;
+}
+
 fpb::AmgOptions to_amg(const fp_amg_config& c) {
   fpb::AmgOptions o;
   o.strength_threshold = c.strength_threshold;
@@ -145,15 +225,39 @@ namespace {
 // hierarchy still built on the host that is transfer-bound, so the
 // default is the host; FRACPREC_B200_DEVICE_SETUP=1 or fp_set_setup_backend(1) selects
 // the device.  The environment is read on first use, not at load.
+// Where build_tpu / build_tup run: 1 = the device-resident setup (dsetup.cu: fine-size products,
+// strength graph and Galerkin products in HBM; the default when a CUDA device is present), 0 = the
+// host setup (setup.cpp, OpenMP; the default without a device, or FRACPREC_B200_SETUP=host).
+int g_setup_device = -1;
 void ensure_setup_backend() {
-  static const bool once = [] {
-    int n = 0;
-    if (std::getenv("FRACPREC_B200_DEVICE_SETUP") != nullptr && cudaGetDeviceCount(&n) == cudaSuccess && n > 0)
-      fpb::set_spgemm_backend(&fpd::spgemm_device);
-    cudaGetLastError();
-    return true;
-  }();
-  (void)once;
+  if (g_setup_device >= 0) return;
+  int n = 0;
+  const bool has = cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+  cudaGetLastError();
+  const char* e = std::getenv("FRACPREC_B200_SETUP");
+  g_setup_device = has && !(e && std::strcmp(e, "host") == 0) ? 1 : 0;
+}
+
+fpb::HostPrecond build_any(const fpd::SystemView& V, const fpb::HostSystem* H, int variant, const fpb::AmgOptions& o,
+                           const std::vector<std::array<double, 3>>& xyz) {
+  ensure_setup_backend();
+  if (g_setup_device) return fpd::build_precond_device(V, H, variant, o, xyz);
+  if (H) return fpb::build_precond(*H, variant, o, xyz);
+  ViewHold none;
+  (void)none;
+  fpb::HostSystem copy;  // the host setup works on owned CSR
+  auto own = [](const fpd::HostCsrView& m) {
+    fpb::Csr A(m.n_rows, m.n_cols);
+    if (m.n_rows == 0) return A;
+    A.rp.assign(m.rp, m.rp + m.n_rows + 1);
+    A.ci.assign(m.ci, m.ci + m.nnz());
+    A.v.assign(m.v, m.v + m.nnz());
+    return A;
+  };
+  copy.n_u = V.n_u, copy.n_t = V.n_t, copy.n_p = V.n_p;
+  copy.A = own(V.A), copy.C1 = own(V.C1), copy.Q1 = own(V.Q1), copy.C2 = own(V.C2);
+  copy.H = own(V.H), copy.Q2 = own(V.Q2), copy.T = own(V.T), copy.F_u = own(V.F_u);
+  return fpb::build_precond(copy, variant, o, xyz);
 }
 }  // namespace
 
@@ -188,10 +292,11 @@ void fp_amg_config_default(fp_amg_config* c) {
 int fp_system_create(const fp_block_system* J, fp_system** out) {
   return guard([&] {
     need(J && out, "fp_system_create: null argument");
-    const fpb::HostSystem H = to_system(*J);
+    ViewHold hold;
+    const fpd::SystemView V = checked_system(*J, hold);
     auto s = std::make_unique<fp_system>();
     fpd::cuda_check(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking), "cudaStreamCreate");
-    s->dev = std::make_unique<fpd::DeviceSystem>(H);
+    s->dev = std::make_unique<fpd::DeviceSystem>(V);
     const int n = s->dev->n();
     s->xin.alloc(n), s->yout.alloc(n);
     *out = s.release();
@@ -241,12 +346,13 @@ int fp_host_precond_build(const fp_block_system* J, const fp_precond_config* cfg
     ensure_setup_backend();
     need(J && cfg && out, "fp_host_precond_build: null argument");
     need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
-    const fpb::HostSystem H = to_system(*J);
+    ViewHold hold;
+    const fpd::SystemView V = checked_system(*J, hold);
     std::vector<std::array<double, 3>> xyz;
     if (coords)
       for (int v = 0; v < n_nodes; ++v) xyz.push_back({coords[3 * v], coords[3 * v + 1], coords[3 * v + 2]});
     auto p = std::make_unique<fp_host_precond>();
-    p->hp = fpb::build_precond(H, cfg->variant, to_amg(cfg->amg), xyz);
+    p->hp = build_any(V, nullptr, cfg->variant, to_amg(cfg->amg), xyz);
     p->hp.factor_solve = cfg->factor_solve;
     *out = p.release();
   });
@@ -270,16 +376,27 @@ int fp_host_precond_matrix(const fp_host_precond* p, int32_t what, int32_t level
     need(p, "null handle");
     const auto& L = p->hp.amg.levels;
     const fpb::Csr* M = nullptr;
+    const fpb::DeviceMatrix* dm = nullptr;  // a device-resident level (device setup)
+    int64_t count = -1;
     if (what == 2)
       M = p->hp.variant == fpb::kTpu ? nullptr : &p->hp.S2;
     else {
       need(level >= 0 && level < int(L.size()), "level out of range");
       M = what == 0 ? &L[level].A : &L[level].P;
+      dm = what == 0 ? L[level].dA.get() : L[level].dP.get();
+      count = what == 0 ? L[level].a_nnz() : L[level].p_nnz();
     }
     need(M != nullptr, "matrix not available for this variant (T is part of the system)");
     if (n_rows) *n_rows = M->n_rows;
     if (n_cols) *n_cols = M->n_cols;
-    if (nnz) *nnz = M->nnz();
+    if (nnz) *nnz = count >= 0 ? count : M->nnz();
+    if (dm && (rp || ci || v)) {
+      const fpb::Csr H = fpd::download_csr(dm->m);
+      if (rp) std::memcpy(rp, H.rp.data(), sizeof(int64_t) * H.rp.size());
+      if (ci) std::memcpy(ci, H.ci.data(), sizeof(int32_t) * H.ci.size());
+      if (v) std::memcpy(v, H.v.data(), sizeof(double) * H.v.size());
+      return;
+    }
     if (rp) std::memcpy(rp, M->rp.data(), sizeof(int64_t) * M->rp.size());
     if (ci) std::memcpy(ci, M->ci.data(), sizeof(int32_t) * M->ci.size());
     if (v) std::memcpy(v, M->v.data(), sizeof(double) * M->v.size());
@@ -514,7 +631,7 @@ int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config
     need(w && cfg && out, "fp_workload_host_precond_build: null argument");
     need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
     auto p = std::make_unique<fp_host_precond>();
-    p->hp = fpb::build_precond(w->w.J, cfg->variant, to_amg(cfg->amg), w->w.coords);
+    p->hp = build_any(fpd::SystemView::of(w->w.J), &w->w.J, cfg->variant, to_amg(cfg->amg), w->w.coords);
     p->hp.factor_solve = cfg->factor_solve;
     *out = p.release();
   });
@@ -524,14 +641,14 @@ int fp_set_setup_backend(int32_t device) {
   return guard([&] {
     ensure_setup_backend();
     if (!device) {
-      fpb::set_spgemm_backend(nullptr);
+      g_setup_device = 0;
       return;
     }
     int n = 0;
     const bool has = cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
     cudaGetLastError();
     need(has, "fp_set_setup_backend: no CUDA device");
-    fpb::set_spgemm_backend(&fpd::spgemm_device);
+    g_setup_device = 1;
   });
 }
 
@@ -539,7 +656,7 @@ int fp_setup_backend(int32_t* device) {
   return guard([&] {
     need(device, "null argument");
     ensure_setup_backend();
-    *device = fpb::spgemm_backend_active() ? 1 : 0;
+    *device = g_setup_device;
   });
 }
 

@@ -23,6 +23,11 @@
 
 namespace fpd {
 
+// layout constants shared by the builders (formats.cu) and the kernels (kernels.cuh)
+constexpr int kSlice = 32;                        // rows (block rows, nodes) per SELL slice
+constexpr int kPipeRows = 32, kPipeW = 32;        // windowed pipeline: rows per slice, entries per window row
+constexpr int kPipeCtasPerSm = 2;                 // two resident pipelines per SM (registers capped at 128)
+
 struct SellView {
   int n_rows = 0;
   const long long* slice_off = nullptr;  // slot index of (slice, k=0, lane=0)

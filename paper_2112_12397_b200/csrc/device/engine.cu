@@ -168,255 +168,77 @@ void launch_level(const DeviceLevel& L, const G& g, const E& e, cudaStream_t s) 
 
 // Few or long rows (coarse levels, R = P^T) stream best one warp per row;
 // many short rows one thread per row in SELL-32 slices.
+// The layouts are built on the device from CSR in HBM (formats.cu); these wrappers upload a host
+// CSR first.
 DMat make_mat(const fpb::Csr& A, bool few_rows_parallel, bool strided) {
-  DMat M;
-  if (strided) {  // row_sum = strided32: plain CSR, one warp per row (or window-staged CTAs of R rows)
-    M.warp = M.strided = true;
-    M.strided_rows = 1;  // one row per CTA: most parallel loads for few-row operators
-    M.csr.n_rows = A.n_rows, M.csr.n_cols = A.n_cols, M.csr.nnz = A.nnz();
-    std::vector<long long> rp(A.rp.begin(), A.rp.end());
-    M.csr.rp.upload(rp);
-    M.csr.ci.upload(A.ci);
-    M.csr.v.upload(A.v);
-    return M;
-  }
-  const double avg = A.n_rows > 0 ? double(A.nnz()) / A.n_rows : 0.0;
-  // SELL's thread-per-row chains need enough rows to hide latency; below ~64k
-  // rows the slice kernel's parallel loads win even for short rows
-  M.warp = A.n_rows > 0 && (avg >= 48.0 || (A.n_rows < 65536 && avg >= 8.0) ||
-                            (few_rows_parallel && A.n_rows < 2048 && avg >= 2.0));
-  if (!M.warp) {
-    M.sell = make_sell(A);
-    return M;
-  }
-  M.slice_rows = A.n_rows >= 2048 ? 32 : 8;
-  if (M.slice_rows == 32) {
-    M.pipe = true;
-    M.pm = make_pipe(A);
-    return M;
-  }
-  M.csr.n_rows = A.n_rows, M.csr.n_cols = A.n_cols, M.csr.nnz = A.nnz();
-  std::vector<long long> rp(A.rp.begin(), A.rp.end());
-  M.csr.rp.upload(rp);
-  M.csr.ci.upload(A.ci);
-  M.csr.v.upload(A.v);
-  return M;
+  return mat_from(upload_csr(A), few_rows_parallel, strided, 0);
 }
-
-// ------------------------------------------------------------ format upload
-DPipe make_pipe(const fpb::Csr& A) {
-  constexpr int kSigma = 4096;  // rows are sorted by length only inside chunks (locality of the gathers)
-  DPipe D;
-  D.n_rows = A.n_rows, D.nnz = A.nnz();
-  D.n_slices = (A.n_rows + kPipeRows - 1) / kPipeRows;
-  std::vector<int> perm(static_cast<size_t>(D.n_slices) * kPipeRows, -1);
-  for (int i = 0; i < A.n_rows; ++i) perm[i] = i;
-  for (int c0 = 0; c0 < A.n_rows; c0 += kSigma) {
-    const int c1 = std::min(A.n_rows, c0 + kSigma);
-    std::stable_sort(perm.begin() + c0, perm.begin() + c1,
-                     [&](int a, int b) { return A.row_len(a) > A.row_len(b); });
-  }
-  std::vector<int> len(perm.size(), 0);
-  std::vector<long long> woff(static_cast<size_t>(D.n_slices) + 1, 0);
-  for (int s = 0; s < D.n_slices; ++s) {
-    int mx = 0;
-    for (int r = 0; r < kPipeRows; ++r) {
-      const int i = perm[size_t(s) * kPipeRows + r];
-      len[size_t(s) * kPipeRows + r] = i >= 0 ? A.row_len(i) : 0;
-      mx = std::max(mx, len[size_t(s) * kPipeRows + r]);
-    }
-    woff[s + 1] = woff[s] + (mx + kPipeW - 1) / kPipeW;
-  }
-  constexpr int64_t kWin = int64_t(kPipeRows) * kPipeW;
-  D.slots = woff.back() * kWin;
-  std::vector<double> v(static_cast<size_t>(D.slots), 0.0);
-  std::vector<int> ci(static_cast<size_t>(D.slots), 0);
-#pragma omp parallel for schedule(dynamic, 64)
-  for (int s = 0; s < D.n_slices; ++s)
-    for (int r = 0; r < kPipeRows; ++r) {
-      const int i = perm[size_t(s) * kPipeRows + r];
-      if (i < 0) continue;
-      const int64_t b = A.rp[i];
-      for (int k = 0; k < A.row_len(i); ++k) {
-        const int64_t idx = (woff[s] + k / kPipeW) * kWin + int64_t(r) * kPipeW + k % kPipeW;
-        v[size_t(idx)] = A.v[size_t(b + k)];
-        ci[size_t(idx)] = A.ci[size_t(b + k)];
-      }
-    }
-  // persistent CTAs (one per SM) over contiguous slice ranges of equal window count
-  int dev = 0, sms = 148;
-  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
-  D.n_ctas = std::max(1, std::min(D.n_slices, sms * kPipeCtasPerSm));
-  std::vector<int> cs(static_cast<size_t>(D.n_ctas) + 1, D.n_slices);
-  cs[0] = 0;
-  const long long tot = woff.back();
-  for (int b = 1; b < D.n_ctas; ++b) {
-    const long long target = (tot * b + D.n_ctas - 1) / D.n_ctas;
-    cs[b] = int(std::lower_bound(woff.begin(), woff.end() - 1, target) - woff.begin());
-    cs[b] = std::max(cs[b], cs[b - 1]);
-  }
-  D.cta_slice.upload(cs);
-  D.woff.upload(woff);
-  D.row.upload(perm);
-  D.len.upload(len);
-  D.v.upload(v);
-  D.ci.upload(ci);
-  return D;
-}
-
-DSell make_sell(const fpb::Csr& A) {
-  DSell D;
-  D.n_rows = A.n_rows, D.n_cols = A.n_cols, D.nnz = A.nnz();
-  D.n_slices = (A.n_rows + kSlice - 1) / kSlice;
-  std::vector<long long> off(static_cast<size_t>(D.n_slices) + 1, 0);
-  std::vector<int> len(static_cast<size_t>(A.n_rows));
-  for (int i = 0; i < A.n_rows; ++i) len[i] = A.row_len(i);
-  for (int s = 0; s < D.n_slices; ++s) {
-    int mx = 0;
-    for (int i = s * kSlice; i < std::min(A.n_rows, (s + 1) * kSlice); ++i) mx = std::max(mx, len[i]);
-    off[s + 1] = off[s] + (long long)mx * kSlice;
-  }
-  D.slots = off[D.n_slices];
-  std::vector<int> cols(static_cast<size_t>(D.slots), 0);
-  std::vector<double> vals(static_cast<size_t>(D.slots), 0.0);
-#pragma omp parallel for schedule(static)
-  for (int i = 0; i < A.n_rows; ++i) {
-    const long long base = off[i / kSlice] + (i % kSlice);
-    for (int k = 0; k < len[i]; ++k) {
-      cols[base + (long long)k * kSlice] = A.ci[A.rp[i] + k];
-      vals[base + (long long)k * kSlice] = A.v[A.rp[i] + k];
-    }
-  }
-  D.off.upload(off);
-  D.len.upload(len);
-  D.cols.upload(cols);
-  D.vals.upload(vals);
-  return D;
-}
-
-DBp3 make_bp3(const fpb::Csr& A) {
-  DBp3 D;
-  if (A.n_rows % 3 != 0 || A.n_rows == 0) return D;
-  const int nn = A.n_rows / 3;
-  bool same = true;
-#pragma omp parallel for schedule(static) reduction(&& : same)
-  for (int n = 0; n < nn; ++n) {
-    const long long r0 = A.rp[3 * n], len = A.rp[3 * n + 1] - r0;
-    for (int d = 1; d < 3 && same; ++d) {
-      const long long rd = A.rp[3 * n + d];
-      if (A.rp[3 * n + d + 1] - rd != len || !std::equal(A.ci.begin() + r0, A.ci.begin() + r0 + len, A.ci.begin() + rd))
-        same = false;
-    }
-  }
-  if (!same) return D;
-  D.n_nodes = nn, D.nnz = A.nnz();
-  const int ns = (nn + kSlice - 1) / kSlice;
-  std::vector<long long> off(static_cast<size_t>(ns) + 1, 0);
-  std::vector<int> len(static_cast<size_t>(nn));
-  for (int n = 0; n < nn; ++n) len[n] = A.row_len(3 * n);
-  for (int s = 0; s < ns; ++s) {
-    int mx = 0;
-    for (int n = s * kSlice; n < std::min(nn, (s + 1) * kSlice); ++n) mx = std::max(mx, len[n]);
-    off[s + 1] = off[s] + (long long)mx * kSlice;
-  }
-  D.slots = off[ns];
-  std::vector<int> cols(static_cast<size_t>(D.slots), 0);
-  std::vector<double> vals(static_cast<size_t>(3 * D.slots), 0.0);
-#pragma omp parallel for schedule(static)
-  for (int n = 0; n < nn; ++n) {
-    const long long s0 = off[n / kSlice];
-    const int lane = n % kSlice;
-    for (int k = 0; k < len[n]; ++k) {
-      cols[s0 + (long long)k * kSlice + lane] = A.ci[A.rp[3 * n] + k];
-      for (int d = 0; d < 3; ++d)
-        vals[3 * (s0 + (long long)k * kSlice) + 32 * d + lane] = A.v[A.rp[3 * n + d] + k];
-    }
-  }
-  D.off.upload(off);
-  D.len.upload(len);
-  D.cols.upload(cols);
-  D.vals.upload(vals);
-  return D;
-}
-
-DBsr3 make_bsr3(const fpb::Csr& A, const std::vector<int>* brows) {
-  if (A.n_rows != A.n_cols || A.n_rows % 3 != 0) throw std::invalid_argument("make_bsr3: needs a square matrix with n % 3 == 0");
-  DBsr3 D;
-  const int nb = brows ? int(brows->size()) : A.n_rows / 3;
-  auto src = [&](int b) { return brows ? (*brows)[b] : b; };  // global block row of block row b
-  D.n_brows = nb;
-  D.n_slices = (nb + kSlice - 1) / kSlice;
-  // block columns of each block row: union over its three scalar rows
-  std::vector<std::vector<int>> bc(static_cast<size_t>(nb));
-#pragma omp parallel for schedule(dynamic, 256)
-  for (int b = 0; b < nb; ++b) {
-    auto& L = bc[b];
-    const int g = src(b);
-    for (int li = 0; li < 3; ++li)
-      for (int64_t k = A.rp[3 * g + li]; k < A.rp[3 * g + li + 1]; ++k) L.push_back(A.ci[k] / 3);
-    std::sort(L.begin(), L.end());
-    L.erase(std::unique(L.begin(), L.end()), L.end());
-  }
-  std::vector<long long> off(static_cast<size_t>(D.n_slices) + 1, 0);
-  std::vector<int> len(static_cast<size_t>(nb));
-  for (int b = 0; b < nb; ++b) len[b] = int(bc[b].size()), D.nblocks += len[b];
-  for (int s = 0; s < D.n_slices; ++s) {
-    int mx = 0;
-    for (int b = s * kSlice; b < std::min(nb, (s + 1) * kSlice); ++b) mx = std::max(mx, len[b]);
-    off[s + 1] = off[s] + (long long)mx * kSlice;
-  }
-  D.slots = off[D.n_slices];
-  std::vector<int> bcols(static_cast<size_t>(D.slots), 0);
-  std::vector<double> vals(static_cast<size_t>(D.slots) * 9, 0.0);
-#pragma omp parallel for schedule(dynamic, 256)
-  for (int b = 0; b < nb; ++b) {
-    const int s = b / kSlice, lane = b % kSlice;
-    const auto& L = bc[b];
-    for (int k = 0; k < len[b]; ++k) bcols[off[s] + (long long)k * kSlice + lane] = L[k];
-    const int g = src(b);
-    for (int li = 0; li < 3; ++li) {
-      size_t slot = 0;
-      for (int64_t q = A.rp[3 * g + li]; q < A.rp[3 * g + li + 1]; ++q) {
-        const int c = A.ci[q], cb = c / 3, j = c % 3;
-        while (L[slot] != cb) ++slot;
-        vals[(off[s] + (long long)slot * kSlice) * 9 + (li * 3 + j) * kSlice + lane] = A.v[q];
-      }
-    }
-  }
-  D.off.upload(off);
-  D.len.upload(len);
-  D.bcols.upload(bcols);
-  D.vals.upload(vals);
-  if (brows) D.brow_map.upload(*brows);
-  return D;
-}
+DSell make_sell(const fpb::Csr& A) { return sell_from(upload_csr(A), 0); }
+DBp3 make_bp3(const fpb::Csr& A) { return bp3_from(upload_csr(A), 0); }
+DBsr3 make_bsr3(const fpb::Csr& A, const std::vector<int>* brows) { return bsr3_from(upload_csr(A), brows, 0); }
 
 // ------------------------------------------------------------------ system
-DeviceSystem::DeviceSystem(const fpb::HostSystem& J) {
-  J.check_shapes();
+namespace {
+__global__ void max_abs_diag_kernel(int n, const long long* rp, const int* ci, const double* v,
+                                    unsigned long long* out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double m = 0.0;
+  if (i < n)
+    for (long long k = rp[i]; k < rp[i + 1]; ++k)
+      if (ci[k] == i) m = fabs(v[k]);  // diag_extract: the (last) diagonal entry of the row
+  // non-negative doubles order like their bit patterns: the max is exact and order-independent
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+double max_abs_diag(const DCsr& A) {
+  DevBuf<unsigned long long> out(1);
+  out.zero();
+  if (A.n_rows) max_abs_diag_kernel<<<unsigned((A.n_rows + 255) / 256), 256>>>(A.n_rows, A.rp.get(), A.ci.get(), A.v.get(), out.get());
+  unsigned long long bits = 0;
+  cuda_check(cudaMemcpy(&bits, out.get(), sizeof(bits), cudaMemcpyDeviceToHost), "max diag");
+  double m;
+  std::memcpy(&m, &bits, sizeof(m));
+  return m;
+}
+}  // namespace
+
+DeviceSystem::DeviceSystem(const fpb::HostSystem& J) : DeviceSystem(SystemView::of(J)) {}
+
+DeviceSystem::DeviceSystem(const SystemView& J) {
   cuda_check(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "side stream");
   cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "fork event");
   cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "join event");
   n_u = J.n_u, n_t = J.n_t, n_p = J.n_p;
   a_bsr3 = n_u % 3 == 0;
-  if (a_bsr3)
-    A = make_bsr3(J.A);
-  else
-    A_sell = make_sell(J.A);
-  C1 = make_sell(J.C1);
-  Q1 = make_sell(J.Q1);
-  C2 = make_sell(J.C2);
-  H = make_sell(J.H);
-  Q2 = make_sell(J.Q2);
-  Q2m = make_mat(J.Q2, true);
-  T = make_sell(J.T);
-  auto max_abs_diag = [](const fpb::Csr& M) {
-    double m = 0.0;
-    for (double v : fpb::diag_extract(M)) m = std::max(m, std::abs(v));
-    return m;
-  };
-  const double da = max_abs_diag(J.A), dh = max_abs_diag(J.H), dt = max_abs_diag(J.T);
+  double da = 0.0;
+  {  // A: one raw upload, the BSR3 layout built on the device, the raw copy freed
+    const DCsr dA = upload_csr(J.A);
+    da = max_abs_diag(dA);
+    if (a_bsr3)
+      A = bsr3_from(dA, nullptr, 0);
+    else
+      A_sell = sell_from(dA, 0);
+  }
+  C1 = sell_from(upload_csr(J.C1), 0);
+  Q1 = sell_from(upload_csr(J.Q1), 0);
+  C2 = sell_from(upload_csr(J.C2), 0);
+  double dh = 0.0, dt = 0.0;
+  {
+    const DCsr dH = upload_csr(J.H);
+    dh = max_abs_diag(dH);
+    H = sell_from(dH, 0);
+  }
+  {
+    DCsr dQ2 = upload_csr(J.Q2);
+    Q2 = sell_from(dQ2, 0);
+    Q2m = mat_from(std::move(dQ2), true, false, 0);
+  }
+  {
+    const DCsr dT = upload_csr(J.T);
+    dt = max_abs_diag(dT);
+    T = sell_from(dT, 0);
+  }
   if (da > 0.0 && dh > 0.0) st = std::sqrt(da / dh);
   if (da > 0.0 && dt > 0.0) sp = std::sqrt(da / dt);
 }
@@ -469,6 +291,35 @@ float fine_l2_keep(const DBsr3& A) {
   return float(std::min(1.0, mb * 1048576.0 / bytes));
 }
 
+namespace {
+DCsr clone_csr(const DCsr& A) {
+  DCsr C;
+  C.n_rows = A.n_rows, C.n_cols = A.n_cols, C.nnz = A.nnz;
+  C.rp.alloc(A.rp.size()), C.ci.alloc(A.ci.size()), C.v.alloc(A.v.size());
+  if (A.rp.size()) cuda_check(cudaMemcpy(C.rp.get(), A.rp.get(), A.rp.bytes(), cudaMemcpyDeviceToDevice), "clone");
+  if (A.ci.size()) cuda_check(cudaMemcpy(C.ci.get(), A.ci.get(), A.ci.bytes(), cudaMemcpyDeviceToDevice), "clone");
+  if (A.v.size()) cuda_check(cudaMemcpy(C.v.get(), A.v.get(), A.v.bytes(), cudaMemcpyDeviceToDevice), "clone");
+  return C;
+}
+// the layout of a borrowed device CSR (the layouts that keep a CSR get their own copy)
+DMat mat_from_ref(const DCsr& A, bool few_rows_parallel, bool strided) {
+  const double avg = A.n_rows > 0 ? double(A.nnz) / A.n_rows : 0.0;
+  const bool warp = A.n_rows > 0 && (avg >= 48.0 || (A.n_rows < 65536 && avg >= 8.0) ||
+                                     (few_rows_parallel && A.n_rows < 2048 && avg >= 2.0));
+  if (strided || (warp && A.n_rows < 2048)) return mat_from(clone_csr(A), few_rows_parallel, strided, 0);
+  if (!warp) {
+    DMat M;
+    M.sell = sell_from(A, 0);
+    return M;
+  }
+  DMat M;
+  M.warp = M.pipe = true;
+  M.slice_rows = 32;
+  M.pm = pipe_from(A, 0);
+  return M;
+}
+}  // namespace
+
 DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
   opt = h.opt;
   if (opt.smoother != 0 && opt.smoother != 2)
@@ -477,18 +328,27 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
         "sequential; see DESIGN.md)");
   const int L = int(h.levels.size());
   lv.resize(static_cast<size_t>(L));
+  // build sources: each level's A (l < L - 1) and P (l >= 1) as device CSR — the device setup's own
+  // (HostLevel::dA / dP), else uploaded; kept until release_build_data (the sparse-rhs subsets)
+  src_A_.assign(size_t(L), nullptr), src_P_.assign(size_t(L), nullptr);
+  auto source = [&](const std::shared_ptr<fpb::DeviceMatrix>& dm, const fpb::Csr& host) -> const DCsr* {
+    if (dm) return &dm->m;
+    own_.push_back(upload_csr(host));
+    return &own_.back();
+  };
   for (int l = 0; l < L; ++l) {
     const fpb::HostLevel& H = h.levels[l];
     DeviceLevel& D = lv[l];
     D.n = H.A.n_rows;
     if (l + 1 < L || L == 1) {
       // coarsest level is solved densely; its A is not needed on the device
+      const DCsr& A = *(src_A_[l] = source(H.dA, H.A));
       if (l == 0 && fine_bsr3 && H.A.n_rows % 3 == 0) {
         D.bsr3 = true;
-        D.Ab = make_bsr3(H.A);
+        D.Ab = bsr3_from(A, nullptr, 0);
         D.Ab.l2_keep = fine_l2_keep(D.Ab);
       } else {
-        D.Am = make_mat(H.A, false, l > 0 && opt.row_sum == 1);
+        D.Am = mat_from_ref(A, false, l > 0 && opt.row_sum == 1);
       }
     }
     if (l > 0) {
@@ -499,12 +359,13 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
       // overrides the threshold (read at upload; the tests use it to force the format).
       long long min_nodes = 200000;
       if (const char* e = std::getenv("FRACPREC_B200_BP3_MIN_NODES")) min_nodes = std::atoll(e);
-      if (l == 1 && lv[0].bsr3 && H.P.n_rows >= 3 * min_nodes) {
-        D.P.bp = make_bp3(H.P);
+      const DCsr& P = *(src_P_[l] = source(H.dP, H.P));
+      D.R = mat_from(transpose_dev(P, 0), false, opt.row_sum == 1, 0);
+      if (l == 1 && lv[0].bsr3 && P.n_rows >= 3 * min_nodes) {
+        D.P.bp = bp3_from(P, 0);
         D.P.bp3 = D.P.bp.n_nodes > 0;
       }
-      if (!D.P.bp3) D.P = make_mat(H.P);
-      D.R = make_mat(fpb::transpose(H.P), false, opt.row_sum == 1);
+      if (!D.P.bp3) D.P = mat_from_ref(P, false, false);
     }
     D.d.upload(H.diag);
     D.b.alloc(D.n), D.x.alloc(D.n), D.xt.alloc(D.n), D.xt2.alloc(D.n), D.xt3.alloc(D.n), D.r.alloc(D.n);
@@ -531,27 +392,49 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
   if (opt.cycles_per_apply > 1) top_x.alloc(fine_n()), top_res.alloc(fine_n()), top_dx.alloc(fine_n());
 }
 
-void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows, const fpb::HostAmg& h) {
+namespace {
+// act[i] = f0[i] or f0[j] for some j in row i (the rows whose residual b - A x^ can be nonzero)
+__global__ void act_rows_kernel(int n, const long long* rp, const int* ci, const unsigned char* f0, unsigned char* act) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned char a = f0[i];
+  for (long long k = rp[i]; k < rp[i + 1] && !a; ++k) a = f0[ci[k]];
+  act[i] = a;
+}
+// coarse[c] = 1 for the columns c of P on active rows (the rows of R = P^T that gather one)
+__global__ void coarse_marks_kernel(int n, const long long* rp, const int* ci, const unsigned char* act,
+                                    unsigned char* coarse) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n || !act[i]) return;
+  for (long long k = rp[i]; k < rp[i + 1]; ++k) coarse[ci[k]] = 1;
+}
+std::vector<long long> download_rp(const DCsr& A) {
+  std::vector<long long> rp(size_t(A.n_rows) + 1, 0);
+  if (A.n_rows) cuda_check(cudaMemcpy(rp.data(), A.rp.get(), sizeof(long long) * rp.size(), cudaMemcpyDeviceToHost), "rp");
+  return rp;
+}
+}  // namespace
+
+void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows) {
   sp_ready = false;
   sp_lv.clear();
-  const int L = int(h.levels.size());
-  if (L < 2 || lv.size() != size_t(L) || !lv[0].bsr3) return;
+  const int L = int(lv.size());
+  if (L < 2 || !lv[0].bsr3 || src_A_.size() != size_t(L)) return;
   std::vector<unsigned char> f0 = rhs_rows;  // rows where this level's rhs can be nonzero
   for (int l = 0; l + 1 < L; ++l) {
-    const fpb::Csr& A = h.levels[l].A;
-    const fpb::Csr& P = h.levels[l + 1].P;
+    if (!src_A_[l] || !src_P_[l + 1]) break;
+    const DCsr& A = *src_A_[l];
+    const DCsr& P = *src_P_[l + 1];
     const int n = A.n_rows;
     if (int(f0.size()) != n) break;
-    // rows whose residual b - A x^ can be nonzero: the rhs support and its structural neighbours
     std::vector<unsigned char> act(static_cast<size_t>(n), 0);
-#pragma omp parallel for schedule(static)
-    for (int i = 0; i < n; ++i) {
-      bool a = f0[i] != 0;
-      for (int64_t k = A.rp[i]; k < A.rp[i + 1] && !a; ++k) a = f0[A.ci[k]] != 0;
-      act[i] = a;
+    {
+      DevBuf<unsigned char> df0, dact(static_cast<size_t>(n));
+      df0.upload(f0);
+      act_rows_kernel<<<unsigned((n + 255) / 256), 256>>>(n, A.rp.get(), A.ci.get(), df0.get(), dact.get());
+      cuda_check(cudaMemcpy(act.data(), dact.get(), size_t(n), cudaMemcpyDeviceToHost), "act");
     }
     SpLevel S;
-    double res_nnz = 0.0;
     if (l == 0) {  // whole 3x3 block rows (a superset)
       if (n % 3 != 0) break;
       std::vector<int> brows;
@@ -560,11 +443,13 @@ void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows, const
         act[3 * bq] = act[3 * bq + 1] = act[3 * bq + 2] = on;
         if (on) brows.push_back(bq);
       }
-      S.fine = make_bsr3(A, &brows);
+      S.fine = bsr3_from(A, &brows, 0);
     } else if (lv[l].Am.strided && lv[l].Am.csr.n_rows >= 2048) {  // the warp-row kernel takes a row list
+      const std::vector<long long> rp = download_rp(A);
       std::vector<int> rows;
+      double res_nnz = 0.0;
       for (int i = 0; i < n; ++i)
-        if (act[i]) rows.push_back(i), res_nnz += double(A.rp[i + 1] - A.rp[i]);
+        if (act[i]) rows.push_back(i), res_nnz += double(rp[size_t(i) + 1] - rp[i]);
       if (rows.size() < size_t(n)) {
         S.res_rows.upload(rows);
         S.res_n = int(rows.size());
@@ -573,16 +458,20 @@ void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows, const
     }
     // rows of R_{l+1} = P_{l+1}^T that gather an active row
     std::vector<unsigned char> coarse(static_cast<size_t>(P.n_cols), 0);
-    for (int i = 0; i < n; ++i)
-      if (act[i])
-        for (int64_t k = P.rp[i]; k < P.rp[i + 1]; ++k) coarse[P.ci[k]] = 1;
+    {
+      DevBuf<unsigned char> dact, dco(static_cast<size_t>(P.n_cols));
+      dact.upload(act);
+      dco.zero();
+      coarse_marks_kernel<<<unsigned((n + 255) / 256), 256>>>(n, P.rp.get(), P.ci.get(), dact.get(), dco.get());
+      cuda_check(cudaMemcpy(coarse.data(), dco.get(), size_t(P.n_cols), cudaMemcpyDeviceToHost), "coarse");
+    }
     const DMat& R = lv[l + 1].R;
     if (R.strided && R.csr.n_rows >= 2048) {
-      std::vector<int64_t> cnt(static_cast<size_t>(P.n_cols), 0);
-      for (int64_t k = 0; k < P.nnz(); ++k) ++cnt[P.ci[k]];
+      std::vector<long long> rrp(size_t(R.csr.n_rows) + 1, 0);
+      cuda_check(cudaMemcpy(rrp.data(), R.csr.rp.get(), sizeof(long long) * rrp.size(), cudaMemcpyDeviceToHost), "R rp");
       std::vector<int> rrows;
       for (int c = 0; c < P.n_cols; ++c)
-        if (coarse[c]) rrows.push_back(c), S.r_bytes += 12.0 * double(cnt[c]) + 8.0;
+        if (coarse[c]) rrows.push_back(c), S.r_bytes += 12.0 * double(rrp[size_t(c) + 1] - rrp[c]) + 8.0;
       S.r_rows.upload(rrows);
       S.r_n = int(rrows.size());
     }
@@ -784,8 +673,9 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
     cuda_check(cudaMemcpy(len.data(), s.Q1.len.get(), sizeof(int) * len.size(), cudaMemcpyDeviceToHost), "Q1 rows");
     std::vector<unsigned char> rows(len.size());
     for (size_t i = 0; i < len.size(); ++i) rows[i] = len[i] > 0;
-    amg->set_sparse_rhs(rows, hp.amg);
+    amg->set_sparse_rhs(rows);
   }
+  amg->release_build_data();
   // pre-factor the H~ blocks with the reference's lu3_factor (deterministic)
   std::vector<double> lu(hp.hblocks);
   std::vector<int> piv(static_cast<size_t>(s.n_p));

@@ -7,6 +7,7 @@
 
 #include <array>
 #include <cstdint>
+#include <deque>
 #include <memory>
 #include <vector>
 
@@ -76,6 +77,14 @@ struct DCsr {
   double matrix_bytes() const { return 12.0 * double(nnz) + 8.0 * (n_rows + 1); }
 };
 
+}  // namespace fpd
+namespace fpb {
+struct DeviceMatrix {  // setup.hpp: a device-resident level operator
+  fpd::DCsr m;
+};
+}  // namespace fpb
+namespace fpd {
+
 struct DPipe {
   int n_rows = 0, n_slices = 0, n_ctas = 0;
   int64_t nnz = 0, slots = 0;
@@ -113,9 +122,48 @@ struct DMat {
 // for short rows (a thread-per-row chain would be the whole kernel's latency)
 DMat make_mat(const fpb::Csr& A, bool few_rows_parallel = false, bool strided = false);
 
+// A host CSR borrowed for an upload (no copy): the reference's layout with 64-bit row offsets.
+struct HostCsrView {
+  int n_rows = 0, n_cols = 0;
+  const int64_t* rp = nullptr;
+  const int* ci = nullptr;
+  const double* v = nullptr;
+  int64_t nnz() const { return n_rows > 0 ? rp[n_rows] : 0; }
+  static HostCsrView of(const fpb::Csr& A) { return {A.n_rows, A.n_cols, A.rp.data(), A.ci.data(), A.v.data()}; }
+};
+struct SystemView {  // BlockSystem (block.hpp:36-45) as borrowed views
+  int n_u = 0, n_t = 0, n_p = 0;
+  HostCsrView A, C1, Q1, C2, H, Q2, T, F_u;
+  static SystemView of(const fpb::HostSystem& J) {
+    return {J.n_u, J.n_t, J.n_p, HostCsrView::of(J.A), HostCsrView::of(J.C1), HostCsrView::of(J.Q1),
+            HostCsrView::of(J.C2), HostCsrView::of(J.H), HostCsrView::of(J.Q2), HostCsrView::of(J.T),
+            HostCsrView::of(J.F_u)};
+  }
+};
+
+// ---- device-side layout builders (formats.cu): CSR in HBM -> the solve path's layouts
+DCsr upload_csr(const HostCsrView& A);
+inline DCsr upload_csr(const fpb::Csr& A) { return upload_csr(HostCsrView::of(A)); }
+fpb::Csr download_csr(const DCsr& A);
+DSell sell_from(const DCsr& A, cudaStream_t s);
+DBp3 bp3_from(const DCsr& A, cudaStream_t s);
+DBsr3 bsr3_from(const DCsr& A, const std::vector<int>* brows, cudaStream_t s);
+DPipe pipe_from(const DCsr& A, cudaStream_t s);
+DCsr transpose_dev(const DCsr& A, cudaStream_t s);  // rows of A^T list the source rows ascending
+DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s);
+
+fpb::Csr host_copy(const HostCsrView& A);
+// C = diag(row_scale) A B on the device, bitwise the host spgemm (spgemm.cu); row_scale may be null
+DCsr spgemm_dev(const DCsr& A, const DCsr& B, const double* row_scale_dev);
+// build_tpu / build_tup with the fine-size setup on the device (dsetup.cu); the AMG levels of the
+// result stay device-resident (HostLevel::dA / dP)
+fpb::HostPrecond build_precond_device(const SystemView& J, const fpb::HostSystem* Jh, int variant,
+                                      const fpb::AmgOptions& opt, const std::vector<std::array<double, 3>>& coords);
+
 class DeviceSystem {
  public:
   explicit DeviceSystem(const fpb::HostSystem& J);
+  explicit DeviceSystem(const SystemView& J);
   ~DeviceSystem();
   DeviceSystem(const DeviceSystem&) = delete;
   DeviceSystem& operator=(const DeviceSystem&) = delete;
@@ -163,7 +211,15 @@ class DeviceAmg {
   // Sparse right-hand sides (t-u-p's second V-cycle: t_u2 = Q1 v_p is +0 off the rows Q1 touches):
   // block rows of level 0 whose residual can be nonzero, and rows of R_1 that can gather a nonzero;
   // every other row's sum is an exact +0, so those rows skip their loads (bitwise the full sweep).
-  void set_sparse_rhs(const std::vector<unsigned char>& rhs_rows, const fpb::HostAmg& h);
+  void set_sparse_rhs(const std::vector<unsigned char>& rhs_rows);
+  // the levels' CSR in HBM while the upload cuts row subsets from them (borrowed from the device
+  // setup or uploaded into own_), dropped by release_build_data
+  std::vector<const DCsr*> src_A_, src_P_;
+  std::deque<DCsr> own_;
+  void release_build_data() {
+    src_A_.clear(), src_P_.clear();
+    own_.clear();
+  }
   struct SpLevel {             // the sparse pass at one level (§10f)
     DBsr3 fine;                // level 0: the operator restricted to the block rows whose residual can be nonzero
     DevBuf<int> res_rows;      // level >= 1: those rows (warp-row kernel row list)

@@ -1,0 +1,459 @@
+// Device-side construction of the solve path's sparse layouts (device.cuh) from CSR resident in
+// HBM.  The CSR arrives either from the host (upload_csr: one raw copy of row offsets, columns and
+// values) or from the device setup (dsetup.cu), and every layout — BSR3-SELL, SELL-32, node-blocked
+// SELL, the windowed pipeline, R = P^T — is built by kernels over it, so the host never loops over
+// the entries of an operator.  Each builder produces exactly the layout the host builders of round 1
+// produced (same slot order, same zero padding); the solve kernels are unchanged.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <numeric>
+
+#include "engine.cuh"
+
+namespace fpd {
+
+namespace {
+
+constexpr int kT = 256;
+
+unsigned grid_for(long long n, int t = kT) { return unsigned(std::max(1LL, std::min((n + t - 1) / t, 1LL << 30))); }
+
+// exclusive prefix sum of n values into out[0..n] (out[n] = total); returns the total
+long long exclusive_scan(const long long* in, long long* out, long long n, cudaStream_t s) {
+  size_t tmp_bytes = 0;
+  cuda_check(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, in, out, n + 1, s), "scan size");
+  DevBuf<unsigned char> tmp(tmp_bytes);
+  cuda_check(cub::DeviceScan::ExclusiveSum(tmp.get(), tmp_bytes, in, out, n + 1, s), "scan");
+  long long total = 0;
+  cuda_check(cudaMemcpyAsync(&total, out + n, sizeof(long long), cudaMemcpyDeviceToHost, s), "scan total");
+  cuda_check(cudaStreamSynchronize(s), "scan sync");
+  return total;
+}
+
+__global__ void row_len_kernel(int n, const long long* rp, int* len) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) len[i] = int(rp[i + 1] - rp[i]);
+}
+
+// per slice of 32 rows: 32 * (longest row); in[n_slices] = 0 (scan input of n_slices + 1)
+__global__ void slice_slots_kernel(int n_rows, int n_slices, const int* len, long long* out) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s > n_slices) return;
+  if (s == n_slices) {
+    out[s] = 0;
+    return;
+  }
+  int mx = 0;
+  for (int r = 0; r < kSlice; ++r) {
+    const long long i = s * kSlice + r;
+    if (i < n_rows) mx = max(mx, len[i]);
+  }
+  out[s] = (long long)mx * kSlice;
+}
+
+__global__ void sell_fill_kernel(int n, const long long* rp, const int* ci, const double* v, const long long* off,
+                                 int* cols, double* vals) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long base = off[i / kSlice] + (i % kSlice);
+  const long long r0 = rp[i], m = rp[i + 1] - r0;
+  for (long long k = 0; k < m; ++k) {
+    cols[base + k * kSlice] = ci[r0 + k];
+    vals[base + k * kSlice] = v[r0 + k];
+  }
+}
+
+// node n: rows 3n..3n+2 share one column pattern (else *ok = 0)
+__global__ void bp3_check_kernel(int nn, const long long* rp, const int* ci, int* ok) {
+  const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (n >= nn) return;
+  const long long r0 = rp[3 * n], len = rp[3 * n + 1] - r0;
+  for (int d = 1; d < 3; ++d) {
+    const long long rd = rp[3 * n + d];
+    if (rp[3 * n + d + 1] - rd != len) {
+      *ok = 0;
+      return;
+    }
+    for (long long k = 0; k < len; ++k)
+      if (ci[r0 + k] != ci[rd + k]) {
+        *ok = 0;
+        return;
+      }
+  }
+}
+
+__global__ void bp3_len_kernel(int nn, const long long* rp, int* len) {
+  const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (n < nn) len[n] = int(rp[3 * n + 1] - rp[3 * n]);
+}
+
+__global__ void bp3_fill_kernel(int nn, const long long* rp, const int* ci, const double* v, const long long* off,
+                                int* cols, double* vals) {
+  const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (n >= nn) return;
+  const long long s0 = off[n / kSlice];
+  const int lane = int(n % kSlice);
+  const long long len = rp[3 * n + 1] - rp[3 * n];
+  for (long long k = 0; k < len; ++k) {
+    cols[s0 + k * kSlice + lane] = ci[rp[3 * n] + k];
+    for (int d = 0; d < 3; ++d) vals[3 * (s0 + k * kSlice) + 32 * d + lane] = v[rp[3 * n + d] + k];
+  }
+}
+
+// Block columns of block row b (global block row g): the union of c / 3 over its three scalar rows,
+// each sorted, so a three-way merge.  fill == false: count; fill == true: write slots.
+template <bool fill>
+__global__ void bsr3_rows_kernel(int nb, const int* brows, const long long* rp, const int* ci, const double* v,
+                                 int* len, const long long* off, int* bcols, double* vals) {
+  const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const long long g = brows ? brows[b] : b;
+  long long p[3], e[3];
+  for (int li = 0; li < 3; ++li) p[li] = rp[3 * g + li], e[li] = rp[3 * g + li + 1];
+  const long long s = b / kSlice;
+  const int lane = int(b % kSlice);
+  int k = 0;
+  for (;;) {
+    int cb = 0x7fffffff;
+    for (int li = 0; li < 3; ++li)
+      if (p[li] < e[li]) cb = min(cb, ci[p[li]] / 3);
+    if (cb == 0x7fffffff) break;
+    if (fill) {
+      const long long slot = off[s] + (long long)k * kSlice;
+      bcols[slot + lane] = cb;
+      for (int li = 0; li < 3; ++li)
+        for (; p[li] < e[li] && ci[p[li]] / 3 == cb; ++p[li])
+          vals[slot * 9 + (li * 3 + ci[p[li]] % 3) * kSlice + lane] = v[p[li]];
+    } else {
+      for (int li = 0; li < 3; ++li)
+        while (p[li] < e[li] && ci[p[li]] / 3 == cb) ++p[li];
+    }
+    ++k;
+  }
+  if (!fill) len[b] = k;
+}
+
+__global__ void pipe_fill_kernel(int n_slices, const int* perm, const long long* woff, const long long* rp,
+                                 const int* ci, const double* v, double* pv, int* pci) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)n_slices * kPipeRows) return;
+  const long long s = t / kPipeRows;
+  const int r = int(t % kPipeRows);
+  const int i = perm[t];
+  if (i < 0) return;
+  constexpr long long kWin = (long long)kPipeRows * kPipeW;
+  const long long r0 = rp[i], m = rp[i + 1] - r0;
+  for (long long k = 0; k < m; ++k) {
+    const long long idx = (woff[s] + k / kPipeW) * kWin + (long long)r * kPipeW + k % kPipeW;
+    pv[idx] = v[r0 + k];
+    pci[idx] = ci[r0 + k];
+  }
+}
+
+// ---- transpose (rows of A^T list the source rows ascending, like the counting transpose)
+__global__ void col_count_kernel(long long nnz, const int* ci, unsigned long long* cnt) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz; k += (long long)gridDim.x * blockDim.x)
+    atomicAdd(cnt + ci[k], 1ull);
+}
+
+__global__ void scatter_t_kernel(int n_rows, const long long* rp, const int* ci, const double* v,
+                                 unsigned long long* next, int* tci, double* tv) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n_rows) return;
+  for (long long k = rp[i]; k < rp[i + 1]; ++k) {
+    const long long pos = (long long)atomicAdd(next + ci[k], 1ull);
+    tci[pos] = int(i);
+    tv[pos] = v[k];
+  }
+}
+
+// sort each row of the transposed matrix by source row (distinct keys): one warp per row, bitonic in
+// shared memory up to kTSort entries; longer rows (rare) by one thread, insertion sort in place
+constexpr int kTSort = 2048;
+constexpr int kTWarps = 4;
+
+__global__ void __launch_bounds__(32 * kTWarps) sort_rows_kernel(int n_rows, const long long* rp, int* ci, double* v) {
+  extern __shared__ unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* keys = reinterpret_cast<int*>(smem) + warp * kTSort;
+  double* vals = reinterpret_cast<double*>(smem + size_t(kTWarps) * kTSort * sizeof(int)) + size_t(warp) * kTSort;
+  for (long long row = blockIdx.x * (long long)kTWarps + warp; row < n_rows; row += (long long)gridDim.x * kTWarps) {
+    const long long r0 = rp[row];
+    const int n = int(rp[row + 1] - r0);
+    if (n <= 1) continue;
+    if (n > kTSort) {
+      if (lane == 0)
+        for (int a = 1; a < n; ++a) {
+          const int kk = ci[r0 + a];
+          const double vv = v[r0 + a];
+          int b = a - 1;
+          for (; b >= 0 && ci[r0 + b] > kk; --b) ci[r0 + b + 1] = ci[r0 + b], v[r0 + b + 1] = v[r0 + b];
+          ci[r0 + b + 1] = kk, v[r0 + b + 1] = vv;
+        }
+      __syncwarp();
+      continue;
+    }
+    int m = 1;
+    while (m < n) m <<= 1;
+    for (int t = lane; t < m; t += 32) {
+      keys[t] = t < n ? ci[r0 + t] : 0x7fffffff;
+      vals[t] = t < n ? v[r0 + t] : 0.0;
+    }
+    __syncwarp();
+    for (int size = 2; size <= m; size <<= 1)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = lane; t < m; t += 32) {
+          const int partner = t ^ stride;
+          if (partner > t) {
+            const bool up = (t & size) == 0;
+            if ((keys[t] > keys[partner]) == up) {
+              const int tk = keys[t];
+              keys[t] = keys[partner], keys[partner] = tk;
+              const double tv = vals[t];
+              vals[t] = vals[partner], vals[partner] = tv;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    for (int t = lane; t < n; t += 32) ci[r0 + t] = keys[t], v[r0 + t] = vals[t];
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host <-> device CSR
+DCsr upload_csr(const HostCsrView& A) {
+  DCsr D;
+  D.n_rows = A.n_rows, D.n_cols = A.n_cols, D.nnz = A.nnz();
+  static_assert(sizeof(long long) == sizeof(int64_t), "row offsets");
+  if (A.n_rows > 0) D.rp.upload(reinterpret_cast<const long long*>(A.rp), size_t(A.n_rows) + 1);
+  else D.rp.alloc(1), D.rp.zero();
+  D.ci.upload(A.ci, size_t(D.nnz));
+  D.v.upload(A.v, size_t(D.nnz));
+  return D;
+}
+
+fpb::Csr host_copy(const HostCsrView& A) {
+  fpb::Csr C(A.n_rows, A.n_cols);
+  if (A.n_rows == 0) return C;
+  C.rp.assign(A.rp, A.rp + A.n_rows + 1);
+  C.ci.assign(A.ci, A.ci + A.nnz());
+  C.v.assign(A.v, A.v + A.nnz());
+  return C;
+}
+
+fpb::Csr download_csr(const DCsr& D) {
+  fpb::Csr A(D.n_rows, D.n_cols);
+  if (D.n_rows > 0)
+    cuda_check(cudaMemcpy(A.rp.data(), D.rp.get(), sizeof(long long) * (size_t(D.n_rows) + 1), cudaMemcpyDeviceToHost),
+               "download rp");
+  A.ci.resize(size_t(D.nnz));
+  A.v.resize(size_t(D.nnz));
+  if (D.nnz) {
+    cuda_check(cudaMemcpy(A.ci.data(), D.ci.get(), sizeof(int) * size_t(D.nnz), cudaMemcpyDeviceToHost), "download ci");
+    cuda_check(cudaMemcpy(A.v.data(), D.v.get(), sizeof(double) * size_t(D.nnz), cudaMemcpyDeviceToHost), "download v");
+  }
+  return A;
+}
+
+// ------------------------------------------------------------------ layouts
+DSell sell_from(const DCsr& A, cudaStream_t s) {
+  DSell D;
+  D.n_rows = A.n_rows, D.n_cols = A.n_cols, D.nnz = A.nnz;
+  D.n_slices = (A.n_rows + kSlice - 1) / kSlice;
+  D.len.alloc(size_t(A.n_rows));
+  if (A.n_rows) row_len_kernel<<<grid_for(A.n_rows), kT, 0, s>>>(A.n_rows, A.rp.get(), D.len.get());
+  DevBuf<long long> sl(size_t(D.n_slices) + 1);
+  D.off.alloc(size_t(D.n_slices) + 1);
+  slice_slots_kernel<<<grid_for(D.n_slices + 1), kT, 0, s>>>(A.n_rows, D.n_slices, D.len.get(), sl.get());
+  D.slots = exclusive_scan(sl.get(), D.off.get(), D.n_slices, s);
+  D.cols.alloc(size_t(D.slots));
+  D.vals.alloc(size_t(D.slots));
+  if (D.slots) {
+    cuda_check(cudaMemsetAsync(D.cols.get(), 0, D.cols.bytes(), s), "memset");
+    cuda_check(cudaMemsetAsync(D.vals.get(), 0, D.vals.bytes(), s), "memset");
+    sell_fill_kernel<<<grid_for(A.n_rows), kT, 0, s>>>(A.n_rows, A.rp.get(), A.ci.get(), A.v.get(), D.off.get(),
+                                                       D.cols.get(), D.vals.get());
+  }
+  cuda_check(cudaStreamSynchronize(s), "sell_from");
+  return D;
+}
+
+DBp3 bp3_from(const DCsr& A, cudaStream_t s) {
+  DBp3 D;
+  if (A.n_rows % 3 != 0 || A.n_rows == 0) return D;
+  const int nn = A.n_rows / 3;
+  DevBuf<int> ok(1);
+  const int one = 1;
+  cuda_check(cudaMemcpyAsync(ok.get(), &one, sizeof(int), cudaMemcpyHostToDevice, s), "flag");
+  bp3_check_kernel<<<grid_for(nn), kT, 0, s>>>(nn, A.rp.get(), A.ci.get(), ok.get());
+  int same = 0;
+  cuda_check(cudaMemcpyAsync(&same, ok.get(), sizeof(int), cudaMemcpyDeviceToHost, s), "flag");
+  cuda_check(cudaStreamSynchronize(s), "bp3 check");
+  if (!same) return D;
+  D.n_nodes = nn, D.nnz = A.nnz;
+  const int ns = (nn + kSlice - 1) / kSlice;
+  D.len.alloc(size_t(nn));
+  bp3_len_kernel<<<grid_for(nn), kT, 0, s>>>(nn, A.rp.get(), D.len.get());
+  DevBuf<long long> sl(size_t(ns) + 1);
+  D.off.alloc(size_t(ns) + 1);
+  slice_slots_kernel<<<grid_for(ns + 1), kT, 0, s>>>(nn, ns, D.len.get(), sl.get());
+  D.slots = exclusive_scan(sl.get(), D.off.get(), ns, s);
+  D.cols.alloc(size_t(D.slots));
+  D.vals.alloc(3 * size_t(D.slots));
+  if (D.slots) {
+    cuda_check(cudaMemsetAsync(D.cols.get(), 0, D.cols.bytes(), s), "memset");
+    cuda_check(cudaMemsetAsync(D.vals.get(), 0, D.vals.bytes(), s), "memset");
+    bp3_fill_kernel<<<grid_for(nn), kT, 0, s>>>(nn, A.rp.get(), A.ci.get(), A.v.get(), D.off.get(), D.cols.get(),
+                                                D.vals.get());
+  }
+  cuda_check(cudaStreamSynchronize(s), "bp3_from");
+  return D;
+}
+
+DBsr3 bsr3_from(const DCsr& A, const std::vector<int>* brows, cudaStream_t s) {
+  if (A.n_rows != A.n_cols || A.n_rows % 3 != 0) throw std::invalid_argument("make_bsr3: needs a square matrix with n % 3 == 0");
+  DBsr3 D;
+  const int nb = brows ? int(brows->size()) : A.n_rows / 3;
+  D.n_brows = nb;
+  D.n_slices = (nb + kSlice - 1) / kSlice;
+  if (brows) D.brow_map.upload(*brows);
+  const int* bm = brows ? D.brow_map.get() : nullptr;
+  D.len.alloc(size_t(nb));
+  if (nb)
+    bsr3_rows_kernel<false><<<grid_for(nb), kT, 0, s>>>(nb, bm, A.rp.get(), A.ci.get(), A.v.get(), D.len.get(), nullptr,
+                                                        nullptr, nullptr);
+  DevBuf<long long> sl(size_t(D.n_slices) + 1);
+  D.off.alloc(size_t(D.n_slices) + 1);
+  slice_slots_kernel<<<grid_for(D.n_slices + 1), kT, 0, s>>>(nb, D.n_slices, D.len.get(), sl.get());
+  D.slots = exclusive_scan(sl.get(), D.off.get(), D.n_slices, s);
+  {  // number of blocks (the ledger's byte count)
+    std::vector<int> len(static_cast<size_t>(nb));
+    if (nb) cuda_check(cudaMemcpy(len.data(), D.len.get(), sizeof(int) * size_t(nb), cudaMemcpyDeviceToHost), "len");
+    D.nblocks = std::accumulate(len.begin(), len.end(), int64_t(0));
+  }
+  D.bcols.alloc(size_t(D.slots));
+  D.vals.alloc(size_t(D.slots) * 9);
+  if (D.slots) {
+    cuda_check(cudaMemsetAsync(D.bcols.get(), 0, D.bcols.bytes(), s), "memset");
+    cuda_check(cudaMemsetAsync(D.vals.get(), 0, D.vals.bytes(), s), "memset");
+    bsr3_rows_kernel<true><<<grid_for(nb), kT, 0, s>>>(nb, bm, A.rp.get(), A.ci.get(), A.v.get(), D.len.get(),
+                                                       D.off.get(), D.bcols.get(), D.vals.get());
+  }
+  cuda_check(cudaStreamSynchronize(s), "bsr3_from");
+  return D;
+}
+
+DPipe pipe_from(const DCsr& A, cudaStream_t s) {
+  constexpr int kSigma = 4096;  // rows are sorted by length only inside chunks (locality of the gathers)
+  DPipe D;
+  D.n_rows = A.n_rows, D.nnz = A.nnz;
+  D.n_slices = (A.n_rows + kPipeRows - 1) / kPipeRows;
+  // the row permutation and the window offsets depend only on the row lengths (host, O(n log))
+  std::vector<long long> rp(size_t(A.n_rows) + 1, 0);
+  if (A.n_rows)
+    cuda_check(cudaMemcpy(rp.data(), A.rp.get(), sizeof(long long) * rp.size(), cudaMemcpyDeviceToHost), "rp");
+  auto row_len = [&](int i) { return int(rp[size_t(i) + 1] - rp[i]); };
+  std::vector<int> perm(static_cast<size_t>(D.n_slices) * kPipeRows, -1);
+  for (int i = 0; i < A.n_rows; ++i) perm[i] = i;
+  for (int c0 = 0; c0 < A.n_rows; c0 += kSigma) {
+    const int c1 = std::min(A.n_rows, c0 + kSigma);
+    std::stable_sort(perm.begin() + c0, perm.begin() + c1, [&](int a, int b) { return row_len(a) > row_len(b); });
+  }
+  std::vector<int> len(perm.size(), 0);
+  std::vector<long long> woff(static_cast<size_t>(D.n_slices) + 1, 0);
+  for (int sl = 0; sl < D.n_slices; ++sl) {
+    int mx = 0;
+    for (int r = 0; r < kPipeRows; ++r) {
+      const int i = perm[size_t(sl) * kPipeRows + r];
+      len[size_t(sl) * kPipeRows + r] = i >= 0 ? row_len(i) : 0;
+      mx = std::max(mx, len[size_t(sl) * kPipeRows + r]);
+    }
+    woff[sl + 1] = woff[sl] + (mx + kPipeW - 1) / kPipeW;
+  }
+  constexpr int64_t kWin = int64_t(kPipeRows) * kPipeW;
+  D.slots = woff.back() * kWin;
+  // persistent CTAs (one per SM) over contiguous slice ranges of equal window count
+  int dev = 0, sms = 148;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+  D.n_ctas = std::max(1, std::min(D.n_slices, sms * kPipeCtasPerSm));
+  std::vector<int> cs(static_cast<size_t>(D.n_ctas) + 1, D.n_slices);
+  cs[0] = 0;
+  const long long tot = woff.back();
+  for (int b = 1; b < D.n_ctas; ++b) {
+    const long long target = (tot * b + D.n_ctas - 1) / D.n_ctas;
+    cs[b] = int(std::lower_bound(woff.begin(), woff.end() - 1, target) - woff.begin());
+    cs[b] = std::max(cs[b], cs[b - 1]);
+  }
+  D.cta_slice.upload(cs);
+  D.woff.upload(woff);
+  D.row.upload(perm);
+  D.len.upload(len);
+  D.v.alloc(size_t(D.slots));
+  D.ci.alloc(size_t(D.slots));
+  if (D.slots) {
+    cuda_check(cudaMemsetAsync(D.v.get(), 0, D.v.bytes(), s), "memset");
+    cuda_check(cudaMemsetAsync(D.ci.get(), 0, D.ci.bytes(), s), "memset");
+    pipe_fill_kernel<<<grid_for((long long)D.n_slices * kPipeRows), kT, 0, s>>>(
+        D.n_slices, D.row.get(), D.woff.get(), A.rp.get(), A.ci.get(), A.v.get(), D.v.get(), D.ci.get());
+  }
+  cuda_check(cudaStreamSynchronize(s), "pipe_from");
+  return D;
+}
+
+DCsr transpose_dev(const DCsr& A, cudaStream_t s) {
+  DCsr T;
+  T.n_rows = A.n_cols, T.n_cols = A.n_rows, T.nnz = A.nnz;
+  DevBuf<unsigned long long> cnt(size_t(A.n_cols) + 1);
+  cuda_check(cudaMemsetAsync(cnt.get(), 0, cnt.bytes(), s), "memset");
+  if (A.nnz) col_count_kernel<<<grid_for(A.nnz), kT, 0, s>>>(A.nnz, A.ci.get(), cnt.get());
+  T.rp.alloc(size_t(A.n_cols) + 1);
+  exclusive_scan(reinterpret_cast<const long long*>(cnt.get()), T.rp.get(), A.n_cols, s);
+  T.ci.alloc(size_t(A.nnz));
+  T.v.alloc(size_t(A.nnz));
+  if (A.nnz) {
+    cuda_check(cudaMemcpyAsync(cnt.get(), T.rp.get(), sizeof(long long) * size_t(A.n_cols), cudaMemcpyDeviceToDevice, s),
+               "next");
+    scatter_t_kernel<<<grid_for(A.n_rows), kT, 0, s>>>(A.n_rows, A.rp.get(), A.ci.get(), A.v.get(), cnt.get(),
+                                                       T.ci.get(), T.v.get());
+    const size_t smem = size_t(kTWarps) * kTSort * (sizeof(int) + sizeof(double));
+    cuda_check(cudaFuncSetAttribute(sort_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem");
+    sort_rows_kernel<<<std::max(1, std::min((T.n_rows + kTWarps - 1) / kTWarps, 148 * 8)), 32 * kTWarps, smem, s>>>(
+        T.n_rows, T.rp.get(), T.ci.get(), T.v.get());
+  }
+  cuda_check(cudaStreamSynchronize(s), "transpose_dev");
+  return T;
+}
+
+DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s) {
+  DMat M;
+  if (strided) {  // row_sum = strided32: plain CSR, one warp per row (or window-staged CTAs of R rows)
+    M.warp = M.strided = true;
+    M.strided_rows = 1;  // one row per CTA: most parallel loads for few-row operators
+    M.csr = std::move(A);
+    return M;
+  }
+  const double avg = A.n_rows > 0 ? double(A.nnz) / A.n_rows : 0.0;
+  // SELL's thread-per-row chains need enough rows to hide latency; below ~64k
+  // rows the slice kernel's parallel loads win even for short rows
+  M.warp = A.n_rows > 0 && (avg >= 48.0 || (A.n_rows < 65536 && avg >= 8.0) ||
+                            (few_rows_parallel && A.n_rows < 2048 && avg >= 2.0));
+  if (!M.warp) {
+    M.sell = sell_from(A, s);
+    return M;
+  }
+  M.slice_rows = A.n_rows >= 2048 ? 32 : 8;
+  if (M.slice_rows == 32) {
+    M.pipe = true;
+    M.pm = pipe_from(A, s);
+    return M;
+  }
+  M.csr = std::move(A);
+  return M;
+}
+
+}  // namespace fpd

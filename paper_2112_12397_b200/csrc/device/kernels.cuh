@@ -14,8 +14,6 @@
 
 namespace fpd {
 
-constexpr int kSlice = 32;
-
 // ------------------------------------------------------------------ gathers
 struct GPlain {  // x_j
   const double* x;
@@ -425,8 +423,7 @@ inline size_t strided_smem_bytes(int R) { return sizeof(double) * size_t(R) * (k
 // so up to kPipeStages windows of loads and gathers are in flight while the
 // consumer sums.  Stage q is handed over with named barriers: FULL = 1 + q
 // (producer arrives, consumer waits), EMPTY = 1 + kPipeStages + q (reverse).
-constexpr int kPipeRows = 32, kPipeW = 32, kPipeStages = 7, kPipeThreads = 32 * (kPipeStages + 1);
-constexpr int kPipeCtasPerSm = 2;  // two resident pipelines per SM (registers capped at 128)
+constexpr int kPipeStages = 7, kPipeThreads = 32 * (kPipeStages + 1);
 constexpr size_t kPipeSmem = sizeof(double) * kPipeStages * kPipeRows * (kPipeW + 1);  // dynamic (> 48 KB)
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }

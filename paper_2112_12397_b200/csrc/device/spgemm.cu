@@ -20,8 +20,11 @@
 #include <stdexcept>
 #include <vector>
 
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include "../host/hcsr.hpp"
-#include "device.cuh"
+#include "engine.cuh"
 
 namespace fpd {
 namespace {
@@ -213,6 +216,79 @@ bool spgemm_device(const fpb::Csr& A, const fpb::Csr& B, std::span<const double>
     cuda_check(cudaMemcpy(C.v.data(), dv, sizeof(double) * size_t(nnz), cudaMemcpyDeviceToHost), "spgemm v");
   }
   return true;
+}
+
+namespace {
+__global__ void widen_counts_kernel(int n, const int* cnt, long long* out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = cnt[i];
+  if (i == n) out[i] = 0;
+}
+}  // namespace
+
+// The same products with operands and result in HBM (the device setup, dsetup.cu).  A product with
+// a row over the hash capacity (none on the BASELINE configs) runs on the host and is uploaded.
+DCsr spgemm_dev(const DCsr& A, const DCsr& B, const double* row_scale_dev) {
+  if (A.n_cols != B.n_rows) throw std::invalid_argument("spgemm: dimension mismatch");
+  static bool attr = [] {
+    cuda_check(cudaFuncSetAttribute(spgemm_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem)),
+               "spgemm smem");
+    cuda_check(cudaFuncSetAttribute(spgemm_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem)),
+               "spgemm smem");
+    return true;
+  }();
+  (void)attr;
+  const int n = A.n_rows;
+  DCsr C;
+  C.n_rows = n, C.n_cols = B.n_cols;
+  C.rp.alloc(size_t(n) + 1);
+  if (n == 0) {
+    C.rp.zero();
+    return C;
+  }
+  const SpView dA{n, A.rp.get(), A.ci.get(), A.v.get()};
+  const SpView dB{B.n_rows, B.rp.get(), B.ci.get(), B.v.get()};
+  DevBuf<int> cnt(static_cast<size_t>(n));
+  int dev = 0, sms = 148;
+  cuda_check(cudaGetDevice(&dev), "device");
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  const int grid = std::max(1, std::min((n + kWarps - 1) / kWarps, sms * 4));
+  spgemm_rows<false><<<grid, kThreads, kSmem>>>(dA, dB, row_scale_dev, cnt.get(), nullptr, nullptr, nullptr);
+  cuda_check(cudaGetLastError(), "spgemm symbolic");
+  int mn = 0;
+  {
+    DevBuf<int> out(1);
+    size_t tb = 0;
+    cuda_check(cub::DeviceReduce::Min(nullptr, tb, cnt.get(), out.get(), n), "min size");
+    DevBuf<unsigned char> tmp(tb);
+    cuda_check(cub::DeviceReduce::Min(tmp.get(), tb, cnt.get(), out.get(), n), "min");
+    cuda_check(cudaMemcpy(&mn, out.get(), sizeof(int), cudaMemcpyDeviceToHost), "min");
+  }
+  if (mn < 0) {  // a row over the hash capacity: the host routine
+    const fpb::Csr hA = download_csr(A), hB = download_csr(B);
+    std::vector<double> sc;
+    if (row_scale_dev) {
+      sc.resize(size_t(n));
+      cuda_check(cudaMemcpy(sc.data(), row_scale_dev, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost), "scale");
+    }
+    return upload_csr(fpb::spgemm(hA, hB, sc));
+  }
+  DevBuf<long long> wide(size_t(n) + 1);
+  widen_counts_kernel<<<unsigned((n + 256) / 256), 256>>>(n, cnt.get(), wide.get());
+  size_t tb = 0;
+  cuda_check(cub::DeviceScan::ExclusiveSum(nullptr, tb, wide.get(), C.rp.get(), n + 1), "scan size");
+  {
+    DevBuf<unsigned char> tmp(tb);
+    cuda_check(cub::DeviceScan::ExclusiveSum(tmp.get(), tb, wide.get(), C.rp.get(), n + 1), "scan");
+  }
+  long long nnz = 0;
+  cuda_check(cudaMemcpy(&nnz, C.rp.get() + n, sizeof(long long), cudaMemcpyDeviceToHost), "nnz");
+  C.nnz = nnz;
+  C.ci.alloc(size_t(nnz));
+  C.v.alloc(size_t(nnz));
+  if (nnz > 0) spgemm_rows<true><<<grid, kThreads, kSmem>>>(dA, dB, row_scale_dev, cnt.get(), C.rp.get(), C.ci.get(), C.v.get());
+  cuda_check(cudaDeviceSynchronize(), "spgemm numeric");
+  return C;
 }
 
 }  // namespace fpd

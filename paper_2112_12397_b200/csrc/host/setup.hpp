@@ -7,6 +7,7 @@
 #pragma once
 
 #include <array>
+#include <memory>
 #include <vector>
 
 #include "hcsr.hpp"
@@ -30,9 +31,18 @@ struct AmgOptions {
   int row_sum = 0;  // 0 ordered (reference order), 1 strided32 on A_l (l >= 1) and R_l
 };
 
+// A level operator built by the device setup (csrc/device/dsetup.cu) stays in HBM: DeviceMatrix is
+// its device CSR (defined in engine.cuh, opaque here).  Such a level's host A / P hold only their
+// shapes; A_nnz / P_nnz give the entry counts and fp_host_precond_matrix downloads on request.
+struct DeviceMatrix;
+
 struct HostLevel {
   Csr A;
   Csr P;  // prolongation from this level to the previous finer one (empty at level 0)
+  std::shared_ptr<DeviceMatrix> dA, dP;  // device-resident A / P (device setup), else null
+  int64_t A_nnz = -1, P_nnz = -1;        // entry counts of device-resident matrices
+  int64_t a_nnz() const { return dA ? A_nnz : A.nnz(); }
+  int64_t p_nnz() const { return dP ? P_nnz : P.nnz(); }
   std::vector<double> diag;
   double lambda_max = 0.0;     // chebyshev: 1.1 x power-iteration estimate of rho(D^-1 A)
   std::vector<int> aggregate;  // fine row -> aggregate id (coarse levels only)
