@@ -208,9 +208,13 @@ int fp_precond_apply(fp_precond* p, const double* x, double* y, int32_t mem);
 int fp_amg_apply(fp_precond* p, const double* r, double* x, int32_t mem);
 /* InnerSolver::call_count / reset_count (precond.hpp:34-42) */
 int64_t fp_precond_inner_calls(fp_precond* p, int32_t reset);
-/* Where the preconditioner setup's sparse products (amg_setup's Galerkin products, the Schur
- * cores) run: 1 = device SpGEMM (bitwise the host routine), 0 = host (default; or set
- * FRACPREC_B200_DEVICE_SETUP=1).  Applies to builds started afterwards. */
+/* Where build_tpu / build_tup run (fp_host_precond_build, fp_workload_host_precond_build):
+ * 1 = on the device (the default when a CUDA device is present): the Schur core, the strength graph,
+ *     the prolongation smoothing and the Galerkin products in HBM, the BFS aggregation and the
+ *     per-aggregate QR on the host; the AMG levels stay device-resident for fp_precond_create
+ *     (fp_host_precond_matrix downloads them on request);
+ * 0 = on the host (OpenMP; FRACPREC_B200_SETUP=host selects it at start-up).
+ * Both build the oracle's hierarchy bit for bit.  Applies to builds started afterwards. */
 int fp_set_setup_backend(int32_t device);
 int fp_setup_backend(int32_t* device);
 /* The factor application the preconditioner resolved to: FP_FACTOR_SWEEP or FP_FACTOR_INVERSE */
@@ -233,6 +237,7 @@ typedef struct fp_profile {
   int32_t level_rows[32];
   int64_t level_nnz[32];
   double vcycle_ms[32];             /* V-cycle from level l down (CUDA graph); level l alone = [l] - [l+1] */
+  double apply_wasted_bytes;        /* bytes one apply streams beyond apply_bytes (explicit block inverses) */
 } fp_profile;
 int fp_precond_profile(fp_precond* p, int32_t reps, fp_profile* out);
 

@@ -253,8 +253,10 @@ long or_precond_inner_calls(void* p, int reset) {
 // GPU uploads).  which: 0 = S (tpu) / S1 (tup), 1 = T (tpu) / S2 (tup)
 const void* or_precond_matrix(void* p, int which) {
   const Pc* pc = static_cast<Pc*>(p);
-  if (pc->tpu) return which == 0 ? &pc->tpu->S : &pc->sys->J.T;
-  return which == 0 ? &pc->tup->S1 : &pc->tup->S2;
+  // the inner operator S~ / S1 lives in the AMG hierarchy's level 0 (the preconditioner drops its copy)
+  if (pc->tpu)
+    return which == 0 ? (pc->tpu->S_solver.amg ? &pc->tpu->S_solver.amg->levels[0].A : &pc->tpu->S) : &pc->sys->J.T;
+  return which == 0 ? (pc->tup->S1_solver.amg ? &pc->tup->S1_solver.amg->levels[0].A : &pc->tup->S1) : &pc->tup->S2;
 }
 int or_precond_hblocks(void* p, double* out) {  // n_p * 9 raw (regularized) H~ blocks
   const Pc* pc = static_cast<Pc*>(p);

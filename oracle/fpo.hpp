@@ -280,7 +280,9 @@ struct AmgHierarchy {
   int num_levels() const { return int(levels.size()); }
 };
 
-AmgHierarchy amg_setup(const CsrMatrix& A, const std::vector<std::vector<double>>& near_null,
+// A is taken by value (amg.hpp:58 takes a const reference): callers that no longer need the
+// operator move it in, so the hierarchy does not hold a second copy of a 25 GB config-5 operator
+AmgHierarchy amg_setup(CsrMatrix A, const std::vector<std::vector<double>>& near_null,
                        const AmgConfig& cfg);
 std::vector<double> amg_apply(const AmgHierarchy& h, std::span<const double> r);
 // EXTENSION: switch the coarse operators' row-sum order (builds / drops the levels' R = P^T)

@@ -67,7 +67,7 @@ class FpProfile(C.Structure):
                 ("fine_resid_bytes", C.c_double), ("fine_post_ms", C.c_double), ("fine_post_bytes", C.c_double),
                 ("band_ms", C.c_double), ("band_bytes", C.c_double), ("coarse_ms", C.c_double),
                 ("n_levels", C.c_int32), ("level_rows", C.c_int32 * 32), ("level_nnz", C.c_int64 * 32),
-                ("vcycle_ms", C.c_double * 32)]
+                ("vcycle_ms", C.c_double * 32), ("apply_wasted_bytes", C.c_double)]
 
 
 class FpAmgLevelDesc(C.Structure):

@@ -503,12 +503,14 @@ def export_snapshot(directory: str, J: BlockSystem, region: str, dt: float = 0.5
 
 
 def set_setup_backend(where: str) -> None:
-    """Run the setup's sparse products on the "device" (bitwise the host routine) or the "host"."""
+    """Where build_tpu / build_tup run: "device" (csrc/device/dsetup.cu: the fine-size products, strength
+    graph and Galerkin products in HBM; the default with a CUDA device) or "host" (OpenMP, setup.cpp).
+    Both build the oracle's hierarchy bit for bit."""
     N.check(N.lib.fp_set_setup_backend(1 if where == "device" else 0))
 
 
 def setup_backend() -> str:
-    """Where the preconditioner setup's sparse products run: "device" or "host" (the default)."""
+    """Where the preconditioner setup runs: "device" (default with a CUDA device) or "host"."""
     d = C.c_int32()
     N.check(N.lib.fp_setup_backend(C.byref(d)))
     return "device" if d.value else "host"

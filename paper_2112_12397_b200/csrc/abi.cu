@@ -564,6 +564,7 @@ int fp_precond_profile(fp_precond* p, int32_t reps, fp_profile* out) {
     out->fine_resid_ms = r.fine_resid_ms, out->fine_resid_bytes = r.fine_resid_bytes;
     out->fine_post_ms = r.fine_post_ms, out->fine_post_bytes = r.fine_post_bytes;
     out->band_ms = r.band_ms, out->band_bytes = r.band_bytes, out->coarse_ms = r.coarse_ms;
+    out->apply_wasted_bytes = r.apply_wasted_bytes;
     const auto& lv = p->dev->amg->lv;
     out->n_levels = int32_t(lv.size());
     for (size_t l = 0; l < lv.size() && l < 32; ++l) {

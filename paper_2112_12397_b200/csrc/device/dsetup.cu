@@ -160,6 +160,71 @@ __global__ void strength_kernel(int n, const long long* arp, const int* aci, con
   }
 }
 
+// With a structurally symmetric A (every level operator here: S1 / S~ and the Galerkin products
+// P^T A P), row i of A^T has row i's columns and A^T(i, j) = A(j, i), found by binary search in row j,
+// so B's rows need no transposed copy.  sym_check_kernel clears *ok on the first entry without a mirror.
+__device__ __forceinline__ long long find_col(const long long* rp, const int* ci, int row, int col) {
+  long long lo = rp[row], hi = rp[row + 1];
+  while (lo < hi) {
+    const long long mid = (lo + hi) >> 1;
+    if (ci[mid] < col) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < rp[row + 1] && ci[lo] == col) ? lo : -1;
+}
+
+__global__ void sym_check_kernel(int n, const long long* rp, const int* ci, int* ok) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (long long k = rp[i]; k < rp[i + 1]; ++k)
+    if (find_col(rp, ci, ci[k], int(i)) < 0) {
+      *ok = 0;
+      return;
+    }
+}
+
+__global__ void bdiag_sym_kernel(int n, const long long* rp, const int* ci, const double* v, double* d) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long k = find_col(rp, ci, int(i), int(i));
+  d[i] = k >= 0 ? b_entry(true, true, v[k], v[k]) : 0.0;
+}
+
+template <bool fill>
+__global__ void strength_sym_kernel(int n, const long long* rp, const int* ci, const double* v, const double* d,
+                                    double theta, long long* cnt, char* isolated, const long long* off, int* nbr,
+                                    double* w) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long long o = fill ? off[i] : 0, strong = 0;
+  int offdiag = 0;
+  const double di = fabs(d[i]);
+  for (long long k = rp[i]; k < rp[i + 1]; ++k) {
+    const int j = ci[k];
+    if (j == i) continue;
+    const double b = b_entry(true, true, v[k], v[find_col(rp, ci, j, int(i))]);
+    if (b != 0.0) ++offdiag;
+    const double thr = theta * sqrt(di * fabs(d[j]));
+    if (fabs(b) > thr) {
+      if (fill) nbr[o] = j, w[o] = fabs(b), ++o;
+      ++strong;
+    }
+  }
+  if (!fill) {
+    cnt[i] = strong;
+    isolated[i] = offdiag == 0 ? 1 : 0;
+  }
+}
+
+// weights of the leftover rows rows[0..m) (amg.cpp:98-111), packed
+__global__ void gather_w_kernel(int m, const int* rows, const long long* off, const double* w, const long long* pos,
+                                double* out) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const long long k0 = off[rows[t]], k1 = off[rows[t] + 1];
+  for (long long k = k0; k < k1; ++k) out[pos[t] + (k - k0)] = w[k];
+}
+
 // rows rows[0..m) of A, packed (the fixed-stress neighbourhoods)
 __global__ void gather_len_kernel(int m, const int* rows, const long long* rp, long long* cnt) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -233,41 +298,66 @@ struct StrengthDev {
   std::vector<int> nbr;
   std::vector<char> isolated;
   DevBuf<double> w;
+  DevBuf<long long> doff;
 };
 
 StrengthDev strength_dev(const DCsr& A, double theta) {
   const int n = A.n_rows;
-  const DCsr At = transpose_dev(A, 0);
-  DevBuf<double> d(static_cast<size_t>(n));
   StrengthDev g;
   if (n == 0) {
     g.off.assign(1, 0);
     return g;
   }
-  bdiag_kernel<<<grid_for(n), kT>>>(n, A.rp.get(), A.ci.get(), A.v.get(), At.rp.get(), At.ci.get(), At.v.get(), d.get());
-  DevBuf<long long> cnt(size_t(n) + 1), off(size_t(n) + 1);
+  DevBuf<double> d(static_cast<size_t>(n));
+  DevBuf<long long> cnt(size_t(n) + 1);
+  g.doff.alloc(size_t(n) + 1);
   DevBuf<char> iso(static_cast<size_t>(n));
   cnt.zero();
-  strength_kernel<false><<<grid_for(n), kT>>>(n, A.rp.get(), A.ci.get(), A.v.get(), At.rp.get(), At.ci.get(), At.v.get(),
-                                              d.get(), theta, cnt.get(), iso.get(), nullptr, nullptr, nullptr);
-  const long long m = scan_counts(cnt, n, off);
-  DevBuf<int> nbr(static_cast<size_t>(m));
-  g.w.alloc(size_t(m));
-  if (m)
-    strength_kernel<true><<<grid_for(n), kT>>>(n, A.rp.get(), A.ci.get(), A.v.get(), At.rp.get(), At.ci.get(),
-                                               At.v.get(), d.get(), theta, nullptr, nullptr, off.get(), nbr.get(),
-                                               g.w.get());
+  int sym = 1;
+  {
+    DevBuf<int> ok(1);
+    cuda_check(cudaMemcpy(ok.get(), &sym, sizeof(int), cudaMemcpyHostToDevice), "flag");
+    sym_check_kernel<<<grid_for(n), kT>>>(n, A.rp.get(), A.ci.get(), ok.get());
+    cuda_check(cudaMemcpy(&sym, ok.get(), sizeof(int), cudaMemcpyDeviceToHost), "flag");
+  }
+  long long m = 0;
+  DevBuf<int> nbr;
+  if (sym) {
+    bdiag_sym_kernel<<<grid_for(n), kT>>>(n, A.rp.get(), A.ci.get(), A.v.get(), d.get());
+    strength_sym_kernel<false><<<grid_for(n), kT>>>(n, A.rp.get(), A.ci.get(), A.v.get(), d.get(), theta, cnt.get(),
+                                                    iso.get(), nullptr, nullptr, nullptr);
+    m = scan_counts(cnt, n, g.doff);
+    nbr.alloc(size_t(m));
+    g.w.alloc(size_t(m));
+    if (m)
+      strength_sym_kernel<true><<<grid_for(n), kT>>>(n, A.rp.get(), A.ci.get(), A.v.get(), d.get(), theta, nullptr,
+                                                     nullptr, g.doff.get(), nbr.get(), g.w.get());
+  } else {
+    const DCsr At = transpose_dev(A, 0);
+    bdiag_kernel<<<grid_for(n), kT>>>(n, A.rp.get(), A.ci.get(), A.v.get(), At.rp.get(), At.ci.get(), At.v.get(),
+                                      d.get());
+    strength_kernel<false><<<grid_for(n), kT>>>(n, A.rp.get(), A.ci.get(), A.v.get(), At.rp.get(), At.ci.get(),
+                                                At.v.get(), d.get(), theta, cnt.get(), iso.get(), nullptr, nullptr,
+                                                nullptr);
+    m = scan_counts(cnt, n, g.doff);
+    nbr.alloc(size_t(m));
+    g.w.alloc(size_t(m));
+    if (m)
+      strength_kernel<true><<<grid_for(n), kT>>>(n, A.rp.get(), A.ci.get(), A.v.get(), At.rp.get(), At.ci.get(),
+                                                 At.v.get(), d.get(), theta, nullptr, nullptr, g.doff.get(), nbr.get(),
+                                                 g.w.get());
+  }
   g.off.resize(size_t(n) + 1);
   g.nbr.resize(size_t(m));
   g.isolated.resize(size_t(n));
-  cuda_check(cudaMemcpy(g.off.data(), off.get(), off.bytes(), cudaMemcpyDeviceToHost), "strength off");
+  cuda_check(cudaMemcpy(g.off.data(), g.doff.get(), g.doff.bytes(), cudaMemcpyDeviceToHost), "strength off");
   if (m) cuda_check(cudaMemcpy(g.nbr.data(), nbr.get(), nbr.bytes(), cudaMemcpyDeviceToHost), "strength nbr");
   cuda_check(cudaMemcpy(g.isolated.data(), iso.get(), iso.bytes(), cudaMemcpyDeviceToHost), "strength isolated");
   return g;
 }
 
-// amg.cpp:60-113 on the host graph; the strongest-neighbour weights of the leftover rows (usually
-// none) are fetched from the device
+// amg.cpp:60-113 on the host graph; the weights of the leftover rows (the strongest-neighbour pass)
+// are gathered on the device in one batch
 std::pair<std::vector<int>, int> aggregate_host(const StrengthDev& g, int n) {
   std::vector<int> agg(static_cast<size_t>(n), -2);
   for (int i = 0; i < n; ++i)
@@ -306,17 +396,29 @@ std::pair<std::vector<int>, int> aggregate_host(const StrengthDev& g, int n) {
       }
     }
   }
-  std::vector<double> w;
-  for (int i = 0; i < n; ++i) {
-    if (agg[i] != -2) continue;
-    const long long k0 = g.off[i], k1 = g.off[i + 1];
-    w.resize(size_t(k1 - k0));
-    if (k1 > k0) cuda_check(cudaMemcpy(w.data(), g.w.get() + k0, sizeof(double) * w.size(), cudaMemcpyDeviceToHost), "w");
+  std::vector<int> left;
+  std::vector<long long> pos(1, 0);
+  for (int i = 0; i < n; ++i)
+    if (agg[i] == -2) left.push_back(i), pos.push_back(pos.back() + g.off[i + 1] - g.off[i]);
+  std::vector<double> w(size_t(pos.back()));
+  if (!left.empty() && pos.back() > 0) {
+    DevBuf<int> drows;
+    DevBuf<long long> dpos;
+    drows.upload(left);
+    dpos.upload(pos);
+    DevBuf<double> dw(w.size());
+    gather_w_kernel<<<grid_for((long long)left.size()), kT>>>(int(left.size()), drows.get(), g.doff.get(), g.w.get(),
+                                                             dpos.get(), dw.get());
+    cuda_check(cudaMemcpy(w.data(), dw.get(), dw.bytes(), cudaMemcpyDeviceToHost), "leftover weights");
+  }
+  for (size_t q = 0; q < left.size(); ++q) {  // in index order: a leftover may join one assigned before it
+    const int i = left[q];
     int best = -1;
     double best_w = -1.0;
-    for (long long k = k0; k < k1; ++k) {
+    for (long long k = g.off[i]; k < g.off[i + 1]; ++k) {
       const int j = g.nbr[k];
-      if (agg[j] >= 0 && w[size_t(k - k0)] > best_w) best_w = w[size_t(k - k0)], best = agg[j];
+      const double wk = w[size_t(pos[q] + (k - g.off[i]))];
+      if (agg[j] >= 0 && wk > best_w) best_w = wk, best = agg[j];
     }
     agg[i] = best >= 0 ? best : n_agg++;
   }

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <chrono>
 #include <cstring>
 #include <stdexcept>
 
@@ -662,10 +663,26 @@ void DeviceAmg::enqueue_apply(const double* r, double* x, const double* sub_from
 }
 
 // --------------------------------------------------------------- precond
+namespace {
+struct UploadClock {  // FRACPREC_B200_VERBOSE: phases of the preconditioner upload
+  bool on = std::getenv("FRACPREC_B200_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[upload] %-26s %8.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
+
 DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) : variant(hp.variant), sys(&s) {
+  UploadClock uclk;
   if (hp.amg.levels.empty() || hp.S().n_rows != s.n_u) throw std::invalid_argument("precond upload: inner operator size != n_u");
   if (int(hp.hblocks.size()) != 9 * s.n_p) throw std::invalid_argument("precond upload: H~ blocks size != 9 n_p");
   amg = std::make_unique<DeviceAmg>(hp.amg, true);
+  uclk.mark("AMG levels");
   const char* sp_env = std::getenv("FRACPREC_B200_SPARSE_RHS");
   if (hp.variant == fpb::kTup && s.Q1.n_rows == s.n_u && !(sp_env && std::atoi(sp_env) == 0)) {
     // t_u2 = Q1 v_p is nonzero only on the rows Q1 touches (fracture-adjacent displacements)
@@ -676,6 +693,7 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
     amg->set_sparse_rhs(rows);
   }
   amg->release_build_data();
+  uclk.mark("sparse-rhs subsets");
   // pre-factor the H~ blocks with the reference's lu3_factor (deterministic)
   std::vector<double> lu(hp.hblocks);
   std::vector<int> piv(static_cast<size_t>(s.n_p));
@@ -698,6 +716,16 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
     band_Uc.upload(F.Uc), band_piv.upload(F.piv);
   for (size_t b = 0; b + 1 < F.block_start.size(); ++b)
     band_max_block = std::max(band_max_block, F.block_start[b + 1] - F.block_start[b]);
+  {  // B_factor: the factor's stored nonzeros (band padding excluded) at 12 B, the diagonal, pivots
+    auto nz = [](const std::vector<double>& v) {
+      long long c = 0;
+#pragma omp parallel for reduction(+ : c)
+      for (long long i = 0; i < (long long)v.size(); ++i) c += v[size_t(i)] != 0.0;
+      return c;
+    };
+    const bool spd = F.kind == fpb::BandFactor::Kind::spd;
+    band_factor_bytes = 12.0 * double(nz(F.Lc) + nz(spd ? F.Lr : F.Uc)) + 8.0 * F.n + (spd ? 0.0 : 4.0 * F.n);
+  }
   band = BandView{F.n, F.kl, F.ku, int(F.block_start.size()) - 1, band_start.get(), band_Lc.get(), band_diag.get(),
                   band_Lr.get(), band_Uc.get(), band_piv.get(), F.kind == fpb::BandFactor::Kind::spd ? 1 : 0,
                   F.pivoted ? 1 : 0};
@@ -731,6 +759,7 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
     dinv = DinvView{band_start.get(), dinv_off.get(), dinv_v.get()};
     dinv_bytes = 8.0 * double(off.back());
   }
+  uclk.mark("H~ / factor");
   const size_t smem = sizeof(double) * (size_t(band_ring_doubles(kBandMaxQ)) + size_t(std::max(band_max_block, 1)));
   if (!inverse && smem > 227 * 1024)
     throw std::invalid_argument("precond upload: fracture block too large for the band solver");
@@ -745,22 +774,24 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
 void DevicePrecond::enqueue_band(const double* rhs, double rs, double* out, double* out2, const double* sub, double os,
                                  int mode, cudaStream_t s, Ledger* L) {
   if (band.n == 0) return;
+  // algorithmic bytes: B_factor = 12 (nnz(L) + nnz(U)) + the diagonal (+ pivots) +
+  // the vectors, in either mode; the explicit inverses' extra bytes are booked as waste
+  const double vec_bytes = 8.0 * band.n * (2 + (mode == 1) + (mode == 2));
   if (inverse) {
     launch(dinv_kernel, dim3(blocks_for(size_t(band.n) * 32, kDinvThreads)), dim3(kDinvThreads), 0, s, "dinv_kernel", dinv, band.n, band.n_blocks,
                                                                                        rhs, rs, out, out2, sub, os, mode);
     cuda_check(cudaGetLastError(), "dinv_kernel launch");
-    if (L) L->add(dinv_bytes + 8.0 * band.n * (2 + (mode == 1) + (mode == 2)));
+    if (L) {
+      L->add(band_factor_bytes + vec_bytes);
+      L->waste(std::max(0.0, dinv_bytes - band_factor_bytes));
+    }
     return;
   }
   launch(band_solve_kernel, dim3(band.n_blocks), dim3(32), sizeof(double) * (band_ring_doubles(kBandMaxQ) + std::max(band_max_block, 1)), s, "band_solve_kernel", 
       band, rhs, rs, out, out2,
                                                                                               sub, os, mode);
   cuda_check(cudaGetLastError(), "band_solve_kernel launch");
-  if (L) {
-    const double n = band.n;
-    const double fb = 8.0 * n * (band.kl + (band.spd ? band.kl : band.ku)) + 8.0 * n + (band.spd ? 0.0 : 4.0 * n);
-    L->add(fb + 8.0 * n * (2 + (mode == 1) + (mode == 2)));
-  }
+  if (L) L->add(band_factor_bytes + vec_bytes);
 }
 
 void DevicePrecond::enqueue_apply(const double* x, double* y, double at, double ap, cudaStream_t s, Ledger* L) {
@@ -1151,7 +1182,7 @@ ProfileResult profile_precond(const DeviceSystem& sys, DevicePrecond& pc, int re
   Ledger la, lj;
   cudaGraphExec_t ga = graph_of([&] { pc.enqueue_apply(x.get(), y.get(), 1.0, 1.0, s, &la); });
   r.apply_ms = timed([&] { cudaGraphLaunch(ga, s); });
-  r.apply_bytes = la.bytes, r.apply_launches = la.launches;
+  r.apply_bytes = la.bytes, r.apply_launches = la.launches, r.apply_wasted_bytes = la.wasted;
   cudaGraphExecDestroy(ga);
   cudaGraphExec_t gj = graph_of([&] { sys.enqueue_apply(x.get(), y.get(), 1.0, 1.0, s, &lj); });
   r.japply_ms = timed([&] { cudaGraphLaunch(gj, s); });

@@ -21,7 +21,9 @@ namespace fpd {
 struct Ledger {
   double bytes = 0.0;
   int launches = 0;
+  double wasted = 0.0;  // bytes a launch streams beyond its algorithmic bytes (explicit block inverses)
   void add(double b) { bytes += b, ++launches; }
+  void waste(double b) { wasted += b; }
 };
 
 struct DSell {
@@ -268,6 +270,7 @@ class DevicePrecond {
   DevBuf<double> dinv_v;
   DevBuf<long long> dinv_off;
   double dinv_bytes = 0;
+  double band_factor_bytes = 0;  // B_factor of SURVEY §8(d): 12 (nnz(L) + nnz(U)) + diagonal (+ pivots)
   DevBuf<double> tt, tu, tp, su, sp_, vp, tu2, vu2, xh;
   long inner_calls = 0;
   int inner_per_apply() const { return variant == 1 ? 2 : 1; }
@@ -303,6 +306,7 @@ struct ProfileResult {
   double apply_ms = 0, apply_bytes = 0, japply_ms = 0, japply_bytes = 0;
   double fine_resid_ms = 0, fine_resid_bytes = 0, fine_post_ms = 0, fine_post_bytes = 0;
   double band_ms = 0, band_bytes = 0, coarse_ms = 0;
+  double apply_wasted_bytes = 0;
   int apply_launches = 0;
   std::vector<double> vcycle_ms;  // graph of the V-cycle from level l down
 };

@@ -4,6 +4,7 @@
 // SELL, the windowed pipeline, R = P^T — is built by kernels over it, so the host never loops over
 // the entries of an operator.  Each builder produces exactly the layout the host builders of round 1
 // produced (same slot order, same zero padding); the solve kernels are unchanged.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -151,75 +152,56 @@ __global__ void pipe_fill_kernel(int n_slices, const int* perm, const long long*
   }
 }
 
-// ---- transpose (rows of A^T list the source rows ascending, like the counting transpose)
+// ---- transpose (rows of A^T list the source rows ascending, like the counting transpose): a STABLE
+// radix sort of the entries by column, taken in row-major order, so equal columns keep ascending rows
 __global__ void col_count_kernel(long long nnz, const int* ci, unsigned long long* cnt) {
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz; k += (long long)gridDim.x * blockDim.x)
     atomicAdd(cnt + ci[k], 1ull);
 }
 
-__global__ void scatter_t_kernel(int n_rows, const long long* rp, const int* ci, const double* v,
-                                 unsigned long long* next, int* tci, double* tv) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n_rows) return;
-  for (long long k = rp[i]; k < rp[i + 1]; ++k) {
-    const long long pos = (long long)atomicAdd(next + ci[k], 1ull);
-    tci[pos] = int(i);
+template <class Idx>
+__global__ void iota_kernel(long long n, Idx* out) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    out[k] = Idx(k);
+}
+
+// entry k of A (row-major) lands at position pos: its row by binary search of the row offsets
+template <class Idx>
+__global__ void gather_t_kernel(long long nnz, int n_rows, const long long* rp, const double* v, const Idx* src,
+                                int* tci, double* tv) {
+  for (long long pos = blockIdx.x * (long long)blockDim.x + threadIdx.x; pos < nnz;
+       pos += (long long)gridDim.x * blockDim.x) {
+    const long long k = (long long)src[pos];
+    int lo = 0, hi = n_rows;  // largest row r with rp[r] <= k
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (rp[mid] <= k) lo = mid;
+      else hi = mid;
+    }
+    tci[pos] = lo;
     tv[pos] = v[k];
   }
 }
 
-// sort each row of the transposed matrix by source row (distinct keys): one warp per row, bitonic in
-// shared memory up to kTSort entries; longer rows (rare) by one thread, insertion sort in place
-constexpr int kTSort = 2048;
-constexpr int kTWarps = 4;
-
-__global__ void __launch_bounds__(32 * kTWarps) sort_rows_kernel(int n_rows, const long long* rp, int* ci, double* v) {
-  extern __shared__ unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int* keys = reinterpret_cast<int*>(smem) + warp * kTSort;
-  double* vals = reinterpret_cast<double*>(smem + size_t(kTWarps) * kTSort * sizeof(int)) + size_t(warp) * kTSort;
-  for (long long row = blockIdx.x * (long long)kTWarps + warp; row < n_rows; row += (long long)gridDim.x * kTWarps) {
-    const long long r0 = rp[row];
-    const int n = int(rp[row + 1] - r0);
-    if (n <= 1) continue;
-    if (n > kTSort) {
-      if (lane == 0)
-        for (int a = 1; a < n; ++a) {
-          const int kk = ci[r0 + a];
-          const double vv = v[r0 + a];
-          int b = a - 1;
-          for (; b >= 0 && ci[r0 + b] > kk; --b) ci[r0 + b + 1] = ci[r0 + b], v[r0 + b + 1] = v[r0 + b];
-          ci[r0 + b + 1] = kk, v[r0 + b + 1] = vv;
-        }
-      __syncwarp();
-      continue;
-    }
-    int m = 1;
-    while (m < n) m <<= 1;
-    for (int t = lane; t < m; t += 32) {
-      keys[t] = t < n ? ci[r0 + t] : 0x7fffffff;
-      vals[t] = t < n ? v[r0 + t] : 0.0;
-    }
-    __syncwarp();
-    for (int size = 2; size <= m; size <<= 1)
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int t = lane; t < m; t += 32) {
-          const int partner = t ^ stride;
-          if (partner > t) {
-            const bool up = (t & size) == 0;
-            if ((keys[t] > keys[partner]) == up) {
-              const int tk = keys[t];
-              keys[t] = keys[partner], keys[partner] = tk;
-              const double tv = vals[t];
-              vals[t] = vals[partner], vals[partner] = tv;
-            }
-          }
-        }
-        __syncwarp();
-      }
-    for (int t = lane; t < n; t += 32) ci[r0 + t] = keys[t], v[r0 + t] = vals[t];
-    __syncwarp();
+template <class Idx>
+void transpose_fill(const DCsr& A, DCsr& T, cudaStream_t s) {
+  int bits = 1;
+  while ((1LL << bits) < (long long)A.n_cols) ++bits;
+  DevBuf<int> kin(size_t(A.nnz)), kout(size_t(A.nnz));
+  DevBuf<Idx> vin(size_t(A.nnz)), vout(size_t(A.nnz));
+  cuda_check(cudaMemcpyAsync(kin.get(), A.ci.get(), kin.bytes(), cudaMemcpyDeviceToDevice, s), "keys");
+  iota_kernel<Idx><<<1184, kT, 0, s>>>(A.nnz, vin.get());
+  size_t tb = 0;
+  cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.get(), kout.get(), vin.get(), vout.get(), A.nnz, 0, bits, s),
+             "radix size");
+  {
+    DevBuf<unsigned char> tmp(tb);
+    cuda_check(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, kin.get(), kout.get(), vin.get(), vout.get(), A.nnz, 0,
+                                               bits, s),
+               "radix sort");
   }
+  kin = DevBuf<int>(), kout = DevBuf<int>(), vin = DevBuf<Idx>();
+  gather_t_kernel<Idx><<<1184, kT, 0, s>>>(A.nnz, A.n_rows, A.rp.get(), A.v.get(), vout.get(), T.ci.get(), T.v.get());
 }
 
 }  // namespace
@@ -416,14 +398,8 @@ DCsr transpose_dev(const DCsr& A, cudaStream_t s) {
   T.ci.alloc(size_t(A.nnz));
   T.v.alloc(size_t(A.nnz));
   if (A.nnz) {
-    cuda_check(cudaMemcpyAsync(cnt.get(), T.rp.get(), sizeof(long long) * size_t(A.n_cols), cudaMemcpyDeviceToDevice, s),
-               "next");
-    scatter_t_kernel<<<grid_for(A.n_rows), kT, 0, s>>>(A.n_rows, A.rp.get(), A.ci.get(), A.v.get(), cnt.get(),
-                                                       T.ci.get(), T.v.get());
-    const size_t smem = size_t(kTWarps) * kTSort * (sizeof(int) + sizeof(double));
-    cuda_check(cudaFuncSetAttribute(sort_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "smem");
-    sort_rows_kernel<<<std::max(1, std::min((T.n_rows + kTWarps - 1) / kTWarps, 148 * 8)), 32 * kTWarps, smem, s>>>(
-        T.n_rows, T.rp.get(), T.ci.get(), T.v.get());
+    if (A.nnz < (1LL << 31)) transpose_fill<int>(A, T, s);
+    else transpose_fill<long long>(A, T, s);
   }
   cuda_check(cudaStreamSynchronize(s), "transpose_dev");
   return T;

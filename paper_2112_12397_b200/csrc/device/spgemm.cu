@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kThreads) spgemm_rows(SpView A, SpView B, cons
   int* keys = reinterpret_cast<int*>(smem) + warp * kCap;
   double* acc = reinterpret_cast<double*>(smem + size_t(kWarps) * kCap * sizeof(int)) + size_t(warp) * kCap;
   for (int row = blockIdx.x * kWarps + warp; row < A.n_rows; row += gridDim.x * kWarps) {
+    if (numeric && cnt[row] > kFill) continue;  // a big row (spgemm_big_rows)
     for (int s = lane; s < kCap; s += 32) {
       keys[s] = -1;
       if (numeric) acc[s] = 0.0;  // first accumulation is (0.0 + p), as on the host
@@ -139,6 +140,125 @@ __global__ void __launch_bounds__(kThreads) spgemm_rows(SpView A, SpView B, cons
     for (int t = lane; t < n; t += 32) cci[o + t] = keys[t], cv[o + t] = acc[t];
     __syncwarp();
   }
+}
+
+// Rows with more distinct columns than a warp's table: one CTA per row, a block-wide table of
+// kCapBig slots in shared memory; the k loop stays sequential (a barrier per k) and the threads take
+// B's row k (distinct columns), so every entry still receives its products in the host's order.
+constexpr int kCapBig = 12288;
+constexpr int kFillBig = kCapBig * 3 / 4;
+constexpr int kBigThreads = 512;
+constexpr size_t kSmemBig = size_t(kCapBig) * (sizeof(int) + sizeof(double));
+
+__device__ __forceinline__ int hslot_big(int j) { return int((unsigned(j) * 2654435761u) % unsigned(kCapBig)); }
+
+__device__ __forceinline__ int hinsert_big(int* keys, int j, int* count) {
+  int s = hslot_big(j);
+  for (int probe = 0; probe < kCapBig; ++probe) {
+    const int prev = atomicCAS(keys + s, -1, j);
+    if (prev == -1) {
+      atomicAdd(count, 1);
+      return s;
+    }
+    if (prev == j) return s;
+    s = s + 1 == kCapBig ? 0 : s + 1;
+  }
+  return -1;
+}
+
+template <bool numeric>
+__global__ void __launch_bounds__(kBigThreads) spgemm_big_rows(SpView A, SpView B, const double* row_scale,
+                                                              const int* rows, int n_big, int* cnt,
+                                                              const long long* crp, int* cci, double* cv) {
+  extern __shared__ unsigned char smem[];
+  __shared__ int count, full, base;
+  int* keys = reinterpret_cast<int*>(smem);
+  double* acc = reinterpret_cast<double*>(smem + size_t(kCapBig) * sizeof(int));
+  for (int q = blockIdx.x; q < n_big; q += gridDim.x) {
+    const int row = rows[q];
+    for (int s = threadIdx.x; s < kCapBig; s += blockDim.x) {
+      keys[s] = -1;
+      if (numeric) acc[s] = 0.0;
+    }
+    if (threadIdx.x == 0) count = 0, full = 0;
+    __syncthreads();
+    const double sc = row_scale ? row_scale[row] : 1.0;
+    bool overflow = false;
+    for (long long ka = A.rp[row]; ka < A.rp[row + 1] && !overflow; ++ka) {
+      const int k = A.ci[ka];
+      const double av = row_scale ? A.v[ka] * sc : A.v[ka];
+      for (long long kb = B.rp[k] + threadIdx.x; kb < B.rp[k + 1]; kb += blockDim.x) {
+        const int s = hinsert_big(keys, B.ci[kb], &count);
+        if (s < 0) {
+          full = 1;
+          continue;
+        }
+        if (numeric) acc[s] = acc[s] + av * B.v[kb];
+      }
+      __syncthreads();
+      overflow = count > kFillBig || full;
+      __syncthreads();
+    }
+    if (!numeric) {
+      if (threadIdx.x == 0) cnt[row] = overflow ? -2 : count;
+      __syncthreads();
+      continue;
+    }
+    // compact used slots to the front in slot order (block-wide prefix over 512-slot chunks)
+    __shared__ int chunk_base;
+    if (threadIdx.x == 0) chunk_base = 0;
+    __syncthreads();
+    const int n = count;
+    for (int s0 = 0; s0 < kCapBig; s0 += blockDim.x) {
+      const int s = s0 + threadIdx.x;
+      const bool has = s < kCapBig && keys[s] != -1;
+      const int kk = has ? keys[s] : 0;
+      const double vv = has ? acc[s] : 0.0;
+      // block-wide exclusive rank of `has`
+      __shared__ int warp_tot[kBigThreads / 32];
+      const unsigned m = __ballot_sync(0xffffffffu, has);
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      if (lane == 0) warp_tot[w] = __popc(m);
+      __syncthreads();
+      int before = 0;
+      for (int t = 0; t < w; ++t) before += warp_tot[t];
+      int tot = 0;
+      for (int t = 0; t < int(blockDim.x >> 5); ++t) tot += warp_tot[t];
+      const int dst = chunk_base + before + __popc(m & ((1u << lane) - 1));
+      __syncthreads();  // every thread has read its slot before any write below
+      if (has) keys[dst] = kk, acc[dst] = vv;
+      __syncthreads();
+      if (threadIdx.x == 0) chunk_base += tot;
+      __syncthreads();
+    }
+    int mm = 1;
+    while (mm < n) mm <<= 1;
+    for (int s = n + threadIdx.x; s < mm; s += blockDim.x) keys[s] = 0x7fffffff;
+    __syncthreads();
+    for (int size = 2; size <= mm; size <<= 1)  // bitonic sort by column (keys distinct)
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int t = threadIdx.x; t < mm / 2; t += blockDim.x) {
+          const int lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const int a = keys[lo], b = keys[hi];
+          if ((a > b) == up) {
+            keys[lo] = b, keys[hi] = a;
+            const double x = acc[lo];
+            acc[lo] = acc[hi], acc[hi] = x;
+          }
+        }
+        __syncthreads();
+      }
+    const long long o = crp[row];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) cci[o + t] = keys[t], cv[o + t] = acc[t];
+    __syncthreads();
+    (void)base;
+  }
+}
+
+__global__ void list_big_rows_kernel(int n, const int* cnt, int* rows, int* n_big) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n && cnt[i] < 0) rows[atomicAdd(n_big, 1)] = int(i);
 }
 
 template <class T>
@@ -255,6 +375,24 @@ DCsr spgemm_dev(const DCsr& A, const DCsr& B, const double* row_scale_dev) {
   const int grid = std::max(1, std::min((n + kWarps - 1) / kWarps, sms * 4));
   spgemm_rows<false><<<grid, kThreads, kSmem>>>(dA, dB, row_scale_dev, cnt.get(), nullptr, nullptr, nullptr);
   cuda_check(cudaGetLastError(), "spgemm symbolic");
+  static bool attr_big = [] {
+    cuda_check(cudaFuncSetAttribute(spgemm_big_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kSmemBig)), "spgemm big smem");
+    cuda_check(cudaFuncSetAttribute(spgemm_big_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kSmemBig)), "spgemm big smem");
+    return true;
+  }();
+  (void)attr_big;
+  // rows over a warp's table: counted again by one CTA each
+  DevBuf<int> big_rows(static_cast<size_t>(n)), n_big_d(1);
+  n_big_d.zero();
+  list_big_rows_kernel<<<unsigned((n + 255) / 256), 256>>>(n, cnt.get(), big_rows.get(), n_big_d.get());
+  int n_big = 0;
+  cuda_check(cudaMemcpy(&n_big, n_big_d.get(), sizeof(int), cudaMemcpyDeviceToHost), "big rows");
+  const int grid_big = std::max(1, std::min(n_big, sms));
+  if (n_big > 0)
+    spgemm_big_rows<false><<<grid_big, kBigThreads, kSmemBig>>>(dA, dB, row_scale_dev, big_rows.get(), n_big,
+                                                                 cnt.get(), nullptr, nullptr, nullptr);
   int mn = 0;
   {
     DevBuf<int> out(1);
@@ -264,7 +402,7 @@ DCsr spgemm_dev(const DCsr& A, const DCsr& B, const double* row_scale_dev) {
     cuda_check(cub::DeviceReduce::Min(tmp.get(), tb, cnt.get(), out.get(), n), "min");
     cuda_check(cudaMemcpy(&mn, out.get(), sizeof(int), cudaMemcpyDeviceToHost), "min");
   }
-  if (mn < 0) {  // a row over the hash capacity: the host routine
+  if (mn < 0) {  // a row over the block table too: the host routine
     const fpb::Csr hA = download_csr(A), hB = download_csr(B);
     std::vector<double> sc;
     if (row_scale_dev) {
@@ -286,7 +424,12 @@ DCsr spgemm_dev(const DCsr& A, const DCsr& B, const double* row_scale_dev) {
   C.nnz = nnz;
   C.ci.alloc(size_t(nnz));
   C.v.alloc(size_t(nnz));
-  if (nnz > 0) spgemm_rows<true><<<grid, kThreads, kSmem>>>(dA, dB, row_scale_dev, cnt.get(), C.rp.get(), C.ci.get(), C.v.get());
+  if (nnz > 0) {
+    spgemm_rows<true><<<grid, kThreads, kSmem>>>(dA, dB, row_scale_dev, cnt.get(), C.rp.get(), C.ci.get(), C.v.get());
+    if (n_big > 0)
+      spgemm_big_rows<true><<<grid_big, kBigThreads, kSmemBig>>>(dA, dB, row_scale_dev, big_rows.get(), n_big,
+                                                                  cnt.get(), C.rp.get(), C.ci.get(), C.v.get());
+  }
   cuda_check(cudaDeviceSynchronize(), "spgemm numeric");
   return C;
 }
