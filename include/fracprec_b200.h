@@ -92,8 +92,13 @@ enum { FP_ROW_SUM_ORDERED = 0, FP_ROW_SUM_STRIDED = 1 };
  * FP_FACTOR_SWEEP   - forward/backward column sweeps on the banded factor;
  * FP_FACTOR_INVERSE - the explicit inverse of every fracture block (columns =
  *                     sweep solves of unit vectors), streamed as a block GEMV;
- * FP_FACTOR_AUTO    - the faster of the two that fits device memory. */
-enum { FP_FACTOR_AUTO = 0, FP_FACTOR_SWEEP = 1, FP_FACTOR_INVERSE = 2 };
+ * FP_FACTOR_PANEL   - the factor cut into panels of one bandwidth, so L and U are
+ *                     block bidiagonal; per panel the dense L_qq^-1, L_qq^-1 L_q,q-1
+ *                     (and U's) are streamed by two chains of cluster steps (needs a
+ *                     factor without row interchanges);
+ * FP_FACTOR_AUTO    - panels when available, else the faster of the other two that
+ *                     fits device memory. */
+enum { FP_FACTOR_AUTO = 0, FP_FACTOR_SWEEP = 1, FP_FACTOR_INVERSE = 2, FP_FACTOR_PANEL = 3 };
 
 /* PrecondConfig (precond.hpp:19-30); inner is always AMG on this path */
 typedef struct fp_precond_config {

@@ -207,7 +207,8 @@ int or_precond_build(void* s, int variant, int inner, const double* amg_d, const
 
 void or_precond_destroy(void* p) { delete static_cast<Pc*>(p); }
 
-// factor_solve: 0 = sweeps (SparseFactor::solve), 1 = explicit block inverse
+// factor_solve: 0 = sweeps (SparseFactor::solve), 1 = explicit block inverse,
+// 2 = panels (a factor without row interchanges)
 int or_precond_set_factor_solve(void* p, int mode) {
   return guard([&] {
     Pc* pc = static_cast<Pc*>(p);
@@ -217,7 +218,19 @@ int or_precond_set_factor_solve(void* p, int mode) {
     } else {
       F.inv.clear(), F.inv_off.clear();
     }
+    if (mode == 2) {
+      if (F.pan.empty()) F.build_panels();
+    } else {
+      F.pan.clear(), F.pan_off.clear(), F.pan_p.clear();
+    }
   });
+}
+
+// 1 when the factor took row interchanges (panel mode unavailable)
+int or_precond_factor_pivots(void* p) {
+  const Pc* pc = static_cast<Pc*>(p);
+  const BandFactor& F = pc->tpu ? pc->tpu->T_factor : pc->tup->S2_factor;
+  return F.pivots() ? 1 : 0;
 }
 
 // row_sum: 0 = ordered (reference), 1 = strided32 on the coarse operators

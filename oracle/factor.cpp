@@ -298,12 +298,154 @@ void BandFactor::build_inverse() {
   }
 }
 
+// ------------------------------------------------- factor_solve = panel (fpo.hpp)
+bool BandFactor::pivots() const {
+  if (kind == Kind::spd) return false;
+  for (int j = 0; j < n; ++j)
+    if (piv[j] != j) return true;
+  return false;
+}
+
+namespace {
+// 32 lane-strided partials over c ascending from 0.0, then the xor tree h = 16..1 (the warp order)
+double strided_dot(const double* row, const double* x, int len) {
+  double v[32];
+  for (int j = 0; j < 32; ++j) {
+    double s = 0.0;
+    for (int c = j; c < len; c += 32) s = s + row[c] * x[c];
+    v[j] = s;
+  }
+  for (int h = 16; h >= 1; h >>= 1) {
+    double w[32];
+    for (int j = 0; j < 32; ++j) w[j] = v[j] + v[j ^ h];
+    std::copy(w, w + 32, v);
+  }
+  return v[0];
+}
+}  // namespace
+
+void BandFactor::build_panels() {
+  if (pivots()) throw std::invalid_argument("factor_solve = panel needs a factor without row interchanges");
+  const int nblk = int(block_start.size()) - 1;
+  pan_p.assign(size_t(nblk), 1);
+  pan_off.assign(size_t(nblk) + 1, 0);
+  const int ub = kind == Kind::spd ? kl : ku;  // stored upper band of U (spd: L^T)
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int b0 = block_start[blk], b1 = block_start[blk + 1];
+    int p = 1;
+    for (int j = b0; j < b1; ++j) {
+      for (int r = 0; r < kl; ++r)
+        if (Lc[size_t(j) * kl + r] != 0.0) p = std::max(p, r + 1);
+      for (int r = 0; r < ub; ++r)
+        if ((kind == Kind::spd ? Lr[size_t(j) * kl + r] : Uc[size_t(j) * ku + r]) != 0.0) p = std::max(p, r + 1);
+    }
+    pan_p[blk] = p;
+    const int m = b1 - b0, P = (m + p - 1) / p;
+    size_t sz = 0;
+    for (int q = 0; q < P; ++q) {
+      const size_t s = size_t(std::min(p, m - q * p));
+      const size_t sp = q > 0 ? size_t(p) : 0, sn = q + 1 < P ? size_t(std::min(p, m - (q + 1) * p)) : 0;
+      sz += s * s + s * sp + s * s + s * sn;
+    }
+    pan_off[blk + 1] = pan_off[blk] + sz;
+  }
+  pan.assign(pan_off.back(), 0.0);
+  // L(gi, gj) / U(gi, gj) from the band storage (0 outside the band)
+  auto Lv = [&](int gi, int gj) { return gi > gj && gi - gj <= kl ? Lc[size_t(gj) * kl + (gi - gj - 1)] : 0.0; };
+  auto Uv = [&](int gi, int gj) {  // strictly upper part (spd: L(gj, gi))
+    if (!(gj > gi)) return 0.0;
+    if (kind == Kind::spd) return gj - gi <= kl ? Lr[size_t(gj) * kl + (gj - gi - 1)] : 0.0;
+    return gj - gi <= ku ? Uc[size_t(gj) * ku + (gj - gi - 1)] : 0.0;
+  };
+#pragma omp parallel for num_threads(threads()) schedule(dynamic)
+  for (int blk = 0; blk < nblk; ++blk) {
+    const int b0 = block_start[blk], m = block_start[blk + 1] - b0, p = pan_p[blk], P = (m + p - 1) / p;
+    double* out = pan.data() + pan_off[blk];
+    std::vector<double> z(static_cast<size_t>(p));
+    for (int q = 0; q < P; ++q) {
+      const int r0 = b0 + q * p, s = std::min(p, m - q * p);
+      const int sp = q > 0 ? p : 0, sn = q + 1 < P ? std::min(p, m - (q + 1) * p) : 0;
+      auto fwd = [&]() {  // z <- L_qq^-1 z (unit lower, column sweeps)
+        for (int j = 0; j < s; ++j) {
+          const double zj = z[j];
+          for (int i = j + 1; i < s; ++i) z[i] -= Lv(r0 + i, r0 + j) * zj;
+        }
+      };
+      auto bwd = [&]() {  // z <- U_qq^-1 z (general: divide by the diagonal; spd: unit)
+        for (int j = s - 1; j >= 0; --j) {
+          double zj = z[j];
+          if (kind == Kind::general) {
+            zj = zj / diag[r0 + j];
+            z[j] = zj;
+          }
+          for (int i = j - 1; i >= 0; --i) z[i] -= Uv(r0 + i, r0 + j) * zj;
+        }
+      };
+      double* H = out;
+      double* G = H + size_t(s) * s;
+      double* K = G + size_t(s) * sp;
+      double* F = K + size_t(s) * s;
+      for (int c = 0; c < s; ++c) {
+        std::fill(z.begin(), z.begin() + s, 0.0);
+        z[c] = 1.0;
+        fwd();
+        for (int i = 0; i < s; ++i) H[size_t(i) * s + c] = z[i];
+        std::fill(z.begin(), z.begin() + s, 0.0);
+        z[c] = 1.0;
+        bwd();
+        for (int i = 0; i < s; ++i) K[size_t(i) * s + c] = z[i];
+      }
+      for (int c = 0; c < sp; ++c) {  // G column c: L(panel q rows, panel q-1 column c)
+        for (int i = 0; i < s; ++i) z[i] = Lv(r0 + i, r0 - sp + c);
+        fwd();
+        for (int i = 0; i < s; ++i) G[size_t(i) * sp + c] = z[i];
+      }
+      for (int c = 0; c < sn; ++c) {  // F column c: U(panel q rows, panel q+1 column c)
+        for (int i = 0; i < s; ++i) z[i] = Uv(r0 + i, r0 + s + c);
+        bwd();
+        for (int i = 0; i < s; ++i) F[size_t(i) * sn + c] = z[i];
+      }
+      out = F + size_t(s) * sn;
+    }
+  }
+}
+
 std::vector<double> BandFactor::solve(std::span<const double> b) const {
   if (int(b.size()) != n) throw std::invalid_argument("SparseFactor::solve: dimension mismatch");
   std::vector<double> x(b.begin(), b.end());
   const int nblk = int(block_start.size()) - 1;
 #pragma omp parallel for num_threads(threads()) schedule(dynamic)
   for (int blk = 0; blk < nblk; ++blk) {
+    if (!pan.empty()) {  // factor_solve = panel
+      const int b0 = block_start[blk], m = block_start[blk + 1] - b0, p = pan_p[blk], P = (m + p - 1) / p;
+      std::vector<double> y(static_cast<size_t>(m));
+      const double* base = pan.data() + pan_off[blk];
+      std::vector<const double*> Kq(static_cast<size_t>(P)), Fq(static_cast<size_t>(P));
+      for (int q = 0; q < P; ++q) {  // forward: y_q = H_q b_q - G_q y_q-1
+        const int s = std::min(p, m - q * p), sp = q > 0 ? p : 0, sn = q + 1 < P ? std::min(p, m - (q + 1) * p) : 0;
+        const double* H = base;
+        const double* G = H + size_t(s) * s;
+        Kq[q] = G + size_t(s) * sp;
+        Fq[q] = Kq[q] + size_t(s) * s;
+        base = Fq[q] + size_t(s) * sn;
+        for (int i = 0; i < s; ++i) {
+          const double sh = strided_dot(H + size_t(i) * s, b.data() + b0 + q * p, s);
+          const double sg = sp ? strided_dot(G + size_t(i) * sp, y.data() + (q - 1) * p, sp) : 0.0;
+          y[size_t(q) * p + i] = sp ? sh - sg : sh;
+        }
+      }
+      if (kind == Kind::spd)
+        for (int i = 0; i < m; ++i) y[i] = y[i] / diag[b0 + i];
+      for (int q = P - 1; q >= 0; --q) {  // backward: x_q = K_q z_q - F_q x_q+1
+        const int s = std::min(p, m - q * p), sn = q + 1 < P ? std::min(p, m - (q + 1) * p) : 0;
+        for (int i = 0; i < s; ++i) {
+          const double sk = strided_dot(Kq[q] + size_t(i) * s, y.data() + q * p, s);
+          const double sf = sn ? strided_dot(Fq[q] + size_t(i) * sn, x.data() + b0 + (q + 1) * p, sn) : 0.0;
+          x[b0 + q * p + i] = sn ? sk - sf : sk;
+        }
+      }
+      continue;
+    }
     if (inv.empty()) {
       solve_block(blk, x.data());
       continue;

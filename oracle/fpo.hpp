@@ -233,6 +233,21 @@ struct BandFactor {
   // c = j (mod 32) (c ascending, from 0.0) combined by an xor tree (factor.cpp).
   std::vector<double> inv;
   std::vector<size_t> inv_off;
+  // factor_solve = panel (only without row interchanges): each block split into panels
+  // of p_b rows, p_b = max(lower bandwidth of its L, upper bandwidth of its U) from the stored
+  // nonzeros, so L and U are block bidiagonal.  Per panel q (s_q rows):
+  //   H_q = L_qq^-1,  G_q = L_qq^-1 L_q,q-1      (forward:  y_q = H_q b_q - G_q y_q-1)
+  //   K_q = U_qq^-1,  F_q = U_qq^-1 U_q,q+1      (backward: x_q = K_q z_q - F_q x_q+1)
+  // (spd: U = L^T unit, z = y / D; general: z = y).  Each is built by the column sweeps of
+  // solve_block applied to the columns of I or of the coupling block; each row product is summed as
+  // 32 lane-strided partials (columns c = j mod 32 ascending, from 0.0) and the xor tree, the two
+  // products of a row combined as (H b) - (G y).  Row-major dense s_q x s_q (H, K), s_q x s_q-1 (G),
+  // s_q x s_q+1 (F) per panel, stacked per block at pan_off[blk].
+  std::vector<int> pan_p;                 // per block: panel size
+  std::vector<size_t> pan_off;            // per block: offset of its panel matrices in pan
+  std::vector<double> pan;                // per block, per panel: H, G, K, F
+  bool pivots() const;                    // general: any row interchange (panel mode unavailable)
+  void build_panels();
   void factor(const CsrMatrix& A, Kind k);
   void build_inverse();
   void solve_block(int blk, double* x) const;  // sweeps on one block, in place

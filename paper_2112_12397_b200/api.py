@@ -131,12 +131,12 @@ class AmgConfig:
         return c
 
 
-_FACTOR_SOLVE = {"auto": 0, "sweep": 1, "inverse": 2}
+_FACTOR_SOLVE = {"auto": 0, "sweep": 1, "inverse": 2, "panel": 3}
 
 
 def _factor_mode(name: str) -> int:
     if name not in _FACTOR_SOLVE:
-        raise ValueError(f"unknown factor_solve {name!r} (auto | sweep | inverse)")
+        raise ValueError(f"unknown factor_solve {name!r} (auto | sweep | inverse | panel)")
     return _FACTOR_SOLVE[name]
 
 
@@ -373,10 +373,10 @@ class GpuPreconditioner:
 
     @property
     def factor_solve(self) -> str:
-        """The factor application this preconditioner resolved to: 'sweep' or 'inverse'."""
+        """The factor application this preconditioner resolved to: 'sweep', 'inverse' or 'panel'."""
         m = C.c_int32()
         N.check(N.lib.fp_precond_factor_solve(self._h, C.byref(m)))
-        return "inverse" if m.value == 2 else "sweep"
+        return {1: "sweep", 2: "inverse", 3: "panel"}[m.value]
 
     def call_count(self) -> int:
         return int(N.lib.fp_precond_inner_calls(self._h, 0))

@@ -345,7 +345,7 @@ int fp_host_precond_build(const fp_block_system* J, const fp_precond_config* cfg
   return guard([&] {
     ensure_setup_backend();
     need(J && cfg && out, "fp_host_precond_build: null argument");
-    need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
+    need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_PANEL, "unknown factor_solve");
     ViewHold hold;
     const fpd::SystemView V = checked_system(*J, hold);
     std::vector<std::array<double, 3>> xyz;
@@ -430,7 +430,7 @@ int fp_host_precond_set_upload(fp_host_precond* p, int32_t row_sum, int32_t fact
   return guard([&] {
     need(p != nullptr, "fp_host_precond_set_upload: null handle");
     need(row_sum == FP_ROW_SUM_ORDERED || row_sum == FP_ROW_SUM_STRIDED, "AmgConfig: unknown row_sum");
-    need(factor_solve >= FP_FACTOR_AUTO && factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
+    need(factor_solve >= FP_FACTOR_AUTO && factor_solve <= FP_FACTOR_PANEL, "unknown factor_solve");
     p->hp.amg.opt.row_sum = row_sum;
     p->hp.factor_solve = factor_solve;
   });
@@ -458,7 +458,7 @@ int fp_precond_upload(fp_system* s, const fp_precond_desc* d, fp_precond** out) 
     hp.hblocks.assign(d->h_blocks, d->h_blocks + 9 * size_t(s->dev->n_p));
     const fpb::Csr F = to_csr(d->factor_matrix, "factor_matrix");
     hp.factor.factor(F, d->variant == FP_TPU ? fpb::BandFactor::Kind::spd : fpb::BandFactor::Kind::general);
-    need(d->factor_solve >= FP_FACTOR_AUTO && d->factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
+    need(d->factor_solve >= FP_FACTOR_AUTO && d->factor_solve <= FP_FACTOR_PANEL, "unknown factor_solve");
     hp.factor_solve = d->factor_solve;
     hp.amg.opt = to_amg(d->amg);
     for (int l = 0; l < d->n_levels; ++l) {
@@ -489,7 +489,7 @@ void fp_precond_destroy(fp_precond* p) { delete p; }
 int fp_precond_factor_solve(const fp_precond* p, int32_t* mode) {
   return guard([&] {
     need(p && mode, "null argument");
-    *mode = p->dev->inverse ? FP_FACTOR_INVERSE : FP_FACTOR_SWEEP;
+    *mode = p->dev->panel ? FP_FACTOR_PANEL : p->dev->inverse ? FP_FACTOR_INVERSE : FP_FACTOR_SWEEP;
   });
 }
 
@@ -630,7 +630,7 @@ int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config
   return guard([&] {
     ensure_setup_backend();
     need(w && cfg && out, "fp_workload_host_precond_build: null argument");
-    need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_INVERSE, "unknown factor_solve");
+    need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_PANEL, "unknown factor_solve");
     auto p = std::make_unique<fp_host_precond>();
     p->hp = build_any(fpd::SystemView::of(w->w.J), &w->w.J, cfg->variant, to_amg(cfg->amg), w->w.coords);
     p->hp.factor_solve = cfg->factor_solve;

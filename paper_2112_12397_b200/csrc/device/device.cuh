@@ -100,6 +100,19 @@ struct DinvView {
   const double* v = nullptr;
 };
 
+// factor_solve = panel: per block, panels of p rows with the dense H, G, K, F of the
+// oracle's BandFactor::build_panels (fpo.hpp), stacked per block at off[blk].
+constexpr int kPanelMax = 256;  // largest panel (bandwidth) the device path takes
+struct PanelView {
+  int n_blocks = 0;
+  const int* block_start = nullptr;
+  const int* p = nullptr;           // panel size per block
+  const long long* off = nullptr;   // per block: offset of its panel matrices
+  const double* m = nullptr;
+  const double* diag = nullptr;     // spd: D (z = y / D between the sweeps); null for general
+  double* scratch = nullptr;        // n doubles: z between the forward and the backward chain
+};
+
 struct DenseLUView {  // coarse-level full-pivot LU, column-major n x n
   int n = 0, rank = 0;
   const double* lu = nullptr;

@@ -729,11 +729,63 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
   band = BandView{F.n, F.kl, F.ku, int(F.block_start.size()) - 1, band_start.get(), band_Lc.get(), band_diag.get(),
                   band_Lr.get(), band_Uc.get(), band_piv.get(), F.kind == fpb::BandFactor::Kind::spd ? 1 : 0,
                   F.pivoted ? 1 : 0};
-  // factor_solve: sweeps (latency bound: ~2 * nb sequential steps per block) or the
-  // explicit block inverses (HBM bound: 8 nb^2 bytes per block, all blocks in one
-  // grid).  Auto picks the inverse when its streaming time is the smaller one and
-  // it fits a quarter of the free device memory.
-  {
+  // factor_solve: panels (~1.3 B_factor streamed, 2 P dependent cluster steps per
+  // block; the default whenever the factor took no row interchanges and its panels fit), sweeps
+  // (latency bound: ~2 nb sequential steps per block) or the explicit block inverses (HBM bound:
+  // 8 nb^2 bytes per block, all blocks in one grid).  Otherwise auto picks the inverse when its
+  // streaming time is the smaller one and it fits a quarter of the free device memory.
+  std::vector<int> pp;  // per block panel size (the oracle's BandFactor::build_panels rule)
+  bool panel_ok = F.n > 0 && !(F.kind == fpb::BandFactor::Kind::general && F.pivoted);
+  if (panel_ok) {
+    const bool spd = F.kind == fpb::BandFactor::Kind::spd;
+    const int ub = spd ? F.kl : F.ku;
+    const int nblk = int(F.block_start.size()) - 1;
+    pp.assign(size_t(nblk), 1);
+#pragma omp parallel for schedule(dynamic)
+    for (int blk = 0; blk < nblk; ++blk) {
+      int p = 1;
+      for (int j = F.block_start[blk]; j < F.block_start[blk + 1]; ++j) {
+        for (int r = 0; r < F.kl; ++r)
+          if (F.Lc[size_t(j) * F.kl + r] != 0.0) p = std::max(p, r + 1);
+        for (int r = 0; r < ub; ++r)
+          if ((spd ? F.Lr[size_t(j) * F.kl + r] : F.Uc[size_t(j) * F.ku + r]) != 0.0) p = std::max(p, r + 1);
+      }
+      pp[blk] = p;
+    }
+    for (int p : pp) panel_ok = panel_ok && p <= kPanelMax;
+  }
+  if (hp.factor_solve == 3 && !panel_ok)
+    throw std::invalid_argument("precond upload: factor_solve = panel needs a factor without row interchanges");
+  panel = hp.factor_solve == 3 || (hp.factor_solve == 0 && panel_ok);
+  if (panel) {
+    const int nblk = int(F.block_start.size()) - 1;
+    std::vector<long long> off(size_t(nblk) + 1, 0);
+    std::vector<int> tb, tq;
+    for (int blk = 0; blk < nblk; ++blk) {
+      const long long m = F.block_start[blk + 1] - F.block_start[blk], p = pp[blk], P = (m + p - 1) / p;
+      long long sz = 0;
+      for (long long q = 0; q < P; ++q) {
+        const long long st = std::min(p, m - q * p), sp = q > 0 ? p : 0, sn = q + 1 < P ? std::min(p, m - (q + 1) * p) : 0;
+        sz += st * st + st * sp + st * st + st * sn;
+        tb.push_back(blk), tq.push_back(int(q));
+      }
+      off[blk + 1] = off[blk] + sz;
+    }
+    pan_p.upload(pp);
+    pan_off.upload(off);
+    pan_m.alloc(size_t(off.back()));
+    pan_scratch.alloc(size_t(F.n));
+    pan_bytes = 8.0 * double(off.back());
+    pview = PanelView{nblk, band_start.get(), pan_p.get(), pan_off.get(), pan_m.get(),
+                      F.kind == fpb::BandFactor::Kind::spd ? band_diag.get() : nullptr, pan_scratch.get()};
+    DevBuf<int> dtb, dtq;
+    dtb.upload(tb), dtq.upload(tq);
+    const long long threads = (long long)tb.size() * 4 * kPanelMax;
+    panel_build_kernel<<<unsigned((threads + 127) / 128), 128>>>(band, pview, dtb.get(), dtq.get(), int(tb.size()),
+                                                                 pan_m.get());
+    cuda_check(cudaDeviceSynchronize(), "panel build");
+  }
+  if (!panel) {
     double inv_bytes = 0.0;
     for (size_t b = 0; b + 1 < F.block_start.size(); ++b) {
       const double nb = F.block_start[b + 1] - F.block_start[b];
@@ -761,9 +813,9 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
   }
   uclk.mark("H~ / factor");
   const size_t smem = sizeof(double) * (size_t(band_ring_doubles(kBandMaxQ)) + size_t(std::max(band_max_block, 1)));
-  if (!inverse && smem > 227 * 1024)
+  if (!inverse && !panel && smem > 227 * 1024)
     throw std::invalid_argument("precond upload: fracture block too large for the band solver");
-  if (!inverse && smem > 48 * 1024)
+  if (!inverse && !panel && smem > 48 * 1024)
     cuda_check(cudaFuncSetAttribute(band_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
                "band smem attribute");
   const int nu = s.n_u, nt = s.n_t, np = s.n_p;
@@ -777,6 +829,15 @@ void DevicePrecond::enqueue_band(const double* rhs, double rs, double* out, doub
   // algorithmic bytes: B_factor = 12 (nnz(L) + nnz(U)) + the diagonal (+ pivots) +
   // the vectors, in either mode; the explicit inverses' extra bytes are booked as waste
   const double vec_bytes = 8.0 * band.n * (2 + (mode == 1) + (mode == 2));
+  if (panel) {
+    launch(panel_solve_kernel, dim3(unsigned(pview.n_blocks) * kPanelCluster), dim3(kPanelThreads), 0, s,
+           "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
+    if (L) {
+      L->add(band_factor_bytes + vec_bytes + 8.0 * band.n);  // + z written and read back between the chains
+      L->waste(std::max(0.0, pan_bytes - band_factor_bytes));
+    }
+    return;
+  }
   if (inverse) {
     launch(dinv_kernel, dim3(blocks_for(size_t(band.n) * 32, kDinvThreads)), dim3(kDinvThreads), 0, s, "dinv_kernel", dinv, band.n, band.n_blocks,
                                                                                        rhs, rs, out, out2, sub, os, mode);

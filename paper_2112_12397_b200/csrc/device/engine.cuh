@@ -266,6 +266,13 @@ class DevicePrecond {
   int band_max_block = 0;
   // factor_solve = inverse: explicit block inverses streamed by dinv_kernel
   bool inverse = false;
+  // factor_solve = panel: block-bidiagonal panels, panel_solve_kernel
+  bool panel = false;
+  PanelView pview{};
+  DevBuf<int> pan_p;
+  DevBuf<long long> pan_off;
+  DevBuf<double> pan_m, pan_scratch;
+  double pan_bytes = 0;
   DinvView dinv{};
   DevBuf<double> dinv_v;
   DevBuf<long long> dinv_off;

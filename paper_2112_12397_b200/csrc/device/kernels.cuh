@@ -994,6 +994,138 @@ __global__ void __launch_bounds__(kDinvThreads) dinv_kernel(DinvView D, int n, i
   }
 }
 
+// ----------------------------------------------- panel (block-bidiagonal) solve
+// factor_solve = panel: one thread-block cluster of kPanelCluster CTAs per fracture
+// block.  The forward chain runs over the block's panels q = 0..P-1:
+//     y_q = H_q (rs b_q) - G_q y_q-1,
+// the backward chain over q = P-1..0:
+//     x_q = K_q z_q - F_q x_q+1      (z = y / D for LDL^T, else y),
+// one warp per row (rows of a panel dealt round-robin over the cluster's warps), each product summed
+// as 32 lane-strided partials + xor tree (the oracle's BandFactor::solve in this mode).  The new panel
+// (y_q or x_q) is written into every CTA's shared memory through distributed shared memory, then one
+// cluster barrier; the matrices stream from HBM once per apply (H, G forward; K, F backward) and
+// their loads do not depend on the chain, so they issue ahead of the barrier.
+constexpr int kPanelCluster = 8, kPanelThreads = 256, kPanelWarps = kPanelCluster * kPanelThreads / 32;
+
+__device__ __forceinline__ double warp_strided_dot(const double* row, const double* x, int len, double xs, int lane) {
+  double s = 0.0;
+  for (int c = lane; c < len; c += 32) s = s + row[c] * (x[c] * xs);
+#pragma unroll
+  for (int h = 16; h >= 1; h >>= 1) s = s + __shfl_xor_sync(0xffffffffu, s, h);
+  return s;
+}
+
+__global__ void __cluster_dims__(kPanelCluster, 1, 1) __launch_bounds__(kPanelThreads)
+    panel_solve_kernel(PanelView V, const double* rhs, double rs, double* out, double* out2, const double* sub,
+                       double os, int out_mode) {
+  pdl_entry();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ double chain[2][kPanelMax];  // the previous panel of the running chain (y or x)
+  const int rank = int(cluster.block_rank());
+  const int blk = blockIdx.x / kPanelCluster;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = rank * (kPanelThreads / 32) + warp;
+  const int b0 = V.block_start[blk], m = V.block_start[blk + 1] - b0, p = V.p[blk], P = (m + p - 1) / p;
+  const double* base = V.m + V.off[blk];
+  // forward chain
+  const double* pq = base;
+  for (int q = 0; q < P; ++q) {
+    const int s = min(p, m - q * p), sp = q > 0 ? p : 0, sn = q + 1 < P ? min(p, m - (q + 1) * p) : 0;
+    const double* H = pq;
+    const double* G = H + (long long)s * s;
+    pq = G + (long long)s * sp + (long long)s * s + (long long)s * sn;  // next panel (skip K, F)
+    for (int i = gw; i < s; i += kPanelWarps) {
+      const double sh = warp_strided_dot(H + (long long)i * s, rhs + b0 + q * p, s, rs, lane);
+      const double sg = sp ? warp_strided_dot(G + (long long)i * sp, chain[(q - 1) & 1], sp, 1.0, lane) : 0.0;
+      const double y = sp ? sh - sg : sh;
+      if (lane < kPanelCluster) *cluster.map_shared_rank(&chain[q & 1][i], lane) = y;
+      if (lane == 0) V.scratch[b0 + q * p + i] = V.diag ? y / V.diag[b0 + q * p + i] : y;
+    }
+    cluster.sync();
+  }
+  // backward chain
+  for (int q = P - 1; q >= 0; --q) {
+    const int s = min(p, m - q * p), sn = q + 1 < P ? min(p, m - (q + 1) * p) : 0;
+    // panel q's matrices: walk from the block start (panel sizes are p except the last)
+    long long o = 0;
+    for (int t = 0; t < q; ++t) {
+      const long long st = min(p, m - t * p), stp = t > 0 ? p : 0, stn = t + 1 < P ? min(p, m - (t + 1) * p) : 0;
+      o += st * st + st * stp + st * st + st * stn;
+    }
+    const double* K = base + o + (long long)s * s + (long long)s * (q > 0 ? p : 0);
+    const double* F = K + (long long)s * s;
+    for (int i = gw; i < s; i += kPanelWarps) {
+      const double sk = warp_strided_dot(K + (long long)i * s, V.scratch + b0 + q * p, s, 1.0, lane);
+      const double sf = sn ? warp_strided_dot(F + (long long)i * sn, chain[(q + 1) & 1], sn, 1.0, lane) : 0.0;
+      const double x = sn ? sk - sf : sk;
+      if (lane < kPanelCluster) *cluster.map_shared_rank(&chain[q & 1][i], lane) = x;
+      if (lane == 0) {
+        const long long r = b0 + (long long)q * p + i;
+        if (out_mode == 1)
+          out[r] = (sub[r] - x) * os;
+        else
+          out[r] = x;
+        if (out_mode == 2) out2[r] = x * os;
+      }
+    }
+    cluster.sync();
+  }
+}
+
+// Builds the panel matrices from the band factor (upload): one thread per (panel, column, matrix),
+// the column sweeps of the oracle's BandFactor::build_panels in the same order.
+__global__ void panel_build_kernel(BandView F, PanelView V, const int* task_blk, const int* task_q, int n_tasks,
+                                   double* pan) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long task = t / (4 * kPanelMax);
+  if (task >= n_tasks) return;
+  const int which = int((t / kPanelMax) % 4), c = int(t % kPanelMax);
+  const int blk = task_blk[task], q = task_q[task];
+  const int b0 = V.block_start[blk], m = V.block_start[blk + 1] - b0, p = V.p[blk], P = (m + p - 1) / p;
+  const int r0 = b0 + q * p, s = min(p, m - q * p), sp = q > 0 ? p : 0, sn = q + 1 < P ? min(p, m - (q + 1) * p) : 0;
+  const int cols = which == 1 ? sp : which == 3 ? sn : s;
+  if (c >= cols) return;
+  long long o = V.off[blk];
+  for (int u = 0; u < q; ++u) {
+    const long long su = min(p, m - u * p), sup = u > 0 ? p : 0, sun = u + 1 < P ? min(p, m - (u + 1) * p) : 0;
+    o += su * su + su * sup + su * su + su * sun;
+  }
+  double* M = pan + o + (which >= 1 ? (long long)s * s : 0) + (which >= 2 ? (long long)s * sp : 0) +
+              (which >= 3 ? (long long)s * s : 0);
+  auto Lv = [&](int gi, int gj) {
+    return gi > gj && gi - gj <= F.kl ? F.Lc[(long long)gj * F.kl + (gi - gj - 1)] : 0.0;
+  };
+  auto Uv = [&](int gi, int gj) {
+    if (!(gj > gi)) return 0.0;
+    if (F.spd) return gj - gi <= F.kl ? F.Lr[(long long)gj * F.kl + (gj - gi - 1)] : 0.0;
+    return gj - gi <= F.ku ? F.Uc[(long long)gj * F.ku + (gj - gi - 1)] : 0.0;
+  };
+  double z[kPanelMax];
+  for (int i = 0; i < s; ++i) z[i] = 0.0;
+  if (which == 0 || which == 2) z[c] = 1.0;
+  if (which == 1)
+    for (int i = 0; i < s; ++i) z[i] = Lv(r0 + i, r0 - sp + c);
+  if (which == 3)
+    for (int i = 0; i < s; ++i) z[i] = Uv(r0 + i, r0 + s + c);
+  if (which <= 1) {
+    for (int j = 0; j < s; ++j) {
+      const double zj = z[j];
+      for (int i = j + 1; i < s; ++i) z[i] -= Lv(r0 + i, r0 + j) * zj;
+    }
+  } else {
+    for (int j = s - 1; j >= 0; --j) {
+      double zj = z[j];
+      if (!F.spd) {
+        zj = zj / F.diag[r0 + j];
+        z[j] = zj;
+      }
+      for (int i = j - 1; i >= 0; --i) z[i] -= Uv(r0 + i, r0 + j) * zj;
+    }
+  }
+  for (int i = 0; i < s; ++i) M[(long long)i * cols + c] = z[i];
+}
+
 // ---------------------------------------------------- coarse dense solve
 // x = Q U^-1 L^-1 P b on the full-pivot LU (restated FullPivLU::solve), one CTA,
 // column sweeps.  LU is column-major so each step reads one contiguous column.

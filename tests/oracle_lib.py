@@ -44,6 +44,7 @@ def _load():
         "or_csr_copy": (C.c_int, [P, C.POINTER(C.c_int64), IP, DP]),
         "or_precond_build": (C.c_int, [P, C.c_int, C.c_int, DP, IP, DP, C.c_int, PP]),
         "or_precond_set_factor_solve": (C.c_int, [P, C.c_int]),
+        "or_precond_factor_pivots": (C.c_int, [P]),
         "or_precond_set_row_sum": (C.c_int, [P, C.c_int]),
         "or_precond_destroy": (None, [P]),
         "or_precond_apply": (C.c_int, [P, DP, DP]),
@@ -204,10 +205,15 @@ class OraclePrecond:
         self.row_sum = mode
 
     def set_factor_solve(self, mode: str) -> None:
-        """'sweep' (SparseFactor::solve) or 'inverse' (explicit block inverse, DESIGN.md §5b)."""
-        assert mode in ("sweep", "inverse"), mode
-        _check(lib.or_precond_set_factor_solve(self.h, 1 if mode == "inverse" else 0))
+        """'sweep' (SparseFactor::solve), 'inverse' (explicit block inverse, DESIGN.md §5b) or 'panel'
+        (block-bidiagonal panels; factors without row interchanges)."""
+        codes = {"sweep": 0, "inverse": 1, "panel": 2}
+        assert mode in codes, mode
+        _check(lib.or_precond_set_factor_solve(self.h, codes[mode]))
         self.factor_solve = mode
+
+    def factor_pivots(self) -> bool:
+        return bool(lib.or_precond_factor_pivots(self.h))
 
     def __del__(self):
         if getattr(self, "h", None):

@@ -185,6 +185,29 @@ def test_oracle_block_inverse_is_the_sweep_operator(variant):
     assert all(np.array_equal(opc.apply(x), r) for x, r in zip(xs, ref))
 
 
+@pytest.mark.parametrize("case", ["2frac", "config1"])
+@pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
+def test_oracle_panel_solve_is_the_sweep_operator(variant, case):
+    """factor_solve = panel: the block-bidiagonal panel form of the same banded factor
+    applies the sweeps' operator up to rounding (1e-12 relative, the apply bar)."""
+    if case == "config1":
+        J = api.Workload(1, 42).system()
+    else:
+        J = small_workload(seed=41, cells=(8, 6, 6), fracs=((0, 0.25, 0.0, 1.0, 0.0, 1.0), (0, 0.75, 0.0, 1.0, 0.5, 1.0)))
+    osys = oracle_system(J)
+    opc = O.OraclePrecond(osys, variant, coords=J.node_coords, strength_threshold=0.0)
+    assert not opc.factor_pivots()  # T (LDL^T) and the workloads' S~2 factor without interchanges
+    rng = np.random.default_rng(7)
+    xs = rng.uniform(-1, 1, (3, J.total_dimension()))
+    ref = [opc.apply(x) for x in xs]
+    opc.set_factor_solve("panel")
+    for x, r in zip(xs, ref):
+        y = opc.apply(x)
+        assert np.linalg.norm(y - r) <= 1e-12 * np.linalg.norm(r), np.linalg.norm(y - r) / np.linalg.norm(r)
+    opc.set_factor_solve("sweep")
+    assert all(np.array_equal(opc.apply(x), r) for x, r in zip(xs, ref))
+
+
 @pytest.mark.parametrize("theta", [0.08, 0.0])
 @pytest.mark.parametrize("variant", ["tpu", "tup", "tup_star"])
 def test_oracle_strided_row_sums_are_the_ordered_operator(variant, theta):

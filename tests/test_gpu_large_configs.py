@@ -67,7 +67,7 @@ def test_large_config_apply_bitwise_and_gmres_history(config, variant):
     log(f"config {config} {variant}: product setup done at {time.perf_counter() - t0:.0f} s")
     x = np.random.default_rng(4).uniform(-1, 1, n)
     xd = torch.tensor(x, device="cuda", dtype=torch.float64)
-    for factor_solve in ("sweep", "inverse"):
+    for factor_solve in ("sweep", "inverse", "panel"):
         opc.set_factor_solve(factor_solve)
         for row_sum in ("ordered", "strided"):
             pc = gpu_precond(hp, op, row_sum, factor_solve)
@@ -75,13 +75,13 @@ def test_large_config_apply_bitwise_and_gmres_history(config, variant):
             opc.set_row_sum(row_sum)
             y, ref = pc.apply(xd).cpu().numpy(), opc.apply(x)
             assert np.array_equal(y, ref), (factor_solve, row_sum, rel(y, ref))
-            if (factor_solve, row_sum) != ("inverse", "strided"):
+            if (factor_solve, row_sum) != ("panel", "strided"):
                 del pc
                 gc.collect()
     del hp
     gc.collect()
     log(f"config {config} {variant}: applies bitwise at {time.perf_counter() - t0:.0f} s")
-    # GMRES(50): the bench's solver (strided rows, CGS, inverse factor) against the oracle in the same
+    # GMRES(50): the bench's solver (strided rows, CGS, panel factor) against the oracle in the same
     # summation modes running the reference's MGS loop
     b = np.random.default_rng(42).uniform(-1, 1, n)
     _, st = api.gmres(op, pc, torch.tensor(b, device="cuda", dtype=torch.float64), tol=1e-10,
