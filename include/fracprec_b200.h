@@ -50,6 +50,7 @@ extern "C" {
 #define FP_SMOOTHER_JACOBI 0
 #define FP_SMOOTHER_SGS 1
 #define FP_SMOOTHER_CHEBYSHEV 2 /* extension: degree-k Chebyshev in D^-1 A (not in the reference) */
+#define FP_SMOOTHER_MCGS 3      /* extension: multicolour symmetric Gauss-Seidel (greedy colouring) */
 
 typedef struct fp_csr {
   int32_t n_rows, n_cols;
@@ -69,7 +70,7 @@ typedef struct fp_block_system {
 typedef struct fp_amg_config {
   double strength_threshold;
   int32_t max_coarse, pre_sweeps, post_sweeps;
-  int32_t smoother; /* the GPU path runs FP_SMOOTHER_JACOBI or FP_SMOOTHER_CHEBYSHEV */
+  int32_t smoother; /* the GPU path runs FP_SMOOTHER_JACOBI, _CHEBYSHEV or _MCGS */
   int32_t prolongation_smoothing;
   int32_t cycles_per_apply;
   double jacobi_omega, stall_ratio;

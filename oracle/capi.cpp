@@ -79,6 +79,7 @@ AmgConfig amg_cfg(const double* d, const int* i) {
     c.post_sweeps = i[2];
     c.smoother = i[3] == 0   ? AmgConfig::Smoother::weighted_jacobi
                  : i[3] == 2 ? AmgConfig::Smoother::chebyshev
+                 : i[3] == 3 ? AmgConfig::Smoother::mcgs
                              : AmgConfig::Smoother::sgs;
     c.prolongation_smoothing = i[4] != 0;
     c.cycles_per_apply = i[5];
@@ -180,7 +181,7 @@ int or_csr_copy(const void* m, int64_t* rp, int* ci, double* v) {
 // --------------------------------------------------------------- precond
 // variant 0 tpu, 1 tup, 2 tup_star; inner 0 amg, 1 direct.
 // amg_d = {strength_threshold, jacobi_omega, stall_ratio, chebyshev_ratio}
-// amg_i = {max_coarse, pre, post, smoother(0 jacobi,1 sgs,2 chebyshev), prolongation_smoothing, cycles, max_levels,
+// amg_i = {max_coarse, pre, post, smoother(0 jacobi,1 sgs,2 chebyshev,3 mcgs), prolongation_smoothing, cycles, max_levels,
 //          chebyshev_degree, power_iterations}
 int or_precond_build(void* s, int variant, int inner, const double* amg_d, const int* amg_i,
                      const double* coords, int n_nodes, void** out) {
@@ -306,6 +307,14 @@ int or_amg_level_aggregates(void* p, int l, int* out) {
   std::memcpy(out, L.fine_aggregate.data(), sizeof(int) * L.fine_aggregate.size());
   return int(L.fine_aggregate.size());
 }
+// mcgs (extension): colour count of a level, and its rows grouped by colour (color_rows / color_off)
+int or_amg_level_colors(void* p, int l, int* rows, int* off) {
+  const AmgLevel& L = static_cast<Pc*>(p)->amg().levels[l];
+  if (rows) std::copy(L.color_rows.begin(), L.color_rows.end(), rows);
+  if (off) std::copy(L.color_off.begin(), L.color_off.end(), off);
+  return int(L.color_off.size()) - 1;
+}
+
 int or_amg_apply(void* p, const double* r, double* x) {
   return guard([&] {
     const AmgHierarchy& h = static_cast<Pc*>(p)->amg();

@@ -260,7 +260,11 @@ struct AmgConfig {
   int max_coarse = 100;
   int pre_sweeps = 1, post_sweeps = 1;
   // chebyshev: EXTENSION (a non-goal of the reference), see amg.cpp
-  enum class Smoother { weighted_jacobi, sgs, chebyshev };
+  // mcgs: EXTENSION — multicolour symmetric Gauss-Seidel: the reference's SGS
+  // update (amg.cpp:115-134) with rows visited colour by colour (a greedy colouring in index order),
+  // forward colours then backward colours; rows of one colour never reference each other, so each
+  // colour is one parallel pass on the GPU.  A different operator from lexicographic SGS (amg.cpp).
+  enum class Smoother { weighted_jacobi, sgs, chebyshev, mcgs };
   Smoother smoother = Smoother::sgs;
   int chebyshev_degree = 2;        // polynomial degree per sweep
   double chebyshev_ratio = 10.0;   // lambda_min = lambda_max / ratio
@@ -284,7 +288,13 @@ struct AmgLevel {
   double lambda_max = 0.0;  // chebyshev: 1.1 x power-iteration estimate of rho(D^-1 A)
   std::vector<int> fine_aggregate;
   std::vector<int> aggregate_offsets;
+  // mcgs: rows grouped by colour (ascending inside a colour), colour c = color_rows[color_off[c] ..)
+  std::vector<int> color_rows, color_off;
 };
+// EXTENSION (mcgs): greedy colouring in index order of a structurally symmetric pattern — row i takes
+// the smallest colour not used by its already coloured neighbours (j < i in row i); returns the rows
+// grouped by colour
+void greedy_coloring(const CsrMatrix& A, std::vector<int>& rows, std::vector<int>& off);
 
 struct AmgHierarchy {
   std::vector<AmgLevel> levels;

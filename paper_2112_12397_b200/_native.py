@@ -17,7 +17,7 @@ LIB_PATH = os.environ.get("FRACPREC_B200_LIB") or os.path.join(_HERE, "_lib", "l
 FP_OK, FP_INVALID_ARGUMENT, FP_NUMERICAL_ERROR, FP_CUDA_ERROR, FP_INTERNAL_ERROR = 0, 1, 2, 3, 4
 FP_MEM_HOST, FP_MEM_DEVICE = 0, 1
 FP_TPU, FP_TUP, FP_TUP_STAR = 0, 1, 2
-FP_SMOOTHER_JACOBI, FP_SMOOTHER_SGS, FP_SMOOTHER_CHEBYSHEV = 0, 1, 2
+FP_SMOOTHER_JACOBI, FP_SMOOTHER_SGS, FP_SMOOTHER_CHEBYSHEV, FP_SMOOTHER_MCGS = 0, 1, 2, 3
 
 
 class NumericalError(RuntimeError):

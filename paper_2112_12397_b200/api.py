@@ -95,8 +95,9 @@ class AmgConfig:
     max_coarse: int = 100
     pre_sweeps: int = 1
     post_sweeps: int = 1
-    # "weighted_jacobi" (reference option), "sgs" (reference default; no GPU path) or
-    # "chebyshev" (extension: degree-k Chebyshev in D^-1 A, restated in the oracle)
+    # "weighted_jacobi" (reference option), "sgs" (reference default; no GPU path), or the extensions
+    # of SURVEY §8(f) item 4, both restated in the oracle: "chebyshev" (degree-k Chebyshev in D^-1 A)
+    # and "multicolor_gs" (symmetric Gauss-Seidel visiting rows colour by colour, greedy colouring)
     smoother: str = "weighted_jacobi"
     prolongation_smoothing: bool = True
     cycles_per_apply: int = 1
@@ -110,7 +111,7 @@ class AmgConfig:
     # as 32 lane-strided partials + xor tree, one warp per row; restated in the oracle)
     row_sum: str = "ordered"
 
-    _SMOOTHERS = {"weighted_jacobi": 0, "sgs": 1, "chebyshev": 2}
+    _SMOOTHERS = {"weighted_jacobi": 0, "sgs": 1, "chebyshev": 2, "multicolor_gs": 3}
     _ROW_SUMS = {"ordered": 0, "strided": 1}
 
     def native(self) -> N.FpAmgConfig:

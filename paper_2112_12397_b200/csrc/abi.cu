@@ -181,7 +181,7 @@ fpb::AmgOptions to_amg(const fp_amg_config& c) {
   o.power_iterations = c.power_iterations;
   o.row_sum = c.row_sum;
   need(o.row_sum == FP_ROW_SUM_ORDERED || o.row_sum == FP_ROW_SUM_STRIDED, "AmgConfig: unknown row_sum");
-  need(o.smoother >= 0 && o.smoother <= 2, "AmgConfig: unknown smoother");
+  need(o.smoother >= 0 && o.smoother <= 3, "AmgConfig: unknown smoother");
   need(o.smoother != 2 || (o.chebyshev_degree >= 1 && o.chebyshev_ratio > 1.0 && o.power_iterations >= 1),
        "AmgConfig: chebyshev needs degree >= 1, ratio > 1, power_iterations >= 1");
   return o;
@@ -471,6 +471,11 @@ int fp_precond_upload(fp_system* s, const fp_precond_desc* d, fp_precond** out) 
     }
     const fpb::Csr& Ac = hp.amg.levels.back().A;
     hp.amg.coarse.compute(Ac.to_dense(), Ac.n_rows);
+    if (hp.amg.opt.smoother == 3)  // multicolour GS (extension): the greedy colouring of the uploaded levels
+      for (size_t l = 0; l + 1 < hp.amg.levels.size(); ++l) {
+        fpb::HostLevel& L = hp.amg.levels[l];
+        fpb::color_rows(L.A.n_rows, L.A.rp.data(), L.A.ci.data(), L.color_rows, L.color_off);
+      }
     if (hp.amg.opt.smoother == 2)  // Chebyshev (extension): the oracle's lambda estimate on the uploaded levels
       for (size_t l = 0; l + 1 < hp.amg.levels.size(); ++l)
         hp.amg.levels[l].lambda_max =

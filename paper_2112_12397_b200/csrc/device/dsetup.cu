@@ -573,6 +573,11 @@ fpb::HostAmg amg_setup_dev(DCsr&& A0, const std::vector<std::vector<double>>& ne
     h.coarse.compute(c.A.to_dense(), c.A.n_rows);
   }
   clk.mark("coarse LU", h.levels.back().A.n_rows);
+  if (opt.smoother == 3)  // multicolour GS (extension): the colouring on the downloaded patterns
+    for (size_t l = 0; l + 1 < h.levels.size(); ++l) {
+      const fpb::Csr Al = download_csr(h.levels[l].dA->m);
+      fpb::color_rows(Al.n_rows, Al.rp.data(), Al.ci.data(), h.levels[l].color_rows, h.levels[l].color_off);
+    }
   if (opt.smoother == 2)  // Chebyshev (extension): the host estimate (index-order sums) on downloaded levels
     for (size_t l = 0; l + 1 < h.levels.size(); ++l) {
       const fpb::Csr Al = download_csr(h.levels[l].dA->m);

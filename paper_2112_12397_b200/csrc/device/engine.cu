@@ -323,10 +323,10 @@ DMat mat_from_ref(const DCsr& A, bool few_rows_parallel, bool strided) {
 
 DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
   opt = h.opt;
-  if (opt.smoother != 0 && opt.smoother != 2)
+  if (opt.smoother != 0 && opt.smoother != 2 && opt.smoother != 3)
     throw std::invalid_argument(
-        "GPU AMG requires smoother = weighted_jacobi or chebyshev (the reference's symmetric Gauss-Seidel is "
-        "sequential; see DESIGN.md)");
+        "GPU AMG requires smoother = weighted_jacobi, chebyshev or multicolor_gs (the reference's lexicographic "
+        "symmetric Gauss-Seidel is sequential; see DESIGN.md)");
   const int L = int(h.levels.size());
   lv.resize(static_cast<size_t>(L));
   // build sources: each level's A (l < L - 1) and P (l >= 1) as device CSR — the device setup's own
@@ -367,6 +367,11 @@ DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
         D.P.bp3 = D.P.bp.n_nodes > 0;
       }
       if (!D.P.bp3) D.P = mat_from_ref(P, false, false);
+    }
+    if (opt.smoother == 3 && l + 1 < L) {  // multicolour GS: CSR copy of the level, colour lists
+      D.gs = clone_csr(*src_A_[l]);
+      D.color_rows.upload(H.color_rows);
+      D.color_off = H.color_off;
     }
     D.d.upload(H.diag);
     D.b.alloc(D.n), D.x.alloc(D.n), D.xt.alloc(D.n), D.xt2.alloc(D.n), D.xt3.alloc(D.n), D.r.alloc(D.n);
@@ -516,6 +521,10 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
     vcycle_chebyshev(l, b, x, sub_from, s, Lg);
     return;
   }
+  if (opt.smoother == 3) {
+    vcycle_mcgs(l, b, x, sub_from, s, Lg);
+    return;
+  }
   // First Jacobi sweep from x = 0 is x = (w b)/d exactly (A 0 = 0, amg.cpp:138-139); it was
   // written by the kernel that produced b (or by presmooth_kernel for an external input).
   if (!xhat) {
@@ -639,6 +648,45 @@ void DeviceAmg::vcycle_chebyshev(int l, const double* b, double* x, const double
     }
 }
 
+// V-cycle with the multicolour symmetric Gauss-Seidel smoother (extension; the oracle's mcgs_sweep):
+// x = 0, pre-sweeps (colours ascending then descending), r = b - A x, restrict, coarse correction,
+// post-sweeps; one launch per colour and direction
+void DeviceAmg::vcycle_mcgs(int l, const double* b, double* x, const double* sub_from, cudaStream_t s, Ledger* Lg) {
+  DeviceLevel& L = lv[l];
+  const int last = n_levels() - 1;
+  const double nd = L.n;
+  double* cur = sub_from ? L.xt2.get() : x;
+  const int nc = int(L.color_off.size()) - 1;
+  const CsrView A{L.gs.n_rows, L.gs.rp.get(), L.gs.ci.get(), L.gs.v.get()};
+  auto sweep = [&]() {
+    for (int pass = 0; pass < 2; ++pass)
+      for (int k = 0; k < nc; ++k) {
+        const int c = pass == 0 ? k : nc - 1 - k;
+        const int r0 = L.color_off[c], m = L.color_off[c + 1] - r0;
+        if (m == 0) continue;
+        launch(mcgs_color_kernel, dim3(blocks_for(m, 128)), dim3(128), 0, s, "mcgs_color_kernel", A,
+               L.color_rows.get() + r0, m, b, L.d.get(), cur);
+      }
+    if (Lg) Lg->add(2.0 * (L.gs.matrix_bytes() + 24.0 * nd));
+  };
+  cuda_check(cudaMemsetAsync(cur, 0, sizeof(double) * size_t(L.n), s), "x = 0");
+  for (int it = 0; it < opt.pre_sweeps; ++it) sweep();
+  launch_level(L, GPlain{cur}, EResid{b, L.r.get()}, s);  // r = b - A x
+  if (Lg) Lg->add(L.a_bytes() + 24.0 * nd);
+  DeviceLevel& C = lv[l + 1];
+  launch_mat(C.R, GPlain{L.r.get()}, EStore{C.b.get()}, s);  // r_c = P^T r  (amg.cpp:166)
+  if (Lg) Lg->add(C.R.matrix_bytes() + 8.0 * nd + 8.0 * C.n);
+  vcycle(l + 1, C.b.get(), C.x.get(), nullptr, nullptr, s, Lg);
+  launch_mat(C.P, GPlain{C.x.get()}, EAddTo{cur, cur}, s);  // x += P e_c  (amg.cpp:168-169)
+  if (Lg) Lg->add(C.P.matrix_bytes() + 8.0 * C.n + 16.0 * nd);
+  for (int it = 0; it < opt.post_sweeps; ++it) sweep();
+  if (sub_from) {
+    launch(axpy_kernel, dim3(blocks_for(L.n, 256)), dim3(256), 0, s, "axpy_kernel", L.n, sub_from, cur, -1.0, x);
+    if (Lg) Lg->add(24.0 * nd);
+  }
+  (void)last;
+}
+
 void DeviceAmg::enqueue_apply(const double* r, double* x, const double* sub_from, cudaStream_t s, Ledger* Lg,
                               double* xhat, bool sparse_rhs) {
   if (n_levels() == 1) xhat = nullptr;  // single level: direct coarse solve, no smoothing
@@ -756,7 +804,19 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
   }
   if (hp.factor_solve == 3 && !panel_ok)
     throw std::invalid_argument("precond upload: factor_solve = panel needs a factor without row interchanges");
-  panel = hp.factor_solve == 3 || (hp.factor_solve == 0 && panel_ok);
+  double inv_bytes = 0.0;  // explicit block inverses: 8 nb^2 per block
+  for (size_t b = 0; b + 1 < F.block_start.size(); ++b) {
+    const double nb = F.block_start[b + 1] - F.block_start[b];
+    inv_bytes += 8.0 * nb * nb;
+  }
+  {  // auto: panels when their two chains (~1.5 us per cluster step) beat streaming the inverses
+    int chain = 0;
+    for (size_t b = 0; b < pp.size(); ++b)
+      chain = std::max(chain, (F.block_start[b + 1] - F.block_start[b] + pp[b] - 1) / pp[b]);
+    const double t_panel = 2.0 * chain * 1.5e-6 + 1.4 * band_factor_bytes / 5.0e12;
+    const double t_inv = inv_bytes / 5.0e12 + 5e-6;
+    panel = hp.factor_solve == 3 || (hp.factor_solve == 0 && panel_ok && t_panel < t_inv);
+  }
   if (panel) {
     const int nblk = int(F.block_start.size()) - 1;
     std::vector<long long> off(size_t(nblk) + 1, 0);
@@ -786,11 +846,6 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
     cuda_check(cudaDeviceSynchronize(), "panel build");
   }
   if (!panel) {
-    double inv_bytes = 0.0;
-    for (size_t b = 0; b + 1 < F.block_start.size(); ++b) {
-      const double nb = F.block_start[b + 1] - F.block_start[b];
-      inv_bytes += 8.0 * nb * nb;
-    }
     size_t free_b = 0, total_b = 0;
     cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
     const bool fits = inv_bytes <= 0.25 * double(free_b);

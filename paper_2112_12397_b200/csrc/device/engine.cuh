@@ -196,6 +196,10 @@ struct DeviceLevel {
   double cheb_theta = 0.0;
   std::vector<double> cheb_c1, cheb_c2;
   DevBuf<double> cd;
+  // multicolour Gauss-Seidel smoother (extension): the level operator as CSR, rows grouped by colour
+  DCsr gs;
+  DevBuf<int> color_rows;
+  std::vector<int> color_off;
   int n = 0;
   double a_bytes() const { return bsr3 ? Ab.matrix_bytes() : Am.matrix_bytes(); }
 };
@@ -250,6 +254,7 @@ class DeviceAmg {
 
  private:
   void vcycle_chebyshev(int l, const double* b, double* x, const double* sub_from, cudaStream_t s, Ledger* L);
+  void vcycle_mcgs(int l, const double* b, double* x, const double* sub_from, cudaStream_t s, Ledger* L);
 };
 
 class DevicePrecond {

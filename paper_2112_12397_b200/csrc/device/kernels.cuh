@@ -994,6 +994,24 @@ __global__ void __launch_bounds__(kDinvThreads) dinv_kernel(DinvView D, int n, i
   }
 }
 
+// ------------------------------------- multicolour Gauss-Seidel (extension)
+// One colour of the multicolour symmetric Gauss-Seidel smoother: rows of a colour never reference
+// each other, so each row of the colour is updated by one thread exactly as the reference's SGS row
+// update (amg.cpp:118-122): s = b_i - sum_{j != i} a_ij x_j (left to right), x_i = s / d_i.
+__global__ void mcgs_color_kernel(CsrView A, const int* rows, int n_rows, const double* b, const double* d,
+                                  double* x) {
+  pdl_entry();
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= n_rows) return;
+  const int i = rows[t];
+  double s = b[i];
+  for (long long k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+    const int j = A.ci[k];
+    if (j != i) s -= A.v[k] * x[j];
+  }
+  x[i] = s / d[i];
+}
+
 // ----------------------------------------------- panel (block-bidiagonal) solve
 // factor_solve = panel: one thread-block cluster of kPanelCluster CTAs per fracture
 // block.  The forward chain runs over the block's panels q = 0..P-1:
@@ -1006,71 +1024,105 @@ __global__ void __launch_bounds__(kDinvThreads) dinv_kernel(DinvView D, int n, i
 // cluster barrier; the matrices stream from HBM once per apply (H, G forward; K, F backward) and
 // their loads do not depend on the chain, so they issue ahead of the barrier.
 constexpr int kPanelCluster = 8, kPanelThreads = 256, kPanelWarps = kPanelCluster * kPanelThreads / 32;
+constexpr int kPanelRows = (kPanelMax + kPanelWarps - 1) / kPanelWarps;  // rows of a panel per warp
+constexpr int kPanelEl = kPanelMax / 32;                                 // entries of a row per lane
 
-__device__ __forceinline__ double warp_strided_dot(const double* row, const double* x, int len, double xs, int lane) {
-  double s = 0.0;
-  for (int c = lane; c < len; c += 32) s = s + row[c] * (x[c] * xs);
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ double warp_tree(double s) {
 #pragma unroll
   for (int h = 16; h >= 1; h >>= 1) s = s + __shfl_xor_sync(0xffffffffu, s, h);
   return s;
+}
+
+// one chain (forward: D = H, C = G, x = rs b; backward: D = K, C = F, x = z) over the block's panels;
+// before each cluster barrier a warp already loads the next panel's coupling rows into registers and
+// forms its local product, so a step's critical path is the barrier plus a shared-memory dot
+template <bool fwd>
+__device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw, int lane, double (*chain)[kPanelMax],
+                                            const double* xin, double xs, double* out, double* out2, const double* sub,
+                                            double os, int out_mode, cooperative_groups::cluster_group& cluster) {
+  const int b0 = V.block_start[blk], m = V.block_start[blk + 1] - b0, p = V.p[blk], P = (m + p - 1) / p;
+  auto rows_of = [&](int q) { return min(p, m - q * p); };
+  auto panel_size = [&](int q) {
+    const long long s = rows_of(q), sp = q > 0 ? p : 0, sn = q + 1 < P ? rows_of(q + 1) : 0;
+    return s * s + s * sp + s * s + s * sn;
+  };
+  double dl[kPanelRows], cr[kPanelRows][kPanelEl];
+  // panel q's local product D_q x_q and coupling rows C_q, for this warp's rows
+  auto prefetch = [&](int q, long long o) {
+    const int s = rows_of(q), sc = fwd ? (q > 0 ? p : 0) : (q + 1 < P ? rows_of(q + 1) : 0);
+    const double* Dm = V.m + o + (fwd ? 0 : (long long)s * s + (long long)s * (q > 0 ? p : 0));
+    const double* Cm = fwd ? Dm + (long long)s * s : Dm + (long long)s * s;
+    const double* xq = xin + b0 + (long long)q * p;
+#pragma unroll
+    for (int r = 0; r < kPanelRows; ++r) {
+      const int i = gw + r * kPanelWarps;
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < kPanelEl; ++e) {
+        const int c = lane + 32 * e;
+        if (i < s && c < s) acc = acc + Dm[(long long)i * s + c] * (xq[c] * xs);
+        cr[r][e] = (i < s && c < sc) ? Cm[(long long)i * sc + c] : 0.0;
+      }
+      dl[r] = warp_tree(acc);
+    }
+  };
+  long long o = V.off[blk];
+  int q = fwd ? 0 : P - 1;
+  if (!fwd)
+    for (int t = 0; t < P - 1; ++t) o += panel_size(t);
+  prefetch(q, o);
+  for (int step = 0; step < P; ++step, q += fwd ? 1 : -1) {
+    const int s = rows_of(q), sc = fwd ? (q > 0 ? p : 0) : (q + 1 < P ? rows_of(q + 1) : 0);
+    const double* prev = chain[(q + (fwd ? -1 : 1)) & 1];
+#pragma unroll
+    for (int r = 0; r < kPanelRows; ++r) {
+      const int i = gw + r * kPanelWarps;
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < kPanelEl; ++e)
+        if (lane + 32 * e < sc) acc = acc + cr[r][e] * prev[lane + 32 * e];
+      acc = warp_tree(acc);
+      if (i < s) {
+        const double v = sc ? dl[r] - acc : dl[r];
+        if (lane < kPanelCluster) *cluster.map_shared_rank(&chain[q & 1][i], lane) = v;
+        if (lane == 0) {
+          const long long row = b0 + (long long)q * p + i;
+          if (fwd) {
+            V.scratch[row] = V.diag ? v / V.diag[row] : v;  // z = y / D (LDL^T), else y
+          } else if (out_mode == 1) {
+            out[row] = (sub[row] - v) * os;
+          } else {
+            out[row] = v;
+            if (out_mode == 2) out2[row] = v * os;
+          }
+        }
+      }
+    }
+    cluster_arrive();
+    const int qn = q + (fwd ? 1 : -1);
+    if (fwd ? qn < P : qn >= 0) {
+      o += fwd ? panel_size(q) : -panel_size(qn);
+      prefetch(qn, o);
+    }
+    cluster_wait();
+  }
 }
 
 __global__ void __cluster_dims__(kPanelCluster, 1, 1) __launch_bounds__(kPanelThreads)
     panel_solve_kernel(PanelView V, const double* rhs, double rs, double* out, double* out2, const double* sub,
                        double os, int out_mode) {
   pdl_entry();
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
+  cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
   __shared__ double chain[2][kPanelMax];  // the previous panel of the running chain (y or x)
   const int rank = int(cluster.block_rank());
   const int blk = blockIdx.x / kPanelCluster;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = rank * (kPanelThreads / 32) + warp;
-  const int b0 = V.block_start[blk], m = V.block_start[blk + 1] - b0, p = V.p[blk], P = (m + p - 1) / p;
-  const double* base = V.m + V.off[blk];
-  // forward chain
-  const double* pq = base;
-  for (int q = 0; q < P; ++q) {
-    const int s = min(p, m - q * p), sp = q > 0 ? p : 0, sn = q + 1 < P ? min(p, m - (q + 1) * p) : 0;
-    const double* H = pq;
-    const double* G = H + (long long)s * s;
-    pq = G + (long long)s * sp + (long long)s * s + (long long)s * sn;  // next panel (skip K, F)
-    for (int i = gw; i < s; i += kPanelWarps) {
-      const double sh = warp_strided_dot(H + (long long)i * s, rhs + b0 + q * p, s, rs, lane);
-      const double sg = sp ? warp_strided_dot(G + (long long)i * sp, chain[(q - 1) & 1], sp, 1.0, lane) : 0.0;
-      const double y = sp ? sh - sg : sh;
-      if (lane < kPanelCluster) *cluster.map_shared_rank(&chain[q & 1][i], lane) = y;
-      if (lane == 0) V.scratch[b0 + q * p + i] = V.diag ? y / V.diag[b0 + q * p + i] : y;
-    }
-    cluster.sync();
-  }
-  // backward chain
-  for (int q = P - 1; q >= 0; --q) {
-    const int s = min(p, m - q * p), sn = q + 1 < P ? min(p, m - (q + 1) * p) : 0;
-    // panel q's matrices: walk from the block start (panel sizes are p except the last)
-    long long o = 0;
-    for (int t = 0; t < q; ++t) {
-      const long long st = min(p, m - t * p), stp = t > 0 ? p : 0, stn = t + 1 < P ? min(p, m - (t + 1) * p) : 0;
-      o += st * st + st * stp + st * st + st * stn;
-    }
-    const double* K = base + o + (long long)s * s + (long long)s * (q > 0 ? p : 0);
-    const double* F = K + (long long)s * s;
-    for (int i = gw; i < s; i += kPanelWarps) {
-      const double sk = warp_strided_dot(K + (long long)i * s, V.scratch + b0 + q * p, s, 1.0, lane);
-      const double sf = sn ? warp_strided_dot(F + (long long)i * sn, chain[(q + 1) & 1], sn, 1.0, lane) : 0.0;
-      const double x = sn ? sk - sf : sk;
-      if (lane < kPanelCluster) *cluster.map_shared_rank(&chain[q & 1][i], lane) = x;
-      if (lane == 0) {
-        const long long r = b0 + (long long)q * p + i;
-        if (out_mode == 1)
-          out[r] = (sub[r] - x) * os;
-        else
-          out[r] = x;
-        if (out_mode == 2) out2[r] = x * os;
-      }
-    }
-    cluster.sync();
-  }
+  panel_chain<true>(V, blk, gw, lane, chain, rhs, rs, nullptr, nullptr, nullptr, 1.0, 0, cluster);
+  panel_chain<false>(V, blk, gw, lane, chain, V.scratch, 1.0, out, out2, sub, os, out_mode, cluster);
 }
 
 // Builds the panel matrices from the band factor (upload): one thread per (panel, column, matrix),

@@ -333,7 +333,39 @@ HostAmg amg_setup(Csr A, const std::vector<std::vector<double>>& near_null, cons
       h.levels[l].lambda_max = chebyshev_lambda_max(h.levels[l].A, h.levels[l].diag, opt.power_iterations);
     plog.mark("chebyshev lambda_max");
   }
+  if (opt.smoother == 3)
+    for (size_t l = 0; l + 1 < h.levels.size(); ++l) {
+      const Csr& A = h.levels[l].A;
+      color_rows(A.n_rows, A.rp.data(), A.ci.data(), h.levels[l].color_rows, h.levels[l].color_off);
+    }
   return h;
+}
+
+void color_rows(int n, const int64_t* rp, const int* ci, std::vector<int>& rows, std::vector<int>& off) {
+  std::vector<int> color(static_cast<size_t>(n), -1);
+  std::vector<int> seen;  // seen[c] == i: colour c is taken by a neighbour of row i
+  int n_colors = 0;
+  for (int i = 0; i < n; ++i) {
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const int j = ci[k];
+      if (j < i) seen[size_t(color[j])] = i;  // earlier rows are coloured
+    }
+    int c = 0;
+    while (c < n_colors && seen[size_t(c)] == i) ++c;
+    color[i] = c;
+    if (c == n_colors) ++n_colors, seen.push_back(-1);
+  }
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+  for (int i = 0; i < n; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) bad |= ci[k] != i && color[ci[k]] == color[i];
+  if (bad) throw std::invalid_argument("mcgs: the level operator's pattern is not structurally symmetric");
+  off.assign(static_cast<size_t>(n_colors) + 1, 0);
+  for (int i = 0; i < n; ++i) ++off[size_t(color[i]) + 1];
+  for (int c = 0; c < n_colors; ++c) off[size_t(c) + 1] += off[c];
+  rows.resize(static_cast<size_t>(n));
+  std::vector<int> next(off.begin(), off.end() - 1);
+  for (int i = 0; i < n; ++i) rows[size_t(next[size_t(color[i])]++)] = i;
 }
 
 double chebyshev_lambda_max(const Csr& A, const std::vector<double>& diag, int iterations) {

@@ -19,7 +19,8 @@ struct AmgOptions {
   int max_coarse = 100;
   int pre_sweeps = 1, post_sweeps = 1;
   int smoother = 0;  // 0 weighted Jacobi (GPU path), 1 symmetric Gauss-Seidel (reference default),
-                     // 2 Chebyshev (extension; restated in oracle/amg.cpp)
+                     // 2 Chebyshev, 3 multicolour symmetric Gauss-Seidel (extensions, SURVEY §8(f)
+                     // item 4; restated in oracle/amg.cpp)
   int chebyshev_degree = 2;
   double chebyshev_ratio = 10.0;
   int power_iterations = 10;
@@ -47,6 +48,7 @@ struct HostLevel {
   double lambda_max = 0.0;     // chebyshev: 1.1 x power-iteration estimate of rho(D^-1 A)
   std::vector<int> aggregate;  // fine row -> aggregate id (coarse levels only)
   std::vector<int> aggregate_offsets;
+  std::vector<int> color_rows, color_off;  // smoother 3: rows grouped by colour (ascending in a colour)
 };
 
 struct HostAmg {
@@ -71,6 +73,11 @@ struct ChebyshevCoefficients {
   std::vector<double> c1, c2;
 };
 ChebyshevCoefficients chebyshev_coefficients(double lambda_max, double ratio, int degree);
+
+// Multicolour smoother (extension): the greedy colouring in row order of a structurally symmetric
+// pattern (each row takes the smallest colour none of its earlier neighbours has), rows grouped by
+// colour — the oracle's greedy_coloring (oracle/amg.cpp) rule
+void color_rows(int n, const int64_t* rp, const int* ci, std::vector<int>& rows, std::vector<int>& off);
 
 // A is taken by value and moved into level 0 (callers std::move the inner operator in)
 HostAmg amg_setup(Csr A, const std::vector<std::vector<double>>& near_null, const AmgOptions& opt);

@@ -58,6 +58,7 @@ def _load():
         "or_amg_level_lambda": (C.c_double, [P, C.c_int]),
         "or_amg_level_aggregates": (C.c_int, [P, C.c_int, IP]),
         "or_amg_apply": (C.c_int, [P, DP, DP]),
+        "or_amg_level_colors": (C.c_int, [P, C.c_int, IP, IP]),
         "or_gmres": (C.c_int, [P, P, DP, C.c_double, C.c_int, C.c_int, C.c_int, DP, IP, DP, C.c_int, DP]),
         "or_block_scaling": (C.c_int, [P, DP]),
         "or_mm_read": (C.c_int, [C.c_char_p, PP]),
@@ -263,6 +264,15 @@ class OraclePrecond:
         out = np.zeros(self.sys.n_p)
         lib.or_precond_vec(self.h, 0, _dp(out))
         return out
+
+    def level_colors(self, level: int) -> tuple:
+        """mcgs (extension): (rows grouped by colour, colour offsets) of a level."""
+        nc = lib.or_amg_level_colors(self.h, level, None, None)
+        n = self.level_matrix(level, 0)[0]
+        rows, off = np.zeros(n, np.int32), np.zeros(nc + 1, np.int32)
+        lib.or_amg_level_colors(self.h, level, rows.ctypes.data_as(C.POINTER(C.c_int)),
+                                off.ctypes.data_as(C.POINTER(C.c_int)))
+        return rows, off
 
     def amg_apply(self, r: np.ndarray) -> np.ndarray:
         r = np.ascontiguousarray(r, np.float64)

@@ -288,3 +288,28 @@ def test_oracle_chebyshev_vcycle_contracts():
         B = np.column_stack([opc.amg_apply(e) for e in np.eye(r)])  # B ~ A^-1
         rho[sm] = max(abs(np.linalg.eigvals(np.eye(r) - B @ A)))
     assert rho[2] < 0.6 and rho[2] < rho[0], rho  # measured: 0.49 vs 1.06
+
+
+def test_oracle_multicolor_gs_vcycle_contracts():
+    """The multicolour symmetric Gauss-Seidel smoother (extension): rows of one
+    colour never couple, and its V-cycle contracts like the reference's lexicographic SGS (and better
+    than weighted Jacobi) on the inner operator."""
+    J = small_workload(seed=44)
+    osys = oracle_system(J)
+    rho = {}
+    for sm in (0, 1, 3):  # weighted Jacobi, lexicographic SGS (reference default), multicolour SGS
+        opc = O.OraclePrecond(osys, "tup", coords=J.node_coords, smoother=sm)
+        r, c, rp, ci, v = opc.level_matrix(0, 0)
+        A = np.zeros((r, c))
+        A[np.repeat(np.arange(r), np.diff(rp)), ci] = v
+        if sm == 3:
+            rows, off = opc.level_colors(0)
+            color = np.empty(r, np.int64)
+            for k in range(len(off) - 1):
+                color[rows[off[k]:off[k + 1]]] = k
+            row_of = np.repeat(np.arange(r), np.diff(rp))
+            off_diag = row_of != ci
+            assert not np.any(color[row_of[off_diag]] == color[ci[off_diag]])
+        B = np.column_stack([opc.amg_apply(e) for e in np.eye(r)])  # B ~ A^-1
+        rho[sm] = max(abs(np.linalg.eigvals(np.eye(r) - B @ A)))
+    assert rho[3] < 0.5 and rho[3] < rho[0], rho

@@ -73,3 +73,42 @@ def test_config2_apply_bitwise_and_gmres_history(variant):
     assert st.iterations == st_ref["iterations"] == 60
     h, hr = np.array(st.relative_residuals), st_ref["history"]
     assert np.allclose(h, hr, rtol=1e-6, atol=0), np.max(np.abs(h / hr - 1))
+
+
+def test_config2_full_gmres_converges_to_the_oracle_solution():
+    """The reference's own GMRES semantics (full, unrestarted: gmres.cpp:24-174) on the bench's
+    workload: it converges, so the solution-level bars apply — the bench's solver
+    (strided rows, CGS, its factor application) against the oracle in the same summation modes running
+    the reference's MGS loop: iteration count within +-2, solution within 1e-8 at rtol 1e-10."""
+    J, osys, op, pc, opc = setup(2, "tup", "strided")
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    O.set_chunked_reductions(True)
+    try:
+        x_ref, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=500, max_iter=500, scaled=True)
+    finally:
+        O.set_chunked_reductions(False)
+    xs, st = api.gmres(op, pc, torch.tensor(b, device="cuda", dtype=torch.float64), tol=1e-10, max_iter=500,
+                       restart=500, scaled=True, orthogonalization="cgs")
+    assert st_ref["converged"] and st.converged, (st_ref["iterations"], st.iterations)
+    assert abs(st.iterations - st_ref["iterations"]) <= 2, (st.iterations, st_ref["iterations"])
+    assert rel(xs.cpu().numpy(), x_ref) <= 1e-8
+
+
+def test_config2_bench_solver_500_steps_tracks_the_reference_order_oracle():
+    """All 500 GMRES(50) steps of the bench's solver (strided rows, CGS, its factor application) against
+    the oracle in the reference's own orders (ordered rows, MGS, banded sweeps): both stop at max_iter
+    (the solve stagnates) and the residual histories agree step by step to 1e-6 relative
+    over the first 100 steps and to 1e-3 over all 500."""
+    J, osys, op, pc, opc = setup(2, "tup", "strided")
+    opc.set_row_sum("ordered")
+    opc.set_factor_solve("sweep")
+    b = np.random.default_rng(42).uniform(-1, 1, J.total_dimension())
+    _, st_ref = O.oracle_gmres(osys, opc, b, tol=1e-10, restart=50, max_iter=500, scaled=True)
+    _, st = api.gmres(op, pc, torch.tensor(b, device="cuda", dtype=torch.float64), tol=1e-10, max_iter=500,
+                      restart=50, scaled=True, orthogonalization="cgs")
+    assert st.converged == st_ref["converged"]
+    assert abs(st.iterations - st_ref["iterations"]) <= 2, (st.iterations, st_ref["iterations"])
+    k = min(len(st.relative_residuals), len(st_ref["history"]))
+    h, hr = np.array(st.relative_residuals[:k]), st_ref["history"][:k]
+    assert np.allclose(h[:100], hr[:100], rtol=1e-6, atol=0), np.max(np.abs(h[:100] / hr[:100] - 1))
+    assert np.allclose(h, hr, rtol=1e-3, atol=0), np.max(np.abs(h / hr - 1))
