@@ -833,6 +833,7 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
     }
     pan_p.upload(pp);
     pan_off.upload(off);
+    pan_pmax = *std::max_element(pp.begin(), pp.end());
     pan_m.alloc(size_t(off.back()));
     pan_scratch.alloc(size_t(F.n));
     pan_bytes = 8.0 * double(off.back());
@@ -885,8 +886,13 @@ void DevicePrecond::enqueue_band(const double* rhs, double rs, double* out, doub
   // the vectors, in either mode; the explicit inverses' extra bytes are booked as waste
   const double vec_bytes = 8.0 * band.n * (2 + (mode == 1) + (mode == 2));
   if (panel) {
-    launch(panel_solve_kernel, dim3(unsigned(pview.n_blocks) * kPanelCluster), dim3(kPanelThreads), 0, s,
-           "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
+    const dim3 g(unsigned(pview.n_blocks) * kPanelCluster), b(kPanelThreads);
+    if (pan_pmax <= 64)
+      launch(panel_solve_kernel<1, 2>, g, b, 0, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
+    else if (pan_pmax <= 128)
+      launch(panel_solve_kernel<2, 4>, g, b, 0, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
+    else
+      launch(panel_solve_kernel<4, 8>, g, b, 0, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
     if (L) {
       L->add(band_factor_bytes + vec_bytes + 8.0 * band.n);  // + z written and read back between the chains
       L->waste(std::max(0.0, pan_bytes - band_factor_bytes));

@@ -278,6 +278,7 @@ class DevicePrecond {
   DevBuf<long long> pan_off;
   DevBuf<double> pan_m, pan_scratch;
   double pan_bytes = 0;
+  int pan_pmax = 0;
   DinvView dinv{};
   DevBuf<double> dinv_v;
   DevBuf<long long> dinv_off;

@@ -1024,9 +1024,6 @@ __global__ void mcgs_color_kernel(CsrView A, const int* rows, int n_rows, const 
 // cluster barrier; the matrices stream from HBM once per apply (H, G forward; K, F backward) and
 // their loads do not depend on the chain, so they issue ahead of the barrier.
 constexpr int kPanelCluster = 8, kPanelThreads = 256, kPanelWarps = kPanelCluster * kPanelThreads / 32;
-constexpr int kPanelRows = (kPanelMax + kPanelWarps - 1) / kPanelWarps;  // rows of a panel per warp
-constexpr int kPanelEl = kPanelMax / 32;                                 // entries of a row per lane
-
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
@@ -1038,38 +1035,42 @@ __device__ __forceinline__ double warp_tree(double s) {
 
 // one chain (forward: D = H, C = G, x = rs b; backward: D = K, C = F, x = z) over the block's panels;
 // before each cluster barrier a warp already loads the next panel's coupling rows into registers and
-// forms its local product, so a step's critical path is the barrier plus a shared-memory dot
-template <bool fwd>
+// forms its local product, so a step's critical path is the barrier plus a shared-memory dot.
+// R rows of a panel per warp and E entries of a row per lane (templated so a step issues only the
+// instructions the block's panel size needs: p <= 64 * R, p <= 32 * E).
+template <bool fwd, int R, int E>
 __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw, int lane, double (*chain)[kPanelMax],
                                             const double* xin, double xs, double* out, double* out2, const double* sub,
                                             double os, int out_mode, cooperative_groups::cluster_group& cluster) {
   const int b0 = V.block_start[blk], m = V.block_start[blk + 1] - b0, p = V.p[blk], P = (m + p - 1) / p;
+  const double* base = V.m + V.off[blk];
   auto rows_of = [&](int q) { return min(p, m - q * p); };
   auto panel_size = [&](int q) {
-    const long long s = rows_of(q), sp = q > 0 ? p : 0, sn = q + 1 < P ? rows_of(q + 1) : 0;
+    const int s = rows_of(q), sp = q > 0 ? p : 0, sn = q + 1 < P ? rows_of(q + 1) : 0;
     return s * s + s * sp + s * s + s * sn;
   };
-  double dl[kPanelRows], cr[kPanelRows][kPanelEl];
+  double dl[R], cr[R][E];
   // panel q's local product D_q x_q and coupling rows C_q, for this warp's rows
-  auto prefetch = [&](int q, long long o) {
+  auto prefetch = [&](int q, int o) {
     const int s = rows_of(q), sc = fwd ? (q > 0 ? p : 0) : (q + 1 < P ? rows_of(q + 1) : 0);
-    const double* Dm = V.m + o + (fwd ? 0 : (long long)s * s + (long long)s * (q > 0 ? p : 0));
-    const double* Cm = fwd ? Dm + (long long)s * s : Dm + (long long)s * s;
-    const double* xq = xin + b0 + (long long)q * p;
+    const double* Dm = base + o + (fwd ? 0 : s * s + s * (q > 0 ? p : 0));
+    const double* Cm = Dm + s * s;
+    const double* xq = xin + b0 + q * p;
 #pragma unroll
-    for (int r = 0; r < kPanelRows; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int i = gw + r * kPanelWarps;
+      if (i - lane >= s - lane) break;  // warp-uniform: i is the same in every lane
       double acc = 0.0;
 #pragma unroll
-      for (int e = 0; e < kPanelEl; ++e) {
+      for (int e = 0; e < E; ++e) {
         const int c = lane + 32 * e;
-        if (i < s && c < s) acc = acc + Dm[(long long)i * s + c] * (xq[c] * xs);
-        cr[r][e] = (i < s && c < sc) ? Cm[(long long)i * sc + c] : 0.0;
+        if (c < s) acc = acc + Dm[i * s + c] * (xq[c] * xs);
+        cr[r][e] = c < sc ? Cm[i * sc + c] : 0.0;
       }
       dl[r] = warp_tree(acc);
     }
   };
-  long long o = V.off[blk];
+  int o = 0;
   int q = fwd ? 0 : P - 1;
   if (!fwd)
     for (int t = 0; t < P - 1; ++t) o += panel_size(t);
@@ -1078,26 +1079,27 @@ __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw,
     const int s = rows_of(q), sc = fwd ? (q > 0 ? p : 0) : (q + 1 < P ? rows_of(q + 1) : 0);
     const double* prev = chain[(q + (fwd ? -1 : 1)) & 1];
 #pragma unroll
-    for (int r = 0; r < kPanelRows; ++r) {
+    for (int r = 0; r < R; ++r) {
       const int i = gw + r * kPanelWarps;
+      if (i >= s) break;  // warp-uniform
       double acc = 0.0;
+      if (sc) {
 #pragma unroll
-      for (int e = 0; e < kPanelEl; ++e)
-        if (lane + 32 * e < sc) acc = acc + cr[r][e] * prev[lane + 32 * e];
-      acc = warp_tree(acc);
-      if (i < s) {
-        const double v = sc ? dl[r] - acc : dl[r];
-        if (lane < kPanelCluster) *cluster.map_shared_rank(&chain[q & 1][i], lane) = v;
-        if (lane == 0) {
-          const long long row = b0 + (long long)q * p + i;
-          if (fwd) {
-            V.scratch[row] = V.diag ? v / V.diag[row] : v;  // z = y / D (LDL^T), else y
-          } else if (out_mode == 1) {
-            out[row] = (sub[row] - v) * os;
-          } else {
-            out[row] = v;
-            if (out_mode == 2) out2[row] = v * os;
-          }
+        for (int e = 0; e < E; ++e)
+          if (lane + 32 * e < sc) acc = acc + cr[r][e] * prev[lane + 32 * e];
+        acc = warp_tree(acc);
+      }
+      const double v = sc ? dl[r] - acc : dl[r];
+      if (lane < kPanelCluster) *cluster.map_shared_rank(&chain[q & 1][i], lane) = v;
+      if (lane == 0) {
+        const long long row = b0 + (long long)q * p + i;
+        if (fwd) {
+          V.scratch[row] = V.diag ? v / V.diag[row] : v;  // z = y / D (LDL^T), else y
+        } else if (out_mode == 1) {
+          out[row] = (sub[row] - v) * os;
+        } else {
+          out[row] = v;
+          if (out_mode == 2) out2[row] = v * os;
         }
       }
     }
@@ -1111,6 +1113,7 @@ __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw,
   }
 }
 
+template <int R, int E>
 __global__ void __cluster_dims__(kPanelCluster, 1, 1) __launch_bounds__(kPanelThreads)
     panel_solve_kernel(PanelView V, const double* rhs, double rs, double* out, double* out2, const double* sub,
                        double os, int out_mode) {
@@ -1121,8 +1124,8 @@ __global__ void __cluster_dims__(kPanelCluster, 1, 1) __launch_bounds__(kPanelTh
   const int blk = blockIdx.x / kPanelCluster;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = rank * (kPanelThreads / 32) + warp;
-  panel_chain<true>(V, blk, gw, lane, chain, rhs, rs, nullptr, nullptr, nullptr, 1.0, 0, cluster);
-  panel_chain<false>(V, blk, gw, lane, chain, V.scratch, 1.0, out, out2, sub, os, out_mode, cluster);
+  panel_chain<true, R, E>(V, blk, gw, lane, chain, rhs, rs, nullptr, nullptr, nullptr, 1.0, 0, cluster);
+  panel_chain<false, R, E>(V, blk, gw, lane, chain, V.scratch, 1.0, out, out2, sub, os, out_mode, cluster);
 }
 
 // Builds the panel matrices from the band factor (upload): one thread per (panel, column, matrix),
