@@ -313,3 +313,30 @@ def test_oracle_multicolor_gs_vcycle_contracts():
         B = np.column_stack([opc.amg_apply(e) for e in np.eye(r)])  # B ~ A^-1
         rho[sm] = max(abs(np.linalg.eigvals(np.eye(r) - B @ A)))
     assert rho[3] < 0.5 and rho[3] < rho[0], rho
+
+
+@pytest.mark.parametrize("name,cells,length,fracs,expect", [
+    # test_model.cpp:93-100: the trivial 2^3 cube (27 nodes, no fracture)
+    ("cube", (2, 2, 2), (1.0, 1.0, 1.0), [], (81, 0, 0)),
+    # test_model.cpp:102-105, presets.cpp test1: x 10 cells, y segments 8/20/8 cells, z 6 cells, the patch
+    # at x = 5 over y cells 8..28 and the full z; the counts depend on the cell topology only, so the y axis is
+    # written with one unit per cell (ticks 8 and 28 exact)
+    ("test1", (10, 36, 6), (10.0, 36.0, 6.0), [(0, 5.0, 8.0, 28.0, 0.0, 6.0)], (8832, 360, 120)),
+    # test_model.cpp:107-110, presets.cpp make_test2a(25): four x-planes over [0.2, 0.8]^2
+    ("test2a-coarse", (25, 25, 25), (1.0, 1.0, 1.0), [(0, x, 0.2, 0.8, 0.2, 0.8) for x in (0.2, 0.4, 0.6, 0.8)],
+     (55080, 2700, 900)),
+    # test_model.cpp:112-121, presets.cpp make_test2b(level): nine x-planes over [0.2, 0.8]^2
+    ("test2b-1", (10, 10, 10), (1.0, 1.0, 1.0), [(0, 0.1 * i, 0.2, 0.8, 0.2, 0.8) for i in range(1, 10)],
+     (4668, 972, 324)),
+    ("test2b-2", (20, 20, 20), (1.0, 1.0, 1.0), [(0, 0.1 * i, 0.2, 0.8, 0.2, 0.8) for i in range(1, 10)],
+     (31050, 3888, 1296)),
+])
+def test_reference_mesh_count_pins(name, cells, length, fracs, expect):
+    """The reference's own mesh pins (/root/reference/proj/tests/unit/test_model.cpp:93-129) re-expressed
+    against the generator that feeds every parity test (workload/workload.cpp restating mesh.cpp's
+    fracture-node duplication): n_u, n_t, n_p and n_t = 3 n_p."""
+    from workload import gen
+
+    S = gen.Workload(spec=dict(cells=cells, length=length, fractures=fracs), seed=1).system(copy=False)
+    assert (S.n_u, S.n_t, S.n_p) == expect
+    assert S.n_t == 3 * S.n_p
