@@ -291,9 +291,9 @@ struct AmgLevel {
   // mcgs: rows grouped by colour (ascending inside a colour), colour c = color_rows[color_off[c] ..)
   std::vector<int> color_rows, color_off;
 };
-// EXTENSION (mcgs): greedy colouring in index order of a structurally symmetric pattern — row i takes
-// the smallest colour not used by its already coloured neighbours (j < i in row i); returns the rows
-// grouped by colour
+// EXTENSION (mcgs): greedy colouring in index order of the pattern of A + A^T — row i takes the
+// smallest colour not used by its already coloured neighbours (j < i with an entry (i, j) or (j, i)), so
+// rows of one colour never reference each other; returns the rows grouped by colour
 void greedy_coloring(const CsrMatrix& A, std::vector<int>& rows, std::vector<int>& off);
 
 struct AmgHierarchy {

@@ -342,24 +342,29 @@ HostAmg amg_setup(Csr A, const std::vector<std::vector<double>>& near_null, cons
 }
 
 void color_rows(int n, const int64_t* rp, const int* ci, std::vector<int>& rows, std::vector<int>& off) {
+  // earlier neighbours in either direction: j < i in row i, and the rows j < i holding an entry (j, i)
+  std::vector<int64_t> tp(static_cast<size_t>(n) + 1, 0);
+  for (int64_t k = 0; k < rp[n]; ++k) ++tp[size_t(ci[k]) + 1];
+  for (int i = 0; i < n; ++i) tp[size_t(i) + 1] += tp[i];
+  std::vector<int> trow(static_cast<size_t>(rp[n]));
+  {
+    std::vector<int64_t> next(tp.begin(), tp.end() - 1);
+    for (int i = 0; i < n; ++i)
+      for (int64_t k = rp[i]; k < rp[i + 1]; ++k) trow[size_t(next[size_t(ci[k])]++)] = i;
+  }
   std::vector<int> color(static_cast<size_t>(n), -1);
   std::vector<int> seen;  // seen[c] == i: colour c is taken by a neighbour of row i
   int n_colors = 0;
   for (int i = 0; i < n; ++i) {
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
-      const int j = ci[k];
-      if (j < i) seen[size_t(color[j])] = i;  // earlier rows are coloured
-    }
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+      if (ci[k] < i) seen[size_t(color[ci[k]])] = i;
+    for (int64_t k = tp[i]; k < tp[i + 1]; ++k)
+      if (trow[k] < i) seen[size_t(color[trow[k]])] = i;
     int c = 0;
     while (c < n_colors && seen[size_t(c)] == i) ++c;
     color[i] = c;
     if (c == n_colors) ++n_colors, seen.push_back(-1);
   }
-  int bad = 0;
-#pragma omp parallel for schedule(static) reduction(| : bad)
-  for (int i = 0; i < n; ++i)
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) bad |= ci[k] != i && color[ci[k]] == color[i];
-  if (bad) throw std::invalid_argument("mcgs: the level operator's pattern is not structurally symmetric");
   off.assign(static_cast<size_t>(n_colors) + 1, 0);
   for (int i = 0; i < n; ++i) ++off[size_t(color[i]) + 1];
   for (int c = 0; c < n_colors; ++c) off[size_t(c) + 1] += off[c];

@@ -74,9 +74,9 @@ struct ChebyshevCoefficients {
 };
 ChebyshevCoefficients chebyshev_coefficients(double lambda_max, double ratio, int degree);
 
-// Multicolour smoother (extension): the greedy colouring in row order of a structurally symmetric
-// pattern (each row takes the smallest colour none of its earlier neighbours has), rows grouped by
-// colour — the oracle's greedy_coloring (oracle/amg.cpp) rule
+// Multicolour smoother (extension): the greedy colouring in row order of the pattern of A + A^T (each
+// row takes the smallest colour none of its earlier neighbours has), rows grouped by colour — the
+// oracle's greedy_coloring (oracle/amg.cpp) rule
 void color_rows(int n, const int64_t* rp, const int* ci, std::vector<int>& rows, std::vector<int>& off);
 
 // A is taken by value and moved into level 0 (callers std::move the inner operator in)
