@@ -4,7 +4,7 @@
  * Jacobian of arXiv 2112.12397).
  *
  * Every entry point replaces one call of the reference's C++ API
- * (/root/reference/proj/core/include/fracprec/*.hpp); the mapping is noted per
+ * (/root/reference/proj/core/include/fracprec/ headers); the mapping is noted per
  * function.  Conventions:
  *   - return value: FP_OK (0) or an error code; fp_last_error() gives the
  *     message (thread-local).  Codes mirror the reference's exception classes:

@@ -33,19 +33,9 @@ struct Rng {  // mt19937_64 with explicit, library-independent mappings
 
 enum class Region : char { stick, slip, open };
 
-struct Face {
-  int minus[4], plus[4];
-  double area, len1, len2;
-  int axis[3];  // frame: normal axis, m1 axis, m2 axis (unit vectors e_axis)
-};
-struct Edge {
-  int k, l;
-  double length, dk, dl;
-};
-struct BcEdge {
-  int k;
-  double length, d;
-};
+using Face = FractureFace;
+using Edge = FractureEdge;
+using BcEdge = FractureBcEdge;
 
 struct Mesh {
   int nn[3], nc[3];
@@ -291,6 +281,152 @@ WorkloadSpec preset_config(int id, uint64_t seed) {
   return s;
 }
 
+// assemble_fracture_blocks (assembly.cpp:229-406): C2 (jump rows, slip derivative), H (stabilization and
+// the slip / open diagonal), T (TPFA, cubic law, stabilization / dt), F_u (pressure-gap coupling) and
+// Q2 = Q2gap + F_u, every block through from_triplets in insertion order
+void assemble_fracture_blocks(const FractureModel& M, const FractureState& S, HostSystem& J) {
+  const int n_u = M.n_u, n_p = M.n_p, n_t = 3 * n_p;
+  if (int(S.region.size()) != n_p || int(S.gap.size()) != n_p || int(S.trac_n.size()) != n_p ||
+      int(S.slip_dir.size()) != n_p || int(S.pressure.size()) != n_p)
+    throw std::invalid_argument("assemble_fracture_blocks: state size != n_p");
+  std::vector<Csr::Triplet> c2, h, t, q2gap, fu;
+  auto jump_row = [&](int f, int row, int comp, double scale) {
+    const Face& fc = M.faces[f];
+    const double w = fc.area / 4.0;
+    for (int v = 0; v < 4; ++v) {
+      if (fc.plus[v] == fc.minus[v]) continue;
+      for (int d = 0; d < 3; ++d) {
+        const double val = scale * w * (fc.axis[comp] == d ? 1.0 : 0.0);
+        if (val == 0.0) continue;
+        const int cp = 3 * fc.plus[v] + d, cm = 3 * fc.minus[v] + d;
+        if (!M.dir[cp]) c2.push_back({row, cp, val});
+        if (!M.dir[cm]) c2.push_back({row, cm, -val});
+      }
+    }
+  };
+  for (int f = 0; f < n_p; ++f) {
+    const Face& fc = M.faces[f];
+    if (S.region[f] == 's') {
+      for (int c = 0; c < 3; ++c) jump_row(f, 3 * f + c, c, 1.0);
+    } else if (S.region[f] == 'l') {
+      jump_row(f, 3 * f, 0, 1.0);
+      const double dg[2] = {S.gap[f][1], S.gap[f][2]};  // gap_prev = 0
+      const double r = std::hypot(dg[0], dg[1]);
+      const double tau = M.cohesion - S.trac_n[f] * M.tan_th;
+      const double thr = std::max(1e-12, 0.1 * std::max(tau, 0.0) / M.k_scale);
+      double mm[2], D[2][2] = {{0, 0}, {0, 0}};
+      if (r >= thr) {
+        mm[0] = dg[0] / r, mm[1] = dg[1] / r;
+        for (int a = 0; a < 2; ++a)
+          for (int b = 0; b < 2; ++b) D[a][b] = (tau / r) * ((a == b ? 1.0 : 0.0) - mm[a] * mm[b]);
+      } else {
+        mm[0] = S.slip_dir[f][0], mm[1] = S.slip_dir[f][1];
+      }
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b)
+          if (D[a][b] != 0.0) jump_row(f, 3 * f + 1 + a, 1 + b, -D[a][b] / M.k_scale);
+      for (int a = 0; a < 2; ++a) {
+        h.push_back({3 * f + 1 + a, 3 * f + 1 + a, -fc.area / M.k_scale});
+        const double dtn = -M.tan_th * mm[a];
+        if (dtn != 0.0) h.push_back({3 * f + 1 + a, 3 * f, (fc.area / M.k_scale) * dtn});
+      }
+    } else {
+      for (int c = 0; c < 3; ++c) h.push_back({3 * f + c, 3 * f + c, -fc.area / M.k_scale});
+    }
+  }
+  auto stab = [&](const Edge& e) {  // beta * (mean face area / E) * |edge| (assembly.cpp:94-97)
+    const double hh = 0.5 * (M.faces[e.k].area + M.faces[e.l].area);
+    return M.stab_beta * (hh / M.E_ref) * e.length;
+  };
+  for (const Edge& e : M.edges) {
+    const bool ck = S.region[e.k] != 'o', cl = S.region[e.l] != 'o';
+    if (!ck && !cl) continue;
+    const double sc = stab(e);
+    for (int c = 0; c < 3; ++c) {
+      if (ck && cl) {
+        h.push_back({3 * e.k + c, 3 * e.k + c, sc});
+        h.push_back({3 * e.l + c, 3 * e.l + c, sc});
+        h.push_back({3 * e.k + c, 3 * e.l + c, -sc});
+        h.push_back({3 * e.l + c, 3 * e.k + c, -sc});
+      } else if (ck) {
+        h.push_back({3 * e.k + c, 3 * e.k + c, sc});
+      } else {
+        h.push_back({3 * e.l + c, 3 * e.l + c, sc});
+      }
+    }
+  }
+  std::vector<double> cf(static_cast<size_t>(n_p)), dcf(static_cast<size_t>(n_p));
+  for (int f = 0; f < n_p; ++f) {
+    const bool open = S.region[f] == 'o';
+    const double g = open ? std::max(S.gap[f][0], 0.0) : 0.0;
+    cf[f] = M.C_f0 + g * g * g / 12.0;
+    dcf[f] = open ? g * g / 4.0 : 0.0;
+  }
+  auto fu_row = [&](int row, int face, double coeff) {
+    if (coeff == 0.0) return;
+    const Face& fc = M.faces[face];
+    for (int v = 0; v < 4; ++v) {
+      if (fc.plus[v] == fc.minus[v]) continue;
+      for (int d = 0; d < 3; ++d) {
+        const double val = coeff * (fc.axis[0] == d ? 1.0 : 0.0) / 4.0;
+        if (val == 0.0) continue;
+        const int cp = 3 * fc.plus[v] + d, cm = 3 * fc.minus[v] + d;
+        if (!M.dir[cp]) fu.push_back({row, cp, val});
+        if (!M.dir[cm]) fu.push_back({row, cm, -val});
+      }
+    }
+  };
+  for (const Edge& e : M.edges) {
+    const double yk = (cf[e.k] / M.mu_f) * e.length / e.dk, yl = (cf[e.l] / M.mu_f) * e.length / e.dl;
+    const double ykl = 2.0 * yk * yl / (yk + yl);
+    t.push_back({e.k, e.k, ykl});
+    t.push_back({e.l, e.l, ykl});
+    t.push_back({e.k, e.l, -ykl});
+    t.push_back({e.l, e.k, -ykl});
+    const double sc = stab(e) / M.dt;
+    t.push_back({e.k, e.k, sc});
+    t.push_back({e.l, e.l, sc});
+    t.push_back({e.k, e.l, -sc});
+    t.push_back({e.l, e.k, -sc});
+    const double dp = S.pressure[e.k] - S.pressure[e.l];
+    if (dp != 0.0) {
+      const double dk = 2.0 * (yl / (yk + yl)) * (yl / (yk + yl)), dl = 2.0 * (yk / (yk + yl)) * (yk / (yk + yl));
+      const double ck = dp * dk * (e.length / (M.mu_f * e.dk)) * dcf[e.k];
+      const double cl = dp * dl * (e.length / (M.mu_f * e.dl)) * dcf[e.l];
+      fu_row(e.k, e.k, ck);
+      fu_row(e.k, e.l, cl);
+      fu_row(e.l, e.k, -ck);
+      fu_row(e.l, e.l, -cl);
+    }
+  }
+  for (const BcEdge& e : M.bc_edges) {
+    const double yb = (cf[e.k] / M.mu_f) * e.length / e.d;
+    t.push_back({e.k, e.k, yb});
+    const double pk = S.pressure[e.k];
+    if (pk != 0.0) fu_row(e.k, e.k, pk * (e.length / (M.mu_f * e.d)) * dcf[e.k]);
+  }
+  for (int f = 0; f < n_p; ++f) {
+    if (S.region[f] != 'o') continue;
+    const Face& fc = M.faces[f];
+    const double w = fc.area / 4.0;
+    for (int v = 0; v < 4; ++v) {
+      if (fc.plus[v] == fc.minus[v]) continue;
+      for (int d = 0; d < 3; ++d) {
+        const double val = (w / M.dt) * (fc.axis[0] == d ? 1.0 : 0.0);
+        if (val == 0.0) continue;
+        const int cp = 3 * fc.plus[v] + d, cm = 3 * fc.minus[v] + d;
+        if (!M.dir[cp]) q2gap.push_back({f, cp, val});
+        if (!M.dir[cm]) q2gap.push_back({f, cm, -val});
+      }
+    }
+  }
+  J.C2 = Csr::from_triplets(n_t, n_u, std::move(c2));
+  J.H = Csr::from_triplets(n_t, n_t, std::move(h));
+  J.T = Csr::from_triplets(n_p, n_p, std::move(t));
+  J.F_u = Csr::from_triplets(n_p, n_u, std::move(fu));
+  J.Q2 = csr_add(Csr::from_triplets(n_p, n_u, std::move(q2gap)), J.F_u, 1.0, 1.0);
+}
+
 Workload generate_workload(const WorkloadSpec& s) {
   Mesh m = build_mesh(s);
   const int n_nodes = int(m.nodes.size()), n_u = 3 * n_nodes, n_p = int(m.faces.size()), n_t = 3 * n_p;
@@ -428,7 +564,7 @@ Workload generate_workload(const WorkloadSpec& s) {
   }
 
   // ---- coupling C1, Q1 (assembly.cpp:190-216)
-  std::vector<Csr::Triplet> c1, q1, c2, h, t, q2gap, fu;
+  std::vector<Csr::Triplet> c1, q1;
   for (int f = 0; f < n_p; ++f) {
     const Face& fc = m.faces[f];
     const double w = fc.area / 4.0;
@@ -454,141 +590,19 @@ Workload generate_workload(const WorkloadSpec& s) {
   J.Q1 = Csr::from_triplets(n_u, n_p, std::move(q1));
 
   // ---- state-dependent blocks (assembly.cpp:229-406)
-  auto jump_row = [&](int f, int row, int comp, double scale) {
-    const Face& fc = m.faces[f];
-    const double w = fc.area / 4.0;
-    for (int v = 0; v < 4; ++v) {
-      if (fc.plus[v] == fc.minus[v]) continue;
-      for (int d = 0; d < 3; ++d) {
-        const double val = scale * w * (fc.axis[comp] == d ? 1.0 : 0.0);
-        if (val == 0.0) continue;
-        const int cp = 3 * fc.plus[v] + d, cm = 3 * fc.minus[v] + d;
-        if (!m.dir[cp]) c2.push_back({row, cp, val});
-        if (!m.dir[cm]) c2.push_back({row, cm, -val});
-      }
-    }
-  };
-  for (int f = 0; f < n_p; ++f) {
-    const Face& fc = m.faces[f];
-    if (region[f] == Region::stick) {
-      for (int c = 0; c < 3; ++c) jump_row(f, 3 * f + c, c, 1.0);
-    } else if (region[f] == Region::slip) {
-      jump_row(f, 3 * f, 0, 1.0);
-      const double dg[2] = {gap[f][1], gap[f][2]};  // gap_prev = 0
-      const double r = std::hypot(dg[0], dg[1]);
-      const double tau = s.cohesion - trac[f][0] * tan_th;
-      const double thr = std::max(1e-12, 0.1 * std::max(tau, 0.0) / k_scale);
-      double mm[2], D[2][2] = {{0, 0}, {0, 0}};
-      if (r >= thr) {
-        mm[0] = dg[0] / r, mm[1] = dg[1] / r;
-        for (int a = 0; a < 2; ++a)
-          for (int b = 0; b < 2; ++b) D[a][b] = (tau / r) * ((a == b ? 1.0 : 0.0) - mm[a] * mm[b]);
-      } else {
-        mm[0] = sdir[f][0], mm[1] = sdir[f][1];
-      }
-      for (int a = 0; a < 2; ++a)
-        for (int b = 0; b < 2; ++b)
-          if (D[a][b] != 0.0) jump_row(f, 3 * f + 1 + a, 1 + b, -D[a][b] / k_scale);
-      for (int a = 0; a < 2; ++a) {
-        h.push_back({3 * f + 1 + a, 3 * f + 1 + a, -fc.area / k_scale});
-        const double dtn = -tan_th * mm[a];
-        if (dtn != 0.0) h.push_back({3 * f + 1 + a, 3 * f, (fc.area / k_scale) * dtn});
-      }
-    } else {
-      for (int c = 0; c < 3; ++c) h.push_back({3 * f + c, 3 * f + c, -fc.area / k_scale});
-    }
-  }
-  auto stab = [&](const Edge& e) {  // beta * (mean face area / E) * |edge| (assembly.cpp:94-97)
-    const double hh = 0.5 * (m.faces[e.k].area + m.faces[e.l].area);
-    return s.stab_beta * (hh / E_ref) * e.length;
-  };
-  for (const Edge& e : m.edges) {
-    const bool ck = region[e.k] != Region::open, cl = region[e.l] != Region::open;
-    if (!ck && !cl) continue;
-    const double sc = stab(e);
-    for (int c = 0; c < 3; ++c) {
-      if (ck && cl) {
-        h.push_back({3 * e.k + c, 3 * e.k + c, sc});
-        h.push_back({3 * e.l + c, 3 * e.l + c, sc});
-        h.push_back({3 * e.k + c, 3 * e.l + c, -sc});
-        h.push_back({3 * e.l + c, 3 * e.k + c, -sc});
-      } else if (ck) {
-        h.push_back({3 * e.k + c, 3 * e.k + c, sc});
-      } else {
-        h.push_back({3 * e.l + c, 3 * e.l + c, sc});
-      }
-    }
-  }
-  std::vector<double> cf(static_cast<size_t>(n_p)), dcf(static_cast<size_t>(n_p));
-  for (int f = 0; f < n_p; ++f) {
-    const bool open = region[f] == Region::open;
-    const double g = open ? std::max(gap[f][0], 0.0) : 0.0;
-    cf[f] = s.C_f0 + g * g * g / 12.0;
-    dcf[f] = open ? g * g / 4.0 : 0.0;
-  }
-  auto fu_row = [&](int row, int face, double coeff) {
-    if (coeff == 0.0) return;
-    const Face& fc = m.faces[face];
-    for (int v = 0; v < 4; ++v) {
-      if (fc.plus[v] == fc.minus[v]) continue;
-      for (int d = 0; d < 3; ++d) {
-        const double val = coeff * (fc.axis[0] == d ? 1.0 : 0.0) / 4.0;
-        if (val == 0.0) continue;
-        const int cp = 3 * fc.plus[v] + d, cm = 3 * fc.minus[v] + d;
-        if (!m.dir[cp]) fu.push_back({row, cp, val});
-        if (!m.dir[cm]) fu.push_back({row, cm, -val});
-      }
-    }
-  };
-  for (const Edge& e : m.edges) {
-    const double yk = (cf[e.k] / s.mu_f) * e.length / e.dk, yl = (cf[e.l] / s.mu_f) * e.length / e.dl;
-    const double ykl = 2.0 * yk * yl / (yk + yl);
-    t.push_back({e.k, e.k, ykl});
-    t.push_back({e.l, e.l, ykl});
-    t.push_back({e.k, e.l, -ykl});
-    t.push_back({e.l, e.k, -ykl});
-    const double sc = stab(e) / s.dt;
-    t.push_back({e.k, e.k, sc});
-    t.push_back({e.l, e.l, sc});
-    t.push_back({e.k, e.l, -sc});
-    t.push_back({e.l, e.k, -sc});
-    const double dp = pres[e.k] - pres[e.l];
-    if (dp != 0.0) {
-      const double dk = 2.0 * (yl / (yk + yl)) * (yl / (yk + yl)), dl = 2.0 * (yk / (yk + yl)) * (yk / (yk + yl));
-      const double ck = dp * dk * (e.length / (s.mu_f * e.dk)) * dcf[e.k];
-      const double cl = dp * dl * (e.length / (s.mu_f * e.dl)) * dcf[e.l];
-      fu_row(e.k, e.k, ck);
-      fu_row(e.k, e.l, cl);
-      fu_row(e.l, e.k, -ck);
-      fu_row(e.l, e.l, -cl);
-    }
-  }
-  for (const BcEdge& e : m.bc_edges) {
-    const double yb = (cf[e.k] / s.mu_f) * e.length / e.d;
-    t.push_back({e.k, e.k, yb});
-    const double pk = pres[e.k];
-    if (pk != 0.0) fu_row(e.k, e.k, pk * (e.length / (s.mu_f * e.d)) * dcf[e.k]);
-  }
-  for (int f = 0; f < n_p; ++f) {
-    if (region[f] != Region::open) continue;
-    const Face& fc = m.faces[f];
-    const double w = fc.area / 4.0;
-    for (int v = 0; v < 4; ++v) {
-      if (fc.plus[v] == fc.minus[v]) continue;
-      for (int d = 0; d < 3; ++d) {
-        const double val = (w / s.dt) * (fc.axis[0] == d ? 1.0 : 0.0);
-        if (val == 0.0) continue;
-        const int cp = 3 * fc.plus[v] + d, cm = 3 * fc.minus[v] + d;
-        if (!m.dir[cp]) q2gap.push_back({f, cp, val});
-        if (!m.dir[cm]) q2gap.push_back({f, cm, -val});
-      }
-    }
-  }
-  J.C2 = Csr::from_triplets(n_t, n_u, std::move(c2));
-  J.H = Csr::from_triplets(n_t, n_t, std::move(h));
-  J.T = Csr::from_triplets(n_p, n_p, std::move(t));
-  J.F_u = Csr::from_triplets(n_p, n_u, std::move(fu));
-  J.Q2 = csr_add(Csr::from_triplets(n_p, n_u, std::move(q2gap)), J.F_u, 1.0, 1.0);
+  FractureModel& M = W.model;
+  M.n_u = n_u, M.n_p = n_p;
+  M.faces = m.faces, M.edges = m.edges, M.bc_edges = m.bc_edges, M.dir = m.dir;
+  M.cohesion = s.cohesion, M.tan_th = tan_th, M.k_scale = k_scale, M.stab_beta = s.stab_beta, M.E_ref = E_ref;
+  M.C_f0 = s.C_f0, M.mu_f = s.mu_f, M.dt = s.dt;
+  FractureState& S = W.state;
+  S.region = W.region;
+  S.gap = gap;
+  S.trac_n.resize(static_cast<size_t>(n_p));
+  for (int f = 0; f < n_p; ++f) S.trac_n[f] = trac[f][0];
+  S.slip_dir = sdir;
+  S.pressure = pres;
+  assemble_fracture_blocks(M, S, J);
   J.check_shapes();
   return W;
 }

@@ -43,8 +43,48 @@ struct WorkloadSpec {
   uint64_t seed = 42;
 };
 
+// The fixed part of the state-dependent assembly (assemble_fracture_blocks, assembly.cpp:229-406): the
+// fracture faces (minus / plus nodes, area, frame), the TPFA edges between faces and to the patch rim,
+// the Dirichlet flags of the displacement dofs and the material constants.
+struct FractureFace {
+  int minus[4], plus[4];
+  double area, len1, len2;
+  int axis[3];  // frame: normal axis, m1 axis, m2 axis (unit vectors e_axis)
+};
+struct FractureEdge {
+  int k, l;
+  double length, dk, dl;
+};
+struct FractureBcEdge {
+  int k;
+  double length, d;
+};
+struct FractureModel {
+  int n_u = 0, n_p = 0;
+  std::vector<FractureFace> faces;
+  std::vector<FractureEdge> edges;
+  std::vector<FractureBcEdge> bc_edges;
+  std::vector<char> dir;  // per displacement dof
+  double cohesion = 0.0, tan_th = 0.6, k_scale = 1.0, stab_beta = 1.0, E_ref = 1.0, C_f0 = 9.87e-15, mu_f = 1e-3,
+         dt = 0.5;
+};
+// FractureState (assembly.hpp): per face the contact region ('s' stick, 'l' slip, 'o' open), the gap
+// increment (normal, m1, m2; the previous gap is 0), the normal traction, the frozen slip direction and
+// the pressure
+struct FractureState {
+  std::string region;
+  std::vector<std::array<double, 3>> gap;
+  std::vector<double> trac_n;
+  std::vector<std::array<double, 2>> slip_dir;
+  std::vector<double> pressure;
+};
+// C2, H, T, F_u and Q2 of J for a state (the reference's Newton-step assembly; the generator's own)
+void assemble_fracture_blocks(const FractureModel& M, const FractureState& S, HostSystem& J);
+
 struct Workload {
   HostSystem J;
+  FractureModel model;
+  FractureState state;
   std::vector<std::array<double, 3>> coords;
   int n_stick = 0, n_slip = 0, n_open = 0, n_fractures = 0;
   double k_scale = 0.0;
