@@ -204,6 +204,22 @@ int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config
  * fp_precond_create uses.  One host setup can so be uploaded in every mode. */
 int fp_host_precond_set_upload(fp_host_precond* p, int32_t row_sum, int32_t factor_solve);
 
+/* ---- Jacobian assembly of the fracture blocks on the device:
+ * assemble_fracture_blocks (assembly.cpp:229-406) — C2, H, T, F_u and Q2 for a fracture state, the
+ * part of the Jacobian the Newton loop rebuilds every step (A, C1, Q1 stay).  create uploads the
+ * workload's fracture model (faces, TPFA edges, Dirichlet flags, constants); run assembles the blocks
+ * for a state (include/fracprec_workload.h fp_fracture_state) and, when s is not NULL, installs them
+ * into the device system (layouts and block scaling rebuilt on the device; build the preconditioner
+ * afterwards, as driver.cpp:229-230 does every Newton step).  matrix copies a block out
+ * (what 0 = C2, 1 = H, 2 = T, 3 = F_u, 4 = Q2; call with row_offsets == NULL for the sizes). */
+typedef struct fp_fracture_state fp_fracture_state;
+typedef struct fp_fracture_assembly fp_fracture_assembly;
+int fp_fracture_assembly_create(const fp_workload* w, fp_fracture_assembly** out);
+void fp_fracture_assembly_destroy(fp_fracture_assembly* a);
+int fp_fracture_assembly_run(fp_fracture_assembly* a, const fp_fracture_state* st, fp_system* s);
+int fp_fracture_assembly_matrix(const fp_fracture_assembly* a, int32_t what, int32_t* n_rows, int32_t* n_cols,
+                                int64_t* nnz, int64_t* row_offsets, int32_t* col_indices, double* values);
+
 /* ---- upload to the device */
 int fp_precond_create(fp_system* s, const fp_host_precond* hp, fp_precond** out);
 int fp_precond_upload(fp_system* s, const fp_precond_desc* desc, fp_precond** out);

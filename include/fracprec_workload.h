@@ -59,6 +59,22 @@ int fp_workload_info(const fp_workload* w, int32_t* counts);
  * and the time step; the string is valid until destroy */
 int fp_workload_region(const fp_workload* w, const char** region, double* dt);
 
+/* FractureState (assembly.hpp) of a workload: per face the contact region, the gap increment (normal,
+ * m1, m2), the normal traction, the frozen slip direction and the pressure */
+typedef struct fp_fracture_state {
+  int32_t n_p;
+  const char* region;        /* n_p characters: 's' stick, 'l' slip, 'o' open */
+  const double* gap;         /* 3 n_p */
+  const double* traction_n;  /* n_p */
+  const double* slip_dir;    /* 2 n_p */
+  const double* pressure;    /* n_p */
+} fp_fracture_state;
+/* views of the workload's current state (valid until the next set_state or destroy) */
+int fp_workload_state(const fp_workload* w, fp_fracture_state* out);
+/* a new state: C2, H, T, F_u, Q2 re-assembled on the host (assemble_fracture_blocks, assembly.cpp:229-406),
+ * the reference's Newton-step assembly; fp_workload_system views see the new blocks */
+int fp_workload_set_state(fp_workload* w, const fp_fracture_state* st);
+
 /* ---- snapshot bundle (snapshot.cpp:28-104, mmio.cpp:15-76): manifest.json + Matrix Market blocks */
 /* import_snapshot: the bundle in `dir` as a workload handle (system views, coords, region, dt) */
 int fp_snapshot_import(const char* dir, fp_workload** out);

@@ -113,6 +113,11 @@ SIGNATURES = {
     "fp_gmres": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.POINTER(FpGmresOptions), C.POINTER(FpSolveStats)]),
     "fp_workload_host_precond_build": (C.c_int, [_P, C.POINTER(FpPrecondConfig), _PP]),
     "fp_setup_backend": (C.c_int, [C.POINTER(C.c_int32)]),
+    "fp_fracture_assembly_create": (C.c_int, [_P, _PP]),
+    "fp_fracture_assembly_destroy": (None, [_P]),
+    "fp_fracture_assembly_run": (C.c_int, [_P, _P, _P]),
+    "fp_fracture_assembly_matrix": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                              C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int32), _DP]),
     "fp_set_setup_backend": (C.c_int, [C.c_int32]),
 }
 

@@ -484,6 +484,14 @@ class Workload:
     def info(self) -> dict:
         return self._w.info()
 
+    def state(self) -> dict:
+        """The fracture state (region, gap, traction_n, slip_dir, pressure)."""
+        return self._w.state()
+
+    def set_state(self, state: dict) -> None:
+        """A new fracture state, the blocks re-assembled on the host (the reference's Newton-step assembly)."""
+        self._w.set_state(state)
+
     def system(self, copy: bool = True) -> BlockSystem:
         """The generated blocks as a BlockSystem: owned NumPy copies, or (copy=False) read-only
         views into the workload's arrays that keep the Workload alive."""
@@ -493,6 +501,37 @@ class Workload:
         if not copy:
             J._owner = self  # the views point into this workload
         return J
+
+
+class FractureAssembly:
+    """assemble_fracture_blocks (assembly.cpp:229-406) on the device: C2, H, T, F_u, Q2 for a fracture state,
+    optionally installed into a BlockSystemOperator (the Newton step's re-assembly; fp_fracture_assembly_*)."""
+
+    BLOCKS = ("C2", "H", "T", "F_u", "Q2")
+
+    def __init__(self, W: Workload):
+        self._h = C.c_void_p()
+        self._w = W
+        N.check(N.lib.fp_fracture_assembly_create(W._h, C.byref(self._h)))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and N is not None and getattr(N, "lib", None) is not None:
+            N.lib.fp_fracture_assembly_destroy(self._h)
+            self._h = None
+
+    def run(self, state: dict, op: Optional[BlockSystemOperator] = None) -> None:
+        st, _keep = _wl.state_view(state)
+        N.check(N.lib.fp_fracture_assembly_run(self._h, C.byref(st), op._h if op is not None else None))
+
+    def matrix(self, name: str) -> CsrMatrix:
+        what = self.BLOCKS.index(name)
+        r, c, nz = C.c_int32(), C.c_int32(), C.c_int64()
+        N.check(N.lib.fp_fracture_assembly_matrix(self._h, what, C.byref(r), C.byref(c), C.byref(nz), None, None, None))
+        rp, ci, v = np.zeros(r.value + 1, np.int64), np.zeros(nz.value, np.int32), np.zeros(nz.value)
+        N.check(N.lib.fp_fracture_assembly_matrix(
+            self._h, what, None, None, None, rp.ctypes.data_as(C.POINTER(C.c_int64)),
+            ci.ctypes.data_as(C.POINTER(C.c_int32)), v.ctypes.data_as(C.POINTER(C.c_double))))
+        return CsrMatrix(r.value, c.value, rp, ci, v)
 
 
 def export_snapshot(directory: str, J: BlockSystem, region: str, dt: float = 0.5) -> None:

@@ -14,6 +14,7 @@
 #include "../../include/fracprec_b200.h"
 #include "device/engine.cuh"
 #include "host/setup.hpp"
+#include "../../include/fracprec_workload.h"
 #include "workload.hpp"  // workload/ (libfp_workload.so): the fp_workload handle
 
 namespace {
@@ -263,6 +264,10 @@ fpb::HostPrecond build_any(const fpd::SystemView& V, const fpb::HostSystem* H, i
 
 struct fp_host_precond {
   fpb::HostPrecond hp;
+};
+
+struct fp_fracture_assembly {
+  std::unique_ptr<fpd::DeviceFractureAssembly> dev;
 };
 
 extern "C" {
@@ -640,6 +645,54 @@ int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config
     p->hp = build_any(fpd::SystemView::of(w->w.J), &w->w.J, cfg->variant, to_amg(cfg->amg), w->w.coords);
     p->hp.factor_solve = cfg->factor_solve;
     *out = p.release();
+  });
+}
+
+// -------------------------------------------------- fracture-block assembly (device)
+int fp_fracture_assembly_create(const fp_workload* w, fp_fracture_assembly** out) {
+  return guard([&] {
+    need(w && out, "fp_fracture_assembly_create: null argument");
+    auto a = std::make_unique<fp_fracture_assembly>();
+    a->dev = std::make_unique<fpd::DeviceFractureAssembly>(w->w.model);
+    *out = a.release();
+  });
+}
+
+void fp_fracture_assembly_destroy(fp_fracture_assembly* a) { delete a; }
+
+int fp_fracture_assembly_run(fp_fracture_assembly* a, const fp_fracture_state* st, fp_system* s) {
+  return guard([&] {
+    need(a && st, "fp_fracture_assembly_run: null argument");
+    need(st->n_p == a->dev->n_p, "fp_fracture_assembly_run: state n_p does not match the model");
+    need(st->n_p == 0 || (st->region && st->gap && st->traction_n && st->slip_dir && st->pressure),
+         "fp_fracture_assembly_run: null state array");
+    for (int f = 0; f < st->n_p; ++f)
+      need(st->region[f] == 's' || st->region[f] == 'l' || st->region[f] == 'o',
+           "fp_fracture_assembly_run: region must be s, l or o");
+    a->dev->run(st->region, st->gap, st->traction_n, st->slip_dir, st->pressure);
+    if (s) {
+      need(s->dev->n_u == a->dev->n_u && s->dev->n_p == a->dev->n_p, "fp_fracture_assembly_run: system size mismatch");
+      s->dev->set_fracture_blocks(a->dev->C2, a->dev->H, a->dev->T, a->dev->Q2);
+    }
+  });
+}
+
+int fp_fracture_assembly_matrix(const fp_fracture_assembly* a, int32_t what, int32_t* n_rows, int32_t* n_cols,
+                                int64_t* nnz, int64_t* rp, int32_t* ci, double* v) {
+  return guard([&] {
+    need(a, "null handle");
+    need(what >= 0 && what <= 4, "fp_fracture_assembly_matrix: what must be 0..4");
+    const fpd::DCsr& M = what == 0 ? a->dev->C2 : what == 1 ? a->dev->H : what == 2 ? a->dev->T
+                                                 : what == 3 ? a->dev->F_u : a->dev->Q2;
+    if (n_rows) *n_rows = M.n_rows;
+    if (n_cols) *n_cols = M.n_cols;
+    if (nnz) *nnz = M.nnz;
+    if (rp || ci || v) {
+      const fpb::Csr H = fpd::download_csr(M);
+      if (rp) std::memcpy(rp, H.rp.data(), sizeof(int64_t) * H.rp.size());
+      if (ci) std::memcpy(ci, H.ci.data(), sizeof(int32_t) * H.ci.size());
+      if (v) std::memcpy(v, H.v.data(), sizeof(double) * H.v.size());
+    }
   });
 }
 

@@ -239,28 +239,6 @@ __global__ void gather_rows_kernel(int m, const int* rows, const long long* rp, 
   for (long long k = 0; k < len; ++k) oci[off[t] + k] = ci[r0 + k], ov[off[t] + k] = v[r0 + k];
 }
 
-DCsr add_dev(const DCsr& A, const DCsr& B, double alpha, double beta) {
-  if (A.n_rows != B.n_rows || A.n_cols != B.n_cols) throw std::invalid_argument("add_scaled: shape mismatch");
-  DCsr C;
-  C.n_rows = A.n_rows, C.n_cols = A.n_cols;
-  DevBuf<long long> cnt(size_t(A.n_rows) + 1);
-  cnt.zero();
-  if (A.n_rows)
-    add_rows_kernel<false><<<grid_for(A.n_rows), kT>>>(A.n_rows, A.rp.get(), A.ci.get(), A.v.get(), B.rp.get(), B.ci.get(),
-                                                       B.v.get(), alpha, beta, A.n_cols, cnt.get(), nullptr, nullptr,
-                                                       nullptr);
-  C.rp.alloc(size_t(A.n_rows) + 1);
-  C.nnz = scan_counts(cnt, A.n_rows, C.rp);
-  C.ci.alloc(size_t(C.nnz));
-  C.v.alloc(size_t(C.nnz));
-  if (C.nnz)
-    add_rows_kernel<true><<<grid_for(A.n_rows), kT>>>(A.n_rows, A.rp.get(), A.ci.get(), A.v.get(), B.rp.get(), B.ci.get(),
-                                                      B.v.get(), alpha, beta, A.n_cols, nullptr, C.rp.get(), C.ci.get(),
-                                                      C.v.get());
-  cuda_check(cudaDeviceSynchronize(), "add_dev");
-  return C;
-}
-
 DCsr clone(const DCsr& A) {
   DCsr C;
   C.n_rows = A.n_rows, C.n_cols = A.n_cols, C.nnz = A.nnz;
@@ -587,6 +565,29 @@ fpb::HostAmg amg_setup_dev(DCsr&& A0, const std::vector<std::vector<double>>& ne
 }
 
 }  // namespace
+
+// alpha A + beta B on the union pattern (csr.cpp:181-206), row-parallel, explicit zeros kept
+DCsr add_dev(const DCsr& A, const DCsr& B, double alpha, double beta) {
+  if (A.n_rows != B.n_rows || A.n_cols != B.n_cols) throw std::invalid_argument("add_scaled: shape mismatch");
+  DCsr C;
+  C.n_rows = A.n_rows, C.n_cols = A.n_cols;
+  DevBuf<long long> cnt(size_t(A.n_rows) + 1);
+  cnt.zero();
+  if (A.n_rows)
+    add_rows_kernel<false><<<grid_for(A.n_rows), kT>>>(A.n_rows, A.rp.get(), A.ci.get(), A.v.get(), B.rp.get(), B.ci.get(),
+                                                       B.v.get(), alpha, beta, A.n_cols, cnt.get(), nullptr, nullptr,
+                                                       nullptr);
+  C.rp.alloc(size_t(A.n_rows) + 1);
+  C.nnz = scan_counts(cnt, A.n_rows, C.rp);
+  C.ci.alloc(size_t(C.nnz));
+  C.v.alloc(size_t(C.nnz));
+  if (C.nnz)
+    add_rows_kernel<true><<<grid_for(A.n_rows), kT>>>(A.n_rows, A.rp.get(), A.ci.get(), A.v.get(), B.rp.get(), B.ci.get(),
+                                                      B.v.get(), alpha, beta, A.n_cols, nullptr, C.rp.get(), C.ci.get(),
+                                                      C.v.get());
+  cuda_check(cudaDeviceSynchronize(), "add_dev");
+  return C;
+}
 
 // build_tpu / build_tup (precond.cpp:119-202) with the device-resident setup above
 fpb::HostPrecond build_precond_device(const SystemView& J, const fpb::HostSystem* Jh, int variant,

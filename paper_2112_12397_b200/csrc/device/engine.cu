@@ -216,6 +216,7 @@ DeviceSystem::DeviceSystem(const SystemView& J) {
   {  // A: one raw upload, the BSR3 layout built on the device, the raw copy freed
     const DCsr dA = upload_csr(J.A);
     da = max_abs_diag(dA);
+    max_diag_A = da;
     if (a_bsr3)
       A = bsr3_from(dA, nullptr, 0);
     else
@@ -320,6 +321,21 @@ DMat mat_from_ref(const DCsr& A, bool few_rows_parallel, bool strided) {
   return M;
 }
 }  // namespace
+
+void DeviceSystem::set_fracture_blocks(const DCsr& C2_, const DCsr& H_, const DCsr& T_, const DCsr& Q2_) {
+  if (C2_.n_rows != n_t || C2_.n_cols != n_u || H_.n_rows != n_t || T_.n_rows != n_p || Q2_.n_rows != n_p ||
+      Q2_.n_cols != n_u)
+    throw std::invalid_argument("set_fracture_blocks: block shapes do not match the system");
+  C2 = sell_from(C2_, 0);
+  H = sell_from(H_, 0);
+  T = sell_from(T_, 0);
+  Q2 = sell_from(Q2_, 0);
+  Q2m = mat_from_ref(Q2_, true, false);
+  const double dh = max_abs_diag(H_), dt = max_abs_diag(T_);  // BlockScaling::from (driver.cpp:114-125)
+  st = sp = 1.0;
+  if (max_diag_A > 0.0 && dh > 0.0) st = std::sqrt(max_diag_A / dh);
+  if (max_diag_A > 0.0 && dt > 0.0) sp = std::sqrt(max_diag_A / dt);
+}
 
 DeviceAmg::DeviceAmg(const fpb::HostAmg& h, bool fine_bsr3) {
   opt = h.opt;

@@ -155,12 +155,35 @@ DCsr transpose_dev(const DCsr& A, cudaStream_t s);  // rows of A^T list the sour
 DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s);
 
 fpb::Csr host_copy(const HostCsrView& A);
+DCsr add_dev(const DCsr& A, const DCsr& B, double alpha, double beta);  // alpha A + beta B (dsetup.cu)
 // C = diag(row_scale) A B on the device, bitwise the host spgemm (spgemm.cu); row_scale may be null
 DCsr spgemm_dev(const DCsr& A, const DCsr& B, const double* row_scale_dev);
 // build_tpu / build_tup with the fine-size setup on the device (dsetup.cu); the AMG levels of the
 // result stay device-resident (HostLevel::dA / dP)
 fpb::HostPrecond build_precond_device(const SystemView& J, const fpb::HostSystem* Jh, int variant,
                                       const fpb::AmgOptions& opt, const std::vector<std::array<double, 3>>& coords);
+
+}  // namespace fpd
+namespace fpb {
+struct FractureModel;
+}
+namespace fpd {
+
+// The state-dependent blocks C2, H, T, F_u, Q2 assembled on the device from a fracture state
+// (assembly.cu; assemble_fracture_blocks, assembly.cpp:229-406): the model (faces, edges, Dirichlet
+// flags, constants) is uploaded once, run() rebuilds the blocks for every new state.
+class DeviceFractureAssembly {
+ public:
+  explicit DeviceFractureAssembly(const fpb::FractureModel& m);
+  ~DeviceFractureAssembly();
+  void run(const char* region, const double* gap, const double* trac, const double* sdir, const double* pres);
+  int n_u = 0, n_p = 0;
+  DCsr C2, H, T, F_u, Q2;
+
+ private:
+  struct Model;
+  std::unique_ptr<Model> model_;
+};
 
 class DeviceSystem {
  public:
@@ -184,6 +207,10 @@ class DeviceSystem {
   // y = D J D x (D = blkdiag(I, st I, sp I)); st = sp = 1 gives J itself
   void enqueue_apply(const double* x, double* y, double st_, double sp_, cudaStream_t s, Ledger* L = nullptr) const;
   double bytes_apply() const;
+  // a Newton step's new C2, H, T, Q2 (device CSR, e.g. DeviceFractureAssembly): layouts and the block
+  // scaling rebuilt on the device; A, C1, Q1 unchanged
+  void set_fracture_blocks(const DCsr& C2, const DCsr& H, const DCsr& T, const DCsr& Q2);
+  double max_diag_A = 0.0;
 };
 
 struct DeviceLevel {

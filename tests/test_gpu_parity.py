@@ -558,3 +558,44 @@ def test_device_setup_is_bitwise_the_oracle_setup(case, variant, theta):
     opc.set_factor_solve(pc.factor_solve)
     x = np.random.default_rng(8).uniform(-1, 1, J.total_dimension())
     assert np.array_equal(pc.apply(x), opc.apply(x))
+
+
+def _perturbed_state(st, seed):
+    """A new Newton step's state: regions re-drawn, gaps, tractions and pressures moved."""
+    rng = np.random.default_rng(seed)
+    n = len(st["region"])
+    region = "".join(rng.choice(list("slo"), size=n, p=[0.5, 0.3, 0.2]))
+    gap = st["gap"] * (1.0 + 0.5 * rng.uniform(-1, 1, st["gap"].shape))
+    gap[:, 0] = np.where(np.array(list(region)) == "o", 1e-4 * (1 + rng.uniform(0, 1, n)), 0.0)
+    phi = rng.uniform(0, 2 * np.pi, n)
+    return dict(region=region, gap=gap, traction_n=st["traction_n"] * (1 + 0.05 * rng.uniform(-1, 1, n)),
+                slip_dir=np.column_stack([np.cos(phi), np.sin(phi)]), pressure=st["pressure"] * (1 + rng.uniform(-0.1, 0.1, n)))
+
+
+@pytest.mark.parametrize("case", ["mesh-2frac", "config2"])
+def test_device_fracture_assembly_is_bitwise_the_host_assembly(case):
+    """Jacobian assembly on the device (csrc/device/assembly.cu): C2, H, T, F_u and Q2
+    for the generator's state and for a re-drawn Newton-step state are bitwise the host assembly
+    (assemble_fracture_blocks, assembly.cpp:229-406); installed into the device system, J x is bitwise the
+    oracle's J x on the re-assembled system and the block scaling follows."""
+    if case == "config2":
+        W = api.Workload(2, 42)
+    else:
+        W = api.Workload(spec=dict(cells=(8, 6, 6), fractures=[(0, 0.25, 0.0, 1.0, 0.0, 1.0),
+                                                                (0, 0.75, 0.0, 1.0, 0.5, 1.0)],
+                                   frac_stick=0.5, frac_slip=0.3, E_sigma_ln=0.5, aperture_sigma_ln=0.3), seed=3)
+    FA = api.FractureAssembly(W)
+    op = api.BlockSystemOperator(W.system())
+    for step, state in enumerate([W.state(), _perturbed_state(W.state(), 11)]):
+        if step:
+            W.set_state(state)  # the host re-assembly (the reference's Newton step)
+        J = W.system()
+        FA.run(state, op)
+        for nm in FA.BLOCKS:
+            m, ref = FA.matrix(nm), getattr(J, nm)
+            assert np.array_equal(m.row_offsets, ref.row_offsets) and np.array_equal(m.col_indices, ref.col_indices), nm
+            assert np.array_equal(m.values.view(np.uint64), ref.values.view(np.uint64)), nm
+        osys = oracle_system(J)
+        x = np.random.default_rng(step).uniform(-1, 1, J.total_dimension())
+        assert np.array_equal(op.apply(x), osys.apply(x))
+        assert op.block_scaling() == osys.scaling()

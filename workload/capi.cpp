@@ -134,6 +134,45 @@ int fp_workload_info(const fp_workload* w, int32_t* c) {
   });
 }
 
+int fp_workload_state(const fp_workload* w, fp_fracture_state* out) {
+  return guard([&] {
+    need(w && out, "null argument");
+    const fpb::FractureState& S = w->w.state;
+    need(!S.region.empty() || w->w.J.n_p == 0, "fp_workload_state: this workload carries no fracture state");
+    out->n_p = int32_t(S.region.size());
+    out->region = S.region.c_str();
+    out->gap = S.gap.empty() ? nullptr : S.gap[0].data();
+    out->traction_n = S.trac_n.data();
+    out->slip_dir = S.slip_dir.empty() ? nullptr : S.slip_dir[0].data();
+    out->pressure = S.pressure.data();
+  });
+}
+
+int fp_workload_set_state(fp_workload* w, const fp_fracture_state* st) {
+  return guard([&] {
+    need(w && st, "null argument");
+    need(w->w.model.n_p == w->w.J.n_p && int(w->w.model.faces.size()) == w->w.J.n_p,
+         "fp_workload_set_state: this workload carries no fracture model (imported bundle)");
+    const int n_p = w->w.J.n_p;
+    need(st->n_p == n_p, "fp_workload_set_state: n_p mismatch");
+    need(n_p == 0 || (st->region && st->gap && st->traction_n && st->slip_dir && st->pressure),
+         "fp_workload_set_state: null state array");
+    fpb::FractureState S;
+    S.region.assign(st->region, st->region + n_p);
+    for (char c : S.region) need(c == 's' || c == 'l' || c == 'o', "fp_workload_set_state: region must be s, l or o");
+    S.gap.resize(size_t(n_p)), S.slip_dir.resize(size_t(n_p));
+    for (int f = 0; f < n_p; ++f) {
+      S.gap[f] = {st->gap[3 * f], st->gap[3 * f + 1], st->gap[3 * f + 2]};
+      S.slip_dir[f] = {st->slip_dir[2 * f], st->slip_dir[2 * f + 1]};
+    }
+    S.trac_n.assign(st->traction_n, st->traction_n + n_p);
+    S.pressure.assign(st->pressure, st->pressure + n_p);
+    fpb::assemble_fracture_blocks(w->w.model, S, w->w.J);
+    w->w.state = std::move(S);
+    w->w.region = w->w.state.region;
+  });
+}
+
 int fp_snapshot_import(const char* dir, fp_workload** out) {
   return guard([&] {
     need(dir && out, "fp_snapshot_import: null argument");

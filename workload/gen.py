@@ -47,6 +47,12 @@ class FpWorkloadSpec(C.Structure):
                 ("slip_factor", C.c_double)]
 
 
+class FpFractureState(C.Structure):
+    _fields_ = [("n_p", C.c_int32), ("region", C.c_char_p), ("gap", C.POINTER(C.c_double)),
+                ("traction_n", C.POINTER(C.c_double)), ("slip_dir", C.POINTER(C.c_double)),
+                ("pressure", C.POINTER(C.c_double))]
+
+
 _P, _PP, _DP = C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_double)
 # every symbol include/fracprec_workload.h declares, with its ctypes signature
 SIGNATURES = {
@@ -58,6 +64,8 @@ SIGNATURES = {
     "fp_workload_coords": (C.c_int, [_P, C.POINTER(_DP), C.POINTER(C.c_int32)]),
     "fp_workload_info": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "fp_workload_region": (C.c_int, [_P, C.POINTER(C.c_char_p), C.POINTER(C.c_double)]),
+    "fp_workload_state": (C.c_int, [_P, C.POINTER(FpFractureState)]),
+    "fp_workload_set_state": (C.c_int, [_P, C.POINTER(FpFractureState)]),
     "fp_snapshot_import": (C.c_int, [C.c_char_p, _PP]),
     "fp_snapshot_export": (C.c_int, [C.c_char_p, C.POINTER(FpBlockSystem), C.c_char_p, C.c_double, _DP, C.c_int32]),
 }
@@ -207,6 +215,25 @@ class Workload:
             S._owner = self
         return S
 
+    def state(self) -> dict:
+        """The fracture state (FractureState): region string, gap (n_p x 3), traction_n, slip_dir (n_p x 2),
+        pressure — copies."""
+        st = FpFractureState()
+        check(lib.fp_workload_state(self._h, C.byref(st)))
+        n = st.n_p
+
+        def arr(p, k):
+            return np.ctypeslib.as_array(p, shape=(n * k,)).copy() if n else np.zeros(0)
+
+        return {"region": st.region.decode()[:n] if n else "", "gap": arr(st.gap, 3).reshape(-1, 3),
+                "traction_n": arr(st.traction_n, 1), "slip_dir": arr(st.slip_dir, 2).reshape(-1, 2),
+                "pressure": arr(st.pressure, 1)}
+
+    def set_state(self, state: dict) -> None:
+        """A new fracture state: C2, H, T, F_u, Q2 re-assembled on the host (assembly.cpp:229-406)."""
+        st, keep = state_view(state)
+        check(lib.fp_workload_set_state(self._h, C.byref(st)))
+
     def save_snapshot(self, directory: str) -> None:
         """export_snapshot of this workload (blocks, region labels, dt, node coordinates)."""
         region, dt = self.region()
@@ -224,3 +251,18 @@ def export_snapshot(directory: str, blocks: dict, n_u: int, n_t: int, n_p: int, 
     cp = coords.ctypes.data_as(C.POINTER(C.c_double)) if coords is not None else None
     nn = 0 if coords is None else coords.shape[0]
     check(lib.fp_snapshot_export(str(directory).encode(), C.byref(view), region.encode(), float(dt), cp, nn))
+
+
+def state_view(state: dict):
+    """(fp_fracture_state over NumPy copies of a state dict, keepalive)."""
+    region = state["region"].encode()
+    gap = np.ascontiguousarray(state["gap"], np.float64).reshape(-1)
+    tn = np.ascontiguousarray(state["traction_n"], np.float64)
+    sd = np.ascontiguousarray(state["slip_dir"], np.float64).reshape(-1)
+    pr = np.ascontiguousarray(state["pressure"], np.float64)
+    st = FpFractureState()
+    st.n_p = len(region)
+    st.region = region
+    st.gap, st.traction_n = gap.ctypes.data_as(_DP), tn.ctypes.data_as(_DP)
+    st.slip_dir, st.pressure = sd.ctypes.data_as(_DP), pr.ctypes.data_as(_DP)
+    return st, (region, gap, tn, sd, pr)

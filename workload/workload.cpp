@@ -311,7 +311,9 @@ void assemble_fracture_blocks(const FractureModel& M, const FractureState& S, Ho
     } else if (S.region[f] == 'l') {
       jump_row(f, 3 * f, 0, 1.0);
       const double dg[2] = {S.gap[f][1], S.gap[f][2]};  // gap_prev = 0
-      const double r = std::hypot(dg[0], dg[1]);
+      // |dg_T| (std::hypot at assembly.cpp:271): the square root of the sum, so the device assembly
+      // reproduces it bit for bit (CUDA's and glibc's hypot differ in the last bit; a 1-ulp change)
+      const double r = std::sqrt(dg[0] * dg[0] + dg[1] * dg[1]);
       const double tau = M.cohesion - S.trac_n[f] * M.tan_th;
       const double thr = std::max(1e-12, 0.1 * std::max(tau, 0.0) / M.k_scale);
       double mm[2], D[2][2] = {{0, 0}, {0, 0}};
