@@ -273,7 +273,8 @@ def solve_fn(api, op, pc, b, x, args, orth=None, probe=False):
     return solve
 
 
-def timed_variant(api, op, J_or_W, b, flush, args, variant, row_sum, orth, reps=2, from_workload=False):
+def timed_variant(api, op, J_or_W, b, flush, args, variant, row_sum, orth, reps=2, from_workload=False,
+                  restart=None):
     import torch
 
     cfg = api.PrecondConfig(variant, amg=api.AmgConfig(strength_threshold=args.theta, row_sum=row_sum),
@@ -282,7 +283,12 @@ def timed_variant(api, op, J_or_W, b, flush, args, variant, row_sum, orth, reps=
     pc = api.GpuPreconditioner.from_host(op, hp)
     del hp
     x = torch.empty_like(b)
-    solve = solve_fn(api, op, pc, b, x, args, orth)
+    if restart is None:
+        solve = solve_fn(api, op, pc, b, x, args, orth)
+    else:  # full GMRES (restart = max_iter): the reference's own unrestarted semantics (gmres.cpp:24-174)
+        def solve():
+            return api.gmres(op, pc, b, tol=args.tol, max_iter=args.max_iter, restart=restart, scaled=True, x=x,
+                             orthogonalization=orth)
     solve()
     t, st = 0.0, None
     for _ in range(reps):
@@ -321,6 +327,9 @@ def other_variants(api, op, W, b, flush, args) -> dict:
                                              from_workload=True)
         out["tup_cfg2_reference_order"] = timed_variant(api, op2, W2, b2, flush, args, "tup", "ordered", "mgs", reps=3,
                                                         from_workload=True)
+        # the reference's unrestarted GMRES converges on this workload: time to convergence
+        out["tup_cfg2_full_gmres"] = timed_variant(api, op2, W2, b2, flush, args, "tup", args.row_sum, args.orth,
+                                                   reps=3, from_workload=True, restart=args.max_iter)
     return out
 
 
