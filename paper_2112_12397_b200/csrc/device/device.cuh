@@ -110,7 +110,8 @@ struct PanelView {
   const long long* off = nullptr;   // per block: offset of its panel matrices
   const double* m = nullptr;
   const double* diag = nullptr;     // spd: D (z = y / D between the sweeps); null for general
-  double* scratch = nullptr;        // n doubles: z between the forward and the backward chain
+  int m_max = 0;                    // largest block (rows): the kernel keeps the block's z in shared memory
+  int p_max_panels = 0;             // most panels of a block: each warp keeps its own rows of x per panel
 };
 
 struct DenseLUView {  // coarse-level full-pivot LU, column-major n x n

@@ -741,6 +741,20 @@ struct UploadClock {  // FRACPREC_B200_VERBOSE: phases of the preconditioner upl
 };
 }  // namespace
 
+namespace {
+// shared memory of panel_solve_kernel: the largest block's z (m_max) + each warp's own rows
+// (most panels x rows per warp of the instantiation the largest panel selects)
+size_t panel_smem_bytes(const fpb::BandFactor& F, const std::vector<int>& pp) {
+  int m_max = 0, P_max = 0, p_max = 1;
+  for (size_t b = 0; b < pp.size(); ++b) {
+    const int m = F.block_start[b + 1] - F.block_start[b];
+    m_max = std::max(m_max, m), P_max = std::max(P_max, (m + pp[b] - 1) / pp[b]), p_max = std::max(p_max, pp[b]);
+  }
+  const int R = p_max <= 64 ? 1 : p_max <= 128 ? 2 : 4;
+  return sizeof(double) * (size_t(m_max) + size_t(kPanelThreads / 32) * size_t(P_max) * R);
+}
+}  // namespace
+
 DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) : variant(hp.variant), sys(&s) {
   UploadClock uclk;
   if (hp.amg.levels.empty() || hp.S().n_rows != s.n_u) throw std::invalid_argument("precond upload: inner operator size != n_u");
@@ -817,6 +831,7 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
       pp[blk] = p;
     }
     for (int p : pp) panel_ok = panel_ok && p <= kPanelMax;
+    panel_ok = panel_ok && panel_smem_bytes(F, pp) <= 220 * 1024;  // the block's z and own rows in shared memory
   }
   if (hp.factor_solve == 3 && !panel_ok)
     throw std::invalid_argument("precond upload: factor_solve = panel needs a factor without row interchanges");
@@ -850,11 +865,20 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
     pan_p.upload(pp);
     pan_off.upload(off);
     pan_pmax = *std::max_element(pp.begin(), pp.end());
+    pan_smem = panel_smem_bytes(F, pp);
+    for (auto k : {panel_solve_kernel<1, 2>, panel_solve_kernel<2, 4>, panel_solve_kernel<4, 8>})
+      cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pan_smem)),
+                 "panel smem attribute");
     pan_m.alloc(size_t(off.back()));
-    pan_scratch.alloc(size_t(F.n));
+
     pan_bytes = 8.0 * double(off.back());
+    int m_max = 0, pmax_panels = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int m = F.block_start[blk + 1] - F.block_start[blk];
+      m_max = std::max(m_max, m), pmax_panels = std::max(pmax_panels, (m + pp[blk] - 1) / pp[blk]);
+    }
     pview = PanelView{nblk, band_start.get(), pan_p.get(), pan_off.get(), pan_m.get(),
-                      F.kind == fpb::BandFactor::Kind::spd ? band_diag.get() : nullptr, pan_scratch.get()};
+                      F.kind == fpb::BandFactor::Kind::spd ? band_diag.get() : nullptr, m_max, pmax_panels};
     DevBuf<int> dtb, dtq;
     dtb.upload(tb), dtq.upload(tq);
     const long long threads = (long long)tb.size() * 4 * kPanelMax;
@@ -903,12 +927,13 @@ void DevicePrecond::enqueue_band(const double* rhs, double rs, double* out, doub
   const double vec_bytes = 8.0 * band.n * (2 + (mode == 1) + (mode == 2));
   if (panel) {
     const dim3 g(unsigned(pview.n_blocks) * kPanelCluster), b(kPanelThreads);
+    const size_t smem = pan_smem;
     if (pan_pmax <= 64)
-      launch(panel_solve_kernel<1, 2>, g, b, 0, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
+      launch(panel_solve_kernel<1, 2>, g, b, smem, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
     else if (pan_pmax <= 128)
-      launch(panel_solve_kernel<2, 4>, g, b, 0, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
+      launch(panel_solve_kernel<2, 4>, g, b, smem, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
     else
-      launch(panel_solve_kernel<4, 8>, g, b, 0, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
+      launch(panel_solve_kernel<4, 8>, g, b, smem, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
     if (L) {
       L->add(band_factor_bytes + vec_bytes + 8.0 * band.n);  // + z written and read back between the chains
       L->waste(std::max(0.0, pan_bytes - band_factor_bytes));

@@ -303,7 +303,8 @@ class DevicePrecond {
   PanelView pview{};
   DevBuf<int> pan_p;
   DevBuf<long long> pan_off;
-  DevBuf<double> pan_m, pan_scratch;
+  DevBuf<double> pan_m;
+  size_t pan_smem = 0;
   double pan_bytes = 0;
   int pan_pmax = 0;
   DinvView dinv{};

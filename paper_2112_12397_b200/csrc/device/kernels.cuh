@@ -1035,13 +1035,16 @@ __device__ __forceinline__ double warp_tree(double s) {
 
 // one chain (forward: D = H, C = G, x = rs b; backward: D = K, C = F, x = z) over the block's panels;
 // before each cluster barrier a warp already loads the next panel's coupling rows into registers and
-// forms its local product, so a step's critical path is the barrier plus a shared-memory dot.
+// forms its local product, so a step's critical path is the barrier plus a shared-memory dot.  A step
+// touches no global memory: the forward chain broadcasts y into every CTA's chain buffer and z = y / D
+// into every CTA's copy of the block's z (zs, the backward chain's input), the backward chain keeps
+// the rows its warps own (own) and writes them out after the last barrier.
 // R rows of a panel per warp and E entries of a row per lane (templated so a step issues only the
 // instructions the block's panel size needs: p <= 64 * R, p <= 32 * E).
 template <bool fwd, int R, int E>
 __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw, int lane, double (*chain)[kPanelMax],
-                                            const double* xin, double xs, double* out, double* out2, const double* sub,
-                                            double os, int out_mode, cooperative_groups::cluster_group& cluster) {
+                                            double* zs, double* own, const double* xin, double xs,
+                                            cooperative_groups::cluster_group& cluster) {
   const int b0 = V.block_start[blk], m = V.block_start[blk + 1] - b0, p = V.p[blk], P = (m + p - 1) / p;
   const double* base = V.m + V.off[blk];
   auto rows_of = [&](int q) { return min(p, m - q * p); };
@@ -1049,17 +1052,17 @@ __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw,
     const int s = rows_of(q), sp = q > 0 ? p : 0, sn = q + 1 < P ? rows_of(q + 1) : 0;
     return s * s + s * sp + s * s + s * sn;
   };
-  double dl[R], cr[R][E];
-  // panel q's local product D_q x_q and coupling rows C_q, for this warp's rows
+  double dl[R], cr[R][E], dg[R];
+  // panel q's local product D_q x_q and coupling rows C_q (and the forward's D), for this warp's rows
   auto prefetch = [&](int q, int o) {
     const int s = rows_of(q), sc = fwd ? (q > 0 ? p : 0) : (q + 1 < P ? rows_of(q + 1) : 0);
     const double* Dm = base + o + (fwd ? 0 : s * s + s * (q > 0 ? p : 0));
     const double* Cm = Dm + s * s;
-    const double* xq = xin + b0 + q * p;
+    const double* xq = fwd ? xin + b0 + q * p : zs + q * p;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = gw + r * kPanelWarps;
-      if (i - lane >= s - lane) break;  // warp-uniform: i is the same in every lane
+      if (i >= s) break;  // warp-uniform
       double acc = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
@@ -1068,6 +1071,7 @@ __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw,
         cr[r][e] = c < sc ? Cm[i * sc + c] : 0.0;
       }
       dl[r] = warp_tree(acc);
+      if (fwd) dg[r] = V.diag ? V.diag[b0 + q * p + i] : 1.0;
     }
   };
   int o = 0;
@@ -1091,16 +1095,11 @@ __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw,
       }
       const double v = sc ? dl[r] - acc : dl[r];
       if (lane < kPanelCluster) *cluster.map_shared_rank(&chain[q & 1][i], lane) = v;
-      if (lane == 0) {
-        const long long row = b0 + (long long)q * p + i;
-        if (fwd) {
-          V.scratch[row] = V.diag ? v / V.diag[row] : v;  // z = y / D (LDL^T), else y
-        } else if (out_mode == 1) {
-          out[row] = (sub[row] - v) * os;
-        } else {
-          out[row] = v;
-          if (out_mode == 2) out2[row] = v * os;
-        }
+      if (fwd) {
+        if (lane >= 8 && lane < 8 + kPanelCluster)  // z = y / D (LDL^T), else y
+          *cluster.map_shared_rank(&zs[q * p + i], lane - 8) = V.diag ? v / dg[r] : v;
+      } else if (lane == 0) {
+        own[q * R + r] = v;
       }
     }
     cluster_arrive();
@@ -1120,12 +1119,30 @@ __global__ void __cluster_dims__(kPanelCluster, 1, 1) __launch_bounds__(kPanelTh
   pdl_entry();
   cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
   __shared__ double chain[2][kPanelMax];  // the previous panel of the running chain (y or x)
+  extern __shared__ double pan_dyn[];     // the block's z (m doubles), then each warp's own x rows
   const int rank = int(cluster.block_rank());
   const int blk = blockIdx.x / kPanelCluster;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = rank * (kPanelThreads / 32) + warp;
-  panel_chain<true, R, E>(V, blk, gw, lane, chain, rhs, rs, nullptr, nullptr, nullptr, 1.0, 0, cluster);
-  panel_chain<false, R, E>(V, blk, gw, lane, chain, V.scratch, 1.0, out, out2, sub, os, out_mode, cluster);
+  const int b0 = V.block_start[blk], m = V.block_start[blk + 1] - b0, p = V.p[blk], P = (m + p - 1) / p;
+  double* zs = pan_dyn;
+  double* own = pan_dyn + V.m_max + warp * (V.p_max_panels * R);
+  panel_chain<true, R, E>(V, blk, gw, lane, chain, zs, own, rhs, rs, cluster);
+  panel_chain<false, R, E>(V, blk, gw, lane, chain, zs, own, zs, 1.0, cluster);
+  if (lane == 0)
+    for (int q = 0; q < P; ++q)
+      for (int r = 0; r < R; ++r) {
+        const int i = gw + r * kPanelWarps;
+        if (i >= min(p, m - q * p)) break;
+        const long long row = b0 + (long long)q * p + i;
+        const double x = own[q * R + r];
+        if (out_mode == 1) {
+          out[row] = (sub[row] - x) * os;
+        } else {
+          out[row] = x;
+          if (out_mode == 2) out2[row] = x * os;
+        }
+      }
 }
 
 // Builds the panel matrices from the band factor (upload): one thread per (panel, column, matrix),
