@@ -45,6 +45,8 @@ typedef struct fp_workload_spec {
 typedef struct fp_workload fp_workload;
 
 const char* fp_workload_last_error(void);
+/* layout fingerprint of the C++ handle types (workload/workload.hpp): the solve library checks it */
+uint64_t fp_workload_layout(void);
 
 /* config_id 1..5 = BASELINE.json configs[0..4] */
 int fp_workload_preset(int32_t config_id, uint64_t seed, fp_workload** out);

@@ -239,6 +239,13 @@ void ensure_setup_backend() {
   g_setup_device = has && !(e && std::strcmp(e, "host") == 0) ? 1 : 0;
 }
 
+// the generator library and this one share fp_workload's C++ layout (workload.hpp): refuse a stale build
+void check_workload_layout() {
+  if (fp_workload_layout() != workload_layout_fingerprint())
+    throw std::runtime_error("libfp_workload.so and libfracprec_b200.so were built from different workload.hpp "
+                             "versions; rebuild both (python -m paper_2112_12397_b200.build)");
+}
+
 fpb::HostPrecond build_any(const fpd::SystemView& V, const fpb::HostSystem* H, int variant, const fpb::AmgOptions& o,
                            const std::vector<std::array<double, 3>>& xyz) {
   ensure_setup_backend();
@@ -640,6 +647,7 @@ int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config
   return guard([&] {
     ensure_setup_backend();
     need(w && cfg && out, "fp_workload_host_precond_build: null argument");
+    check_workload_layout();
     need(cfg->factor_solve >= FP_FACTOR_AUTO && cfg->factor_solve <= FP_FACTOR_PANEL, "unknown factor_solve");
     auto p = std::make_unique<fp_host_precond>();
     p->hp = build_any(fpd::SystemView::of(w->w.J), &w->w.J, cfg->variant, to_amg(cfg->amg), w->w.coords);
@@ -652,6 +660,7 @@ int fp_workload_host_precond_build(const fp_workload* w, const fp_precond_config
 int fp_fracture_assembly_create(const fp_workload* w, fp_fracture_assembly** out) {
   return guard([&] {
     need(w && out, "fp_fracture_assembly_create: null argument");
+    check_workload_layout();
     auto a = std::make_unique<fp_fracture_assembly>();
     a->dev = std::make_unique<fpd::DeviceFractureAssembly>(w->w.model);
     *out = a.release();

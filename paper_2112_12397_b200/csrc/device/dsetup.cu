@@ -225,6 +225,125 @@ __global__ void gather_w_kernel(int m, const int* rows, const long long* off, co
   for (long long k = k0; k < k1; ++k) out[pos[t] + (k - k0)] = w[k];
 }
 
+// ---- tentative prolongation (amg.cpp:214-257): one thread per aggregate runs the column-pivoted
+// Householder QR of its near-null block B (m rows x k columns): pivot = first column of largest remaining
+// norm (norms recomputed each step), reflectors in Eigen's makeHouseholder form, rank |R_jj| >
+// 1e-12 max(1, |R_00|), Q = the first `rank` columns of H_0 ... H_mn-1 applied to unit vectors,
+// Rp = R(0:rank, :) P^T.  W (m x k, column-major) and Q live in per-aggregate global scratch.
+__device__ double householder_dev(double* x, int len) {
+  double tail = 0.0;
+  for (int i = 1; i < len; ++i) tail += x[i] * x[i];
+  const double c0 = x[0];
+  if (tail <= 2.2250738585072014e-308) {  // DBL_MIN
+    for (int i = 1; i < len; ++i) x[i] = 0.0;
+    return 0.0;
+  }
+  double beta = sqrt(c0 * c0 + tail);
+  if (c0 >= 0.0) beta = -beta;
+  const double denom = c0 - beta;
+  for (int i = 1; i < len; ++i) x[i] = x[i] / denom;
+  x[0] = beta;
+  return (beta - c0) / beta;
+}
+
+constexpr int kQrMaxK = 8;
+
+__global__ void qr_aggregates_kernel(int n_agg, int k, int n, const int* a_off, const int* a_rows, const double* nn,
+                                     double* W, double* Q, int* rank_out, double* Rp) {
+  const long long a = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (a >= n_agg) return;
+  const int r0 = a_off[a], m = a_off[a + 1] - r0;
+  double* w = W + (long long)r0 * k;  // column c at w + c m
+  for (int c = 0; c < k; ++c)
+    for (int r = 0; r < m; ++r) w[c * m + r] = nn[(long long)c * n + a_rows[r0 + r]];
+  int perm[kQrMaxK];
+  double tau[kQrMaxK];
+  for (int j = 0; j < k; ++j) perm[j] = j;
+  const int mn = min(m, k);
+  for (int j = 0; j < mn; ++j) {
+    int p = j;
+    double best = -1.0;
+    for (int c = j; c < k; ++c) {
+      double sq = 0.0;
+      for (int i = j; i < m; ++i) sq += w[c * m + i] * w[c * m + i];
+      if (sq > best) best = sq, p = c;
+    }
+    if (p != j) {
+      for (int i = 0; i < m; ++i) {
+        const double t = w[j * m + i];
+        w[j * m + i] = w[p * m + i], w[p * m + i] = t;
+      }
+      const int t = perm[j];
+      perm[j] = perm[p], perm[p] = t;
+    }
+    tau[j] = householder_dev(w + j * m + j, m - j);
+    for (int c = j + 1; c < k; ++c) {
+      double sv = w[c * m + j];
+      for (int i = j + 1; i < m; ++i) sv += w[j * m + i] * w[c * m + i];
+      sv *= tau[j];
+      w[c * m + j] -= sv;
+      for (int i = j + 1; i < m; ++i) w[c * m + i] -= sv * w[j * m + i];
+    }
+  }
+  const double r00 = mn > 0 ? fabs(w[0]) : 0.0;
+  const double tol = 1e-12 * fmax(1.0, r00);
+  int rank = 0;
+  for (int j = 0; j < mn; ++j)
+    if (fabs(w[j * m + j]) > tol) ++rank;
+  rank_out[a] = rank;
+  double* q = Q + (long long)r0 * k;  // column c at q + c m
+  for (int c = 0; c < rank; ++c) {
+    double* qc = q + c * m;
+    for (int i = 0; i < m; ++i) qc[i] = 0.0;
+    qc[c] = 1.0;
+    for (int j = min(c, mn - 1); j >= 0; --j) {
+      double sv = qc[j];
+      for (int i = j + 1; i < m; ++i) sv += w[j * m + i] * qc[i];
+      sv *= tau[j];
+      qc[j] -= sv;
+      for (int i = j + 1; i < m; ++i) qc[i] -= sv * w[j * m + i];
+    }
+  }
+  double* rp = Rp + a * (long long)k * k;
+  for (int r = 0; r < rank; ++r) {
+    for (int j = 0; j < k; ++j) rp[r * k + j] = 0.0;
+    for (int j = r; j < k; ++j) rp[r * k + perm[j]] = w[j * m + r];
+  }
+}
+
+// tentative P: row i (in aggregate a at local position r) holds the nonzero Q entries of a in
+// ascending coarse column order; fill == false counts them
+template <bool fill>
+__global__ void ptent_kernel(int n, int k, const int* agg, const int* local, const int* a_off, const int* rank,
+                             const int* coff, const double* Q, long long* cnt, const long long* rp, int* ci, double* v) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long long c_out = 0, o = fill ? rp[i] : 0;
+  const int a = agg[i];
+  if (a >= 0) {
+    const int m = a_off[a + 1] - a_off[a];
+    const double* q = Q + (long long)a_off[a] * k;
+    for (int c = 0; c < rank[a]; ++c) {
+      const double val = q[c * m + local[i]];
+      if (val != 0.0) {
+        if (fill) ci[o] = coff[a] + c, v[o] = val, ++o;
+        ++c_out;
+      }
+    }
+  }
+  if (!fill) cnt[i] = c_out;
+}
+
+// the next level's near-null space: nnc[c][coff[a] + r] = Rp_a(r, c) (amg.cpp:269-274)
+__global__ void coarse_nn_kernel(int n_agg, int k, int nc, const int* rank, const int* coff, const double* Rp,
+                                 double* nnc) {
+  const long long a = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (a >= n_agg) return;
+  const double* rp = Rp + a * (long long)k * k;
+  for (int r = 0; r < rank[a]; ++r)
+    for (int c = 0; c < k; ++c) nnc[(long long)c * nc + coff[a] + r] = rp[r * k + c];
+}
+
 // rows rows[0..m) of A, packed (the fixed-stress neighbourhoods)
 __global__ void gather_len_kernel(int m, const int* rows, const long long* rp, long long* cnt) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -429,6 +548,13 @@ fpb::HostAmg amg_setup_dev(DCsr&& A0, const std::vector<std::vector<double>>& ne
       near_null.empty() ? std::vector<std::vector<double>>{std::vector<double>(size_t(A0.n_rows), 1.0)} : near_null;
   for (const auto& v : nn)
     if (int(v.size()) != A0.n_rows) throw std::invalid_argument("amg_setup: near-null vector length mismatch");
+  const int k = int(nn.size());
+  DevBuf<double> nn_dev(size_t(k) * A0.n_rows);  // the near-null vectors, k columns of n
+  for (int c = 0; c < k; ++c)
+    if (A0.n_rows)
+      cuda_check(cudaMemcpy(nn_dev.get() + size_t(c) * A0.n_rows, nn[c].data(), sizeof(double) * A0.n_rows,
+                            cudaMemcpyHostToDevice), "near-null upload");
+  nn.clear();
   {
     fpb::HostLevel f;
     f.diag = diag_dev(A0);
@@ -454,7 +580,6 @@ fpb::HostAmg amg_setup_dev(DCsr&& A0, const std::vector<std::vector<double>>& ne
     }
     clk.mark("aggregate (host BFS)", n_agg);
     if (n_agg == 0) break;
-    const int k = int(nn.size());
     std::vector<int> a_off(static_cast<size_t>(n_agg) + 1, 0), a_rows;
     for (int i = 0; i < n; ++i)
       if (agg[i] >= 0) ++a_off[size_t(agg[i]) + 1];
@@ -465,50 +590,44 @@ fpb::HostAmg amg_setup_dev(DCsr&& A0, const std::vector<std::vector<double>>& ne
       for (int i = 0; i < n; ++i)
         if (agg[i] >= 0) a_rows[next[agg[i]]++] = i;
     }
-    std::vector<std::vector<double>> qs(static_cast<size_t>(n_agg)), rps(static_cast<size_t>(n_agg));
+    if (k > kQrMaxK) throw std::invalid_argument("amg_setup: more than 8 near-null vectors");
+    // per-aggregate QR and the tentative P on the device (nn: k vectors of n, column-major in HBM)
+    DevBuf<int> d_aoff, d_arows, d_agg, d_local, d_rank(static_cast<size_t>(n_agg)), d_coff;
+    d_aoff.upload(a_off), d_arows.upload(a_rows), d_agg.upload(agg);
+    std::vector<int> local(static_cast<size_t>(n), -1);
+    for (int ag = 0; ag < n_agg; ++ag)
+      for (int r = a_off[ag]; r < a_off[ag + 1]; ++r) local[a_rows[r]] = r - a_off[ag];
+    d_local.upload(local);
+    DevBuf<double> W(size_t(a_off[n_agg]) * k), Qd(size_t(a_off[n_agg]) * k), Rp(size_t(n_agg) * k * k);
+    if (n_agg)
+      qr_aggregates_kernel<<<grid_for(n_agg), kT>>>(n_agg, k, n, d_aoff.get(), d_arows.get(), nn_dev.get(), W.get(),
+                                                     Qd.get(), d_rank.get(), Rp.get());
     std::vector<int> rank(static_cast<size_t>(n_agg));
-#pragma omp parallel for schedule(dynamic, 64)
-    for (int a = 0; a < n_agg; ++a) {
-      const int m = a_off[a + 1] - a_off[a];
-      std::vector<double> B(size_t(m) * k);
-      for (int c = 0; c < k; ++c)
-        for (int r = 0; r < m; ++r) B[size_t(c) * m + r] = nn[c][a_rows[a_off[a] + r]];
-      rank[a] = fpb::qr_colpiv(m, k, B, qs[a], rps[a]);
-    }
+    if (n_agg) cuda_check(cudaMemcpy(rank.data(), d_rank.get(), sizeof(int) * rank.size(), cudaMemcpyDeviceToHost), "ranks");
+    W = DevBuf<double>();
     std::vector<int> coff(static_cast<size_t>(n_agg) + 1, 0);
-    for (int a = 0; a < n_agg; ++a) coff[size_t(a) + 1] = coff[a] + rank[a];
+    for (int ag = 0; ag < n_agg; ++ag) coff[size_t(ag) + 1] = coff[ag] + rank[ag];
     const int nc = coff[n_agg];
     if (nc == 0) break;
-    fpb::Csr Pt_host(n, nc);  // tentative P (host), then uploaded
+    d_coff.upload(coff);
+    DCsr P;
+    P.n_rows = n, P.n_cols = nc;
     {
-      std::vector<int> local(static_cast<size_t>(n), -1);
-      for (int a = 0; a < n_agg; ++a)
-        for (int r = a_off[a]; r < a_off[a + 1]; ++r) local[a_rows[r]] = r - a_off[a];
-      for (int i = 0; i < n; ++i) {
-        int cnt = 0;
-        if (agg[i] >= 0) {
-          const int a = agg[i], m = a_off[a + 1] - a_off[a];
-          for (int c = 0; c < rank[a]; ++c) cnt += qs[a][size_t(c) * m + local[i]] != 0.0;
-        }
-        Pt_host.rp[size_t(i) + 1] = Pt_host.rp[i] + cnt;
-      }
-      Pt_host.ci.resize(static_cast<size_t>(Pt_host.rp[n]));
-      Pt_host.v.resize(static_cast<size_t>(Pt_host.rp[n]));
-#pragma omp parallel for schedule(static)
-      for (int i = 0; i < n; ++i) {
-        if (agg[i] < 0) continue;
-        const int a = agg[i], m = a_off[a + 1] - a_off[a];
-        int64_t p = Pt_host.rp[i];
-        for (int c = 0; c < rank[a]; ++c) {
-          const double v = qs[a][size_t(c) * m + local[i]];
-          if (v != 0.0) Pt_host.ci[p] = coff[a] + c, Pt_host.v[p] = v, ++p;
-        }
-      }
+      DevBuf<long long> cnt(size_t(n) + 1);
+      cnt.zero();
+      ptent_kernel<false><<<grid_for(n), kT>>>(n, k, d_agg.get(), d_local.get(), d_aoff.get(), d_rank.get(),
+                                               d_coff.get(), Qd.get(), cnt.get(), nullptr, nullptr, nullptr);
+      P.rp.alloc(size_t(n) + 1);
+      P.nnz = scan_counts(cnt, n, P.rp);
+      P.ci.alloc(size_t(P.nnz)), P.v.alloc(size_t(P.nnz));
+      if (P.nnz)
+        ptent_kernel<true><<<grid_for(n), kT>>>(n, k, d_agg.get(), d_local.get(), d_aoff.get(), d_rank.get(),
+                                                d_coff.get(), Qd.get(), nullptr, P.rp.get(), P.ci.get(), P.v.get());
     }
-    qs.clear();
-    DCsr P = upload_csr(Pt_host);
-    Pt_host = fpb::Csr();
-    clk.mark("tentative P (host QR)", P.nnz);
+    DevBuf<double> nnc(size_t(k) * nc);
+    if (n_agg) coarse_nn_kernel<<<grid_for(n_agg), kT>>>(n_agg, k, nc, d_rank.get(), d_coff.get(), Rp.get(), nnc.get());
+    cuda_check(cudaDeviceSynchronize(), "tentative P");
+    clk.mark("tentative P (device QR)", P.nnz);
     if (opt.prolongation_smoothing) {  // P - w D^-1 A P
       std::vector<double> dinv(static_cast<size_t>(n));
       for (int i = 0; i < n; ++i) dinv[i] = 1.0 / fine.diag[i];
@@ -527,11 +646,7 @@ fpb::HostAmg amg_setup_dev(DCsr&& A0, const std::vector<std::vector<double>>& ne
       Ac = spgemm_dev(Pt, AP, nullptr);
     }
     clk.mark("P^T (A P)", Ac.nnz);
-    std::vector<std::vector<double>> nnc(static_cast<size_t>(k), std::vector<double>(static_cast<size_t>(nc), 0.0));
-    for (int a = 0; a < n_agg; ++a)
-      for (int r = 0; r < rank[a]; ++r)
-        for (int c = 0; c < k; ++c) nnc[c][coff[a] + r] = rps[a][size_t(r) * k + c];
-    nn = std::move(nnc);
+    nn_dev = std::move(nnc);
     fpb::HostLevel next;
     next.diag = diag_dev(Ac);
     next.A = shape_only(Ac.n_rows, Ac.n_cols);

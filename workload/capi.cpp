@@ -68,6 +68,8 @@ extern "C" {
 
 const char* fp_workload_last_error(void) { return g_err.c_str(); }
 
+uint64_t fp_workload_layout(void) { return workload_layout_fingerprint(); }
+
 int fp_workload_preset(int32_t id, uint64_t seed, fp_workload** out) {
   return guard([&] {
     need(out != nullptr, "fp_workload_preset: null out");

@@ -57,6 +57,7 @@ _P, _PP, _DP = C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_double)
 # every symbol include/fracprec_workload.h declares, with its ctypes signature
 SIGNATURES = {
     "fp_workload_last_error": (C.c_char_p, []),
+    "fp_workload_layout": (C.c_uint64, []),
     "fp_workload_preset": (C.c_int, [C.c_int32, C.c_uint64, _PP]),
     "fp_workload_custom": (C.c_int, [C.POINTER(FpWorkloadSpec), _PP]),
     "fp_workload_destroy": (None, [_P]),

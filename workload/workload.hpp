@@ -101,3 +101,11 @@ Workload generate_workload(const WorkloadSpec& spec);
 struct fp_workload {
   fpb::Workload w;
 };
+
+// Layout fingerprint of the shared handle types: the solve library reads fp_workload's members directly
+// (it is built against this header), so it checks at use that the loaded generator library was built
+// from the same header (fp_workload_layout, include/fracprec_workload.h)
+constexpr unsigned long long workload_layout_fingerprint() {
+  return (unsigned long long)sizeof(fpb::Workload) ^ ((unsigned long long)sizeof(fpb::FractureModel) << 16) ^
+         ((unsigned long long)sizeof(fpb::FractureState) << 32) ^ ((unsigned long long)sizeof(fpb::HostSystem) << 48);
+}
