@@ -156,7 +156,7 @@ class OracleSystem:
         return cls(h)
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:
             lib.or_system_destroy(self.h)
             self.h = None
 
@@ -217,7 +217,7 @@ class OraclePrecond:
         return bool(lib.or_precond_factor_pivots(self.h))
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:
             lib.or_precond_destroy(self.h)
             self.h = None
 
