@@ -54,7 +54,7 @@ def parse(argv=None):
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--variant", default="tup", choices=["tup", "tpu", "tup_star"])
     ap.add_argument("--theta", type=float, default=0.0, help="AMG strength_threshold (amg.hpp:20)")
-    ap.add_argument("--factor-solve", default="auto", choices=["auto", "sweep", "inverse"],
+    ap.add_argument("--factor-solve", default="auto", choices=["auto", "sweep", "inverse", "panel"],
                     help="T / S~2 application (DESIGN.md §5b)")
     ap.add_argument("--restart", type=int, default=50)
     ap.add_argument("--row-sum", default="strided", choices=["ordered", "strided"],

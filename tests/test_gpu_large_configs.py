@@ -101,11 +101,17 @@ def test_large_config_apply_bitwise_and_gmres_history(config, variant):
     assert np.allclose(h, hr, rtol=1e-6, atol=0), np.max(np.abs(h / hr - 1))
 
 
+CONFIG5_VARIANTS = os.environ.get("FRACPREC_CONFIG5_VARIANTS", "tup").split(",")
+
+
 @pytest.mark.skipif(os.environ.get("FRACPREC_SKIP_CONFIG5") == "1", reason="FRACPREC_SKIP_CONFIG5=1")
-@pytest.mark.parametrize("variant", ["tup", "tpu"])
+@pytest.mark.parametrize("variant", CONFIG5_VARIANTS)
 def test_config5_apply_bitwise(variant):
-    """configs[4] at full size (27.6M unknowns, A with 2.1e9 entries, int64 offsets): one application
-    of each variant, GPU (product-built hierarchy) bitwise the oracle's (oracle-built hierarchy)."""
+    """configs[4] at full size (27.6M unknowns, A with 2.1e9 entries, int64 offsets): one application,
+    GPU (product-built hierarchy) bitwise the oracle's (oracle-built hierarchy).  t-u-p (the bench's
+    variant) by default; FRACPREC_CONFIG5_VARIANTS=tpu runs t-p-u — one variant per pytest process,
+    since the oracle's setup peaks near 170 GB of host memory and two back to back do not fit in one
+    process on a 196 GB box (profiles/round2/config5_tpu_bitwise.log is that run)."""
     t0 = time.perf_counter()
     W = api.Workload(5, 42)
     J = W.system(copy=False)
