@@ -1,6 +1,6 @@
 """Parity at BASELINE.json's large configs (north_star: "5-30M-unknown configs"):
 configs[2] (80^3, 3 fractures, 1.73M unknowns), configs[3] (100^3, 10 planes, 3.78M) and
-configs[4] (256x256x128, 40 fractures, 27.6M), both preconditioner variants, GPU (product-built
+configs[4] (256x256x128, 40 fractures, 27.6M; one apply per variant), both preconditioner variants, GPU (product-built
 hierarchy, uploaded) against the CPU oracle (its own setup, on every host core; oracle/par.hpp) on
 the same seeded inputs.
 
@@ -8,8 +8,8 @@ Bars: one preconditioner application bitwise (so within 1e-12) in both coarse ro
 both factor applications; GMRES(50) over >= 100 iterations (both sides run the same steps: the
 solves stagnate) with the iteration count within +-2 and the relative-residual history
 matched step by step.  conftest.py runs this module first so `-x` cannot hide it behind a slower
-failure.  Config 5 needs ~150 GB of host memory for the oracle's setup and the product's at once;
-the product's host data is freed after the upload.
+failure.  Config 5's oracle setup peaks near 170 GB of host memory (the product's device setup and
+upload finish and free their host data first).
 """
 import gc
 import os
