@@ -227,11 +227,23 @@ def run_reference(args) -> dict:
                               threads=cores)}
 
 
+def mapped_product_libraries() -> list:
+    """Shared objects of the B200 package mapped into this process (/proc/self/maps)."""
+    try:
+        maps = open("/proc/self/maps").read().splitlines()
+    except OSError:
+        return []
+    return sorted({ln.split()[-1] for ln in maps if "libfracprec_b200" in ln or "paper_2112_12397_b200" in ln})
+
+
 def reference_main(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     r = run_reference(args)
+    loaded = mapped_product_libraries()
+    if loaded:  # the reference arm must not touch the product (VERDICT r1 item 3)
+        raise SystemExit(f"reference arm mapped the B200 library: {loaded}")
     line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * float(np.mean(r["steps_s"])), 1),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -246,7 +258,7 @@ def reference_main(args):
             "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
                              "sample": r["sample"]},
             "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "setup_s": r["setup_s"], "generate_s": r["generate_s"],
+            "setup_s": r["setup_s"], "generate_s": r["generate_s"], "product_libraries_mapped": loaded,
             "note": "the reference (Eigen3/LAPACKE C++) is not buildable here; the oracle restatement is timed"}
     print(json.dumps(line), flush=True)
 
