@@ -54,6 +54,9 @@ struct CsrView {  // plain CSR, 64-bit offsets (warp-per-row kernel)
   const int* ci = nullptr;
   const double* v = nullptr;
   const int* row_map = nullptr;  // optional (csr_warp_kernel): compute only rows row_map[0 .. n_rows)
+  // optional (csr_warp_kernel): groups of consecutive rows share one column list (the coarse dofs of
+  // an aggregate); entry k of row r has its value at v[k] and its column at ci[cp[r] + (k - rp[r])]
+  const long long* cp = nullptr;
 };
 
 // Windowed slices for the ordered long-row pipeline (csr_pipe_kernel): rows

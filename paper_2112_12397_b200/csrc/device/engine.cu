@@ -301,6 +301,10 @@ DCsr clone_csr(const DCsr& A) {
   if (A.rp.size()) cuda_check(cudaMemcpy(C.rp.get(), A.rp.get(), A.rp.bytes(), cudaMemcpyDeviceToDevice), "clone");
   if (A.ci.size()) cuda_check(cudaMemcpy(C.ci.get(), A.ci.get(), A.ci.bytes(), cudaMemcpyDeviceToDevice), "clone");
   if (A.v.size()) cuda_check(cudaMemcpy(C.v.get(), A.v.get(), A.v.bytes(), cudaMemcpyDeviceToDevice), "clone");
+  if (A.cp.size()) {
+    C.cp.alloc(A.cp.size()), C.nci = A.nci;
+    cuda_check(cudaMemcpy(C.cp.get(), A.cp.get(), A.cp.bytes(), cudaMemcpyDeviceToDevice), "clone");
+  }
   return C;
 }
 // the layout of a borrowed device CSR (the layouts that keep a CSR get their own copy)
@@ -475,7 +479,8 @@ void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows) {
       if (rows.size() < size_t(n)) {
         S.res_rows.upload(rows);
         S.res_n = int(rows.size());
-        S.res_bytes = 12.0 * res_nnz + 8.0 * S.res_n;
+        const DCsr& Ad = lv[l].Am.csr;  // the layout's own copy (its columns may be shared per aggregate)
+        S.res_bytes = (8.0 + Ad.index_bytes_per_entry()) * res_nnz + (4.0 + Ad.row_bytes()) * S.res_n;
       }
     }
     // rows of R_{l+1} = P_{l+1}^T that gather an active row
@@ -493,7 +498,9 @@ void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows) {
       cuda_check(cudaMemcpy(rrp.data(), R.csr.rp.get(), sizeof(long long) * rrp.size(), cudaMemcpyDeviceToHost), "R rp");
       std::vector<int> rrows;
       for (int c = 0; c < P.n_cols; ++c)
-        if (coarse[c]) rrows.push_back(c), S.r_bytes += 12.0 * double(rrp[size_t(c) + 1] - rrp[c]) + 8.0;
+        if (coarse[c])
+          rrows.push_back(c), S.r_bytes += (8.0 + R.csr.index_bytes_per_entry()) * double(rrp[size_t(c) + 1] - rrp[c]) +
+                                           4.0 + R.csr.row_bytes();
       S.r_rows.upload(rrows);
       S.r_n = int(rrows.size());
     }

@@ -75,8 +75,17 @@ struct DCsr {
   DevBuf<long long> rp;
   DevBuf<int> ci;
   DevBuf<double> v;
-  CsrView view() const { return {n_rows, rp.get(), ci.get(), v.get()}; }
-  double matrix_bytes() const { return 12.0 * double(nnz) + 8.0 * (n_rows + 1); }
+  // shared column lists (formats.cu share_columns): ci holds nci < nnz indices, cp the per-row offset
+  DevBuf<long long> cp;
+  int64_t nci = 0;
+  CsrView view() const {
+    CsrView V{n_rows, rp.get(), ci.get(), v.get()};
+    V.cp = cp.size() ? cp.get() : nullptr;
+    return V;
+  }
+  double index_bytes_per_entry() const { return cp.size() && nnz > 0 ? 4.0 * double(nci) / double(nnz) : 4.0; }
+  double row_bytes() const { return cp.size() ? 16.0 : 8.0; }  // offsets read per row
+  double matrix_bytes() const { return (8.0 + index_bytes_per_entry()) * double(nnz) + row_bytes() * (n_rows + 1); }
 };
 
 }  // namespace fpd
@@ -153,6 +162,10 @@ DBsr3 bsr3_from(const DCsr& A, const std::vector<int>* brows, cudaStream_t s);
 DPipe pipe_from(const DCsr& A, cudaStream_t s);
 DCsr transpose_dev(const DCsr& A, cudaStream_t s);  // rows of A^T list the source rows ascending
 DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s);
+// When every group of `group` consecutive rows of A has one column list, store it once per group
+// (ci shrinks by the group size, cp gives each row its list); returns false and leaves A as it is
+// otherwise.  The entries and their order per row do not change.
+bool share_columns(DCsr& A, int group, cudaStream_t s);
 
 fpb::Csr host_copy(const HostCsrView& A);
 DCsr add_dev(const DCsr& A, const DCsr& B, double alpha, double beta);  // alpha A + beta B (dsetup.cu)

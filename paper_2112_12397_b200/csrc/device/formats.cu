@@ -8,6 +8,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 
 #include "engine.cuh"
@@ -405,12 +406,77 @@ DCsr transpose_dev(const DCsr& A, cudaStream_t s) {
   return T;
 }
 
+namespace {
+// group g = rows g*G .. g*G+G-1: every row of the group has the first row's length and columns
+// (a warp per group; the last, shorter group of n % G rows is compared the same way)
+__global__ void group_check_kernel(int n, int G, const long long* rp, const int* ci, int* ok) {
+  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long r0 = g * G;
+  if (r0 >= n) return;
+  const long long b0 = rp[r0], len = rp[r0 + 1] - b0;
+  for (int j = 1; j < G && r0 + j < n; ++j) {
+    const long long bj = rp[r0 + j];
+    bool same = rp[r0 + j + 1] - bj == len;
+    for (long long k = lane; same && k < len; k += 32) same = ci[b0 + k] == ci[bj + k];
+    if (!same) *ok = 0;
+  }
+}
+__global__ void group_len_kernel(int n, int G, long long ng, const long long* rp, long long* glen) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (g > ng) return;
+  glen[g] = g < ng ? rp[g * G + 1] - rp[g * G] : 0;
+}
+__global__ void group_fill_kernel(int n, int G, const long long* rp, const int* ci, const long long* goff, int* cci,
+                                  long long* cp) {
+  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long r0 = g * G;
+  if (r0 >= n) return;
+  const long long b0 = rp[r0], len = rp[r0 + 1] - b0, o = goff[g];
+  for (long long k = lane; k < len; k += 32) cci[o + k] = ci[b0 + k];
+  for (int j = lane; j < G && r0 + j < n; j += 32) cp[r0 + j] = o;
+}
+}  // namespace
+
+bool share_columns(DCsr& A, int G, cudaStream_t s) {
+  if (G < 2 || A.n_rows < G || A.nnz == 0 || A.cp.size()) return false;
+  const long long ng = (A.n_rows + (long long)G - 1) / G;
+  DevBuf<int> ok(1);
+  const int one = 1;
+  cuda_check(cudaMemcpyAsync(ok.get(), &one, sizeof(int), cudaMemcpyHostToDevice, s), "share ok");
+  group_check_kernel<<<grid_for(ng * 32), kT, 0, s>>>(A.n_rows, G, A.rp.get(), A.ci.get(), ok.get());
+  int h_ok = 0;
+  cuda_check(cudaMemcpyAsync(&h_ok, ok.get(), sizeof(int), cudaMemcpyDeviceToHost, s), "share ok");
+  cuda_check(cudaStreamSynchronize(s), "share_columns check");
+  if (!h_ok) return false;
+  DevBuf<long long> glen(size_t(ng) + 1), goff(size_t(ng) + 1);
+  group_len_kernel<<<grid_for(ng + 1), kT, 0, s>>>(A.n_rows, G, ng, A.rp.get(), glen.get());
+  const long long nci = exclusive_scan(glen.get(), goff.get(), ng, s);
+  DevBuf<int> cci{size_t(nci)};
+  A.cp.alloc(size_t(A.n_rows) + 1);
+  group_fill_kernel<<<grid_for(ng * 32), kT, 0, s>>>(A.n_rows, G, A.rp.get(), A.ci.get(), goff.get(), cci.get(),
+                                                   A.cp.get());
+  cuda_check(cudaMemcpyAsync(A.cp.get() + A.n_rows, &nci, sizeof(long long), cudaMemcpyHostToDevice, s), "share cp end");
+  cuda_check(cudaStreamSynchronize(s), "share_columns");
+  A.ci = std::move(cci);
+  A.nci = nci;
+  return true;
+}
+
 DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s) {
   DMat M;
   if (strided) {  // row_sum = strided32: plain CSR, one warp per row (or window-staged CTAs of R rows)
     M.warp = M.strided = true;
     M.strided_rows = 1;  // one row per CTA: most parallel loads for few-row operators
     M.csr = std::move(A);
+    // the warp-row kernel's operators (A_l, R_l of an aggregation hierarchy): the coarse dofs of an
+    // aggregate (6 with the rigid-body near-null space, else 3) have one column list — keep it once
+    // per aggregate: 12 -> 8.7 B per entry.  FRACPREC_B200_SHARED_COLS=0 keeps plain CSR.
+    const char* e = std::getenv("FRACPREC_B200_SHARED_COLS");
+    if (M.csr.n_rows >= 2048 && !(e && std::atoi(e) == 0))
+      for (int G : {6, 3, 2})
+        if (M.csr.n_rows % G == 0 && share_columns(M.csr, G, s)) break;
     return M;
   }
   const double avg = A.n_rows > 0 ? double(A.nnz) / A.n_rows : 0.0;

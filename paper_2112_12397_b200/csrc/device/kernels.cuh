@@ -324,14 +324,16 @@ __global__ void __launch_bounds__(256) csr_warp_kernel(CsrView A, G g, E epi) {
   const int grow = A.row_map ? A.row_map[row] : row;  // row subset: sum global row grow
   typename E::P pre{};
   if (lane == 0) pre = epi.load(grow);
-  const long long k1 = A.rp[grow + 1];
+  const long long k0 = A.rp[grow], k1 = A.rp[grow + 1];
+  // column of entry k at ci[k] (shared column lists: the group's list, offset by the row's start)
+  const int* __restrict__ ci = A.cp ? A.ci + (A.cp[grow] - k0) : A.ci;
   double s = 0.0;
-  long long k = A.rp[grow] + lane;
+  long long k = k0 + lane;
   for (; k + 32 * (U - 1) < k1; k += 32 * U) {
     int c[U];
     double v[U], x[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) c[u] = __ldg(A.ci + k + 32 * u), v[u] = __ldg(A.v + k + 32 * u);
+    for (int u = 0; u < U; ++u) c[u] = __ldg(ci + k + 32 * u), v[u] = __ldg(A.v + k + 32 * u);
 #pragma unroll
     for (int u = 0; u < U; ++u) x[u] = g(c[u]);
 #pragma unroll
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(256) csr_warp_kernel(CsrView A, G g, E epi) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool in = k + 32 * u < k1;
-      c[u] = in ? __ldg(A.ci + k + 32 * u) : 0;
+      c[u] = in ? __ldg(ci + k + 32 * u) : 0;
       v[u] = in ? __ldg(A.v + k + 32 * u) : 0.0;
     }
     double x[U];

@@ -112,3 +112,21 @@ def test_config2_bench_solver_500_steps_tracks_the_reference_order_oracle():
     h, hr = np.array(st.relative_residuals[:k]), st_ref["history"][:k]
     assert np.allclose(h[:100], hr[:100], rtol=1e-6, atol=0), np.max(np.abs(h[:100] / hr[:100] - 1))
     assert np.allclose(h, hr, rtol=1e-3, atol=0), np.max(np.abs(h / hr - 1))
+
+
+@pytest.mark.parametrize("variant", ["tpu", "tup"])
+def test_config2_shared_column_lists_bitwise(variant, monkeypatch):
+    """The warp-row operators (A_l, R_l with >= 2048 rows, row_sum = strided) keep one column list
+    per aggregate (the 6 coarse dofs of an aggregate share their pattern): fewer index bytes, the
+    same entries in the same order, so the apply stays bitwise the oracle's and the plain-CSR one's."""
+    J, osys, op, pc, opc = setup(2, variant, "strided")  # default: shared lists where the pattern allows
+    monkeypatch.setenv("FRACPREC_B200_SHARED_COLS", "0")
+    amg = api.AmgConfig(strength_threshold=0.0, row_sum="strided")
+    pc_plain = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, api.PrecondConfig(variant, amg=amg)))
+    monkeypatch.delenv("FRACPREC_B200_SHARED_COLS")
+    assert pc.traffic()["apply_bytes"] < pc_plain.traffic()["apply_bytes"]  # the shared lists did engage
+    x = np.random.default_rng(5).uniform(-1, 1, J.total_dimension())
+    xd = torch.tensor(x, device="cuda", dtype=torch.float64)
+    y = pc.apply(xd).cpu().numpy()
+    assert np.array_equal(y, pc_plain.apply(xd).cpu().numpy())
+    assert np.array_equal(y, opc.apply(x))

@@ -16,8 +16,13 @@ timeout 1500 ncu --set full --import-source on --clock-control none --profile-fr
   -o gpurun_out/full_cfg5 -f python tools/profile_solve.py 5 tup 1 cgs strided > gpurun_out/ncu_full.log 2>&1
 echo "full capture rc=$?"
 ncu -i gpurun_out/full_cfg5.ncu-rep --page raw --csv > gpurun_out/full_cfg5_raw.csv 2>/dev/null
-for tool in memcheck racecheck synccheck; do
+python tools/ncu_full_summary.py gpurun_out/full_cfg5_raw.csv gpurun_out/ncu_full_cfg5.json \
+  "ncu --set full --clock-control none, one GMRES(50) iteration of config 5 (tools/profile_solve.py 5 tup 1 cgs strided)"
+# gpurun copies back at most 64 MiB: keep the report only when it is small
+[ "$(stat -c %s gpurun_out/full_cfg5.ncu-rep 2>/dev/null || echo 0)" -gt 30000000 ] && rm -f gpurun_out/full_cfg5.ncu-rep
+du -sh gpurun_out
+if [ "$SKIP_SANITIZERS" != "1" ]; then for tool in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize.py \
     > gpurun_out/sanitizer_$tool.log 2>&1
   echo "sanitizer $tool rc=$?"
-done
+done; fi
