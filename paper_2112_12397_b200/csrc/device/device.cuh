@@ -40,12 +40,18 @@ struct SellView {
 // scalar rows of a node share one column pattern, so a slot holds one column index and
 // three values.  SELL-32 over nodes: slot (slice s, k, lane) at q = slice_off[s] + 32 k + lane;
 // its column at cols[q], its values at vals[3 (slice_off[s] + 32 k) + 32 d + lane], d = 0..2.
+// Nodes are sorted by length inside windows of kBp3Window nodes before they are sliced (slot ->
+// node in `node`, -1 = padding), so the 32 nodes of a slice have nearly one length and a slice
+// stores (and streams) almost no padding.
+constexpr int kBp3Window = 2048;
 struct Bp3View {
   int n_nodes = 0;
   const long long* slice_off = nullptr;
   const int* node_len = nullptr;
   const int* cols = nullptr;
   const double* vals = nullptr;
+  int n_slots = 0;            // 32 * slices
+  const int* node = nullptr;  // n_slots: the node of slot (slice, lane)
 };
 
 struct CsrView {  // plain CSR, 64-bit offsets (warp-per-row kernel)

@@ -4,6 +4,7 @@
 #include <omp.h>
 
 #include <algorithm>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -90,7 +91,7 @@ void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s) {
 template <class G, class E>
 void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s, const int* rows = nullptr, int n_sub = 0) {
   if (A.bp3) {
-    launch(bp3_kernel<G, E>, dim3(blocks_for(A.bp.n_nodes, 256)), dim3(256), 0, s, "bp3_kernel", A.bp.view(), g, e);
+    launch(bp3_kernel<G, E>, dim3(blocks_for((long long)A.bp.node.size(), 256)), dim3(256), 0, s, "bp3_kernel", A.bp.view(), g, e);
     cuda_check(cudaGetLastError(), "bp3_kernel launch");
     return;
   }
@@ -100,9 +101,10 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s, const int
       CsrView V = A.csr.view();
       if (rows) V.row_map = rows, V.n_rows = n_sub;  // row subset (sparse right-hand side)
       if (V.n_rows == 0) return;
-      // 8 entries per lane per round above 256 entries per row (A/B: config 3 apply 1.874 -> 1.860 ms)
-      if (A.csr.nnz > 256LL * A.csr.n_rows)
-        launch(csr_warp_kernel<8, G, E>, dim3(blocks_for(V.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", V, g, e);
+      // 8 entries per lane per round above 256 entries per row (A/B: config 3 apply 1.874 -> 1.860 ms; from
+      // 96 or 160 entries on, or 16 per round, measured slower at configs 3-5: occupancy beats round count)
+      const long long u8_avg = 256;
+      if (A.csr.nnz > u8_avg * A.csr.n_rows)        launch(csr_warp_kernel<8, G, E>, dim3(blocks_for(V.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", V, g, e);
       else
         launch(csr_warp_kernel<4, G, E>, dim3(blocks_for(V.n_rows, 8)), dim3(256), 0, s, "csr_warp_kernel", V, g, e);
     } else {
@@ -757,7 +759,7 @@ size_t panel_smem_bytes(const fpb::BandFactor& F, const std::vector<int>& pp) {
     const int m = F.block_start[b + 1] - F.block_start[b];
     m_max = std::max(m_max, m), P_max = std::max(P_max, (m + pp[b] - 1) / pp[b]), p_max = std::max(p_max, pp[b]);
   }
-  const int R = p_max <= 64 ? 1 : p_max <= 128 ? 2 : 4;
+  const int R = p_max <= 128 ? 1 : 2;
   return sizeof(double) * (size_t(m_max) + size_t(kPanelThreads / 32) * size_t(P_max) * R);
 }
 }  // namespace
@@ -873,7 +875,7 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
     pan_off.upload(off);
     pan_pmax = *std::max_element(pp.begin(), pp.end());
     pan_smem = panel_smem_bytes(F, pp);
-    for (auto k : {panel_solve_kernel<1, 2>, panel_solve_kernel<2, 4>, panel_solve_kernel<4, 8>})
+    for (auto k : {panel_solve_kernel<1, 2>, panel_solve_kernel<1, 4>, panel_solve_kernel<2, 8>})
       cuda_check(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pan_smem)),
                  "panel smem attribute");
     pan_m.alloc(size_t(off.back()));
@@ -938,9 +940,9 @@ void DevicePrecond::enqueue_band(const double* rhs, double rs, double* out, doub
     if (pan_pmax <= 64)
       launch(panel_solve_kernel<1, 2>, g, b, smem, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
     else if (pan_pmax <= 128)
-      launch(panel_solve_kernel<2, 4>, g, b, smem, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
+      launch(panel_solve_kernel<1, 4>, g, b, smem, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
     else
-      launch(panel_solve_kernel<4, 8>, g, b, smem, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
+      launch(panel_solve_kernel<2, 8>, g, b, smem, s, "panel_solve_kernel", pview, rhs, rs, out, out2, sub, os, mode);
     if (L) {
       L->add(band_factor_bytes + vec_bytes + 8.0 * band.n);  // + z written and read back between the chains
       L->waste(std::max(0.0, pan_bytes - band_factor_bytes));
@@ -1055,7 +1057,8 @@ GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart
   }
   big_nblk_ = int((n_ + kBigTile - 1) / kBigTile);
   partial_.alloc(size_t(std::max({(2 * ldr_ + 4) * (long long)mgs_grid_, (long long)red_grid_,
-                                  (ldr_ + 2) * (long long)big_nblk_})));
+                                  (ldr_ + 2) * (long long)big_nblk_,
+                                  (ldr_ + 2) * 8LL * sm_count()})));  // cgs_big_project_dots: one value per resident block
   big_coef_.alloc(size_t(ldr_ + 2));
   big_state_.alloc(1);
   cuda_check(cudaHostAlloc(&status_h_, 2 * sizeof(GmresStatus), cudaHostAllocMapped), "cudaHostAlloc");
@@ -1134,12 +1137,48 @@ void GmresSolver::launch_mgs(MgsArgs& a, int orth, cudaStream_t s) {
     CgsBigArgs b{a, big_nblk_, partial_.get(), big_coef_.get(), big_state_.get(), 0};
     cuda_check(cudaMemsetAsync(big_state_.get(), 0, sizeof(CgsState), s), "cgs state");
     const dim3 tiles(big_nblk_), one(1), T(kBigT);
-    for (int pass = 0; pass < 2; ++pass) {
-      b.pass = pass;
-      launch(cgs_big_dots, tiles, T, 0, s, "cgs_big_dots", b);
-      launch(cgs_big_reduce, one, T, 0, s, "cgs_big_reduce", b);
-      launch(cgs_big_project, tiles, T, 0, s, "cgs_big_project", b);
-      launch(cgs_big_norm, one, T, 0, s, "cgs_big_norm", b, pass);
+    const int ncol = a.m + 1;
+    static const bool fuse_env = [] {
+      const char* e = std::getenv("FRACPREC_B200_CGS_FUSE");
+      return !(e && std::atoi(e) == 0);
+    }();
+    if (fuse_env && ncol <= 52) {
+      // first projection + the second pass's dots in one pass over the basis (cgs_big_project_dots)
+      auto fused = [&](auto kern) {
+        static std::map<const void*, int> occ;  // blocks per SM, per instantiation
+        int& per_sm = occ[reinterpret_cast<const void*>(kern)];
+        if (!per_sm) {
+          cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFuseT, 0), "cgs fuse occupancy");
+          per_sm = std::max(per_sm, 1);
+        }
+        const int grid = int(std::min<long long>((n_ + kFuseT - 1) / kFuseT, (long long)per_sm * sm_count()));
+        b.pass = 0;
+        launch(cgs_big_dots, tiles, T, 0, s, "cgs_big_dots", b);
+        launch(cgs_big_reduce, one, T, 0, s, "cgs_big_reduce", b);
+        CgsBigArgs f = b;  // the fused kernel's partials: `grid` values per set, ||w'||^2 in set m + 1
+        f.nblk = grid, f.norm_set = ncol;
+        launch(kern, dim3(grid), dim3(kFuseT), 0, s, "cgs_big_project_dots", f);
+        launch(cgs_big_norm, one, T, 0, s, "cgs_big_norm", f, 0);
+        f.pass = 1;
+        launch(cgs_big_reduce, one, T, 0, s, "cgs_big_reduce", f);
+        b.pass = 1;
+        launch(cgs_big_project, tiles, T, 0, s, "cgs_big_project", b);
+        launch(cgs_big_norm, one, T, 0, s, "cgs_big_norm", b, 1);
+      };
+      if (ncol <= 13)
+        fused(cgs_big_project_dots<13>);
+      else if (ncol <= 26)
+        fused(cgs_big_project_dots<26>);
+      else
+        fused(cgs_big_project_dots<52>);
+    } else {
+      for (int pass = 0; pass < 2; ++pass) {
+        b.pass = pass;
+        launch(cgs_big_dots, tiles, T, 0, s, "cgs_big_dots", b);
+        launch(cgs_big_reduce, one, T, 0, s, "cgs_big_reduce", b);
+        launch(cgs_big_project, tiles, T, 0, s, "cgs_big_project", b);
+        launch(cgs_big_norm, one, T, 0, s, "cgs_big_norm", b, pass);
+      }
     }
     launch(cgs_big_normalize, tiles, T, 0, s, "cgs_big_normalize", b);
     return;

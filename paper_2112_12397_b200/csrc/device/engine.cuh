@@ -56,11 +56,13 @@ struct DBp3 {  // node-blocked rows (Bp3View)
   int n_nodes = 0;
   int64_t nnz = 0, slots = 0;
   DevBuf<long long> off;
-  DevBuf<int> len, cols;
+  DevBuf<int> len, cols, node;
   DevBuf<double> vals;
-  Bp3View view() const { return {n_nodes, off.get(), len.get(), cols.get(), vals.get()}; }
+  Bp3View view() const {
+    return {n_nodes, off.get(), len.get(), cols.get(), vals.get(), int(node.size()), node.get()};
+  }
   // format bytes: one column index per node entry + three values
-  double matrix_bytes() const { return 28.0 * double(nnz) / 3.0 + 4.0 * (n_nodes + 1); }
+  double matrix_bytes() const { return 28.0 * double(nnz) / 3.0 + 4.0 * (n_nodes + 1) + 4.0 * double(node.size()); }
 };
 // empty (n_nodes = 0) unless the three rows of every node share one column pattern
 DBp3 make_bp3(const fpb::Csr& A);
@@ -162,10 +164,10 @@ DBsr3 bsr3_from(const DCsr& A, const std::vector<int>* brows, cudaStream_t s);
 DPipe pipe_from(const DCsr& A, cudaStream_t s);
 DCsr transpose_dev(const DCsr& A, cudaStream_t s);  // rows of A^T list the source rows ascending
 DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s);
-// When every group of `group` consecutive rows of A has one column list, store it once per group
-// (ci shrinks by the group size, cp gives each row its list); returns false and leaves A as it is
-// otherwise.  The entries and their order per row do not change.
-bool share_columns(DCsr& A, int group, cudaStream_t s);
+// Rows with exactly their predecessor's columns share that row's list (ci shrinks, cp gives each
+// row its list); returns false and leaves A as it is when under 1/8 of the indices would go.  The
+// entries and their order per row do not change.
+bool share_columns(DCsr& A, cudaStream_t s);
 
 fpb::Csr host_copy(const HostCsrView& A);
 DCsr add_dev(const DCsr& A, const DCsr& B, double alpha, double beta);  // alpha A + beta B (dsetup.cu)

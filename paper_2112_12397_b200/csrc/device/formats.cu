@@ -90,12 +90,38 @@ __global__ void bp3_len_kernel(int nn, const long long* rp, int* len) {
   if (n < nn) len[n] = int(rp[3 * n + 1] - rp[3 * n]);
 }
 
-__global__ void bp3_fill_kernel(int nn, const long long* rp, const int* ci, const double* v, const long long* off,
-                                int* cols, double* vals) {
+// sort key of node n: its window in the high bits, then longest first inside the window
+__global__ void bp3_key_kernel(int nn, const int* len, unsigned long long* key, int* val) {
   const long long n = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (n >= nn) return;
-  const long long s0 = off[n / kSlice];
-  const int lane = int(n % kSlice);
+  key[n] = ((unsigned long long)(n / kBp3Window) << 32) | (unsigned)(0x7fffffff - len[n]);
+  val[n] = int(n);
+}
+// slot -> node (sorted order, -1 past the end) and the slots of each slice
+__global__ void bp3_slots_kernel(int nn, int ns, const int* sorted, const int* len, int* node, long long* out) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s > ns) return;
+  if (s == ns) {
+    out[s] = 0;
+    return;
+  }
+  int mx = 0;
+  for (int r = 0; r < kSlice; ++r) {
+    const long long q = s * kSlice + r;
+    const int n = q < nn ? sorted[q] : -1;
+    node[q] = n;
+    if (n >= 0) mx = max(mx, len[n]);
+  }
+  out[s] = (long long)mx * kSlice;
+}
+__global__ void bp3_fill_kernel(int n_slots, const int* node, const long long* rp, const int* ci, const double* v,
+                                const long long* off, int* cols, double* vals) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= n_slots) return;
+  const long long n = node[q];
+  if (n < 0) return;
+  const long long s0 = off[q / kSlice];
+  const int lane = int(q % kSlice);
   const long long len = rp[3 * n + 1] - rp[3 * n];
   for (long long k = 0; k < len; ++k) {
     cols[s0 + k * kSlice + lane] = ci[rp[3 * n] + k];
@@ -281,17 +307,32 @@ DBp3 bp3_from(const DCsr& A, cudaStream_t s) {
   const int ns = (nn + kSlice - 1) / kSlice;
   D.len.alloc(size_t(nn));
   bp3_len_kernel<<<grid_for(nn), kT, 0, s>>>(nn, A.rp.get(), D.len.get());
+  // nodes by (window, length descending): stable radix sort of 64-bit keys
+  DevBuf<int> sorted{size_t(nn)};
+  {
+    DevBuf<unsigned long long> kin{size_t(nn)}, kout{size_t(nn)};
+    DevBuf<int> vin{size_t(nn)};
+    bp3_key_kernel<<<grid_for(nn), kT, 0, s>>>(nn, D.len.get(), kin.get(), vin.get());
+    size_t tb = 0;
+    cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.get(), kout.get(), vin.get(), sorted.get(), nn, 0, 64, s),
+               "bp3 sort size");
+    DevBuf<unsigned char> tmp(tb);
+    cuda_check(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, kin.get(), kout.get(), vin.get(), sorted.get(), nn, 0, 64, s),
+               "bp3 sort");
+    cuda_check(cudaStreamSynchronize(s), "bp3 sort");
+  }
   DevBuf<long long> sl(size_t(ns) + 1);
   D.off.alloc(size_t(ns) + 1);
-  slice_slots_kernel<<<grid_for(ns + 1), kT, 0, s>>>(nn, ns, D.len.get(), sl.get());
+  D.node.alloc(size_t(ns) * kSlice);
+  bp3_slots_kernel<<<grid_for(ns + 1), kT, 0, s>>>(nn, ns, sorted.get(), D.len.get(), D.node.get(), sl.get());
   D.slots = exclusive_scan(sl.get(), D.off.get(), ns, s);
   D.cols.alloc(size_t(D.slots));
   D.vals.alloc(3 * size_t(D.slots));
   if (D.slots) {
     cuda_check(cudaMemsetAsync(D.cols.get(), 0, D.cols.bytes(), s), "memset");
     cuda_check(cudaMemsetAsync(D.vals.get(), 0, D.vals.bytes(), s), "memset");
-    bp3_fill_kernel<<<grid_for(nn), kT, 0, s>>>(nn, A.rp.get(), A.ci.get(), A.v.get(), D.off.get(), D.cols.get(),
-                                                D.vals.get());
+    bp3_fill_kernel<<<grid_for((long long)ns * kSlice), kT, 0, s>>>(ns * kSlice, D.node.get(), A.rp.get(), A.ci.get(),
+                                                                  A.v.get(), D.off.get(), D.cols.get(), D.vals.get());
   }
   cuda_check(cudaStreamSynchronize(s), "bp3_from");
   return D;
@@ -407,57 +448,52 @@ DCsr transpose_dev(const DCsr& A, cudaStream_t s) {
 }
 
 namespace {
-// group g = rows g*G .. g*G+G-1: every row of the group has the first row's length and columns
-// (a warp per group; the last, shorter group of n % G rows is compared the same way)
-__global__ void group_check_kernel(int n, int G, const long long* rp, const int* ci, int* ok) {
-  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+// own[r] = 0 when row r has exactly row r - 1's columns (it will read that row's list), else its
+// length; a warp per row.  own[n] = 0 (scan input of n + 1 values).
+__global__ void same_cols_kernel(int n, const long long* rp, const int* ci, long long* own) {
+  const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const long long r0 = g * G;
-  if (r0 >= n) return;
-  const long long b0 = rp[r0], len = rp[r0 + 1] - b0;
-  for (int j = 1; j < G && r0 + j < n; ++j) {
-    const long long bj = rp[r0 + j];
-    bool same = rp[r0 + j + 1] - bj == len;
-    for (long long k = lane; same && k < len; k += 32) same = ci[b0 + k] == ci[bj + k];
-    if (!same) *ok = 0;
+  if (r > n) return;
+  if (r == n) {
+    if (lane == 0) own[r] = 0;
+    return;
   }
+  const long long b1 = rp[r], len = rp[r + 1] - b1;
+  bool same = r > 0 && rp[r] - rp[r - 1] == len;
+  if (same) {
+    const long long b0 = rp[r - 1];
+    for (long long k = lane; same && k < len; k += 32) same = ci[b0 + k] == ci[b1 + k];
+  }
+  same = __all_sync(0xffffffffu, same);
+  if (lane == 0) own[r] = same ? 0 : len;
 }
-__global__ void group_len_kernel(int n, int G, long long ng, const long long* rp, long long* glen) {
-  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (g > ng) return;
-  glen[g] = g < ng ? rp[g * G + 1] - rp[g * G] : 0;
-}
-__global__ void group_fill_kernel(int n, int G, const long long* rp, const int* ci, const long long* goff, int* cci,
-                                  long long* cp) {
-  const long long g = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+// cp[r] = (lists kept up to and including row r) - len(r): the start of row r's own list, or of the
+// list of the first row of its run of equal patterns; rows that own a list copy it there
+__global__ void shared_cols_fill_kernel(int n, const long long* rp, const int* ci, const long long* own,
+                                        const long long* excl, int* cci, long long* cp) {
+  const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const long long r0 = g * G;
-  if (r0 >= n) return;
-  const long long b0 = rp[r0], len = rp[r0 + 1] - b0, o = goff[g];
-  for (long long k = lane; k < len; k += 32) cci[o + k] = ci[b0 + k];
-  for (int j = lane; j < G && r0 + j < n; j += 32) cp[r0 + j] = o;
+  if (r >= n) return;
+  const long long b = rp[r], len = rp[r + 1] - b;
+  const long long start = excl[r] + own[r] - len;
+  if (lane == 0) cp[r] = start;
+  if (own[r] != 0)
+    for (long long k = lane; k < len; k += 32) cci[start + k] = ci[b + k];
 }
 }  // namespace
 
-bool share_columns(DCsr& A, int G, cudaStream_t s) {
-  if (G < 2 || A.n_rows < G || A.nnz == 0 || A.cp.size()) return false;
-  const long long ng = (A.n_rows + (long long)G - 1) / G;
-  DevBuf<int> ok(1);
-  const int one = 1;
-  cuda_check(cudaMemcpyAsync(ok.get(), &one, sizeof(int), cudaMemcpyHostToDevice, s), "share ok");
-  group_check_kernel<<<grid_for(ng * 32), kT, 0, s>>>(A.n_rows, G, A.rp.get(), A.ci.get(), ok.get());
-  int h_ok = 0;
-  cuda_check(cudaMemcpyAsync(&h_ok, ok.get(), sizeof(int), cudaMemcpyDeviceToHost, s), "share ok");
-  cuda_check(cudaStreamSynchronize(s), "share_columns check");
-  if (!h_ok) return false;
-  DevBuf<long long> glen(size_t(ng) + 1), goff(size_t(ng) + 1);
-  group_len_kernel<<<grid_for(ng + 1), kT, 0, s>>>(A.n_rows, G, ng, A.rp.get(), glen.get());
-  const long long nci = exclusive_scan(glen.get(), goff.get(), ng, s);
+bool share_columns(DCsr& A, cudaStream_t s) {
+  if (A.n_rows < 2 || A.nnz == 0 || A.cp.size()) return false;
+  const long long n = A.n_rows;
+  DevBuf<long long> own(size_t(n) + 1), excl(size_t(n) + 1);
+  same_cols_kernel<<<grid_for((n + 1) * 32), kT, 0, s>>>(A.n_rows, A.rp.get(), A.ci.get(), own.get());
+  const long long nci = exclusive_scan(own.get(), excl.get(), n, s);
+  if (nci > A.nnz - A.nnz / 8) return false;  // under 1/8 of the index bytes saved: keep plain CSR
   DevBuf<int> cci{size_t(nci)};
-  A.cp.alloc(size_t(A.n_rows) + 1);
-  group_fill_kernel<<<grid_for(ng * 32), kT, 0, s>>>(A.n_rows, G, A.rp.get(), A.ci.get(), goff.get(), cci.get(),
-                                                   A.cp.get());
-  cuda_check(cudaMemcpyAsync(A.cp.get() + A.n_rows, &nci, sizeof(long long), cudaMemcpyHostToDevice, s), "share cp end");
+  A.cp.alloc(size_t(n) + 1);
+  shared_cols_fill_kernel<<<grid_for(n * 32), kT, 0, s>>>(A.n_rows, A.rp.get(), A.ci.get(), own.get(), excl.get(),
+                                                        cci.get(), A.cp.get());
+  cuda_check(cudaMemcpyAsync(A.cp.get() + n, &nci, sizeof(long long), cudaMemcpyHostToDevice, s), "share cp end");
   cuda_check(cudaStreamSynchronize(s), "share_columns");
   A.ci = std::move(cci);
   A.nci = nci;
@@ -471,12 +507,11 @@ DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s) {
     M.strided_rows = 1;  // one row per CTA: most parallel loads for few-row operators
     M.csr = std::move(A);
     // the warp-row kernel's operators (A_l, R_l of an aggregation hierarchy): the coarse dofs of an
-    // aggregate (6 with the rigid-body near-null space, else 3) have one column list — keep it once
-    // per aggregate: 12 -> 8.7 B per entry.  FRACPREC_B200_SHARED_COLS=0 keeps plain CSR.
+    // aggregate mostly have one column list — a row with exactly its predecessor's columns reads that
+    // row's list, so the list is stored (and streamed from HBM) once per run: 12 -> ~8.7 B per entry.
+    // FRACPREC_B200_SHARED_COLS=0 keeps plain CSR.
     const char* e = std::getenv("FRACPREC_B200_SHARED_COLS");
-    if (M.csr.n_rows >= 2048 && !(e && std::atoi(e) == 0))
-      for (int G : {6, 3, 2})
-        if (M.csr.n_rows % G == 0 && share_columns(M.csr, G, s)) break;
+    if (M.csr.n_rows >= 2048 && !(e && std::atoi(e) == 0)) share_columns(M.csr, s);
     return M;
   }
   const double avg = A.n_rows > 0 ? double(A.nnz) / A.n_rows : 0.0;

@@ -201,11 +201,13 @@ __global__ void __launch_bounds__(256) sell_kernel(SellView A, G g, E epi) {
 template <class G, class E, int U = 4>
 __global__ void __launch_bounds__(256) bp3_kernel(Bp3View A, G g, E epi) {
   pdl_entry();
-  const int node = blockIdx.x * blockDim.x + threadIdx.x;
-  if (node >= A.n_nodes) return;
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  if (slot >= A.n_slots) return;
+  const int node = A.node[slot];  // nodes sorted by length inside windows (less padding per slice)
+  if (node < 0) return;
   const auto p0 = epi.load(3 * node), p1 = epi.load(3 * node + 1), p2 = epi.load(3 * node + 2);
-  const long long s0 = A.slice_off[node >> 5];
-  const int lane = node & 31, len = A.node_len[node];
+  const long long s0 = A.slice_off[slot >> 5];
+  const int lane = slot & 31, len = A.node_len[node];
   const int* __restrict__ C = A.cols + s0 + lane;
   const double* __restrict__ V = A.vals + 3 * s0 + lane;
   double a = 0.0, b = 0.0, c = 0.0;
@@ -1025,7 +1027,7 @@ __global__ void mcgs_color_kernel(CsrView A, const int* rows, int n_rows, const 
 // (y_q or x_q) is written into every CTA's shared memory through distributed shared memory, then one
 // cluster barrier; the matrices stream from HBM once per apply (H, G forward; K, F backward) and
 // their loads do not depend on the chain, so they issue ahead of the barrier.
-constexpr int kPanelCluster = 8, kPanelThreads = 256, kPanelWarps = kPanelCluster * kPanelThreads / 32;
+constexpr int kPanelCluster = 8, kPanelThreads = 512, kPanelWarps = kPanelCluster * kPanelThreads / 32;
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 
@@ -1042,7 +1044,7 @@ __device__ __forceinline__ double warp_tree(double s) {
 // into every CTA's copy of the block's z (zs, the backward chain's input), the backward chain keeps
 // the rows its warps own (own) and writes them out after the last barrier.
 // R rows of a panel per warp and E entries of a row per lane (templated so a step issues only the
-// instructions the block's panel size needs: p <= 64 * R, p <= 32 * E).
+// instructions the block's panel size needs: p <= 128 * R, p <= 32 * E).
 template <bool fwd, int R, int E>
 __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw, int lane, double (*chain)[kPanelMax],
                                             double* zs, double* own, const double* xin, double xs,

@@ -130,3 +130,4 @@ def test_config2_shared_column_lists_bitwise(variant, monkeypatch):
     y = pc.apply(xd).cpu().numpy()
     assert np.array_equal(y, pc_plain.apply(xd).cpu().numpy())
     assert np.array_equal(y, opc.apply(x))
+
