@@ -65,6 +65,24 @@ struct CsrView {  // plain CSR, 64-bit offsets (warp-per-row kernel)
   const long long* cp = nullptr;
 };
 
+// Quad-per-row layout for the strided32 row sums of operators with many rows (AMG level 1 and its
+// restriction at the large configs).  Rows are sorted by length inside windows of kSrtWindow rows
+// and cut into slices of 8 (slot -> row in `row`, -1 = padding); a warp takes a slice, four lanes
+// per row: lane (rl, q) owns the partials 8 q .. 8 q + 7 of row rl and, in round t, the row's entries
+// 32 t + 8 q + u (u = 0..7).  Values: vals[slice_off[slice] + ((8 t + u) * 8 + rl) * 4 + q], so the
+// warp's u-th load of a round is one 256-byte line; columns: CSR lists shared by runs of
+// equal-pattern rows (share_columns), entry k of row r at ci[cp[r] + k].
+constexpr int kSrtWindow = 2048, kSrtRows = 8;
+struct SrtView {
+  int n_slices = 0;
+  const int* row = nullptr;              // 8 per slice
+  const long long* slice_off = nullptr;  // n_slices + 1; a slice holds 256 values per round
+  const int* row_len = nullptr;
+  const long long* cp = nullptr;
+  const int* ci = nullptr;
+  const double* vals = nullptr;
+};
+
 // Windowed slices for the ordered long-row pipeline (csr_pipe_kernel): rows
 // grouped 32 to a slice (sorted by length inside chunks of 4096 rows to cut
 // padding), each slice stored as windows of 32 x 32 slots [window][row][lane]

@@ -4,7 +4,6 @@
 #include <omp.h>
 
 #include <algorithm>
-#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -97,6 +96,12 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s, const int
   }
   if (A.strided) {
     if (A.csr.n_rows == 0) return;
+    if (A.srt && !rows) {  // many rows: four lanes per row (full launches; row subsets take the warp-row kernel)
+      const SrtView V = A.sr.view();
+      launch(srt_kernel<G, E>, dim3(blocks_for(V.n_slices, 8)), dim3(256), 0, s, "srt_kernel", V, g, e);
+      cuda_check(cudaGetLastError(), "srt_kernel launch");
+      return;
+    }
     if (A.csr.n_rows >= 2048) {
       CsrView V = A.csr.view();
       if (rows) V.row_map = rows, V.n_rows = n_sub;  // row subset (sparse right-hand side)
@@ -1057,8 +1062,7 @@ GmresSolver::GmresSolver(const DeviceSystem& sys, DevicePrecond& pc, int restart
   }
   big_nblk_ = int((n_ + kBigTile - 1) / kBigTile);
   partial_.alloc(size_t(std::max({(2 * ldr_ + 4) * (long long)mgs_grid_, (long long)red_grid_,
-                                  (ldr_ + 2) * (long long)big_nblk_,
-                                  (ldr_ + 2) * 8LL * sm_count()})));  // cgs_big_project_dots: one value per resident block
+                                  (ldr_ + 2) * (long long)big_nblk_})));
   big_coef_.alloc(size_t(ldr_ + 2));
   big_state_.alloc(1);
   cuda_check(cudaHostAlloc(&status_h_, 2 * sizeof(GmresStatus), cudaHostAllocMapped), "cudaHostAlloc");
@@ -1137,48 +1141,12 @@ void GmresSolver::launch_mgs(MgsArgs& a, int orth, cudaStream_t s) {
     CgsBigArgs b{a, big_nblk_, partial_.get(), big_coef_.get(), big_state_.get(), 0};
     cuda_check(cudaMemsetAsync(big_state_.get(), 0, sizeof(CgsState), s), "cgs state");
     const dim3 tiles(big_nblk_), one(1), T(kBigT);
-    const int ncol = a.m + 1;
-    static const bool fuse_env = [] {
-      const char* e = std::getenv("FRACPREC_B200_CGS_FUSE");
-      return !(e && std::atoi(e) == 0);
-    }();
-    if (fuse_env && ncol <= 52) {
-      // first projection + the second pass's dots in one pass over the basis (cgs_big_project_dots)
-      auto fused = [&](auto kern) {
-        static std::map<const void*, int> occ;  // blocks per SM, per instantiation
-        int& per_sm = occ[reinterpret_cast<const void*>(kern)];
-        if (!per_sm) {
-          cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFuseT, 0), "cgs fuse occupancy");
-          per_sm = std::max(per_sm, 1);
-        }
-        const int grid = int(std::min<long long>((n_ + kFuseT - 1) / kFuseT, (long long)per_sm * sm_count()));
-        b.pass = 0;
-        launch(cgs_big_dots, tiles, T, 0, s, "cgs_big_dots", b);
-        launch(cgs_big_reduce, one, T, 0, s, "cgs_big_reduce", b);
-        CgsBigArgs f = b;  // the fused kernel's partials: `grid` values per set, ||w'||^2 in set m + 1
-        f.nblk = grid, f.norm_set = ncol;
-        launch(kern, dim3(grid), dim3(kFuseT), 0, s, "cgs_big_project_dots", f);
-        launch(cgs_big_norm, one, T, 0, s, "cgs_big_norm", f, 0);
-        f.pass = 1;
-        launch(cgs_big_reduce, one, T, 0, s, "cgs_big_reduce", f);
-        b.pass = 1;
-        launch(cgs_big_project, tiles, T, 0, s, "cgs_big_project", b);
-        launch(cgs_big_norm, one, T, 0, s, "cgs_big_norm", b, 1);
-      };
-      if (ncol <= 13)
-        fused(cgs_big_project_dots<13>);
-      else if (ncol <= 26)
-        fused(cgs_big_project_dots<26>);
-      else
-        fused(cgs_big_project_dots<52>);
-    } else {
-      for (int pass = 0; pass < 2; ++pass) {
-        b.pass = pass;
-        launch(cgs_big_dots, tiles, T, 0, s, "cgs_big_dots", b);
-        launch(cgs_big_reduce, one, T, 0, s, "cgs_big_reduce", b);
-        launch(cgs_big_project, tiles, T, 0, s, "cgs_big_project", b);
-        launch(cgs_big_norm, one, T, 0, s, "cgs_big_norm", b, pass);
-      }
+    for (int pass = 0; pass < 2; ++pass) {
+      b.pass = pass;
+      launch(cgs_big_dots, tiles, T, 0, s, "cgs_big_dots", b);
+      launch(cgs_big_reduce, one, T, 0, s, "cgs_big_reduce", b);
+      launch(cgs_big_project, tiles, T, 0, s, "cgs_big_project", b);
+      launch(cgs_big_norm, one, T, 0, s, "cgs_big_norm", b, pass);
     }
     launch(cgs_big_normalize, tiles, T, 0, s, "cgs_big_normalize", b);
     return;

@@ -98,6 +98,21 @@ struct DeviceMatrix {  // setup.hpp: a device-resident level operator
 }  // namespace fpb
 namespace fpd {
 
+struct DSrt {  // quad-per-row strided32 layout (SrtView)
+  int n_rows = 0;
+  int64_t nnz = 0, nci = 0, slots = 0;
+  DevBuf<int> row, len, ci;
+  DevBuf<long long> off, cp;
+  DevBuf<double> vals;
+  SrtView view() const {
+    return {int(row.size() / kSrtRows), row.get(), off.get(), len.get(), cp.get(), ci.get(), vals.get()};
+  }
+  // values once, the shared column lists once, per row: slot -> row, length, list offset (+ slice offsets)
+  double matrix_bytes() const { return 8.0 * double(nnz) + 4.0 * double(nci) + 17.0 * n_rows; }
+};
+// the layout of A (same entries, same order per row); shares column lists where rows allow
+DSrt srt_from(const DCsr& A, cudaStream_t s);
+
 struct DPipe {
   int n_rows = 0, n_slices = 0, n_ctas = 0;
   int64_t nnz = 0, slots = 0;
@@ -121,6 +136,8 @@ struct DMat {
   bool strided = false;  // row_sum = strided32 (extension): csr_warp_kernel / csr_slice_strided_kernel
   bool bp3 = false;      // node-blocked rows (finest prolongation): bp3_kernel
   DBp3 bp;
+  bool srt = false;      // strided && many rows: quad-per-row srt_kernel for full launches (csr stays for row subsets)
+  DSrt sr;
   int strided_rows = 4;  // rows per CTA of csr_slice_strided_kernel
   DSell sell;
   DCsr csr;
@@ -128,7 +145,7 @@ struct DMat {
   int n_rows() const { return bp3 ? 3 * bp.n_nodes : pipe ? pm.n_rows : warp ? csr.n_rows : sell.n_rows; }
   int64_t nnz() const { return bp3 ? bp.nnz : pipe ? pm.nnz : warp ? csr.nnz : sell.nnz; }
   double matrix_bytes() const {
-    return bp3 ? bp.matrix_bytes() : pipe ? pm.matrix_bytes() : warp ? csr.matrix_bytes() : sell.matrix_bytes();
+    return bp3 ? bp.matrix_bytes() : srt ? sr.matrix_bytes() : pipe ? pm.matrix_bytes() : warp ? csr.matrix_bytes() : sell.matrix_bytes();
   }
 };
 // few_rows_parallel: operators with under 2048 rows take the row-parallel slice kernel even

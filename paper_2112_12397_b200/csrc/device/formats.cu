@@ -291,6 +291,92 @@ DSell sell_from(const DCsr& A, cudaStream_t s) {
   return D;
 }
 
+namespace {
+__global__ void srt_key_kernel(int n, const int* len, unsigned long long* key, int* val) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  key[i] = ((unsigned long long)(i / kSrtWindow) << 32) | (unsigned)(0x7fffffff - len[i]);
+  val[i] = int(i);
+}
+// slot -> row in sorted order (-1 past the end), and the values of each slice of 8 rows: 256 per round
+// of 32 entries of its longest row
+__global__ void srt_slots_kernel(int n, int ns, const int* sorted, const int* len, int* row, long long* out) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s > ns) return;
+  if (s == ns) {
+    out[s] = 0;
+    return;
+  }
+  int mx = 0;
+  for (int r = 0; r < kSrtRows; ++r) {
+    const long long q = s * kSrtRows + r;
+    const int i = q < n ? sorted[q] : -1;
+    row[q] = i;
+    if (i >= 0) mx = max(mx, len[i]);
+  }
+  out[s] = (long long)((mx + 31) / 32) * 32 * kSrtRows;
+}
+__global__ void srt_fill_kernel(int n_slots, const int* row, const long long* rp, const double* v, const long long* off,
+                                double* vals) {
+  const long long slot = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (slot >= n_slots) return;
+  const long long r = row[slot];
+  if (r < 0) return;
+  const int rl = int(slot % kSrtRows);
+  const long long base = off[slot / kSrtRows], r0 = rp[r], m = rp[r + 1] - r0;
+  for (long long k = 0; k < m; ++k) {
+    const long long t = k / 32, q = (k % 32) / 8, u = k % 8;
+    vals[base + ((8 * t + u) * kSrtRows + rl) * 4 + q] = v[r0 + k];
+  }
+}
+}  // namespace
+
+DSrt srt_from(const DCsr& A, cudaStream_t s) {
+  DSrt D;
+  const int n = A.n_rows;
+  D.n_rows = n, D.nnz = A.nnz;
+  if (n == 0) return D;
+  const int ns = (n + kSrtRows - 1) / kSrtRows;
+  D.len.alloc(size_t(n));
+  row_len_kernel<<<grid_for(n), kT, 0, s>>>(n, A.rp.get(), D.len.get());
+  // rows by (window, length descending): a stable sort, so a run of equal-pattern rows stays together
+  DevBuf<int> sorted{size_t(n)};
+  {
+    DevBuf<unsigned long long> kin{size_t(n)}, kout{size_t(n)};
+    DevBuf<int> vin{size_t(n)};
+    srt_key_kernel<<<grid_for(n), kT, 0, s>>>(n, D.len.get(), kin.get(), vin.get());
+    size_t tb = 0;
+    cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.get(), kout.get(), vin.get(), sorted.get(), n, 0, 64, s),
+               "srt sort size");
+    DevBuf<unsigned char> tmp(tb);
+    cuda_check(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, kin.get(), kout.get(), vin.get(), sorted.get(), n, 0, 64, s),
+               "srt sort");
+    cuda_check(cudaStreamSynchronize(s), "srt sort");
+  }
+  DevBuf<long long> sl(size_t(ns) + 1);
+  D.off.alloc(size_t(ns) + 1);
+  D.row.alloc(size_t(ns) * kSrtRows);
+  srt_slots_kernel<<<grid_for(ns + 1), kT, 0, s>>>(n, ns, sorted.get(), D.len.get(), D.row.get(), sl.get());
+  D.slots = exclusive_scan(sl.get(), D.off.get(), ns, s);
+  D.vals.alloc(size_t(D.slots));
+  cuda_check(cudaMemsetAsync(D.vals.get(), 0, D.vals.bytes(), s), "memset");
+  srt_fill_kernel<<<grid_for((long long)ns * kSrtRows), kT, 0, s>>>(ns * kSrtRows, D.row.get(), A.rp.get(), A.v.get(),
+                                                                  D.off.get(), D.vals.get());
+  // the columns: shared lists where A has them (share_columns), else its own CSR lists
+  D.cp.alloc(size_t(n) + 1);
+  if (A.cp.size()) {
+    D.nci = A.nci;
+    cuda_check(cudaMemcpyAsync(D.cp.get(), A.cp.get(), D.cp.bytes(), cudaMemcpyDeviceToDevice, s), "srt cp");
+  } else {
+    D.nci = A.nnz;
+    cuda_check(cudaMemcpyAsync(D.cp.get(), A.rp.get(), D.cp.bytes(), cudaMemcpyDeviceToDevice, s), "srt cp");
+  }
+  D.ci.alloc(size_t(D.nci));
+  cuda_check(cudaMemcpyAsync(D.ci.get(), A.ci.get(), D.ci.bytes(), cudaMemcpyDeviceToDevice, s), "srt ci");
+  cuda_check(cudaStreamSynchronize(s), "srt_from");
+  return D;
+}
+
 DBp3 bp3_from(const DCsr& A, cudaStream_t s) {
   DBp3 D;
   if (A.n_rows % 3 != 0 || A.n_rows == 0) return D;
@@ -512,6 +598,15 @@ DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s) {
     // FRACPREC_B200_SHARED_COLS=0 keeps plain CSR.
     const char* e = std::getenv("FRACPREC_B200_SHARED_COLS");
     if (M.csr.n_rows >= 2048 && !(e && std::atoi(e) == 0)) share_columns(M.csr, s);
+    // enough rows to fill the machine with four lanes per row: the strided32 sums from sorted slices
+    // (srt_kernel); the CSR stays for the row-subset launches of the sparse right-hand side.
+    // FRACPREC_B200_SRT_MIN_ROWS overrides the threshold (tests force it on small levels; 0 = never).
+    long long srt_min = 131072;
+    if (const char* q = std::getenv("FRACPREC_B200_SRT_MIN_ROWS")) srt_min = std::atoll(q);
+    if (srt_min > 0 && M.csr.n_rows >= srt_min) {
+      M.sr = srt_from(M.csr, s);
+      M.srt = true;
+    }
     return M;
   }
   const double avg = A.n_rows > 0 ? double(A.nnz) / A.n_rows : 0.0;

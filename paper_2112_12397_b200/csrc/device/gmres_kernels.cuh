@@ -600,7 +600,6 @@ struct CgsBigArgs {
   double* coef;        // ncol + 1: this pass's coefficients (+ ||w||^2)
   CgsState* st;
   int pass;            // 0: first pass, 1: the DGKS second pass
-  int norm_set = 0;    // cgs_big_norm sums the ||w||^2 partials of set norm_set (nblk per set)
 };
 
 __device__ __forceinline__ double big_block_sum(double v, double* red) {  // valid in thread 0
@@ -729,65 +728,6 @@ __global__ void __launch_bounds__(kBigT) cgs_big_project(CgsBigArgs b) {
   if (threadIdx.x == 0) b.part[blockIdx.x] = t;
 }
 
-// First projection fused with the second pass's dot products: the DGKS second pass runs in almost
-// every step (bench: 484 of 500), and its coefficients <V_i, w'> need the basis entries the first
-// projection w' = w - sum_i coef_i V_i has just read.  A thread keeps its entry of all m + 1 basis
-// columns in registers (every load of an entry issued before the first use), projects (i ascending:
-// the entry is bitwise cgs_big_project's), and accumulates its products v_i w' over the grid-stride
-// loop; one block reduction per coefficient at the end.  One pass over V instead of two.  The dots
-// are speculative (cgs_big_reduce / cgs_big_project of pass 1 exit when the test says no second
-// pass).  Partials: set i (i <= m) of gridDim.x values each, ||w'||^2 in set m + 1.
-// MC = register columns (m + 1 <= MC); 2 blocks per SM up to 26 columns, else 1.
-constexpr int kFuseT = 256;
-template <int MC>
-__global__ void __launch_bounds__(kFuseT, MC <= 26 ? 2 : 1) cgs_big_project_dots(CgsBigArgs b) {
-  if (b.st->abort) return;
-  __shared__ double red[kFuseT / 32];
-  __shared__ double c[MC];
-  const MgsArgs& a = b.a;
-  const int ncol = a.m + 1;
-  for (int i = threadIdx.x; i < MC; i += kFuseT) c[i] = i < ncol ? b.coef[i] : 0.0;
-  __syncthreads();
-  double* wg = a.V + (long long)(a.m + 1) * a.ldv;
-  double acc[MC];
-#pragma unroll
-  for (int i = 0; i < MC; ++i) acc[i] = 0.0;
-  double n2 = 0.0;
-  for (long long k = (long long)blockIdx.x * kFuseT + threadIdx.x; k < a.n; k += (long long)gridDim.x * kFuseT) {
-    double v[MC];
-#pragma unroll
-    for (int i = 0; i < MC; ++i) v[i] = i < ncol ? __ldcs(a.V + (long long)i * a.ldv + k) : 0.0;
-    double w = wg[k];
-#pragma unroll
-    for (int i = 0; i < MC; ++i)
-      if (i < ncol) w = w - c[i] * v[i];
-    wg[k] = w;
-    n2 += w * w;
-#pragma unroll
-    for (int i = 0; i < MC; ++i)
-      if (i < ncol) acc[i] += v[i] * w;
-  }
-  auto block_total = [&](double v) {  // valid in thread 0
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double t = 0.0;
-    if (threadIdx.x == 0)
-      for (int q = 0; q < kFuseT / 32; ++q) t += red[q];
-    __syncthreads();
-    return t;
-  };
-#pragma unroll
-  for (int i = 0; i < MC; ++i) {
-    if (i < ncol) {  // block-uniform
-      const double t = block_total(acc[i]);
-      if (threadIdx.x == 0) b.part[(long long)i * gridDim.x + blockIdx.x] = t;
-    }
-  }
-  const double t = block_total(n2);
-  if (threadIdx.x == 0) b.part[(long long)ncol * gridDim.x + blockIdx.x] = t;
-}
-
 // ||w|| after a pass (fixed order), the DGKS test after the first, and after the last
 // pass the status, h[m+1] and the Givens update (mgs_finish); one block
 __global__ void __launch_bounds__(kBigT) cgs_big_norm(CgsBigArgs b, int last) {
@@ -796,7 +736,7 @@ __global__ void __launch_bounds__(kBigT) cgs_big_norm(CgsBigArgs b, int last) {
   __shared__ double sm[40];
   if (!(b.pass == 1 && !b.st->reorth)) {  // the pass ran: its norm
     double v = 0.0;
-    for (int t = threadIdx.x; t < b.nblk; t += kBigT) v += b.part[(long long)b.norm_set * b.nblk + t];
+    for (int t = threadIdx.x; t < b.nblk; t += kBigT) v += b.part[t];
     const double tot = big_block_sum(v, sm);
     if (threadIdx.x == 0) b.st->hnext = sqrt(tot);
   }

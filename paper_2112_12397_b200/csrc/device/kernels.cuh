@@ -361,6 +361,57 @@ __global__ void __launch_bounds__(256) csr_warp_kernel(CsrView A, G g, E epi) {
   if (lane == 0) epi(grow, s, pre);
 }
 
+// many rows (>= ~131k): four lanes per row over sorted slices of 8 rows (SrtView), still the strided32
+// sum.  Lane (rl, q) keeps the partials 8 q .. 8 q + 7 of row rl (entry k -> partial k mod 32, each in
+// order from +0.0); the xor tree's levels h = 16 and 8 are shuffles between the row's four lanes
+// (partial l ^ 16 lives in lane q ^ 2, l ^ 8 in q ^ 1), the levels 4, 2, 1 add inside the lane, every
+// addition "own + partner" as in xor_tree32 — lane q = 0's partial 0 ends as that tree's lane-0
+// result bit for bit.  All 8 loads of a lane's round are issued together; the warp's u-th value load
+// is one 256-byte line, the column lists (shared by the rows of an aggregate) come through L1.
+template <class G, class E>
+__global__ void __launch_bounds__(256, 3) srt_kernel(SrtView A, G g, E epi) {
+  pdl_entry();
+  const int slice = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (slice >= A.n_slices) return;  // warp-uniform
+  const int lane = threadIdx.x & 31, rl = lane >> 2, q = lane & 3;
+  const int row = A.row[slice * kSrtRows + rl];
+  const int len = row >= 0 ? A.row_len[row] : 0;
+  typename E::P pre{};
+  if (q == 0 && row >= 0) pre = epi.load(row);
+  const long long o0 = A.slice_off[slice];
+  const int rounds = int((A.slice_off[slice + 1] - o0) >> 8);  // 256 values per round
+  const int* __restrict__ C = A.ci + (row >= 0 ? A.cp[row] : 0) + 8 * q;
+  const double* __restrict__ V = A.vals + o0 + lane;
+  double s[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s[u] = 0.0;
+  for (int t = 0; t < rounds; ++t) {
+    const int k0 = 32 * t + 8 * q;
+    int c[8];
+    double v[8], x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool in = k0 + u < len;
+      c[u] = in ? __ldg(C + 32 * t + u) : 0;
+      v[u] = in ? __ldg(V + (8 * t + u) * 32) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = k0 + u < len ? g(c[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (k0 + u < len) s[u] = s[u] + v[u] * x[u];
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s[u] = s[u] + __shfl_xor_sync(0xffffffffu, s[u], 2);  // h = 16
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s[u] = s[u] + __shfl_xor_sync(0xffffffffu, s[u], 1);  // h = 8
+#pragma unroll
+  for (int h = 4; h > 0; h >>= 1)
+#pragma unroll
+    for (int u = 0; u < h; ++u) s[u] = s[u] + s[u + h];
+  if (q == 0 && row >= 0) epi(row, s[0], pre);
+}
+
 // few long rows: R rows per CTA of 512 threads; in each window of W = 4096 / R
 // entries per row every thread loads 8 entries (one round of loads for the whole
 // window) and stores their products in shared memory; warp r then adds row r's

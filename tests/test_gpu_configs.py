@@ -131,3 +131,21 @@ def test_config2_shared_column_lists_bitwise(variant, monkeypatch):
     assert np.array_equal(y, pc_plain.apply(xd).cpu().numpy())
     assert np.array_equal(y, opc.apply(x))
 
+
+@pytest.mark.parametrize("variant", ["tpu", "tup"])
+def test_config2_quad_per_row_strided_layout_bitwise(variant, monkeypatch):
+    """The quad-per-row strided32 layout (srt_kernel: slices of 8 length-sorted rows, four lanes per row, 32 partials
+    and the xor tree split between shuffles and in-lane additions; taken from 131k rows on, forced here onto every
+    coarse operator of config 2) gives the warp-per-row kernel's sums bit for bit: the apply stays
+    bitwise the oracle's."""
+    monkeypatch.setenv("FRACPREC_B200_SRT_MIN_ROWS", "1")
+    J, osys, op, pc, opc = setup(2, variant, "strided")
+    monkeypatch.delenv("FRACPREC_B200_SRT_MIN_ROWS")
+    x = np.random.default_rng(7).uniform(-1, 1, J.total_dimension())
+    xd = torch.tensor(x, device="cuda", dtype=torch.float64)
+    assert np.array_equal(pc.apply(xd).cpu().numpy(), opc.apply(x))
+    monkeypatch.setenv("FRACPREC_B200_SRT_MIN_ROWS", "0")
+    amg = api.AmgConfig(strength_threshold=0.0, row_sum="strided")
+    pc_warp = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, api.PrecondConfig(variant, amg=amg)))
+    assert pc.traffic()["apply_bytes"] != pc_warp.traffic()["apply_bytes"]  # the layout did engage
+    assert np.array_equal(pc.apply(xd).cpu().numpy(), pc_warp.apply(xd).cpu().numpy())
