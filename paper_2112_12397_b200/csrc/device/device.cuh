@@ -34,7 +34,12 @@ struct SellView {
   const int* row_len = nullptr;
   const int* cols = nullptr;
   const double* vals = nullptr;
+  // optional (sell_kernel only): rows sorted by length inside windows of kSellWindow rows before
+  // slicing, slot -> row (-1 = padding); null: slot = row
+  int n_slots = 0;
+  const int* rows = nullptr;
 };
+constexpr int kSellWindow = 2048;
 
 // Node-blocked rows (the finest prolongation P_1 with a 3x3-block fine level): the three
 // scalar rows of a node share one column pattern, so a slot holds one column index and

@@ -59,9 +59,9 @@ void launch_sell(const DSell& A, const G& g, const E& e, cudaStream_t s) {
   if (A.n_rows == 0) return;
   // 8 entries per round from 16 entries per row on (P_1: A/B config 2 apply 0.3521 -> 0.3510 ms)
   if (A.nnz >= 16LL * A.n_rows)
-    launch(sell_kernel<G, E, 8>, dim3(blocks_for(A.n_rows, 256)), dim3(256), 0, s, "sell_kernel", A.view(), g, e);
+    launch(sell_kernel<G, E, 8>, dim3(blocks_for((long long)A.n_slices * kSlice, 256)), dim3(256), 0, s, "sell_kernel", A.view(), g, e);
   else
-    launch(sell_kernel<G, E>, dim3(blocks_for(A.n_rows, 256)), dim3(256), 0, s, "sell_kernel", A.view(), g, e);
+    launch(sell_kernel<G, E>, dim3(blocks_for((long long)A.n_slices * kSlice, 256)), dim3(256), 0, s, "sell_kernel", A.view(), g, e);
   cuda_check(cudaGetLastError(), "sell_kernel launch");
 }
 
@@ -322,7 +322,7 @@ DMat mat_from_ref(const DCsr& A, bool few_rows_parallel, bool strided) {
   if (strided || (warp && A.n_rows < 2048)) return mat_from(clone_csr(A), few_rows_parallel, strided, 0);
   if (!warp) {
     DMat M;
-    M.sell = sell_from(A, 0);
+    M.sell = sell_from(A, 0, sell_sorted());
     return M;
   }
   DMat M;
@@ -1141,10 +1141,17 @@ void GmresSolver::launch_mgs(MgsArgs& a, int orth, cudaStream_t s) {
     CgsBigArgs b{a, big_nblk_, partial_.get(), big_coef_.get(), big_state_.get(), 0};
     cuda_check(cudaMemsetAsync(big_state_.get(), 0, sizeof(CgsState), s), "cgs state");
     const dim3 tiles(big_nblk_), one(1), T(kBigT);
+    if (cgs_dots_smem_bytes(restart_) > 48 * 1024) {
+      static bool set = false;
+      if (!set)
+        cuda_check(cudaFuncSetAttribute(cgs_big_dots, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(cgs_dots_smem_bytes(kCgsMaxCols))), "cgs dots smem attribute");
+      set = true;
+    }
     for (int pass = 0; pass < 2; ++pass) {
       b.pass = pass;
-      launch(cgs_big_dots, tiles, T, 0, s, "cgs_big_dots", b);
-      launch(cgs_big_reduce, one, T, 0, s, "cgs_big_reduce", b);
+      launch(cgs_big_dots, tiles, T, cgs_dots_smem_bytes(restart_), s, "cgs_big_dots", b);
+      launch(cgs_big_reduce, dim3(a.m + 1 + (pass == 0 ? 1 : 0)), T, 0, s, "cgs_big_reduce", b);
       launch(cgs_big_project, tiles, T, 0, s, "cgs_big_project", b);
       launch(cgs_big_norm, one, T, 0, s, "cgs_big_norm", b, pass);
     }

@@ -31,10 +31,12 @@ struct DSell {
   long long slots = 0;
   int64_t nnz = 0;
   DevBuf<long long> off;
-  DevBuf<int> len, cols;
+  DevBuf<int> len, cols, rows;  // rows: slot -> row of the length-sorted variant (sell_from(.., sorted))
   DevBuf<double> vals;
-  SellView view() const { return {n_rows, off.get(), len.get(), cols.get(), vals.get()}; }
-  double matrix_bytes() const { return 12.0 * double(nnz) + 4.0 * (n_rows + 1); }  // CSR-equivalent
+  SellView view() const {
+    return {n_rows, off.get(), len.get(), cols.get(), vals.get(), int(rows.size()), rows.size() ? rows.get() : nullptr};
+  }
+  double matrix_bytes() const { return 12.0 * double(nnz) + 4.0 * (n_rows + 1) + 4.0 * double(rows.size()); }  // CSR-equivalent
 };
 
 struct DBsr3 {
@@ -175,12 +177,14 @@ struct SystemView {  // BlockSystem (block.hpp:36-45) as borrowed views
 DCsr upload_csr(const HostCsrView& A);
 inline DCsr upload_csr(const fpb::Csr& A) { return upload_csr(HostCsrView::of(A)); }
 fpb::Csr download_csr(const DCsr& A);
-DSell sell_from(const DCsr& A, cudaStream_t s);
+// sorted: rows sorted by length inside windows before slicing (for sell_kernel launches only)
+DSell sell_from(const DCsr& A, cudaStream_t s, bool sorted = false);
 DBp3 bp3_from(const DCsr& A, cudaStream_t s);
 DBsr3 bsr3_from(const DCsr& A, const std::vector<int>* brows, cudaStream_t s);
 DPipe pipe_from(const DCsr& A, cudaStream_t s);
 DCsr transpose_dev(const DCsr& A, cudaStream_t s);  // rows of A^T list the source rows ascending
 DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s);
+bool sell_sorted();
 // Rows with exactly their predecessor's columns share that row's list (ci shrinks, cp gives each
 // row its list); returns false and leaves A as it is when under 1/8 of the indices would go.  The
 // entries and their order per row do not change.

@@ -269,7 +269,23 @@ fpb::Csr download_csr(const DCsr& D) {
 }
 
 // ------------------------------------------------------------------ layouts
-DSell sell_from(const DCsr& A, cudaStream_t s) {
+namespace {
+__global__ void sell_fill_sorted_kernel(int n_slots, const int* rows, const long long* rp, const int* ci, const double* v,
+                                        const long long* off, int* cols, double* vals) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (q >= n_slots) return;
+  const long long i = rows[q];
+  if (i < 0) return;
+  const long long base = off[q / kSlice] + (q % kSlice);
+  const long long r0 = rp[i], m = rp[i + 1] - r0;
+  for (long long k = 0; k < m; ++k) {
+    cols[base + k * kSlice] = ci[r0 + k];
+    vals[base + k * kSlice] = v[r0 + k];
+  }
+}
+}  // namespace
+
+DSell sell_from(const DCsr& A, cudaStream_t s, bool sorted) {
   DSell D;
   D.n_rows = A.n_rows, D.n_cols = A.n_cols, D.nnz = A.nnz;
   D.n_slices = (A.n_rows + kSlice - 1) / kSlice;
@@ -277,6 +293,36 @@ DSell sell_from(const DCsr& A, cudaStream_t s) {
   if (A.n_rows) row_len_kernel<<<grid_for(A.n_rows), kT, 0, s>>>(A.n_rows, A.rp.get(), D.len.get());
   DevBuf<long long> sl(size_t(D.n_slices) + 1);
   D.off.alloc(size_t(D.n_slices) + 1);
+  if (sorted && A.n_rows > kSlice) {
+    // rows by (window, length descending), then slices of 32: almost no padding per slice
+    const int n = A.n_rows;
+    DevBuf<int> order{size_t(n)};
+    {
+      DevBuf<unsigned long long> kin{size_t(n)}, kout{size_t(n)};
+      DevBuf<int> vin{size_t(n)};
+      bp3_key_kernel<<<grid_for(n), kT, 0, s>>>(n, D.len.get(), kin.get(), vin.get());
+      size_t tb = 0;
+      cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin.get(), kout.get(), vin.get(), order.get(), n, 0, 64, s),
+                 "sell sort size");
+      DevBuf<unsigned char> tmp(tb);
+      cuda_check(cub::DeviceRadixSort::SortPairs(tmp.get(), tb, kin.get(), kout.get(), vin.get(), order.get(), n, 0, 64, s),
+                 "sell sort");
+      cuda_check(cudaStreamSynchronize(s), "sell sort");
+    }
+    D.rows.alloc(size_t(D.n_slices) * kSlice);
+    bp3_slots_kernel<<<grid_for(D.n_slices + 1), kT, 0, s>>>(n, D.n_slices, order.get(), D.len.get(), D.rows.get(), sl.get());
+    D.slots = exclusive_scan(sl.get(), D.off.get(), D.n_slices, s);
+    D.cols.alloc(size_t(D.slots));
+    D.vals.alloc(size_t(D.slots));
+    if (D.slots) {
+      cuda_check(cudaMemsetAsync(D.cols.get(), 0, D.cols.bytes(), s), "memset");
+      cuda_check(cudaMemsetAsync(D.vals.get(), 0, D.vals.bytes(), s), "memset");
+      sell_fill_sorted_kernel<<<grid_for((long long)D.n_slices * kSlice), kT, 0, s>>>(
+          D.n_slices * kSlice, D.rows.get(), A.rp.get(), A.ci.get(), A.v.get(), D.off.get(), D.cols.get(), D.vals.get());
+    }
+    cuda_check(cudaStreamSynchronize(s), "sell_from");
+    return D;
+  }
   slice_slots_kernel<<<grid_for(D.n_slices + 1), kT, 0, s>>>(A.n_rows, D.n_slices, D.len.get(), sl.get());
   D.slots = exclusive_scan(sl.get(), D.off.get(), D.n_slices, s);
   D.cols.alloc(size_t(D.slots));
@@ -586,6 +632,11 @@ bool share_columns(DCsr& A, cudaStream_t s) {
   return true;
 }
 
+bool sell_sorted() {  // FRACPREC_B200_SELL_SORTED=0: plain SELL-32 for the thread-per-row operators
+  const char* e = std::getenv("FRACPREC_B200_SELL_SORTED");
+  return !(e && std::atoi(e) == 0);
+}
+
 DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s) {
   DMat M;
   if (strided) {  // row_sum = strided32: plain CSR, one warp per row (or window-staged CTAs of R rows)
@@ -615,7 +666,7 @@ DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s) {
   M.warp = A.n_rows > 0 && (avg >= 48.0 || (A.n_rows < 65536 && avg >= 8.0) ||
                             (few_rows_parallel && A.n_rows < 2048 && avg >= 2.0));
   if (!M.warp) {
-    M.sell = sell_from(A, s);
+    M.sell = sell_from(A, s, sell_sorted());
     return M;
   }
   M.slice_rows = A.n_rows >= 2048 ? 32 : 8;

@@ -614,12 +614,16 @@ __device__ __forceinline__ double big_block_sum(double v, double* red) {  // val
   return t;
 }
 
-// tile partials of <V_i, w> (i <= m) and, in the first pass, ||w||^2 (w = J z is copied to V_{m+1})
+// tile partials of <V_i, w> (i <= m) and, in the first pass, ||w||^2 (w = J z is copied to V_{m+1}).
+// Each warp leaves its sum of a column in shared memory; after one barrier a thread per column adds
+// the 16 warp sums in warp order (big_block_sum's order, without its two barriers per column).
 __global__ void __launch_bounds__(kBigT) cgs_big_dots(CgsBigArgs b) {
   if (b.st->abort || (b.pass == 1 && !b.st->reorth)) return;
-  __shared__ double red[kBigT / 32];
+  extern __shared__ double wsum[];  // (m + 2) x 16 warp sums (dynamic: cgs_dots_smem_bytes)
+  constexpr int kW = kBigT / 32;
   const MgsArgs& a = b.a;
   const int ncol = a.m + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long lo = (long long)blockIdx.x * kBigTile;
   double* wg = a.V + (long long)(a.m + 1) * a.ldv;
   double wr[kBigE];
@@ -631,6 +635,10 @@ __global__ void __launch_bounds__(kBigT) cgs_big_dots(CgsBigArgs b) {
     if (b.pass == 0 && k < a.n) wg[k] = wr[j];
     n2 += wr[j] * wr[j];
   }
+  auto warp_sum = [](double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+  };
   for (int i0 = 0; i0 < ncol; i0 += kBigB) {
     double acc[kBigB] = {};
     double v[kBigB][kBigE];
@@ -647,41 +655,48 @@ __global__ void __launch_bounds__(kBigT) cgs_big_dots(CgsBigArgs b) {
       for (int j = 0; j < kBigE; ++j) acc[u] += v[u][j] * wr[j];
 #pragma unroll
     for (int u = 0; u < kBigB; ++u) {
-      const double t = big_block_sum(acc[u], red);
-      if (threadIdx.x == 0 && i0 + u < ncol) b.part[(long long)(i0 + u) * b.nblk + blockIdx.x] = t;
+      const double t = warp_sum(acc[u]);
+      if (lane == 0 && i0 + u < ncol) wsum[(i0 + u) * kW + warp] = t;
     }
   }
   if (b.pass == 0) {
-    const double t = big_block_sum(n2, red);
-    if (threadIdx.x == 0) b.part[(long long)ncol * b.nblk + blockIdx.x] = t;
+    const double t = warp_sum(n2);
+    if (lane == 0) wsum[ncol * kW + warp] = t;
+  }
+  __syncthreads();
+  const int nsets = ncol + (b.pass == 0 ? 1 : 0);
+  for (int i = threadIdx.x; i < nsets; i += kBigT) {
+    double t = 0.0;
+    for (int q = 0; q < kW; ++q) t += wsum[i * kW + q];
+    b.part[(long long)i * b.nblk + blockIdx.x] = t;
   }
 }
 
-// coefficients: warp q sums the tile partials of sets q, q + 16, ... (lane-strided, then an
-// xor tree); the first pass also sets h and ||w_pre||, the second adds to h (gmres.cpp:96-102)
+inline size_t cgs_dots_smem_bytes(int restart) { return sizeof(double) * size_t(restart + 2) * (kBigT / 32); }
+
+// coefficients: block i sums the tile partials of set i (thread-strided, then the fixed-order block
+// sum); the first pass also sets h and ||w_pre||, the second adds to h (gmres.cpp:96-102).
+// Grid: m + 1 blocks, + 1 in the first pass (||w||^2).
 __global__ void __launch_bounds__(kBigT) cgs_big_reduce(CgsBigArgs b) {
   if (b.st->abort || (b.pass == 1 && !b.st->reorth)) return;
+  __shared__ double red[kBigT / 32];
   const MgsArgs& a = b.a;
-  const int ncol = a.m + 1, nsets = ncol + (b.pass == 0 ? 1 : 0);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = warp; i < nsets; i += kBigT / 32) {
-    double v = 0.0;
-    for (int t = lane; t < b.nblk; t += 32) v += b.part[(long long)i * b.nblk + t];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) {
-      if (i < ncol) {
-        b.coef[i] = v;
-        a.h[i] = b.pass == 0 ? v : a.h[i] + v;
-      } else {
-        b.st->wnorm_pre = sqrt(v);
-      }
+  const int ncol = a.m + 1, i = blockIdx.x;
+  double v = 0.0;
+  for (int t = threadIdx.x; t < b.nblk; t += kBigT) v += b.part[(long long)i * b.nblk + t];
+  const double tot = big_block_sum(v, red);
+  if (threadIdx.x != 0) return;
+  if (i < ncol) {
+    b.coef[i] = tot;
+    a.h[i] = b.pass == 0 ? tot : a.h[i] + tot;
+  } else {
+    const double wn = sqrt(tot);
+    b.st->wnorm_pre = wn;
+    if (!isfinite(wn)) {
+      b.st->abort = 1;
+      a.status->nonfinite = 1;
+      a.status->wnorm_pre = wn;
     }
-  }
-  __syncthreads();
-  if (b.pass == 0 && threadIdx.x == 0 && !isfinite(b.st->wnorm_pre)) {
-    b.st->abort = 1;
-    a.status->nonfinite = 1;
-    a.status->wnorm_pre = b.st->wnorm_pre;
   }
 }
 

@@ -34,9 +34,8 @@ struct GPresmooth {  // first Jacobi sweep from x = 0: (omega * b_j) / d_j  (amg
 // One SELL-32 row, left to right (csr.cpp:109-119).  U entries per batch: all U column and
 // value loads (then all U gathers) are issued before the U ordered adds.
 template <class G, int U = 4>
-__device__ __forceinline__ double sell_row(const SellView& A, int row, const G& g) {
-  const long long base = A.slice_off[row >> 5] + (row & 31);
-  const int len = A.row_len[row];
+__device__ __forceinline__ double sell_row_at(const SellView& A, int slot, int len, const G& g) {
+  const long long base = A.slice_off[slot >> 5] + (slot & 31);
   const int* __restrict__ C = A.cols + base;
   const double* __restrict__ V = A.vals + base;
   double s = 0.0;
@@ -53,6 +52,10 @@ __device__ __forceinline__ double sell_row(const SellView& A, int row, const G& 
   }
   for (; k < len; ++k) s = s + __ldg(V + 32 * k) * g(__ldg(C + 32 * k));
   return s;
+}
+template <class G, int U = 4>
+__device__ __forceinline__ double sell_row(const SellView& A, int row, const G& g) {  // slot = row
+  return sell_row_at<G, U>(A, row, A.row_len[row], g);
 }
 
 // ---------------------------------------------------------------- epilogues
@@ -189,10 +192,17 @@ struct EJu {
 template <class G, class E, int U = 4>
 __global__ void __launch_bounds__(256) sell_kernel(SellView A, G g, E epi) {
   pdl_entry();
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= A.n_rows) return;
+  const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+  int row = slot;
+  if (A.rows) {  // length-sorted slices
+    if (slot >= A.n_slots) return;
+    row = A.rows[slot];
+    if (row < 0) return;
+  } else if (row >= A.n_rows) {
+    return;
+  }
   const auto pre = epi.load(row);
-  epi(row, sell_row<G, U>(A, row, g), pre);
+  epi(row, sell_row_at<G, U>(A, slot, A.row_len[row], g), pre);
 }
 
 // Node-blocked rows (Bp3View): one thread per node, its three scalar rows summed left to
