@@ -22,7 +22,7 @@ python tools/ncu_full_summary.py gpurun_out/full_cfg5_raw.csv gpurun_out/ncu_ful
 [ "$(stat -c %s gpurun_out/full_cfg5.ncu-rep 2>/dev/null || echo 0)" -gt 30000000 ] && rm -f gpurun_out/full_cfg5.ncu-rep
 du -sh gpurun_out
 if [ "$SKIP_SANITIZERS" != "1" ]; then for tool in memcheck racecheck synccheck; do
-  timeout 1200 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize.py \
+  timeout 1000 compute-sanitizer --tool $tool --print-limit 50 python tools/sanitize.py \
     > gpurun_out/sanitizer_$tool.log 2>&1
   echo "sanitizer $tool rc=$?"
 done; fi

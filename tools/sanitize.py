@@ -5,7 +5,7 @@
 
 Covers: the system upload and device layouts (BSR3, SELL, node-blocked, windowed pipeline, R = P^T),
 the device setup (SpGEMM incl. the block-per-row path, strength graph, transpose), the preconditioner
-applies (t-p-u, t-u-p, t-u-p*; ordered / strided rows; sweep / inverse / panel factor; Jacobi,
+applies (t-p-u, t-u-p, t-u-p*; ordered / strided rows incl. the quad-per-row layout; sweep / inverse / panel factor; Jacobi,
 Chebyshev, multicolour GS), the cooperative MGS / CGS Arnoldi kernels with the one-ahead step and a
 mid-cycle restage (restart 120), the large-n orthogonalization chain, and the fracture-block assembly.
 Prints one line per phase; exits non-zero on any CUDA error.
@@ -59,6 +59,11 @@ def main():
     os.environ["FRACPREC_B200_BP3_MIN_NODES"] = "1000"
     J2 = api.Workload(2, 42).system()
     run_case(J2, "tup", "ordered", "auto")
+    # the quad-per-row strided layout forced onto every coarse operator (shared column lists, sorted slices)
+    os.environ["FRACPREC_B200_SRT_MIN_ROWS"] = "1"
+    run_case(J2, "tup", "strided", "auto")
+    run_case(J, "tpu", "strided", "auto")
+    del os.environ["FRACPREC_B200_SRT_MIN_ROWS"]
     op = api.BlockSystemOperator(J2)
     pc = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J2, api.PrecondConfig(
         "tup", amg=api.AmgConfig(strength_threshold=0.0, row_sum="strided"))))
