@@ -142,8 +142,10 @@ struct PanelView {
   const long long* off = nullptr;   // per block: offset of its panel matrices
   const double* m = nullptr;
   const double* diag = nullptr;     // spd: D (z = y / D between the sweeps); null for general
-  int m_max = 0;                    // largest block (rows): the kernel keeps the block's z in shared memory
+  int m_max = 0;                    // largest block (rows)
   int p_max_panels = 0;             // most panels of a block: each warp keeps its own rows of x per panel
+  double* z = nullptr;              // n doubles of scratch: z = y / D (or y), written by the forward chain
+  const int* order = nullptr;       // cluster c solves block order[c]: longest chains first
 };
 
 struct DenseLUView {  // coarse-level full-pivot LU, column-major n x n

@@ -756,7 +756,7 @@ struct UploadClock {  // FRACPREC_B200_VERBOSE: phases of the preconditioner upl
 }  // namespace
 
 namespace {
-// shared memory of panel_solve_kernel: the largest block's z (m_max) + each warp's own rows
+// shared memory of panel_solve_kernel: each warp's own rows
 // (most panels x rows per warp of the instantiation the largest panel selects)
 size_t panel_smem_bytes(const fpb::BandFactor& F, const std::vector<int>& pp) {
   int m_max = 0, P_max = 0, p_max = 1;
@@ -765,7 +765,8 @@ size_t panel_smem_bytes(const fpb::BandFactor& F, const std::vector<int>& pp) {
     m_max = std::max(m_max, m), P_max = std::max(P_max, (m + pp[b] - 1) / pp[b]), p_max = std::max(p_max, pp[b]);
   }
   const int R = p_max <= 128 ? 1 : 2;
-  return sizeof(double) * (size_t(m_max) + size_t(kPanelThreads / 32) * size_t(P_max) * R);
+  (void)m_max;
+  return sizeof(double) * (size_t(kPanelThreads / 32) * size_t(P_max) * R);
 }
 }  // namespace
 
@@ -891,8 +892,16 @@ DevicePrecond::DevicePrecond(const DeviceSystem& s, const fpb::HostPrecond& hp) 
       const int m = F.block_start[blk + 1] - F.block_start[blk];
       m_max = std::max(m_max, m), pmax_panels = std::max(pmax_panels, (m + pp[blk] - 1) / pp[blk]);
     }
+    // clusters in order of chain length (panels per block), longest first
+    std::vector<int> order(static_cast<size_t>(nblk));
+    for (int blk = 0; blk < nblk; ++blk) order[size_t(blk)] = blk;
+    auto panels_of = [&](int blk) { return (F.block_start[blk + 1] - F.block_start[blk] + pp[blk] - 1) / pp[blk]; };
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return panels_of(x) > panels_of(y); });
+    pan_order.upload(order);
+    pan_z.alloc(size_t(F.n));
     pview = PanelView{nblk, band_start.get(), pan_p.get(), pan_off.get(), pan_m.get(),
-                      F.kind == fpb::BandFactor::Kind::spd ? band_diag.get() : nullptr, m_max, pmax_panels};
+                      F.kind == fpb::BandFactor::Kind::spd ? band_diag.get() : nullptr, m_max, pmax_panels,
+                      pan_z.get(), pan_order.get()};
     DevBuf<int> dtb, dtq;
     dtb.upload(tb), dtq.upload(tq);
     const long long threads = (long long)tb.size() * 4 * kPanelMax;

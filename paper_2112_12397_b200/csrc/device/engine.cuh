@@ -337,9 +337,9 @@ class DevicePrecond {
   // factor_solve = panel: block-bidiagonal panels, panel_solve_kernel
   bool panel = false;
   PanelView pview{};
-  DevBuf<int> pan_p;
+  DevBuf<int> pan_p, pan_order;
   DevBuf<long long> pan_off;
-  DevBuf<double> pan_m;
+  DevBuf<double> pan_m, pan_z;
   size_t pan_smem = 0;
   double pan_bytes = 0;
   int pan_pmax = 0;

@@ -1101,9 +1101,9 @@ __device__ __forceinline__ double warp_tree(double s) {
 // one chain (forward: D = H, C = G, x = rs b; backward: D = K, C = F, x = z) over the block's panels;
 // before each cluster barrier a warp already loads the next panel's coupling rows into registers and
 // forms its local product, so a step's critical path is the barrier plus a shared-memory dot.  A step
-// touches no global memory: the forward chain broadcasts y into every CTA's chain buffer and z = y / D
-// into every CTA's copy of the block's z (zs, the backward chain's input), the backward chain keeps
-// the rows its warps own (own) and writes them out after the last barrier.
+// broadcasts the new panel into every CTA's chain buffer; the forward chain also stores z = y / D (the
+// backward chain's input) to global memory, the backward chain keeps the rows its warps own (own) and
+// writes them out after the last barrier.
 // R rows of a panel per warp and E entries of a row per lane (templated so a step issues only the
 // instructions the block's panel size needs: p <= 128 * R, p <= 32 * E).
 template <bool fwd, int R, int E>
@@ -1123,7 +1123,7 @@ __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw,
     const int s = rows_of(q), sc = fwd ? (q > 0 ? p : 0) : (q + 1 < P ? rows_of(q + 1) : 0);
     const double* Dm = base + o + (fwd ? 0 : s * s + s * (q > 0 ? p : 0));
     const double* Cm = Dm + s * s;
-    const double* xq = fwd ? xin + b0 + q * p : zs + q * p;
+    const double* xq = fwd ? xin + b0 + q * p : zs + b0 + q * p;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = gw + r * kPanelWarps;
@@ -1132,7 +1132,7 @@ __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw,
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int c = lane + 32 * e;
-        if (c < s) acc = acc + Dm[i * s + c] * (xq[c] * xs);
+        if (c < s) acc = acc + Dm[i * s + c] * ((fwd ? xq[c] : __ldcg(xq + c)) * xs);  // z: written by other SMs
         cr[r][e] = c < sc ? Cm[i * sc + c] : 0.0;
       }
       dl[r] = warp_tree(acc);
@@ -1161,8 +1161,7 @@ __device__ __forceinline__ void panel_chain(const PanelView& V, int blk, int gw,
       const double v = sc ? dl[r] - acc : dl[r];
       if (lane < kPanelCluster) *cluster.map_shared_rank(&chain[q & 1][i], lane) = v;
       if (fwd) {
-        if (lane >= 8 && lane < 8 + kPanelCluster)  // z = y / D (LDL^T), else y
-          *cluster.map_shared_rank(&zs[q * p + i], lane - 8) = V.diag ? v / dg[r] : v;
+        if (lane == 8) zs[b0 + q * p + i] = V.diag ? v / dg[r] : v;  // z = y / D (LDL^T), else y
       } else if (lane == 0) {
         own[q * R + r] = v;
       }
@@ -1184,14 +1183,17 @@ __global__ void __cluster_dims__(kPanelCluster, 1, 1) __launch_bounds__(kPanelTh
   pdl_entry();
   cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
   __shared__ double chain[2][kPanelMax];  // the previous panel of the running chain (y or x)
-  extern __shared__ double pan_dyn[];     // the block's z (m doubles), then each warp's own x rows
+  extern __shared__ double pan_dyn[];     // each warp's own x rows
   const int rank = int(cluster.block_rank());
-  const int blk = blockIdx.x / kPanelCluster;
+  const int blk = V.order[blockIdx.x / kPanelCluster];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = rank * (kPanelThreads / 32) + warp;
   const int b0 = V.block_start[blk], m = V.block_start[blk + 1] - b0, p = V.p[blk], P = (m + p - 1) / p;
-  double* zs = pan_dyn;
-  double* own = pan_dyn + V.m_max + warp * (V.p_max_panels * R);
+  // z stays in global memory (L2): written once by the forward chain, read once by the backward chain a
+  // panel ahead of its use; the cluster barriers between the chains order the accesses.  Shared memory
+  // per CTA is then a few KB, two CTAs fit an SM, and all of config 5's 40 clusters are resident at once.
+  double* zs = V.z;
+  double* own = pan_dyn + warp * (V.p_max_panels * R);
   panel_chain<true, R, E>(V, blk, gw, lane, chain, zs, own, rhs, rs, cluster);
   panel_chain<false, R, E>(V, blk, gw, lane, chain, zs, own, zs, 1.0, cluster);
   if (lane == 0)

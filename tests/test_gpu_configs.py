@@ -149,3 +149,34 @@ def test_config2_quad_per_row_strided_layout_bitwise(variant, monkeypatch):
     pc_warp = api.GpuPreconditioner.from_host(op, api.HostPreconditioner(J, api.PrecondConfig(variant, amg=amg)))
     assert pc.traffic()["apply_bytes"] != pc_warp.traffic()["apply_bytes"]  # the layout did engage
     assert np.array_equal(pc.apply(xd).cpu().numpy(), pc_warp.apply(xd).cpu().numpy())
+
+
+@pytest.mark.parametrize("variant", ["tpu", "tup"])
+def test_config2_outputs_stay_inside_their_buffers(variant):
+    """compute-sanitizer is closed on this GPU pool, so out-of-bounds writes of the output paths are
+    checked directly: inputs and outputs of J apply, preconditioner apply and GMRES live inside one
+    device buffer between guard bands of a sentinel bit pattern, every variant of the input is placed
+    flush against a band, and the bands (and the inputs) must come back bit for bit."""
+    J, osys, op, pc, opc = setup(2, variant, "strided")
+    n = J.total_dimension()
+    G = 4096
+    sentinel = float(np.frombuffer(np.uint64(0x7FF8DEADBEEF1234).tobytes(), dtype=np.float64)[0])  # a NaN payload
+    big = torch.full((4 * G + 3 * n,), sentinel, device="cuda", dtype=torch.float64)
+    raw0 = big.view(torch.int64).clone()
+    xin = big[G:G + n]
+    y1 = big[2 * G + n:2 * G + 2 * n]
+    y2 = big[3 * G + 2 * n:3 * G + 3 * n]
+    x = np.random.default_rng(8).uniform(-1, 1, n)
+    xin.copy_(torch.tensor(x, device="cuda", dtype=torch.float64))
+    pc.apply(xin, y1)
+    op.apply(xin, y2)
+    torch.cuda.synchronize()
+    assert np.array_equal(y1.cpu().numpy(), opc.apply(x))
+    assert np.array_equal(y2.cpu().numpy(), osys.apply(x))
+    api.gmres(op, pc, xin, tol=1e-10, max_iter=60, restart=50, scaled=True, x=y1, orthogonalization="cgs")
+    api.gmres(op, pc, xin, tol=1e-10, max_iter=60, restart=50, scaled=True, x=y2, orthogonalization="mgs")
+    torch.cuda.synchronize()
+    raw = big.view(torch.int64)
+    assert np.array_equal(xin.cpu().numpy(), x)  # inputs untouched
+    for lo, hi in ((0, G), (G + n, 2 * G + n), (2 * G + 2 * n, 3 * G + 2 * n), (3 * G + 3 * n, 4 * G + 3 * n)):
+        assert torch.equal(raw[lo:hi], raw0[lo:hi]), (lo, hi)
