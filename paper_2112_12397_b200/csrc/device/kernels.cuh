@@ -385,25 +385,40 @@ __global__ void __launch_bounds__(256, 3) srt_kernel(SrtView A, G g, E epi) {
   if (slice >= A.n_slices) return;  // warp-uniform
   const int lane = threadIdx.x & 31, rl = lane >> 2, q = lane & 3;
   const int row = A.row[slice * kSrtRows + rl];
-  const int len = row >= 0 ? A.row_len[row] : 0;
+  // a padding lane (row < 0, last slice only) runs the unpredicated rounds on the slice's first row's
+  // column list and its own zero values; its sums are never stored
+  const int rowv = row >= 0 ? row : A.row[slice * kSrtRows];
+  const int lenv = A.row_len[rowv], len = row >= 0 ? lenv : 0;
   typename E::P pre{};
   if (q == 0 && row >= 0) pre = epi.load(row);
   const long long o0 = A.slice_off[slice];
   const int rounds = int((A.slice_off[slice + 1] - o0) >> 8);  // 256 values per round
-  const int* __restrict__ C = A.ci + (row >= 0 ? A.cp[row] : 0) + 8 * q;
+  const int full = __reduce_min_sync(0xffffffffu, lenv) >> 5;  // rounds in which every row has 32 entries
+  const int* __restrict__ C = A.ci + A.cp[rowv] + 8 * q;
   const double* __restrict__ V = A.vals + o0 + lane;
   double s[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) s[u] = 0.0;
-  for (int t = 0; t < rounds; ++t) {
+  int t = 0;
+  for (; t < full; ++t, C += 32, V += 256) {  // the rows of a sorted slice have nearly one length: most rounds
+    int c[8];
+    double v[8], x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) c[u] = __ldg(C + u), v[u] = __ldg(V + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = g(c[u]);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] = s[u] + v[u] * x[u];
+  }
+  for (; t < rounds; ++t, C += 32, V += 256) {  // ragged end: entry k0 + u exists for k0 + u < len
     const int k0 = 32 * t + 8 * q;
     int c[8];
     double v[8], x[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const bool in = k0 + u < len;
-      c[u] = in ? __ldg(C + 32 * t + u) : 0;
-      v[u] = in ? __ldg(V + (8 * t + u) * 32) : 0.0;
+      c[u] = in ? __ldg(C + u) : 0;
+      v[u] = in ? __ldg(V + 32 * u) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) x[u] = k0 + u < len ? g(c[u]) : 0.0;
