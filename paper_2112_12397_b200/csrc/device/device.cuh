@@ -86,6 +86,7 @@ struct SrtView {
   const long long* cp = nullptr;
   const int* ci = nullptr;
   const double* vals = nullptr;
+  const int* out_row = nullptr;  // optional (row-subset copy): local row r is the operator's row out_row[r]
 };
 
 // Windowed slices for the ordered long-row pipeline (csr_pipe_kernel): rows

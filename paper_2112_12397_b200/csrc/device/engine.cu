@@ -86,6 +86,14 @@ void launch_bsr3(const DBsr3& A, const G& g, const E& e, cudaStream_t s) {
   cuda_check(cudaGetLastError(), "bsr3_kernel launch");
 }
 
+template <class G, class E>
+void launch_srt(const DSrt& A, const G& g, const E& e, cudaStream_t s) {
+  const SrtView V = A.view();
+  if (V.n_slices == 0) return;
+  launch(srt_kernel<G, E>, dim3(blocks_for(V.n_slices, 8)), dim3(256), 0, s, "srt_kernel", V, g, e);
+  cuda_check(cudaGetLastError(), "srt_kernel launch");
+}
+
 // rows / n_sub: compute only rows rows[0 .. n_sub) (honoured by the strided warp-row kernel)
 template <class G, class E>
 void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s, const int* rows = nullptr, int n_sub = 0) {
@@ -96,10 +104,8 @@ void launch_mat(const DMat& A, const G& g, const E& e, cudaStream_t s, const int
   }
   if (A.strided) {
     if (A.csr.n_rows == 0) return;
-    if (A.srt && !rows) {  // many rows: four lanes per row (full launches; row subsets take the warp-row kernel)
-      const SrtView V = A.sr.view();
-      launch(srt_kernel<G, E>, dim3(blocks_for(V.n_slices, 8)), dim3(256), 0, s, "srt_kernel", V, g, e);
-      cuda_check(cudaGetLastError(), "srt_kernel launch");
+    if (A.srt && !rows) {  // many rows: four lanes per row (row subsets: their own copy, or the warp-row kernel)
+      launch_srt(A.sr, g, e, s);
       return;
     }
     if (A.csr.n_rows >= 2048) {
@@ -453,6 +459,8 @@ void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows) {
   sp_lv.clear();
   const int L = int(lv.size());
   if (L < 2 || !lv[0].bsr3 || src_A_.size() != size_t(L)) return;
+  const char* sub_e = std::getenv("FRACPREC_B200_SRT_SUBSETS");  // 0: row subsets stay on the warp-row kernel
+  const bool srt_subsets = !(sub_e && std::atoi(sub_e) == 0);
   std::vector<unsigned char> f0 = rhs_rows;  // rows where this level's rhs can be nonzero
   for (int l = 0; l + 1 < L; ++l) {
     if (!src_A_[l] || !src_P_[l + 1]) break;
@@ -488,6 +496,10 @@ void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows) {
         S.res_n = int(rows.size());
         const DCsr& Ad = lv[l].Am.csr;  // the layout's own copy (its columns may be shared per aggregate)
         S.res_bytes = (8.0 + Ad.index_bytes_per_entry()) * res_nnz + (4.0 + Ad.row_bytes()) * S.res_n;
+        if (lv[l].Am.srt && srt_subsets) {  // the level runs the quad-per-row kernel: so does its row subset, on a copy
+          S.res_srt = srt_subset_from(Ad, rows, 0);
+          S.res_bytes = S.res_srt.matrix_bytes() + 4.0 * S.res_n;
+        }
       }
     }
     // rows of R_{l+1} = P_{l+1}^T that gather an active row
@@ -510,6 +522,10 @@ void DeviceAmg::set_sparse_rhs(const std::vector<unsigned char>& rhs_rows) {
                                            4.0 + R.csr.row_bytes();
       S.r_rows.upload(rrows);
       S.r_n = int(rrows.size());
+      if (R.srt && srt_subsets && S.r_n > 0) {
+        S.r_srt = srt_subset_from(R.csr, rrows, 0);
+        S.r_bytes = S.r_srt.matrix_bytes() + 4.0 * S.r_n;
+      }
     }
     S.r.alloc(size_t(n)), S.r.zero();
     S.bnext.alloc(size_t(P.n_cols)), S.bnext.zero();
@@ -592,7 +608,10 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
     launch_bsr3(S->fine, GPlain{cur}, EResid{b, rr}, s);  // r = b - A x on the active rows
     if (Lg) Lg->add(S->fine.matrix_bytes() + 8.0 * nd + 24.0 * 3.0 * S->fine.n_brows);
   } else if (sp && S->res_n > 0) {
-    launch_mat(L.Am, GPlain{cur}, EResid{b, rr}, s, S->res_rows.get(), S->res_n);
+    if (S->res_srt.n_rows > 0)
+      launch_srt(S->res_srt, GPlain{cur}, EResid{b, rr}, s);
+    else
+      launch_mat(L.Am, GPlain{cur}, EResid{b, rr}, s, S->res_rows.get(), S->res_n);
     if (Lg) Lg->add(S->res_bytes + 8.0 * nd + 24.0 * S->res_n);
   } else {
     launch_level(L, GPlain{cur}, EResid{b, rr}, s);  // r = b - A x
@@ -604,10 +623,16 @@ void DeviceAmg::vcycle(int l, const double* b, double* x, const double* sub_from
     cuda_check(cudaMemsetAsync(C.xt.get(), 0, sizeof(double) * C.n, s), "memset xh_c");
   const int* rrows = rsub ? S->r_rows.get() : nullptr;
   const int rn = rsub ? S->r_n : 0;
-  if (coarse_next)
+  if (rsub && S->r_srt.n_rows > 0) {  // the subset's own quad-per-row copy
+    if (coarse_next)
+      launch_srt(S->r_srt, GPlain{rr}, EStore{bc}, s);
+    else
+      launch_srt(S->r_srt, GPlain{rr}, EStorePre{bc, C.d.get(), w, C.xt.get()}, s);
+  } else if (coarse_next) {
     launch_mat(C.R, GPlain{rr}, EStore{bc}, s, rrows, rn);  // r_c = P^T r  (amg.cpp:166)
-  else
+  } else {
     launch_mat(C.R, GPlain{rr}, EStorePre{bc, C.d.get(), w, C.xt.get()}, s, rrows, rn);
+  }
   if (Lg) Lg->add((rsub ? S->r_bytes : C.R.matrix_bytes()) + 8.0 * nd + 8.0 * C.n * (coarse_next ? 1 : 3));
   if (sp && l + 1 < int(sp_lv.size()) && !coarse_next) {
     vcycle(l + 1, bc, C.x.get(), nullptr, C.xt.get(), s, Lg, true);

@@ -103,17 +103,21 @@ namespace fpd {
 struct DSrt {  // quad-per-row strided32 layout (SrtView)
   int n_rows = 0;
   int64_t nnz = 0, nci = 0, slots = 0;
-  DevBuf<int> row, len, ci;
+  DevBuf<int> row, len, ci, out_row;  // out_row: set for a row-subset copy (srt_subset_from)
   DevBuf<long long> off, cp;
   DevBuf<double> vals;
   SrtView view() const {
-    return {int(row.size() / kSrtRows), row.get(), off.get(), len.get(), cp.get(), ci.get(), vals.get()};
+    return {int(row.size() / kSrtRows), row.get(), off.get(), len.get(), cp.get(), ci.get(), vals.get(),
+            out_row.size() ? out_row.get() : nullptr};
   }
   // values once, the shared column lists once, per row: slot -> row, length, list offset (+ slice offsets)
   double matrix_bytes() const { return 8.0 * double(nnz) + 4.0 * double(nci) + 17.0 * n_rows; }
 };
 // the layout of A (same entries, same order per row); shares column lists where rows allow
 DSrt srt_from(const DCsr& A, cudaStream_t s);
+// the same layout for the rows rows[0 .. m) of A only (A may carry shared column lists); local row t
+// computes A's row rows[t]
+DSrt srt_subset_from(const DCsr& A, const std::vector<int>& rows, cudaStream_t s);
 
 struct DPipe {
   int n_rows = 0, n_slices = 0, n_ctas = 0;
@@ -294,9 +298,11 @@ class DeviceAmg {
     DevBuf<int> res_rows;      // level >= 1: those rows (warp-row kernel row list)
     int res_n = 0;
     double res_bytes = 0.0;
+    DSrt res_srt;              // ... or their quad-per-row copy when the level's operator uses that layout
     DevBuf<int> r_rows;        // rows of R_{l+1} that can gather a nonzero
     int r_n = 0;
     double r_bytes = 0.0;
+    DSrt r_srt;
     DevBuf<double> r, bnext;   // this level's residual and the next level's rhs: +0 off the active rows
   };
   std::vector<SpLevel> sp_lv;  // levels 0 .. sp_lv.size()-1 run the sparse pass

@@ -423,6 +423,45 @@ DSrt srt_from(const DCsr& A, cudaStream_t s) {
   return D;
 }
 
+namespace {
+__global__ void subset_len_kernel(int m, const int* rows, const long long* rp, long long* cnt) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t > m) return;
+  cnt[t] = t < m ? rp[rows[t] + 1] - rp[rows[t]] : 0;
+}
+// a warp per subset row: values from rp, columns from the row's list (cp with shared lists, else rp)
+__global__ void subset_gather_kernel(int m, const int* rows, const long long* rp, const long long* cp, const int* ci,
+                                     const double* v, const long long* off, int* oci, double* ov) {
+  const long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= m) return;
+  const long long r = rows[t], r0 = rp[r], len = rp[r + 1] - r0, c0 = cp ? cp[r] : r0, o = off[t];
+  for (long long k = lane; k < len; k += 32) oci[o + k] = ci[c0 + k], ov[o + k] = v[r0 + k];
+}
+}  // namespace
+
+DSrt srt_subset_from(const DCsr& A, const std::vector<int>& rows, cudaStream_t s) {
+  const int m = int(rows.size());
+  DCsr S;  // the subset as a CSR of its own (plain columns), then the usual builders
+  S.n_rows = m, S.n_cols = A.n_cols;
+  DevBuf<int> drows;
+  drows.upload(rows);
+  DevBuf<long long> cnt(size_t(m) + 1);
+  S.rp.alloc(size_t(m) + 1);
+  subset_len_kernel<<<grid_for(m + 1), kT, 0, s>>>(m, drows.get(), A.rp.get(), cnt.get());
+  S.nnz = exclusive_scan(cnt.get(), S.rp.get(), m, s);
+  S.ci.alloc(size_t(S.nnz)), S.v.alloc(size_t(S.nnz));
+  if (m)
+    subset_gather_kernel<<<grid_for((long long)m * 32), kT, 0, s>>>(m, drows.get(), A.rp.get(),
+                                                                   A.cp.size() ? A.cp.get() : nullptr, A.ci.get(),
+                                                                   A.v.get(), S.rp.get(), S.ci.get(), S.v.get());
+  cuda_check(cudaStreamSynchronize(s), "srt subset gather");
+  share_columns(S, s);
+  DSrt D = srt_from(S, s);
+  D.out_row = std::move(drows);
+  return D;
+}
+
 DBp3 bp3_from(const DCsr& A, cudaStream_t s) {
   DBp3 D;
   if (A.n_rows % 3 != 0 || A.n_rows == 0) return D;
@@ -652,7 +691,7 @@ DMat mat_from(DCsr&& A, bool few_rows_parallel, bool strided, cudaStream_t s) {
     // enough rows to fill the machine with four lanes per row: the strided32 sums from sorted slices
     // (srt_kernel); the CSR stays for the row-subset launches of the sparse right-hand side.
     // FRACPREC_B200_SRT_MIN_ROWS overrides the threshold (tests force it on small levels; 0 = never).
-    long long srt_min = 131072;
+    long long srt_min = 65536;
     if (const char* q = std::getenv("FRACPREC_B200_SRT_MIN_ROWS")) srt_min = std::atoll(q);
     if (srt_min > 0 && M.csr.n_rows >= srt_min) {
       M.sr = srt_from(M.csr, s);

@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(256) csr_warp_kernel(CsrView A, G g, E epi) {
   if (lane == 0) epi(grow, s, pre);
 }
 
-// many rows (>= ~131k): four lanes per row over sorted slices of 8 rows (SrtView), still the strided32
+// many rows (>= 65,536): four lanes per row over sorted slices of 8 rows (SrtView), still the strided32
 // sum.  Lane (rl, q) keeps the partials 8 q .. 8 q + 7 of row rl (entry k -> partial k mod 32, each in
 // order from +0.0); the xor tree's levels h = 16 and 8 are shuffles between the row's four lanes
 // (partial l ^ 16 lives in lane q ^ 2, l ^ 8 in q ^ 1), the levels 4, 2, 1 add inside the lane, every
@@ -389,8 +389,9 @@ __global__ void __launch_bounds__(256, 3) srt_kernel(SrtView A, G g, E epi) {
   // column list and its own zero values; its sums are never stored
   const int rowv = row >= 0 ? row : A.row[slice * kSrtRows];
   const int lenv = A.row_len[rowv], len = row >= 0 ? lenv : 0;
+  const int orow = row >= 0 && A.out_row ? A.out_row[row] : row;  // a row-subset copy computes row out_row[row]
   typename E::P pre{};
-  if (q == 0 && row >= 0) pre = epi.load(row);
+  if (q == 0 && row >= 0) pre = epi.load(orow);
   const long long o0 = A.slice_off[slice];
   const int rounds = int((A.slice_off[slice + 1] - o0) >> 8);  // 256 values per round
   const int full = __reduce_min_sync(0xffffffffu, lenv) >> 5;  // rounds in which every row has 32 entries
@@ -434,7 +435,7 @@ __global__ void __launch_bounds__(256, 3) srt_kernel(SrtView A, G g, E epi) {
   for (int h = 4; h > 0; h >>= 1)
 #pragma unroll
     for (int u = 0; u < h; ++u) s[u] = s[u] + s[u + h];
-  if (q == 0 && row >= 0) epi(row, s[0], pre);
+  if (q == 0 && row >= 0) epi(orow, s[0], pre);
 }
 
 // few long rows: R rows per CTA of 512 threads; in each window of W = 4096 / R

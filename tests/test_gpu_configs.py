@@ -135,7 +135,7 @@ def test_config2_shared_column_lists_bitwise(variant, monkeypatch):
 @pytest.mark.parametrize("variant", ["tpu", "tup"])
 def test_config2_quad_per_row_strided_layout_bitwise(variant, monkeypatch):
     """The quad-per-row strided32 layout (srt_kernel: slices of 8 length-sorted rows, four lanes per row, 32 partials
-    and the xor tree split between shuffles and in-lane additions; taken from 131k rows on, forced here onto every
+    and the xor tree split between shuffles and in-lane additions; taken from 65,536 rows on, forced here onto every
     coarse operator of config 2) gives the warp-per-row kernel's sums bit for bit: the apply stays
     bitwise the oracle's."""
     monkeypatch.setenv("FRACPREC_B200_SRT_MIN_ROWS", "1")
