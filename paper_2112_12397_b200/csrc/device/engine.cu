@@ -90,6 +90,7 @@ template <class G, class E>
 void launch_srt(const DSrt& A, const G& g, const E& e, cudaStream_t s) {
   const SrtView V = A.view();
   if (V.n_slices == 0) return;
+  // 3 blocks of 256 threads per SM (80 registers): 4 (64 registers) and 2 (125) measured slower at configs 3-5
   launch(srt_kernel<G, E>, dim3(blocks_for(V.n_slices, 8)), dim3(256), 0, s, "srt_kernel", V, g, e);
   cuda_check(cudaGetLastError(), "srt_kernel launch");
 }
