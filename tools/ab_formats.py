@@ -20,7 +20,7 @@ variant = os.environ.get("AB_VARIANT", "tup")
 W = api.Workload(cfg, 42)
 J = W.system(copy=False)
 hp = api.HostPreconditioner.from_workload(W, api.PrecondConfig(variant, amg=api.AmgConfig(strength_threshold=0.0,
-                                                                                          row_sum="strided")))
+                                                                                          row_sum=os.environ.get("AB_ROW_SUM", "strided"))))
 op = api.BlockSystemOperator(J)
 for st in settings:
     kv = [x.split("=", 1) for x in st.split(",") if x]
